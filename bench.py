@@ -1,0 +1,352 @@
+"""Benchmark of the LAMPS scheduling pass (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
+
+One step = one lamps_schedule_step over the whole request pool: A0 events,
+A1 strategy argmin, A2 memory-over-time score, A3 starvation + keys, A4 radix
+sort, A5 admission.  Workload (N=1): config C5, the 1M-request
+pool (2^20 slots, GPT-J profile) BASELINE.json's metric is quoted on.  Metric:
+scheduling decisions/s = eligible (READY) requests decided per step / device
+time per step.  Inputs are resident in HBM; L2 (126 MB) is flushed before
+every timed step by writing a 256 MiB buffer (outside the timed events).
+
+For N > 1 (torchrun) every rank owns an independent 1M-request shard
+(weak scaling, "replicas"); time is the max over ranks.
+
+--impl reference times the CPU oracle (oracle/, plain C, one core) as it
+stands on the same workload: the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scheduling decisions/s and µs per step at 1M-request pool; % HBM peak"
+UNIT = "decisions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import gen
+    import oracle as O
+    cname = args.config
+    cfg = gen.lib_config(cname)
+    snap = gen.snapshot(cname, seed=0, id_base=(1 << 20) * 7 + 99)
+    kv = gen.CONFIGS[cname]["kv_total"]
+    full = args.steps + args.warmup <= 60
+    if not full:  # bounded sample: a 2^18-slot pool of the same workload
+        cfg["capacity"] = 1 << 18
+        snap = gen.snapshot(cname, seed=0, n=1 << 18, capacity=1 << 18)
+    p = O.OraclePool(cfg)
+    p.load(snap, snap["next_id"])
+    for _ in range(args.warmup):
+        p.step(kv_total=kv)
+    t0 = time.perf_counter()
+    ne = 0
+    for _ in range(args.steps):
+        r = p.step(kv_total=kv)
+        ne += r["n_eligible"]
+    dt = time.perf_counter() - t0
+    v = ne / dt
+    sample = (f"full {cname} pool ({cfg['capacity']} slots)" if full else
+              f"{cname} workload, 2^18-slot sample") + f", {args.steps} oracle steps"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": {"workload": f"{cname}: 1M-request pool" if full else cname,
+                                            "slots": cfg["capacity"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def cpu_baseline(cname, seconds=12.0):
+    import gen
+    import oracle as O
+    cfg = gen.lib_config(cname)
+    snap = gen.snapshot(cname, seed=0, id_base=(1 << 20) * 7 + 99)
+    p = O.OraclePool(cfg)
+    p.load(snap, snap["next_id"])
+    kv = gen.CONFIGS[cname]["kv_total"]
+    t0 = time.perf_counter()
+    n, ne = 0, 0
+    while True:
+        r = p.step(kv_total=kv)
+        n += 1
+        ne += r["n_eligible"]
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": ne / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} oracle steps over the full {cname} pool ({cfg['capacity']} slots), "
+                      f"{1e3 * dt / n:.0f} ms/step, single-threaded C"}
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    from paper_2410_18248_b200 import LAMPS_TIMING, Scheduler
+    from paper_2410_18248_b200.lamps import EVENT_DTYPE, SEGMENT_DTYPE
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cname = args.config
+    cfg = gen.lib_config(cname)
+    kv = gen.CONFIGS[cname]["kv_total"]
+    cap = cfg["capacity"]
+    id_base = (1 << 20) * 7 + 99
+    snap = gen.snapshot(cname, seed=rank, id_base=id_base)
+    stream = torch.cuda.current_stream()
+
+    s = Scheduler(cfg, stream=stream)
+    s.import_pool(snap, snap["id_base"], snap["next_id"])
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-only timing (value): async steps, inputs resident, L2 flushed
+    for _ in range(args.warmup):
+        flush.zero_()
+        s.step_async(kv)
+    r0 = s.result()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            s.step_async(kv)
+            ends[k].record(stream)
+        barrier()
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+    res = s.result()
+    n_elig = res["n_eligible"]
+    kernels, passes = s.stats()
+    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    ne_t = torch.tensor([float(n_elig)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ne_t, op=dist.ReduceOp.SUM)
+    ms_max, ne_sum = float(ms_t.item()), float(ne_t.item())
+    value = ne_sum / (ms_max / 1e3)
+
+    # ---- per-kernel breakdown (separate handle with CUDA events between kernels)
+    sp = Scheduler(cfg, flags=LAMPS_TIMING, stream=stream)
+    sp.import_pool(snap, snap["id_base"], snap["next_id"])
+    for _ in range(args.warmup):
+        flush.zero_()
+        sp.step_async(kv)
+    sp.timing()
+    for _ in range(args.steps):
+        flush.zero_()
+        sp.step_async(kv)
+    phase_ms, nst = sp.timing()
+    _, sp_passes = sp.stats()
+    sp.close()
+    phase = [x / nst for x in phase_ms]  # ms per step per phase
+
+    # ---- end to end through the public API (host events in, host result out)
+    e2e_steps = args.e2e_steps or args.steps
+    # leave 8192 free slots in the id window so arrivals can be submitted
+    snap_e = gen.snapshot(cname, seed=rank, id_base=id_base, n=cap - 8192)
+    s.import_pool(snap_e, snap_e["id_base"], snap_e["next_id"])
+    prev = s.step(kv_total=kv)["admitted_id"]
+    paused, h2d, d2h = [], 0, 0
+    barrier()
+    t0 = time.perf_counter()
+    ne_e2e = 0
+    for k in range(e2e_steps):
+        # engine report for the previous batch: 2 finish, 2 call their API
+        ev = np.zeros(min(4, len(prev)), EVENT_DTYPE)
+        for j in range(len(ev)):
+            ev[j]["id"], ev[j]["kind"] = prev[j], 2 if j < 2 else 1
+        # API returns for requests paused earlier, then 2 new arrivals into the freed slots
+        if paused:
+            ids = np.asarray(paused[:2], np.uint64)
+            nxt = np.zeros(len(ids), SEGMENT_DTYPE)
+            nxt["pre_len"], nxt["has_api"] = 50, 0
+            s.api_return(ids, np.full(len(ids), 16, np.uint32), nxt)
+            h2d += ids.nbytes + 4 * len(ids) + nxt.nbytes
+            paused = paused[2:]
+        out = s.step(ev, kv)
+        h2d += ev.nbytes
+        paused += [int(x) for x in ev["id"][2:]]
+        segs = np.zeros(2, SEGMENT_DTYPE)
+        segs["prompt_len"], segs["pre_len"], segs["has_api"], segs["api_seconds"] = 300, 100, 1, 1.5
+        segs["resp_len"], segs["post_len"] = 64, 50
+        rc, _ = s.submit_rc(segs)
+        h2d += segs.nbytes if rc == 0 else 0
+        d2h += 64 + 9 * out["n_admitted"] + 8 * out["n_preempted"]
+        ne_e2e += out["n_eligible"]
+        prev = out["admitted_id"]
+    torch.cuda.synchronize()
+    dt_e2e = time.perf_counter() - t0
+    e2e_t = torch.tensor([dt_e2e, float(ne_e2e)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        mx = e2e_t[:1].clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = e2e_t[1:].clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dt_e2e, ne_e2e = float(mx.item()), float(sm.item())
+    e2e_value = ne_e2e / dt_e2e
+
+    if rank == 0:
+        peak, peak_src = measured_peak_hbm()
+        # algorithmic bytes: K1 reads 28 B/slot of SoA, writes 4 B/slot
+        # state and 8 B/eligible key; each radix pass reads + writes 8 B/key
+        k1_bytes = 32 * cap + 8 * n_elig
+        pass_bytes = 16 * n_elig
+        sort_pass_ms = phase[2] / max(sp_passes, 1)
+        kernels_tbl = {
+            "k1_score": {"ms": phase[1], "bytes": k1_bytes, "GBps": k1_bytes / (phase[1] * 1e6)},
+            "k2_sort_pass": {"ms": sort_pass_ms, "launches": sp_passes, "bytes": pass_bytes,
+                             "GBps": pass_bytes / (sort_pass_ms * 1e6) if sort_pass_ms else None},
+            "k0_events_ms": phase[0], "k3_admit_ms": phase[3],
+        }
+        dom = "k2_sort_pass" if phase[2] >= phase[1] else "k1_score"
+        ach = kernels_tbl[dom]["GBps"]
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(dom)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "us_per_step": ms_max * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": f"{cname}: 1M-request pool (2^20 slots), GPT-J profile, "
+                                   f"{n_elig} READY per shard", "slots_per_gpu": cap,
+                       "kv_total_blocks": kv, "max_batch": cfg["max_batch"],
+                       "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
+                       "l2": "flushed before every timed step (256 MiB write)",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak if ach else None, "traffic": traffic,
+                         "peak_source": peak_src},
+            "kernels": kernels_tbl,
+            "phase_ms_per_step": {"k0_events": phase[0], "k1_score": phase[1], "k2_sort": phase[2],
+                                  "k3_admit": phase[3]},
+            "sort_passes": passes,
+            "gpu_launches": kernels * args.steps,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
+                    "d2h_bytes_per_step": d2h / e2e_steps,
+                    "ms_per_step": 1e3 * dt_e2e / e2e_steps,
+                    "path": "lamps_api_return + lamps_schedule_step + lamps_submit (host buffers)"},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cname)
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,255 @@
+/*
+ * lamps.h -- C ABI of the B200-native LAMPS scheduling pass (liblamps.so).
+ *
+ * LAMPS = "LLM API- and Memory-based Predictive Scheduling", arXiv 2410.18248
+ * ("Fast Inference for Augmented Large Language Models").  Citations "P:<n>"
+ * are lines of that paper's text; "R<n>" are the readings listed in
+ * DESIGN.md where the paper is silent or ambiguous.
+ *
+ * One call of lamps_schedule_step is one iteration of Algorithm 1
+ * over the whole request pool, run as one batched GPU pass on the handle's
+ * CUDA stream:
+ *   A0  apply the engine's events for the previously admitted batch
+ *   A1  per READY request with an API: memory waste of Preserve / Discard /
+ *       Swap (Eq. 1-3) and the argmin
+ *   A2  memory-over-time score
+ *   A3  starvation tag (Alg.1) and the 64-bit sort key
+ *   A4  radix sort of the keys = ranked order (Alg.1)
+ *   A5  admission: longest prefix of the ranked order whose KV-block demand
+ *       fits the budget and max_batch (Alg.1), counters
+ *
+ * All device state is integer (tokens, KV blocks, ticks).  The only floating
+ * point input, the predicted API duration in seconds, is quantised on the host
+ * at ingest (R22).  No call falls back to the CPU: without a usable CUDA
+ * device lamps_init fails with LAMPS_ECUDA.
+ *
+ * Threading: a handle is single-owner and not thread-safe; distinct handles
+ * are independent.  Every call is synchronous with respect to the host unless
+ * its name ends in _async.  On any error return the handle's state is
+ * unchanged and lamps_last_error() describes the failure.
+ */
+#ifndef LAMPS_H
+#define LAMPS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes -------------------------------------------------------- */
+#define LAMPS_OK 0
+#define LAMPS_EINVAL (-1)  /* bad argument / infeasible request / bad event */
+#define LAMPS_ENOSPC (-2)  /* pool full: the new id's slot is still occupied */
+#define LAMPS_ENOENT (-3)  /* unknown id, or id in the wrong state for the call */
+#define LAMPS_ENOTSUP (-4) /* feature not available in this build */
+#define LAMPS_ECUDA (-5)   /* CUDA runtime error (no device, launch failure, ...) */
+#define LAMPS_ENCCL (-6)   /* NCCL error (multi-GPU merge) */
+
+/* ---- request states (Alg.1: WaitingQueue, PQueue, DQueue, SQueue) -------- */
+#define LAMPS_FREE 0u
+#define LAMPS_READY 1u
+#define LAMPS_PAUSED_P 2u
+#define LAMPS_PAUSED_D 3u
+#define LAMPS_PAUSED_S 4u
+
+/* ---- handling strategies ------------------------------------- */
+#define LAMPS_PRESERVE 0u
+#define LAMPS_DISCARD 1u
+#define LAMPS_SWAP 2u
+#define LAMPS_NONE 3u /* request has no further API call */
+
+/* ---- engine events (Alg.1) --------------------------- */
+#define LAMPS_EV_API_CALL 1u /* the token just generated triggered the API call */
+#define LAMPS_EV_FINISHED 2u /* the request completed */
+
+/* ---- config flags --------------------------------------------------------- */
+#define LAMPS_DEBUG_OUT 1u /* keep per-slot W_P, W_D, W_S and score for export */
+#define LAMPS_TIMING 2u    /* record CUDA events around each phase (lamps_timing_read) */
+
+#define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
+
+typedef struct lamps_s lamps_t;
+
+/*
+ * Predictions for one segment of a request: its decode tokens up to its next
+ * API call (or to completion), that API's duration and response length, and
+ * the decode tokens after it (a multi-API request is a
+ * chain of segments, each ending with one API call).
+ */
+typedef struct {
+    uint32_t prompt_len;  /* lamps_submit only: initial context tokens */
+    uint32_t pre_len;     /* predicted decode tokens before the API (or in total) */
+    uint32_t resp_len;    /* predicted API response tokens           (has_api) */
+    uint32_t post_len;    /* predicted decode tokens after the API    (has_api) */
+    double api_seconds;   /* predicted API duration T_INT, seconds    (has_api);
+                             quantised to ticks = llround(s * ticks_per_second) */
+    uint32_t has_api;     /* 0 or 1; 0: resp_len, post_len, api_seconds ignored */
+    uint32_t reserved;
+} lamps_segment;
+
+/* An engine report about a request admitted by the previous step. */
+typedef struct {
+    uint64_t id;
+    uint32_t kind; /* LAMPS_EV_API_CALL or LAMPS_EV_FINISHED */
+    uint32_t reserved;
+} lamps_event;
+
+typedef struct {
+    uint32_t capacity;      /* pool slots: power of 2, <= 2^23; slot = id mod capacity */
+    uint32_t block_tokens;  /* B, tokens per KV block: power of 2 (paged KV) */
+    uint64_t tau;           /* ticks per decode iteration (R3); < 2^48 */
+    uint64_t A1, A2;        /* T_fwd(c) = (A1*c + A2*c^2) >> SH ticks (R1); < 2^48 */
+    uint64_t S0, S1;        /* T_swap(c) = c ? (S0 + S1*c) >> SH : 0 ticks (R2); < 2^48 */
+    uint32_t SH;            /* fixed-point shift, <= 63 */
+    uint64_t c_other;       /* C_other tokens (profiled, R4); < 2^32 */
+    double ticks_per_second;          /* ingest quantisation scale, finite > 0 */
+    uint32_t starvation_threshold;    /* StarvationT >= 1 (100 in P:1085) */
+    uint32_t max_batch;               /* runningBatch size limit, 1..16384 */
+    uint64_t kv_capacity_blocks;      /* static KV capacity: infeasibility check at
+                                         ingest; every step's kv_total must be <= it */
+    uint32_t score_bits, id_bits;     /* key layout: score_bits + id_bits + 1 <= 64,
+                                         2^id_bits >= capacity */
+    void* stream;                     /* cudaStream_t to run on (NULL = legacy default) */
+    uint32_t flags;                   /* LAMPS_DEBUG_OUT */
+    uint32_t reserved;
+} lamps_config;
+
+/*
+ * Result of one step.  Host arrays are owned by the handle and stay valid until
+ * the next call on it.  Device arrays likewise (they live in the workspace).
+ */
+typedef struct {
+    uint64_t n_eligible;           /* |WaitingQueue| = READY requests this step */
+    uint64_t pinned;               /* KV blocks held by Preserve-paused requests (R23) */
+    uint64_t budget;               /* kv_total - pinned, clamped at 0 */
+    uint64_t budget_used;          /* sum of demand blk(ctx+1) over the admitted (R19) */
+    uint32_t n_admitted;           /* |runningBatch| */
+    uint32_t n_preempted;          /* admitted last step, READY now, not admitted now */
+    uint32_t blocked_head;         /* n_eligible > 0 and nothing admitted */
+    uint32_t reserved;
+    uint64_t id_base;              /* ids of this step's keys are id_base + (key & (2^id_bits-1)) */
+    const uint64_t* admitted_ids;        /* host, ranked order, n_admitted */
+    const uint8_t* admitted_strategy;    /* host, LAMPS_PRESERVE.. for each admitted */
+    const uint64_t* preempted_ids;       /* host, n_preempted */
+    const uint64_t* d_ranked_keys;       /* device, n_eligible ascending unique keys:
+                                            key = (!starving << (SB+IB)) | (score << IB)
+                                                  | (id - id_base) */
+    const uint32_t* d_admitted_slots;    /* device, n_admitted */
+} lamps_step_out;
+
+/*
+ * Snapshot view of the pool, one entry per slot (all arrays of length
+ * capacity, caller-owned host memory).  Used by lamps_pool_import /
+ * lamps_pool_export for tests, benches and checkpoints.
+ * dbg_w (3 per slot: W_P, W_D, W_S) and dbg_score are export-only and need
+ * LAMPS_DEBUG_OUT; they hold the values of the last step for READY slots.
+ */
+typedef struct {
+    uint64_t* id;
+    uint32_t *state, *has_api, *starving, *strategy, *cnt;
+    uint32_t *ctx, *pre_rem, *api_ticks, *resp_len, *post_len, *pending;
+    uint64_t* dbg_w;     /* may be NULL */
+    uint64_t* dbg_score; /* may be NULL */
+} lamps_pool_io;
+
+/*
+ * lamps_init -- create a handle.  Two-phase: with d_workspace == NULL only
+ * *ws_bytes is written (device bytes needed, 256-byte aligned).  Then call
+ * again with a device buffer of at least that size (e.g. a torch uint8 CUDA
+ * tensor) that the caller keeps alive until lamps_free.  The library never
+ * allocates device memory itself; it allocates pinned host staging buffers.
+ * Errors: EINVAL (NULL pointer, invalid config field), ECUDA.
+ */
+int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lamps_t** out);
+
+/*
+ * lamps_submit -- Alg.1 intake: n new requests arrive, in order.
+ * Ids are assigned consecutively in arrival order and written to ids_out.
+ * Each starts READY with ctx = prompt_len and owes its prefill,
+ * pending = T_fwd(prompt_len).  Errors (nothing submitted):
+ * EINVAL (NULL, has_api > 1, NaN/inf/negative/out-of-range duration,
+ * prompt+pre+resp+post > LAMPS_INGEST_LIMIT, peak demand blk(...) >
+ * kv_capacity_blocks), ENOSPC (the slot of a new id still holds a live request).
+ */
+int lamps_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, uint64_t* ids_out);
+
+/*
+ * lamps_api_return -- Alg.1: the API of each PAUSED request ids[k]
+ * returned actual_resp_len[k] tokens; next[k] holds the predictions of its
+ * next segment (prompt_len ignored).  ctx grows by the response; the request
+ * owes (R10) by its handling strategy D: T_fwd(ctx'), S: T_swap(C_i) +
+ * T_fwd(ctx') - T_fwd(C_i), P: T_fwd(ctx') - T_fwd(C_i); it becomes READY.
+ * Errors: ENOENT (unknown id or not PAUSED), EINVAL (duplicate id, bad
+ * segment, infeasible) -- nothing applied.
+ */
+int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_resp_len,
+                     const lamps_segment* next, uint32_t n);
+
+/*
+ * lamps_schedule_step -- one scheduling iteration (A0..A5 above).
+ * ev[0..n_ev) (host memory) reports what happened to requests admitted by the
+ * previous step; every other previously admitted request generated one token.
+ * kv_total_blocks is the KV capacity available this step (<= kv_capacity_blocks).
+ * Fills *out and returns after the GPU pass completed.
+ * Errors: EINVAL (event for an id not admitted by the previous step,
+ * duplicate event, unknown kind, kv_total_blocks too large), ECUDA.
+ */
+int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev,
+                        uint64_t kv_total_blocks, lamps_step_out* out);
+
+/* lamps_free -- release the handle (not the caller's workspace). */
+int lamps_free(lamps_t* h);
+
+/* ---- auxiliary entry points ---------------------------------------------- */
+
+/* Last error message of the handle (static storage, never NULL). */
+const char* lamps_last_error(const lamps_t* h);
+
+/*
+ * lamps_schedule_step_async -- the same step with no events, enqueued on the
+ * handle's stream without waiting: nothing is copied to the host.  For
+ * engines that capture the pass in their own stream/graph and for device-only
+ * timing.  Fetch the result with lamps_step_result (which synchronises).
+ */
+int lamps_schedule_step_async(lamps_t* h, uint64_t kv_total_blocks);
+
+/* Synchronise and fill *out with the last step's result. */
+int lamps_step_result(lamps_t* h, lamps_step_out* out);
+
+/*
+ * lamps_pool_import -- replace the whole pool with a snapshot (io arrays of
+ * length capacity).  Live slots (state != FREE) must hold ids with
+ * id mod capacity == slot and id_base <= id < next_id, next_id - id_base <=
+ * capacity.  The previous admitted list is cleared.  Errors: EINVAL.
+ */
+int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uint64_t next_id);
+
+/* lamps_pool_export -- copy the pool (and debug values if requested) to io. */
+int lamps_pool_export(lamps_t* h, lamps_pool_io* io);
+
+/* Copy the last step's ranked keys (n_eligible of them) to host memory. */
+int lamps_ranked_keys(lamps_t* h, uint64_t* host_out, uint64_t max_keys, uint64_t* n_out);
+
+/*
+ * Device-side launch statistics of the last step, for benches: the number of
+ * kernels it launched and the number of radix passes that did work.
+ */
+int lamps_step_stats(lamps_t* h, uint32_t* kernels_launched, uint32_t* sort_passes);
+
+/*
+ * With LAMPS_TIMING: device time per phase summed over the steps recorded
+ * since the last read (at most 4096 steps are kept), in milliseconds:
+ * ms[0] = A0 events kernel, ms[1] = A1-A3 score/key kernel, ms[2] = A4 sort
+ * (all radix passes), ms[3] = A5 admission kernel.  Synchronises the stream.
+ */
+int lamps_timing_read(lamps_t* h, double ms[4], uint32_t* n_steps);
+
+/* Library version (major << 16 | minor). */
+uint32_t lamps_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAMPS_H */

@@ -1,0 +1,629 @@
+// lamps_api.cu -- host runtime behind include/lamps.h.
+//
+// Validation, ingest quantisation, the host shadow of request liveness (id
+// window, paused/ready), workspace carving, pinned staging and the launch
+// sequence of one step: K0 events -> K1 score/key -> K2 radix passes -> K3
+// admission.  Every step of the method runs in the kernels; the host only
+// moves inputs and outputs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lamps.h"
+#include "lamps_internal.h"
+
+using namespace lamps;
+
+namespace {
+
+constexpr uint32_t kIngestChunk = 65536;
+constexpr uint32_t kTimingRing = 4096;
+constexpr size_t kAlign = 256;
+enum : uint8_t { H_FREE = 0, H_READY = 1, H_PAUSED = 2 };
+
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// Ingest quantisation (reading R22): ticks = round-half-away(seconds * tps),
+// one IEEE double multiply; accepted iff the result is in [0, 2^32 - 1].
+bool quantize(double seconds, double tps, uint32_t* out) {
+    if (!std::isfinite(seconds) || seconds < 0.0) return false;
+    volatile double x = seconds * tps;
+    const double xv = x;
+    if (!(xv >= 0.0) || !(xv < 4294967295.5)) return false;
+    const double r = std::round(xv);
+    if (r > 4294967295.0) return false;
+    *out = (uint32_t)r;
+    return true;
+}
+
+struct Layout {
+    size_t off = 0;
+    size_t take(size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes);
+        return o;
+    }
+};
+
+}  // namespace
+
+struct lamps_s {
+    lamps_config cfg{};
+    cudaStream_t stream = nullptr;
+    Cost cost{};
+    Bufs b{};
+    uint32_t cap = 0, cap_pad = 0, score_grid = 0;
+    uint8_t* ws = nullptr;
+    // device ingest staging (inside the workspace)
+    void* d_ingest = nullptr;
+    uint32_t* d_gather = nullptr;
+    // host shadow
+    std::vector<uint8_t> hstate;
+    uint64_t next_id = 0, id_base = 0;
+    uint32_t step = 0;
+    std::vector<uint64_t> prev_adm;
+    bool prev_known = true;
+    uint64_t last_id_base = 0;
+    uint32_t last_kernels = 0;
+    // pinned host buffers
+    void* h_ingest = nullptr;
+    lamps_event* h_ev = nullptr;
+    Ctl* h_ctl = nullptr;
+    uint64_t* h_adm_ids = nullptr;
+    uint8_t* h_adm_strat = nullptr;
+    uint64_t* h_pre_ids = nullptr;
+    bool have_result = false;
+    // timing ring
+    std::vector<cudaEvent_t> tev;
+    uint32_t t_count = 0, t_head = 0;
+    std::string err;
+};
+
+namespace {
+
+int fail(lamps_t* h, int code, const std::string& msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+int cuda_fail(lamps_t* h, cudaError_t e, const char* where) {
+    return fail(h, LAMPS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(h, call)                                        \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+    } while (0)
+
+bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+const char* validate_cfg(const lamps_config* c) {
+    const uint64_t lim = 1ull << 48;
+    if (!pow2(c->capacity) || c->capacity > (1u << 23)) return "capacity must be a power of 2 <= 2^23";
+    if (!pow2(c->block_tokens)) return "block_tokens must be a power of 2";
+    if (c->tau >= lim || c->A1 >= lim || c->A2 >= lim || c->S0 >= lim || c->S1 >= lim)
+        return "tau, A1, A2, S0, S1 must be < 2^48";
+    if (c->SH > 63) return "SH must be <= 63";
+    if (c->c_other > 0xffffffffull) return "c_other must be < 2^32";
+    if (!std::isfinite(c->ticks_per_second) || !(c->ticks_per_second > 0.0))
+        return "ticks_per_second must be finite and > 0";
+    if (c->starvation_threshold == 0) return "starvation_threshold must be >= 1";
+    if (c->max_batch == 0 || c->max_batch > (uint32_t)kMaxBatch) return "max_batch must be 1..16384";
+    if (c->score_bits == 0 || c->id_bits == 0 || c->score_bits + c->id_bits + 1 > 64)
+        return "need score_bits, id_bits >= 1 and score_bits + id_bits + 1 <= 64";
+    if (c->id_bits < 64 && (1ull << c->id_bits) < c->capacity) return "2^id_bits must be >= capacity";
+    return nullptr;
+}
+
+size_t carve(lamps_t* h, uint8_t* base) {
+    // base == nullptr: size only
+    const uint32_t cap_pad = h->cap_pad;
+    const uint32_t max_tiles = (cap_pad + kSortTile - 1) / kSortTile;
+    const uint32_t mb = h->cfg.max_batch;
+    Layout L;
+    size_t o_soa[8];
+    for (int i = 0; i < 8; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
+    size_t o_keys0 = L.take(((size_t)cap_pad + kSortTile) * 8);
+    size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
+    size_t o_hist = L.take(kDigits * kBins * 4);
+    size_t o_offs = L.take(kDigits * kBins * 4);
+    size_t o_status = L.take((size_t)max_tiles * kBins * 8);
+    size_t o_ctl = L.take(sizeof(Ctl));
+    size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
+    size_t o_ai0 = L.take((size_t)mb * 8), o_ai1 = L.take((size_t)mb * 8);
+    size_t o_at0 = L.take(mb), o_at1 = L.take(mb);
+    size_t o_pre = L.take((size_t)mb * 8);
+    size_t o_ev = L.take((size_t)mb * sizeof(lamps_event));
+    size_t o_ing = L.take((size_t)kIngestChunk * sizeof(SubmitRec));
+    size_t o_gat = L.take((size_t)kIngestChunk * 4);
+    size_t o_dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? L.take((size_t)cap_pad * 32) : 0;
+    if (!base) return L.off;
+    uint32_t* soa[8];
+    for (int i = 0; i < 8; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
+    h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7]};
+    h->b.keys[0] = reinterpret_cast<uint64_t*>(base + o_keys0);
+    h->b.keys[1] = reinterpret_cast<uint64_t*>(base + o_keys1);
+    h->b.hist = reinterpret_cast<uint32_t*>(base + o_hist);
+    h->b.offs = reinterpret_cast<uint32_t*>(base + o_offs);
+    h->b.status = reinterpret_cast<unsigned long long*>(base + o_status);
+    h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);
+    h->b.adm_slot[0] = reinterpret_cast<uint32_t*>(base + o_as0);
+    h->b.adm_slot[1] = reinterpret_cast<uint32_t*>(base + o_as1);
+    h->b.adm_id[0] = reinterpret_cast<uint64_t*>(base + o_ai0);
+    h->b.adm_id[1] = reinterpret_cast<uint64_t*>(base + o_ai1);
+    h->b.adm_strat[0] = base + o_at0;
+    h->b.adm_strat[1] = base + o_at1;
+    h->b.pre_id = reinterpret_cast<uint64_t*>(base + o_pre);
+    h->b.events = base + o_ev;
+    h->d_ingest = base + o_ing;
+    h->d_gather = reinterpret_cast<uint32_t*>(base + o_gat);
+    h->b.dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? reinterpret_cast<unsigned long long*>(base + o_dbg)
+                                                  : nullptr;
+    h->b.max_tiles = max_tiles;
+    return L.off;
+}
+
+// segment validation shared by submit and api_return; ctx0 = context before the segment
+const char* check_segment(const lamps_t* h, uint64_t ctx0, const lamps_segment& s, uint32_t* ticks) {
+    if (s.has_api > 1) return "has_api must be 0 or 1";
+    uint64_t total = ctx0 + s.pre_len;
+    *ticks = 0;
+    if (s.has_api) {
+        total += (uint64_t)s.resp_len + s.post_len;
+        if (!quantize(s.api_seconds, h->cfg.ticks_per_second, ticks))
+            return "api_seconds is NaN, infinite, negative or out of range after quantisation";
+    }
+    if (total > LAMPS_INGEST_LIMIT) return "request longer than LAMPS_INGEST_LIMIT tokens";
+    const uint64_t B = h->cfg.block_tokens;
+    if ((total + B - 1) / B > h->cfg.kv_capacity_blocks)
+        return "request can never fit: peak KV demand exceeds kv_capacity_blocks";
+    return nullptr;
+}
+
+bool id_live(const lamps_t* h, uint64_t id) {
+    if (id < h->id_base || id >= h->next_id) return false;
+    return h->hstate[id & h->cost.cap_mask] != H_FREE;
+}
+
+void advance_id_base(lamps_t* h) {
+    while (h->id_base < h->next_id && h->hstate[h->id_base & h->cost.cap_mask] == H_FREE) h->id_base++;
+}
+
+void record_timing(lamps_t* h, int k) {
+    if (!(h->cfg.flags & LAMPS_TIMING)) return;
+    cudaEventRecord(h->tev[(size_t)h->t_head * 5 + k], h->stream);
+}
+
+// Enqueue K0..K3 for one step on the handle's stream.
+int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
+    const bool timing = (h->cfg.flags & LAMPS_TIMING) != 0;
+    if (timing && h->t_count == kTimingRing) return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
+    h->step++;
+    StepArgs a{};
+    a.kv_total = kv_total;
+    a.id_base = h->id_base;
+    a.id_base_mod = (uint32_t)(h->id_base & h->cost.cap_mask);
+    a.step = h->step;
+    a.epoch = h->step * 8u;
+    a.n_ev = n_ev;
+    a.max_batch = h->cfg.max_batch;
+    a.parity = h->step & 1u;
+    h->last_id_base = h->id_base;
+    record_timing(h, 0);
+    CU(h, launch_events(h->b, h->cost, a, h->stream));
+    record_timing(h, 1);
+    CU(h, launch_score(h->b, h->cost, a, (int)h->score_grid, h->stream));
+    record_timing(h, 2);
+    CU(h, launch_sort(h->b, h->cost, a, h->cap_pad, h->stream, nullptr));
+    record_timing(h, 3);
+    CU(h, launch_admit(h->b, h->cost, a, h->stream));
+    record_timing(h, 4);
+    if (timing) {
+        h->t_head = (h->t_head + 1) % kTimingRing;
+        h->t_count++;
+    }
+    h->last_kernels = 3 + kDigits;
+    h->have_result = true;
+    return LAMPS_OK;
+}
+
+int fetch_result(lamps_t* h, lamps_step_out* out) {
+    CU(h, cudaMemcpyAsync(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    const Ctl& C = *h->h_ctl;
+    const uint32_t par = h->step & 1u;
+    if (C.n_admitted) {
+        CU(h, cudaMemcpyAsync(h->h_adm_ids, h->b.adm_id[par], (size_t)C.n_admitted * 8,
+                              cudaMemcpyDeviceToHost, h->stream));
+        CU(h, cudaMemcpyAsync(h->h_adm_strat, h->b.adm_strat[par], C.n_admitted,
+                              cudaMemcpyDeviceToHost, h->stream));
+    }
+    if (C.n_preempted)
+        CU(h, cudaMemcpyAsync(h->h_pre_ids, h->b.pre_id, (size_t)C.n_preempted * 8,
+                              cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    h->prev_adm.assign(h->h_adm_ids, h->h_adm_ids + C.n_admitted);
+    h->prev_known = true;
+    if (out) {
+        std::memset(out, 0, sizeof(*out));
+        out->n_eligible = C.n_elig_out;
+        out->pinned = C.pinned_out;
+        out->budget = C.budget;
+        out->budget_used = C.budget_used;
+        out->n_admitted = C.n_admitted;
+        out->n_preempted = C.n_preempted;
+        out->blocked_head = C.blocked_head;
+        out->id_base = h->last_id_base;
+        out->admitted_ids = h->h_adm_ids;
+        out->admitted_strategy = h->h_adm_strat;
+        out->preempted_ids = h->h_pre_ids;
+        out->d_ranked_keys = h->b.keys[C.n_passes & 1u];
+        out->d_admitted_slots = h->b.adm_slot[par];
+    }
+    return LAMPS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t lamps_version(void) { return (1u << 16) | 0u; }
+
+const char* lamps_last_error(const lamps_t* h) {
+    if (!h) return "null handle";
+    return h->err.c_str();
+}
+
+int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lamps_t** out) {
+    if (!cfg || !ws_bytes) return LAMPS_EINVAL;
+    if (validate_cfg(cfg)) return LAMPS_EINVAL;
+    lamps_t tmp;
+    tmp.cfg = *cfg;
+    tmp.cap = cfg->capacity;
+    tmp.cap_pad = std::max<uint32_t>(cfg->capacity, 1024u);
+    const size_t need = carve(&tmp, nullptr);
+    if (!d_workspace) {
+        *ws_bytes = need;
+        return LAMPS_OK;
+    }
+    if (!out) return LAMPS_EINVAL;
+    if (*ws_bytes < need || (reinterpret_cast<uintptr_t>(d_workspace) & (kAlign - 1))) return LAMPS_EINVAL;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return LAMPS_ECUDA;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, d_workspace) != cudaSuccess || attr.type != cudaMemoryTypeDevice)
+        return LAMPS_EINVAL;
+
+    lamps_t* h = new lamps_t();
+    h->cfg = *cfg;
+    h->stream = static_cast<cudaStream_t>(cfg->stream);
+    h->cap = cfg->capacity;
+    h->cap_pad = tmp.cap_pad;
+    h->ws = static_cast<uint8_t*>(d_workspace);
+    carve(h, h->ws);
+    Cost& c = h->cost;
+    c.tau = cfg->tau; c.A1 = cfg->A1; c.A2 = cfg->A2; c.S0 = cfg->S0; c.S1 = cfg->S1;
+    c.c_other = cfg->c_other; c.SH = cfg->SH;
+    c.B = cfg->block_tokens;
+    c.lgB = 0;
+    while ((1u << c.lgB) < c.B) c.lgB++;
+    c.T = cfg->starvation_threshold;
+    c.SB = cfg->score_bits; c.IB = cfg->id_bits;
+    c.score_max = (cfg->score_bits >= 64) ? ~0ull : ((1ull << cfg->score_bits) - 1ull);
+    c.cap = cfg->capacity; c.cap_mask = cfg->capacity - 1u;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t groups = (h->cap + 3) / 4;
+    const uint32_t want = (groups + kScoreThreads - 1) / kScoreThreads;
+    h->score_grid = std::max<uint32_t>(1, std::min<uint32_t>(want, (uint32_t)sms * 4));
+    h->hstate.assign(h->cap, H_FREE);
+    auto cleanup = [&](int code, const char*) { lamps_free(h); return code; };
+    if (cudaMemsetAsync(h->ws, 0, need, h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "memset");
+    if (cudaHostAlloc(&h->h_ingest, (size_t)kIngestChunk * sizeof(SubmitRec), cudaHostAllocDefault) ||
+        cudaHostAlloc((void**)&h->h_ev, (size_t)cfg->max_batch * sizeof(lamps_event), cudaHostAllocDefault) ||
+        cudaHostAlloc((void**)&h->h_ctl, sizeof(Ctl), cudaHostAllocDefault) ||
+        cudaHostAlloc((void**)&h->h_adm_ids, (size_t)cfg->max_batch * 8, cudaHostAllocDefault) ||
+        cudaHostAlloc((void**)&h->h_adm_strat, cfg->max_batch, cudaHostAllocDefault) ||
+        cudaHostAlloc((void**)&h->h_pre_ids, (size_t)cfg->max_batch * 8, cudaHostAllocDefault))
+        return cleanup(LAMPS_ECUDA, "cudaHostAlloc");
+    if (cfg->flags & LAMPS_TIMING) {
+        h->tev.resize((size_t)kTimingRing * 5);
+        for (auto& e : h->tev)
+            if (cudaEventCreate(&e) != cudaSuccess) return cleanup(LAMPS_ECUDA, "event");
+    }
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "sync");
+    *out = h;
+    return LAMPS_OK;
+}
+
+int lamps_free(lamps_t* h) {
+    if (!h) return LAMPS_EINVAL;
+    cudaStreamSynchronize(h->stream);
+    for (auto& e : h->tev)
+        if (e) cudaEventDestroy(e);
+    if (h->h_ingest) cudaFreeHost(h->h_ingest);
+    if (h->h_ev) cudaFreeHost(h->h_ev);
+    if (h->h_ctl) cudaFreeHost(h->h_ctl);
+    if (h->h_adm_ids) cudaFreeHost(h->h_adm_ids);
+    if (h->h_adm_strat) cudaFreeHost(h->h_adm_strat);
+    if (h->h_pre_ids) cudaFreeHost(h->h_pre_ids);
+    delete h;
+    return LAMPS_OK;
+}
+
+int lamps_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, uint64_t* ids_out) {
+    if (!h) return LAMPS_EINVAL;
+    if (n && !segs) return fail(h, LAMPS_EINVAL, "segs is NULL");
+    std::vector<uint32_t> ticks(n);
+    for (uint32_t k = 0; k < n; k++) {
+        if (const char* m = check_segment(h, segs[k].prompt_len, segs[k], &ticks[k]))
+            return fail(h, LAMPS_EINVAL, std::string("submit[") + std::to_string(k) + "]: " + m);
+    }
+    if (h->next_id + n - h->id_base > h->cap) return fail(h, LAMPS_ENOSPC, "pool full (id window)");
+    for (uint32_t k = 0; k < n; k++)
+        if (h->hstate[(h->next_id + k) & h->cost.cap_mask] != H_FREE)
+            return fail(h, LAMPS_ENOSPC, "pool full (slot occupied)");
+    SubmitRec* rec = static_cast<SubmitRec*>(h->h_ingest);
+    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
+        const uint32_t m = std::min(kIngestChunk, n - k0);
+        for (uint32_t i = 0; i < m; i++) {
+            const lamps_segment& s = segs[k0 + i];
+            SubmitRec& r = rec[i];
+            r.slot = (uint32_t)((h->next_id + k0 + i) & h->cost.cap_mask);
+            r.ctx = s.prompt_len;
+            r.pre = s.pre_len;
+            r.has = s.has_api;
+            r.api = s.has_api ? ticks[k0 + i] : 0u;
+            r.resp = s.has_api ? s.resp_len : 0u;
+            r.post = s.has_api ? s.post_len : 0u;
+            r.pad = 0;
+        }
+        CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(SubmitRec), cudaMemcpyHostToDevice, h->stream));
+        CU(h, launch_submit(h->b.pool, h->cost, static_cast<const SubmitRec*>(h->d_ingest), m, h->stream));
+        CU(h, cudaStreamSynchronize(h->stream));  // staging reuse
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        h->hstate[(h->next_id + k) & h->cost.cap_mask] = H_READY;
+        if (ids_out) ids_out[k] = h->next_id + k;
+    }
+    h->next_id += n;
+    return LAMPS_OK;
+}
+
+int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_resp_len,
+                     const lamps_segment* next, uint32_t n) {
+    if (!h) return LAMPS_EINVAL;
+    if (n && (!ids || !actual_resp_len || !next)) return fail(h, LAMPS_EINVAL, "NULL argument");
+    for (uint32_t k = 0; k < n; k++) {
+        if (!id_live(h, ids[k]) || h->hstate[ids[k] & h->cost.cap_mask] != H_PAUSED)
+            return fail(h, LAMPS_ENOENT, "api_return: id unknown or not paused");
+    }
+    {
+        std::vector<uint64_t> s(ids, ids + n);
+        std::sort(s.begin(), s.end());
+        if (std::adjacent_find(s.begin(), s.end()) != s.end())
+            return fail(h, LAMPS_EINVAL, "api_return: duplicate id");
+    }
+    std::vector<uint32_t> ticks(n), ctx(n);
+    // current context of each request (device state) for the ingest checks
+    uint32_t* slots = static_cast<uint32_t*>(h->h_ingest);
+    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
+        const uint32_t m = std::min(kIngestChunk, n - k0);
+        for (uint32_t i = 0; i < m; i++) slots[i] = (uint32_t)(ids[k0 + i] & h->cost.cap_mask);
+        CU(h, cudaMemcpyAsync(h->d_ingest, slots, (size_t)m * 4, cudaMemcpyHostToDevice, h->stream));
+        CU(h, launch_gather_u32(h->b.pool.ctx, static_cast<const uint32_t*>(h->d_ingest), h->d_gather, m,
+                                h->stream));
+        CU(h, cudaMemcpyAsync(ctx.data() + k0, h->d_gather, (size_t)m * 4, cudaMemcpyDeviceToHost, h->stream));
+        CU(h, cudaStreamSynchronize(h->stream));
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        if (const char* m = check_segment(h, (uint64_t)ctx[k] + actual_resp_len[k], next[k], &ticks[k]))
+            return fail(h, LAMPS_EINVAL, std::string("api_return[") + std::to_string(k) + "]: " + m);
+    }
+    ReturnRec* rec = static_cast<ReturnRec*>(h->h_ingest);
+    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
+        const uint32_t m = std::min(kIngestChunk, n - k0);
+        for (uint32_t i = 0; i < m; i++) {
+            const lamps_segment& s = next[k0 + i];
+            ReturnRec& r = rec[i];
+            r.slot = (uint32_t)(ids[k0 + i] & h->cost.cap_mask);
+            r.actual = actual_resp_len[k0 + i];
+            r.pre = s.pre_len;
+            r.has = s.has_api;
+            r.api = s.has_api ? ticks[k0 + i] : 0u;
+            r.resp = s.has_api ? s.resp_len : 0u;
+            r.post = s.has_api ? s.post_len : 0u;
+            r.pad = 0;
+        }
+        CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(ReturnRec), cudaMemcpyHostToDevice, h->stream));
+        CU(h, launch_api_return(h->b.pool, h->cost, static_cast<const ReturnRec*>(h->d_ingest), m, h->stream));
+        CU(h, cudaStreamSynchronize(h->stream));
+    }
+    for (uint32_t k = 0; k < n; k++) h->hstate[ids[k] & h->cost.cap_mask] = H_READY;
+    return LAMPS_OK;
+}
+
+int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks,
+                        lamps_step_out* out) {
+    if (!h) return LAMPS_EINVAL;
+    if (n_ev && !ev) return fail(h, LAMPS_EINVAL, "events is NULL");
+    if (kv_total_blocks > h->cfg.kv_capacity_blocks)
+        return fail(h, LAMPS_EINVAL, "kv_total_blocks exceeds kv_capacity_blocks");
+    if (n_ev) {
+        if (!h->prev_known) {  // previous step ran async: fetch its admitted list
+            int rc = fetch_result(h, nullptr);
+            if (rc) return rc;
+        }
+        if (n_ev > h->prev_adm.size()) return fail(h, LAMPS_EINVAL, "more events than admitted requests");
+        std::vector<uint64_t> prev(h->prev_adm);
+        std::sort(prev.begin(), prev.end());
+        std::vector<uint64_t> seen;
+        seen.reserve(n_ev);
+        for (uint32_t e = 0; e < n_ev; e++) {
+            if (ev[e].kind != LAMPS_EV_API_CALL && ev[e].kind != LAMPS_EV_FINISHED)
+                return fail(h, LAMPS_EINVAL, "unknown event kind");
+            if (!std::binary_search(prev.begin(), prev.end(), ev[e].id))
+                return fail(h, LAMPS_EINVAL, "event for a request not admitted by the previous step");
+            seen.push_back(ev[e].id);
+        }
+        std::sort(seen.begin(), seen.end());
+        if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
+            return fail(h, LAMPS_EINVAL, "duplicate event id");
+        std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
+        CU(h, cudaMemcpyAsync(const_cast<void*>(h->b.events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
+                              cudaMemcpyHostToDevice, h->stream));
+        for (uint32_t e = 0; e < n_ev; e++)
+            h->hstate[ev[e].id & h->cost.cap_mask] = ev[e].kind == LAMPS_EV_FINISHED ? H_FREE : H_PAUSED;
+        advance_id_base(h);
+    }
+    int rc = enqueue_step(h, kv_total_blocks, n_ev);
+    if (rc) return rc;
+    return fetch_result(h, out);
+}
+
+int lamps_schedule_step_async(lamps_t* h, uint64_t kv_total_blocks) {
+    if (!h) return LAMPS_EINVAL;
+    if (kv_total_blocks > h->cfg.kv_capacity_blocks)
+        return fail(h, LAMPS_EINVAL, "kv_total_blocks exceeds kv_capacity_blocks");
+    int rc = enqueue_step(h, kv_total_blocks, 0);
+    if (rc) return rc;
+    h->prev_known = false;
+    return LAMPS_OK;
+}
+
+int lamps_step_result(lamps_t* h, lamps_step_out* out) {
+    if (!h || !out) return LAMPS_EINVAL;
+    if (!h->have_result) return fail(h, LAMPS_EINVAL, "no step has run");
+    return fetch_result(h, out);
+}
+
+int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uint64_t next_id) {
+    if (!h || !io) return LAMPS_EINVAL;
+    if (!io->id || !io->state || !io->has_api || !io->starving || !io->strategy || !io->cnt || !io->ctx ||
+        !io->pre_rem || !io->api_ticks || !io->resp_len || !io->post_len || !io->pending)
+        return fail(h, LAMPS_EINVAL, "import: NULL array");
+    if (next_id < id_base || next_id - id_base > h->cap) return fail(h, LAMPS_EINVAL, "import: bad id window");
+    const uint32_t cap = h->cap, cp = h->cap_pad;
+    std::vector<uint32_t> sfc(cp, 0u);
+    std::vector<uint8_t> hs(cap, H_FREE);
+    for (uint32_t s = 0; s < cap; s++) {
+        const uint32_t st = io->state[s];
+        if (st > LAMPS_PAUSED_S) return fail(h, LAMPS_EINVAL, "import: bad state");
+        if (st == LAMPS_FREE) continue;
+        const uint64_t id = io->id[s];
+        if (id < id_base || id >= next_id || (id & h->cost.cap_mask) != s)
+            return fail(h, LAMPS_EINVAL, "import: id outside the window or in the wrong slot");
+        if (io->has_api[s] > 1 || io->starving[s] > 1 || io->strategy[s] > 3 || io->cnt[s] > 65535)
+            return fail(h, LAMPS_EINVAL, "import: field out of range");
+        sfc[s] = sfc_pack(st, io->has_api[s], io->starving[s], io->strategy[s], io->cnt[s]);
+        hs[s] = st == LAMPS_READY ? H_READY : H_PAUSED;
+    }
+    const Pool& P = h->b.pool;
+    const uint32_t* src[6] = {io->ctx, io->pre_rem, io->api_ticks, io->resp_len, io->post_len, io->pending};
+    uint32_t* dst[6] = {P.ctx, P.pre, P.api, P.resp, P.post, P.pend};
+    std::vector<uint32_t> tmp(cp, 0u);
+    CU(h, cudaMemcpyAsync(P.sfc, sfc.data(), (size_t)cp * 4, cudaMemcpyHostToDevice, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    for (int f = 0; f < 6; f++) {
+        for (uint32_t s = 0; s < cap; s++) tmp[s] = io->state[s] == LAMPS_FREE ? 0u : src[f][s];
+        CU(h, cudaMemcpyAsync(dst[f], tmp.data(), (size_t)cp * 4, cudaMemcpyHostToDevice, h->stream));
+        CU(h, cudaStreamSynchronize(h->stream));
+    }
+    CU(h, cudaMemsetAsync(P.stamp, 0, (size_t)cp * 4, h->stream));
+    CU(h, cudaMemsetAsync(h->b.ctl, 0, sizeof(Ctl), h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    h->hstate.swap(hs);
+    h->id_base = id_base;
+    h->next_id = next_id;
+    advance_id_base(h);
+    h->prev_adm.clear();
+    h->prev_known = true;
+    h->have_result = false;
+    return LAMPS_OK;
+}
+
+int lamps_pool_export(lamps_t* h, lamps_pool_io* io) {
+    if (!h || !io) return LAMPS_EINVAL;
+    if ((io->dbg_w || io->dbg_score) && !h->b.dbg)
+        return fail(h, LAMPS_EINVAL, "export: debug values need LAMPS_DEBUG_OUT");
+    const uint32_t cap = h->cap;
+    const Pool& P = h->b.pool;
+    std::vector<uint32_t> sfc(cap);
+    CU(h, cudaStreamSynchronize(h->stream));
+    CU(h, cudaMemcpy(sfc.data(), P.sfc, (size_t)cap * 4, cudaMemcpyDeviceToHost));
+    const uint32_t* src[6] = {P.ctx, P.pre, P.api, P.resp, P.post, P.pend};
+    uint32_t* dst[6] = {io->ctx, io->pre_rem, io->api_ticks, io->resp_len, io->post_len, io->pending};
+    for (int f = 0; f < 6; f++)
+        if (dst[f]) CU(h, cudaMemcpy(dst[f], src[f], (size_t)cap * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t s = 0; s < cap; s++) {
+        const uint32_t w = sfc[s];
+        if (io->state) io->state[s] = sfc_state(w);
+        if (io->has_api) io->has_api[s] = sfc_has(w);
+        if (io->starving) io->starving[s] = sfc_starv(w);
+        if (io->strategy) io->strategy[s] = sfc_strat(w);
+        if (io->cnt) io->cnt[s] = sfc_cnt(w);
+        if (io->id)
+            io->id[s] = sfc_state(w) == LAMPS_FREE ? 0ull
+                                                    : h->id_base + ((s - h->id_base) & h->cost.cap_mask);
+    }
+    if (io->dbg_w || io->dbg_score) {
+        std::vector<unsigned long long> d((size_t)cap * 4);
+        CU(h, cudaMemcpy(d.data(), h->b.dbg, (size_t)cap * 32, cudaMemcpyDeviceToHost));
+        for (uint32_t s = 0; s < cap; s++) {
+            if (io->dbg_w)
+                for (int k = 0; k < 3; k++) io->dbg_w[3 * (size_t)s + k] = d[4 * (size_t)s + k];
+            if (io->dbg_score) io->dbg_score[s] = d[4 * (size_t)s + 3];
+        }
+    }
+    return LAMPS_OK;
+}
+
+int lamps_ranked_keys(lamps_t* h, uint64_t* host_out, uint64_t max_keys, uint64_t* n_out) {
+    if (!h || !n_out) return LAMPS_EINVAL;
+    CU(h, cudaMemcpyAsync(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    const uint64_t n = h->h_ctl->n_elig;
+    *n_out = n;
+    if (host_out && max_keys) {
+        const uint64_t m = std::min(n, max_keys);
+        if (m) CU(h, cudaMemcpy(host_out, h->b.keys[h->h_ctl->n_passes & 1u], m * 8, cudaMemcpyDeviceToHost));
+    }
+    return LAMPS_OK;
+}
+
+int lamps_step_stats(lamps_t* h, uint32_t* kernels_launched, uint32_t* sort_passes) {
+    if (!h) return LAMPS_EINVAL;
+    CU(h, cudaMemcpyAsync(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    if (kernels_launched) *kernels_launched = h->last_kernels;
+    if (sort_passes) *sort_passes = h->h_ctl->n_passes;
+    return LAMPS_OK;
+}
+
+int lamps_timing_read(lamps_t* h, double ms[4], uint32_t* n_steps) {
+    if (!h || !ms) return LAMPS_EINVAL;
+    if (!(h->cfg.flags & LAMPS_TIMING)) return fail(h, LAMPS_EINVAL, "timing needs LAMPS_TIMING");
+    CU(h, cudaStreamSynchronize(h->stream));
+    for (int k = 0; k < 4; k++) ms[k] = 0.0;
+    const uint32_t n = h->t_count;
+    const uint32_t first = (h->t_head + kTimingRing - n) % kTimingRing;
+    for (uint32_t i = 0; i < n; i++) {
+        const size_t r = (size_t)((first + i) % kTimingRing) * 5;
+        for (int k = 0; k < 4; k++) {
+            float t = 0.f;
+            CU(h, cudaEventElapsedTime(&t, h->tev[r + k], h->tev[r + k + 1]));
+            ms[k] += t;
+        }
+    }
+    if (n_steps) *n_steps = n;
+    h->t_count = 0;
+    return LAMPS_OK;
+}
+
+}  // extern "C"

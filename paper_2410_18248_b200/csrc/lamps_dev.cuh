@@ -1,0 +1,114 @@
+// lamps_dev.cuh -- device-side arithmetic of the LAMPS pass (sm_100a).
+//
+// Integer only.  Every quantity is exact: 64x64->128-bit products, sums kept
+// in 128 bits, clamps at the end.  These functions are the GPU path's own
+// implementation (closed forms, no loops); the CPU oracle under oracle/ is an
+// independent transcription with explicit summation.
+#pragma once
+#include <cstdint>
+
+namespace lamps {
+
+typedef unsigned __int128 u128;
+
+// Packed per-slot state word `sfc` (one u32 per slot in the SoA):
+//   bits 0..2  state (FREE, READY, PAUSED_P, PAUSED_D, PAUSED_S)
+//   bit  3     has_api     bit 4 starving (sticky)
+//   bits 5..6  strategy    (label of the last pass / frozen at API entry)
+//   bits 16..31 cnt        (StarvationCnt, Alg.1, saturating)
+enum : uint32_t { ST_FREE = 0, ST_READY = 1, ST_PP = 2, ST_PD = 3, ST_PS = 4 };
+enum : uint32_t { STR_P = 0, STR_D = 1, STR_S = 2, STR_NONE = 3 };
+enum : uint32_t { EV_API_CALL = 1, EV_FINISHED = 2 };
+
+__host__ __device__ __forceinline__ uint32_t sfc_state(uint32_t w) { return w & 7u; }
+__host__ __device__ __forceinline__ uint32_t sfc_has(uint32_t w) { return (w >> 3) & 1u; }
+__host__ __device__ __forceinline__ uint32_t sfc_starv(uint32_t w) { return (w >> 4) & 1u; }
+__host__ __device__ __forceinline__ uint32_t sfc_strat(uint32_t w) { return (w >> 5) & 3u; }
+__host__ __device__ __forceinline__ uint32_t sfc_cnt(uint32_t w) { return w >> 16; }
+__host__ __device__ __forceinline__ uint32_t sfc_pack(uint32_t st, uint32_t has, uint32_t starv,
+                                                      uint32_t strat, uint32_t cnt) {
+    return st | (has << 3) | (starv << 4) | (strat << 5) | (cnt << 16);
+}
+
+// Per-handle constants, passed by value as a kernel parameter (constant bank).
+struct Cost {
+    uint64_t tau, A1, A2, S0, S1, c_other;
+    uint64_t score_max;  // 2^SB - 1
+    uint32_t SH, lgB, B, T;
+    uint32_t SB, IB, cap_mask, cap;
+};
+
+// Pool SoA (device pointers into the workspace), 16-byte aligned, padded.
+struct Pool {
+    uint32_t *sfc, *ctx, *pre, *api, *resp, *post, *pend;
+    uint32_t* stamp;  // step number at which the slot was last admitted
+};
+
+__device__ __forceinline__ uint64_t sat64(u128 x) {
+    return (uint64_t)(x >> 64) ? ~0ull : (uint64_t)x;
+}
+
+// ceil(n / B), B = 2^lgB (n < 2^40 so no overflow)
+__device__ __forceinline__ uint64_t blk(uint64_t n, const Cost& c) {
+    return (n + c.B - 1) >> c.lgB;
+}
+
+// T_fwd(x) = (A1 x + A2 x^2) >> SH  (R1; prefill shape k1 n^2 d)
+__device__ __forceinline__ uint64_t t_fwd(uint64_t x, const Cost& c) {
+    u128 sq = (u128)x * x;
+    u128 v = (u128)c.A1 * x + (u128)c.A2 * sq;
+    return sat64(v >> c.SH);
+}
+
+// T_swap(x) = x ? (S0 + S1 x) >> SH : 0  (R2)
+__device__ __forceinline__ uint64_t t_swap(uint64_t x, const Cost& c) {
+    if (x == 0) return 0;
+    return sat64(((u128)c.S0 + (u128)c.S1 * x) >> c.SH);
+}
+
+// Eq. (1)-(3), M dropped (R5); C_i = ctx + pre,
+// C_batch = C_i + C_other (R4).  Returns the first-min strategy in P, D, S order.
+__device__ __forceinline__ uint32_t strategy_of(uint64_t ctx, uint64_t pre, uint64_t api,
+                                                const Cost& c, uint64_t* wp_o = nullptr,
+                                                uint64_t* wd_o = nullptr,
+                                                uint64_t* ws_o = nullptr) {
+    const uint64_t ci = ctx + pre;
+    const uint64_t cb = ci + c.c_other;
+    const uint64_t wp = sat64((u128)api * ci);
+    const uint64_t wd = sat64((u128)t_fwd(ci, c) * cb);
+    const uint64_t ws = sat64(((u128)t_swap(ci, c) * cb) << 1);
+    if (wp_o) { *wp_o = wp; *wd_o = wd; *ws_o = ws; }
+    return (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
+}
+
+// F(n) = sum_{j=1..n} ceil(j/B) = B Q(Q+1)/2 + R(Q+1), n = Q B + R (closed form)
+__device__ __forceinline__ u128 ramp_prefix(uint64_t n, const Cost& c) {
+    const uint64_t Q = n >> c.lgB, R = n & (c.B - 1);
+    const u128 q = (u128)Q * (Q + 1);
+    return ((q >> 1) << c.lgB) + (u128)R * (Q + 1);
+}
+
+// Memory-over-time score, readings R7-R10:
+// pending rectangle + pre-API ramp + API phase by strategy + post-API ramp,
+// in KV blocks x ticks, clamped at 2^SB - 1.
+__device__ __forceinline__ uint64_t score_of(uint64_t ctx, uint64_t pre, uint64_t api,
+                                             uint64_t resp, uint64_t post, uint64_t pend,
+                                             uint32_t has, uint32_t strat, const Cost& c) {
+    const uint64_t ci = ctx + pre;
+    u128 s = (u128)blk(ctx, c) * pend;
+    s += (u128)c.tau * (ramp_prefix(ci, c) - ramp_prefix(ctx, c));
+    if (has) {
+        const uint64_t cr = ci + resp;
+        if (strat == STR_P) {
+            s += (u128)blk(ci, c) * api;
+        } else if (strat == STR_D) {
+            s += (u128)blk(cr, c) * t_fwd(cr, c);
+        } else if (strat == STR_S) {
+            s += ((u128)blk(ci, c) * t_swap(ci, c)) << 1;
+        }
+        s += (u128)c.tau * (ramp_prefix(cr + post, c) - ramp_prefix(cr, c));
+    }
+    return s > (u128)c.score_max ? c.score_max : (uint64_t)s;
+}
+
+}  // namespace lamps

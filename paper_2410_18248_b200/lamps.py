@@ -1,0 +1,301 @@
+"""ctypes binding of liblamps.so (include/lamps.h).
+
+Argument marshalling only: every step of the scheduling pass runs in the CUDA
+kernels behind the C ABI.  PyTorch provides the device workspace (a uint8 CUDA
+tensor the handle keeps alive) and the stream.  If the library or a CUDA device
+is missing, calls raise -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+LAMPS_OK, LAMPS_EINVAL, LAMPS_ENOSPC, LAMPS_ENOENT, LAMPS_ENOTSUP, LAMPS_ECUDA, LAMPS_ENCCL = 0, -1, -2, -3, -4, -5, -6
+LAMPS_FREE, LAMPS_READY, LAMPS_PAUSED_P, LAMPS_PAUSED_D, LAMPS_PAUSED_S = 0, 1, 2, 3, 4
+LAMPS_PRESERVE, LAMPS_DISCARD, LAMPS_SWAP, LAMPS_NONE = 0, 1, 2, 3
+LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
+LAMPS_DEBUG_OUT, LAMPS_TIMING = 1, 2
+
+u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+
+
+class lamps_segment(ctypes.Structure):
+    _fields_ = [("prompt_len", u32), ("pre_len", u32), ("resp_len", u32), ("post_len", u32),
+                ("api_seconds", dbl), ("has_api", u32), ("reserved", u32)]
+
+
+class lamps_event(ctypes.Structure):
+    _fields_ = [("id", u64), ("kind", u32), ("reserved", u32)]
+
+
+class lamps_config(ctypes.Structure):
+    _fields_ = [("capacity", u32), ("block_tokens", u32), ("tau", u64), ("A1", u64), ("A2", u64),
+                ("S0", u64), ("S1", u64), ("SH", u32), ("c_other", u64),
+                ("ticks_per_second", dbl), ("starvation_threshold", u32), ("max_batch", u32),
+                ("kv_capacity_blocks", u64), ("score_bits", u32), ("id_bits", u32),
+                ("stream", vp), ("flags", u32), ("reserved", u32)]
+
+
+class lamps_step_out(ctypes.Structure):
+    _fields_ = [("n_eligible", u64), ("pinned", u64), ("budget", u64), ("budget_used", u64),
+                ("n_admitted", u32), ("n_preempted", u32), ("blocked_head", u32), ("reserved", u32),
+                ("id_base", u64), ("admitted_ids", ctypes.POINTER(u64)),
+                ("admitted_strategy", ctypes.POINTER(ctypes.c_uint8)),
+                ("preempted_ids", ctypes.POINTER(u64)), ("d_ranked_keys", vp),
+                ("d_admitted_slots", vp)]
+
+
+class lamps_pool_io(ctypes.Structure):
+    _fields_ = [("id", vp), ("state", vp), ("has_api", vp), ("starving", vp), ("strategy", vp),
+                ("cnt", vp), ("ctx", vp), ("pre_rem", vp), ("api_ticks", vp), ("resp_len", vp),
+                ("post_len", vp), ("pending", vp), ("dbg_w", vp), ("dbg_score", vp)]
+
+
+SEGMENT_DTYPE = np.dtype([("prompt_len", np.uint32), ("pre_len", np.uint32), ("resp_len", np.uint32),
+                          ("post_len", np.uint32), ("api_seconds", np.float64), ("has_api", np.uint32),
+                          ("reserved", np.uint32)], align=True)
+EVENT_DTYPE = np.dtype([("id", np.uint64), ("kind", np.uint32), ("reserved", np.uint32)], align=True)
+POOL_U32_FIELDS = ("state", "has_api", "starving", "strategy", "cnt", "ctx", "pre_rem", "api_ticks",
+                   "resp_len", "post_len", "pending")
+
+_L = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load liblamps.so (building it first if it is missing or stale)."""
+    global _L
+    if _L is None:
+        path = _build.LIB
+        if not os.path.exists(path) or _build.stale():
+            _build.build()
+        L = ctypes.CDLL(path)
+        c_int, P = ctypes.c_int, ctypes.POINTER
+        sig = {
+            "lamps_init": (c_int, [P(lamps_config), vp, P(ctypes.c_size_t), P(vp)]),
+            "lamps_submit": (c_int, [vp, vp, u32, vp]),
+            "lamps_api_return": (c_int, [vp, vp, vp, vp, u32]),
+            "lamps_schedule_step": (c_int, [vp, vp, u32, u64, P(lamps_step_out)]),
+            "lamps_free": (c_int, [vp]),
+            "lamps_last_error": (ctypes.c_char_p, [vp]),
+            "lamps_schedule_step_async": (c_int, [vp, u64]),
+            "lamps_step_result": (c_int, [vp, P(lamps_step_out)]),
+            "lamps_pool_import": (c_int, [vp, P(lamps_pool_io), u64, u64]),
+            "lamps_pool_export": (c_int, [vp, P(lamps_pool_io)]),
+            "lamps_ranked_keys": (c_int, [vp, vp, u64, P(u64)]),
+            "lamps_step_stats": (c_int, [vp, P(u32), P(u32)]),
+            "lamps_timing_read": (c_int, [vp, P(dbl), P(u32)]),
+            "lamps_version": (u32, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _L = L
+    return _L
+
+
+class LampsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"lamps error {code}: {msg}")
+        self.code = code
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(vp)
+
+
+# ---- thin wrappers with the C names (return codes, no exceptions) ----------
+def lamps_init(cfg: lamps_config, d_workspace, ws_bytes: int):
+    h = vp()
+    n = ctypes.c_size_t(ws_bytes)
+    rc = lib().lamps_init(ctypes.byref(cfg), d_workspace, ctypes.byref(n), ctypes.byref(h))
+    return rc, h, n.value
+
+
+def lamps_workspace_bytes(cfg: lamps_config) -> int:
+    n = ctypes.c_size_t(0)
+    rc = lib().lamps_init(ctypes.byref(cfg), None, ctypes.byref(n), None)
+    if rc != LAMPS_OK:
+        raise LampsError(rc, "invalid config")
+    return n.value
+
+
+def lamps_submit(h, segs: np.ndarray, ids_out: np.ndarray) -> int:
+    return lib().lamps_submit(h, _p(segs), len(segs), _p(ids_out))
+
+
+def lamps_api_return(h, ids: np.ndarray, actual: np.ndarray, nxt: np.ndarray) -> int:
+    return lib().lamps_api_return(h, _p(ids), _p(actual), _p(nxt), len(ids))
+
+
+def lamps_schedule_step(h, ev: np.ndarray, kv_total: int, out: lamps_step_out) -> int:
+    return lib().lamps_schedule_step(h, _p(ev) if len(ev) else None, len(ev), kv_total, ctypes.byref(out))
+
+
+def lamps_free(h) -> int:
+    return lib().lamps_free(h)
+
+
+def lamps_last_error(h) -> str:
+    return lib().lamps_last_error(h).decode()
+
+
+# ---- Scheduler: the user-facing object --------------------------------------
+class Scheduler:
+    """One LAMPS scheduling pass handle on the current CUDA device.
+
+    cfg: dict with the lamps_config integer fields (see gen.lib_config for an
+    example).  flags: LAMPS_DEBUG_OUT | LAMPS_TIMING.
+    """
+
+    def __init__(self, cfg: dict, flags: int = 0, stream=None, device=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise LampsError(LAMPS_ECUDA, "no CUDA device: the LAMPS pass has no CPU fallback")
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        c = lamps_config()
+        for name, _ in lamps_config._fields_:
+            if name in cfg:
+                setattr(c, name, cfg[name])
+        c.flags = flags
+        c.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        self.cfg = c
+        self.capacity = int(cfg["capacity"])
+        self.max_batch = int(cfg["max_batch"])
+        self.id_bits, self.score_bits = int(cfg["id_bits"]), int(cfg["score_bits"])
+        n = lamps_workspace_bytes(c)
+        self.workspace = torch.empty(n, dtype=torch.uint8, device=self.device)
+        rc, h, _ = lamps_init(c, ctypes.c_void_p(self.workspace.data_ptr()), n)
+        if rc != LAMPS_OK:
+            raise LampsError(rc, "lamps_init failed")
+        self.h = h
+        self._out = lamps_step_out()
+
+    def _check(self, rc):
+        if rc != LAMPS_OK:
+            raise LampsError(rc, lamps_last_error(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lamps_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- ingest
+    @staticmethod
+    def segments(rows) -> np.ndarray:
+        rows = list(rows)
+        a = np.zeros(len(rows), SEGMENT_DTYPE)
+        for k, r in enumerate(rows):
+            for f in ("prompt_len", "pre_len", "resp_len", "post_len", "api_seconds", "has_api"):
+                a[k][f] = r.get(f, 0)
+        return a
+
+    def submit(self, segs: np.ndarray) -> np.ndarray:
+        segs = np.ascontiguousarray(segs, SEGMENT_DTYPE)
+        ids = np.zeros(max(len(segs), 1), np.uint64)
+        self._check(lamps_submit(self.h, segs, ids))
+        return ids[:len(segs)]
+
+    def submit_rc(self, segs: np.ndarray):
+        segs = np.ascontiguousarray(segs, SEGMENT_DTYPE)
+        ids = np.zeros(max(len(segs), 1), np.uint64)
+        return lamps_submit(self.h, segs, ids), ids[:len(segs)]
+
+    def api_return_rc(self, ids, actual, nxt) -> int:
+        return lamps_api_return(self.h, np.ascontiguousarray(ids, np.uint64),
+                                np.ascontiguousarray(actual, np.uint32),
+                                np.ascontiguousarray(nxt, SEGMENT_DTYPE))
+
+    def api_return(self, ids, actual, nxt):
+        self._check(self.api_return_rc(ids, actual, nxt))
+
+    # ---- step
+    def _result(self, out: lamps_step_out) -> dict:
+        na, npr = out.n_admitted, out.n_preempted
+        return {
+            "rc": 0, "n_eligible": int(out.n_eligible), "pinned": int(out.pinned),
+            "budget": int(out.budget), "budget_used": int(out.budget_used), "n_admitted": int(na),
+            "n_preempted": int(npr), "blocked_head": int(out.blocked_head), "id_base": int(out.id_base),
+            "admitted_id": np.ctypeslib.as_array(out.admitted_ids, (na,)).copy() if na else np.zeros(0, np.uint64),
+            "admitted_strategy": np.ctypeslib.as_array(out.admitted_strategy, (na,)).copy() if na else np.zeros(0, np.uint8),
+            "preempted_id": np.ctypeslib.as_array(out.preempted_ids, (npr,)).copy() if npr else np.zeros(0, np.uint64),
+        }
+
+    def step_rc(self, events=None, kv_total: int = 0):
+        ev = np.zeros(0, EVENT_DTYPE) if events is None else np.ascontiguousarray(events, EVENT_DTYPE)
+        rc = lamps_schedule_step(self.h, ev, int(kv_total), self._out)
+        return rc
+
+    def step(self, events=None, kv_total: int = 0) -> dict:
+        self._check(self.step_rc(events, kv_total))
+        return self._result(self._out)
+
+    def step_async(self, kv_total: int):
+        self._check(lib().lamps_schedule_step_async(self.h, int(kv_total)))
+
+    def result(self) -> dict:
+        self._check(lib().lamps_step_result(self.h, ctypes.byref(self._out)))
+        return self._result(self._out)
+
+    def ranked_keys(self) -> np.ndarray:
+        n = u64(0)
+        self._check(lib().lamps_ranked_keys(self.h, None, 0, ctypes.byref(n)))
+        a = np.zeros(max(int(n.value), 1), np.uint64)
+        self._check(lib().lamps_ranked_keys(self.h, _p(a), int(n.value), ctypes.byref(n)))
+        return a[:int(n.value)]
+
+    def decode_keys(self, keys: np.ndarray, id_base: int):
+        IB, SB = self.id_bits, self.score_bits
+        keys = keys.astype(np.uint64)
+        idoff = keys & np.uint64((1 << IB) - 1)
+        score = (keys >> np.uint64(IB)) & np.uint64((1 << SB) - 1)
+        starving = 1 - ((keys >> np.uint64(IB + SB)) & np.uint64(1))
+        return idoff + np.uint64(id_base), score, starving.astype(np.uint8)
+
+    def stats(self):
+        k, p = u32(0), u32(0)
+        self._check(lib().lamps_step_stats(self.h, ctypes.byref(k), ctypes.byref(p)))
+        return int(k.value), int(p.value)
+
+    def timing(self):
+        ms = (dbl * 4)()
+        n = u32(0)
+        self._check(lib().lamps_timing_read(self.h, ms, ctypes.byref(n)))
+        return list(ms), int(n.value)
+
+    # ---- snapshots
+    def import_pool(self, fields: dict, id_base: int, next_id: int):
+        cap = self.capacity
+        keep = {"id": np.ascontiguousarray(np.asarray(fields["id"])[:cap], np.uint64)}
+        for f in POOL_U32_FIELDS:
+            keep[f] = np.ascontiguousarray(np.asarray(fields[f])[:cap], np.uint32)
+        io = lamps_pool_io(**{k: _p(v) for k, v in keep.items()})
+        self._check(lib().lamps_pool_import(self.h, ctypes.byref(io), int(id_base), int(next_id)))
+
+    def export_pool(self, debug: bool = False) -> dict:
+        cap = self.capacity
+        out = {"id": np.zeros(cap, np.uint64)}
+        for f in POOL_U32_FIELDS:
+            out[f] = np.zeros(cap, np.uint32)
+        io = lamps_pool_io(**{k: _p(v) for k, v in out.items()})
+        if debug:
+            out["dbg_w"] = np.zeros(3 * cap, np.uint64)
+            out["dbg_score"] = np.zeros(cap, np.uint64)
+            io.dbg_w, io.dbg_score = _p(out["dbg_w"]), _p(out["dbg_score"])
+        self._check(lib().lamps_pool_export(self.h, ctypes.byref(io)))
+        if debug:
+            w = out.pop("dbg_w").reshape(cap, 3)
+            out["W_P"], out["W_D"], out["W_S"] = w[:, 0].copy(), w[:, 1].copy(), w[:, 2].copy()
+            out["score"] = out.pop("dbg_score")
+        return out
