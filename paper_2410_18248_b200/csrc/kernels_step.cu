@@ -74,97 +74,88 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 }
 
 // ---------------------------------------------------------------------------
-// K0: A0 -- the previously admitted batch ran one iteration; apply events.
-// One CTA.  Also resets the per-step accumulators read by K1/K2.
-// Paper: iteration-level semantics P:610-611; routing Alg.1 P:1014-1022;
-// removal P:1004; counter reset on API entry unless starving P:1085.
+// A0 -- the previously admitted batch ran one iteration: every
+// admitted slot carries SFC_RAN (set by K3).  Slots without an event get
+// ctx += 1, pre_rem -= 1 (floor 0), pending = 0 inside K1 (fused, no extra pass
+// over memory).  K0 handles only the engine's events and runs only when there
+// are any: API_CALL routes the request to P/D/S by argmin waste at C_i = ctx
+// (Alg.1) and resets its counter unless starving;
+// FINISHED frees the slot.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_events(Bufs b, Cost c, StepArgs a) {
-    Ctl* ctl = b.ctl;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t n_prev = ctl->n_admitted;  // previous K3's result
-    for (uint32_t i = tid; i < kDigits * kBins; i += blockDim.x) b.hist[i] = 0;
-    const uint32_t prev = a.parity ^ 1u;
+__global__ void __launch_bounds__(256) k_events(Bufs b, Cost c, StepArgs a) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.n_ev) return;
     const Pool& P = b.pool;
-    for (uint32_t k = tid; k < n_prev; k += blockDim.x) {
-        const uint32_t s = b.adm_slot[prev][k];
-        if (sfc_state(P.sfc[s]) != ST_READY) continue;
-        P.ctx[s] = P.ctx[s] + 1u;
-        const uint32_t pr = P.pre[s];
-        P.pre[s] = pr ? pr - 1u : 0u;
-        P.pend[s] = 0u;
+    const DevEvent E = static_cast<const DevEvent*>(b.events)[e];
+    const uint32_t s = (uint32_t)E.id & c.cap_mask;
+    const uint32_t w = P.sfc[s];
+    if (E.kind == EV_FINISHED) {
+        P.sfc[s] = 0u;
+        return;
     }
-    __syncthreads();
-    const DevEvent* ev = static_cast<const DevEvent*>(b.events);
-    for (uint32_t e = tid; e < a.n_ev; e += blockDim.x) {
-        const DevEvent E = ev[e];
-        const uint32_t s = (uint32_t)E.id & c.cap_mask;
-        const uint32_t w = P.sfc[s];
-        if (E.kind == EV_FINISHED) {
-            P.sfc[s] = 0u;
-        } else {
-            P.pre[s] = 0u;
-            const uint32_t st = strategy_of(P.ctx[s], 0, P.api[s], c);
-            const uint32_t starv = sfc_starv(w);
-            P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u);
-        }
-    }
-    if (tid == 0) {
-        ctl->n_prev = n_prev;
-        ctl->n_elig = 0;
-        ctl->k1_done = 0;
-        ctl->pinned = 0;
-        ctl->n_passes = 0;
-#pragma unroll
-        for (int d = 0; d < kDigits; d++) ctl->tile_ctr[d] = 0;
-    }
+    const uint32_t ctx = P.ctx[s] + ((w & SFC_RAN) ? 1u : 0u);  // this iteration's token
+    P.ctx[s] = ctx;
+    P.pre[s] = 0u;
+    P.pend[s] = 0u;
+    const uint32_t st = strategy_of(ctx, 0, P.api[s], c);
+    const uint32_t starv = sfc_starv(w);
+    P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u);
 }
 
 // ---------------------------------------------------------------------------
-// K1: A1 strategy, A2 score, A3 starvation + key, fused with the compaction of
-// eligible keys, the eight digit histograms of the radix sort, the pinned
-// Preserve sum and (last CTA) the sort plan.  Four slots per thread through
-// 128-bit loads of the SoA.
+// K1: A0 default update (fused), A1 strategy, A2 score, A3 starvation + key,
+// compaction of the eligible keys, the pinned Preserve sum and the per-block
+// OR/AND of the keys (the sort skips digit positions that never vary).
+// Four slots per thread through 128-bit loads of the SoA.
 // ---------------------------------------------------------------------------
 template <bool DBG>
 __global__ void __launch_bounds__(kScoreThreads) k_score(Bufs b, Cost c, StepArgs a) {
-    __shared__ uint32_t sh_hist[kDigits * kBins];
     __shared__ uint32_t sh_warp[kScoreThreads / 32];
-    __shared__ unsigned long long sh_pin[kScoreThreads / 32];
+    __shared__ unsigned long long sh_red[3][kScoreThreads / 32];
     __shared__ uint32_t sh_base;
-    __shared__ bool sh_last;
-    const uint32_t tid = threadIdx.x;
-    for (uint32_t i = tid; i < kDigits * kBins; i += kScoreThreads) sh_hist[i] = 0;
-    __syncthreads();
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
 
     const Pool& P = b.pool;
     const uint32_t ngroups = (c.cap + 3u) >> 2;  // SoA arrays are padded to a multiple of 4
-    const uint4* sfc4 = reinterpret_cast<const uint4*>(P.sfc);
-    const uint4* ctx4 = reinterpret_cast<const uint4*>(P.ctx);
-    const uint4* pre4 = reinterpret_cast<const uint4*>(P.pre);
-    const uint4* api4 = reinterpret_cast<const uint4*>(P.api);
-    const uint4* resp4 = reinterpret_cast<const uint4*>(P.resp);
-    const uint4* post4 = reinterpret_cast<const uint4*>(P.post);
-    const uint4* pend4 = reinterpret_cast<const uint4*>(P.pend);
-    uint64_t* keys_out = b.keys[0];
     const uint32_t key_top = c.SB + c.IB;
-    unsigned long long pinned = 0;
+    unsigned long long pinned = 0, kor = 0, kand = ~0ull;
 
     for (uint32_t g0 = blockIdx.x * kScoreThreads; g0 < ngroups; g0 += gridDim.x * kScoreThreads) {
         const uint32_t g = g0 + tid;
         const bool in = g < ngroups;
         uint4 w4 = make_uint4(0, 0, 0, 0), cx = w4, pr = w4, ap = w4, rs = w4, po = w4, pe = w4;
         if (in) {
-            w4 = sfc4[g]; cx = ctx4[g]; pr = pre4[g]; ap = api4[g];
-            rs = resp4[g]; po = post4[g]; pe = pend4[g];
+            w4 = __ldcs(reinterpret_cast<const uint4*>(P.sfc) + g);
+            cx = __ldcs(reinterpret_cast<const uint4*>(P.ctx) + g);
+            pr = __ldcs(reinterpret_cast<const uint4*>(P.pre) + g);
+            ap = __ldcs(reinterpret_cast<const uint4*>(P.api) + g);
+            rs = __ldcs(reinterpret_cast<const uint4*>(P.resp) + g);
+            po = __ldcs(reinterpret_cast<const uint4*>(P.post) + g);
+            pe = __ldcs(reinterpret_cast<const uint4*>(P.pend) + g);
         }
         uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
-        const uint32_t cv[4] = {cx.x, cx.y, cx.z, cx.w};
-        const uint32_t prv[4] = {pr.x, pr.y, pr.z, pr.w};
+        uint32_t cv[4] = {cx.x, cx.y, cx.z, cx.w};
+        uint32_t prv[4] = {pr.x, pr.y, pr.z, pr.w};
+        uint32_t pev[4] = {pe.x, pe.y, pe.z, pe.w};
         const uint32_t apv[4] = {ap.x, ap.y, ap.z, ap.w};
         const uint32_t rsv[4] = {rs.x, rs.y, rs.z, rs.w};
         const uint32_t pov[4] = {po.x, po.y, po.z, po.w};
-        const uint32_t pev[4] = {pe.x, pe.y, pe.z, pe.w};
+        // A0: the previous batch generated one token each
+        bool ran = false;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (wv[j] & SFC_RAN) {
+                ran = true;
+                cv[j] += 1u;
+                prv[j] = prv[j] ? prv[j] - 1u : 0u;
+                pev[j] = 0u;
+            }
+        }
+        if (ran) {
+            reinterpret_cast<uint4*>(P.ctx)[g] = make_uint4(cv[0], cv[1], cv[2], cv[3]);
+            reinterpret_cast<uint4*>(P.pre)[g] = make_uint4(prv[0], prv[1], prv[2], prv[3]);
+            reinterpret_cast<uint4*>(P.pend)[g] = make_uint4(pev[0], pev[1], pev[2], pev[3]);
+        }
         uint64_t key[4];
         uint32_t nk = 0;
 #pragma unroll
@@ -174,17 +165,28 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Bufs b, Cost c, StepArg
             if (st == ST_PP) pinned += blk(cv[j], c);
             if (st != ST_READY) continue;
             const uint32_t has = sfc_has(w);
-            uint64_t wp = 0, wd = 0, ws = 0;
-            uint32_t strat = STR_NONE;
-            if (has) strat = strategy_of(cv[j], prv[j], apv[j], c, &wp, &wd, &ws);
-            const uint64_t sc = score_of(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, strat, c);
+            uint64_t wp, wd, ws, sc;
+            uint32_t strat;
+            const uint64_t span = (uint64_t)cv[j] + prv[j] + (has ? (uint64_t)rsv[j] + pov[j] : 0ull);
+            if (c.fast && span < kFastCtxLimit) {
+                strat = strategy_score64(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, c, &sc,
+                                         &wp, &wd, &ws);
+            } else {
+                wp = wd = ws = 0;
+                strat = STR_NONE;
+                if (has) strat = strategy_of(cv[j], prv[j], apv[j], c, &wp, &wd, &ws);
+                sc = score_of(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, strat, c);
+            }
             const uint32_t cnt = sfc_cnt(w);
             const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
             const uint32_t cnt2 = cnt < 65535u ? cnt + 1u : 65535u;
             wv[j] = sfc_pack(ST_READY, has, starv, strat, cnt2);
             const uint32_t slot = 4u * g + (uint32_t)j;
             const uint32_t idoff = (slot - a.id_base_mod) & c.cap_mask;
-            key[nk++] = ((uint64_t)(starv ^ 1u) << key_top) | (sc << c.IB) | idoff;
+            const uint64_t k = ((uint64_t)(starv ^ 1u) << key_top) | (sc << c.IB) | idoff;
+            key[nk++] = k;
+            kor |= k;
+            kand &= k;
             if (DBG) {
                 unsigned long long* d = b.dbg + 4ull * slot;
                 d[0] = wp; d[1] = wd; d[2] = ws; d[3] = sc;
@@ -192,68 +194,66 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Bufs b, Cost c, StepArg
         }
         if (in) reinterpret_cast<uint4*>(P.sfc)[g] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
 
-        // compaction: one atomic per CTA iteration
-        uint32_t tot;
-        const uint32_t off = block_excl_scan_u32<kScoreThreads>(nk, sh_warp, &tot);
-        if (tid == 0) sh_base = tot ? atomicAdd(&b.ctl->n_elig, tot) : 0u;
-        __syncthreads();
-        const uint32_t base = sh_base + off;
-        for (uint32_t j = 0; j < nk; j++) {
-            const uint64_t k = key[j];
-            keys_out[base + j] = k;
+        // compaction: warp prefix by shuffles, one global atomic per CTA iteration
+        uint32_t x = nk;
 #pragma unroll
-            for (int d = 0; d < kDigits; d++)
-                atomicAdd(&sh_hist[d * kBins + (uint32_t)((k >> (8 * d)) & 0xffu)], 1u);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) sh_warp[warp] = x;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < kScoreThreads / 32; w++) {
+                const uint32_t v = sh_warp[w];
+                sh_warp[w] = t;
+                t += v;
+            }
+            sh_base = t ? atomicAdd(&b.ctl->n_elig, t) : 0u;
         }
         __syncthreads();
+        uint64_t* dst = b.keys[0] + sh_base + sh_warp[warp] + (x - nk);
+        for (uint32_t j = 0; j < nk; j++) dst[j] = key[j];
+        __syncthreads();
     }
 
-    // flush histograms and the pinned sum
-    for (uint32_t i = tid; i < kDigits * kBins; i += kScoreThreads) {
-        const uint32_t v = sh_hist[i];
-        if (v) atomicAdd(&b.hist[i], v);
-    }
+    // block reductions: pinned sum, key OR / AND
 #pragma unroll
-    for (int o = 16; o; o >>= 1) pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
-    if (lane_id() == 0) sh_pin[tid >> 5] = pinned;
+    for (int o = 16; o; o >>= 1) {
+        pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+        kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+    }
+    if (lane == 0) {
+        sh_red[0][warp] = pinned;
+        sh_red[1][warp] = kor;
+        sh_red[2][warp] = kand;
+    }
     __syncthreads();
     if (tid == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < kScoreThreads / 32; w++) t += sh_pin[w];
+        unsigned long long t = 0, o = 0, n = ~0ull;
+        for (int w = 0; w < kScoreThreads / 32; w++) {
+            t += sh_red[0][w];
+            o |= sh_red[1][w];
+            n &= sh_red[2][w];
+        }
         if (t) atomicAdd(&b.ctl->pinned, t);
+        b.kmask[blockIdx.x] = o;
+        b.kmask[b.score_grid + blockIdx.x] = n;
     }
-
-    // last CTA: build the sort plan (skip digit positions that are constant)
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) sh_last = atomicAdd(&b.ctl->k1_done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!sh_last) return;
-    __threadfence();
-    const uint32_t n = __ldcg(&b.ctl->n_elig);
-    uint32_t np = 0;
-    for (int d = 0; d < kDigits; d++) {
-        const uint32_t v = tid < kBins ? __ldcg(&b.hist[d * kBins + tid]) : 0u;
-        const int constant = __syncthreads_or(n > 0 && v == n);
-        if (n == 0 || constant) continue;
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan_u32<kScoreThreads>(v, sh_warp, &tot);
-        if (tid < kBins) b.offs[np * kBins + tid] = ex;
-        if (tid == 0) b.ctl->shift[np] = 8u * d;
-        np++;
-    }
-    if (tid == 0) b.ctl->n_passes = np;
 }
 
 // ---------------------------------------------------------------------------
 // K3: A5 admission.  One CTA.  budget = kv_total - pinned (R23); demand of the
-// k-th ranked request = blk(ctx+1) (R19); exclusive prefix sum over the head
-// window W = min(n_elig, max_batch, budget) (every demand is >= 1 block);
-// cut = longest prefix with sum <= budget (Alg.1, R15).  Then the
-// outputs, counter reset of the admitted (Alg.1) and the preempted list.
+// k-th ranked request = blk(ctx+1) (R19); exclusive prefix over the head window
+// W = min(n_elig, max_batch, budget) (every demand is >= 1 block), in chunks of
+// 1024 ranks, stopping at the first chunk that does not fit completely;
+// cut = longest prefix with sum <= budget (Alg.1, R15).  Outputs,
+// counter reset of the admitted (Alg.1), the preempted list, and the
+// per-step accumulators reset for the next step.
 // ---------------------------------------------------------------------------
-constexpr int kAdmitItems = kMaxBatch / kAdmitThreads;  // 16
-
 __global__ void __launch_bounds__(kAdmitThreads) k_admit(Bufs b, Cost c, StepArgs a) {
     __shared__ unsigned long long sh_w64[kAdmitThreads / 32];
     __shared__ uint32_t sh_w32[kAdmitThreads / 32];
@@ -262,79 +262,61 @@ __global__ void __launch_bounds__(kAdmitThreads) k_admit(Bufs b, Cost c, StepArg
     const uint32_t tid = threadIdx.x;
     const uint64_t n_elig = ctl->n_elig;
     const uint64_t pinned = ctl->pinned;
+    const uint32_t n_prev = ctl->n_admitted;
     const uint64_t budget = a.kv_total > pinned ? a.kv_total - pinned : 0ull;
     uint64_t Wn = n_elig < a.max_batch ? n_elig : a.max_batch;
     if (budget < Wn) Wn = budget;
     const uint64_t* keys = b.keys[ctl->n_passes & 1u];
-    const uint64_t idmask = (c.IB >= 64) ? ~0ull : ((1ull << c.IB) - 1ull);
-
-    uint32_t slot[kAdmitItems];
-    unsigned long long dem[kAdmitItems];
-    uint64_t idoff[kAdmitItems];
-    unsigned long long tsum = 0;
-#pragma unroll
-    for (int i = 0; i < kAdmitItems; i++) {
-        const uint32_t k = tid * kAdmitItems + i;
-        dem[i] = 0; slot[i] = 0; idoff[i] = 0;
-        if (k < Wn) {
-            idoff[i] = keys[k] & idmask;
-            slot[i] = (uint32_t)((a.id_base + idoff[i]) & c.cap_mask);
-            dem[i] = blk((uint64_t)P.ctx[slot[i]] + 1u, c);
-        }
-        tsum += dem[i];
-    }
-    unsigned long long total;
-    unsigned long long run = block_excl_scan_u64<kAdmitThreads>(tsum, sh_w64, &total);
-    uint32_t fit = 0;
-    unsigned long long incl[kAdmitItems];
-#pragma unroll
-    for (int i = 0; i < kAdmitItems; i++) {
-        run += dem[i];
-        incl[i] = run;
-        const uint32_t k = tid * kAdmitItems + i;
-        if (k < Wn && run <= budget) fit++;
-    }
-    uint32_t cut;
-    (void)block_excl_scan_u32<kAdmitThreads>(fit, sh_w32, &cut);
+    const uint64_t idmask = (1ull << c.IB) - 1ull;
     const uint32_t par = a.parity;
-#pragma unroll
-    for (int i = 0; i < kAdmitItems; i++) {
-        const uint32_t k = tid * kAdmitItems + i;
-        if (k < cut) {
-            const uint32_t s = slot[i];
-            const uint32_t w = P.sfc[s];
-            b.adm_slot[par][k] = s;
-            b.adm_id[par][k] = a.id_base + idoff[i];
-            b.adm_strat[par][k] = (uint8_t)sfc_strat(w);
-            P.stamp[s] = a.step;
-            P.sfc[s] = w & 0xffffu;  // StarvationCnt <- 0
-            if (k == cut - 1) ctl->budget_used = incl[i];
+
+    unsigned long long carry = 0;
+    uint32_t cut = 0;
+    for (uint32_t base = 0; base < Wn; base += kAdmitThreads) {
+        const uint32_t k = base + tid;
+        uint32_t slot = 0;
+        uint64_t idoff = 0;
+        unsigned long long dem = 0;
+        if (k < Wn) {
+            idoff = keys[k] & idmask;
+            slot = (uint32_t)((a.id_base + idoff) & c.cap_mask);
+            dem = blk((uint64_t)P.ctx[slot] + 1u, c);
         }
+        unsigned long long tot;
+        const unsigned long long incl = carry + block_excl_scan_u64<kAdmitThreads>(dem, sh_w64, &tot) + dem;
+        const bool fit = k < Wn && incl <= budget;
+        const uint32_t nfit = (uint32_t)__syncthreads_count(fit);
+        if (fit) {
+            const uint32_t w = P.sfc[slot];
+            b.adm_slot[par][k] = slot;
+            b.adm_id[par][k] = a.id_base + idoff;
+            b.adm_strat[par][k] = (uint8_t)sfc_strat(w);
+            P.stamp[slot] = a.step;
+            P.sfc[slot] = (w & 0xffffu) | SFC_RAN;  // StarvationCnt <- 0; runs this iteration
+            if (k == base + nfit - 1) ctl->budget_used = incl;
+        }
+        cut += nfit;
+        carry += tot;
+        const uint32_t chunk = (uint32_t)min((uint64_t)kAdmitThreads, Wn - base);
+        if (nfit < chunk) break;
     }
     if (tid == 0 && cut == 0) ctl->budget_used = 0;
     __syncthreads();
 
-    // preempted: admitted last step, still READY, not admitted now
-    const uint32_t n_prev = ctl->n_prev;
+    // preempted: admitted last step, still READY, not admitted now (in the previous rank order)
     const uint32_t prev = par ^ 1u;
-    uint32_t flag[kAdmitItems];
-    uint32_t nf = 0;
-#pragma unroll
-    for (int i = 0; i < kAdmitItems; i++) {
-        const uint32_t k = tid * kAdmitItems + i;
-        flag[i] = 0;
+    uint32_t npre = 0;
+    for (uint32_t base = 0; base < n_prev; base += kAdmitThreads) {
+        const uint32_t k = base + tid;
+        uint32_t f = 0;
         if (k < n_prev) {
             const uint32_t s = b.adm_slot[prev][k];
-            flag[i] = (sfc_state(P.sfc[s]) == ST_READY && P.stamp[s] != a.step) ? 1u : 0u;
+            f = (sfc_state(P.sfc[s]) == ST_READY && P.stamp[s] != a.step) ? 1u : 0u;
         }
-        nf += flag[i];
-    }
-    uint32_t npre;
-    uint32_t pos = block_excl_scan_u32<kAdmitThreads>(nf, sh_w32, &npre);
-#pragma unroll
-    for (int i = 0; i < kAdmitItems; i++) {
-        const uint32_t k = tid * kAdmitItems + i;
-        if (flag[i]) b.pre_id[pos++] = b.adm_id[prev][k];
+        uint32_t tot;
+        const uint32_t pos = block_excl_scan_u32<kAdmitThreads>(f, sh_w32, &tot);
+        if (f) b.pre_id[npre + pos] = b.adm_id[prev][k];
+        npre += tot;
     }
     if (tid == 0) {
         ctl->n_admitted = cut;
@@ -343,6 +325,8 @@ __global__ void __launch_bounds__(kAdmitThreads) k_admit(Bufs b, Cost c, StepArg
         ctl->budget = budget;
         ctl->n_elig_out = n_elig;
         ctl->pinned_out = pinned;
+        ctl->n_elig = 0;  // accumulators of the next step
+        ctl->pinned = 0;
     }
 }
 
@@ -390,7 +374,7 @@ __global__ void k_api_return(Pool P, Cost c, const ReturnRec* rec, uint32_t n) {
     P.api[s] = r.api;
     P.resp[s] = r.resp;
     P.post[s] = r.post;
-    P.sfc[s] = sfc_pack(ST_READY, r.has, sfc_starv(w), sfc_strat(w), sfc_cnt(w));
+    P.sfc[s] = sfc_pack(ST_READY, r.has, sfc_starv(w), sfc_strat(w), sfc_cnt(w));  // RAN clear
 }
 
 __global__ void k_gather_u32(const uint32_t* src, const uint32_t* slots, uint32_t* out, uint32_t n) {
@@ -408,7 +392,8 @@ cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* d_slots, uint
 }
 
 cudaError_t launch_events(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s) {
-    k_events<<<1, 1024, 0, s>>>(b, c, a);
+    if (!a.n_ev) return cudaSuccess;
+    k_events<<<(a.n_ev + 255) / 256, 256, 0, s>>>(b, c, a);
     return cudaGetLastError();
 }
 

@@ -57,7 +57,7 @@ struct lamps_s {
     cudaStream_t stream = nullptr;
     Cost cost{};
     Bufs b{};
-    uint32_t cap = 0, cap_pad = 0, score_grid = 0;
+    uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
     void* d_ingest = nullptr;
@@ -124,16 +124,14 @@ const char* validate_cfg(const lamps_config* c) {
 size_t carve(lamps_t* h, uint8_t* base) {
     // base == nullptr: size only
     const uint32_t cap_pad = h->cap_pad;
-    const uint32_t max_tiles = (cap_pad + kSortTile - 1) / kSortTile;
     const uint32_t mb = h->cfg.max_batch;
     Layout L;
     size_t o_soa[8];
     for (int i = 0; i < 8; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
     size_t o_keys0 = L.take(((size_t)cap_pad + kSortTile) * 8);
     size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
-    size_t o_hist = L.take(kDigits * kBins * 4);
-    size_t o_offs = L.take(kDigits * kBins * 4);
-    size_t o_status = L.take((size_t)max_tiles * kBins * 8);
+    size_t o_kmask = L.take((size_t)2 * h->score_grid * 8);
+    size_t o_bsum = L.take((size_t)2 * h->sort_grid * kBins * 4);
     size_t o_ctl = L.take(sizeof(Ctl));
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
     size_t o_ai0 = L.take((size_t)mb * 8), o_ai1 = L.take((size_t)mb * 8);
@@ -149,9 +147,10 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7]};
     h->b.keys[0] = reinterpret_cast<uint64_t*>(base + o_keys0);
     h->b.keys[1] = reinterpret_cast<uint64_t*>(base + o_keys1);
-    h->b.hist = reinterpret_cast<uint32_t*>(base + o_hist);
-    h->b.offs = reinterpret_cast<uint32_t*>(base + o_offs);
-    h->b.status = reinterpret_cast<unsigned long long*>(base + o_status);
+    h->b.kmask = reinterpret_cast<unsigned long long*>(base + o_kmask);
+    h->b.blocksum = reinterpret_cast<uint32_t*>(base + o_bsum);
+    h->b.score_grid = h->score_grid;
+    h->b.sort_grid = h->sort_grid;
     h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);
     h->b.adm_slot[0] = reinterpret_cast<uint32_t*>(base + o_as0);
     h->b.adm_slot[1] = reinterpret_cast<uint32_t*>(base + o_as1);
@@ -165,8 +164,26 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->d_gather = reinterpret_cast<uint32_t*>(base + o_gat);
     h->b.dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? reinterpret_cast<unsigned long long*>(base + o_dbg)
                                                   : nullptr;
-    h->b.max_tiles = max_tiles;
     return L.off;
+}
+
+// Grid sizes.  Device attributes are needed only when a device exists; the
+// size query (phase 1 of lamps_init) assumes the largest B200 grids so the
+// reported size is an upper bound.
+void grids(lamps_t* h, bool query_device) {
+    int sms = 148, score_occ = 8, sort_occ = 1;
+    if (query_device) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sort_occ = sort_blocks_per_sm();
+    }
+    (void)score_occ;
+    const uint32_t groups = (h->cap + 3) / 4;
+    const uint32_t want = (groups + kScoreThreads - 1) / kScoreThreads;
+    h->score_grid = std::max<uint32_t>(1, std::min<uint32_t>(want, (uint32_t)sms * 7));
+    h->sort_grid = (uint32_t)std::max(1, sms * std::max(sort_occ, 1));
+    if (!query_device) h->sort_grid = std::max<uint32_t>(h->sort_grid, 148u * 2u);
 }
 
 // segment validation shared by submit and api_return; ctx0 = context before the segment
@@ -220,7 +237,7 @@ int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     record_timing(h, 1);
     CU(h, launch_score(h->b, h->cost, a, (int)h->score_grid, h->stream));
     record_timing(h, 2);
-    CU(h, launch_sort(h->b, h->cost, a, h->cap_pad, h->stream, nullptr));
+    CU(h, launch_sort(h->b, h->cost, a, h->stream));
     record_timing(h, 3);
     CU(h, launch_admit(h->b, h->cost, a, h->stream));
     record_timing(h, 4);
@@ -228,7 +245,7 @@ int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         h->t_head = (h->t_head + 1) % kTimingRing;
         h->t_count++;
     }
-    h->last_kernels = 3 + kDigits;
+    h->last_kernels = 3 + (n_ev ? 1 : 0);
     h->have_result = true;
     return LAMPS_OK;
 }
@@ -287,6 +304,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     tmp.cfg = *cfg;
     tmp.cap = cfg->capacity;
     tmp.cap_pad = std::max<uint32_t>(cfg->capacity, 1024u);
+    grids(&tmp, false);
     const size_t need = carve(&tmp, nullptr);
     if (!d_workspace) {
         *ws_bytes = need;
@@ -306,6 +324,15 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     h->cap = cfg->capacity;
     h->cap_pad = tmp.cap_pad;
     h->ws = static_cast<uint8_t*>(d_workspace);
+    grids(h, true);
+    if (h->sort_grid > tmp.sort_grid || h->score_grid > tmp.score_grid) {
+        delete h;
+        return LAMPS_ENOTSUP;  // device larger than the sizing assumption
+    }
+    if ((uint64_t)h->sort_grid * kSortMaxTilesPerCta * kSortTile < h->cap) {
+        delete h;
+        return LAMPS_ENOTSUP;
+    }
     carve(h, h->ws);
     Cost& c = h->cost;
     c.tau = cfg->tau; c.A1 = cfg->A1; c.A2 = cfg->A2; c.S0 = cfg->S0; c.S1 = cfg->S1;
@@ -317,11 +344,8 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     c.SB = cfg->score_bits; c.IB = cfg->id_bits;
     c.score_max = (cfg->score_bits >= 64) ? ~0ull : ((1ull << cfg->score_bits) - 1ull);
     c.cap = cfg->capacity; c.cap_mask = cfg->capacity - 1u;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint32_t groups = (h->cap + 3) / 4;
-    const uint32_t want = (groups + kScoreThreads - 1) / kScoreThreads;
-    h->score_grid = std::max<uint32_t>(1, std::min<uint32_t>(want, (uint32_t)sms * 4));
+    c.fast = (cfg->A1 < (1ull << 37) && cfg->S1 < (1ull << 37) && cfg->A2 < (1ull << 11) &&
+              cfg->S0 < (1ull << 62) && cfg->tau < (1ull << 26) && cfg->c_other < (1ull << 26)) ? 1u : 0u;
     h->hstate.assign(h->cap, H_FREE);
     auto cleanup = [&](int code, const char*) { lamps_free(h); return code; };
     if (cudaMemsetAsync(h->ws, 0, need, h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "memset");
@@ -588,7 +612,7 @@ int lamps_ranked_keys(lamps_t* h, uint64_t* host_out, uint64_t max_keys, uint64_
     if (!h || !n_out) return LAMPS_EINVAL;
     CU(h, cudaMemcpyAsync(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
-    const uint64_t n = h->h_ctl->n_elig;
+    const uint64_t n = h->h_ctl->n_elig_out;
     *n_out = n;
     if (host_out && max_keys) {
         const uint64_t m = std::min(n, max_keys);

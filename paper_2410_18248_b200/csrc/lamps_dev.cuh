@@ -30,13 +30,21 @@ __host__ __device__ __forceinline__ uint32_t sfc_pack(uint32_t st, uint32_t has,
     return st | (has << 3) | (starv << 4) | (strat << 5) | (cnt << 16);
 }
 
+constexpr uint32_t SFC_RAN = 1u << 7;  // admitted by the previous step (A0 pending)
+
 // Per-handle constants, passed by value as a kernel parameter (constant bank).
 struct Cost {
     uint64_t tau, A1, A2, S0, S1, c_other;
     uint64_t score_max;  // 2^SB - 1
     uint32_t SH, lgB, B, T;
     uint32_t SB, IB, cap_mask, cap;
+    uint32_t fast;       // constants satisfy the 64-bit fast-path bounds (host-checked)
 };
+
+// Bounds under which every intermediate of the fast path below fits in 64 bits
+// (products that may not are saturating): A1, S1 < 2^37; A2 < 2^11; S0 < 2^62;
+// tau, c_other < 2^26 (host) and every context value c < 2^25 (per slot).
+constexpr uint64_t kFastCtxLimit = 1ull << 25;
 
 // Pool SoA (device pointers into the workspace), 16-byte aligned, padded.
 struct Pool {
@@ -109,6 +117,61 @@ __device__ __forceinline__ uint64_t score_of(uint64_t ctx, uint64_t pre, uint64_
         s += (u128)c.tau * (ramp_prefix(cr + post, c) - ramp_prefix(cr, c));
     }
     return s > (u128)c.score_max ? c.score_max : (uint64_t)s;
+}
+
+// ---------------------------------------------------------------------------
+// 64-bit fast path.  Exact for the clamped results: T_fwd and T_swap are exact
+// under the bounds; a product that could exceed 2^64 saturates, and the sums
+// saturate, which cannot change min(sum, 2^SB - 1) (SB <= 63) or the argmin
+// (a saturated waste is >= 2^64 - 1, exactly as the exact value is clamped).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mul_sat(uint64_t a, uint64_t b) {
+    return __umul64hi(a, b) ? ~0ull : a * b;
+}
+__device__ __forceinline__ uint64_t add_sat(uint64_t a, uint64_t b) {
+    const uint64_t s = a + b;
+    return s < a ? ~0ull : s;
+}
+__device__ __forceinline__ uint64_t t_fwd64(uint64_t x, const Cost& c) {  // x < 2^25
+    return (c.A1 * x + c.A2 * (x * x)) >> c.SH;
+}
+__device__ __forceinline__ uint64_t t_swap64(uint64_t x, const Cost& c) {  // x < 2^25
+    return x ? (c.S0 + c.S1 * x) >> c.SH : 0ull;
+}
+__device__ __forceinline__ uint64_t ramp_prefix64(uint64_t n, const Cost& c) {  // n < 2^26
+    const uint64_t Q = n >> c.lgB, R = n & (c.B - 1);
+    return (((Q * (Q + 1)) >> 1) << c.lgB) + R * (Q + 1);
+}
+
+// strategy + score for one READY slot, fast path.  Requires has -> ctx+pre+resp+post < 2^25.
+__device__ __forceinline__ uint32_t strategy_score64(uint64_t ctx, uint64_t pre, uint64_t api,
+                                                     uint64_t resp, uint64_t post, uint64_t pend,
+                                                     uint32_t has, const Cost& c, uint64_t* score,
+                                                     uint64_t* wp_o, uint64_t* wd_o, uint64_t* ws_o) {
+    const uint64_t ci = ctx + pre;
+    uint64_t s = add_sat(mul_sat((ctx + c.B - 1) >> c.lgB, pend),
+                         mul_sat(c.tau, ramp_prefix64(ci, c) - ramp_prefix64(ctx, c)));
+    uint32_t strat = STR_NONE;
+    uint64_t wp = 0, wd = 0, ws = 0;
+    if (has) {
+        const uint64_t cb = ci + c.c_other;
+        const uint64_t tf = t_fwd64(ci, c), ts = t_swap64(ci, c);
+        wp = api * ci;
+        wd = mul_sat(tf, cb);
+        ws = mul_sat(ts, cb << 1);
+        strat = (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
+        const uint64_t bci = (ci + c.B - 1) >> c.lgB;
+        const uint64_t cr = ci + resp;
+        uint64_t a;
+        if (strat == STR_P) a = bci * api;
+        else if (strat == STR_D) a = mul_sat((cr + c.B - 1) >> c.lgB, t_fwd64(cr, c));
+        else a = mul_sat(bci << 1, ts);
+        s = add_sat(s, a);
+        s = add_sat(s, mul_sat(c.tau, ramp_prefix64(cr + post, c) - ramp_prefix64(cr, c)));
+    }
+    *score = s > c.score_max ? c.score_max : s;
+    *wp_o = wp; *wd_o = wd; *ws_o = ws;
+    return strat;
 }
 
 }  // namespace lamps

@@ -10,23 +10,23 @@ namespace lamps {
 
 constexpr int kDigits = 8;          // 8-bit digits of a 64-bit key
 constexpr int kBins = 256;
-constexpr int kSortThreads = 256;   // onesweep pass CTA
-constexpr int kSortItems = 8;       // keys per thread
-constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys per tile
+constexpr int kSortThreads = 1024;  // persistent sort CTA (one per SM)
+constexpr int kSortItems = 8;       // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;  // 8192 keys per tile
+constexpr int kSortMaxTilesPerCta = 8;               // capacity <= 2^23 over >= 128 CTAs
 constexpr int kScoreThreads = 256;  // K1 CTA
 constexpr int kAdmitThreads = 1024; // K3 (single CTA)
 constexpr int kMaxBatch = 16384;
 
 // Device control block: per-step counters, the sort plan and the step summary.
 struct Ctl {
-    // ---- written by K0 (zeroed), K1
+    // ---- accumulated by K1, reset by K3 for the next step
     uint32_t n_elig;                 // compacted eligible keys (K1 atomics)
-    uint32_t k1_done;                // K1 finished-CTA counter (last-block plan)
+    uint32_t pad0;
     unsigned long long pinned;       // sum over PAUSED_P of blk(ctx)
-    // ---- sort plan (K1 last block)
-    uint32_t n_passes;               // radix passes that do work
-    uint32_t shift[kDigits];         // bit offset of each active pass's digit
-    uint32_t tile_ctr[kDigits];      // dynamic tile ids per pass
+    // ---- sort (K2)
+    uint32_t n_passes;               // radix passes that did work (K2 block 0)
+    uint32_t bar_count, bar_gen;     // K2 grid barrier
     // ---- summary (K3)
     uint32_t n_admitted, n_preempted, blocked_head, n_prev;
     unsigned long long budget, budget_used;
@@ -47,9 +47,9 @@ struct StepArgs {
 struct Bufs {
     Pool pool;
     Ctl* ctl;
-    uint32_t* hist;          // [kDigits][kBins]  global digit histograms
-    uint32_t* offs;          // [kDigits][kBins]  exclusive prefix per active pass
-    unsigned long long* status;  // [max_tiles][kBins] decoupled look-back words
+    unsigned long long* kmask;   // [2][score_grid]  per-K1-block OR / AND of its keys
+    uint32_t* blocksum;      // [2][sort_grid][kBins]  per-K2-block digit counts, by pass parity
+    uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity
     uint64_t* adm_id[2];     // admitted ids
@@ -57,15 +57,14 @@ struct Bufs {
     uint64_t* pre_id;        // preempted ids
     const void* events;      // lamps_event[max_batch] (device)
     unsigned long long* dbg; // [cap][4] W_P, W_D, W_S, score (LAMPS_DEBUG_OUT) or null
-    uint32_t max_tiles;
 };
 
 // launchers (kernels_step.cu / kernels_sort.cu)
 cudaError_t launch_events(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 cudaError_t launch_score(const Bufs& b, const Cost& c, const StepArgs& a, int grid,
                          cudaStream_t s);
-cudaError_t launch_sort(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t cap,
-                        cudaStream_t s, cudaEvent_t* mid_events);
+cudaError_t launch_sort(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
+int sort_blocks_per_sm();  // occupancy of the persistent sort kernel
 cudaError_t launch_admit(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 
 // ingest records (host -> device staging)
