@@ -344,8 +344,8 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     c.SB = cfg->score_bits; c.IB = cfg->id_bits;
     c.score_max = (cfg->score_bits >= 64) ? ~0ull : ((1ull << cfg->score_bits) - 1ull);
     c.cap = cfg->capacity; c.cap_mask = cfg->capacity - 1u;
-    c.fast = (cfg->A1 < (1ull << 37) && cfg->S1 < (1ull << 37) && cfg->A2 < (1ull << 11) &&
-              cfg->S0 < (1ull << 62) && cfg->tau < (1ull << 26) && cfg->c_other < (1ull << 26)) ? 1u : 0u;
+    c.fast = (cfg->A1 < (1ull << 32) && cfg->S0 < (1ull << 32) && cfg->S1 < (1ull << 32) &&
+              cfg->tau < (1ull << 32) && cfg->A2 < (1ull << 12) && cfg->c_other < (1ull << 26)) ? 1u : 0u;
     h->hstate.assign(h->cap, H_FREE);
     auto cleanup = [&](int code, const char*) { lamps_free(h); return code; };
     if (cudaMemsetAsync(h->ws, 0, need, h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "memset");

@@ -41,9 +41,7 @@ struct Cost {
     uint32_t fast;       // constants satisfy the 64-bit fast-path bounds (host-checked)
 };
 
-// Bounds under which every intermediate of the fast path below fits in 64 bits
-// (products that may not are saturating): A1, S1 < 2^37; A2 < 2^11; S0 < 2^62;
-// tau, c_other < 2^26 (host) and every context value c < 2^25 (per slot).
+// Per-slot bound of the fast path (see strategy_score32): ctx+pre+resp+post < 2^25.
 constexpr uint64_t kFastCtxLimit = 1ull << 25;
 
 // Pool SoA (device pointers into the workspace), 16-byte aligned, padded.
@@ -120,54 +118,69 @@ __device__ __forceinline__ uint64_t score_of(uint64_t ctx, uint64_t pre, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// 64-bit fast path.  Exact for the clamped results: T_fwd and T_swap are exact
-// under the bounds; a product that could exceed 2^64 saturates, and the sums
-// saturate, which cannot change min(sum, 2^SB - 1) (SB <= 63) or the argmin
-// (a saturated waste is >= 2^64 - 1, exactly as the exact value is clamped).
+// Fast path: 32x32->64 products (IMAD.WIDE.U32) instead of 64-bit emulation.
+// Host bounds (Cost::fast): A1, S0, S1, tau < 2^32; A2 < 2^12; c_other < 2^26;
+// per slot: ctx + pre + resp + post < 2^25.  Under them T_fwd, T_swap, W_P and
+// every ramp are exact in 64 bits; a product that may exceed 2^64 saturates and
+// sums saturate, which cannot change min(sum, 2^SB - 1) (SB <= 63) nor the
+// argmin (a saturated waste equals the exact value clamped to 2^64 - 1).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t mul_sat(uint64_t a, uint64_t b) {
-    return __umul64hi(a, b) ? ~0ull : a * b;
+__device__ __forceinline__ uint64_t wide(uint32_t a, uint32_t b) { return (uint64_t)a * b; }
+
+// saturating (64-bit x 32-bit) product
+__device__ __forceinline__ uint64_t mul64x32_sat(uint64_t a, uint32_t b) {
+    const uint64_t lo = wide((uint32_t)a, b);
+    const uint64_t hi = wide((uint32_t)(a >> 32), b);   // contributes hi << 32
+    if (hi >> 32) return ~0ull;
+    const uint64_t r = lo + (hi << 32);
+    return r < lo ? ~0ull : r;
 }
 __device__ __forceinline__ uint64_t add_sat(uint64_t a, uint64_t b) {
     const uint64_t s = a + b;
     return s < a ? ~0ull : s;
 }
-__device__ __forceinline__ uint64_t t_fwd64(uint64_t x, const Cost& c) {  // x < 2^25
-    return (c.A1 * x + c.A2 * (x * x)) >> c.SH;
+// T_fwd(x) = (A1 x + A2 x^2) >> SH, x < 2^25: A1 x < 2^57, A2 x^2 < 2^62
+__device__ __forceinline__ uint64_t t_fwd32(uint32_t x, const Cost& c) {
+    const uint64_t sq = wide(x, x);
+    const uint64_t v = wide((uint32_t)c.A1, x) + mul64x32_sat(sq, (uint32_t)c.A2);
+    return v >> c.SH;
 }
-__device__ __forceinline__ uint64_t t_swap64(uint64_t x, const Cost& c) {  // x < 2^25
-    return x ? (c.S0 + c.S1 * x) >> c.SH : 0ull;
+// T_swap(x) = x ? (S0 + S1 x) >> SH : 0, x < 2^25
+__device__ __forceinline__ uint64_t t_swap32(uint32_t x, const Cost& c) {
+    return x ? (c.S0 + wide((uint32_t)c.S1, x)) >> c.SH : 0ull;
 }
-__device__ __forceinline__ uint64_t ramp_prefix64(uint64_t n, const Cost& c) {  // n < 2^26
-    const uint64_t Q = n >> c.lgB, R = n & (c.B - 1);
-    return (((Q * (Q + 1)) >> 1) << c.lgB) + R * (Q + 1);
+// F(n) = sum_{j=1..n} ceil(j/B) = B Q(Q+1)/2 + R(Q+1), n = Q B + R, n < 2^25
+__device__ __forceinline__ uint64_t ramp32(uint32_t n, const Cost& c) {
+    const uint32_t Q = n >> c.lgB, R = n & (c.B - 1u);
+    return ((wide(Q, Q + 1u) >> 1) << c.lgB) + wide(R, Q + 1u);
 }
 
-// strategy + score for one READY slot, fast path.  Requires has -> ctx+pre+resp+post < 2^25.
-__device__ __forceinline__ uint32_t strategy_score64(uint64_t ctx, uint64_t pre, uint64_t api,
-                                                     uint64_t resp, uint64_t post, uint64_t pend,
+// strategy (A1) and score (A2) of one READY slot on the fast path
+__device__ __forceinline__ uint32_t strategy_score32(uint32_t ctx, uint32_t pre, uint32_t api,
+                                                     uint32_t resp, uint32_t post, uint32_t pend,
                                                      uint32_t has, const Cost& c, uint64_t* score,
                                                      uint64_t* wp_o, uint64_t* wd_o, uint64_t* ws_o) {
-    const uint64_t ci = ctx + pre;
-    uint64_t s = add_sat(mul_sat((ctx + c.B - 1) >> c.lgB, pend),
-                         mul_sat(c.tau, ramp_prefix64(ci, c) - ramp_prefix64(ctx, c)));
+    const uint32_t ci = ctx + pre;
+    const uint32_t tau = (uint32_t)c.tau;
+    uint64_t s = add_sat(wide((ctx + c.B - 1u) >> c.lgB, pend),
+                         mul64x32_sat(ramp32(ci, c) - ramp32(ctx, c), tau));
     uint32_t strat = STR_NONE;
     uint64_t wp = 0, wd = 0, ws = 0;
     if (has) {
-        const uint64_t cb = ci + c.c_other;
-        const uint64_t tf = t_fwd64(ci, c), ts = t_swap64(ci, c);
-        wp = api * ci;
-        wd = mul_sat(tf, cb);
-        ws = mul_sat(ts, cb << 1);
+        const uint32_t cb = ci + (uint32_t)c.c_other;  // < 2^27
+        const uint64_t tf = t_fwd32(ci, c), ts = t_swap32(ci, c);
+        wp = wide(api, ci);
+        wd = mul64x32_sat(tf, cb);
+        ws = mul64x32_sat(ts, cb << 1);
         strat = (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
-        const uint64_t bci = (ci + c.B - 1) >> c.lgB;
-        const uint64_t cr = ci + resp;
+        const uint32_t bci = (ci + c.B - 1u) >> c.lgB;
+        const uint32_t cr = ci + resp;
         uint64_t a;
-        if (strat == STR_P) a = bci * api;
-        else if (strat == STR_D) a = mul_sat((cr + c.B - 1) >> c.lgB, t_fwd64(cr, c));
-        else a = mul_sat(bci << 1, ts);
+        if (strat == STR_P) a = wide(bci, api);
+        else if (strat == STR_D) a = mul64x32_sat(t_fwd32(cr, c), (cr + c.B - 1u) >> c.lgB);
+        else a = mul64x32_sat(ts, bci << 1);
         s = add_sat(s, a);
-        s = add_sat(s, mul_sat(c.tau, ramp_prefix64(cr + post, c) - ramp_prefix64(cr, c)));
+        s = add_sat(s, mul64x32_sat(ramp32(cr + post, c) - ramp32(cr, c), tau));
     }
     *score = s > c.score_max ? c.score_max : s;
     *wp_o = wp; *wd_o = wd; *ws_o = ws;

@@ -1,0 +1,241 @@
+// step_dev.cuh -- device bodies shared by the multi-kernel path (K1, K3) and the
+// fused cooperative step kernel: scoring of a group of four slots (A0 default
+// update, A1, A2, A3 + key) and the single-CTA admission (A5).
+#pragma once
+#include "lamps_internal.h"
+
+namespace lamps {
+
+struct DevEvent {
+    unsigned long long id;
+    uint32_t kind, reserved;
+};
+
+// block-wide exclusive scans (all NT threads call; totals in *tot)
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh_warp, uint32_t* tot) {
+    constexpr int NW = NT / 32;
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) sh_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < (unsigned)NW ? sh_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= (unsigned)o) t += y;
+        }
+        if (lane < (unsigned)NW) sh_warp[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t before = w ? sh_warp[w - 1] : 0u;
+    *tot = sh_warp[NW - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+template <int NT>
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v,
+                                                                  unsigned long long* sh_warp,
+                                                                  unsigned long long* tot) {
+    constexpr int NW = NT / 32;
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) sh_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long t = lane < (unsigned)NW ? sh_warp[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= (unsigned)o) t += y;
+        }
+        if (lane < (unsigned)NW) sh_warp[lane] = t;
+    }
+    __syncthreads();
+    const unsigned long long before = w ? sh_warp[w - 1] : 0ull;
+    *tot = sh_warp[NW - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+// One group of four consecutive slots g*4..g*4+3 (128-bit loads of the SoA).
+// A0 (fused): slots admitted by the previous step (SFC_RAN) generated one
+// token: ctx += 1, pre_rem -= 1 (floor 0), pending = 0.
+// A1 strategy argmin of Eq. (1)-(3), A2 score, A3 starvation, counter +1
+// (reset by admission), 64-bit key.  Returns the number of keys written to key[].
+template <bool DBG>
+__device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, uint32_t id_base_mod,
+                                                unsigned long long* dbg, uint32_t g, uint64_t (&key)[4],
+                                                unsigned long long& pinned) {
+    const uint4 w4 = __ldcs(reinterpret_cast<const uint4*>(P.sfc) + g);
+    const uint4 cx = __ldcs(reinterpret_cast<const uint4*>(P.ctx) + g);
+    const uint4 pr = __ldcs(reinterpret_cast<const uint4*>(P.pre) + g);
+    const uint4 ap = __ldcs(reinterpret_cast<const uint4*>(P.api) + g);
+    const uint4 rs = __ldcs(reinterpret_cast<const uint4*>(P.resp) + g);
+    const uint4 po = __ldcs(reinterpret_cast<const uint4*>(P.post) + g);
+    const uint4 pe = __ldcs(reinterpret_cast<const uint4*>(P.pend) + g);
+    uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+    uint32_t cv[4] = {cx.x, cx.y, cx.z, cx.w};
+    uint32_t prv[4] = {pr.x, pr.y, pr.z, pr.w};
+    uint32_t pev[4] = {pe.x, pe.y, pe.z, pe.w};
+    const uint32_t apv[4] = {ap.x, ap.y, ap.z, ap.w};
+    const uint32_t rsv[4] = {rs.x, rs.y, rs.z, rs.w};
+    const uint32_t pov[4] = {po.x, po.y, po.z, po.w};
+    bool ran = false;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (wv[j] & SFC_RAN) {
+            ran = true;
+            cv[j] += 1u;
+            prv[j] = prv[j] ? prv[j] - 1u : 0u;
+            pev[j] = 0u;
+        }
+    }
+    if (ran) {
+        reinterpret_cast<uint4*>(P.ctx)[g] = make_uint4(cv[0], cv[1], cv[2], cv[3]);
+        reinterpret_cast<uint4*>(P.pre)[g] = make_uint4(prv[0], prv[1], prv[2], prv[3]);
+        reinterpret_cast<uint4*>(P.pend)[g] = make_uint4(pev[0], pev[1], pev[2], pev[3]);
+    }
+    const uint32_t key_top = c.SB + c.IB;
+    uint32_t nk = 0;
+    bool any_ready = false;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const uint32_t w = wv[j];
+        const uint32_t st = sfc_state(w);
+        if (st == ST_PP) pinned += blk(cv[j], c);
+        key[j] = 0;
+        if (st != ST_READY) continue;
+        any_ready = true;
+        const uint32_t has = sfc_has(w);
+        uint64_t wp, wd, ws, sc;
+        uint32_t strat;
+        const uint64_t span = (uint64_t)cv[j] + prv[j] + (has ? (uint64_t)rsv[j] + pov[j] : 0ull);
+        if (c.fast && span < kFastCtxLimit) {
+            strat = strategy_score32(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, c, &sc, &wp, &wd, &ws);
+        } else {
+            wp = wd = ws = 0;
+            strat = STR_NONE;
+            if (has) strat = strategy_of(cv[j], prv[j], apv[j], c, &wp, &wd, &ws);
+            sc = score_of(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, strat, c);
+        }
+        const uint32_t cnt = sfc_cnt(w);
+        const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
+        const uint32_t cnt2 = cnt < 65535u ? cnt + 1u : 65535u;
+        wv[j] = sfc_pack(ST_READY, has, starv, strat, cnt2);
+        const uint32_t slot = 4u * g + (uint32_t)j;
+        const uint32_t idoff = (slot - id_base_mod) & c.cap_mask;
+        // keys are packed to the front of key[] in slot order (predicated, no dynamic index)
+        const uint64_t k = ((uint64_t)(starv ^ 1u) << key_top) | (sc << c.IB) | idoff;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (q == (int)nk) key[q] = k;
+        nk++;
+        if (DBG) {
+            unsigned long long* d = dbg + 4ull * slot;
+            d[0] = wp; d[1] = wd; d[2] = ws; d[3] = sc;
+        }
+    }
+    if (any_ready) reinterpret_cast<uint4*>(P.sfc)[g] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    return nk;
+}
+
+// A5 admission by one 1024-thread CTA over the ranked keys (see k_admit).
+struct AdmitSmem {
+    unsigned long long w64[32];
+    uint32_t w32[32];
+};
+
+__device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const StepArgs& a,
+                                          const uint64_t* keys, uint64_t n_elig, uint64_t pinned,
+                                          AdmitSmem& sm) {
+    constexpr int NT = 1024;
+    Ctl* ctl = b.ctl;
+    const Pool& P = b.pool;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t n_prev = ctl->n_admitted;
+    const uint64_t budget = a.kv_total > pinned ? a.kv_total - pinned : 0ull;
+    uint64_t Wn = n_elig < a.max_batch ? n_elig : a.max_batch;
+    if (budget < Wn) Wn = budget;
+    const uint64_t idmask = (1ull << c.IB) - 1ull;
+    const uint32_t par = a.parity, prev = par ^ 1u;
+
+    // prefetch the previous admitted list (independent of the ranking)
+    uint32_t pslot = 0, pw = 0;
+    if (tid < n_prev) {
+        pslot = b.adm_slot[prev][tid];
+        pw = P.sfc[pslot];
+    }
+    unsigned long long carry = 0;
+    uint32_t cut = 0;
+    for (uint32_t base = 0; base < Wn; base += NT) {
+        const uint32_t k = base + tid;
+        uint32_t slot = 0;
+        uint64_t idoff = 0;
+        unsigned long long dem = 0;
+        if (k < Wn) {
+            idoff = keys[k] & idmask;
+            slot = (uint32_t)((a.id_base + idoff) & c.cap_mask);
+            dem = blk((uint64_t)P.ctx[slot] + 1u, c);
+        }
+        unsigned long long tot;
+        const unsigned long long incl = carry + block_excl_scan_u64<NT>(dem, sm.w64, &tot) + dem;
+        const bool fit = k < Wn && incl <= budget;
+        const uint32_t nfit = (uint32_t)__syncthreads_count(fit);
+        if (fit) {
+            const uint32_t w = P.sfc[slot];
+            b.adm_slot[par][k] = slot;
+            b.adm_id[par][k] = a.id_base + idoff;
+            b.adm_strat[par][k] = (uint8_t)sfc_strat(w);
+            P.stamp[slot] = a.step;
+            P.sfc[slot] = (w & 0xffffu) | SFC_RAN;  // StarvationCnt <- 0; runs this iteration
+            if (k == base + nfit - 1) ctl->budget_used = incl;
+        }
+        cut += nfit;
+        carry += tot;
+        const uint32_t chunk = (uint32_t)min((uint64_t)NT, Wn - base);
+        if (nfit < chunk) break;
+    }
+    if (tid == 0 && cut == 0) ctl->budget_used = 0;
+    __syncthreads();
+
+    // preempted: admitted last step, still READY, not admitted now (previous rank order)
+    uint32_t npre = 0;
+    for (uint32_t base = 0; base < n_prev; base += NT) {
+        const uint32_t k = base + tid;
+        uint32_t f = 0;
+        if (k < n_prev) {
+            const uint32_t s = base ? b.adm_slot[prev][k] : pslot;
+            const uint32_t w = base ? P.sfc[s] : pw;
+            f = (sfc_state(w) == ST_READY && P.stamp[s] != a.step) ? 1u : 0u;
+        }
+        uint32_t tot;
+        const uint32_t pos = block_excl_scan_u32<NT>(f, sm.w32, &tot);
+        if (f) b.pre_id[npre + pos] = b.adm_id[prev][k];
+        npre += tot;
+    }
+    if (tid == 0) {
+        ctl->n_admitted = cut;
+        ctl->n_preempted = npre;
+        ctl->blocked_head = (n_elig > 0 && cut == 0) ? 1u : 0u;
+        ctl->budget = budget;
+        ctl->n_elig_out = n_elig;
+        ctl->pinned_out = pinned;
+        ctl->n_elig = 0;  // accumulators of the next step
+        ctl->pinned = 0;
+    }
+}
+
+}  // namespace lamps
