@@ -67,6 +67,8 @@ extern "C" {
 /* ---- config flags --------------------------------------------------------- */
 #define LAMPS_DEBUG_OUT 1u /* keep per-slot W_P, W_D, W_S and score for export */
 #define LAMPS_TIMING 2u    /* record CUDA events around each phase (lamps_timing_read) */
+#define LAMPS_MULTI_KERNEL 4u   /* use the 3-kernel path even where the fused step kernel fits */
+#define LAMPS_FORCE_FALLBACK 8u /* fused path: always take the global-LSD fallback (tests) */
 
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 

@@ -1,0 +1,356 @@
+// kernels_fused.cu -- the whole scheduling step (A0 default update .. A5) as
+// ONE cooperative kernel, one 1024-thread CTA per SM, for pools whose per-SM
+// share of keys fits in shared memory (capacity <= #SM * kKcap).
+//
+//   S  score: each CTA scores its contiguous range of slots (A0 fused, A1, A2,
+//      A3, key) and keeps its keys in shared memory
+//   H  bucket histogram of its keys; the bucket is an exact monotone function
+//      of the key, (starving, bit length of the score, next kBucketM score
+//      bits) -- "float-like" buckets adapt to the dynamic range of the scores
+//   -- barrier --
+//   T  transposed count exchange: CTA c scans buckets j = c (mod G) over all
+//      CTAs (exclusive prefix per CTA, total per bucket)
+//   -- barrier --
+//   X  bucket bases (scan of the totals) and scatter of the keys into bucket
+//      order in global memory; every CTA derives the bucket-aligned key range
+//      it will sort
+//   -- barrier --
+//   L  each CTA loads its range (<= kKcap keys) into shared memory and LSD
+//      radix-sorts it there (8-bit digits over the bits that vary within the
+//      range, stable warp multisplit); writes the final ranked keys.  If any
+//      range exceeds kKcap (a huge bucket of near-equal scores) every CTA runs
+//      the grid-synchronous global LSD sort instead (sort_dev.cuh).
+//   A  CTA 0 admits (A5) as soon as the head of the order it needs is sorted.
+#include "sort_dev.cuh"
+#include "step_dev.cuh"
+
+namespace lamps {
+
+namespace {
+
+constexpr int kFT = 1024;                   // threads per CTA
+constexpr int kFW = kFT / 32;               // warps
+constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
+constexpr int kBucketM = 7;                 // score bits per octave
+constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
+constexpr int kLocalItems = kKcap / kFT;    // 12
+
+struct PhaseS {                  // S, H, T, X
+    uint64_t kbuf[kKcap];        // 96 KB: this CTA's keys
+    uint32_t cnt[kMaxBuckets];   // 58 KB: bucket counts -> scatter cursors
+    uint32_t w32[kFW];
+    unsigned long long red[3][kFW];
+    uint32_t nk, base;
+};
+struct PhaseL {                  // L
+    uint64_t a[kKcap];           // 96 KB
+    uint64_t b[kKcap];           // 96 KB
+    uint16_t whist[kFW][kBins];  // 16 KB
+    uint32_t part[4][kBins];     // 4 KB
+    uint32_t texcl[kBins];
+    uint32_t scan[kFW];
+    unsigned long long red[2][kFW];
+};
+union FusedSmem {
+    PhaseS s;
+    PhaseL l;
+    SortSmem g;
+    AdmitSmem adm;
+};
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint32_t half) {
+    const uint32_t ns = (uint32_t)(key >> (c.SB + c.IB)) & 1u;  // 1 = not starving
+    const uint64_t sc = (key >> c.IB) & c.score_max;
+    const uint32_t e = 64u - (uint32_t)__clzll((long long)sc);  // bit length
+    uint32_t fb;
+    if (e <= (uint32_t)kBucketM)
+        fb = (uint32_t)sc;
+    else
+        fb = ((e - kBucketM) << kBucketM) + (uint32_t)((sc >> (e - 1 - kBucketM)) & ((1u << kBucketM) - 1));
+    return ns * half + fb;
+}
+
+// stable LSD sort of n keys in shared memory (src -> alternating), returns the buffer holding the result
+__device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned long long vary) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint64_t* src = sm.a;
+    uint64_t* dst = sm.b;
+    const uint32_t per_warp = 32u * kLocalItems;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int dpos = 0; dpos < kDigits; dpos++) {
+        if (!((vary >> (8 * dpos)) & 0xffull)) continue;
+        const uint32_t shift = 8u * dpos;
+        for (uint32_t i = tid; i < kFW * kBins; i += kFT) (&sm.whist[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t pk[kLocalItems];  // digit << 16 | rank (digit 256 = empty)
+#pragma unroll
+        for (int j = 0; j < kLocalItems; j++) {
+            const uint32_t li = warp * per_warp + j * 32 + lane;
+            const uint32_t d = li < n ? (uint32_t)(src[li] >> shift) & 0xffu : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t leader = __ffs(peers) - 1u;
+            uint32_t prior = 0;
+            if (d < 256u && lane == leader) {
+                prior = sm.whist[warp][d];
+                sm.whist[warp][d] = (uint16_t)(prior + __popc(peers));
+            }
+            prior = __shfl_sync(0xffffffffu, prior, leader);
+            pk[j] = (d << 16) | (prior + __popc(peers & lt_mask));
+            __syncwarp();
+        }
+        __syncthreads();
+        // per digit: exclusive prefix over the 32 warps, 4 threads per digit (8 warps each)
+        {
+            const uint32_t d = tid & 255u, q = tid >> 8;
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < kFW / 4; w++) run += sm.whist[q * (kFW / 4) + w][d];
+            sm.part[q][d] = run;
+            __syncthreads();
+            uint32_t before = 0, tot = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; qq++) {
+                const uint32_t v = sm.part[qq][d];
+                before += (uint32_t)qq < q ? v : 0u;
+                tot += v;
+            }
+#pragma unroll
+            for (int w = 0; w < kFW / 4; w++) {
+                uint16_t& h = sm.whist[q * (kFW / 4) + w][d];
+                const uint32_t v = h;
+                h = (uint16_t)before;
+                before += v;
+            }
+            const uint32_t e = digit_excl_scan(sm.scan, tid < kBins ? tot : 0u);
+            if (tid < kBins) sm.texcl[tid] = e;
+            __syncthreads();
+        }
+#pragma unroll
+        for (int j = 0; j < kLocalItems; j++) {
+            const uint32_t d = pk[j] >> 16;
+            if (d < 256u) {
+                const uint32_t li = warp * per_warp + j * 32 + lane;
+                dst[sm.texcl[d] + sm.whist[warp][d] + (pk[j] & 0xffffu)] = src[li];
+            }
+        }
+        __syncthreads();
+        uint64_t* t = src; src = dst; dst = t;
+    }
+    return src;
+}
+
+template <bool DBG>
+__global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
+    Ctl* ctl = b.ctl;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t G = gridDim.x, bid = blockIdx.x;
+    const uint32_t half = (c.SB <= (uint32_t)kBucketM) ? (1u << c.SB) : ((c.SB - kBucketM + 1u) << kBucketM);
+    const uint32_t NB = 2u * half;
+    uint32_t* H = b.blocksum;  // [G][NB] bucket counts -> exclusive prefix over CTAs
+    uint32_t* T = b.blocksum + (size_t)G * NB;  // [NB] bucket totals
+
+    // ---------------- S: score this CTA's slots, keys into shared memory
+    if (tid == 0) sm.s.nk = 0;
+    for (uint32_t i = tid; i < NB; i += kFT) sm.s.cnt[i] = 0;
+    __syncthreads();
+    const uint32_t ngroups = (c.cap + 3u) >> 2;
+    const uint32_t gpc = (ngroups + G - 1) / G;
+    const uint32_t g_lo = min(ngroups, bid * gpc), g_hi = min(ngroups, g_lo + gpc);
+    unsigned long long pinned = 0, kor = 0, kand = ~0ull;
+    for (uint32_t g0 = g_lo; g0 < g_hi; g0 += kFT) {
+        const uint32_t g = g0 + tid;
+        uint64_t key[4];
+        uint32_t nk = 0;
+        if (g < g_hi) nk = score_group<DBG>(b.pool, c, a.id_base_mod, b.dbg, g, key, pinned);
+        uint32_t tot;
+        const uint32_t off = block_excl_scan_u32<kFT>(nk, sm.s.w32, &tot);
+        const uint32_t base = sm.s.nk;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if ((uint32_t)j < nk) {
+                sm.s.kbuf[base + off + j] = key[j];
+                kor |= key[j];
+                kand &= key[j];
+                atomicAdd(&sm.s.cnt[bucket_of(key[j], c, half)], 1u);
+            }
+        __syncthreads();
+        if (tid == 0) sm.s.nk = base + tot;
+        __syncthreads();
+    }
+    const uint32_t nk_cta = sm.s.nk;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+        kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+    }
+    if (lane == 0) {
+        sm.s.red[0][warp] = pinned;
+        sm.s.red[1][warp] = kor;
+        sm.s.red[2][warp] = kand;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t = 0, o = 0, n = ~0ull;
+        for (int w = 0; w < kFW; w++) {
+            t += sm.s.red[0][w];
+            o |= sm.s.red[1][w];
+            n &= sm.s.red[2][w];
+        }
+        b.pin_part[bid] = t;
+        b.kmask[bid] = o;
+        b.kmask[G + bid] = n;
+    }
+    // ---------------- H: publish this CTA's bucket counts
+    for (uint32_t j = tid; j < NB; j += kFT) H[(size_t)bid * NB + j] = sm.s.cnt[j];
+    grid_barrier(ctl, G);
+
+    // ---------------- T: buckets j = bid (mod G): exclusive prefix over CTAs, total
+    for (uint32_t j = bid + warp * G; j < NB; j += kFW * G) {
+        uint32_t carry = 0;
+        for (uint32_t r0 = 0; r0 < G; r0 += 32) {
+            const uint32_t r = r0 + lane;
+            const uint32_t v = r < G ? __ldcg(&H[(size_t)r * NB + j]) : 0u;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (r < G) H[(size_t)r * NB + j] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) T[j] = carry;
+    }
+    grid_barrier(ctl, G);
+
+    // ---------------- X: bucket bases, scatter into bucket order, ranges
+    // cursor(j) = start(j) + keys of bucket j in CTAs before this one, start = excl-scan of T
+    {
+        const uint32_t per = (NB + kFT - 1) / kFT;
+        const uint32_t j0 = min(NB, tid * per), j1 = min(NB, j0 + per);
+        uint32_t s = 0;
+        for (uint32_t j = j0; j < j1; j++) s += __ldcg(&T[j]);
+        uint32_t tot;
+        uint32_t run = block_excl_scan_u32<kFT>(s, sm.s.w32, &tot);
+        for (uint32_t j = j0; j < j1; j++) {
+            sm.s.cnt[j] = run + __ldcg(&H[(size_t)bid * NB + j]);
+            run += __ldcg(&T[j]);
+        }
+        if (tid == 0) sm.s.base = tot;  // total number of keys
+    }
+    __syncthreads();
+    const uint32_t n = sm.s.base;
+    for (uint32_t i = tid; i < nk_cta; i += kFT) {
+        const uint64_t k = sm.s.kbuf[i];
+        const uint32_t pos = atomicAdd(&sm.s.cnt[bucket_of(k, c, half)], 1u);  // order within a bucket is free
+        b.keys[0][pos] = k;
+    }
+    __syncthreads();
+    {   // start(j) again (the cursors were consumed)
+        const uint32_t per = (NB + kFT - 1) / kFT;
+        const uint32_t j0 = min(NB, tid * per), j1 = min(NB, j0 + per);
+        uint32_t s = 0;
+        for (uint32_t j = j0; j < j1; j++) s += __ldcg(&T[j]);
+        uint32_t tot;
+        uint32_t run = block_excl_scan_u32<kFT>(s, sm.s.w32, &tot);
+        for (uint32_t j = j0; j < j1; j++) {
+            sm.s.cnt[j] = run;
+            run += __ldcg(&T[j]);
+        }
+    }
+    __syncthreads();
+    // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
+    // bucket with start >= q_r by binary search; the largest range decides the fallback
+    uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now
+    if (tid <= G) {
+        const uint32_t q = (uint32_t)(((uint64_t)tid * n) / G);
+        uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sm.s.cnt[mid] >= q) hi = mid; else lo = mid + 1;
+        }
+        rb[tid] = (tid == G || lo == NB) ? n : sm.s.cnt[lo];
+    }
+    __syncthreads();
+    uint32_t mx = 0;
+    if (tid < G) mx = rb[tid + 1] - rb[tid];
+    const bool fallback = (a.flags & kStepForceFallback) ||
+                          __syncthreads_or(mx > (uint32_t)kKcap);
+    const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
+    grid_barrier(ctl, G);
+
+    // ---------------- L: sort the key ranges
+    uint32_t final_buf, passes;
+    if (!fallback) {
+        const uint32_t rn = r_hi - r_lo;
+        for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
+        unsigned long long o = 0, an = ~0ull;
+        for (uint32_t i = tid; i < rn; i += kFT) { o |= sm.l.a[i]; an &= sm.l.a[i]; }
+#pragma unroll
+        for (int s = 16; s; s >>= 1) {
+            o |= __shfl_xor_sync(0xffffffffu, o, s);
+            an &= __shfl_xor_sync(0xffffffffu, an, s);
+        }
+        if (lane == 0) { sm.l.red[0][warp] = o; sm.l.red[1][warp] = an; }
+        __syncthreads();
+        o = 0; an = ~0ull;
+        for (int w = 0; w < kFW; w++) { o |= sm.l.red[0][w]; an &= sm.l.red[1][w]; }
+        __syncthreads();
+        const uint64_t* res = local_lsd(sm.l, rn, rn ? (o ^ an) : 0ull);
+        for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = res[i];
+        final_buf = 1;
+        passes = 1;
+    } else {
+        passes = lsd_sort_global(b, n, b.kmask, G, sm.g);
+        final_buf = passes & 1u;
+    }
+
+    // ---------------- A: admission by CTA 0
+    // CTA 0 may start as soon as the head it needs is sorted: without the fallback
+    // the keys [0, rb[1]) are sorted by CTA 0 itself.
+    const uint32_t need = min(n, a.max_batch);
+    const bool wait = fallback || r_end0 < need;
+    if (wait) grid_barrier(ctl, G);
+    if (bid != 0) return;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t = 0;
+        for (uint32_t i = 0; i < G; i++) t += __ldcg(&b.pin_part[i]);
+        sm.adm.w64[0] = t;
+        ctl->n_passes = passes;
+        ctl->final_buf = final_buf;
+        ctl->fallbacks += fallback ? 1u : 0u;
+    }
+    __syncthreads();
+    const unsigned long long pinned_all = sm.adm.w64[0];
+    __syncthreads();
+    admit_cta(b, c, a, b.keys[final_buf], n, pinned_all, sm.adm);
+}
+
+}  // namespace
+
+size_t fused_smem_bytes() { return sizeof(FusedSmem); }
+
+int fused_blocks_per_sm() {
+    int nb = 0;
+    cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
+    cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused<false>, kFT, sizeof(FusedSmem));
+    return nb;
+}
+
+uint32_t fused_max_buckets() { return kMaxBuckets; }
+
+cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t grid, cudaStream_t s) {
+    Bufs bb = b;
+    Cost cc = c;
+    StepArgs aa = a;
+    void* args[] = {&bb, &cc, &aa};
+    const void* fn = b.dbg ? (const void*)k_fused<true> : (const void*)k_fused<false>;
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFT), args, sizeof(FusedSmem), s);
+}
+
+}  // namespace lamps

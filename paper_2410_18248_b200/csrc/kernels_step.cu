@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Bufs b, Cost c, StepArg
 __global__ void __launch_bounds__(kAdmitThreads) k_admit(Bufs b, Cost c, StepArgs a) {
     __shared__ AdmitSmem sm;
     const Ctl* ctl = b.ctl;
-    admit_cta(b, c, a, b.keys[ctl->n_passes & 1u], ctl->n_elig, ctl->pinned, sm);
+    admit_cta(b, c, a, b.keys[ctl->final_buf & 1u], ctl->n_elig, ctl->pinned, sm);
 }
 
 // ---------------------------------------------------------------------------

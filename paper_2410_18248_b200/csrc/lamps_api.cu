@@ -57,7 +57,8 @@ struct lamps_s {
     cudaStream_t stream = nullptr;
     Cost cost{};
     Bufs b{};
-    uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0;
+    uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
+    bool fused = false;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
     void* d_ingest = nullptr;
@@ -130,8 +131,12 @@ size_t carve(lamps_t* h, uint8_t* base) {
     for (int i = 0; i < 8; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
     size_t o_keys0 = L.take(((size_t)cap_pad + kSortTile) * 8);
     size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
-    size_t o_kmask = L.take((size_t)2 * h->score_grid * 8);
-    size_t o_bsum = L.take((size_t)2 * h->sort_grid * kBins * 4);
+    const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
+    size_t o_kmask = L.take((size_t)2 * gmax * 8);
+    size_t o_pin = L.take((size_t)gmax * 8);
+    const size_t bsum_lsd = (size_t)2 * gmax * kBins * 4;
+    const size_t bsum_fused = h->fused ? ((size_t)h->fused_grid + 1) * fused_max_buckets() * 4 : 0;
+    size_t o_bsum = L.take(std::max(bsum_lsd, bsum_fused));
     size_t o_ctl = L.take(sizeof(Ctl));
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
     size_t o_ai0 = L.take((size_t)mb * 8), o_ai1 = L.take((size_t)mb * 8);
@@ -148,6 +153,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.keys[0] = reinterpret_cast<uint64_t*>(base + o_keys0);
     h->b.keys[1] = reinterpret_cast<uint64_t*>(base + o_keys1);
     h->b.kmask = reinterpret_cast<unsigned long long*>(base + o_kmask);
+    h->b.pin_part = reinterpret_cast<unsigned long long*>(base + o_pin);
     h->b.blocksum = reinterpret_cast<uint32_t*>(base + o_bsum);
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;
@@ -171,14 +177,24 @@ size_t carve(lamps_t* h, uint8_t* base) {
 // size query (phase 1 of lamps_init) assumes the largest B200 grids so the
 // reported size is an upper bound.
 void grids(lamps_t* h, bool query_device) {
-    int sms = 148, score_occ = 8, sort_occ = 1;
+    int sms = 148, sort_occ = 1, fused_occ = 1;
     if (query_device) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         sort_occ = sort_blocks_per_sm();
+        fused_occ = fused_blocks_per_sm();
     }
-    (void)score_occ;
+    h->fused_grid = (uint32_t)std::max(1, sms * std::max(fused_occ, 1));
+    {
+        const uint32_t groups = (h->cap + 3) / 4;
+        const uint32_t gpc = (groups + h->fused_grid - 1) / h->fused_grid;
+        h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && gpc * 4u <= (uint32_t)kFusedKcap && fused_occ >= 1;
+    }
+    if (!query_device) {  // size query: assume the fused path may be chosen
+        h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && h->cap <= 148u * (uint32_t)kFusedKcap;
+        h->fused_grid = std::max<uint32_t>(h->fused_grid, 296u);
+    }
     const uint32_t groups = (h->cap + 3) / 4;
     const uint32_t want = (groups + kScoreThreads - 1) / kScoreThreads;
     h->score_grid = std::max<uint32_t>(1, std::min<uint32_t>(want, (uint32_t)sms * 7));
@@ -232,20 +248,27 @@ int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.max_batch = h->cfg.max_batch;
     a.parity = h->step & 1u;
     h->last_id_base = h->id_base;
+    a.flags = (h->cfg.flags & LAMPS_FORCE_FALLBACK) ? kStepForceFallback : 0u;
     record_timing(h, 0);
     CU(h, launch_events(h->b, h->cost, a, h->stream));
     record_timing(h, 1);
-    CU(h, launch_score(h->b, h->cost, a, (int)h->score_grid, h->stream));
-    record_timing(h, 2);
-    CU(h, launch_sort(h->b, h->cost, a, h->stream));
-    record_timing(h, 3);
-    CU(h, launch_admit(h->b, h->cost, a, h->stream));
+    if (h->fused) {
+        CU(h, launch_fused(h->b, h->cost, a, h->fused_grid, h->stream));
+        record_timing(h, 2);
+        record_timing(h, 3);
+    } else {
+        CU(h, launch_score(h->b, h->cost, a, (int)h->score_grid, h->stream));
+        record_timing(h, 2);
+        CU(h, launch_sort(h->b, h->cost, a, h->stream));
+        record_timing(h, 3);
+        CU(h, launch_admit(h->b, h->cost, a, h->stream));
+    }
     record_timing(h, 4);
     if (timing) {
         h->t_head = (h->t_head + 1) % kTimingRing;
         h->t_count++;
     }
-    h->last_kernels = 3 + (n_ev ? 1 : 0);
+    h->last_kernels = (h->fused ? 1 : 3) + (n_ev ? 1 : 0);
     h->have_result = true;
     return LAMPS_OK;
 }
@@ -280,7 +303,7 @@ int fetch_result(lamps_t* h, lamps_step_out* out) {
         out->admitted_ids = h->h_adm_ids;
         out->admitted_strategy = h->h_adm_strat;
         out->preempted_ids = h->h_pre_ids;
-        out->d_ranked_keys = h->b.keys[C.n_passes & 1u];
+        out->d_ranked_keys = h->b.keys[C.final_buf & 1u];
         out->d_admitted_slots = h->b.adm_slot[par];
     }
     return LAMPS_OK;
@@ -325,7 +348,8 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     h->cap_pad = tmp.cap_pad;
     h->ws = static_cast<uint8_t*>(d_workspace);
     grids(h, true);
-    if (h->sort_grid > tmp.sort_grid || h->score_grid > tmp.score_grid) {
+    if (h->sort_grid > tmp.sort_grid || h->score_grid > tmp.score_grid ||
+        (h->fused && (!tmp.fused || h->fused_grid > tmp.fused_grid))) {
         delete h;
         return LAMPS_ENOTSUP;  // device larger than the sizing assumption
     }
@@ -616,7 +640,7 @@ int lamps_ranked_keys(lamps_t* h, uint64_t* host_out, uint64_t max_keys, uint64_
     *n_out = n;
     if (host_out && max_keys) {
         const uint64_t m = std::min(n, max_keys);
-        if (m) CU(h, cudaMemcpy(host_out, h->b.keys[h->h_ctl->n_passes & 1u], m * 8, cudaMemcpyDeviceToHost));
+        if (m) CU(h, cudaMemcpy(host_out, h->b.keys[h->h_ctl->final_buf & 1u], m * 8, cudaMemcpyDeviceToHost));
     }
     return LAMPS_OK;
 }

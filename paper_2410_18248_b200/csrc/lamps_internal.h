@@ -17,6 +17,8 @@ constexpr int kSortMaxTilesPerCta = 8;               // capacity <= 2^23 over >=
 constexpr int kScoreThreads = 256;  // K1 CTA
 constexpr int kAdmitThreads = 1024; // K3 (single CTA)
 constexpr int kMaxBatch = 16384;
+constexpr int kFusedKcap = 12288;    // keys per SM kept in shared memory by the fused step kernel
+constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
 
 // Device control block: per-step counters, the sort plan and the step summary.
 struct Ctl {
@@ -25,8 +27,10 @@ struct Ctl {
     uint32_t pad0;
     unsigned long long pinned;       // sum over PAUSED_P of blk(ctx)
     // ---- sort (K2)
-    uint32_t n_passes;               // radix passes that did work (K2 block 0)
-    uint32_t bar_count, bar_gen;     // K2 grid barrier
+    uint32_t n_passes;               // radix passes that did work
+    uint32_t final_buf;              // keys[final_buf] holds the ranked order
+    uint32_t fallbacks;              // fused steps that needed the global LSD fallback
+    uint32_t bar_count, bar_gen;     // grid barrier of the cooperative kernels
     // ---- summary (K3)
     uint32_t n_admitted, n_preempted, blocked_head, n_prev;
     unsigned long long budget, budget_used;
@@ -42,13 +46,15 @@ struct StepArgs {
     uint32_t n_ev;
     uint32_t max_batch;
     uint32_t parity;        // admitted list buffer written this step
+    uint32_t flags;         // kStepForceFallback
 };
 
 struct Bufs {
     Pool pool;
     Ctl* ctl;
-    unsigned long long* kmask;   // [2][score_grid]  per-K1-block OR / AND of its keys
-    uint32_t* blocksum;      // [2][sort_grid][kBins]  per-K2-block digit counts, by pass parity
+    unsigned long long* kmask;   // [2][max(score_grid, sort_grid)] per-block OR / AND of keys
+    unsigned long long* pin_part;  // [sort_grid] per-CTA pinned sums (fused kernel)
+    uint32_t* blocksum;      // LSD: [2][grid][kBins] digit counts; fused: [grid+1][buckets]
     uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity
@@ -65,6 +71,10 @@ cudaError_t launch_score(const Bufs& b, const Cost& c, const StepArgs& a, int gr
                          cudaStream_t s);
 cudaError_t launch_sort(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 int sort_blocks_per_sm();  // occupancy of the persistent sort kernel
+size_t fused_smem_bytes();
+int fused_blocks_per_sm();
+uint32_t fused_max_buckets();
+cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t grid, cudaStream_t s);
 cudaError_t launch_admit(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 
 // ingest records (host -> device staging)

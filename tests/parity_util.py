@@ -8,9 +8,12 @@ FIELDS = ("state", "has_api", "starving", "strategy", "cnt", "ctx", "pre_rem", "
           "resp_len", "post_len", "pending")
 
 
-def make_pair(cfg: dict, debug=True):
+PATH_FLAGS = {"fused": 0, "multi": 4, "fallback": 8}  # LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK
+
+
+def make_pair(cfg: dict, debug=True, path="fused"):
     from paper_2410_18248_b200 import Scheduler, LAMPS_DEBUG_OUT
-    s = Scheduler(cfg, flags=LAMPS_DEBUG_OUT if debug else 0)
+    s = Scheduler(cfg, flags=(LAMPS_DEBUG_OUT if debug else 0) | PATH_FLAGS[path])
     o = O.OraclePool(cfg)
     return s, o
 
@@ -68,13 +71,13 @@ def compare_state(s, o, r=None, where=""):
         assert np.array_equal(e["strategy"][ready], r["strategy"][ready].astype(np.uint32)), where
 
 
-def snapshot_step_parity(cname, seed=0, id_base=0, steps=3, debug=True, **over):
+def snapshot_step_parity(cname, seed=0, id_base=0, steps=3, debug=True, path="fused", **over):
     cfg = gen.lib_config(cname, **{k: v for k, v in over.items() if k in ("max_batch", "starvation_threshold", "score_bits", "id_bits")})
     snap = gen.snapshot(cname, seed=seed, id_base=id_base,
                         **{k: v for k, v in over.items() if k in ("n", "capacity")})
     if "capacity" in over:
         cfg["capacity"] = over["capacity"]
-    s, o = make_pair(cfg, debug=debug)
+    s, o = make_pair(cfg, debug=debug, path=path)
     load_both(s, o, snap)
     kv = over.get("kv_total", gen.CONFIGS[cname]["kv_total"])
     outs = []

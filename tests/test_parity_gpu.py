@@ -16,32 +16,61 @@ from parity_util import (compare_outputs, compare_state, load_both, make_pair, s
 pytestmark = pytest.mark.gpu
 
 
+PATHS = ["fused", "multi", "fallback"]
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("cname,seed,id_base", [
     ("C1", 0, 0), ("C1", 1, 5), ("C2", 0, 0), ("C2", 1, 12345), ("C3", 0, 0), ("C3", 2, 777),
     ("C4", 0, 0), ("C4", 1, 3 * 131072 + 17),
 ])
-def test_snapshot_parity(cname, seed, id_base):
-    snapshot_step_parity(cname, seed=seed, id_base=id_base, steps=3)
+def test_snapshot_parity(cname, seed, id_base, path):
+    snapshot_step_parity(cname, seed=seed, id_base=id_base, steps=3, path=path)
 
 
 @pytest.mark.slow
-def test_c5_full_size_parity():
+@pytest.mark.parametrize("path", ["fused", "multi"])
+def test_c5_full_size_parity(path):
     # BASELINE.json's 1M-request pool in the launch configuration bench.py times
-    snapshot_step_parity("C5", seed=0, id_base=(1 << 20) * 7 + 99, steps=2)
+    snapshot_step_parity("C5", seed=0, id_base=(1 << 20) * 7 + 99, steps=2, path=path)
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 2047, 2048, 2049, 4095, 4096, 4097, 6143])
-def test_tile_boundaries(n):
-    # ragged tails around the 2048-key sort tile and the 1024-slot score tile
-    snapshot_step_parity("C2", seed=n, n=n, capacity=8192, steps=2)
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("n", [1, 2, 5, 1023, 1024, 1025, 8191, 8192, 8193, 12287, 12288, 12289, 30000])
+def test_tile_boundaries(n, path):
+    # ragged tails around the 8192-key sort tile, the 12288-key shared-memory range and
+    # the 1024-thread score rounds
+    snapshot_step_parity("C2", seed=n, n=n, capacity=32768, steps=2, path=path)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("cap", [1, 2, 4, 8])
-def test_tiny_capacity(cap):
-    snapshot_step_parity("C1", seed=cap, n=cap, capacity=cap, steps=3)
+def test_tiny_capacity(cap, path):
+    snapshot_step_parity("C1", seed=cap, n=cap, capacity=cap, steps=3, path=path)
 
 
-def _custom(cfg_over, recs, kv, steps=2, id_base=0):
+@pytest.mark.parametrize("path", ["fused", "multi"])
+def test_equal_scores_large_bucket(path):
+    # 40000 identical requests: one bucket far larger than a shared-memory range,
+    # so the fused kernel must take its in-kernel global LSD fallback; order = ids
+    n = 40000
+    snap = gen.snapshot("C4", seed=9, n=n, capacity=65536, id_base=65536 * 3 + 5)
+    for f, v in (("state", 1), ("has_api", 1), ("ctx", 700), ("pre_rem", 40), ("api_ticks", 500000),
+                 ("resp_len", 96), ("post_len", 30), ("pending", 0), ("starving", 0), ("cnt", 3)):
+        live = snap["state"] != 0
+        snap[f][live] = v
+    cfg = gen.lib_config("C4")
+    cfg["capacity"] = 65536
+    from parity_util import compare_outputs, compare_state, load_both, make_pair
+    s, o = make_pair(cfg, debug=False, path=path)
+    load_both(s, o, snap)
+    for t in range(2):
+        g, r = s.step(kv_total=10000), o.step(kv_total=10000)
+        compare_outputs(s, g, r, where=f"equal t={t}")
+    compare_state(s, o)
+
+
+def _custom(cfg_over, recs, kv, steps=2, id_base=0, path="fused"):
     cfg = gen.lib_config("C1")
     cfg.update(cfg_over)
     cap = cfg["capacity"]
@@ -54,7 +83,7 @@ def _custom(cfg_over, recs, kv, steps=2, id_base=0):
             snap[k][sl] = v
         snap["state"][sl] = r.get("state", O.READY)
     snap["id_base"], snap["next_id"] = id_base, id_base + len(recs)
-    s, o = make_pair(cfg)
+    s, o = make_pair(cfg, path=path)
     load_both(s, o, snap)
     for t in range(steps):
         g, r = s.step(kv_total=kv), o.step(kv_total=kv, debug=True)
@@ -63,43 +92,49 @@ def _custom(cfg_over, recs, kv, steps=2, id_base=0):
     return g
 
 
-def test_empty_pool_and_zero_budget():
-    g = _custom(dict(capacity=16), [], kv=10)
+@pytest.mark.parametrize("path", PATHS)
+def test_empty_pool_and_zero_budget(path):
+    g = _custom(dict(capacity=16), [], kv=10, path=path)
     assert g["n_eligible"] == 0 and g["blocked_head"] == 0
     recs = [dict(ctx=10, pre_rem=5) for _ in range(5)]
-    g = _custom(dict(capacity=16), recs, kv=0)
+    g = _custom(dict(capacity=16), recs, kv=0, path=path)
     assert g["n_admitted"] == 0 and g["blocked_head"] == 1
 
 
-def test_all_equal_scores_break_ties_by_id():
+@pytest.mark.parametrize("path", PATHS)
+def test_all_equal_scores_break_ties_by_id(path):
     recs = [dict(ctx=100, pre_rem=50, has_api=1, api_ticks=10 ** 6, resp_len=8, post_len=9) for _ in range(16)]
-    g = _custom(dict(capacity=16, max_batch=7), recs, kv=10 ** 6, id_base=(1 << 30) + 3)
+    g = _custom(dict(capacity=16, max_batch=7), recs, kv=10 ** 6, id_base=(1 << 30) + 3, path=path)
     assert list(g["admitted_id"]) == list(range((1 << 30) + 3, (1 << 30) + 10))
 
 
-def test_all_starving_and_threshold_boundary():
+@pytest.mark.parametrize("path", PATHS)
+def test_all_starving_and_threshold_boundary(path):
     recs = [dict(ctx=50 + i, pre_rem=10 * i, starving=1) for i in range(8)]
     recs += [dict(ctx=5, pre_rem=1, cnt=99), dict(ctx=5, pre_rem=1, cnt=100)]
-    _custom(dict(capacity=16, max_batch=3, starvation_threshold=100), recs, kv=10 ** 4, steps=4)
+    _custom(dict(capacity=16, max_batch=3, starvation_threshold=100), recs, kv=10 ** 4, steps=4, path=path)
 
 
-def test_max_batch_one_and_misprediction():
+@pytest.mark.parametrize("path", PATHS)
+def test_max_batch_one_and_misprediction(path):
     recs = [dict(ctx=10 * i, pre_rem=0, has_api=1, api_ticks=5, resp_len=3, post_len=2) for i in range(6)]
-    _custom(dict(capacity=8, max_batch=1), recs, kv=10 ** 4, steps=6)
+    _custom(dict(capacity=8, max_batch=1), recs, kv=10 ** 4, steps=6, path=path)
 
 
-def test_score_saturation_and_narrow_id_window():
+@pytest.mark.parametrize("path", PATHS)
+def test_score_saturation_and_narrow_id_window(path):
     recs = [dict(ctx=1000 + i, pre_rem=400, has_api=1, api_ticks=10 ** 9, resp_len=8, post_len=100)
             for i in range(16)]
-    _custom(dict(capacity=16, score_bits=12, id_bits=4), recs, kv=10 ** 4, id_base=2 ** 40 + 11)
+    _custom(dict(capacity=16, score_bits=12, id_bits=4), recs, kv=10 ** 4, id_base=2 ** 40 + 11, path=path)
 
 
-def test_extreme_cost_constants_saturate_like_the_oracle():
+@pytest.mark.parametrize("path", PATHS)
+def test_extreme_cost_constants_saturate_like_the_oracle(path):
     big = (1 << 48) - 1
     recs = [dict(ctx=(1 << 24) - 5 * i, pre_rem=3000 * i, has_api=1, api_ticks=(1 << 32) - 1 - i,
                  resp_len=7 * i, post_len=1000, pending=(1 << 32) - 1) for i in range(8)]
     _custom(dict(capacity=8, A1=big, A2=big, S0=big, S1=big, tau=big, c_other=(1 << 32) - 1, SH=3,
-                 score_bits=50, id_bits=13, kv_capacity_blocks=1 << 62), recs, kv=1 << 40)
+                 score_bits=50, id_bits=13, kv_capacity_blocks=1 << 62), recs, kv=1 << 40, path=path)
 
 
 def test_quantiser_parity_through_submit():
@@ -146,10 +181,10 @@ def test_ingest_errors_match_oracle():
     assert s.step_rc(None, 101) == O.EINVAL and o.step(None, 101)["rc"] == O.EINVAL
 
 
-def closed_loop(cname, n_req, steps, initial, per_step, kv=None, seed=0, state_every=10, **over):
+def closed_loop(cname, n_req, steps, initial, per_step, kv=None, seed=0, state_every=10, path="fused", **over):
     cfg = gen.lib_config(cname, **over)
     kv = gen.CONFIGS[cname]["kv_total"] if kv is None else kv
-    s, o = make_pair(cfg, debug=False)
+    s, o = make_pair(cfg, debug=False, path=path)
     reqs = gen.requests(cname, n_req, seed=seed)
     drv = gen.ClosedLoop(reqs, gen.PROFILES[gen.CONFIGS[cname]["profile"]]["tau"], initial, per_step, seed)
     prev = []
@@ -191,13 +226,15 @@ def test_closed_loop_c1_starvation_fires():
     assert st["starving"] > 0 and st["pre"] > 0
 
 
-def test_closed_loop_c2():
-    st = closed_loop("C2", 1500, 150, 600, 6.0)
+@pytest.mark.parametrize("path", PATHS)
+def test_closed_loop_c2(path):
+    st = closed_loop("C2", 1500, 150, 600, 6.0, path=path)
     assert st["api"] > 0 and st["fin"] > 0
 
 
-def test_closed_loop_c3_multi_api():
-    st = closed_loop("C3", 1500, 150, 600, 6.0)
+@pytest.mark.parametrize("path", PATHS)
+def test_closed_loop_c3_multi_api(path):
+    st = closed_loop("C3", 1500, 150, 600, 6.0, path=path)
     assert st["api"] > 0
 
 
