@@ -34,10 +34,12 @@ constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
 constexpr int kBucketM = 7;                 // score bits per octave
 constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
 constexpr int kLocalItems = kKcap / kFT;    // 12
+constexpr int kTRows = 8;                   // count exchange: up to 256 CTAs
 
 struct PhaseS {                  // S, H, T, X
     uint64_t kbuf[kKcap];        // 96 KB: this CTA's keys
     uint32_t cnt[kMaxBuckets];   // 58 KB: bucket counts -> scatter cursors
+    uint32_t start[kMaxBuckets]; // 58 KB: bucket totals -> bucket start positions
     uint32_t w32[kFW];
     unsigned long long red[3][kFW];
     uint32_t nk, base;
@@ -70,33 +72,41 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint3
     return ns * half + fb;
 }
 
-// stable LSD sort of n keys in shared memory (src -> alternating), returns the buffer holding the result
+// Stable LSD sort of n (<= kKcap) keys in shared memory over the 8-bit digit
+// positions where `vary` has bits; returns the buffer holding the result.
+// Keys are spread evenly over the 32 warps: warp w owns the contiguous
+// segment [w*32*ipt, (w+1)*32*ipt), item j of lane l is position
+// w*32*ipt + j*32 + l, so (warp, j, lane) order is array order (stability).
 __device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned long long vary) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     uint64_t* src = sm.a;
     uint64_t* dst = sm.b;
-    const uint32_t per_warp = 32u * kLocalItems;
+    const uint32_t ipt = (n + kFT - 1) / kFT;  // items per lane, <= kLocalItems
+    const uint32_t seg = 32u * ipt;
     const uint32_t lt_mask = (1u << lane) - 1u;
     for (int dpos = 0; dpos < kDigits; dpos++) {
         if (!((vary >> (8 * dpos)) & 0xffull)) continue;
         const uint32_t shift = 8u * dpos;
         for (uint32_t i = tid; i < kFW * kBins; i += kFT) (&sm.whist[0][0])[i] = 0;
         __syncthreads();
-        uint32_t pk[kLocalItems];  // digit << 16 | rank (digit 256 = empty)
+        uint32_t pk[kLocalItems];  // digit << 16 | rank within the warp (digit 256 = empty)
 #pragma unroll
         for (int j = 0; j < kLocalItems; j++) {
-            const uint32_t li = warp * per_warp + j * 32 + lane;
-            const uint32_t d = li < n ? (uint32_t)(src[li] >> shift) & 0xffu : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t leader = __ffs(peers) - 1u;
-            uint32_t prior = 0;
-            if (d < 256u && lane == leader) {
-                prior = sm.whist[warp][d];
-                sm.whist[warp][d] = (uint16_t)(prior + __popc(peers));
+            pk[j] = 256u << 16;
+            if ((uint32_t)j < ipt) {  // warp-uniform
+                const uint32_t li = warp * seg + j * 32 + lane;
+                const uint32_t d = li < n ? (uint32_t)(src[li] >> shift) & 0xffu : 256u;
+                const uint32_t peers = digit_peers(d);
+                const uint32_t leader = __ffs(peers) - 1u;
+                uint32_t prior = 0;
+                if (d < 256u && lane == leader) {
+                    prior = sm.whist[warp][d];
+                    sm.whist[warp][d] = (uint16_t)(prior + __popc(peers));
+                }
+                prior = __shfl_sync(0xffffffffu, prior, leader);
+                pk[j] = (d << 16) | (prior + __popc(peers & lt_mask));
+                __syncwarp();
             }
-            prior = __shfl_sync(0xffffffffu, prior, leader);
-            pk[j] = (d << 16) | (prior + __popc(peers & lt_mask));
-            __syncwarp();
         }
         __syncthreads();
         // per digit: exclusive prefix over the 32 warps, 4 threads per digit (8 warps each)
@@ -129,7 +139,7 @@ __device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned 
         for (int j = 0; j < kLocalItems; j++) {
             const uint32_t d = pk[j] >> 16;
             if (d < 256u) {
-                const uint32_t li = warp * per_warp + j * 32 + lane;
+                const uint32_t li = warp * seg + j * 32 + lane;
                 dst[sm.texcl[d] + sm.whist[warp][d] + (pk[j] & 0xffffu)] = src[li];
             }
         }
@@ -207,37 +217,51 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     for (uint32_t j = tid; j < NB; j += kFT) H[(size_t)bid * NB + j] = sm.s.cnt[j];
     grid_barrier(ctl, G);
 
-    // ---------------- T: buckets j = bid (mod G): exclusive prefix over CTAs, total
+    // ---------------- T: buckets j = bid (mod G): exclusive prefix over CTAs, total.
+    // One warp per bucket; lane l holds rows l, l+32, ... (G <= 32*kTRows), loads batched.
     for (uint32_t j = bid + warp * G; j < NB; j += kFW * G) {
+        uint32_t v[kTRows];
+#pragma unroll
+        for (int i = 0; i < kTRows; i++) {
+            const uint32_t r = 32u * i + lane;
+            v[i] = r < G ? __ldcg(&H[(size_t)r * NB + j]) : 0u;
+        }
         uint32_t carry = 0;
-        for (uint32_t r0 = 0; r0 < G; r0 += 32) {
-            const uint32_t r = r0 + lane;
-            const uint32_t v = r < G ? __ldcg(&H[(size_t)r * NB + j]) : 0u;
-            uint32_t x = v;
+#pragma unroll
+        for (int i = 0; i < kTRows; i++) {
+            const uint32_t r = 32u * i + lane;
+            uint32_t x = v[i];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= (uint32_t)o) x += y;
             }
-            if (r < G) H[(size_t)r * NB + j] = carry + x - v;
+            if (r < G) H[(size_t)r * NB + j] = carry + x - v[i];
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
         if (lane == 0) T[j] = carry;
     }
     grid_barrier(ctl, G);
 
-    // ---------------- X: bucket bases, scatter into bucket order, ranges
-    // cursor(j) = start(j) + keys of bucket j in CTAs before this one, start = excl-scan of T
+    // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
+    // bucket order; cursor(j) = start(j) + keys of bucket j in the CTAs before this one
+    for (uint32_t j = tid; j < NB; j += kFT) {
+        sm.s.start[j] = __ldcg(&T[j]);
+        sm.s.cnt[j] = __ldcg(&H[(size_t)bid * NB + j]);
+    }
+    __syncthreads();
     {
         const uint32_t per = (NB + kFT - 1) / kFT;
         const uint32_t j0 = min(NB, tid * per), j1 = min(NB, j0 + per);
         uint32_t s = 0;
-        for (uint32_t j = j0; j < j1; j++) s += __ldcg(&T[j]);
+        for (uint32_t j = j0; j < j1; j++) s += sm.s.start[j];
         uint32_t tot;
         uint32_t run = block_excl_scan_u32<kFT>(s, sm.s.w32, &tot);
         for (uint32_t j = j0; j < j1; j++) {
-            sm.s.cnt[j] = run + __ldcg(&H[(size_t)bid * NB + j]);
-            run += __ldcg(&T[j]);
+            const uint32_t t = sm.s.start[j];
+            sm.s.start[j] = run;
+            sm.s.cnt[j] += run;
+            run += t;
         }
         if (tid == 0) sm.s.base = tot;  // total number of keys
     }
@@ -249,19 +273,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         b.keys[0][pos] = k;
     }
     __syncthreads();
-    {   // start(j) again (the cursors were consumed)
-        const uint32_t per = (NB + kFT - 1) / kFT;
-        const uint32_t j0 = min(NB, tid * per), j1 = min(NB, j0 + per);
-        uint32_t s = 0;
-        for (uint32_t j = j0; j < j1; j++) s += __ldcg(&T[j]);
-        uint32_t tot;
-        uint32_t run = block_excl_scan_u32<kFT>(s, sm.s.w32, &tot);
-        for (uint32_t j = j0; j < j1; j++) {
-            sm.s.cnt[j] = run;
-            run += __ldcg(&T[j]);
-        }
-    }
-    __syncthreads();
     // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
     // bucket with start >= q_r by binary search; the largest range decides the fallback
     uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now
@@ -270,9 +281,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (sm.s.cnt[mid] >= q) hi = mid; else lo = mid + 1;
+            if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
         }
-        rb[tid] = (tid == G || lo == NB) ? n : sm.s.cnt[lo];
+        rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
     }
     __syncthreads();
     uint32_t mx = 0;

@@ -189,7 +189,8 @@ void grids(lamps_t* h, bool query_device) {
     {
         const uint32_t groups = (h->cap + 3) / 4;
         const uint32_t gpc = (groups + h->fused_grid - 1) / h->fused_grid;
-        h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && gpc * 4u <= (uint32_t)kFusedKcap && fused_occ >= 1;
+        h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && gpc * 4u <= (uint32_t)kFusedKcap && fused_occ >= 1 &&
+                   h->fused_grid <= 256u;  // count exchange covers up to 256 CTAs
     }
     if (!query_device) {  // size query: assume the fused path may be chosen
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && h->cap <= 148u * (uint32_t)kFusedKcap;
@@ -200,6 +201,31 @@ void grids(lamps_t* h, bool query_device) {
     h->score_grid = std::max<uint32_t>(1, std::min<uint32_t>(want, (uint32_t)sms * 7));
     h->sort_grid = (uint32_t)std::max(1, sms * std::max(sort_occ, 1));
     if (!query_device) h->sort_grid = std::max<uint32_t>(h->sort_grid, 148u * 2u);
+}
+
+// Cost::fast: prove, with exact 128-bit arithmetic, that the unchecked 64-bit
+// fast path (lamps_dev.cuh strategy_score_fast) cannot overflow for any slot
+// whose context values stay below L = kFastCtxLimit: every intermediate and the
+// final sum must stay < 2^63.
+bool fast_bounds_ok(const lamps_config& c) {
+    typedef unsigned __int128 U;
+    const U L = (U)kFastCtxLimit, lim = (U)1 << 63;
+    const U api_max = 0xffffffffull, pend_max = 0xffffffffull;
+    const U tf_in = (U)c.A1 * L + (U)c.A2 * L * L;         // T_fwd before the shift
+    const U ts_in = (U)c.S0 + (U)c.S1 * L;
+    if (tf_in >= lim || ts_in >= lim) return false;
+    const U tf = tf_in >> c.SH, ts = ts_in >> c.SH;
+    const U cb = L + c.c_other;
+    const U blkL = (L + c.block_tokens - 1) / c.block_tokens;
+    const U ramp = L * blkL;                                // >= F(n) for n <= L
+    const U wd = tf * cb, ws = 2 * ts * cb, wp = api_max * L;
+    if (wd >= lim || ws >= lim || wp >= lim) return false;
+    const U t_pend = blkL * pend_max, t_ramp = (U)c.tau * ramp;
+    U t_api = blkL * api_max;
+    if (blkL * tf > t_api) t_api = blkL * tf;
+    if (2 * blkL * ts > t_api) t_api = 2 * blkL * ts;
+    if (L * c.block_tokens >= lim) return false;
+    return t_pend + 2 * t_ramp + t_api < lim;
 }
 
 // segment validation shared by submit and api_return; ctx0 = context before the segment
@@ -368,8 +394,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     c.SB = cfg->score_bits; c.IB = cfg->id_bits;
     c.score_max = (cfg->score_bits >= 64) ? ~0ull : ((1ull << cfg->score_bits) - 1ull);
     c.cap = cfg->capacity; c.cap_mask = cfg->capacity - 1u;
-    c.fast = (cfg->A1 < (1ull << 32) && cfg->S0 < (1ull << 32) && cfg->S1 < (1ull << 32) &&
-              cfg->tau < (1ull << 32) && cfg->A2 < (1ull << 12) && cfg->c_other < (1ull << 26)) ? 1u : 0u;
+    c.fast = fast_bounds_ok(*cfg) ? 1u : 0u;
     h->hstate.assign(h->cap, H_FREE);
     auto cleanup = [&](int code, const char*) { lamps_free(h); return code; };
     if (cudaMemsetAsync(h->ws, 0, need, h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "memset");

@@ -41,8 +41,8 @@ struct Cost {
     uint32_t fast;       // constants satisfy the 64-bit fast-path bounds (host-checked)
 };
 
-// Per-slot bound of the fast path (see strategy_score32): ctx+pre+resp+post < 2^25.
-constexpr uint64_t kFastCtxLimit = 1ull << 25;
+// Per-slot bound of the fast path (see strategy_score_fast): ctx+pre+resp+post < 2^20.
+constexpr uint64_t kFastCtxLimit = 1ull << 20;
 
 // Pool SoA (device pointers into the workspace), 16-byte aligned, padded.
 struct Pool {
@@ -118,73 +118,69 @@ __device__ __forceinline__ uint64_t score_of(uint64_t ctx, uint64_t pre, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// Fast path: 32x32->64 products (IMAD.WIDE.U32) instead of 64-bit emulation.
-// Host bounds (Cost::fast): A1, S0, S1, tau < 2^32; A2 < 2^12; c_other < 2^26;
-// per slot: ctx + pre + resp + post < 2^25.  Under them T_fwd, T_swap, W_P and
-// every ramp are exact in 64 bits; a product that may exceed 2^64 saturates and
-// sums saturate, which cannot change min(sum, 2^SB - 1) (SB <= 63) nor the
-// argmin (a saturated waste equals the exact value clamped to 2^64 - 1).
+// Fast path: plain 64-bit arithmetic with no overflow checks.  The host sets
+// Cost::fast only when, for every context value c < kFastCtxLimit (2^20
+// tokens), it has proven with exact 128-bit arithmetic that every product and
+// every sum below stays < 2^63 (see fast_bounds_ok in lamps_api.cu); the kernel
+// takes this path for a slot iff ctx + pre + resp + post < 2^20.  Under those
+// bounds the results equal the exact ones (no clamp can trigger except the
+// final min with 2^SB - 1, which is applied).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t wide(uint32_t a, uint32_t b) { return (uint64_t)a * b; }
-
-// saturating (64-bit x 32-bit) product
-__device__ __forceinline__ uint64_t mul64x32_sat(uint64_t a, uint32_t b) {
-    const uint64_t lo = wide((uint32_t)a, b);
-    const uint64_t hi = wide((uint32_t)(a >> 32), b);   // contributes hi << 32
-    if (hi >> 32) return ~0ull;
-    const uint64_t r = lo + (hi << 32);
-    return r < lo ? ~0ull : r;
+__device__ __forceinline__ uint64_t t_fwd_fast(uint32_t x, const Cost& c) {
+    return (c.A1 * x + c.A2 * ((uint64_t)x * x)) >> c.SH;
 }
-__device__ __forceinline__ uint64_t add_sat(uint64_t a, uint64_t b) {
-    const uint64_t s = a + b;
-    return s < a ? ~0ull : s;
+__device__ __forceinline__ uint64_t t_swap_fast(uint32_t x, const Cost& c) {
+    return x ? (c.S0 + c.S1 * x) >> c.SH : 0ull;
 }
-// T_fwd(x) = (A1 x + A2 x^2) >> SH, x < 2^25: A1 x < 2^57, A2 x^2 < 2^62
-__device__ __forceinline__ uint64_t t_fwd32(uint32_t x, const Cost& c) {
-    const uint64_t sq = wide(x, x);
-    const uint64_t v = wide((uint32_t)c.A1, x) + mul64x32_sat(sq, (uint32_t)c.A2);
-    return v >> c.SH;
-}
-// T_swap(x) = x ? (S0 + S1 x) >> SH : 0, x < 2^25
-__device__ __forceinline__ uint64_t t_swap32(uint32_t x, const Cost& c) {
-    return x ? (c.S0 + wide((uint32_t)c.S1, x)) >> c.SH : 0ull;
-}
-// F(n) = sum_{j=1..n} ceil(j/B) = B Q(Q+1)/2 + R(Q+1), n = Q B + R, n < 2^25
-__device__ __forceinline__ uint64_t ramp32(uint32_t n, const Cost& c) {
+// F(n) = sum_{j=1..n} ceil(j/B) = B Q(Q+1)/2 + R(Q+1), n = Q B + R
+__device__ __forceinline__ uint64_t ramp_fast(uint32_t n, const Cost& c) {
     const uint32_t Q = n >> c.lgB, R = n & (c.B - 1u);
-    return ((wide(Q, Q + 1u) >> 1) << c.lgB) + wide(R, Q + 1u);
+    return ((((uint64_t)Q * (Q + 1u)) >> 1) << c.lgB) + (uint64_t)R * (Q + 1u);
 }
 
 // strategy (A1) and score (A2) of one READY slot on the fast path
-__device__ __forceinline__ uint32_t strategy_score32(uint32_t ctx, uint32_t pre, uint32_t api,
-                                                     uint32_t resp, uint32_t post, uint32_t pend,
-                                                     uint32_t has, const Cost& c, uint64_t* score,
-                                                     uint64_t* wp_o, uint64_t* wd_o, uint64_t* ws_o) {
+__device__ __forceinline__ uint32_t strategy_score_fast(uint32_t ctx, uint32_t pre, uint32_t api,
+                                                        uint32_t resp, uint32_t post, uint32_t pend,
+                                                        uint32_t has, const Cost& c, uint64_t* score,
+                                                        uint64_t* wp_o, uint64_t* wd_o, uint64_t* ws_o) {
     const uint32_t ci = ctx + pre;
-    const uint32_t tau = (uint32_t)c.tau;
-    uint64_t s = add_sat(wide((ctx + c.B - 1u) >> c.lgB, pend),
-                         mul64x32_sat(ramp32(ci, c) - ramp32(ctx, c), tau));
+    uint64_t s = (uint64_t)((ctx + c.B - 1u) >> c.lgB) * pend + c.tau * (ramp_fast(ci, c) - ramp_fast(ctx, c));
     uint32_t strat = STR_NONE;
     uint64_t wp = 0, wd = 0, ws = 0;
     if (has) {
-        const uint32_t cb = ci + (uint32_t)c.c_other;  // < 2^27
-        const uint64_t tf = t_fwd32(ci, c), ts = t_swap32(ci, c);
-        wp = wide(api, ci);
-        wd = mul64x32_sat(tf, cb);
-        ws = mul64x32_sat(ts, cb << 1);
+        const uint64_t cb = (uint64_t)ci + c.c_other;
+        const uint64_t tf = t_fwd_fast(ci, c), ts = t_swap_fast(ci, c);
+        wp = (uint64_t)api * ci;
+        wd = tf * cb;
+        ws = (ts * cb) << 1;
         strat = (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
         const uint32_t bci = (ci + c.B - 1u) >> c.lgB;
         const uint32_t cr = ci + resp;
         uint64_t a;
-        if (strat == STR_P) a = wide(bci, api);
-        else if (strat == STR_D) a = mul64x32_sat(t_fwd32(cr, c), (cr + c.B - 1u) >> c.lgB);
-        else a = mul64x32_sat(ts, bci << 1);
-        s = add_sat(s, a);
-        s = add_sat(s, mul64x32_sat(ramp32(cr + post, c) - ramp32(cr, c), tau));
+        if (strat == STR_P) a = (uint64_t)bci * api;
+        else if (strat == STR_D) a = t_fwd_fast(cr, c) * ((cr + c.B - 1u) >> c.lgB);
+        else a = (ts * bci) << 1;
+        s += a + c.tau * (ramp_fast(cr + post, c) - ramp_fast(cr, c));
     }
     *score = s > c.score_max ? c.score_max : s;
     *wp_o = wp; *wd_o = wd; *ws_o = ws;
     return strat;
+}
+
+// Lanes of the warp holding the same 8-bit digit d (0..255; 256 = empty lane),
+// from 9 ballots: a multisplit that avoids __match_any_sync (measured as the
+// dominant latency of the in-SM ranking on B200).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+    const bool valid = d < 256u;
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    uint32_t m = valid ? vm : ~vm;
+#pragma unroll
+    for (int bit = 0; bit < 8; bit++) {
+        const uint32_t on = (d >> bit) & 1u;
+        const uint32_t bb = __ballot_sync(0xffffffffu, on);
+        m &= on ? bb : ~bb;
+    }
+    return m;
 }
 
 }  // namespace lamps

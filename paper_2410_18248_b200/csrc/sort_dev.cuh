@@ -58,7 +58,7 @@ __device__ __forceinline__ void rank_tile(const uint64_t* __restrict__ in, uint3
 #pragma unroll
     for (int j = 0; j < kSortItems; j++) {
         const uint32_t d = dig[j];
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = digit_peers(d);
         const uint32_t leader = __ffs(peers) - 1u;
         uint32_t prior = 0;
         if (d < 256u && lane == leader) {

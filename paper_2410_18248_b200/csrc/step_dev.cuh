@@ -124,7 +124,7 @@ __device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, ui
         uint32_t strat;
         const uint64_t span = (uint64_t)cv[j] + prv[j] + (has ? (uint64_t)rsv[j] + pov[j] : 0ull);
         if (c.fast && span < kFastCtxLimit) {
-            strat = strategy_score32(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, c, &sc, &wp, &wd, &ws);
+            strat = strategy_score_fast(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, c, &sc, &wp, &wd, &ws);
         } else {
             wp = wd = ws = 0;
             strat = STR_NONE;
