@@ -44,13 +44,26 @@ struct PhaseS {                  // S, H, T, X
     unsigned long long red[3][kFW];
     uint32_t nk, base;
 };
+constexpr int kSubBits = 12;                // local MSD digit
+constexpr int kSubBuckets = 1 << kSubBits;
+constexpr uint32_t kMaxRankM = 32;          // largest sub-bucket ranked by comparison
 struct PhaseL {                  // L
     uint64_t a[kKcap];           // 96 KB
     uint64_t b[kKcap];           // 96 KB
-    uint16_t whist[kFW][kBins];  // 16 KB
-    uint32_t part[4][kBins];     // 4 KB
-    uint32_t texcl[kBins];
-    uint32_t scan[kFW];
+    union {
+        struct {                         // local LSD (fallback)
+            uint16_t whist[kFW][kBins];  // 16 KB
+            uint32_t part[4][kBins];     // 4 KB
+            uint32_t texcl[kBins];
+            uint32_t scan[kFW];
+        };
+        struct {                         // local MSD + rank
+            uint32_t cnt[kSubBuckets];   // 16 KB
+            uint32_t pos[kSubBuckets];   // 16 KB
+            uint32_t w32[kFW];
+            uint32_t maxm;
+        };
+    };
     unsigned long long red[2][kFW];
 };
 union FusedSmem {
@@ -149,6 +162,55 @@ __device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned 
     return src;
 }
 
+// Sort of the n keys of a range in shared memory (sm.a), returns the buffer
+// holding the result.  One MSD step: count and scatter by the 12 highest bits
+// that vary in the range (shared-memory atomics; the order inside a
+// sub-bucket is then fixed exactly below), then every key finds its final
+// place inside its sub-bucket by counting the smaller keys there (keys are
+// unique).  If some sub-bucket holds more than kMaxRankM keys (many keys with
+// nearly equal scores), the range is sorted by the stable LSD instead.
+__device__ __forceinline__ uint64_t* local_sort(PhaseL& sm, uint32_t n, unsigned long long vary) {
+    const uint32_t tid = threadIdx.x;
+    if (n <= 1 || vary == 0) return sm.a;
+    const int h = 63 - __clzll((long long)vary);
+    const uint32_t lo = h >= kSubBits - 1 ? (uint32_t)(h - (kSubBits - 1)) : 0u;
+    const uint32_t dmask = kSubBuckets - 1;
+    for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.cnt[i] = 0;
+    if (tid == 0) sm.maxm = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.cnt[(uint32_t)(sm.a[i] >> lo) & dmask], 1u);
+    __syncthreads();
+    {   // exclusive scan of the counts: 4 consecutive counters per thread
+        const uint32_t c0 = sm.cnt[4 * tid], c1 = sm.cnt[4 * tid + 1], c2 = sm.cnt[4 * tid + 2],
+                       c3 = sm.cnt[4 * tid + 3];
+        uint32_t tot;
+        const uint32_t e = block_excl_scan_u32<kFT>(c0 + c1 + c2 + c3, sm.w32, &tot);
+        sm.pos[4 * tid] = e;
+        sm.pos[4 * tid + 1] = e + c0;
+        sm.pos[4 * tid + 2] = e + c0 + c1;
+        sm.pos[4 * tid + 3] = e + c0 + c1 + c2;
+        const uint32_t m = max(max(c0, c1), max(c2, c3));
+        if (m > kMaxRankM) atomicMax(&sm.maxm, m);
+    }
+    __syncthreads();
+    if (sm.maxm > kMaxRankM) return local_lsd(sm, n, vary);  // block-uniform
+    for (uint32_t i = tid; i < n; i += kFT) {
+        const uint64_t k = sm.a[i];
+        sm.b[atomicAdd(&sm.pos[(uint32_t)(k >> lo) & dmask], 1u)] = k;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kFT) {  // pos[d] is now the end of sub-bucket d
+        const uint64_t k = sm.b[i];
+        const uint32_t d = (uint32_t)(k >> lo) & dmask;
+        const uint32_t e = sm.pos[d], s0 = e - sm.cnt[d];
+        uint32_t r = 0;
+        for (uint32_t q = s0; q < e; q++) r += sm.b[q] < k ? 1u : 0u;
+        sm.a[s0 + r] = k;
+    }
+    __syncthreads();
+    return sm.a;
+}
+
 template <bool DBG>
 __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -217,37 +279,47 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     for (uint32_t j = tid; j < NB; j += kFT) H[(size_t)bid * NB + j] = sm.s.cnt[j];
     grid_barrier(ctl, G);
 
-    // ---------------- T: buckets j = bid (mod G): exclusive prefix over CTAs, total.
-    // One warp per bucket; lane l holds rows l, l+32, ... (G <= 32*kTRows), loads batched.
-    for (uint32_t j = bid + warp * G; j < NB; j += kFW * G) {
-        uint32_t v[kTRows];
-#pragma unroll
-        for (int i = 0; i < kTRows; i++) {
-            const uint32_t r = 32u * i + lane;
-            v[i] = r < G ? __ldcg(&H[(size_t)r * NB + j]) : 0u;
-        }
-        uint32_t carry = 0;
-#pragma unroll
-        for (int i = 0; i < kTRows; i++) {
-            const uint32_t r = 32u * i + lane;
-            uint32_t x = v[i];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= (uint32_t)o) x += y;
+    // ---------------- T: CTA bid owns buckets [jb0, jb1): it loads that column block of
+    // the count matrix (coalesced row segments) into shared memory, scans each column
+    // down the CTAs (exclusive prefix per CTA, total per bucket) and writes it back.
+    {
+        const uint32_t jb0 = (uint32_t)(((uint64_t)NB * bid) / G), jb1 = (uint32_t)(((uint64_t)NB * (bid + 1)) / G);
+        const uint32_t w = jb1 - jb0;
+        uint32_t* tile = sm.s.cnt;  // G x w (the bucket counts are already published)
+        for (uint32_t r = warp; r < G; r += kFW)
+            for (uint32_t j = lane; j < w; j += 32) tile[r * w + j] = __ldcg(&H[(size_t)r * NB + jb0 + j]);
+        __syncthreads();
+        for (uint32_t j = tid; j < w; j += kFT) {
+            uint32_t run = 0;
+            for (uint32_t r = 0; r < G; r++) {
+                const uint32_t v = tile[r * w + j];
+                tile[r * w + j] = run;
+                run += v;
             }
-            if (r < G) H[(size_t)r * NB + j] = carry + x - v[i];
-            carry += __shfl_sync(0xffffffffu, x, 31);
+            T[jb0 + j] = run;
         }
-        if (lane == 0) T[j] = carry;
+        __syncthreads();
+        for (uint32_t r = warp; r < G; r += kFW)
+            for (uint32_t j = lane; j < w; j += 32) H[(size_t)r * NB + jb0 + j] = tile[r * w + j];
     }
     grid_barrier(ctl, G);
 
     // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
     // bucket order; cursor(j) = start(j) + keys of bucket j in the CTAs before this one
-    for (uint32_t j = tid; j < NB; j += kFT) {
-        sm.s.start[j] = __ldcg(&T[j]);
-        sm.s.cnt[j] = __ldcg(&H[(size_t)bid * NB + j]);
+    {
+        constexpr int kPer = (kMaxBuckets + kFT - 1) / kFT;  // 15
+        uint32_t tv[kPer], hv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; u++) {
+            const uint32_t j = tid + (uint32_t)u * kFT;
+            tv[u] = j < NB ? __ldcg(&T[j]) : 0u;
+            hv[u] = j < NB ? __ldcg(&H[(size_t)bid * NB + j]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; u++) {
+            const uint32_t j = tid + (uint32_t)u * kFT;
+            if (j < NB) { sm.s.start[j] = tv[u]; sm.s.cnt[j] = hv[u]; }
+        }
     }
     __syncthreads();
     {
@@ -310,7 +382,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         o = 0; an = ~0ull;
         for (int w = 0; w < kFW; w++) { o |= sm.l.red[0][w]; an &= sm.l.red[1][w]; }
         __syncthreads();
-        const uint64_t* res = local_lsd(sm.l, rn, rn ? (o ^ an) : 0ull);
+        const uint64_t* res = local_sort(sm.l, rn, rn ? (o ^ an) : 0ull);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = res[i];
         final_buf = 1;
         passes = 1;
@@ -343,6 +415,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
 
 }  // namespace
 
+static_assert(sizeof(FusedSmem) <= 232448, "fused kernel shared memory exceeds 227 KB");
 size_t fused_smem_bytes() { return sizeof(FusedSmem); }
 
 int fused_blocks_per_sm() {

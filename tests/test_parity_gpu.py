@@ -70,6 +70,25 @@ def test_equal_scores_large_bucket(path):
     compare_state(s, o)
 
 
+@pytest.mark.parametrize("path", PATHS)
+def test_many_equal_scores_in_one_range(path):
+    # 3000 identical requests among 6000: one sub-bucket far above the rank-by-comparison
+    # limit inside a shared-memory range, so the fused kernel's local LSD fallback runs
+    snap = gen.snapshot("C2", seed=4, n=6000, capacity=8192, id_base=8192 * 2 + 1)
+    idx = np.nonzero(snap["state"] != 0)[0][::2]
+    for f, v in (("state", 1), ("has_api", 1), ("ctx", 400), ("pre_rem", 25), ("api_ticks", 700000),
+                 ("resp_len", 64), ("post_len", 60), ("pending", 0), ("starving", 0), ("cnt", 1)):
+        snap[f][idx] = v
+    cfg = gen.lib_config("C2")
+    cfg["capacity"] = 8192
+    s, o = make_pair(cfg, debug=True, path=path)
+    load_both(s, o, snap)
+    for t in range(2):
+        g, r = s.step(kv_total=3000), o.step(kv_total=3000, debug=True)
+        compare_outputs(s, g, r, where=f"equal-range t={t}")
+        compare_state(s, o, r, where=f"equal-range t={t}")
+
+
 def _custom(cfg_over, recs, kv, steps=2, id_base=0, path="fused"):
     cfg = gen.lib_config("C1")
     cfg.update(cfg_over)
