@@ -69,6 +69,7 @@ extern "C" {
 #define LAMPS_TIMING 2u    /* record CUDA events around each phase (lamps_timing_read) */
 #define LAMPS_MULTI_KERNEL 4u   /* use the 3-kernel path even where the fused step kernel fits */
 #define LAMPS_FORCE_FALLBACK 8u /* fused path: always take the global-LSD fallback (tests) */
+#define LAMPS_TRACE 16u         /* fused path: record SM clock at phase boundaries (lamps_trace_read) */
 
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 
@@ -247,6 +248,15 @@ int lamps_step_stats(lamps_t* h, uint32_t* kernels_launched, uint32_t* sort_pass
  * (all radix passes), ms[3] = A5 admission kernel.  Synchronises the stream.
  */
 int lamps_timing_read(lamps_t* h, double ms[4], uint32_t* n_steps);
+
+/*
+ * With LAMPS_TRACE on the fused path: the SM clock (clock64) of every CTA at
+ * the phase boundaries of the last step, out[cta * 16 + k], k = 0 start,
+ * 1 scored, 2 counts published, 3 after barrier 1, 4 count exchange done,
+ * 5 after barrier 2, 6 scattered, 7 after barrier 3, 8 range sorted,
+ * 9 admission done (CTA 0).  *n_cta receives the grid size.
+ */
+int lamps_trace_read(lamps_t* h, uint64_t* out, uint32_t max_words, uint32_t* n_cta);
 
 /* Library version (major << 16 | minor). */
 uint32_t lamps_version(void);

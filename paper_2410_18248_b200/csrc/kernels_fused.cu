@@ -211,6 +211,11 @@ __device__ __forceinline__ uint64_t* local_sort(PhaseL& sm, uint32_t n, unsigned
     return sm.a;
 }
 
+#define TRACE(k)                                                                         \
+    do {                                                                                 \
+        if (b.trace && threadIdx.x == 0) b.trace[blockIdx.x * kTraceSlots + (k)] = clock64(); \
+    } while (0)
+
 template <bool DBG>
 __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -223,6 +228,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     uint32_t* H = b.blocksum;  // [G][NB] bucket counts -> exclusive prefix over CTAs
     uint32_t* T = b.blocksum + (size_t)G * NB;  // [NB] bucket totals
 
+    TRACE(0);
     // ---------------- S: score this CTA's slots, keys into shared memory
     if (tid == 0) sm.s.nk = 0;
     for (uint32_t i = tid; i < NB; i += kFT) sm.s.cnt[i] = 0;
@@ -275,9 +281,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         b.kmask[bid] = o;
         b.kmask[G + bid] = n;
     }
+    TRACE(1);
     // ---------------- H: publish this CTA's bucket counts
     for (uint32_t j = tid; j < NB; j += kFT) H[(size_t)bid * NB + j] = sm.s.cnt[j];
+    TRACE(2);
     grid_barrier(ctl, G);
+    TRACE(3);
 
     // ---------------- T: CTA bid owns buckets [jb0, jb1): it loads that column block of
     // the count matrix (coalesced row segments) into shared memory, scans each column
@@ -302,7 +311,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         for (uint32_t r = warp; r < G; r += kFW)
             for (uint32_t j = lane; j < w; j += 32) H[(size_t)r * NB + jb0 + j] = tile[r * w + j];
     }
+    TRACE(4);
     grid_barrier(ctl, G);
+    TRACE(5);
 
     // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
     // bucket order; cursor(j) = start(j) + keys of bucket j in the CTAs before this one
@@ -363,7 +374,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const bool fallback = (a.flags & kStepForceFallback) ||
                           __syncthreads_or(mx > (uint32_t)kKcap);
     const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
+    TRACE(6);
     grid_barrier(ctl, G);
+    TRACE(7);
 
     // ---------------- L: sort the key ranges
     uint32_t final_buf, passes;
@@ -391,6 +404,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         final_buf = passes & 1u;
     }
 
+    TRACE(8);
     // ---------------- A: admission by CTA 0
     // CTA 0 may start as soon as the head it needs is sorted: without the fallback
     // the keys [0, rb[1]) are sorted by CTA 0 itself.
@@ -411,6 +425,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const unsigned long long pinned_all = sm.adm.w64[0];
     __syncthreads();
     admit_cta(b, c, a, b.keys[final_buf], n, pinned_all, sm.adm);
+    TRACE(9);
 }
 
 }  // namespace

@@ -146,6 +146,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_ing = L.take((size_t)kIngestChunk * sizeof(SubmitRec));
     size_t o_gat = L.take((size_t)kIngestChunk * 4);
     size_t o_dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? L.take((size_t)cap_pad * 32) : 0;
+    size_t o_trace = (h->cfg.flags & LAMPS_TRACE) ? L.take((size_t)gmax * kTraceSlots * 8) : 0;
     if (!base) return L.off;
     uint32_t* soa[8];
     for (int i = 0; i < 8; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
@@ -170,6 +171,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->d_gather = reinterpret_cast<uint32_t*>(base + o_gat);
     h->b.dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? reinterpret_cast<unsigned long long*>(base + o_dbg)
                                                   : nullptr;
+    h->b.trace = (h->cfg.flags & LAMPS_TRACE) ? reinterpret_cast<unsigned long long*>(base + o_trace) : nullptr;
     return L.off;
 }
 
@@ -676,6 +678,17 @@ int lamps_step_stats(lamps_t* h, uint32_t* kernels_launched, uint32_t* sort_pass
     CU(h, cudaStreamSynchronize(h->stream));
     if (kernels_launched) *kernels_launched = h->last_kernels;
     if (sort_passes) *sort_passes = h->h_ctl->n_passes;
+    return LAMPS_OK;
+}
+
+int lamps_trace_read(lamps_t* h, uint64_t* out, uint32_t max_words, uint32_t* n_cta) {
+    if (!h || !out || !n_cta) return LAMPS_EINVAL;
+    if (!h->b.trace) return fail(h, LAMPS_EINVAL, "tracing needs LAMPS_TRACE");
+    if (!h->fused) return fail(h, LAMPS_ENOTSUP, "tracing is implemented for the fused path");
+    CU(h, cudaStreamSynchronize(h->stream));
+    const size_t words = std::min<size_t>(max_words, (size_t)h->fused_grid * kTraceSlots);
+    CU(h, cudaMemcpy(out, h->b.trace, words * 8, cudaMemcpyDeviceToHost));
+    *n_cta = h->fused_grid;
     return LAMPS_OK;
 }
 

@@ -18,7 +18,7 @@ LAMPS_OK, LAMPS_EINVAL, LAMPS_ENOSPC, LAMPS_ENOENT, LAMPS_ENOTSUP, LAMPS_ECUDA, 
 LAMPS_FREE, LAMPS_READY, LAMPS_PAUSED_P, LAMPS_PAUSED_D, LAMPS_PAUSED_S = 0, 1, 2, 3, 4
 LAMPS_PRESERVE, LAMPS_DISCARD, LAMPS_SWAP, LAMPS_NONE = 0, 1, 2, 3
 LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
-LAMPS_DEBUG_OUT, LAMPS_TIMING = 1, 2
+LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE = 1, 2, 4, 8, 16
 
 u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 
@@ -88,6 +88,7 @@ def lib() -> ctypes.CDLL:
             "lamps_ranked_keys": (c_int, [vp, vp, u64, P(u64)]),
             "lamps_step_stats": (c_int, [vp, P(u32), P(u32)]),
             "lamps_timing_read": (c_int, [vp, P(dbl), P(u32)]),
+            "lamps_trace_read": (c_int, [vp, vp, u32, P(u32)]),
             "lamps_version": (u32, []),
         }
         for name, (res, args) in sig.items():
@@ -267,6 +268,13 @@ class Scheduler:
         k, p = u32(0), u32(0)
         self._check(lib().lamps_step_stats(self.h, ctypes.byref(k), ctypes.byref(p)))
         return int(k.value), int(p.value)
+
+    def trace(self):
+        """Per-CTA SM clocks at the fused kernel's phase boundaries (LAMPS_TRACE)."""
+        out = np.zeros(512 * 16, np.uint64)
+        n = u32(0)
+        self._check(lib().lamps_trace_read(self.h, _p(out), len(out), ctypes.byref(n)))
+        return out[:n.value * 16].reshape(n.value, 16)
 
     def timing(self):
         ms = (dbl * 4)()
