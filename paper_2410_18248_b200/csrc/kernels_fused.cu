@@ -298,14 +298,21 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         for (uint32_t r = warp; r < G; r += kFW)
             for (uint32_t j = lane; j < w; j += 32) tile[r * w + j] = __ldcg(&H[(size_t)r * NB + jb0 + j]);
         __syncthreads();
-        for (uint32_t j = tid; j < w; j += kFT) {
-            uint32_t run = 0;
-            for (uint32_t r = 0; r < G; r++) {
-                const uint32_t v = tile[r * w + j];
-                tile[r * w + j] = run;
-                run += v;
+        for (uint32_t j = warp; j < w; j += kFW) {  // one warp per column, lanes over CTAs
+            uint32_t carry = 0;
+            for (uint32_t r0 = 0; r0 < G; r0 += 32) {
+                const uint32_t r = r0 + lane;
+                const uint32_t v = r < G ? tile[r * w + j] : 0u;
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
+                }
+                if (r < G) tile[r * w + j] = carry + x - v;
+                carry += __shfl_sync(0xffffffffu, x, 31);
             }
-            T[jb0 + j] = run;
+            if (lane == 0) T[jb0 + j] = carry;
         }
         __syncthreads();
         for (uint32_t r = warp; r < G; r += kFW)
@@ -333,6 +340,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         }
     }
     __syncthreads();
+    TRACE(10);
     {
         const uint32_t per = (NB + kFT - 1) / kFT;
         const uint32_t j0 = min(NB, tid * per), j1 = min(NB, j0 + per);
@@ -349,6 +357,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         if (tid == 0) sm.s.base = tot;  // total number of keys
     }
     __syncthreads();
+    TRACE(11);
     const uint32_t n = sm.s.base;
     for (uint32_t i = tid; i < nk_cta; i += kFT) {
         const uint64_t k = sm.s.kbuf[i];
@@ -356,6 +365,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         b.keys[0][pos] = k;
     }
     __syncthreads();
+    TRACE(12);
     // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
     // bucket with start >= q_r by binary search; the largest range decides the fallback
     uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now
@@ -383,6 +393,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     if (!fallback) {
         const uint32_t rn = r_hi - r_lo;
         for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
+        TRACE(13);
         unsigned long long o = 0, an = ~0ull;
         for (uint32_t i = tid; i < rn; i += kFT) { o |= sm.l.a[i]; an &= sm.l.a[i]; }
 #pragma unroll
@@ -396,6 +407,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         for (int w = 0; w < kFW; w++) { o |= sm.l.red[0][w]; an &= sm.l.red[1][w]; }
         __syncthreads();
         const uint64_t* res = local_sort(sm.l, rn, rn ? (o ^ an) : 0ull);
+        TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = res[i];
         final_buf = 1;
         passes = 1;
@@ -412,18 +424,19 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const bool wait = fallback || r_end0 < need;
     if (wait) grid_barrier(ctl, G);
     if (bid != 0) return;
-    __syncthreads();
+    unsigned long long pinned_all;
+    {
+        unsigned long long v = tid < G ? __ldcg(&b.pin_part[tid]) : 0ull;
+        unsigned long long tot;
+        (void)block_excl_scan_u64<kFT>(v, sm.adm.w64, &tot);
+        pinned_all = tot;
+    }
     if (tid == 0) {
-        unsigned long long t = 0;
-        for (uint32_t i = 0; i < G; i++) t += __ldcg(&b.pin_part[i]);
-        sm.adm.w64[0] = t;
         ctl->n_passes = passes;
         ctl->final_buf = final_buf;
         ctl->fallbacks += fallback ? 1u : 0u;
     }
-    __syncthreads();
-    const unsigned long long pinned_all = sm.adm.w64[0];
-    __syncthreads();
+    TRACE(15);
     admit_cta(b, c, a, b.keys[final_buf], n, pinned_all, sm.adm);
     TRACE(9);
 }

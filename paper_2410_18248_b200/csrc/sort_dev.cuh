@@ -20,21 +20,26 @@ struct SortSmem {
     uint32_t n_pass;
 };
 
-// Sense-reversing grid barrier for a cooperative launch (all CTAs resident).
+// Grid barrier for a cooperative launch (all CTAs resident).  Thread 0 of each
+// CTA arrives with a release-ordered atomic and the last arriver publishes the
+// new generation with a release store; waiters poll it with acquire loads.
+// __syncthreads on both sides extends the ordering to the whole CTA.
 __device__ __forceinline__ void grid_barrier(Ctl* ctl, uint32_t nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile uint32_t* gen = &ctl->bar_gen;
-        const uint32_t g = *gen;
-        __threadfence();
-        if (atomicAdd(&ctl->bar_count, 1u) == nblocks - 1) {
-            ctl->bar_count = 0;
-            __threadfence();
-            atomicAdd(&ctl->bar_gen, 1u);
+        uint32_t g;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&ctl->bar_gen) : "memory");
+        uint32_t old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ctl->bar_count) : "memory");
+        if (old == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(&ctl->bar_count) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&ctl->bar_gen), "r"(g + 1) : "memory");
         } else {
-            while (*gen == g) __nanosleep(32);
+            uint32_t cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&ctl->bar_gen) : "memory");
+            } while (cur == g);
         }
-        __threadfence();
     }
     __syncthreads();
 }

@@ -26,7 +26,6 @@ if os.environ.get("TRACE"):
     from paper_2410_18248_b200 import LAMPS_TRACE
     st = Scheduler(cfg, flags=LAMPS_TRACE)
     st.import_pool(snap, snap["id_base"], snap["next_id"])
-    names = ["score", "publish", "barrier1", "exchange", "barrier2", "scatter", "barrier3", "sort", "admit"]
     acc = []
     for it in range(10):
         flush.zero_()
@@ -35,10 +34,14 @@ if os.environ.get("TRACE"):
         if it >= 3:
             acc.append(t)
     t = np.stack(acc)  # steps x cta x 16
-    d = np.diff(t[:, :, :10], axis=2) / 1.965e3  # us at max clock
-    print("phase durations us (median over steps; max over CTAs / mean over CTAs):")
-    for k, nm in enumerate(names):
-        col = d[:, :, k] if k < 8 else d[:, :1, k]
-        print(f"  {nm:10s} max {np.median(col.max(axis=1)):7.2f}  mean {np.median(col.mean(axis=1)):7.2f}")
-    tot = (t[:, 0, 9] - t[:, :, 0].min(axis=1)) / 1.965e3
-    print("  CTA0 start->admit done (us, median):", float(np.median(tot)))
+    segs = [("score", 0, 1), ("publish", 1, 2), ("barrier1", 2, 3), ("exchange", 3, 4), ("barrier2", 4, 5),
+            ("X load T/H", 5, 10), ("X starts", 10, 11), ("X scatter", 11, 12), ("X ranges", 12, 6),
+            ("barrier3", 6, 7), ("L load", 7, 13), ("L sort", 13, 14), ("L store", 14, 8),
+            ("A pinned", 8, 15), ("A admit", 15, 9)]
+    print("phase durations us (median over steps of max / mean over CTAs):")
+    for nm, a0, a1 in segs:
+        d = (t[:, :, a1] - t[:, :, a0]) / 1.965e3
+        if a0 >= 8 and a1 in (15, 9):
+            d = d[:, :1]
+        print(f"  {nm:12s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
+    ms, nst = st.timing() if False else (None, None)
