@@ -46,7 +46,8 @@ struct PhaseS {                  // S, H, T, X
 };
 constexpr int kSubBits = 12;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
-constexpr uint32_t kMaxRankM = 32;          // largest sub-bucket ranked by comparison
+constexpr uint32_t kMaxRankM = 256;         // largest sub-bucket ranked by comparison
+constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
 struct PhaseL {                  // L
     uint64_t a[kKcap];           // 96 KB
     uint64_t b[kKcap];           // 96 KB
@@ -229,34 +230,78 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     uint32_t* T = b.blocksum + (size_t)G * NB;  // [NB] bucket totals
 
     TRACE(0);
-    // ---------------- S: score this CTA's slots, keys into shared memory
+    // ---------------- S: score this CTA's slots, keys into shared memory.  The seven SoA
+    // words of each chunk of 1024 slots are staged by cp.async (double buffered) while
+    // the previous chunk is scored, one slot per thread.
     if (tid == 0) sm.s.nk = 0;
     for (uint32_t i = tid; i < NB; i += kFT) sm.s.cnt[i] = 0;
-    __syncthreads();
     const uint32_t ngroups = (c.cap + 3u) >> 2;
     const uint32_t gpc = (ngroups + G - 1) / G;
-    const uint32_t g_lo = min(ngroups, bid * gpc), g_hi = min(ngroups, g_lo + gpc);
-    unsigned long long pinned = 0, kor = 0, kand = ~0ull;
-    for (uint32_t g0 = g_lo; g0 < g_hi; g0 += kFT) {
-        const uint32_t g = g0 + tid;
-        uint64_t key[4];
-        uint32_t nk = 0;
-        if (g < g_hi) nk = score_group<DBG>(b.pool, c, a.id_base_mod, b.dbg, g, key, pinned);
-        uint32_t tot;
-        const uint32_t off = block_excl_scan_u32<kFT>(nk, sm.s.w32, &tot);
-        const uint32_t base = sm.s.nk;
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-            if ((uint32_t)j < nk) {
-                sm.s.kbuf[base + off + j] = key[j];
-                kor |= key[j];
-                kand &= key[j];
-                atomicAdd(&sm.s.cnt[bucket_of(key[j], c, half)], 1u);
+    const uint32_t s_lo = 4u * min(ngroups, bid * gpc), s_hi = 4u * min(ngroups, bid * gpc + gpc);
+    const uint32_t nchunk = (s_hi - s_lo + kChunk - 1) / kChunk;
+    uint32_t* stage = sm.s.start;  // [2][7][kChunk] words
+    auto issue = [&](uint32_t ch) {
+        const uint32_t base = s_lo + ch * kChunk, buf = ch & 1u;
+        for (uint32_t q = tid; q < 7u * (kChunk / 4); q += kFT) {
+            const uint32_t ai = q / (kChunk / 4), p4 = 4u * (q % (kChunk / 4));
+            if (base + p4 < s_hi) {
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&stage[(buf * 7u + ai) * kChunk + p4]);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(b.pool.sfc + (size_t)ai * b.pool.stride + base + p4) : "memory");
             }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (nchunk) issue(0);
+    __syncthreads();
+    unsigned long long pinned = 0, kor = 0, kand = ~0ull;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (uint32_t ch = 0; ch < nchunk; ch++) {
+        if (ch + 1 < nchunk) {
+            issue(ch + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
         __syncthreads();
-        if (tid == 0) sm.s.nk = base + tot;
+        const uint32_t slot = s_lo + ch * kChunk + tid;
+        const uint32_t* sw = stage + (ch & 1u) * 7u * kChunk + tid;
+        bool have = false;
+        uint64_t key = 0;
+        if (slot < s_hi) {
+            uint32_t w = sw[0], ctx = sw[kChunk], pre = sw[2 * kChunk], pend = sw[6 * kChunk];
+            if (w & SFC_RAN) {  // A0: the previous batch generated one token
+                ctx += 1u;
+                pre = pre ? pre - 1u : 0u;
+                pend = 0u;
+                b.pool.ctx[slot] = ctx;
+                b.pool.pre[slot] = pre;
+                b.pool.pend[slot] = 0u;
+            }
+            const uint32_t st = sfc_state(w);
+            if (st == ST_PP) pinned += blk(ctx, c);
+            if (st == ST_READY) {
+                have = score_slot<DBG>(c, a.id_base_mod, b.dbg, slot, w, ctx, pre, sw[3 * kChunk],
+                                       sw[4 * kChunk], sw[5 * kChunk], pend, key);
+                b.pool.sfc[slot] = w;
+            }
+        }
+        // warp-aggregated compaction (the order of keys in kbuf does not matter)
+        const uint32_t m = __ballot_sync(0xffffffffu, have);
+        if (m) {
+            const uint32_t leader = __ffs(m) - 1u;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(&sm.s.nk, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (have) {
+                sm.s.kbuf[base + __popc(m & lt_mask)] = key;
+                kor |= key;
+                kand &= key;
+                atomicAdd(&sm.s.cnt[bucket_of(key, c, half)], 1u);
+            }
+        }
         __syncthreads();
     }
+    __syncthreads();
     const uint32_t nk_cta = sm.s.nk;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -285,18 +330,31 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // ---------------- H: publish this CTA's bucket counts
     for (uint32_t j = tid; j < NB; j += kFT) H[(size_t)bid * NB + j] = sm.s.cnt[j];
     TRACE(2);
-    grid_barrier(ctl, G);
+    uint32_t bar = a.step * kBarPerStep;
+    grid_barrier(b.flags, G, ++bar);
     TRACE(3);
 
     // ---------------- T: CTA bid owns buckets [jb0, jb1): it loads that column block of
     // the count matrix (coalesced row segments) into shared memory, scans each column
     // down the CTAs (exclusive prefix per CTA, total per bucket) and writes it back.
     {
-        const uint32_t jb0 = (uint32_t)(((uint64_t)NB * bid) / G), jb1 = (uint32_t)(((uint64_t)NB * (bid + 1)) / G);
+        const uint32_t jb0 = (NB * bid) / G, jb1 = (NB * (bid + 1)) / G;
         const uint32_t w = jb1 - jb0;
         uint32_t* tile = sm.s.cnt;  // G x w (the bucket counts are already published)
-        for (uint32_t r = warp; r < G; r += kFW)
-            for (uint32_t j = lane; j < w; j += 32) tile[r * w + j] = __ldcg(&H[(size_t)r * NB + jb0 + j]);
+        const uint32_t nt = G * w;
+        for (uint32_t q0 = 0; q0 < nt; q0 += 8 * kFT) {  // 8 loads in flight per thread
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint32_t q = q0 + (uint32_t)u * kFT + tid;
+                v[u] = q < nt ? __ldcg(&H[(size_t)(q / w) * NB + jb0 + q % w]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint32_t q = q0 + (uint32_t)u * kFT + tid;
+                if (q < nt) tile[q] = v[u];
+            }
+        }
         __syncthreads();
         for (uint32_t j = warp; j < w; j += kFW) {  // one warp per column, lanes over CTAs
             uint32_t carry = 0;
@@ -315,11 +373,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             if (lane == 0) T[jb0 + j] = carry;
         }
         __syncthreads();
-        for (uint32_t r = warp; r < G; r += kFW)
-            for (uint32_t j = lane; j < w; j += 32) H[(size_t)r * NB + jb0 + j] = tile[r * w + j];
+        for (uint32_t q = tid; q < nt; q += kFT) H[(size_t)(q / w) * NB + jb0 + q % w] = tile[q];
     }
     TRACE(4);
-    grid_barrier(ctl, G);
+    grid_barrier(b.flags, G, ++bar);
     TRACE(5);
 
     // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
@@ -341,20 +398,45 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     }
     __syncthreads();
     TRACE(10);
-    {
-        const uint32_t per = (NB + kFT - 1) / kFT;
-        const uint32_t j0 = min(NB, tid * per), j1 = min(NB, j0 + per);
-        uint32_t s = 0;
-        for (uint32_t j = j0; j < j1; j++) s += sm.s.start[j];
-        uint32_t tot;
-        uint32_t run = block_excl_scan_u32<kFT>(s, sm.s.w32, &tot);
-        for (uint32_t j = j0; j < j1; j++) {
-            const uint32_t t = sm.s.start[j];
-            sm.s.start[j] = run;
-            sm.s.cnt[j] += run;
-            run += t;
+    {   // exclusive scan of the totals; warp w owns a contiguous chunk, lane-strided (no bank conflicts)
+        const uint32_t wc = ((NB + kFW * 32 - 1) / (kFW * 32)) * 32;
+        const uint32_t j0 = warp * wc;
+        uint32_t carry = 0;
+        for (uint32_t r = 0; r < wc; r += 32) {
+            const uint32_t j = j0 + r + lane;
+            const uint32_t v = j < NB ? sm.s.start[j] : 0u;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (j < NB) sm.s.start[j] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (tid == 0) sm.s.base = tot;  // total number of keys
+        if (lane == 0) sm.s.w32[warp] = carry;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = sm.s.w32[lane];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            sm.s.w32[lane] = x - v;
+            if (lane == 31) sm.s.base = x;  // total number of keys
+        }
+        __syncthreads();
+        const uint32_t off = sm.s.w32[warp];
+        for (uint32_t r = 0; r < wc; r += 32) {
+            const uint32_t j = j0 + r + lane;
+            if (j < NB) {
+                const uint32_t st = sm.s.start[j] + off;
+                sm.s.start[j] = st;
+                sm.s.cnt[j] += st;  // scatter cursor
+            }
+        }
     }
     __syncthreads();
     TRACE(11);
@@ -370,7 +452,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // bucket with start >= q_r by binary search; the largest range decides the fallback
     uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now
     if (tid <= G) {
-        const uint32_t q = (uint32_t)(((uint64_t)tid * n) / G);
+        const uint32_t q = (tid * n) / G;  // < 2^32: n <= 2^23, G <= 256
         uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
@@ -385,7 +467,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                           __syncthreads_or(mx > (uint32_t)kKcap);
     const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
     TRACE(6);
-    grid_barrier(ctl, G);
+    grid_barrier(b.flags, G, ++bar);
     TRACE(7);
 
     // ---------------- L: sort the key ranges
@@ -412,7 +494,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         final_buf = 1;
         passes = 1;
     } else {
-        passes = lsd_sort_global(b, n, b.kmask, G, sm.g);
+        passes = lsd_sort_global(b, n, b.kmask, G, sm.g, bar);
         final_buf = passes & 1u;
     }
 
@@ -422,7 +504,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // the keys [0, rb[1]) are sorted by CTA 0 itself.
     const uint32_t need = min(n, a.max_batch);
     const bool wait = fallback || r_end0 < need;
-    if (wait) grid_barrier(ctl, G);
+    if (wait) grid_barrier(b.flags, G, ++bar);
     if (bid != 0) return;
     unsigned long long pinned_all;
     {

@@ -28,11 +28,12 @@ namespace lamps {
 
 namespace {
 
-__global__ void __launch_bounds__(kSortThreads, 1) k_sort(Bufs b) {
+__global__ void __launch_bounds__(kSortThreads, 1) k_sort(Bufs b, StepArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
     const uint32_t n = __ldcg(&b.ctl->n_elig);
-    const uint32_t np = lsd_sort_global(b, n, b.kmask, b.score_grid, sm);
+    uint32_t bar = a.step * kBarPerStep;
+    const uint32_t np = lsd_sort_global(b, n, b.kmask, b.score_grid, sm, bar);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         b.ctl->n_passes = np;
         b.ctl->final_buf = np & 1u;
@@ -50,9 +51,9 @@ int sort_blocks_per_sm() {
 
 cudaError_t launch_sort(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s) {
     (void)c;
-    (void)a;
     Bufs bb = b;
-    void* args[] = {&bb};
+    StepArgs aa = a;
+    void* args[] = {&bb, &aa};
     return cudaLaunchCooperativeKernel((const void*)k_sort, dim3(b.sort_grid), dim3(kSortThreads), args,
                                        sizeof(SortSmem), s);
 }

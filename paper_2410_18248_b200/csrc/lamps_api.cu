@@ -134,6 +134,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
     size_t o_kmask = L.take((size_t)2 * gmax * 8);
     size_t o_pin = L.take((size_t)gmax * 8);
+    size_t o_flags = L.take((size_t)gmax * 4);
     const size_t bsum_lsd = (size_t)2 * gmax * kBins * 4;
     const size_t bsum_fused = h->fused ? ((size_t)h->fused_grid + 1) * fused_max_buckets() * 4 : 0;
     size_t o_bsum = L.take(std::max(bsum_lsd, bsum_fused));
@@ -150,11 +151,14 @@ size_t carve(lamps_t* h, uint8_t* base) {
     if (!base) return L.off;
     uint32_t* soa[8];
     for (int i = 0; i < 8; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
-    h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7]};
+    h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7], cap_pad};
+    for (int i = 1; i < 8; i++)
+        if (soa[i] != soa[0] + (size_t)i * cap_pad) return 0;  // layout invariant used by the kernels
     h->b.keys[0] = reinterpret_cast<uint64_t*>(base + o_keys0);
     h->b.keys[1] = reinterpret_cast<uint64_t*>(base + o_keys1);
     h->b.kmask = reinterpret_cast<unsigned long long*>(base + o_kmask);
     h->b.pin_part = reinterpret_cast<unsigned long long*>(base + o_pin);
+    h->b.flags = reinterpret_cast<uint32_t*>(base + o_flags);
     h->b.blocksum = reinterpret_cast<uint32_t*>(base + o_bsum);
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;

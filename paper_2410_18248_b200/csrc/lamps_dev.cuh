@@ -48,6 +48,7 @@ constexpr uint64_t kFastCtxLimit = 1ull << 20;
 struct Pool {
     uint32_t *sfc, *ctx, *pre, *api, *resp, *post, *pend;
     uint32_t* stamp;  // step number at which the slot was last admitted
+    uint32_t stride;  // words between consecutive SoA arrays (ctx == sfc + stride, ...)
 };
 
 __device__ __forceinline__ uint64_t sat64(u128 x) {

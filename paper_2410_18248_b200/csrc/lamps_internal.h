@@ -20,6 +20,7 @@ constexpr int kMaxBatch = 16384;
 constexpr int kFusedKcap = 12288;    // keys per SM kept in shared memory by the fused step kernel
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
 constexpr int kTraceSlots = 16;
+constexpr uint32_t kBarPerStep = 64;  // grid-barrier values reserved per step
 
 // Device control block: per-step counters, the sort plan and the step summary.
 struct Ctl {
@@ -65,6 +66,7 @@ struct Bufs {
     const void* events;      // lamps_event[max_batch] (device)
     unsigned long long* dbg; // [cap][4] W_P, W_D, W_S, score (LAMPS_DEBUG_OUT) or null
     unsigned long long* trace;  // [grid][16] clock64 at phase boundaries (LAMPS_TRACE) or null
+    uint32_t* flags;         // [grid] grid-barrier flags
 };
 
 // launchers (kernels_step.cu / kernels_sort.cu)

@@ -152,6 +152,36 @@ __device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, ui
     return nk;
 }
 
+// One slot given its seven SoA words (A0 default update already applied by the
+// caller).  Returns true and the key if the slot is READY; updates *w (sfc).
+template <bool DBG>
+__device__ __forceinline__ bool score_slot(const Cost& c, uint32_t id_base_mod, unsigned long long* dbg,
+                                           uint32_t slot, uint32_t& w, uint32_t ctx, uint32_t pre,
+                                           uint32_t api, uint32_t resp, uint32_t post, uint32_t pend,
+                                           uint64_t& key) {
+    const uint32_t has = sfc_has(w);
+    uint64_t wp, wd, ws, sc;
+    uint32_t strat;
+    const uint64_t span = (uint64_t)ctx + pre + (has ? (uint64_t)resp + post : 0ull);
+    if (c.fast && span < kFastCtxLimit) {
+        strat = strategy_score_fast(ctx, pre, api, resp, post, pend, has, c, &sc, &wp, &wd, &ws);
+    } else {
+        wp = wd = ws = 0;
+        strat = STR_NONE;
+        if (has) strat = strategy_of(ctx, pre, api, c, &wp, &wd, &ws);
+        sc = score_of(ctx, pre, api, resp, post, pend, has, strat, c);
+    }
+    const uint32_t cnt = sfc_cnt(w);
+    const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
+    w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u);
+    key = ((uint64_t)(starv ^ 1u) << (c.SB + c.IB)) | (sc << c.IB) | ((slot - id_base_mod) & c.cap_mask);
+    if (DBG) {
+        unsigned long long* d = dbg + 4ull * slot;
+        d[0] = wp; d[1] = wd; d[2] = ws; d[3] = sc;
+    }
+    return true;
+}
+
 // A5 admission by one 1024-thread CTA over the ranked keys (see k_admit).
 struct AdmitSmem {
     unsigned long long w64[32];
