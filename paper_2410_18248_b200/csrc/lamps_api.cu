@@ -134,7 +134,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
     size_t o_kmask = L.take((size_t)2 * gmax * 8);
     size_t o_pin = L.take((size_t)gmax * 8);
-    size_t o_flags = L.take((size_t)gmax * 4);
+    size_t o_flags = L.take((size_t)32 * 4 * (2 + 16));  // grid barrier: release word, 16 group counters, root
     const size_t bsum_lsd = (size_t)2 * gmax * kBins * 4;
     const size_t bsum_fused = h->fused ? ((size_t)h->fused_grid + 1) * fused_max_buckets() * 4 : 0;
     size_t o_bsum = L.take(std::max(bsum_lsd, bsum_fused));
@@ -216,6 +216,10 @@ void grids(lamps_t* h, bool query_device) {
 bool fast_bounds_ok(const lamps_config& c) {
     typedef unsigned __int128 U;
     const U L = (U)kFastCtxLimit, lim = (U)1 << 63;
+    const uint64_t m32 = 1ull << 32;
+    if (c.A1 >= m32 || c.A2 >= m32 || c.S0 >= m32 || c.S1 >= m32 || c.tau >= m32 || c.c_other >= (1ull << 26))
+        return false;
+    if ((uint64_t)L * L >= (1ull << 40)) return false;  // mul32x40 operand bound
     const U api_max = 0xffffffffull, pend_max = 0xffffffffull;
     const U tf_in = (U)c.A1 * L + (U)c.A2 * L * L;         // T_fwd before the shift
     const U ts_in = (U)c.S0 + (U)c.S1 * L;

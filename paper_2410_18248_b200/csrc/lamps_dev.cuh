@@ -119,24 +119,31 @@ __device__ __forceinline__ uint64_t score_of(uint64_t ctx, uint64_t pre, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// Fast path: plain 64-bit arithmetic with no overflow checks.  The host sets
-// Cost::fast only when, for every context value c < kFastCtxLimit (2^20
-// tokens), it has proven with exact 128-bit arithmetic that every product and
-// every sum below stays < 2^63 (see fast_bounds_ok in lamps_api.cu); the kernel
+// Fast path: 32x32->64 products, no overflow checks.  The host sets
+// Cost::fast only when A1, A2, S0, S1, tau < 2^32, c_other < 2^26 and, for every
+// context value c < kFastCtxLimit (2^20 tokens), it has proven with exact
+// 128-bit arithmetic that every product and every sum below stays < 2^63 (see
+// fast_bounds_ok in lamps_api.cu); the kernel
 // takes this path for a slot iff ctx + pre + resp + post < 2^20.  Under those
 // bounds the results equal the exact ones (no clamp can trigger except the
 // final min with 2^SB - 1, which is applied).
 // ---------------------------------------------------------------------------
+// (fast path: A1, A2, S0, S1, tau < 2^32 and every context value x < 2^20, host-checked)
+__device__ __forceinline__ uint64_t wide32(uint32_t a, uint32_t b) { return (uint64_t)a * b; }
+// 32-bit a times a 64-bit b < 2^40
+__device__ __forceinline__ uint64_t mul32x40(uint32_t a, uint64_t b) {
+    return wide32(a, (uint32_t)b) + (wide32(a, (uint32_t)(b >> 32)) << 32);
+}
 __device__ __forceinline__ uint64_t t_fwd_fast(uint32_t x, const Cost& c) {
-    return (c.A1 * x + c.A2 * ((uint64_t)x * x)) >> c.SH;
+    return (wide32((uint32_t)c.A1, x) + mul32x40((uint32_t)c.A2, wide32(x, x))) >> c.SH;
 }
 __device__ __forceinline__ uint64_t t_swap_fast(uint32_t x, const Cost& c) {
-    return x ? (c.S0 + c.S1 * x) >> c.SH : 0ull;
+    return x ? (c.S0 + wide32((uint32_t)c.S1, x)) >> c.SH : 0ull;
 }
 // F(n) = sum_{j=1..n} ceil(j/B) = B Q(Q+1)/2 + R(Q+1), n = Q B + R
 __device__ __forceinline__ uint64_t ramp_fast(uint32_t n, const Cost& c) {
     const uint32_t Q = n >> c.lgB, R = n & (c.B - 1u);
-    return ((((uint64_t)Q * (Q + 1u)) >> 1) << c.lgB) + (uint64_t)R * (Q + 1u);
+    return ((wide32(Q, Q + 1u) >> 1) << c.lgB) + wide32(R, Q + 1u);
 }
 
 // strategy (A1) and score (A2) of one READY slot on the fast path
@@ -144,24 +151,25 @@ __device__ __forceinline__ uint32_t strategy_score_fast(uint32_t ctx, uint32_t p
                                                         uint32_t resp, uint32_t post, uint32_t pend,
                                                         uint32_t has, const Cost& c, uint64_t* score,
                                                         uint64_t* wp_o, uint64_t* wd_o, uint64_t* ws_o) {
+    const uint32_t tau = (uint32_t)c.tau;
     const uint32_t ci = ctx + pre;
-    uint64_t s = (uint64_t)((ctx + c.B - 1u) >> c.lgB) * pend + c.tau * (ramp_fast(ci, c) - ramp_fast(ctx, c));
+    uint64_t s = wide32((ctx + c.B - 1u) >> c.lgB, pend) + mul32x40(tau, ramp_fast(ci, c) - ramp_fast(ctx, c));
     uint32_t strat = STR_NONE;
     uint64_t wp = 0, wd = 0, ws = 0;
     if (has) {
-        const uint64_t cb = (uint64_t)ci + c.c_other;
+        const uint32_t cb = ci + (uint32_t)c.c_other;  // < 2^27
         const uint64_t tf = t_fwd_fast(ci, c), ts = t_swap_fast(ci, c);
-        wp = (uint64_t)api * ci;
+        wp = wide32(api, ci);
         wd = tf * cb;
         ws = (ts * cb) << 1;
         strat = (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
         const uint32_t bci = (ci + c.B - 1u) >> c.lgB;
         const uint32_t cr = ci + resp;
         uint64_t a;
-        if (strat == STR_P) a = (uint64_t)bci * api;
+        if (strat == STR_P) a = wide32(bci, api);
         else if (strat == STR_D) a = t_fwd_fast(cr, c) * ((cr + c.B - 1u) >> c.lgB);
         else a = (ts * bci) << 1;
-        s += a + c.tau * (ramp_fast(cr + post, c) - ramp_fast(cr, c));
+        s += a + mul32x40(tau, ramp_fast(cr + post, c) - ramp_fast(cr, c));
     }
     *score = s > c.score_max ? c.score_max : s;
     *wp_o = wp; *wd_o = wd; *ws_o = ws;

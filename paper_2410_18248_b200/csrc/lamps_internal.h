@@ -66,7 +66,7 @@ struct Bufs {
     const void* events;      // lamps_event[max_batch] (device)
     unsigned long long* dbg; // [cap][4] W_P, W_D, W_S, score (LAMPS_DEBUG_OUT) or null
     unsigned long long* trace;  // [grid][16] clock64 at phase boundaries (LAMPS_TRACE) or null
-    uint32_t* flags;         // [grid] grid-barrier flags
+    uint32_t* flags;         // grid barrier words (see sort_dev.cuh)
 };
 
 // launchers (kernels_step.cu / kernels_sort.cu)

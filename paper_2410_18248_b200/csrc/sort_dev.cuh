@@ -20,27 +20,35 @@ struct SortSmem {
     uint32_t n_pass;
 };
 
-// Grid barrier for a cooperative launch (all CTAs resident): every CTA
-// publishes the barrier's value in its own flag (release store) and warp 0 of
-// every CTA polls all flags (acquire loads) until each has reached the value.
-// No same-address atomics (148 serialized L2 atomics cost ~1.7 us on B200);
-// values grow monotonically across barriers and steps, so flags never reset.
-__device__ __forceinline__ void grid_barrier(uint32_t* flags, uint32_t nblocks, uint32_t value) {
+// Grid barrier for a cooperative launch (all CTAs resident), two-level: CTAs
+// arrive on one of kBarGroups group counters (separate 128-byte lines, so
+// same-address atomics serialize only within a group); the last arriver of a
+// group arrives on the root counter; the last root arriver publishes the
+// barrier value with a release store that every CTA polls (acquire).  Values
+// grow monotonically across barriers and steps; counters self-reset.
+constexpr uint32_t kBarGroups = 16;
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks, uint32_t value) {
     __syncthreads();
-    if (threadIdx.x < 32) {
-        const uint32_t lane = threadIdx.x;
-        if (lane == 0)
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(value) : "memory");
-        bool done;
-        do {
-            bool ok = true;
-            for (uint32_t i = lane; i < nblocks; i += 32) {
-                uint32_t v;
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
-                ok = ok && (int)(v - value) >= 0;
+    if (threadIdx.x == 0) {
+        const uint32_t g = blockIdx.x % kBarGroups;
+        const uint32_t gsize = nblocks / kBarGroups + (g < nblocks % kBarGroups ? 1u : 0u);
+        const uint32_t ngroups = nblocks < kBarGroups ? nblocks : kBarGroups;
+        uint32_t* gcnt = bar + 32u * (1u + g);  // group counters, 128 B apart
+        uint32_t* root = bar + 32u * (1u + kBarGroups);
+        uint32_t old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(gcnt) : "memory");
+        if (old == gsize - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(gcnt) : "memory");
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(root) : "memory");
+            if (old == ngroups - 1) {
+                asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(root) : "memory");
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(value) : "memory");
             }
-            done = __all_sync(0xffffffffu, ok);
-        } while (!done);
+        }
+        uint32_t cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while ((int)(cur - value) < 0);
     }
     __syncthreads();
 }
