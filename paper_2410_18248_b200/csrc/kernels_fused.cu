@@ -48,6 +48,7 @@ constexpr int kSubBits = 12;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
 constexpr uint32_t kMaxRankM = 256;         // largest sub-bucket ranked by comparison
 constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
+constexpr int kMaxBig = kKcap / (kMaxRankM + 1) + 1;  // sub-buckets > kMaxRankM in one range
 struct PhaseL {                  // L
     uint64_t a[kKcap];           // 96 KB
     uint64_t b[kKcap];           // 96 KB
@@ -62,8 +63,11 @@ struct PhaseL {                  // L
             uint32_t cnt[kSubBuckets];   // 16 KB
             uint32_t pos[kSubBuckets];   // 16 KB
             uint32_t w32[kFW];
-            uint32_t maxm;
+            uint32_t nbig;
         };
+    };
+    union {                              // big sub-buckets awaiting the segment LSD
+        struct { uint32_t big_lo[kMaxBig], big_n[kMaxBig]; };
     };
     unsigned long long red[2][kFW];
 };
@@ -86,15 +90,15 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint3
     return ns * half + fb;
 }
 
-// Stable LSD sort of n (<= kKcap) keys in shared memory over the 8-bit digit
-// positions where `vary` has bits; returns the buffer holding the result.
-// Keys are spread evenly over the 32 warps: warp w owns the contiguous
-// segment [w*32*ipt, (w+1)*32*ipt), item j of lane l is position
-// w*32*ipt + j*32 + l, so (warp, j, lane) order is array order (stability).
-__device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned long long vary) {
+// Stable LSD sort of the n (<= kKcap) keys at src[0..n) in shared memory over the
+// 8-bit digit positions where `vary` has bits, ping-ponging with dst[0..n);
+// returns the buffer holding the result.  Keys are spread evenly over the 32
+// warps: warp w owns the contiguous segment [w*32*ipt, (w+1)*32*ipt), item j of
+// lane l is position w*32*ipt + j*32 + l, so (warp, j, lane) order is array
+// order (stability).  Ranks come from a ballot multisplit (digit_peers).
+__device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint64_t* src, uint64_t* dst, uint32_t n,
+                                               unsigned long long vary) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    uint64_t* src = sm.a;
-    uint64_t* dst = sm.b;
     const uint32_t ipt = (n + kFT - 1) / kFT;  // items per lane, <= kLocalItems
     const uint32_t seg = 32u * ipt;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -123,8 +127,7 @@ __device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned 
             }
         }
         __syncthreads();
-        // per digit: exclusive prefix over the 32 warps, 4 threads per digit (8 warps each)
-        {
+        {   // per digit: exclusive prefix over the 32 warps, 4 threads per digit (8 warps each)
             const uint32_t d = tid & 255u, q = tid >> 8;
             uint32_t run = 0;
 #pragma unroll
@@ -163,38 +166,58 @@ __device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint32_t n, unsigned 
     return src;
 }
 
-// Sort of the n keys of a range in shared memory (sm.a), returns the buffer
-// holding the result.  One MSD step: count and scatter by the 12 highest bits
-// that vary in the range (shared-memory atomics; the order inside a
-// sub-bucket is then fixed exactly below), then every key finds its final
-// place inside its sub-bucket by counting the smaller keys there (keys are
-// unique).  If some sub-bucket holds more than kMaxRankM keys (many keys with
-// nearly equal scores), the range is sorted by the stable LSD instead.
-__device__ __forceinline__ uint64_t* local_sort(PhaseL& sm, uint32_t n, unsigned long long vary) {
+__device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint32_t n,
+                                             unsigned long long& o, unsigned long long& an) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    o = 0; an = ~0ull;
+    for (uint32_t i = tid; i < n; i += kFT) { o |= x[i]; an &= x[i]; }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+        an &= __shfl_xor_sync(0xffffffffu, an, s);
+    }
+    if (lane == 0) { sm.red[0][warp] = o; sm.red[1][warp] = an; }
+    __syncthreads();
+    o = 0; an = ~0ull;
+    for (int w = 0; w < kFW; w++) { o |= sm.red[0][w]; an &= sm.red[1][w]; }
+    __syncthreads();
+}
+
+// Sort of the n keys of a range in shared memory (sm.a), result in sm.a.  One
+// MSD step: count and scatter by the 12 highest bits that vary in the range
+// (shared-memory atomics; the order inside a sub-bucket is fixed exactly
+// below), then every key of a sub-bucket of <= kMaxRankM keys finds its final
+// place by counting the smaller keys there (keys are unique).  Larger
+// sub-buckets (many keys with (nearly) equal scores) are sorted one by one by
+// the stable LSD over the bits that vary inside them (mostly the id bits).
+__device__ __forceinline__ void local_sort(PhaseL& sm, uint32_t n, unsigned long long vary) {
     const uint32_t tid = threadIdx.x;
-    if (n <= 1 || vary == 0) return sm.a;
+    if (n <= 1 || vary == 0) return;
     const int h = 63 - __clzll((long long)vary);
     const uint32_t lo = h >= kSubBits - 1 ? (uint32_t)(h - (kSubBits - 1)) : 0u;
     const uint32_t dmask = kSubBuckets - 1;
     for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.cnt[i] = 0;
-    if (tid == 0) sm.maxm = 0;
+    if (tid == 0) sm.nbig = 0;
     __syncthreads();
     for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.cnt[(uint32_t)(sm.a[i] >> lo) & dmask], 1u);
     __syncthreads();
-    {   // exclusive scan of the counts: 4 consecutive counters per thread
+    {   // exclusive scan of the counts: 4 consecutive counters per thread; list the big sub-buckets
         const uint32_t c0 = sm.cnt[4 * tid], c1 = sm.cnt[4 * tid + 1], c2 = sm.cnt[4 * tid + 2],
                        c3 = sm.cnt[4 * tid + 3];
         uint32_t tot;
         const uint32_t e = block_excl_scan_u32<kFT>(c0 + c1 + c2 + c3, sm.w32, &tot);
-        sm.pos[4 * tid] = e;
-        sm.pos[4 * tid + 1] = e + c0;
-        sm.pos[4 * tid + 2] = e + c0 + c1;
-        sm.pos[4 * tid + 3] = e + c0 + c1 + c2;
-        const uint32_t m = max(max(c0, c1), max(c2, c3));
-        if (m > kMaxRankM) atomicMax(&sm.maxm, m);
+        const uint32_t st[4] = {e, e + c0, e + c0 + c1, e + c0 + c1 + c2};
+        const uint32_t cc[4] = {c0, c1, c2, c3};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            sm.pos[4 * tid + q] = st[q];
+            if (cc[q] > kMaxRankM) {
+                const uint32_t k = atomicAdd(&sm.nbig, 1u);
+                if (k < kMaxBig) { sm.big_lo[k] = st[q]; sm.big_n[k] = cc[q]; }
+            }
+        }
     }
     __syncthreads();
-    if (sm.maxm > kMaxRankM) return local_lsd(sm, n, vary);  // block-uniform
     for (uint32_t i = tid; i < n; i += kFT) {
         const uint64_t k = sm.a[i];
         sm.b[atomicAdd(&sm.pos[(uint32_t)(k >> lo) & dmask], 1u)] = k;
@@ -203,13 +226,23 @@ __device__ __forceinline__ uint64_t* local_sort(PhaseL& sm, uint32_t n, unsigned
     for (uint32_t i = tid; i < n; i += kFT) {  // pos[d] is now the end of sub-bucket d
         const uint64_t k = sm.b[i];
         const uint32_t d = (uint32_t)(k >> lo) & dmask;
-        const uint32_t e = sm.pos[d], s0 = e - sm.cnt[d];
+        const uint32_t e = sm.pos[d], m = sm.cnt[d], s0 = e - m;
+        if (m > kMaxRankM) { sm.a[i] = k; continue; }  // big: sorted below
         uint32_t r = 0;
         for (uint32_t q = s0; q < e; q++) r += sm.b[q] < k ? 1u : 0u;
         sm.a[s0 + r] = k;
     }
     __syncthreads();
-    return sm.a;
+    const uint32_t nbig = min(sm.nbig, (uint32_t)kMaxBig);
+    for (uint32_t t = 0; t < nbig; t++) {
+        const uint32_t s0 = sm.big_lo[t], m = sm.big_n[t];
+        unsigned long long o, an;
+        block_or_and(sm, sm.a + s0, m, o, an);
+        const uint64_t* r = local_lsd(sm, sm.a + s0, sm.b + s0, m, o ^ an);
+        if (r != sm.a + s0)
+            for (uint32_t i = tid; i < m; i += kFT) sm.a[s0 + i] = r[i];
+        __syncthreads();
+    }
 }
 
 #define TRACE(k)                                                                         \
@@ -476,21 +509,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         const uint32_t rn = r_hi - r_lo;
         for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
         TRACE(13);
-        unsigned long long o = 0, an = ~0ull;
-        for (uint32_t i = tid; i < rn; i += kFT) { o |= sm.l.a[i]; an &= sm.l.a[i]; }
-#pragma unroll
-        for (int s = 16; s; s >>= 1) {
-            o |= __shfl_xor_sync(0xffffffffu, o, s);
-            an &= __shfl_xor_sync(0xffffffffu, an, s);
-        }
-        if (lane == 0) { sm.l.red[0][warp] = o; sm.l.red[1][warp] = an; }
-        __syncthreads();
-        o = 0; an = ~0ull;
-        for (int w = 0; w < kFW; w++) { o |= sm.l.red[0][w]; an &= sm.l.red[1][w]; }
-        __syncthreads();
-        const uint64_t* res = local_sort(sm.l, rn, rn ? (o ^ an) : 0ull);
+        unsigned long long o, an;
+        block_or_and(sm.l, sm.l.a, rn, o, an);
+        local_sort(sm.l, rn, rn ? (o ^ an) : 0ull);
         TRACE(14);
-        for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = res[i];
+        for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;
         passes = 1;
     } else {

@@ -219,7 +219,7 @@ bool fast_bounds_ok(const lamps_config& c) {
     const uint64_t m32 = 1ull << 32;
     if (c.A1 >= m32 || c.A2 >= m32 || c.S0 >= m32 || c.S1 >= m32 || c.tau >= m32 || c.c_other >= (1ull << 26))
         return false;
-    if ((uint64_t)L * L >= (1ull << 40)) return false;  // mul32x40 operand bound
+    if ((L - 1) * (L - 1) >= ((U)1 << 40)) return false;  // mul32x40 operand bound (x^2, ramps)
     const U api_max = 0xffffffffull, pend_max = 0xffffffffull;
     const U tf_in = (U)c.A1 * L + (U)c.A2 * L * L;         // T_fwd before the shift
     const U ts_in = (U)c.S0 + (U)c.S1 * L;
