@@ -190,7 +190,8 @@ __device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint
 // place by counting the smaller keys there (keys are unique).  Larger
 // sub-buckets (many keys with (nearly) equal scores) are sorted one by one by
 // the stable LSD over the bits that vary inside them (mostly the id bits).
-__device__ __forceinline__ void local_sort(PhaseL& sm, uint32_t n, unsigned long long vary) {
+__device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
+                                           unsigned long long vary) {
     const uint32_t tid = threadIdx.x;
     if (n <= 1 || vary == 0) return;
     const int h = 63 - __clzll((long long)vary);
@@ -199,7 +200,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint32_t n, unsigned long
     for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.cnt[i] = 0;
     if (tid == 0) sm.nbig = 0;
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.cnt[(uint32_t)(sm.a[i] >> lo) & dmask], 1u);
+    for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.cnt[(uint32_t)(A[i] >> lo) & dmask], 1u);
     __syncthreads();
     {   // exclusive scan of the counts: 4 consecutive counters per thread; list the big sub-buckets
         const uint32_t c0 = sm.cnt[4 * tid], c1 = sm.cnt[4 * tid + 1], c2 = sm.cnt[4 * tid + 2],
@@ -219,28 +220,28 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint32_t n, unsigned long
     }
     __syncthreads();
     for (uint32_t i = tid; i < n; i += kFT) {
-        const uint64_t k = sm.a[i];
-        sm.b[atomicAdd(&sm.pos[(uint32_t)(k >> lo) & dmask], 1u)] = k;
+        const uint64_t k = A[i];
+        Bf[atomicAdd(&sm.pos[(uint32_t)(k >> lo) & dmask], 1u)] = k;
     }
     __syncthreads();
     for (uint32_t i = tid; i < n; i += kFT) {  // pos[d] is now the end of sub-bucket d
-        const uint64_t k = sm.b[i];
+        const uint64_t k = Bf[i];
         const uint32_t d = (uint32_t)(k >> lo) & dmask;
         const uint32_t e = sm.pos[d], m = sm.cnt[d], s0 = e - m;
-        if (m > kMaxRankM) { sm.a[i] = k; continue; }  // big: sorted below
+        if (m > kMaxRankM) { A[i] = k; continue; }  // big: sorted below
         uint32_t r = 0;
-        for (uint32_t q = s0; q < e; q++) r += sm.b[q] < k ? 1u : 0u;
-        sm.a[s0 + r] = k;
+        for (uint32_t q = s0; q < e; q++) r += Bf[q] < k ? 1u : 0u;
+        A[s0 + r] = k;
     }
     __syncthreads();
     const uint32_t nbig = min(sm.nbig, (uint32_t)kMaxBig);
     for (uint32_t t = 0; t < nbig; t++) {
         const uint32_t s0 = sm.big_lo[t], m = sm.big_n[t];
         unsigned long long o, an;
-        block_or_and(sm, sm.a + s0, m, o, an);
-        const uint64_t* r = local_lsd(sm, sm.a + s0, sm.b + s0, m, o ^ an);
-        if (r != sm.a + s0)
-            for (uint32_t i = tid; i < m; i += kFT) sm.a[s0 + i] = r[i];
+        block_or_and(sm, A + s0, m, o, an);
+        const uint64_t* r = local_lsd(sm, A + s0, Bf + s0, m, o ^ an);
+        if (r != A + s0)
+            for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
         __syncthreads();
     }
 }
@@ -509,9 +510,21 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         const uint32_t rn = r_hi - r_lo;
         for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
         TRACE(13);
+        // starving keys come first; sort the two parts separately (each with the bits that
+        // vary inside it), so the starving flag does not take the MSD digit
+        const uint32_t key_top = c.SB + c.IB;
+        uint32_t ns = 0;
+        for (uint32_t i = tid; i < rn; i += kFT) ns += ((sm.l.a[i] >> key_top) & 1ull) ? 0u : 1u;
+        {
+            uint32_t tot;
+            (void)block_excl_scan_u32<kFT>(ns, sm.l.w32, &tot);
+            ns = tot;
+        }
         unsigned long long o, an;
-        block_or_and(sm.l, sm.l.a, rn, o, an);
-        local_sort(sm.l, rn, rn ? (o ^ an) : 0ull);
+        block_or_and(sm.l, sm.l.a, ns, o, an);
+        local_sort(sm.l, sm.l.a, sm.l.b, ns, ns ? (o ^ an) : 0ull);
+        block_or_and(sm.l, sm.l.a + ns, rn - ns, o, an);
+        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, rn > ns ? (o ^ an) : 0ull);
         TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;
