@@ -33,7 +33,7 @@ constexpr int kFW = kFT / 32;               // warps
 constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
 constexpr int kBucketM = 7;                 // score bits per octave
 constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
-constexpr int kLocalItems = kKcap / kFT;    // 12
+constexpr int kLocalItems = kKcap / kFT;    // 10
 constexpr int kTRows = 8;                   // count exchange: up to 256 CTAs
 
 struct PhaseS {                  // S, H, T, X
@@ -44,9 +44,9 @@ struct PhaseS {                  // S, H, T, X
     unsigned long long red[3][kFW];
     uint32_t nk, base;
 };
-constexpr int kSubBits = 12;                // local MSD digit
+constexpr int kSubBits = 14;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
-constexpr uint32_t kMaxRankM = 256;         // largest sub-bucket ranked by comparison
+constexpr uint32_t kMaxRankM = 64;          // largest sub-bucket ranked by comparison
 constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
 constexpr int kMaxBig = kKcap / (kMaxRankM + 1) + 1;  // sub-buckets > kMaxRankM in one range
 struct PhaseL {                  // L
@@ -60,10 +60,10 @@ struct PhaseL {                  // L
             uint32_t scan[kFW];
         };
         struct {                         // local MSD + rank
-            uint32_t cnt[kSubBuckets];   // 16 KB
-            uint32_t pos[kSubBuckets];   // 16 KB
+            uint32_t pos[kSubBuckets];   // 64 KB: counts -> starts -> ends
             uint32_t w32[kFW];
             uint32_t nbig;
+            unsigned long long mm[2][kFW];
         };
     };
     union {                              // big sub-buckets awaiting the segment LSD
@@ -183,56 +183,111 @@ __device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint
     __syncthreads();
 }
 
-// Sort of the n keys of a range in shared memory (sm.a), result in sm.a.  One
-// MSD step: count and scatter by the 12 highest bits that vary in the range
-// (shared-memory atomics; the order inside a sub-bucket is fixed exactly
-// below), then every key of a sub-bucket of <= kMaxRankM keys finds its final
-// place by counting the smaller keys there (keys are unique).  Larger
-// sub-buckets (many keys with (nearly) equal scores) are sorted one by one by
-// the stable LSD over the bits that vary inside them (mostly the id bits).
+// Float-like digit of a score: exact below 2^mb, else (bit length - mb) << mb plus
+// the mb bits below the leading one.  Monotone in the score.
+__device__ __forceinline__ uint32_t flt_digit(uint64_t sc, uint32_t mb) {
+    const uint32_t e = 64u - (uint32_t)__clzll((long long)sc);
+    if (e <= mb) return (uint32_t)sc;
+    return ((e - mb) << mb) + (uint32_t)((sc >> (e - 1 - mb)) & ((1u << mb) - 1u));
+}
+
+// Sort of the n keys at A[0..n) (same starving flag) in shared memory, result in
+// A (Bf is scratch).  One MSD step: count and scatter by a 14-bit float-like digit
+// of the score (relative to the smallest in the part, so heavy-tailed score
+// ranges still spread over the digit space); the order inside a group is then
+// fixed exactly: every key of a group of <= kMaxRankM keys counts the smaller
+// keys there (keys are unique).  Larger groups (many keys with (nearly) equal
+// scores) are sorted one by one by the stable LSD over the bits that vary
+// inside them (mostly the id bits).
 __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
-                                           unsigned long long vary) {
-    const uint32_t tid = threadIdx.x;
-    if (n <= 1 || vary == 0) return;
-    const int h = 63 - __clzll((long long)vary);
-    const uint32_t lo = h >= kSubBits - 1 ? (uint32_t)(h - (kSubBits - 1)) : 0u;
-    const uint32_t dmask = kSubBuckets - 1;
-    for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.cnt[i] = 0;
+                                           const Cost& c) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (n <= 1) return;
+    // score range of the part -> mantissa bits mb so that the digit span fits 14 bits
+    unsigned long long smin = ~0ull, smax = 0;
+    for (uint32_t i = tid; i < n; i += kFT) {
+        const unsigned long long sc = (A[i] >> c.IB) & c.score_max;
+        smin = sc < smin ? sc : smin;
+        smax = sc > smax ? sc : smax;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, smin, o), y = __shfl_xor_sync(0xffffffffu, smax, o);
+        smin = x < smin ? x : smin;
+        smax = y > smax ? y : smax;
+    }
+    if (lane == 0) { sm.mm[0][warp] = smin; sm.mm[1][warp] = smax; }
     if (tid == 0) sm.nbig = 0;
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.cnt[(uint32_t)(A[i] >> lo) & dmask], 1u);
+    smin = ~0ull; smax = 0;
+    for (int w = 0; w < kFW; w++) {
+        smin = sm.mm[0][w] < smin ? sm.mm[0][w] : smin;
+        smax = sm.mm[1][w] > smax ? sm.mm[1][w] : smax;
+    }
+    uint32_t mb = kSubBits;
+    while (mb > 0 && flt_digit(smax, mb) - flt_digit(smin, mb) >= (uint32_t)kSubBuckets) mb--;
+    const uint32_t dlo = flt_digit(smin, mb);
+#define DIGIT(k) (flt_digit(((k) >> c.IB) & c.score_max, mb) - dlo)
+    for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.pos[i] = 0;
     __syncthreads();
-    {   // exclusive scan of the counts: 4 consecutive counters per thread; list the big sub-buckets
-        const uint32_t c0 = sm.cnt[4 * tid], c1 = sm.cnt[4 * tid + 1], c2 = sm.cnt[4 * tid + 2],
-                       c3 = sm.cnt[4 * tid + 3];
-        uint32_t tot;
-        const uint32_t e = block_excl_scan_u32<kFT>(c0 + c1 + c2 + c3, sm.w32, &tot);
-        const uint32_t st[4] = {e, e + c0, e + c0 + c1, e + c0 + c1 + c2};
-        const uint32_t cc[4] = {c0, c1, c2, c3};
+    for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.pos[DIGIT(A[i])], 1u);
+    __syncthreads();
+    {   // counts -> exclusive starts; warp w owns a contiguous chunk, lane-strided (no bank conflicts)
+        constexpr uint32_t wc = kSubBuckets / kFW;  // 512
+        const uint32_t j0 = warp * wc;
+        uint32_t carry = 0;
+        for (uint32_t r = 0; r < wc; r += 32) {
+            const uint32_t j = j0 + r + lane;
+            const uint32_t v = sm.pos[j];
+            uint32_t x = v;
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            sm.pos[4 * tid + q] = st[q];
-            if (cc[q] > kMaxRankM) {
-                const uint32_t k = atomicAdd(&sm.nbig, 1u);
-                if (k < kMaxBig) { sm.big_lo[k] = st[q]; sm.big_n[k] = cc[q]; }
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
             }
+            sm.pos[j] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
+        if (lane == 0) sm.w32[warp] = carry;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = sm.w32[lane];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            sm.w32[lane] = x - v;
+        }
+        __syncthreads();
+        const uint32_t off = sm.w32[warp];
+        for (uint32_t r = 0; r < wc; r += 32) sm.pos[j0 + r + lane] += off;
     }
     __syncthreads();
     for (uint32_t i = tid; i < n; i += kFT) {
         const uint64_t k = A[i];
-        Bf[atomicAdd(&sm.pos[(uint32_t)(k >> lo) & dmask], 1u)] = k;
+        Bf[atomicAdd(&sm.pos[DIGIT(k)], 1u)] = k;
     }
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += kFT) {  // pos[d] is now the end of sub-bucket d
+    // pos[d] is now the end of group d, its start the end of group d-1
+    for (uint32_t i = tid; i < n; i += kFT) {
         const uint64_t k = Bf[i];
-        const uint32_t d = (uint32_t)(k >> lo) & dmask;
-        const uint32_t e = sm.pos[d], m = sm.cnt[d], s0 = e - m;
-        if (m > kMaxRankM) { A[i] = k; continue; }  // big: sorted below
+        const uint32_t d = DIGIT(k);
+        const uint32_t e = sm.pos[d], s0 = d ? sm.pos[d - 1] : 0u, m = e - s0;
+        if (m > kMaxRankM) {
+            A[i] = k;  // sorted below
+            if (i == s0) {
+                const uint32_t t = atomicAdd(&sm.nbig, 1u);
+                if (t < (uint32_t)kMaxBig) { sm.big_lo[t] = s0; sm.big_n[t] = m; }
+            }
+            continue;
+        }
         uint32_t r = 0;
         for (uint32_t q = s0; q < e; q++) r += Bf[q] < k ? 1u : 0u;
         A[s0 + r] = k;
     }
+#undef DIGIT
     __syncthreads();
     const uint32_t nbig = min(sm.nbig, (uint32_t)kMaxBig);
     for (uint32_t t = 0; t < nbig; t++) {
@@ -520,11 +575,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             (void)block_excl_scan_u32<kFT>(ns, sm.l.w32, &tot);
             ns = tot;
         }
-        unsigned long long o, an;
-        block_or_and(sm.l, sm.l.a, ns, o, an);
-        local_sort(sm.l, sm.l.a, sm.l.b, ns, ns ? (o ^ an) : 0ull);
-        block_or_and(sm.l, sm.l.a + ns, rn - ns, o, an);
-        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, rn > ns ? (o ^ an) : 0ull);
+        local_sort(sm.l, sm.l.a, sm.l.b, ns, c);
+        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, c);
         TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;

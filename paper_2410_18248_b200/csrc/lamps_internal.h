@@ -17,7 +17,7 @@ constexpr int kSortMaxTilesPerCta = 8;               // capacity <= 2^23 over >=
 constexpr int kScoreThreads = 256;  // K1 CTA
 constexpr int kAdmitThreads = 1024; // K3 (single CTA)
 constexpr int kMaxBatch = 16384;
-constexpr int kFusedKcap = 12288;    // keys per SM kept in shared memory by the fused step kernel
+constexpr int kFusedKcap = 10240;    // keys per SM kept in shared memory by the fused step kernel
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
 constexpr int kTraceSlots = 16;
 constexpr uint32_t kBarPerStep = 64;  // grid-barrier values reserved per step
