@@ -200,7 +200,8 @@ __device__ __forceinline__ uint32_t flt_digit(uint64_t sc, uint32_t mb) {
 // scores) are sorted one by one by the stable LSD over the bits that vary
 // inside them (mostly the id bits).
 __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
-                                           const Cost& c) {
+                                           const Cost& c, unsigned long long* tr) {
+#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     if (n <= 1) return;
     // score range of the part -> mantissa bits mb so that the digit span fits 14 bits
@@ -226,6 +227,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
     }
     uint32_t mb = kSubBits;
     while (mb > 0 && flt_digit(smax, mb) - flt_digit(smin, mb) >= (uint32_t)kSubBuckets) mb--;
+    LTRACE(0);
     const uint32_t dlo = flt_digit(smin, mb);
 #define DIGIT(k) (flt_digit(((k) >> c.IB) & c.score_max, mb) - dlo)
     for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.pos[i] = 0;
@@ -265,11 +267,13 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
         for (uint32_t r = 0; r < wc; r += 32) sm.pos[j0 + r + lane] += off;
     }
     __syncthreads();
+    LTRACE(1);
     for (uint32_t i = tid; i < n; i += kFT) {
         const uint64_t k = A[i];
         Bf[atomicAdd(&sm.pos[DIGIT(k)], 1u)] = k;
     }
     __syncthreads();
+    LTRACE(2);
     // pos[d] is now the end of group d, its start the end of group d-1
     for (uint32_t i = tid; i < n; i += kFT) {
         const uint64_t k = Bf[i];
@@ -289,7 +293,9 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
     }
 #undef DIGIT
     __syncthreads();
+    LTRACE(3);
     const uint32_t nbig = min(sm.nbig, (uint32_t)kMaxBig);
+    if (tr && tid == 0) tr[5] = nbig;
     for (uint32_t t = 0; t < nbig; t++) {
         const uint32_t s0 = sm.big_lo[t], m = sm.big_n[t];
         unsigned long long o, an;
@@ -299,6 +305,8 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
         __syncthreads();
     }
+    LTRACE(4);
+#undef LTRACE
 }
 
 #define TRACE(k)                                                                         \
@@ -575,8 +583,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             (void)block_excl_scan_u32<kFT>(ns, sm.l.w32, &tot);
             ns = tot;
         }
-        local_sort(sm.l, sm.l.a, sm.l.b, ns, c);
-        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, c);
+        unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
+        local_sort(sm.l, sm.l.a, sm.l.b, ns, c, tr ? tr + 16 : nullptr);
+        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, c, tr ? tr + 24 : nullptr);
         TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;

@@ -19,7 +19,7 @@ constexpr int kAdmitThreads = 1024; // K3 (single CTA)
 constexpr int kMaxBatch = 16384;
 constexpr int kFusedKcap = 10240;    // keys per SM kept in shared memory by the fused step kernel
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 32;
 constexpr uint32_t kBarPerStep = 64;  // grid-barrier values reserved per step
 
 // Device control block: per-step counters, the sort plan and the step summary.
