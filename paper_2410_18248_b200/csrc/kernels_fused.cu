@@ -48,7 +48,7 @@ constexpr int kSubBits = 14;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
 constexpr uint32_t kMaxRankM = 64;          // largest sub-bucket ranked by comparison
 constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
-constexpr int kMaxBig = kKcap / (kMaxRankM + 1) + 1;  // sub-buckets > kMaxRankM in one range
+constexpr int kMaxBig = 48;                 // big groups handled by the second MSD level (else full LSD)
 struct PhaseL {                  // L
     uint64_t a[kKcap];           // 96 KB
     uint64_t b[kKcap];           // 96 KB
@@ -63,19 +63,19 @@ struct PhaseL {                  // L
             uint32_t pos[kSubBuckets];   // 64 KB: counts -> starts -> ends
             uint32_t w32[kFW];
             uint32_t nbig;
-            unsigned long long mm[2][kFW];
         };
     };
-    union {                              // big sub-buckets awaiting the segment LSD
-        struct { uint32_t big_lo[kMaxBig], big_n[kMaxBig]; };
-    };
+    // big groups of the first MSD level: start, size, second-level shift/bits/counter base
+    uint32_t big_lo[kMaxBig], big_n[kMaxBig], big_sh[kMaxBig], big_db[kMaxBig], big_base[kMaxBig], big_cum[kMaxBig];
+    uint32_t n3;                                  // groups left for the segment LSD
+    uint32_t g3_lo[kMaxBig], g3_n[kMaxBig];
     unsigned long long red[2][kFW];
+    AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
 };
 union FusedSmem {
     PhaseS s;
     PhaseL l;
     SortSmem g;
-    AdmitSmem adm;
 };
 
 __device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint32_t half) {
@@ -217,13 +217,13 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
         smin = x < smin ? x : smin;
         smax = y > smax ? y : smax;
     }
-    if (lane == 0) { sm.mm[0][warp] = smin; sm.mm[1][warp] = smax; }
+    if (lane == 0) { sm.red[0][warp] = smin; sm.red[1][warp] = smax; }
     if (tid == 0) sm.nbig = 0;
     __syncthreads();
     smin = ~0ull; smax = 0;
     for (int w = 0; w < kFW; w++) {
-        smin = sm.mm[0][w] < smin ? sm.mm[0][w] : smin;
-        smax = sm.mm[1][w] > smax ? sm.mm[1][w] : smax;
+        smin = sm.red[0][w] < smin ? sm.red[0][w] : smin;
+        smax = sm.red[1][w] > smax ? sm.red[1][w] : smax;
     }
     uint32_t mb = kSubBits;
     while (mb > 0 && flt_digit(smax, mb) - flt_digit(smin, mb) >= (uint32_t)kSubBuckets) mb--;
@@ -294,16 +294,156 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
 #undef DIGIT
     __syncthreads();
     LTRACE(3);
-    const uint32_t nbig = min(sm.nbig, (uint32_t)kMaxBig);
+    const uint32_t nbig = sm.nbig;
     if (tr && tid == 0) tr[5] = nbig;
-    for (uint32_t t = 0; t < nbig; t++) {
-        const uint32_t s0 = sm.big_lo[t], m = sm.big_n[t];
+    if (nbig > (uint32_t)kMaxBig) {  // pathological: too many big groups -> stable LSD of the whole part
         unsigned long long o, an;
-        block_or_and(sm, A + s0, m, o, an);
-        const uint64_t* r = local_lsd(sm, A + s0, Bf + s0, m, o ^ an);
-        if (r != A + s0)
-            for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
+        block_or_and(sm, A, n, o, an);
+        const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
+        if (r != A)
+            for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
         __syncthreads();
+    } else if (nbig) {
+        // ---- second MSD level for the big groups, all at once: per group the
+        // top db varying bits of its keys (db ~ log2(size) + 1) index a counter
+        // block of its own; one scan over all blocks gives positions.
+        if (tid == 0) sm.n3 = 0;
+        for (uint32_t g = warp; g < nbig; g += kFW) {
+            const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g];
+            unsigned long long o = 0, an = ~0ull;
+            for (uint32_t i = lane; i < m; i += 32) { o |= A[s0 + i]; an &= A[s0 + i]; }
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                o |= __shfl_xor_sync(0xffffffffu, o, sh);
+                an &= __shfl_xor_sync(0xffffffffu, an, sh);
+            }
+            if (lane == 0) {
+                const unsigned long long v = o ^ an;  // non-zero: keys are unique and m > 1
+                const int h = 63 - __clzll((long long)v);
+                uint32_t db = 33u - (uint32_t)__clz(m);  // ceil(log2(m)) + 1
+                db = db > (uint32_t)kSubBits ? (uint32_t)kSubBits : db;
+                sm.big_sh[g] = h + 1 >= (int)db ? (uint32_t)(h + 1 - (int)db) : 0u;
+                sm.big_db[g] = db;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {  // counter-block bases and key offsets, group order
+            uint32_t base = 0, cum = 0;
+            for (uint32_t g0 = 0; g0 < nbig; g0 += 32) {
+                const uint32_t g = g0 + lane;
+                const uint32_t sz = g < nbig ? (1u << sm.big_db[g]) : 0u, mm = g < nbig ? sm.big_n[g] : 0u;
+                uint32_t xs = sz, xm = mm;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ym = __shfl_up_sync(0xffffffffu, xm, o);
+                    if (lane >= (uint32_t)o) { xs += ys; xm += ym; }
+                }
+                if (g < nbig) { sm.big_base[g] = base + xs - sz; sm.big_cum[g] = cum + xm - mm; }
+                base += __shfl_sync(0xffffffffu, xs, 31);
+                cum += __shfl_sync(0xffffffffu, xm, 31);
+            }
+        }
+        __syncthreads();
+        const uint32_t last = nbig - 1;
+        const uint32_t ncnt = sm.big_base[last] + (1u << sm.big_db[last]);
+        if (ncnt <= (uint32_t)kSubBuckets) {
+            for (uint32_t i = tid; i < ncnt; i += kFT) sm.pos[i] = 0;
+            __syncthreads();
+            for (uint32_t g = warp; g < nbig; g += kFW) {
+                const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
+                const uint32_t bs = sm.big_base[g];
+                for (uint32_t i = lane; i < m; i += 32) atomicAdd(&sm.pos[bs + ((uint32_t)(A[s0 + i] >> sh) & dm)], 1u);
+            }
+            __syncthreads();
+            {   // exclusive scan of pos[0..ncnt): warp w owns a contiguous chunk, lane-strided
+                const uint32_t wc = ((ncnt + kFW * 32 - 1) / (kFW * 32)) * 32;
+                const uint32_t j0 = warp * wc;
+                uint32_t carry = 0;
+                for (uint32_t r = 0; r < wc; r += 32) {
+                    const uint32_t j = j0 + r + lane;
+                    const uint32_t v = j < ncnt ? sm.pos[j] : 0u;
+                    uint32_t x = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= (uint32_t)o) x += y;
+                    }
+                    if (j < ncnt) sm.pos[j] = carry + x - v;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) sm.w32[warp] = carry;
+                __syncthreads();
+                if (warp == 0) {
+                    const uint32_t v = sm.w32[lane];
+                    uint32_t x = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= (uint32_t)o) x += y;
+                    }
+                    sm.w32[lane] = x - v;
+                }
+                __syncthreads();
+                const uint32_t off = sm.w32[warp];
+                for (uint32_t r = 0; r < wc; r += 32) {
+                    const uint32_t j = j0 + r + lane;
+                    if (j < ncnt) sm.pos[j] += off;
+                }
+            }
+            __syncthreads();
+            for (uint32_t g = warp; g < nbig; g += kFW) {  // scatter into Bf, group-relative
+                const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
+                const uint32_t bs = sm.big_base[g], cum = sm.big_cum[g];
+                for (uint32_t i = lane; i < m; i += 32) {
+                    const uint64_t k = A[s0 + i];
+                    Bf[s0 + atomicAdd(&sm.pos[bs + ((uint32_t)(k >> sh) & dm)], 1u) - cum] = k;
+                }
+            }
+            __syncthreads();
+            for (uint32_t g = warp; g < nbig; g += kFW) {  // rank inside the second-level groups
+                const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
+                const uint32_t bs = sm.big_base[g], cum = sm.big_cum[g];
+                for (uint32_t i = lane; i < m; i += 32) {
+                    const uint64_t k = Bf[s0 + i];
+                    const uint32_t d = (uint32_t)(k >> sh) & dm;
+                    const uint32_t e = sm.pos[bs + d] - cum, st = (d ? sm.pos[bs + d - 1] : cum) - cum, m2 = e - st;
+                    if (m2 > kMaxRankM) {
+                        A[s0 + i] = k;
+                        if (i == st) {
+                            const uint32_t t = atomicAdd(&sm.n3, 1u);
+                            if (t < (uint32_t)kMaxBig) { sm.g3_lo[t] = s0 + st; sm.g3_n[t] = m2; }
+                        }
+                        continue;
+                    }
+                    uint32_t r = 0;
+                    for (uint32_t q = st; q < e; q++) r += Bf[s0 + q] < k ? 1u : 0u;
+                    A[s0 + st + r] = k;
+                }
+            }
+            __syncthreads();
+        } else {  // too many counters: every big group goes to the segment LSD
+            if (tid < nbig) { sm.g3_lo[tid] = sm.big_lo[tid]; sm.g3_n[tid] = sm.big_n[tid]; }
+            if (tid == 0) sm.n3 = nbig;
+            __syncthreads();
+        }
+        const uint32_t n3 = sm.n3;
+        if (n3 > (uint32_t)kMaxBig) {  // pathological: stable LSD of the whole part
+            unsigned long long o, an;
+            block_or_and(sm, A, n, o, an);
+            const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
+            if (r != A)
+                for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
+            __syncthreads();
+        }
+        for (uint32_t t = 0; t < (n3 > (uint32_t)kMaxBig ? 0u : n3); t++) {
+            const uint32_t s0 = sm.g3_lo[t], m = sm.g3_n[t];
+            unsigned long long o, an;
+            block_or_and(sm, A + s0, m, o, an);
+            const uint64_t* r = local_lsd(sm, A + s0, Bf + s0, m, o ^ an);
+            if (r != A + s0)
+                for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
+            __syncthreads();
+        }
     }
     LTRACE(4);
 #undef LTRACE
@@ -549,7 +689,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // bucket with start >= q_r by binary search; the largest range decides the fallback
     uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now
     if (tid <= G) {
-        const uint32_t q = (tid * n) / G;  // < 2^32: n <= 2^23, G <= 256
+        // CTA 0 sorts only the head (about 2 * max_batch keys) so it can start the
+        // admission early; the other CTAs share the rest evenly
+        const uint32_t head = min(n, max(2u * a.max_batch, n / (4u * G)));
+        const uint32_t q = tid == 0 ? 0u : head + (uint32_t)(((uint64_t)(tid - 1) * (n - head)) / (G - 1 ? G - 1 : 1));
         uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
@@ -607,7 +750,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     {
         unsigned long long v = tid < G ? __ldcg(&b.pin_part[tid]) : 0ull;
         unsigned long long tot;
-        (void)block_excl_scan_u64<kFT>(v, sm.adm.w64, &tot);
+        (void)block_excl_scan_u64<kFT>(v, sm.l.adm.w64, &tot);
         pinned_all = tot;
     }
     if (tid == 0) {
@@ -616,7 +759,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         ctl->fallbacks += fallback ? 1u : 0u;
     }
     TRACE(15);
-    admit_cta(b, c, a, b.keys[final_buf], n, pinned_all, sm.adm);
+    // the head of the order is still in shared memory unless the fallback ran
+    admit_cta(b, c, a, fallback ? b.keys[final_buf] : sm.l.a, n, pinned_all, sm.l.adm);
     TRACE(9);
 }
 
