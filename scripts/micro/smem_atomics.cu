@@ -5,18 +5,18 @@
 #include <cstdint>
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k(uint32_t* out, int iters, uint32_t seed) {
-    __shared__ uint32_t cnt[16384];
-    for (int i = threadIdx.x; i < 16384; i += 1024) cnt[i] = 0;
+    __shared__ uint32_t cnt[8192];
+    for (int i = threadIdx.x; i < 8192; i += 1024) cnt[i] = 0;
     __syncthreads();
     uint32_t x = seed ^ (threadIdx.x * 2654435761u) ^ (blockIdx.x * 97u);
     uint32_t acc = 0;
     for (int i = 0; i < iters; i++) {
         x = x * 1664525u + 1013904223u;
-        uint32_t d = x >> 18;
+        uint32_t d = x >> 19;
         if (MODE == 0) acc += atomicAdd(&cnt[d], 1u);
         else if (MODE == 1) atomicAdd(&cnt[d], 1u);
-        else if (MODE == 2) { acc += cnt[(threadIdx.x + i * 32) & 16383]; }
-        else { cnt[(threadIdx.x * 16 + i) & 16383] += 1; }  // private column RMW (conflict-prone layout)
+        else if (MODE == 2) { acc += cnt[(threadIdx.x + i * 32) & 8191]; }
+        else { cnt[(threadIdx.x * 16 + i) & 8191] += 1; }  // private column RMW (conflict-prone layout)
     }
     __syncthreads();
     out[blockIdx.x * 1024 + threadIdx.x] = acc + cnt[threadIdx.x];
