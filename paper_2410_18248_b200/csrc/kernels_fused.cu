@@ -232,8 +232,10 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
 #define DIGIT(k) (flt_digit(((k) >> c.IB) & c.score_max, mb) - dlo)
     for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.pos[i] = 0;
     __syncthreads();
+    LTRACE(6);
     for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.pos[DIGIT(A[i])], 1u);
     __syncthreads();
+    LTRACE(7);
     {   // counts -> exclusive starts; warp w owns a contiguous chunk, lane-strided (no bank conflicts)
         constexpr uint32_t wc = kSubBuckets / kFW;  // 512
         const uint32_t j0 = warp * wc;

@@ -49,6 +49,10 @@ if os.environ.get("TRACE"):
                            ("scatter", base + 1, base + 2), ("rank", base + 2, base + 3), ("big LSD", base + 3, base + 4)):
             d = (t[:, :, a1] - t[:, :, a0]) / 1.965e3
             print(f"  L.{part}.{nm:11s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
+        if base == 24:
+            for nm, a0, a1 in (("zero", 24, 30), ("count", 30, 31), ("scan", 31, 25)):
+                d = (t[:, :, a1] - t[:, :, a0]) / 1.965e3
+                print(f"  L.{part}.{nm:11s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
         nb = t[:, :, base + 5]
         print(f"  L.{part}.nbig       max {int(nb.max())} mean {nb.mean():.2f}")
     ms, nst = st.timing() if False else (None, None)
