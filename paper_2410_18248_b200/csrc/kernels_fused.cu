@@ -40,7 +40,7 @@ struct PhaseS {                  // S, H, T, X
     uint64_t kbuf[kKcap];        // 96 KB: this CTA's keys
     uint32_t cnt[kMaxBuckets];   // 58 KB: bucket counts -> scatter cursors
     uint32_t start[kMaxBuckets]; // 58 KB: bucket totals -> bucket start positions
-    uint32_t w32[kFW];
+    uint32_t w32[kFW + 1];
     unsigned long long red[3][kFW];
     uint32_t nk, base;
 };
@@ -61,7 +61,7 @@ struct PhaseL {                  // L
         };
         struct {                         // local MSD + rank
             uint32_t pos[kSubBuckets];   // 64 KB: counts -> starts -> ends
-            uint32_t w32[kFW];
+            uint32_t w32[kFW + 1];
             uint32_t nbig;
         };
     };
@@ -236,39 +236,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
     for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.pos[DIGIT(A[i])], 1u);
     __syncthreads();
     LTRACE(7);
-    {   // counts -> exclusive starts; warp w owns a contiguous chunk, lane-strided (no bank conflicts)
-        constexpr uint32_t wc = kSubBuckets / kFW;  // 512
-        const uint32_t j0 = warp * wc;
-        uint32_t carry = 0;
-        for (uint32_t r = 0; r < wc; r += 32) {
-            const uint32_t j = j0 + r + lane;
-            const uint32_t v = sm.pos[j];
-            uint32_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            sm.pos[j] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (lane == 0) sm.w32[warp] = carry;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = sm.w32[lane];
-            uint32_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            sm.w32[lane] = x - v;
-        }
-        __syncthreads();
-        const uint32_t off = sm.w32[warp];
-        for (uint32_t r = 0; r < wc; r += 32) sm.pos[j0 + r + lane] += off;
-    }
-    __syncthreads();
+    (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, kSubBuckets, sm.w32);
     LTRACE(1);
     for (uint32_t i = tid; i < n; i += kFT) {
         const uint64_t k = A[i];
@@ -290,6 +258,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             continue;
         }
         uint32_t r = 0;
+#pragma unroll 8
         for (uint32_t q = s0; q < e; q++) r += Bf[q] < k ? 1u : 0u;
         A[s0 + r] = k;
     }
@@ -357,42 +326,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
                 for (uint32_t i = lane; i < m; i += 32) atomicAdd(&sm.pos[bs + ((uint32_t)(A[s0 + i] >> sh) & dm)], 1u);
             }
             __syncthreads();
-            {   // exclusive scan of pos[0..ncnt): warp w owns a contiguous chunk, lane-strided
-                const uint32_t wc = ((ncnt + kFW * 32 - 1) / (kFW * 32)) * 32;
-                const uint32_t j0 = warp * wc;
-                uint32_t carry = 0;
-                for (uint32_t r = 0; r < wc; r += 32) {
-                    const uint32_t j = j0 + r + lane;
-                    const uint32_t v = j < ncnt ? sm.pos[j] : 0u;
-                    uint32_t x = v;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= (uint32_t)o) x += y;
-                    }
-                    if (j < ncnt) sm.pos[j] = carry + x - v;
-                    carry += __shfl_sync(0xffffffffu, x, 31);
-                }
-                if (lane == 0) sm.w32[warp] = carry;
-                __syncthreads();
-                if (warp == 0) {
-                    const uint32_t v = sm.w32[lane];
-                    uint32_t x = v;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= (uint32_t)o) x += y;
-                    }
-                    sm.w32[lane] = x - v;
-                }
-                __syncthreads();
-                const uint32_t off = sm.w32[warp];
-                for (uint32_t r = 0; r < wc; r += 32) {
-                    const uint32_t j = j0 + r + lane;
-                    if (j < ncnt) sm.pos[j] += off;
-                }
-            }
-            __syncthreads();
+            (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, ncnt, sm.w32);
             for (uint32_t g = warp; g < nbig; g += kFW) {  // scatter into Bf, group-relative
                 const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
                 const uint32_t bs = sm.big_base[g], cum = sm.big_cum[g];
@@ -418,6 +352,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
                         continue;
                     }
                     uint32_t r = 0;
+#pragma unroll 8
                     for (uint32_t q = st; q < e; q++) r += Bf[s0 + q] < k ? 1u : 0u;
                     A[s0 + st + r] = k;
                 }
@@ -595,19 +530,29 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             }
         }
         __syncthreads();
-        for (uint32_t j = warp; j < w; j += kFW) {  // one warp per column, lanes over CTAs
-            uint32_t carry = 0;
-            for (uint32_t r0 = 0; r0 < G; r0 += 32) {
-                const uint32_t r = r0 + lane;
-                const uint32_t v = r < G ? tile[r * w + j] : 0u;
-                uint32_t x = v;
+        for (uint32_t j = warp; j < w; j += kFW) {  // one warp per column, lanes over CTAs (ILP over rows)
+            uint32_t v[kTRows], x[kTRows];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= (uint32_t)o) x += y;
+            for (int i = 0; i < kTRows; i++) {
+                const uint32_t r = 32u * i + lane;
+                v[i] = r < G ? tile[r * w + j] : 0u;
+                x[i] = v[i];
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int i = 0; i < kTRows; i++) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x[i], o);
+                    if (lane >= (uint32_t)o) x[i] += y;
                 }
-                if (r < G) tile[r * w + j] = carry + x - v;
-                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            uint32_t carry = 0;
+#pragma unroll
+            for (int i = 0; i < kTRows; i++) {
+                const uint32_t r = 32u * i + lane;
+                const uint32_t t = __shfl_sync(0xffffffffu, x[i], 31);
+                if (r < G) tile[r * w + j] = carry + x[i] - v[i];
+                carry += t;
             }
             if (lane == 0) T[jb0 + j] = carry;
         }
@@ -637,45 +582,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     }
     __syncthreads();
     TRACE(10);
-    {   // exclusive scan of the totals; warp w owns a contiguous chunk, lane-strided (no bank conflicts)
-        const uint32_t wc = ((NB + kFW * 32 - 1) / (kFW * 32)) * 32;
-        const uint32_t j0 = warp * wc;
-        uint32_t carry = 0;
-        for (uint32_t r = 0; r < wc; r += 32) {
-            const uint32_t j = j0 + r + lane;
-            const uint32_t v = j < NB ? sm.s.start[j] : 0u;
-            uint32_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            if (j < NB) sm.s.start[j] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (lane == 0) sm.s.w32[warp] = carry;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = sm.s.w32[lane];
-            uint32_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            sm.s.w32[lane] = x - v;
-            if (lane == 31) sm.s.base = x;  // total number of keys
-        }
-        __syncthreads();
-        const uint32_t off = sm.s.w32[warp];
-        for (uint32_t r = 0; r < wc; r += 32) {
-            const uint32_t j = j0 + r + lane;
-            if (j < NB) {
-                const uint32_t st = sm.s.start[j] + off;
-                sm.s.start[j] = st;
-                sm.s.cnt[j] += st;  // scatter cursor
-            }
-        }
+    // bucket starts = exclusive scan of the totals; scatter cursors = starts + this CTA's prefix
+    {
+        const uint32_t tot = smem_excl_scan<kFT, (kMaxBuckets + kFT - 1) / kFT>(sm.s.start, NB, sm.s.w32, sm.s.cnt);
+        if (tid == 0) sm.s.base = tot;  // total number of keys
     }
     __syncthreads();
     TRACE(11);
