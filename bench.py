@@ -224,6 +224,7 @@ def run_ours(args, rank, world, local):
     res = s.result()
     n_elig = res["n_eligible"]
     kernels, passes = s.stats()
+    fused = kernels == 1
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     ne_t = torch.tensor([float(n_elig)], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -232,20 +233,34 @@ def run_ours(args, rank, world, local):
     ms_max, ne_sum = float(ms_t.item()), float(ne_t.item())
     value = ne_sum / (ms_max / 1e3)
 
-    # ---- per-kernel breakdown (separate handle with CUDA events between kernels)
-    sp = Scheduler(cfg, flags=LAMPS_TIMING, stream=stream)
+    # ---- per-kernel breakdown (separate handle with CUDA events between kernels, plus
+    # the fused kernel's per-phase SM-clock trace)
+    from paper_2410_18248_b200 import LAMPS_TRACE
+    sp = Scheduler(cfg, flags=LAMPS_TIMING | LAMPS_TRACE, stream=stream)
     sp.import_pool(snap, snap["id_base"], snap["next_id"])
     for _ in range(args.warmup):
         flush.zero_()
         sp.step_async(kv)
     sp.timing()
+    traces = []
     for _ in range(args.steps):
         flush.zero_()
         sp.step_async(kv)
+        if fused and len(traces) < 10:
+            traces.append(sp.trace().astype(np.int64))
     phase_ms, nst = sp.timing()
-    _, sp_passes = sp.stats()
+    sp_kernels, sp_passes = sp.stats()
     sp.close()
-    phase = [x / nst for x in phase_ms]  # ms per step per phase
+    phase = [x / nst for x in phase_ms]  # ms per step: [events, score or fused, sort, admit]
+    trace_us = None
+    if fused and traces:
+        t = np.stack(traces)
+        segs = [("score", 0, 1), ("publish", 1, 2), ("barrier1", 2, 3), ("count_exchange", 3, 4),
+                ("barrier2", 4, 5), ("bucket_scatter", 5, 6), ("barrier3", 6, 7), ("range_sort", 7, 8)]
+        mhz = float(clk.summary().get("sm_mhz") or 1965.0)
+        trace_us = {nm: round(float(np.median((t[:, :, b1] - t[:, :, a1]).max(axis=1))) / mhz, 2)
+                    for nm, a1, b1 in segs}
+        trace_us["admission_cta0"] = round(float(np.median(t[:, 0, 9] - t[:, 0, 8])) / mhz, 2)
 
     # ---- end to end through the public API (host events in, host result out)
     e2e_steps = args.e2e_steps or args.steps
@@ -293,18 +308,24 @@ def run_ours(args, rank, world, local):
 
     if rank == 0:
         peak, peak_src = measured_peak_hbm()
-        # algorithmic bytes: K1 reads 28 B/slot of SoA, writes 4 B/slot
-        # state and 8 B/eligible key; the sort reads + writes 8 B/key per radix pass
-        k1_bytes = 32 * cap + 8 * n_elig
-        sort_bytes = 16 * n_elig * sp_passes
-        kernels_tbl = {
-            "k1_score": {"ms": phase[1], "bytes": k1_bytes, "GBps": k1_bytes / (phase[1] * 1e6)},
-            "k2_sort": {"ms": phase[2], "passes": sp_passes, "bytes": sort_bytes,
-                        "GBps": sort_bytes / (phase[2] * 1e6) if phase[2] else None,
-                        "keys_per_s": n_elig / (phase[2] * 1e-3) if phase[2] else None},
-            "k0_events": {"ms": phase[0]}, "k3_admit": {"ms": phase[3]},
-        }
-        dom = "k2_sort" if phase[2] >= phase[1] else "k1_score"
+        # algorithmic bytes of one step: the SoA is read once (28 B/slot),
+        # the state word written once (4 B/slot), and the keys written and read once (16 B/key)
+        step_bytes = 32 * cap + 16 * n_elig
+        if fused:
+            dom = "k_fused"
+            kernels_tbl = {"k_fused": {"ms": phase[1], "bytes": step_bytes, "GBps": step_bytes / (phase[1] * 1e6),
+                                       "phase_us": trace_us},
+                           "k0_events": {"ms": phase[0], "launched": False}}
+        else:
+            k1_bytes = 32 * cap + 8 * n_elig
+            sort_bytes = 16 * n_elig * sp_passes
+            kernels_tbl = {
+                "k1_score": {"ms": phase[1], "bytes": k1_bytes, "GBps": k1_bytes / (phase[1] * 1e6)},
+                "k2_sort": {"ms": phase[2], "passes": sp_passes, "bytes": sort_bytes,
+                            "GBps": sort_bytes / (phase[2] * 1e6) if phase[2] else None},
+                "k3_admit": {"ms": phase[3]}, "k0_events": {"ms": phase[0]},
+            }
+            dom = "k2_sort" if phase[2] >= phase[1] else "k1_score"
         ach = kernels_tbl[dom]["GBps"]
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -319,7 +340,7 @@ def run_ours(args, rank, world, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
             "config": {"workload": f"{cname}: 1M-request pool (2^20 slots), GPT-J profile, "
-                                   f"{n_elig} READY per shard", "slots_per_gpu": cap,
+                                   f"{n_elig} READY per shard", "slots_per_gpu": cap, "eligible_per_gpu": n_elig,
                        "kv_total_blocks": kv, "max_batch": cfg["max_batch"],
                        "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
                        "l2": "flushed before every timed step (256 MiB write)",
@@ -328,8 +349,7 @@ def run_ours(args, rank, world, local):
                          "frac": ach / peak if ach else None, "traffic": traffic,
                          "peak_source": peak_src},
             "kernels": kernels_tbl,
-            "phase_ms_per_step": {"k0_events": phase[0], "k1_score": phase[1], "k2_sort": phase[2],
-                                  "k3_admit": phase[3]},
+            "path": "fused cooperative step kernel" if fused else "3-kernel path",
             "sort_passes": passes,
             "gpu_launches": kernels * args.steps,
             "clocks": clk.summary(),
