@@ -44,11 +44,11 @@ struct PhaseS {                  // S, H, T, X
     unsigned long long red[3][kFW];
     uint32_t nk, base;
 };
-constexpr int kSubBits = 14;                // local MSD digit
+constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
-constexpr uint32_t kMaxRankM = 64;          // largest sub-bucket ranked by comparison
+constexpr uint32_t kMaxRankM = 16;          // largest group ranked by comparison
 constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
-constexpr int kMaxBig = 48;                 // big groups handled by the second MSD level (else full LSD)
+constexpr int kMaxBig = 1024;               // big groups handled by the second MSD level (else full LSD)
 struct PhaseL {                  // L
     uint64_t a[kKcap];           // 96 KB
     uint64_t b[kKcap];           // 96 KB
@@ -60,15 +60,18 @@ struct PhaseL {                  // L
             uint32_t scan[kFW];
         };
         struct {                         // local MSD + rank
-            uint32_t pos[kSubBuckets];   // 64 KB: counts -> starts -> ends
+            uint32_t pos[kSubBuckets];   // 32 KB: counts -> starts -> ends
             uint32_t w32[kFW + 1];
             uint32_t nbig;
         };
     };
-    // big groups of the first MSD level: start, size, second-level shift/bits/counter base
-    uint32_t big_lo[kMaxBig], big_n[kMaxBig], big_sh[kMaxBig], big_db[kMaxBig], big_base[kMaxBig], big_cum[kMaxBig];
+    // big groups of the first MSD level: start, size, key offset (prefix of sizes),
+    // second-level shift / digit bits / counter base; OR / AND of their keys
+    uint16_t big_lo[kMaxBig], big_n[kMaxBig], big_cum[kMaxBig], big_base[kMaxBig];
+    uint8_t big_sh[kMaxBig], big_db[kMaxBig];
+    unsigned long long big_or[kMaxBig / 4], big_and[kMaxBig / 4];  // first kMaxBig/4 groups of a batch
     uint32_t n3;                                  // groups left for the segment LSD
-    uint32_t g3_lo[kMaxBig], g3_n[kMaxBig];
+    uint16_t g3_lo[kMaxBig], g3_n[kMaxBig];
     unsigned long long red[2][kFW];
     AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
 };
@@ -253,7 +256,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             A[i] = k;  // sorted below
             if (i == s0) {
                 const uint32_t t = atomicAdd(&sm.nbig, 1u);
-                if (t < (uint32_t)kMaxBig) { sm.big_lo[t] = s0; sm.big_n[t] = m; }
+                if (t < (uint32_t)kMaxBig) { sm.big_lo[t] = (uint16_t)s0; sm.big_n[t] = (uint16_t)m; }
             }
             continue;
         }
@@ -275,111 +278,141 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
         __syncthreads();
     } else if (nbig) {
-        // ---- second MSD level for the big groups, all at once: per group the
-        // top db varying bits of its keys (db ~ log2(size) + 1) index a counter
-        // block of its own; one scan over all blocks gives positions.
+        // ---- second MSD level for the big groups, flat over all their keys: per group the
+        // top db varying bits of its keys (db = ceil(log2 size), <= 13) index a counter
+        // block of its own; one scan over a batch of blocks gives positions.
         if (tid == 0) sm.n3 = 0;
-        for (uint32_t g = warp; g < nbig; g += kFW) {
-            const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g];
-            unsigned long long o = 0, an = ~0ull;
-            for (uint32_t i = lane; i < m; i += 32) { o |= A[s0 + i]; an &= A[s0 + i]; }
-#pragma unroll
-            for (int sh = 16; sh; sh >>= 1) {
-                o |= __shfl_xor_sync(0xffffffffu, o, sh);
-                an &= __shfl_xor_sync(0xffffffffu, an, sh);
-            }
-            if (lane == 0) {
-                const unsigned long long v = o ^ an;  // non-zero: keys are unique and m > 1
-                const int h = 63 - __clzll((long long)v);
-                uint32_t db = 33u - (uint32_t)__clz(m);  // ceil(log2(m)) + 1
-                db = db > (uint32_t)kSubBits ? (uint32_t)kSubBits : db;
-                sm.big_sh[g] = h + 1 >= (int)db ? (uint32_t)(h + 1 - (int)db) : 0u;
-                sm.big_db[g] = db;
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {  // counter-block bases and key offsets, group order
-            uint32_t base = 0, cum = 0;
+        if (warp == 0) {  // key offsets: exclusive prefix of the group sizes
+            uint32_t cum = 0;
             for (uint32_t g0 = 0; g0 < nbig; g0 += 32) {
-                const uint32_t g = g0 + lane;
-                const uint32_t sz = g < nbig ? (1u << sm.big_db[g]) : 0u, mm = g < nbig ? sm.big_n[g] : 0u;
-                uint32_t xs = sz, xm = mm;
+                const uint32_t g = g0 + lane, mm = g < nbig ? sm.big_n[g] : 0u;
+                uint32_t x = mm;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ym = __shfl_up_sync(0xffffffffu, xm, o);
-                    if (lane >= (uint32_t)o) { xs += ys; xm += ym; }
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
                 }
-                if (g < nbig) { sm.big_base[g] = base + xs - sz; sm.big_cum[g] = cum + xm - mm; }
-                base += __shfl_sync(0xffffffffu, xs, 31);
-                cum += __shfl_sync(0xffffffffu, xm, 31);
+                if (g < nbig) sm.big_cum[g] = (uint16_t)(cum + x - mm);
+                cum += __shfl_sync(0xffffffffu, x, 31);
             }
+            if (lane == 0) sm.w32[kFW] = cum;
         }
         __syncthreads();
-        const uint32_t last = nbig - 1;
-        const uint32_t ncnt = sm.big_base[last] + (1u << sm.big_db[last]);
-        if (ncnt <= (uint32_t)kSubBuckets) {
+        const uint32_t K = sm.w32[kFW];
+        // flat key index f -> group g (binary search over the prefix of sizes) and position
+        auto group_of = [&](uint32_t f, uint32_t g0, uint32_t g1) {
+            uint32_t lo_ = g0, hi_ = g1;
+            while (hi_ - lo_ > 1) {
+                const uint32_t mid = (lo_ + hi_) >> 1;
+                if (sm.big_cum[mid] <= f) lo_ = mid; else hi_ = mid;
+            }
+            return lo_;
+        };
+        for (uint32_t gb = 0; gb < nbig;) {  // batches of groups whose masks / counters fit
+            const uint32_t ge = min(nbig, gb + (uint32_t)(kMaxBig / 4));
+            for (uint32_t g = gb + tid; g < ge; g += kFT) { sm.big_or[g - gb] = 0; sm.big_and[g - gb] = ~0ull; }
+            __syncthreads();
+            const uint32_t f0 = sm.big_cum[gb], f1 = ge < nbig ? (uint32_t)sm.big_cum[ge] : K;
+            for (uint32_t f = f0 + tid; f < f1; f += kFT) {
+                const uint32_t g = group_of(f, gb, ge);
+                const uint64_t k = A[sm.big_lo[g] + (f - sm.big_cum[g])];
+                atomicOr(&sm.big_or[g - gb], k);
+                atomicAnd(&sm.big_and[g - gb], k);
+            }
+            __syncthreads();
+            if (warp == 0) {  // shift, bits, counter bases; cut the batch where the counters end
+                uint32_t base = 0, cut = ge;
+                for (uint32_t g0 = gb; g0 < ge; g0 += 32) {
+                    const uint32_t g = g0 + lane;
+                    uint32_t sz = 0;
+                    if (g < ge) {
+                        const unsigned long long v = sm.big_or[g - gb] ^ sm.big_and[g - gb];  // m > 1, unique keys
+                        const int h = 63 - __clzll((long long)v);
+                        uint32_t db = 32u - (uint32_t)__clz((uint32_t)sm.big_n[g] - 1u);  // ceil(log2 m)
+                        db = db > (uint32_t)kSubBits ? (uint32_t)kSubBits : db;
+                        sm.big_sh[g] = (uint8_t)(h + 1 >= (int)db ? h + 1 - (int)db : 0);
+                        sm.big_db[g] = (uint8_t)db;
+                        sz = 1u << db;
+                    }
+                    uint32_t x = sz;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= (uint32_t)o) x += y;
+                    }
+                    if (g < ge) sm.big_base[g] = (uint16_t)min(base + x - sz, 65535u);
+                    const uint32_t ob = __ballot_sync(0xffffffffu, g < ge && base + x > (uint32_t)kSubBuckets);
+                    if (ob && cut == ge) cut = g0 + __ffs(ob) - 1;
+                    base += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) sm.w32[kFW - 1] = cut > gb ? cut : gb + 1;  // at least one group
+            }
+            __syncthreads();
+            const uint32_t gcut = sm.w32[kFW - 1];
+            const uint32_t fc = gcut < nbig ? (uint32_t)sm.big_cum[gcut] : K;
+            const uint32_t ncnt = min((uint32_t)kSubBuckets,
+                                      (uint32_t)sm.big_base[gcut - 1] + (1u << sm.big_db[gcut - 1]));
             for (uint32_t i = tid; i < ncnt; i += kFT) sm.pos[i] = 0;
             __syncthreads();
-            for (uint32_t g = warp; g < nbig; g += kFW) {
-                const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
-                const uint32_t bs = sm.big_base[g];
-                for (uint32_t i = lane; i < m; i += 32) atomicAdd(&sm.pos[bs + ((uint32_t)(A[s0 + i] >> sh) & dm)], 1u);
+            for (uint32_t f = f0 + tid; f < fc; f += kFT) {
+                const uint32_t g = group_of(f, gb, gcut);
+                const uint64_t k = A[sm.big_lo[g] + (f - sm.big_cum[g])];
+                atomicAdd(&sm.pos[sm.big_base[g] + ((uint32_t)(k >> sm.big_sh[g]) & ((1u << sm.big_db[g]) - 1u))], 1u);
             }
             __syncthreads();
             (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, ncnt, sm.w32);
-            for (uint32_t g = warp; g < nbig; g += kFW) {  // scatter into Bf, group-relative
-                const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
-                const uint32_t bs = sm.big_base[g], cum = sm.big_cum[g];
-                for (uint32_t i = lane; i < m; i += 32) {
-                    const uint64_t k = A[s0 + i];
-                    Bf[s0 + atomicAdd(&sm.pos[bs + ((uint32_t)(k >> sh) & dm)], 1u) - cum] = k;
-                }
+            // positions: group g's keys occupy [cum_g, cum_g + m_g) of the batch's scan space
+            for (uint32_t f = f0 + tid; f < fc; f += kFT) {
+                const uint32_t g = group_of(f, gb, gcut);
+                const uint32_t lo_g = sm.big_lo[g], cum_g = sm.big_cum[g];
+                const uint64_t k = A[lo_g + (f - cum_g)];
+                const uint32_t d = sm.big_base[g] + ((uint32_t)(k >> sm.big_sh[g]) & ((1u << sm.big_db[g]) - 1u));
+                Bf[lo_g + atomicAdd(&sm.pos[d], 1u) - (cum_g - f0)] = k;
             }
             __syncthreads();
-            for (uint32_t g = warp; g < nbig; g += kFW) {  // rank inside the second-level groups
-                const uint32_t s0 = sm.big_lo[g], m = sm.big_n[g], sh = sm.big_sh[g], dm = (1u << sm.big_db[g]) - 1u;
-                const uint32_t bs = sm.big_base[g], cum = sm.big_cum[g];
-                for (uint32_t i = lane; i < m; i += 32) {
-                    const uint64_t k = Bf[s0 + i];
-                    const uint32_t d = (uint32_t)(k >> sh) & dm;
-                    const uint32_t e = sm.pos[bs + d] - cum, st = (d ? sm.pos[bs + d - 1] : cum) - cum, m2 = e - st;
-                    if (m2 > kMaxRankM) {
-                        A[s0 + i] = k;
-                        if (i == st) {
-                            const uint32_t t = atomicAdd(&sm.n3, 1u);
-                            if (t < (uint32_t)kMaxBig) { sm.g3_lo[t] = s0 + st; sm.g3_n[t] = m2; }
-                        }
-                        continue;
+            for (uint32_t f = f0 + tid; f < fc; f += kFT) {  // rank inside the second-level groups
+                const uint32_t g = group_of(f, gb, gcut);
+                const uint32_t lo_g = sm.big_lo[g], cum_g = sm.big_cum[g], bs = sm.big_base[g];
+                const uint32_t i = f - cum_g;
+                const uint64_t k = Bf[lo_g + i];
+                const uint32_t d = (uint32_t)(k >> sm.big_sh[g]) & ((1u << sm.big_db[g]) - 1u);
+                // pos[] now holds ends in the batch scan space; group g starts at cum_g - f0 there
+                const uint32_t gz = cum_g - f0;
+                const uint32_t e = sm.pos[bs + d] - gz, st = (d ? sm.pos[bs + d - 1] - gz : 0u), m2 = e - st;
+                if (m2 > kMaxRankM) {
+                    A[lo_g + i] = k;
+                    if (i == st) {
+                        const uint32_t t = atomicAdd(&sm.n3, 1u);
+                        if (t < (uint32_t)kMaxBig) { sm.g3_lo[t] = (uint16_t)(lo_g + st); sm.g3_n[t] = (uint16_t)m2; }
                     }
-                    uint32_t r = 0;
-#pragma unroll 8
-                    for (uint32_t q = st; q < e; q++) r += Bf[s0 + q] < k ? 1u : 0u;
-                    A[s0 + st + r] = k;
+                    continue;
                 }
+                uint32_t r = 0;
+#pragma unroll 8
+                for (uint32_t q = st; q < e; q++) r += Bf[lo_g + q] < k ? 1u : 0u;
+                A[lo_g + st + r] = k;
             }
             __syncthreads();
-        } else {  // too many counters: every big group goes to the segment LSD
-            if (tid < nbig) { sm.g3_lo[tid] = sm.big_lo[tid]; sm.g3_n[tid] = sm.big_n[tid]; }
-            if (tid == 0) sm.n3 = nbig;
-            __syncthreads();
+            gb = gcut;
         }
         const uint32_t n3 = sm.n3;
-        if (n3 > (uint32_t)kMaxBig) {  // pathological: stable LSD of the whole part
+        if (n3 > 32u) {  // pathological: stable LSD of the whole part
             unsigned long long o, an;
             block_or_and(sm, A, n, o, an);
             const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
             if (r != A)
                 for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
             __syncthreads();
-        }
-        for (uint32_t t = 0; t < (n3 > (uint32_t)kMaxBig ? 0u : n3); t++) {
-            const uint32_t s0 = sm.g3_lo[t], m = sm.g3_n[t];
-            unsigned long long o, an;
-            block_or_and(sm, A + s0, m, o, an);
-            const uint64_t* r = local_lsd(sm, A + s0, Bf + s0, m, o ^ an);
-            if (r != A + s0)
-                for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
-            __syncthreads();
+        } else {
+            for (uint32_t t = 0; t < n3; t++) {
+                const uint32_t s0 = sm.g3_lo[t], m = sm.g3_n[t];
+                unsigned long long o, an;
+                block_or_and(sm, A + s0, m, o, an);
+                const uint64_t* r = local_lsd(sm, A + s0, Bf + s0, m, o ^ an);
+                if (r != A + s0)
+                    for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
+                __syncthreads();
+            }
         }
     }
     LTRACE(4);
