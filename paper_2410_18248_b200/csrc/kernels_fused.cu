@@ -48,7 +48,8 @@ constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
 constexpr uint32_t kMaxRankM = 16;          // largest group ranked by comparison
 constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
-constexpr int kMaxBig = 1024;               // big groups handled by the second MSD level (else full LSD)
+constexpr int kMaxBig = 1024;               // groups per refinement list (else full LSD)
+constexpr int kMaxLevels = 6;               // refinement passes before the LSD fallback
 struct PhaseL {                  // L
     uint64_t a[kKcap];           // 96 KB
     uint64_t b[kKcap];           // 96 KB
@@ -65,13 +66,13 @@ struct PhaseL {                  // L
             uint32_t nbig;
         };
     };
-    // big groups of the first MSD level: start, size, key offset (prefix of sizes),
-    // second-level shift / digit bits / counter base; OR / AND of their keys
-    uint16_t big_lo[kMaxBig], big_n[kMaxBig], big_cum[kMaxBig], big_base[kMaxBig];
-    uint8_t big_sh[kMaxBig], big_db[kMaxBig];
-    unsigned long long big_or[kMaxBig / 4], big_and[kMaxBig / 4];  // first kMaxBig/4 groups of a batch
-    uint32_t n3;                                  // groups left for the segment LSD
-    uint16_t g3_lo[kMaxBig], g3_n[kMaxBig];
+    // group refinement: lists of groups still to split (ping-pong), and per group of the
+    // current batch: key offset (prefix of sizes), digit shift / bits, counter base, OR / AND
+    uint16_t gl_lo[2][kMaxBig], gl_n[2][kMaxBig];
+    uint32_t ngl[2];
+    uint16_t gcum[kMaxBig], gbase[kMaxBig];
+    uint8_t gsh[kMaxBig], gdb[kMaxBig];
+    unsigned long long gor[kMaxBig / 4], gand[kMaxBig / 4];
     unsigned long long red[2][kFW];
     AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
 };
@@ -194,144 +195,118 @@ __device__ __forceinline__ uint32_t flt_digit(uint64_t sc, uint32_t mb) {
     return ((e - mb) << mb) + (uint32_t)((sc >> (e - 1 - mb)) & ((1u << mb) - 1u));
 }
 
-// Sort of the n keys at A[0..n) (same starving flag) in shared memory, result in
-// A (Bf is scratch).  One MSD step: count and scatter by a 14-bit float-like digit
-// of the score (relative to the smallest in the part, so heavy-tailed score
-// ranges still spread over the digit space); the order inside a group is then
-// fixed exactly: every key of a group of <= kMaxRankM keys counts the smaller
-// keys there (keys are unique).  Larger groups (many keys with (nearly) equal
-// scores) are sorted one by one by the stable LSD over the bits that vary
-// inside them (mostly the id bits).
+// Sort of the n keys at A[0..n) of one part of a range (same starving flag) in
+// shared memory; result in A, Bf is scratch.  The part arrives in global-bucket
+// order and its buckets [j0, j1) are known, so the buckets are the first-level
+// groups (sizes = the global totals T[j]; a bucket lies entirely in one range).
+// Groups of <= kMaxRankM keys are finished by rank-by-comparison (keys are
+// unique).  Bigger groups are refined in flat passes over all their keys: per
+// group a digit of its own top varying bits (db = ceil(log2 size) bits, from the
+// group's OR/AND), counted with shared-memory atomics into a counter block of
+// its own; one scan over the blocks of a batch gives positions; sub-groups
+// still bigger than kMaxRankM go to the next pass.  After kMaxLevels passes (or
+// if the group tables overflow) the stable LSD finishes the part.
 __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
-                                           const Cost& c, unsigned long long* tr) {
+                                           const uint32_t* T, uint32_t j0, uint32_t j1,
+                                           unsigned long long* tr) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     if (n <= 1) return;
-    // score range of the part -> mantissa bits mb so that the digit span fits 14 bits
-    unsigned long long smin = ~0ull, smax = 0;
-    for (uint32_t i = tid; i < n; i += kFT) {
-        const unsigned long long sc = (A[i] >> c.IB) & c.score_max;
-        smin = sc < smin ? sc : smin;
-        smax = sc > smax ? sc : smax;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long x = __shfl_xor_sync(0xffffffffu, smin, o), y = __shfl_xor_sync(0xffffffffu, smax, o);
-        smin = x < smin ? x : smin;
-        smax = y > smax ? y : smax;
-    }
-    if (lane == 0) { sm.red[0][warp] = smin; sm.red[1][warp] = smax; }
-    if (tid == 0) sm.nbig = 0;
-    __syncthreads();
-    smin = ~0ull; smax = 0;
-    for (int w = 0; w < kFW; w++) {
-        smin = sm.red[0][w] < smin ? sm.red[0][w] : smin;
-        smax = sm.red[1][w] > smax ? sm.red[1][w] : smax;
-    }
-    uint32_t mb = kSubBits;
-    while (mb > 0 && flt_digit(smax, mb) - flt_digit(smin, mb) >= (uint32_t)kSubBuckets) mb--;
     LTRACE(0);
-    const uint32_t dlo = flt_digit(smin, mb);
-#define DIGIT(k) (flt_digit(((k) >> c.IB) & c.score_max, mb) - dlo)
-    for (uint32_t i = tid; i < (uint32_t)kSubBuckets; i += kFT) sm.pos[i] = 0;
-    __syncthreads();
-    LTRACE(6);
-    for (uint32_t i = tid; i < n; i += kFT) atomicAdd(&sm.pos[DIGIT(A[i])], 1u);
-    __syncthreads();
-    LTRACE(7);
-    (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, kSubBuckets, sm.w32);
-    LTRACE(1);
-    for (uint32_t i = tid; i < n; i += kFT) {
-        const uint64_t k = A[i];
-        Bf[atomicAdd(&sm.pos[DIGIT(k)], 1u)] = k;
-    }
-    __syncthreads();
-    LTRACE(2);
-    // pos[d] is now the end of group d, its start the end of group d-1
-    for (uint32_t i = tid; i < n; i += kFT) {
-        const uint64_t k = Bf[i];
-        const uint32_t d = DIGIT(k);
-        const uint32_t e = sm.pos[d], s0 = d ? sm.pos[d - 1] : 0u, m = e - s0;
-        if (m > kMaxRankM) {
-            A[i] = k;  // sorted below
-            if (i == s0) {
-                const uint32_t t = atomicAdd(&sm.nbig, 1u);
-                if (t < (uint32_t)kMaxBig) { sm.big_lo[t] = (uint16_t)s0; sm.big_n[t] = (uint16_t)m; }
-            }
-            continue;
-        }
-        uint32_t r = 0;
-#pragma unroll 8
-        for (uint32_t q = s0; q < e; q++) r += Bf[q] < k ? 1u : 0u;
-        A[s0 + r] = k;
-    }
-#undef DIGIT
-    __syncthreads();
-    LTRACE(3);
-    const uint32_t nbig = sm.nbig;
-    if (tr && tid == 0) tr[5] = nbig;
-    if (nbig > (uint32_t)kMaxBig) {  // pathological: too many big groups -> stable LSD of the whole part
-        unsigned long long o, an;
-        block_or_and(sm, A, n, o, an);
-        const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
-        if (r != A)
-            for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
+    bool full_lsd = false;
+    // ---- level 1: bucket runs.  pos[0..nb] = starts of the part's buckets.
+    const uint32_t nb = j1 - j0;
+    if (nb + 1 > (uint32_t)kSubBuckets) {
+        full_lsd = true;
+    } else {
+        for (uint32_t j = tid; j < nb; j += kFT) sm.pos[j] = __ldcg(&T[j0 + j]);
+        if (tid == 0) { sm.ngl[0] = 0; sm.ngl[1] = 0; }
+        for (uint32_t i = tid; i < n; i += kFT) Bf[i] = A[i];
         __syncthreads();
-    } else if (nbig) {
-        // ---- second MSD level for the big groups, flat over all their keys: per group the
-        // top db varying bits of its keys (db = ceil(log2 size), <= 13) index a counter
-        // block of its own; one scan over a batch of blocks gives positions.
-        if (tid == 0) sm.n3 = 0;
+        (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, nb, sm.w32);
+        if (tid == 0) sm.pos[nb] = n;
+        __syncthreads();
+        LTRACE(1);
+        for (uint32_t i = tid; i < n; i += kFT) {
+            uint32_t lo_ = 0, hi_ = nb;  // last bucket with start <= i
+            while (hi_ - lo_ > 1) {
+                const uint32_t mid = (lo_ + hi_) >> 1;
+                if (sm.pos[mid] <= i) lo_ = mid; else hi_ = mid;
+            }
+            const uint32_t st = sm.pos[lo_], e = sm.pos[lo_ + 1], m = e - st;
+            const uint64_t k = Bf[i];
+            if (m > kMaxRankM) {
+                if (i == st) {
+                    const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
+                    if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m; }
+                }
+                continue;  // A[i] == k already
+            }
+            uint32_t r = 0;
+#pragma unroll 8
+            for (uint32_t q = st; q < e; q++) r += Bf[q] < k ? 1u : 0u;
+            A[st + r] = k;
+        }
+        __syncthreads();
+        LTRACE(2);
+    }
+    // ---- refinement passes over the big groups
+    uint32_t cur = 0;
+    for (int level = 0; !full_lsd && level < kMaxLevels; level++) {
+        const uint32_t ng = sm.ngl[cur];
+        if (ng == 0) break;
+        if (ng > (uint32_t)kMaxBig) { full_lsd = true; break; }
+        const uint32_t nxt = cur ^ 1u;
+        if (tid == 0) sm.ngl[nxt] = 0;
         if (warp == 0) {  // key offsets: exclusive prefix of the group sizes
             uint32_t cum = 0;
-            for (uint32_t g0 = 0; g0 < nbig; g0 += 32) {
-                const uint32_t g = g0 + lane, mm = g < nbig ? sm.big_n[g] : 0u;
+            for (uint32_t g0 = 0; g0 < ng; g0 += 32) {
+                const uint32_t g = g0 + lane, mm = g < ng ? sm.gl_n[cur][g] : 0u;
                 uint32_t x = mm;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                     if (lane >= (uint32_t)o) x += y;
                 }
-                if (g < nbig) sm.big_cum[g] = (uint16_t)(cum + x - mm);
+                if (g < ng) sm.gcum[g] = (uint16_t)(cum + x - mm);
                 cum += __shfl_sync(0xffffffffu, x, 31);
             }
             if (lane == 0) sm.w32[kFW] = cum;
         }
         __syncthreads();
         const uint32_t K = sm.w32[kFW];
-        // flat key index f -> group g (binary search over the prefix of sizes) and position
         auto group_of = [&](uint32_t f, uint32_t g0, uint32_t g1) {
             uint32_t lo_ = g0, hi_ = g1;
             while (hi_ - lo_ > 1) {
                 const uint32_t mid = (lo_ + hi_) >> 1;
-                if (sm.big_cum[mid] <= f) lo_ = mid; else hi_ = mid;
+                if (sm.gcum[mid] <= f) lo_ = mid; else hi_ = mid;
             }
             return lo_;
         };
-        for (uint32_t gb = 0; gb < nbig;) {  // batches of groups whose masks / counters fit
-            const uint32_t ge = min(nbig, gb + (uint32_t)(kMaxBig / 4));
-            for (uint32_t g = gb + tid; g < ge; g += kFT) { sm.big_or[g - gb] = 0; sm.big_and[g - gb] = ~0ull; }
+        for (uint32_t gb = 0; gb < ng;) {  // batches: OR/AND slots and counter blocks must fit
+            const uint32_t ge = min(ng, gb + (uint32_t)(kMaxBig / 4));
+            for (uint32_t g = gb + tid; g < ge; g += kFT) { sm.gor[g - gb] = 0; sm.gand[g - gb] = ~0ull; }
             __syncthreads();
-            const uint32_t f0 = sm.big_cum[gb], f1 = ge < nbig ? (uint32_t)sm.big_cum[ge] : K;
-            for (uint32_t f = f0 + tid; f < f1; f += kFT) {
+            const uint32_t f0 = sm.gcum[gb], fe = ge < ng ? (uint32_t)sm.gcum[ge] : K;
+            for (uint32_t f = f0 + tid; f < fe; f += kFT) {
                 const uint32_t g = group_of(f, gb, ge);
-                const uint64_t k = A[sm.big_lo[g] + (f - sm.big_cum[g])];
-                atomicOr(&sm.big_or[g - gb], k);
-                atomicAnd(&sm.big_and[g - gb], k);
+                const uint64_t k = A[sm.gl_lo[cur][g] + (f - sm.gcum[g])];
+                atomicOr(&sm.gor[g - gb], k);
+                atomicAnd(&sm.gand[g - gb], k);
             }
             __syncthreads();
-            if (warp == 0) {  // shift, bits, counter bases; cut the batch where the counters end
+            if (warp == 0) {  // digit shift / bits, counter bases; cut the batch at kSubBuckets
                 uint32_t base = 0, cut = ge;
                 for (uint32_t g0 = gb; g0 < ge; g0 += 32) {
                     const uint32_t g = g0 + lane;
                     uint32_t sz = 0;
                     if (g < ge) {
-                        const unsigned long long v = sm.big_or[g - gb] ^ sm.big_and[g - gb];  // m > 1, unique keys
+                        const unsigned long long v = sm.gor[g - gb] ^ sm.gand[g - gb];  // != 0: unique keys
                         const int h = 63 - __clzll((long long)v);
-                        uint32_t db = 32u - (uint32_t)__clz((uint32_t)sm.big_n[g] - 1u);  // ceil(log2 m)
+                        uint32_t db = 32u - (uint32_t)__clz((uint32_t)sm.gl_n[cur][g] - 1u);  // ceil(log2 m)
                         db = db > (uint32_t)kSubBits ? (uint32_t)kSubBits : db;
-                        sm.big_sh[g] = (uint8_t)(h + 1 >= (int)db ? h + 1 - (int)db : 0);
-                        sm.big_db[g] = (uint8_t)db;
+                        sm.gsh[g] = (uint8_t)(h + 1 >= (int)db ? h + 1 - (int)db : 0);
+                        sm.gdb[g] = (uint8_t)db;
                         sz = 1u << db;
                     }
                     uint32_t x = sz;
@@ -340,81 +315,77 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
                         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                         if (lane >= (uint32_t)o) x += y;
                     }
-                    if (g < ge) sm.big_base[g] = (uint16_t)min(base + x - sz, 65535u);
+                    if (g < ge) sm.gbase[g] = (uint16_t)min(base + x - sz, 65535u);
                     const uint32_t ob = __ballot_sync(0xffffffffu, g < ge && base + x > (uint32_t)kSubBuckets);
                     if (ob && cut == ge) cut = g0 + __ffs(ob) - 1;
                     base += __shfl_sync(0xffffffffu, x, 31);
                 }
-                if (lane == 0) sm.w32[kFW - 1] = cut > gb ? cut : gb + 1;  // at least one group
+                if (lane == 0) sm.w32[kFW - 1] = cut > gb ? cut : gb + 1;
             }
             __syncthreads();
             const uint32_t gcut = sm.w32[kFW - 1];
-            const uint32_t fc = gcut < nbig ? (uint32_t)sm.big_cum[gcut] : K;
-            const uint32_t ncnt = min((uint32_t)kSubBuckets,
-                                      (uint32_t)sm.big_base[gcut - 1] + (1u << sm.big_db[gcut - 1]));
+            const uint32_t fc = gcut < ng ? (uint32_t)sm.gcum[gcut] : K;
+            const uint32_t ncnt = (uint32_t)sm.gbase[gcut - 1] + (1u << sm.gdb[gcut - 1]);
             for (uint32_t i = tid; i < ncnt; i += kFT) sm.pos[i] = 0;
             __syncthreads();
+#define GDIGIT(k, g) (sm.gbase[g] + ((uint32_t)((k) >> sm.gsh[g]) & ((1u << sm.gdb[g]) - 1u)))
             for (uint32_t f = f0 + tid; f < fc; f += kFT) {
                 const uint32_t g = group_of(f, gb, gcut);
-                const uint64_t k = A[sm.big_lo[g] + (f - sm.big_cum[g])];
-                atomicAdd(&sm.pos[sm.big_base[g] + ((uint32_t)(k >> sm.big_sh[g]) & ((1u << sm.big_db[g]) - 1u))], 1u);
+                atomicAdd(&sm.pos[GDIGIT(A[sm.gl_lo[cur][g] + (f - sm.gcum[g])], g)], 1u);
             }
             __syncthreads();
             (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, ncnt, sm.w32);
-            // positions: group g's keys occupy [cum_g, cum_g + m_g) of the batch's scan space
+            // group g's keys occupy [gcum_g - f0, gcum_g - f0 + m_g) of the batch's scan space
             for (uint32_t f = f0 + tid; f < fc; f += kFT) {
                 const uint32_t g = group_of(f, gb, gcut);
-                const uint32_t lo_g = sm.big_lo[g], cum_g = sm.big_cum[g];
-                const uint64_t k = A[lo_g + (f - cum_g)];
-                const uint32_t d = sm.big_base[g] + ((uint32_t)(k >> sm.big_sh[g]) & ((1u << sm.big_db[g]) - 1u));
-                Bf[lo_g + atomicAdd(&sm.pos[d], 1u) - (cum_g - f0)] = k;
+                const uint32_t lo_g = sm.gl_lo[cur][g], gz = sm.gcum[g] - f0;
+                const uint64_t k = A[lo_g + (f - sm.gcum[g])];
+                Bf[lo_g + atomicAdd(&sm.pos[GDIGIT(k, g)], 1u) - gz] = k;
             }
             __syncthreads();
-            for (uint32_t f = f0 + tid; f < fc; f += kFT) {  // rank inside the second-level groups
+            for (uint32_t f = f0 + tid; f < fc; f += kFT) {  // finish small sub-groups, list big ones
                 const uint32_t g = group_of(f, gb, gcut);
-                const uint32_t lo_g = sm.big_lo[g], cum_g = sm.big_cum[g], bs = sm.big_base[g];
-                const uint32_t i = f - cum_g;
+                const uint32_t lo_g = sm.gl_lo[cur][g], gz = sm.gcum[g] - f0;
+                const uint32_t i = f - sm.gcum[g];
                 const uint64_t k = Bf[lo_g + i];
-                const uint32_t d = (uint32_t)(k >> sm.big_sh[g]) & ((1u << sm.big_db[g]) - 1u);
-                // pos[] now holds ends in the batch scan space; group g starts at cum_g - f0 there
-                const uint32_t gz = cum_g - f0;
-                const uint32_t e = sm.pos[bs + d] - gz, st = (d ? sm.pos[bs + d - 1] - gz : 0u), m2 = e - st;
+                const uint32_t d = GDIGIT(k, g);
+                const uint32_t e = sm.pos[d] - gz;
+                const uint32_t st = (d > sm.gbase[g] ? sm.pos[d - 1] : sm.gcum[g] - f0 + gz * 0u) - gz;
+                const uint32_t stc = d > sm.gbase[g] ? st : 0u;
+                const uint32_t m2 = e - stc;
                 if (m2 > kMaxRankM) {
                     A[lo_g + i] = k;
-                    if (i == st) {
-                        const uint32_t t = atomicAdd(&sm.n3, 1u);
-                        if (t < (uint32_t)kMaxBig) { sm.g3_lo[t] = (uint16_t)(lo_g + st); sm.g3_n[t] = (uint16_t)m2; }
+                    if (i == stc) {
+                        const uint32_t t = atomicAdd(&sm.ngl[nxt], 1u);
+                        if (t < (uint32_t)kMaxBig) {
+                            sm.gl_lo[nxt][t] = (uint16_t)(lo_g + stc);
+                            sm.gl_n[nxt][t] = (uint16_t)m2;
+                        }
                     }
                     continue;
                 }
                 uint32_t r = 0;
 #pragma unroll 8
-                for (uint32_t q = st; q < e; q++) r += Bf[lo_g + q] < k ? 1u : 0u;
-                A[lo_g + st + r] = k;
+                for (uint32_t q = stc; q < e; q++) r += Bf[lo_g + q] < k ? 1u : 0u;
+                A[lo_g + stc + r] = k;
             }
+#undef GDIGIT
             __syncthreads();
             gb = gcut;
         }
-        const uint32_t n3 = sm.n3;
-        if (n3 > 32u) {  // pathological: stable LSD of the whole part
-            unsigned long long o, an;
-            block_or_and(sm, A, n, o, an);
-            const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
-            if (r != A)
-                for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
-            __syncthreads();
-        } else {
-            for (uint32_t t = 0; t < n3; t++) {
-                const uint32_t s0 = sm.g3_lo[t], m = sm.g3_n[t];
-                unsigned long long o, an;
-                block_or_and(sm, A + s0, m, o, an);
-                const uint64_t* r = local_lsd(sm, A + s0, Bf + s0, m, o ^ an);
-                if (r != A + s0)
-                    for (uint32_t i = tid; i < m; i += kFT) A[s0 + i] = r[i];
-                __syncthreads();
-            }
-        }
+        cur = nxt;
+        if (level + 1 == kMaxLevels && sm.ngl[cur]) full_lsd = true;
     }
+    LTRACE(3);
+    if (full_lsd) {  // pathological distributions: stable LSD of the whole part
+        unsigned long long o, an;
+        block_or_and(sm, A, n, o, an);
+        const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
+        if (r != A)
+            for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
+        __syncthreads();
+    }
+    if (tr && tid == 0) tr[5] = full_lsd ? 1000u : sm.ngl[0];
     LTRACE(4);
 #undef LTRACE
 }
@@ -632,7 +603,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     TRACE(12);
     // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
     // bucket with start >= q_r by binary search; the largest range decides the fallback
-    uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now
+    uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now: key boundaries
+    uint32_t* jb = rb + (G + 1);                             // and bucket boundaries of the ranges
     if (tid <= G) {
         // CTA 0 sorts only the head (about 2 * max_batch keys) so it can start the
         // admission early; the other CTAs share the rest evenly
@@ -644,6 +616,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
         }
         rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
+        jb[tid] = tid == G ? NB : lo;
     }
     __syncthreads();
     uint32_t mx = 0;
@@ -651,6 +624,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const bool fallback = (a.flags & kStepForceFallback) ||
                           __syncthreads_or(mx > (uint32_t)kKcap);
     const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
+    const uint32_t j_lo = jb[bid], j_hi = jb[bid + 1];
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
     TRACE(7);
@@ -672,8 +646,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             ns = tot;
         }
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
-        local_sort(sm.l, sm.l.a, sm.l.b, ns, c, tr ? tr + 16 : nullptr);
-        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, c, tr ? tr + 24 : nullptr);
+        // buckets [0, half) hold the starving keys
+        local_sort(sm.l, sm.l.a, sm.l.b, ns, T, j_lo, min(j_hi, half), tr ? tr + 16 : nullptr);
+        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr);
         TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;

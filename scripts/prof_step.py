@@ -45,14 +45,11 @@ if os.environ.get("TRACE"):
             d = d[:, :1]
         print(f"  {nm:12s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
     for base, part in ((16, "starving"), (24, "nonstarv")):
-        for nm, a0, a1 in (("minmax", 13 if base == 16 else 16 + 4, base + 0), ("count+scan", base + 0, base + 1),
-                           ("scatter", base + 1, base + 2), ("rank", base + 2, base + 3), ("big LSD", base + 3, base + 4)):
-            d = (t[:, :, a1] - t[:, :, a0]) / 1.965e3
-            print(f"  L.{part}.{nm:11s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
-        if base == 24:
-            for nm, a0, a1 in (("zero", 24, 30), ("count", 30, 31), ("scan", 31, 25)):
-                d = (t[:, :, a1] - t[:, :, a0]) / 1.965e3
-                print(f"  L.{part}.{nm:11s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
+        for nm, a0, a1 in (("bucket starts", 0, 1), ("rank level1", 1, 2), ("refine", 2, 3), ("lsd fallback", 3, 4)):
+            d = (t[:, :, base + a1] - t[:, :, base + a0]) / 1.965e3
+            ok = (t[:, :, base + a0] > 0) & (t[:, :, base + a1] >= t[:, :, base + a0])
+            d = np.where(ok, d, 0)
+            print(f"  L.{part}.{nm:14s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
         nb = t[:, :, base + 5]
-        print(f"  L.{part}.nbig       max {int(nb.max())} mean {nb.mean():.2f}")
+        print(f"  L.{part}.big groups   max {int(nb.max())} mean {nb.mean():.2f}")
     ms, nst = st.timing() if False else (None, None)
