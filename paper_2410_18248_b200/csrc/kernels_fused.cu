@@ -285,15 +285,24 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
         };
         for (uint32_t gb = 0; gb < ng;) {  // batches: OR/AND slots and counter blocks must fit
             const uint32_t ge = min(ng, gb + (uint32_t)(kMaxBig / 4));
-            for (uint32_t g = gb + tid; g < ge; g += kFT) { sm.gor[g - gb] = 0; sm.gand[g - gb] = ~0ull; }
-            __syncthreads();
-            const uint32_t f0 = sm.gcum[gb], fe = ge < ng ? (uint32_t)sm.gcum[ge] : K;
-            for (uint32_t f = f0 + tid; f < fe; f += kFT) {
-                const uint32_t g = group_of(f, gb, ge);
-                const uint64_t k = A[sm.gl_lo[cur][g] + (f - sm.gcum[g])];
-                atomicOr(&sm.gor[g - gb], k);
-                atomicAnd(&sm.gand[g - gb], k);
+            // OR / AND of each group's keys: one warp per group, shuffle reduction (64-bit
+            // shared-memory atomicOr/And would be CAS loops on a handful of addresses)
+            for (uint32_t g = gb + warp; g < ge; g += kFW) {
+                const uint32_t lo_g = sm.gl_lo[cur][g], m = sm.gl_n[cur][g];
+                unsigned long long o = 0, an = ~0ull;
+                for (uint32_t i = lane; i < m; i += 32) {
+                    const uint64_t k = A[lo_g + i];
+                    o |= k;
+                    an &= k;
+                }
+#pragma unroll
+                for (int sh = 16; sh; sh >>= 1) {
+                    o |= __shfl_xor_sync(0xffffffffu, o, sh);
+                    an &= __shfl_xor_sync(0xffffffffu, an, sh);
+                }
+                if (lane == 0) { sm.gor[g - gb] = o; sm.gand[g - gb] = an; }
             }
+            const uint32_t f0 = sm.gcum[gb];
             __syncthreads();
             if (warp == 0) {  // digit shift / bits, counter bases; cut the batch at kSubBuckets
                 uint32_t base = 0, cut = ge;
