@@ -46,7 +46,7 @@ struct PhaseS {                  // S, H, T, X
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
-constexpr uint32_t kMaxRankM = 16;          // largest group ranked by comparison
+constexpr uint32_t kMaxRankM = 32;          // largest group ranked by comparison
 constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
 constexpr int kMaxBig = 1024;               // groups per refinement list (else full LSD)
 constexpr int kMaxLevels = 6;               // refinement passes before the LSD fallback
