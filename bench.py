@@ -10,8 +10,10 @@ scheduling decisions/s = eligible (READY) requests decided per step / device
 time per step.  Inputs are resident in HBM; L2 (126 MB) is flushed before
 every timed step by writing a 256 MiB buffer (outside the timed events).
 
-For N > 1 (torchrun) every rank owns an independent 1M-request shard
-(weak scaling, "replicas"); time is the max over ranks.
+For N > 1 (torchrun) every rank owns its own 1M-request shard (weak scaling)
+and the ranks admit ONE global batch: each ranks its shard, one NCCL
+all-gather of the top-K records, an identical merge + cut on every rank
+(DESIGN.md section 8); time is the max over ranks.
 
 --impl reference times the CPU oracle (oracle/, plain C, one core) as it
 stands on the same workload: the reference arm of this tier.
@@ -189,7 +191,12 @@ def run_ours(args, rank, world, local):
     snap = gen.snapshot(cname, seed=rank, id_base=id_base)
     stream = torch.cuda.current_stream()
 
-    s = Scheduler(cfg, stream=stream)
+    nccl_id = None
+    if world > 1:  # one NCCL all-gather per step for the global admission merge
+        obj = [Scheduler.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    s = Scheduler(cfg, stream=stream, world=world, rank=rank, nccl_id=nccl_id)
     s.import_pool(snap, snap["id_base"], snap["next_id"])
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device="cuda")
@@ -224,7 +231,7 @@ def run_ours(args, rank, world, local):
     res = s.result()
     n_elig = res["n_eligible"]
     kernels, passes = s.stats()
-    fused = kernels == 1
+    fused = kernels == (1 if world == 1 else 2)
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     ne_t = torch.tensor([float(n_elig)], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -236,31 +243,33 @@ def run_ours(args, rank, world, local):
     # ---- per-kernel breakdown (separate handle with CUDA events between kernels, plus
     # the fused kernel's per-phase SM-clock trace)
     from paper_2410_18248_b200 import LAMPS_TRACE
-    sp = Scheduler(cfg, flags=LAMPS_TIMING | LAMPS_TRACE, stream=stream)
-    sp.import_pool(snap, snap["id_base"], snap["next_id"])
-    for _ in range(args.warmup):
-        flush.zero_()
-        sp.step_async(kv)
-    sp.timing()
-    traces = []
-    for _ in range(args.steps):
-        flush.zero_()
-        sp.step_async(kv)
-        if fused and len(traces) < 10:
-            traces.append(sp.trace().astype(np.int64))
-    phase_ms, nst = sp.timing()
-    sp_kernels, sp_passes = sp.stats()
-    sp.close()
-    phase = [x / nst for x in phase_ms]  # ms per step: [events, score or fused, sort, admit]
-    trace_us = None
-    if fused and traces:
-        t = np.stack(traces)
-        segs = [("score", 0, 1), ("publish", 1, 2), ("barrier1", 2, 3), ("count_exchange", 3, 4),
-                ("barrier2", 4, 5), ("bucket_scatter", 5, 6), ("barrier3", 6, 7), ("range_sort", 7, 8)]
-        mhz = float(clk.summary().get("sm_mhz") or 1965.0)
-        trace_us = {nm: round(float(np.median((t[:, :, b1] - t[:, :, a1]).max(axis=1))) / mhz, 2)
-                    for nm, a1, b1 in segs}
-        trace_us["admission_cta0"] = round(float(np.median(t[:, 0, 9] - t[:, 0, 8])) / mhz, 2)
+    phase, trace_us, sp_passes = None, None, passes
+    sp = Scheduler(cfg, flags=LAMPS_TIMING | LAMPS_TRACE, stream=stream) if world == 1 else None
+    if sp is not None:
+      sp.import_pool(snap, snap["id_base"], snap["next_id"])
+      for _ in range(args.warmup):
+          flush.zero_()
+          sp.step_async(kv)
+      sp.timing()
+      traces = []
+      for _ in range(args.steps):
+          flush.zero_()
+          sp.step_async(kv)
+          if fused and len(traces) < 10:
+              traces.append(sp.trace().astype(np.int64))
+      phase_ms, nst = sp.timing()
+      sp_kernels, sp_passes = sp.stats()
+      sp.close()
+      phase = [x / nst for x in phase_ms]  # ms per step: [events, score or fused, sort, admit]
+      trace_us = None
+      if fused and traces:
+          t = np.stack(traces)
+          segs = [("score", 0, 1), ("publish", 1, 2), ("barrier1", 2, 3), ("count_exchange", 3, 4),
+                  ("barrier2", 4, 5), ("bucket_scatter", 5, 6), ("barrier3", 6, 7), ("range_sort", 7, 8)]
+          mhz = float(clk.summary().get("sm_mhz") or 1965.0)
+          trace_us = {nm: round(float(np.median((t[:, :, b1] - t[:, :, a1]).max(axis=1))) / mhz, 2)
+                      for nm, a1, b1 in segs}
+          trace_us["admission_cta0"] = round(float(np.median(t[:, 0, 9] - t[:, 0, 8])) / mhz, 2)
 
     # ---- end to end through the public API (host events in, host result out)
     e2e_steps = args.e2e_steps or args.steps
@@ -311,7 +320,10 @@ def run_ours(args, rank, world, local):
         # algorithmic bytes of one step: the SoA is read once (28 B/slot),
         # the state word written once (4 B/slot), and the keys written and read once (16 B/key)
         step_bytes = 32 * cap + 16 * n_elig
-        if fused:
+        if phase is None:  # multi-GPU: whole step (fused kernel + all-gather + merge), max over ranks
+            dom = "k_fused+merge"
+            kernels_tbl = {dom: {"ms": ms_max, "bytes": step_bytes, "GBps": step_bytes / (ms_max * 1e6)}}
+        elif fused:
             dom = "k_fused"
             kernels_tbl = {"k_fused": {"ms": phase[1], "bytes": step_bytes, "GBps": step_bytes / (phase[1] * 1e6),
                                        "phase_us": trace_us},
@@ -344,7 +356,8 @@ def run_ours(args, rank, world, local):
                        "kv_total_blocks": kv, "max_batch": cfg["max_batch"],
                        "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
                        "l2": "flushed before every timed step (256 MiB write)",
-                       "parallelism": f"replicas x{world}"},
+                       "parallelism": (f"{world} shards x 1M, one NCCL all-gather of the top-{cfg['max_batch']} "
+                                       f"per step for the global admission") if world > 1 else "1 shard"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak if ach else None, "traffic": traffic,
                          "peak_source": peak_src},

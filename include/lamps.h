@@ -115,9 +115,18 @@ typedef struct {
     uint32_t score_bits, id_bits;     /* key layout: score_bits + id_bits + 1 <= 64,
                                          2^id_bits >= capacity */
     void* stream;                     /* cudaStream_t to run on (NULL = legacy default) */
-    uint32_t flags;                   /* LAMPS_DEBUG_OUT */
-    uint32_t reserved;
+    uint32_t flags;                   /* LAMPS_DEBUG_OUT, LAMPS_TIMING, ... */
+    /* ---- multi-GPU: shard-parallel pools, global admission ------ */
+    uint32_t world;                   /* number of shards (ranks); 0 or 1 = single shard */
+    uint32_t rank;                    /* this shard, < world.  Shard r owns the global ids
+                                         g with g mod world == r; its local id l is g / world */
+    uint32_t transport;               /* LAMPS_XPORT_NCCL or LAMPS_XPORT_LOOPBACK */
+    const void* nccl_id;              /* 128-byte ncclUniqueId (all ranks the same; from
+                                         lamps_nccl_unique_id on one rank) */
 } lamps_config;
+
+#define LAMPS_XPORT_NCCL 0u     /* one ncclAllGather per step over NVLink (libnccl.so.2) */
+#define LAMPS_XPORT_LOOPBACK 1u /* all shards in this process on one device: lamps_group_step */
 
 /*
  * Result of one step.  Host arrays are owned by the handle and stay valid until
@@ -258,6 +267,31 @@ int lamps_timing_read(lamps_t* h, double ms[4], uint32_t* n_steps);
  * *n_cta receives the grid size.
  */
 int lamps_trace_read(lamps_t* h, uint64_t* out, uint32_t max_words, uint32_t* n_cta);
+
+/*
+ * Multi-GPU.  With world > 1 a step ranks every shard's requests locally, takes
+ * the head K (= max_batch, the GLOBAL batch limit) of the local order as
+ * records, exchanges them with ONE all-gather, merges the world sorted runs
+ * identically on every rank and cuts the global order against the global
+ * budget (sum of kv_total - sum of pinned) and K; each rank admits its own
+ * prefix.  The result equals one step over the union pool (global ids).
+ * lamps_step_out then holds: n_eligible, pinned, n_admitted, n_preempted local;
+ * budget, budget_used, blocked_head global.  Requires the fused path
+ * (capacity <= #SM * 10240) and world * max_batch <= 8192.
+ *
+ * lamps_nccl_unique_id: fill out[128] with a new ncclUniqueId (LAMPS_ENCCL if
+ * libnccl.so.2 cannot be loaded); broadcast it to every rank before lamps_init.
+ */
+int lamps_nccl_unique_id(void* out128);
+
+/*
+ * Loopback transport: one step of `world` shards that live in this process on
+ * one device (handles created with transport LAMPS_XPORT_LOOPBACK, ranks
+ * 0..world-1, same stream).  ev[r] / n_ev[r] / kv_total[r] / out[r] are the
+ * per-shard arguments of lamps_schedule_step.  The all-gather is a device copy.
+ */
+int lamps_group_step(lamps_t* const* h, uint32_t world, const lamps_event* const* ev,
+                     const uint32_t* n_ev, const uint64_t* kv_total, lamps_step_out* out);
 
 /* Library version (major << 16 | minor). */
 uint32_t lamps_version(void);

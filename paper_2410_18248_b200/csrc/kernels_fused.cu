@@ -187,14 +187,6 @@ __device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint
     __syncthreads();
 }
 
-// Float-like digit of a score: exact below 2^mb, else (bit length - mb) << mb plus
-// the mb bits below the leading one.  Monotone in the score.
-__device__ __forceinline__ uint32_t flt_digit(uint64_t sc, uint32_t mb) {
-    const uint32_t e = 64u - (uint32_t)__clzll((long long)sc);
-    if (e <= mb) return (uint32_t)sc;
-    return ((e - mb) << mb) + (uint32_t)((sc >> (e - 1 - mb)) & ((1u << mb) - 1u));
-}
-
 // Sort of the n keys at A[0..n) of one part of a range (same starving flag) in
 // shared memory; result in A, Bf is scratch.  The part arrives in global-bucket
 // order and its buckets [j0, j1) are known, so the buckets are the first-level
@@ -671,7 +663,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // ---------------- A: admission by CTA 0
     // CTA 0 may start as soon as the head it needs is sorted: without the fallback
     // the keys [0, rb[1]) are sorted by CTA 0 itself.
-    const uint32_t need = min(n, a.max_batch);
+    const uint32_t need = min(n, a.max_batch);  // the admission (or the merge records) reads keys [0, need)
     const bool wait = fallback || r_end0 < need;
     if (wait) grid_barrier(b.flags, G, ++bar);
     if (bid != 0) return;
@@ -688,8 +680,35 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         ctl->fallbacks += fallback ? 1u : 0u;
     }
     TRACE(15);
-    // the head of the order is still in shared memory unless the fallback ran
-    admit_cta(b, c, a, fallback ? b.keys[final_buf] : sm.l.a, n, pinned_all, sm.l.adm);
+    const uint64_t* head = wait ? b.keys[final_buf] : sm.l.a;  // CTA 0 holds [0, need) itself unless it waited
+    if (a.flags & kStepMerge) {
+        // multi-GPU: publish this rank's head as exchange records instead of admitting
+        const uint32_t K = a.max_batch, nv = min(n, K);
+        const uint64_t idmask = (1ull << c.IB) - 1ull;
+        for (uint32_t i = tid; i < nv; i += kFT) {
+            const uint64_t k = head[i];
+            const uint64_t lid = a.id_base + (k & idmask);
+            const uint32_t slot = (uint32_t)(lid & c.cap_mask);
+            MergeRec r;
+            r.sk = k >> c.IB;
+            r.gid = lid * a.world + a.rank;
+            r.demand = (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
+            r.slot = slot;
+            r.pad = 0;
+            b.xsend[1 + i] = r;
+        }
+        if (tid == 0) {
+            MergeHdr* h = reinterpret_cast<MergeHdr*>(b.xsend);
+            h->pinned = pinned_all;
+            h->kv_total = a.kv_total;
+            h->n_valid = nv;
+            h->n_local = n;
+            h->pad = 0;
+        }
+        TRACE(9);
+        return;
+    }
+    admit_cta(b, c, a, head, n, pinned_all, sm.l.adm);
     TRACE(9);
 }
 

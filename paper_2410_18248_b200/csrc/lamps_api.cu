@@ -6,6 +6,7 @@
 // admission.  Every step of the method runs in the kernels; the host only
 // moves inputs and outputs.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -41,6 +42,32 @@ bool quantize(double seconds, double tps, uint32_t* out) {
     return true;
 }
 
+// ---- NCCL, loaded at run time (only multi-GPU handles need it) ----------------
+typedef void* nccl_comm_t;
+struct NcclApi {
+    void* so = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    int (*commInitRank)(nccl_comm_t*, int, const void* /* by value 128 B, see call */, int) = nullptr;
+    int (*allGather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*commDestroy)(nccl_comm_t) = nullptr;
+    const char* (*getErrorString)(int) = nullptr;
+    bool load() {
+        if (so) return true;
+        so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!so) so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!so) return false;
+        getUniqueId = (int (*)(void*))dlsym(so, "ncclGetUniqueId");
+        allGather = (int (*)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t))dlsym(so, "ncclAllGather");
+        commDestroy = (int (*)(nccl_comm_t))dlsym(so, "ncclCommDestroy");
+        getErrorString = (const char* (*)(int))dlsym(so, "ncclGetErrorString");
+        return getUniqueId && allGather && commDestroy && dlsym(so, "ncclCommInitRank");
+    }
+};
+NcclApi g_nccl;
+struct NcclId { char internal[128]; };  // ncclUniqueId is passed by value
+typedef int (*CommInitRankFn)(nccl_comm_t*, int, NcclId, int);
+constexpr int kNcclUint8 = 1;  // ncclUint8 in ncclDataType_t
+
 struct Layout {
     size_t off = 0;
     size_t take(size_t bytes) {
@@ -59,6 +86,8 @@ struct lamps_s {
     Bufs b{};
     uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
     bool fused = false;
+    uint32_t world = 1, rank = 0;
+    nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
     void* d_ingest = nullptr;
@@ -119,6 +148,12 @@ const char* validate_cfg(const lamps_config* c) {
     if (c->score_bits == 0 || c->id_bits == 0 || c->score_bits + c->id_bits + 1 > 64)
         return "need score_bits, id_bits >= 1 and score_bits + id_bits + 1 <= 64";
     if (c->id_bits < 64 && (1ull << c->id_bits) < c->capacity) return "2^id_bits must be >= capacity";
+    if (c->world > 1) {
+        if (c->world > 32 || c->rank >= c->world) return "need rank < world <= 32";
+        if ((uint64_t)c->world * c->max_batch > kMergeMaxRecords) return "world * max_batch must be <= 8192";
+        if (c->transport > LAMPS_XPORT_LOOPBACK) return "unknown transport";
+        if (c->transport == LAMPS_XPORT_NCCL && !c->nccl_id) return "NCCL transport needs nccl_id";
+    }
     return nullptr;
 }
 
@@ -148,7 +183,12 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_gat = L.take((size_t)kIngestChunk * 4);
     size_t o_dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? L.take((size_t)cap_pad * 32) : 0;
     size_t o_trace = (h->cfg.flags & LAMPS_TRACE) ? L.take((size_t)gmax * kTraceSlots * 8) : 0;
+    const uint32_t world = h->cfg.world > 1 ? h->cfg.world : 1;
+    size_t o_xs = world > 1 ? L.take(((size_t)mb + 1) * sizeof(MergeRec)) : 0;
+    size_t o_xr = world > 1 ? L.take((size_t)world * ((size_t)mb + 1) * sizeof(MergeRec)) : 0;
     if (!base) return L.off;
+    h->b.xsend = world > 1 ? reinterpret_cast<MergeRec*>(base + o_xs) : nullptr;
+    h->b.xrecv = world > 1 ? reinterpret_cast<MergeRec*>(base + o_xr) : nullptr;
     uint32_t* soa[8];
     for (int i = 0; i < 8; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
     h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7], cap_pad};
@@ -270,10 +310,7 @@ void record_timing(lamps_t* h, int k) {
 }
 
 // Enqueue K0..K3 for one step on the handle's stream.
-int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
-    const bool timing = (h->cfg.flags & LAMPS_TIMING) != 0;
-    if (timing && h->t_count == kTimingRing) return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
-    h->step++;
+StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     StepArgs a{};
     a.kv_total = kv_total;
     a.id_base = h->id_base;
@@ -283,8 +320,20 @@ int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.n_ev = n_ev;
     a.max_batch = h->cfg.max_batch;
     a.parity = h->step & 1u;
-    h->last_id_base = h->id_base;
     a.flags = (h->cfg.flags & LAMPS_FORCE_FALLBACK) ? kStepForceFallback : 0u;
+    a.world = h->world;
+    a.rank = h->rank;
+    if (h->world > 1) a.flags |= kStepMerge;
+    return a;
+}
+
+// phase 1: events, scoring, ranking (and, single shard, admission)
+int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
+    const bool timing = (h->cfg.flags & LAMPS_TIMING) != 0;
+    if (timing && h->t_count == kTimingRing) return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
+    h->step++;
+    const StepArgs a = make_args(h, kv_total, n_ev);
+    h->last_id_base = h->id_base;
     record_timing(h, 0);
     CU(h, launch_events(h->b, h->cost, a, h->stream));
     record_timing(h, 1);
@@ -299,14 +348,39 @@ int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         record_timing(h, 3);
         CU(h, launch_admit(h->b, h->cost, a, h->stream));
     }
+    h->last_kernels = (h->fused ? 1 : 3) + (n_ev ? 1 : 0);
+    return LAMPS_OK;
+}
+
+// phase 2 (world > 1): exchange the top-K records, merge, admit this rank's share
+int enqueue_phase2(lamps_t* h, uint64_t kv_total, uint32_t n_ev, bool exchange) {
+    if (h->world > 1) {
+        const StepArgs a = make_args(h, kv_total, n_ev);
+        if (exchange) {
+            const size_t bytes = ((size_t)h->cfg.max_batch + 1) * sizeof(MergeRec);
+            const int r = g_nccl.allGather(h->b.xsend, h->b.xrecv, bytes, kNcclUint8, h->comm, h->stream);
+            if (r != 0)
+                return fail(h, LAMPS_ENCCL, std::string("ncclAllGather: ") +
+                                                (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+        }
+        CU(h, launch_merge(h->b, h->cost, a, h->stream));
+        h->last_kernels += 1;
+    }
     record_timing(h, 4);
-    if (timing) {
+    if (h->cfg.flags & LAMPS_TIMING) {
         h->t_head = (h->t_head + 1) % kTimingRing;
         h->t_count++;
     }
-    h->last_kernels = (h->fused ? 1 : 3) + (n_ev ? 1 : 0);
     h->have_result = true;
     return LAMPS_OK;
+}
+
+int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
+    if (h->world > 1 && h->cfg.transport != LAMPS_XPORT_NCCL)
+        return fail(h, LAMPS_EINVAL, "loopback shards step together: use lamps_group_step");
+    int rc = enqueue_phase1(h, kv_total, n_ev);
+    if (rc) return rc;
+    return enqueue_phase2(h, kv_total, n_ev, true);
 }
 
 int fetch_result(lamps_t* h, lamps_step_out* out) {
@@ -393,6 +467,12 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
         delete h;
         return LAMPS_ENOTSUP;
     }
+    h->world = cfg->world > 1 ? cfg->world : 1;
+    h->rank = cfg->world > 1 ? cfg->rank : 0;
+    if (h->world > 1 && !h->fused) {
+        delete h;
+        return LAMPS_ENOTSUP;  // multi-GPU merge is implemented on the fused path
+    }
     carve(h, h->ws);
     Cost& c = h->cost;
     c.tau = cfg->tau; c.A1 = cfg->A1; c.A2 = cfg->A2; c.S0 = cfg->S0; c.S1 = cfg->S1;
@@ -421,6 +501,13 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
             if (cudaEventCreate(&e) != cudaSuccess) return cleanup(LAMPS_ECUDA, "event");
     }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "sync");
+    if (h->world > 1 && cfg->transport == LAMPS_XPORT_NCCL) {
+        if (!g_nccl.load()) return cleanup(LAMPS_ENCCL, "libnccl.so.2 not loadable");
+        NcclId id;
+        std::memcpy(id.internal, cfg->nccl_id, sizeof(id.internal));
+        CommInitRankFn init = (CommInitRankFn)dlsym(g_nccl.so, "ncclCommInitRank");
+        if (init(&h->comm, (int)h->world, id, (int)h->rank) != 0) return cleanup(LAMPS_ENCCL, "ncclCommInitRank");
+    }
     *out = h;
     return LAMPS_OK;
 }
@@ -428,6 +515,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
 int lamps_free(lamps_t* h) {
     if (!h) return LAMPS_EINVAL;
     cudaStreamSynchronize(h->stream);
+    if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
     for (auto& e : h->tev)
         if (e) cudaEventDestroy(e);
     if (h->h_ingest) cudaFreeHost(h->h_ingest);
@@ -532,9 +620,9 @@ int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_res
     return LAMPS_OK;
 }
 
-int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks,
-                        lamps_step_out* out) {
-    if (!h) return LAMPS_EINVAL;
+// host-side part of a step: validate the events against the previous admitted
+// list, stage them to the device, update the liveness shadow (state unchanged on error)
+int prepare_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks) {
     if (n_ev && !ev) return fail(h, LAMPS_EINVAL, "events is NULL");
     if (kv_total_blocks > h->cfg.kv_capacity_blocks)
         return fail(h, LAMPS_EINVAL, "kv_total_blocks exceeds kv_capacity_blocks");
@@ -565,9 +653,55 @@ int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64
             h->hstate[ev[e].id & h->cost.cap_mask] = ev[e].kind == LAMPS_EV_FINISHED ? H_FREE : H_PAUSED;
         advance_id_base(h);
     }
-    int rc = enqueue_step(h, kv_total_blocks, n_ev);
+    return LAMPS_OK;
+}
+
+int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks,
+                        lamps_step_out* out) {
+    if (!h) return LAMPS_EINVAL;
+    int rc = prepare_step(h, ev, n_ev, kv_total_blocks);
+    if (rc) return rc;
+    rc = enqueue_step(h, kv_total_blocks, n_ev);
     if (rc) return rc;
     return fetch_result(h, out);
+}
+
+int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* const* ev, const uint32_t* n_ev,
+                     const uint64_t* kv_total, lamps_step_out* out) {
+    if (!hs || !n_ev || !kv_total || world < 2 || world > 32) return LAMPS_EINVAL;
+    for (uint32_t r = 0; r < world; r++) {
+        if (!hs[r] || hs[r]->world != world || hs[r]->rank != r || hs[r]->cfg.transport != LAMPS_XPORT_LOOPBACK ||
+            hs[r]->cfg.max_batch != hs[0]->cfg.max_batch || hs[r]->stream != hs[0]->stream)
+            return fail(hs[0], LAMPS_EINVAL, "group: handles must be loopback ranks 0..world-1 on one stream");
+    }
+    for (uint32_t r = 0; r < world; r++) {
+        int rc = prepare_step(hs[r], ev ? ev[r] : nullptr, n_ev[r], kv_total[r]);
+        if (rc) return rc;  // earlier shards were validated and staged only (no kernel ran yet)
+    }
+    for (uint32_t r = 0; r < world; r++) {
+        int rc = enqueue_phase1(hs[r], kv_total[r], n_ev[r]);
+        if (rc) return rc;
+    }
+    const size_t bytes = ((size_t)hs[0]->cfg.max_batch + 1) * sizeof(MergeRec);
+    for (uint32_t d = 0; d < world; d++)
+        for (uint32_t r = 0; r < world; r++)
+            CU(hs[d], cudaMemcpyAsync(reinterpret_cast<uint8_t*>(hs[d]->b.xrecv) + r * bytes, hs[r]->b.xsend, bytes,
+                                      cudaMemcpyDeviceToDevice, hs[d]->stream));
+    for (uint32_t r = 0; r < world; r++) {
+        int rc = enqueue_phase2(hs[r], kv_total[r], n_ev[r], false);
+        if (rc) return rc;
+    }
+    for (uint32_t r = 0; r < world; r++) {
+        int rc = fetch_result(hs[r], out ? &out[r] : nullptr);
+        if (rc) return rc;
+    }
+    return LAMPS_OK;
+}
+
+int lamps_nccl_unique_id(void* out128) {
+    if (!out128) return LAMPS_EINVAL;
+    if (!g_nccl.load()) return LAMPS_ENCCL;
+    return g_nccl.getUniqueId(out128) == 0 ? LAMPS_OK : LAMPS_ENCCL;
 }
 
 int lamps_schedule_step_async(lamps_t* h, uint64_t kv_total_blocks) {

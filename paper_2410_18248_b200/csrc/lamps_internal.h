@@ -19,6 +19,22 @@ constexpr int kAdmitThreads = 1024; // K3 (single CTA)
 constexpr int kMaxBatch = 16384;
 constexpr int kFusedKcap = 10240;    // keys per SM kept in shared memory by the fused step kernel
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
+constexpr uint32_t kStepMerge = 2u;          // StepArgs.flags: emit top-K records, no local admission
+constexpr uint32_t kMergeMaxRecords = 8192;  // world * max_batch limit of the merge kernel
+
+// multi-GPU exchange: per rank one header followed by K records (32 B each)
+struct MergeHdr {
+    unsigned long long pinned, kv_total;
+    uint32_t n_valid, n_local;
+    unsigned long long pad;
+};
+struct MergeRec {
+    unsigned long long sk;   // (!starving << SB) | score
+    unsigned long long gid;  // global id = local id * world + rank
+    uint32_t demand, slot;
+    unsigned long long pad;
+};
+static_assert(sizeof(MergeHdr) == 32 && sizeof(MergeRec) == 32, "exchange records are 32 B");
 constexpr int kTraceSlots = 32;
 constexpr uint32_t kBarPerStep = 64;  // grid-barrier values reserved per step
 
@@ -48,7 +64,8 @@ struct StepArgs {
     uint32_t n_ev;
     uint32_t max_batch;
     uint32_t parity;        // admitted list buffer written this step
-    uint32_t flags;         // kStepForceFallback
+    uint32_t flags;         // kStepForceFallback, kStepMerge
+    uint32_t world, rank;   // multi-GPU shards
 };
 
 struct Bufs {
@@ -67,6 +84,8 @@ struct Bufs {
     unsigned long long* dbg; // [cap][4] W_P, W_D, W_S, score (LAMPS_DEBUG_OUT) or null
     unsigned long long* trace;  // [grid][16] clock64 at phase boundaries (LAMPS_TRACE) or null
     uint32_t* flags;         // grid barrier words (see sort_dev.cuh)
+    MergeRec* xsend;         // [1 + K] header + top-K records of this rank (world > 1)
+    MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
 };
 
 // launchers (kernels_step.cu / kernels_sort.cu)
@@ -79,6 +98,7 @@ size_t fused_smem_bytes();
 int fused_blocks_per_sm();
 uint32_t fused_max_buckets();
 cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t grid, cudaStream_t s);
+cudaError_t launch_merge(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 cudaError_t launch_admit(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 
 // ingest records (host -> device staging)

@@ -19,6 +19,7 @@ LAMPS_FREE, LAMPS_READY, LAMPS_PAUSED_P, LAMPS_PAUSED_D, LAMPS_PAUSED_S = 0, 1, 
 LAMPS_PRESERVE, LAMPS_DISCARD, LAMPS_SWAP, LAMPS_NONE = 0, 1, 2, 3
 LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
 LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE = 1, 2, 4, 8, 16
+LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK = 0, 1
 
 u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 
@@ -37,7 +38,8 @@ class lamps_config(ctypes.Structure):
                 ("S0", u64), ("S1", u64), ("SH", u32), ("c_other", u64),
                 ("ticks_per_second", dbl), ("starvation_threshold", u32), ("max_batch", u32),
                 ("kv_capacity_blocks", u64), ("score_bits", u32), ("id_bits", u32),
-                ("stream", vp), ("flags", u32), ("reserved", u32)]
+                ("stream", vp), ("flags", u32), ("world", u32), ("rank", u32), ("transport", u32),
+                ("nccl_id", vp)]
 
 
 class lamps_step_out(ctypes.Structure):
@@ -89,6 +91,8 @@ def lib() -> ctypes.CDLL:
             "lamps_step_stats": (c_int, [vp, P(u32), P(u32)]),
             "lamps_timing_read": (c_int, [vp, P(dbl), P(u32)]),
             "lamps_trace_read": (c_int, [vp, vp, u32, P(u32)]),
+            "lamps_nccl_unique_id": (c_int, [vp]),
+            "lamps_group_step": (c_int, [vp, u32, vp, vp, vp, vp]),
             "lamps_version": (u32, []),
         }
         for name, (res, args) in sig.items():
@@ -152,7 +156,8 @@ class Scheduler:
     example).  flags: LAMPS_DEBUG_OUT | LAMPS_TIMING.
     """
 
-    def __init__(self, cfg: dict, flags: int = 0, stream=None, device=None):
+    def __init__(self, cfg: dict, flags: int = 0, stream=None, device=None, world: int = 1, rank: int = 0,
+                 transport: int = LAMPS_XPORT_NCCL, nccl_id: bytes = None):
         import torch
         if not torch.cuda.is_available():
             raise LampsError(LAMPS_ECUDA, "no CUDA device: the LAMPS pass has no CPU fallback")
@@ -165,6 +170,10 @@ class Scheduler:
                 setattr(c, name, cfg[name])
         c.flags = flags
         c.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        c.world, c.rank, c.transport = world, rank, transport
+        self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        c.nccl_id = ctypes.cast(self._nccl_id, vp) if self._nccl_id is not None else None
+        self.world, self.rank = world, rank
         self.cfg = c
         self.capacity = int(cfg["capacity"])
         self.max_batch = int(cfg["max_batch"])
@@ -281,6 +290,31 @@ class Scheduler:
         n = u32(0)
         self._check(lib().lamps_timing_read(self.h, ms, ctypes.byref(n)))
         return list(ms), int(n.value)
+
+    # ---- multi-GPU
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        rc = lib().lamps_nccl_unique_id(buf)
+        if rc != LAMPS_OK:
+            raise LampsError(rc, "ncclGetUniqueId failed (libnccl.so.2)")
+        return buf.raw
+
+    @staticmethod
+    def group_step(shards, events=None, kv_totals=None) -> list:
+        """One step of loopback shards (same device and stream), see lamps_group_step."""
+        W = len(shards)
+        evs = [np.zeros(0, EVENT_DTYPE) if events is None or events[r] is None
+               else np.ascontiguousarray(events[r], EVENT_DTYPE) for r in range(W)]
+        ev_ptrs = (vp * W)(*[e.ctypes.data if len(e) else None for e in evs])
+        n_ev = (u32 * W)(*[len(e) for e in evs])
+        kv = (u64 * W)(*[int(x) for x in kv_totals])
+        outs = (lamps_step_out * W)()
+        hs = (vp * W)(*[s.h for s in shards])
+        rc = lib().lamps_group_step(hs, W, ev_ptrs, n_ev, kv, outs)
+        if rc != LAMPS_OK:
+            raise LampsError(rc, lamps_last_error(shards[0].h))
+        return [shards[r]._result(outs[r]) for r in range(W)]
 
     # ---- snapshots
     def import_pool(self, fields: dict, id_base: int, next_id: int):

@@ -1,0 +1,73 @@
+"""Multi-GPU global admission on one device through the loopback
+transport: `world` shards step together (lamps_group_step); the exchange is a
+device copy instead of the NCCL all-gather, the merge kernel is the one the
+NCCL path runs.  Every shard must equal one oracle step over the union pool."""
+import numpy as np
+import pytest
+
+import gen
+import oracle as O
+from shard_util import FIELDS, restrict, split_kv, union_and_shards
+
+pytestmark = pytest.mark.gpu
+
+
+def run(cname, world, cap_l, n_union, kv_union, steps=3, seed=0, **over):
+    from paper_2410_18248_b200 import Scheduler
+    from paper_2410_18248_b200.lamps import LAMPS_XPORT_LOOPBACK
+    import torch
+    cfg_l, cfg_u, u, shards = union_and_shards(cname, world, cap_l, n_union, seed=seed, **over)
+    stream = torch.cuda.current_stream()
+    S = [Scheduler(cfg_l, world=world, rank=r, transport=LAMPS_XPORT_LOOPBACK, stream=stream)
+         for r in range(world)]
+    for r in range(world):
+        S[r].import_pool(shards[r], shards[r]["id_base"], shards[r]["next_id"])
+    o = O.OraclePool(cfg_u)
+    o.load(u, u["next_id"])
+    kvs = split_kv(kv_union, world)
+    for t in range(steps):
+        outs = Scheduler.group_step(S, None, kvs)
+        ro = o.step(kv_total=kv_union)
+        assert ro["rc"] == 0
+        for r in range(world):
+            g = outs[r]
+            where = f"{cname} W={world} t={t} r={r}"
+            assert list(g["admitted_id"]) == list(restrict(ro["admitted_id"], world, r)), where
+            assert list(g["preempted_id"]) == list(restrict(ro["preempted_id"], world, r)), where
+            assert g["budget"] == ro["budget"] and g["budget_used"] == ro["budget_used"], where
+            assert g["blocked_head"] == ro["blocked_head"], where
+            # local ranked order == global order restricted to the shard
+            ids, score, starv = S[r].decode_keys(S[r].ranked_keys(), g["id_base"])
+            mine = ro["ranked_id"] % world == r
+            assert np.array_equal(ids, ro["ranked_id"][mine] // world), where
+            assert np.array_equal(score, ro["ranked_score"][mine]), where
+            assert np.array_equal(starv, ro["ranked_starving"][mine]), where
+            # whole shard state == union state restricted
+            e = S[r].export_pool()
+            P = o.pool
+            live = (P["state"] != 0) & (P["id"].astype(np.int64) % world == r)
+            lids = P["id"][live].astype(np.int64) // world
+            for f in FIELDS:
+                assert np.array_equal(e[f][lids % cap_l], P[f][live].astype(np.uint32)), (where, f)
+        assert sum(x["n_admitted"] for x in outs) == ro["n_admitted"]
+    for s in S:
+        s.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_merge_c2(world):
+    run("C2", world, 2048, 1800, 3000, max_batch=256)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_loopback_merge_c4(world):
+    run("C4", world, 16384, 100000, 10000, max_batch=1024)
+
+
+def test_loopback_merge_tight_budget_and_small_k():
+    run("C3", 4, 1024, 3000, 80, max_batch=7)
+
+
+def test_loopback_merge_empty_shard():
+    # a union of 3 requests over 4 shards: one shard has nothing
+    run("C1", 4, 16, 3, 292, max_batch=16)
