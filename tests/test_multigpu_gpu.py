@@ -59,9 +59,9 @@ def test_loopback_merge_c2(world):
     run("C2", world, 2048, 1800, 3000, max_batch=256)
 
 
-@pytest.mark.parametrize("world", [2, 8])
-def test_loopback_merge_c4(world):
-    run("C4", world, 16384, 100000, 10000, max_batch=1024)
+@pytest.mark.parametrize("world,cap_l", [(2, 65536), (8, 16384)])
+def test_loopback_merge_c4(world, cap_l):
+    run("C4", world, cap_l, 100000, 10000, max_batch=1024)
 
 
 def test_loopback_merge_tight_budget_and_small_k():
