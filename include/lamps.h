@@ -70,6 +70,9 @@ extern "C" {
 #define LAMPS_MULTI_KERNEL 4u   /* use the 3-kernel path even where the fused step kernel fits */
 #define LAMPS_FORCE_FALLBACK 8u /* fused path: always take the global-LSD fallback (tests) */
 #define LAMPS_TRACE 16u         /* fused path: record SM clock at phase boundaries (lamps_trace_read) */
+#define LAMPS_MERGE 32u         /* world <= 1: still run the multi-shard exchange + merge over a 1-rank
+                                   NCCL communicator (transport NCCL, nccl_id required); tests the
+                                   NCCL path on one GPU */
 
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 

@@ -87,6 +87,7 @@ struct lamps_s {
     uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
     bool fused = false;
     uint32_t world = 1, rank = 0;
+    bool merge = false;  // merge_mode(cfg)
     nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
@@ -148,14 +149,19 @@ const char* validate_cfg(const lamps_config* c) {
     if (c->score_bits == 0 || c->id_bits == 0 || c->score_bits + c->id_bits + 1 > 64)
         return "need score_bits, id_bits >= 1 and score_bits + id_bits + 1 <= 64";
     if (c->id_bits < 64 && (1ull << c->id_bits) < c->capacity) return "2^id_bits must be >= capacity";
-    if (c->world > 1) {
-        if (c->world > 32 || c->rank >= c->world) return "need rank < world <= 32";
+    if (c->world > 1 || (c->flags & LAMPS_MERGE)) {
+        if (c->world > 32 || c->rank >= (c->world > 1 ? c->world : 1u)) return "need rank < world <= 32";
         if ((uint64_t)c->world * c->max_batch > kMergeMaxRecords) return "world * max_batch must be <= 8192";
         if (c->transport > LAMPS_XPORT_LOOPBACK) return "unknown transport";
         if (c->transport == LAMPS_XPORT_NCCL && !c->nccl_id) return "NCCL transport needs nccl_id";
+        if (c->world <= 1 && c->transport != LAMPS_XPORT_NCCL) return "LAMPS_MERGE at world 1 needs the NCCL transport";
     }
     return nullptr;
 }
+
+// the multi-shard path (records, all-gather, merge kernel): world > 1, or a
+// 1-rank NCCL communicator when LAMPS_MERGE is set (exercises the exchange on one GPU)
+bool merge_mode(const lamps_config& c) { return c.world > 1 || (c.flags & LAMPS_MERGE); }
 
 size_t carve(lamps_t* h, uint8_t* base) {
     // base == nullptr: size only
@@ -184,11 +190,12 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? L.take((size_t)cap_pad * 32) : 0;
     size_t o_trace = (h->cfg.flags & LAMPS_TRACE) ? L.take((size_t)gmax * kTraceSlots * 8) : 0;
     const uint32_t world = h->cfg.world > 1 ? h->cfg.world : 1;
-    size_t o_xs = world > 1 ? L.take(((size_t)mb + 1) * sizeof(MergeRec)) : 0;
-    size_t o_xr = world > 1 ? L.take((size_t)world * ((size_t)mb + 1) * sizeof(MergeRec)) : 0;
+    const bool merge = merge_mode(h->cfg);
+    size_t o_xs = merge ? L.take(((size_t)mb + 1) * sizeof(MergeRec)) : 0;
+    size_t o_xr = merge ? L.take((size_t)world * ((size_t)mb + 1) * sizeof(MergeRec)) : 0;
     if (!base) return L.off;
-    h->b.xsend = world > 1 ? reinterpret_cast<MergeRec*>(base + o_xs) : nullptr;
-    h->b.xrecv = world > 1 ? reinterpret_cast<MergeRec*>(base + o_xr) : nullptr;
+    h->b.xsend = merge ? reinterpret_cast<MergeRec*>(base + o_xs) : nullptr;
+    h->b.xrecv = merge ? reinterpret_cast<MergeRec*>(base + o_xr) : nullptr;
     uint32_t* soa[8];
     for (int i = 0; i < 8; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
     h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7], cap_pad};
@@ -323,7 +330,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.flags = (h->cfg.flags & LAMPS_FORCE_FALLBACK) ? kStepForceFallback : 0u;
     a.world = h->world;
     a.rank = h->rank;
-    if (h->world > 1) a.flags |= kStepMerge;
+    if (h->merge) a.flags |= kStepMerge;
     return a;
 }
 
@@ -354,7 +361,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
 
 // phase 2 (world > 1): exchange the top-K records, merge, admit this rank's share
 int enqueue_phase2(lamps_t* h, uint64_t kv_total, uint32_t n_ev, bool exchange) {
-    if (h->world > 1) {
+    if (h->merge) {
         const StepArgs a = make_args(h, kv_total, n_ev);
         if (exchange) {
             const size_t bytes = ((size_t)h->cfg.max_batch + 1) * sizeof(MergeRec);
@@ -469,7 +476,8 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     }
     h->world = cfg->world > 1 ? cfg->world : 1;
     h->rank = cfg->world > 1 ? cfg->rank : 0;
-    if (h->world > 1 && !h->fused) {
+    h->merge = merge_mode(*cfg);
+    if (h->merge && !h->fused) {
         delete h;
         return LAMPS_ENOTSUP;  // multi-GPU merge is implemented on the fused path
     }
@@ -501,7 +509,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
             if (cudaEventCreate(&e) != cudaSuccess) return cleanup(LAMPS_ECUDA, "event");
     }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "sync");
-    if (h->world > 1 && cfg->transport == LAMPS_XPORT_NCCL) {
+    if (h->merge && cfg->transport == LAMPS_XPORT_NCCL) {
         if (!g_nccl.load()) return cleanup(LAMPS_ENCCL, "libnccl.so.2 not loadable");
         NcclId id;
         std::memcpy(id.internal, cfg->nccl_id, sizeof(id.internal));

@@ -18,7 +18,7 @@ LAMPS_OK, LAMPS_EINVAL, LAMPS_ENOSPC, LAMPS_ENOENT, LAMPS_ENOTSUP, LAMPS_ECUDA, 
 LAMPS_FREE, LAMPS_READY, LAMPS_PAUSED_P, LAMPS_PAUSED_D, LAMPS_PAUSED_S = 0, 1, 2, 3, 4
 LAMPS_PRESERVE, LAMPS_DISCARD, LAMPS_SWAP, LAMPS_NONE = 0, 1, 2, 3
 LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
-LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE = 1, 2, 4, 8, 16
+LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE, LAMPS_MERGE = 1, 2, 4, 8, 16, 32
 LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK = 0, 1
 
 u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p

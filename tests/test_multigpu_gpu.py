@@ -71,3 +71,34 @@ def test_loopback_merge_tight_budget_and_small_k():
 def test_loopback_merge_empty_shard():
     # a union of 3 requests over 4 shards: one shard has nothing
     run("C1", 4, 16, 3, 292, max_batch=16)
+
+
+def test_nccl_one_rank_merge_path():
+    """LAMPS_MERGE at world 1: the NCCL exchange (dlopen'd libnccl, a 1-rank
+    communicator, ncclAllGather) + merge kernel, stepped with events, against the oracle."""
+    import torch
+    from paper_2410_18248_b200 import LAMPS_MERGE, Scheduler
+    cfg = gen.lib_config("C2")
+    snap = gen.snapshot("C2", seed=3, id_base=77)
+    s = Scheduler(cfg, flags=LAMPS_MERGE, world=1, rank=0, nccl_id=Scheduler.nccl_unique_id(),
+                  stream=torch.cuda.current_stream())
+    s.import_pool(snap, snap["id_base"], snap["next_id"])
+    o = O.OraclePool(cfg)
+    o.load(snap, snap["next_id"])
+    kv = gen.CONFIGS["C2"]["kv_total"]
+    prev = np.zeros(0, np.int64)
+    from paper_2410_18248_b200.lamps import EVENT_DTYPE
+    for t in range(4):
+        ev = np.zeros(min(3, len(prev)), EVENT_DTYPE)
+        for j in range(len(ev)):
+            ev[j]["id"], ev[j]["kind"] = prev[j], 2 if j == 0 else 1
+        g = s.step(ev, kv)
+        oev = np.zeros(len(ev), O.EVENT_DTYPE)
+        oev["id"], oev["kind"] = ev["id"], ev["kind"]
+        ro = o.step(oev, kv_total=kv)
+        assert list(g["admitted_id"]) == list(ro["admitted_id"]), t
+        assert list(g["preempted_id"]) == list(ro["preempted_id"]), t
+        assert g["budget"] == ro["budget"] and g["budget_used"] == ro["budget_used"], t
+        prev = np.asarray(g["admitted_id"], np.int64)
+    assert s.stats()[0] == 2 + 1  # events + fused + merge
+    s.close()
