@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--merge", action="store_true",
+                    help="N=1: run the multi-shard exchange + merge over a 1-rank NCCL communicator")
     return ap.parse_args()
 
 
@@ -191,12 +193,16 @@ def run_ours(args, rank, world, local):
     snap = gen.snapshot(cname, seed=rank, id_base=id_base)
     stream = torch.cuda.current_stream()
 
-    nccl_id = None
+    nccl_id, mflags = None, 0
     if world > 1:  # one NCCL all-gather per step for the global admission merge
         obj = [Scheduler.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    s = Scheduler(cfg, stream=stream, world=world, rank=rank, nccl_id=nccl_id)
+    elif args.merge:
+        from paper_2410_18248_b200 import LAMPS_MERGE
+        nccl_id, mflags = Scheduler.nccl_unique_id(), LAMPS_MERGE
+    merged = world > 1 or args.merge
+    s = Scheduler(cfg, flags=mflags, stream=stream, world=world, rank=rank, nccl_id=nccl_id)
     s.import_pool(snap, snap["id_base"], snap["next_id"])
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device="cuda")
@@ -231,7 +237,7 @@ def run_ours(args, rank, world, local):
     res = s.result()
     n_elig = res["n_eligible"]
     kernels, passes = s.stats()
-    fused = kernels == (1 if world == 1 else 2)
+    fused = kernels == (2 if merged else 1)
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     ne_t = torch.tensor([float(n_elig)], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -244,7 +250,7 @@ def run_ours(args, rank, world, local):
     # the fused kernel's per-phase SM-clock trace)
     from paper_2410_18248_b200 import LAMPS_TRACE
     phase, trace_us, sp_passes = None, None, passes
-    sp = Scheduler(cfg, flags=LAMPS_TIMING | LAMPS_TRACE, stream=stream) if world == 1 else None
+    sp = Scheduler(cfg, flags=LAMPS_TIMING | LAMPS_TRACE, stream=stream) if not merged else None
     if sp is not None:
       sp.import_pool(snap, snap["id_base"], snap["next_id"])
       for _ in range(args.warmup):
@@ -357,12 +363,14 @@ def run_ours(args, rank, world, local):
                        "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
                        "l2": "flushed before every timed step (256 MiB write)",
                        "parallelism": (f"{world} shards x 1M, one NCCL all-gather of the top-{cfg['max_batch']} "
-                                       f"per step for the global admission") if world > 1 else "1 shard"},
+                                       f"per step for the global admission") if world > 1 else
+                                      ("1 shard, exchange + merge over a 1-rank NCCL communicator" if merged
+                                       else "1 shard")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak if ach else None, "traffic": traffic,
                          "peak_source": peak_src},
             "kernels": kernels_tbl,
-            "path": "fused cooperative step kernel" if fused else "3-kernel path",
+            "path": ("fused cooperative step kernel" + (" + NCCL all-gather + merge kernel" if merged else "")) if fused else "3-kernel path",
             "sort_passes": passes,
             "gpu_launches": kernels * args.steps,
             "clocks": clk.summary(),
