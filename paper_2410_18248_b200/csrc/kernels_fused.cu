@@ -647,6 +647,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             ns = tot;
         }
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
+        if (tr && tid == 0) { tr[30] = rn; tr[31] = ns; }
         // buckets [0, half) hold the starving keys
         local_sort(sm.l, sm.l.a, sm.l.b, ns, T, j_lo, min(j_hi, half), tr ? tr + 16 : nullptr);
         local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr);

@@ -53,3 +53,10 @@ if os.environ.get("TRACE"):
         nb = t[:, :, base + 5]
         print(f"  L.{part}.big groups   max {int(nb.max())} mean {nb.mean():.2f}")
     ms, nst = st.timing() if False else (None, None)
+    if os.environ.get("PERCTA"):
+        t0 = acc[-1]
+        print("cta  keys  starving  Lsort_us  Lstarv_refine  Lnon_refine  big_s big_n  end_us")
+        for cta in range(t0.shape[0]):
+            r = t0[cta]
+            print(f"{cta:3d} {r[30]:6d} {r[31]:6d} {(r[14]-r[13])/1965:8.2f} {(r[19]-r[18])/1965 if r[18] else 0:8.2f} "
+                  f"{(r[27]-r[26])/1965 if r[26] else 0:8.2f} {r[21]:5d} {r[29]:5d} {(r[8]-t0[:,0].min())/1965:8.2f}")
