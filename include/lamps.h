@@ -263,10 +263,12 @@ int lamps_timing_read(lamps_t* h, double ms[4], uint32_t* n_steps);
 
 /*
  * With LAMPS_TRACE on the fused path: the SM clock (clock64) of every CTA at
- * the phase boundaries of the last step, out[cta * 32 + k], k = 0 start,
+ * the phase boundaries of the last step, out[cta * 64 + k], k = 0 start,
  * 1 scored, 2 counts published, 3 after barrier 1, 4 count exchange done,
  * 5 after barrier 2, 6 scattered, 7 after barrier 3, 8 range sorted,
- * 9 admission done (CTA 0), 10..15 sub-phases, 16..31 range-sort sub-phases.
+ * 9 admission done (CTA 0), 10..15 sub-phases, 16..31 range-sort sub-phases,
+ * 30/31 range size / starving keys, 32..63 refinement levels of the
+ * non-starving part (diagnostics; layout may change).
  * *n_cta receives the grid size.
  */
 int lamps_trace_read(lamps_t* h, uint64_t* out, uint32_t max_words, uint32_t* n_cta);

@@ -200,7 +200,7 @@ __device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint
 // if the group tables overflow) the stable LSD finishes the part.
 __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
                                            const uint32_t* T, uint32_t j0, uint32_t j1,
-                                           unsigned long long* tr) {
+                                           unsigned long long* tr, unsigned long long* xtr = nullptr) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     if (n <= 1) return;
@@ -246,6 +246,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
     uint32_t cur = 0;
     for (int level = 0; !full_lsd && level < kMaxLevels; level++) {
         const uint32_t ng = sm.ngl[cur];
+        if (xtr && tid == 0) { xtr[2 * level] = clock64(); xtr[2 * level + 1] = ng; }
         if (ng == 0) break;
         if (ng > (uint32_t)kMaxBig) { full_lsd = true; break; }
         const uint32_t nxt = cur ^ 1u;
@@ -296,6 +297,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             }
             const uint32_t f0 = sm.gcum[gb];
             __syncthreads();
+            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[16] = clock64();
             if (warp == 0) {  // digit shift / bits, counter bases; cut the batch at kSubBuckets
                 uint32_t base = 0, cut = ge;
                 for (uint32_t g0 = gb; g0 < ge; g0 += 32) {
@@ -335,7 +337,9 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
                 atomicAdd(&sm.pos[GDIGIT(A[sm.gl_lo[cur][g] + (f - sm.gcum[g])], g)], 1u);
             }
             __syncthreads();
+            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[17] = clock64();
             (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, ncnt, sm.w32);
+            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[18] = clock64();
             // group g's keys occupy [gcum_g - f0, gcum_g - f0 + m_g) of the batch's scan space
             for (uint32_t f = f0 + tid; f < fc; f += kFT) {
                 const uint32_t g = group_of(f, gb, gcut);
@@ -344,6 +348,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
                 Bf[lo_g + atomicAdd(&sm.pos[GDIGIT(k, g)], 1u) - gz] = k;
             }
             __syncthreads();
+            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[19] = clock64();
             for (uint32_t f = f0 + tid; f < fc; f += kFT) {  // finish small sub-groups, list big ones
                 const uint32_t g = group_of(f, gb, gcut);
                 const uint32_t lo_g = sm.gl_lo[cur][g], gz = sm.gcum[g] - f0;
@@ -372,12 +377,14 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             }
 #undef GDIGIT
             __syncthreads();
+            if (xtr && tid == 0 && level == 0 && gb == 0) { xtr[20] = clock64(); xtr[21] = gcut; xtr[22] = fc - f0; }
             gb = gcut;
         }
         cur = nxt;
         if (level + 1 == kMaxLevels && sm.ngl[cur]) full_lsd = true;
     }
     LTRACE(3);
+    if (xtr && tid == 0) xtr[14] = clock64();
     if (full_lsd) {  // pathological distributions: stable LSD of the whole part
         unsigned long long o, an;
         block_or_and(sm, A, n, o, an);
@@ -647,10 +654,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             ns = tot;
         }
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
-        if (tr && tid == 0) { tr[30] = rn; tr[31] = ns; }
+        if (tr && tid == 0) {
+            tr[30] = rn; tr[31] = ns;
+            for (int q = 32; q < 64; q++) tr[q] = 0;
+        }
         // buckets [0, half) hold the starving keys
         local_sort(sm.l, sm.l.a, sm.l.b, ns, T, j_lo, min(j_hi, half), tr ? tr + 16 : nullptr);
-        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr);
+        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr,
+                   tr ? tr + 32 : nullptr);
         TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;

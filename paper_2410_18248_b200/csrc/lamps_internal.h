@@ -35,7 +35,7 @@ struct MergeRec {
     unsigned long long pad;
 };
 static_assert(sizeof(MergeHdr) == 32 && sizeof(MergeRec) == 32, "exchange records are 32 B");
-constexpr int kTraceSlots = 32;
+constexpr int kTraceSlots = 64;
 constexpr uint32_t kBarPerStep = 64;  // grid-barrier values reserved per step
 
 // Device control block: per-step counters, the sort plan and the step summary.

@@ -280,10 +280,10 @@ class Scheduler:
 
     def trace(self):
         """Per-CTA SM clocks at the fused kernel's phase boundaries (LAMPS_TRACE)."""
-        out = np.zeros(512 * 32, np.uint64)
+        out = np.zeros(512 * 64, np.uint64)
         n = u32(0)
         self._check(lib().lamps_trace_read(self.h, _p(out), len(out), ctypes.byref(n)))
-        return out[:n.value * 32].reshape(n.value, 32)
+        return out[:n.value * 64].reshape(n.value, 64)
 
     def timing(self):
         ms = (dbl * 4)()

@@ -60,3 +60,19 @@ if os.environ.get("TRACE"):
             r = t0[cta]
             print(f"{cta:3d} {r[30]:6d} {r[31]:6d} {(r[14]-r[13])/1965:8.2f} {(r[19]-r[18])/1965 if r[18] else 0:8.2f} "
                   f"{(r[27]-r[26])/1965 if r[26] else 0:8.2f} {r[21]:5d} {r[29]:5d} {(r[8]-t0[:,0].min())/1965:8.2f}")
+    if os.environ.get("LEVELS"):
+        t0 = acc[-1]
+        print("cta  keys  per-level (us, groups) of the non-starving part; level-0 substeps or/and,count,scan,scatter,final")
+        for cta in range(t0.shape[0]):
+            r = t0[cta, 32:]
+            lv = []
+            for k in range(7):
+                if r[2 * k] == 0:
+                    break
+                nxt = r[2 * k + 2] if k < 6 and r[2 * k + 2] else r[14]
+                lv.append(f"L{k}:{(nxt - r[2*k]) / 1965:.2f}us/{r[2*k+1]}g")
+            ss = ""
+            if r[16]:
+                b = [r[0], r[16], r[17], r[18], r[19], r[20]]
+                ss = " sub " + ",".join(f"{(b[i+1]-b[i]) / 1965:.2f}" for i in range(5)) + f" cut {r[21]} keys {r[22]}"
+            print(f"{cta:3d} {t0[cta,30]:6d} " + " ".join(lv) + ss)
