@@ -187,63 +187,18 @@ __device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint
     __syncthreads();
 }
 
-// Sort of the n keys at A[0..n) of one part of a range (same starving flag) in
-// shared memory; result in A, Bf is scratch.  The part arrives in global-bucket
-// order and its buckets [j0, j1) are known, so the buckets are the first-level
-// groups (sizes = the global totals T[j]; a bucket lies entirely in one range).
-// Groups of <= kMaxRankM keys are finished by rank-by-comparison (keys are
-// unique).  Bigger groups are refined in flat passes over all their keys: per
-// group a digit of its own top varying bits (db = ceil(log2 size) bits, from the
-// group's OR/AND), counted with shared-memory atomics into a counter block of
-// its own; one scan over the blocks of a batch gives positions; sub-groups
-// still bigger than kMaxRankM go to the next pass.  After kMaxLevels passes (or
-// if the group tables overflow) the stable LSD finishes the part.
-__device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
-                                           const uint32_t* T, uint32_t j0, uint32_t j1,
-                                           unsigned long long* tr, unsigned long long* xtr = nullptr) {
-#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
+// Refinement of the groups listed in sm.gl_lo[0] / gl_n[0] (sm.ngl[0] of them; keys
+// at A[lo, lo+n), Bf scratch at the same offsets) until every group is <= kMaxRankM
+// keys and ranked.  Each pass: per group a digit of its own top varying bits (db =
+// ceil(log2 size) bits, from the group's OR/AND), counted with shared-memory atomics
+// into a counter block of its own; one scan over the blocks of a batch gives
+// positions; sub-groups still bigger than kMaxRankM go to the next pass.  Returns
+// true if the lists overflowed or kMaxLevels passes did not finish (the caller
+// then sorts the whole part by LSD).
+__device__ __forceinline__ bool refine_groups(PhaseL& sm, uint64_t* A, uint64_t* Bf, unsigned long long* xtr) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    if (n <= 1) return;
-    LTRACE(0);
-    bool full_lsd = false;
-    // ---- level 1: bucket runs.  pos[0..nb] = starts of the part's buckets.
-    const uint32_t nb = j1 - j0;
-    if (nb + 1 > (uint32_t)kSubBuckets) {
-        full_lsd = true;
-    } else {
-        for (uint32_t j = tid; j < nb; j += kFT) sm.pos[j] = __ldcg(&T[j0 + j]);
-        if (tid == 0) { sm.ngl[0] = 0; sm.ngl[1] = 0; }
-        for (uint32_t i = tid; i < n; i += kFT) Bf[i] = A[i];
-        __syncthreads();
-        (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, nb, sm.w32);
-        if (tid == 0) sm.pos[nb] = n;
-        __syncthreads();
-        LTRACE(1);
-        for (uint32_t i = tid; i < n; i += kFT) {
-            uint32_t lo_ = 0, hi_ = nb;  // last bucket with start <= i
-            while (hi_ - lo_ > 1) {
-                const uint32_t mid = (lo_ + hi_) >> 1;
-                if (sm.pos[mid] <= i) lo_ = mid; else hi_ = mid;
-            }
-            const uint32_t st = sm.pos[lo_], e = sm.pos[lo_ + 1], m = e - st;
-            const uint64_t k = Bf[i];
-            if (m > kMaxRankM) {
-                if (i == st) {
-                    const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
-                    if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m; }
-                }
-                continue;  // A[i] == k already
-            }
-            uint32_t r = 0;
-#pragma unroll 8
-            for (uint32_t q = st; q < e; q++) r += Bf[q] < k ? 1u : 0u;
-            A[st + r] = k;
-        }
-        __syncthreads();
-        LTRACE(2);
-    }
-    // ---- refinement passes over the big groups
     uint32_t cur = 0;
+    bool full_lsd = false;
     for (int level = 0; !full_lsd && level < kMaxLevels; level++) {
         const uint32_t ng = sm.ngl[cur];
         if (xtr && tid == 0) { xtr[2 * level] = clock64(); xtr[2 * level + 1] = ng; }
@@ -338,7 +293,7 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
             }
             __syncthreads();
             if (xtr && tid == 0 && level == 0 && gb == 0) xtr[17] = clock64();
-            (void)smem_excl_scan<kFT, kSubBuckets / kFT>(sm.pos, ncnt, sm.w32);
+            (void)smem_excl_scan<kFT, kSubBuckets / kFT + 1>(sm.pos, ncnt, sm.w32);
             if (xtr && tid == 0 && level == 0 && gb == 0) xtr[18] = clock64();
             // group g's keys occupy [gcum_g - f0, gcum_g - f0 + m_g) of the batch's scan space
             for (uint32_t f = f0 + tid; f < fc; f += kFT) {
@@ -383,6 +338,66 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
         cur = nxt;
         if (level + 1 == kMaxLevels && sm.ngl[cur]) full_lsd = true;
     }
+    return full_lsd;
+}
+
+// Sort of the n keys at A[0..n) of one part of a range (same starving flag) in
+// shared memory; result in A, Bf is scratch.  The part arrives in global-bucket
+// order and its buckets [j0, j1) are known, so the buckets are the first-level
+// groups (sizes = the global totals T[j]; a bucket lies entirely in one range).
+// Groups of <= kMaxRankM keys are finished by rank-by-comparison (keys are
+// unique).  Bigger groups are refined in flat passes over all their keys: per
+// group a digit of its own top varying bits (db = ceil(log2 size) bits, from the
+// group's OR/AND), counted with shared-memory atomics into a counter block of
+// its own; one scan over the blocks of a batch gives positions; sub-groups
+// still bigger than kMaxRankM go to the next pass.  After kMaxLevels passes (or
+// if the group tables overflow) the stable LSD finishes the part.
+__device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
+                                           const uint32_t* T, uint32_t j0, uint32_t j1,
+                                           unsigned long long* tr, unsigned long long* xtr = nullptr) {
+#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
+    const uint32_t tid = threadIdx.x;
+    if (n <= 1) return;
+    LTRACE(0);
+    bool full_lsd = false;
+    // ---- level 1: bucket runs.  pos[0..nb] = starts of the part's buckets.
+    const uint32_t nb = j1 - j0;
+    if (nb + 1 > (uint32_t)kSubBuckets) {
+        full_lsd = true;
+    } else {
+        for (uint32_t j = tid; j < nb; j += kFT) sm.pos[j] = __ldcg(&T[j0 + j]);
+        if (tid == 0) { sm.ngl[0] = 0; sm.ngl[1] = 0; }
+        for (uint32_t i = tid; i < n; i += kFT) Bf[i] = A[i];
+        __syncthreads();
+        (void)smem_excl_scan<kFT, kSubBuckets / kFT + 1>(sm.pos, nb, sm.w32);
+        if (tid == 0) sm.pos[nb] = n;
+        __syncthreads();
+        LTRACE(1);
+        for (uint32_t i = tid; i < n; i += kFT) {
+            uint32_t lo_ = 0, hi_ = nb;  // last bucket with start <= i
+            while (hi_ - lo_ > 1) {
+                const uint32_t mid = (lo_ + hi_) >> 1;
+                if (sm.pos[mid] <= i) lo_ = mid; else hi_ = mid;
+            }
+            const uint32_t st = sm.pos[lo_], e = sm.pos[lo_ + 1], m = e - st;
+            const uint64_t k = Bf[i];
+            if (m > kMaxRankM) {
+                if (i == st) {
+                    const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
+                    if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m; }
+                }
+                continue;  // A[i] == k already
+            }
+            uint32_t r = 0;
+#pragma unroll 8
+            for (uint32_t q = st; q < e; q++) r += Bf[q] < k ? 1u : 0u;
+            A[st + r] = k;
+        }
+        __syncthreads();
+        LTRACE(2);
+    }
+    // ---- refinement passes over the big groups
+    if (!full_lsd) full_lsd = refine_groups(sm, A, Bf, xtr);
     LTRACE(3);
     if (xtr && tid == 0) xtr[14] = clock64();
     if (full_lsd) {  // pathological distributions: stable LSD of the whole part
@@ -394,6 +409,135 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
         __syncthreads();
     }
     if (tr && tid == 0) tr[5] = full_lsd ? 1000u : sm.ngl[0];
+    LTRACE(4);
+#undef LTRACE
+}
+
+// Digit of key k inside its bucket J: the top db bits of the bits below those the
+// bucket fixes.  A bucket with exponent e > kBucketM fixes the score's top
+// kBucketM + 1 bits, so the varying part is (low e-1-kBucketM score bits, id
+// offset); an exact bucket (score < 2^kBucketM) varies only in the id offset.  The
+// id offset (id - id_base, the key's low bits) is < cap = 2^lg_cap, so it is packed
+// into lg_cap bits (not IB) and its top bits carry information.  Monotone in the key
+// within a bucket, so (bucket, digit) order is key order.
+__device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t db, const Cost& c,
+                                              uint32_t half, uint32_t lg_cap) {
+    const uint32_t fb = J >= half ? J - half : J;
+    const uint64_t idoff = k & (uint64_t)c.cap_mask;
+    uint64_t v = idoff;
+    uint32_t wv = lg_cap;
+    if (fb >= (1u << kBucketM)) {
+        const uint32_t ls = (fb >> kBucketM) - 1u;  // e - 1 - kBucketM, e = (fb >> kBucketM) + kBucketM
+        v |= ((k >> c.IB) & ((1ull << ls) - 1ull)) << lg_cap;
+        wv += ls;
+    }
+    return wv >= db ? (uint32_t)(v >> (wv - db)) : (uint32_t)(v << (db - wv));
+}
+
+// Sort of a CTA's key range (rn <= kKcap keys in global src, buckets [j_lo, j_hi),
+// j_hi - j_lo < kSubBuckets) into sm.a.  Keys stay in registers (<= kLocalItems per
+// thread).  One counting pass: each bucket of m keys gets 2^ceil(log2 m) counters
+// (the bucket's exact size is the global total T[j]: a bucket lies entirely in one
+// range) indexed by sub_digit, so the sub-buckets hold ~1 key; keys of sub-buckets
+// of <= kMaxRankM keys are ranked by comparison, bigger ones (many near-equal keys)
+// go to refine_groups, and an LSD of the whole range is the last resort.
+__device__ __forceinline__ void range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
+                                           const uint32_t* T, uint32_t j_lo, uint32_t j_hi, const Cost& c,
+                                           uint32_t half, unsigned long long* tr) {
+#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
+    const uint32_t tid = threadIdx.x;
+    const uint32_t nb = j_hi - j_lo;
+    const uint32_t lg_cap = 31u - (uint32_t)__clz(c.cap);
+    uint32_t* P = sm.pos;                                  // per bucket: start | counter base << 14
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);     // <= 2 * kKcap counters
+    uint64_t* A = sm.a;
+    LTRACE(0);
+    uint64_t k[kLocalItems];
+#pragma unroll
+    for (int u = 0; u < kLocalItems; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        k[u] = i < rn ? __ldcg(src + i) : 0ull;
+    }
+    for (uint32_t j = tid; j < nb; j += kFT) {
+        const uint32_t m = __ldcg(&T[j_lo + j]);
+        const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
+        P[j] = m | ((1u << db) << 14);
+    }
+    if (tid == 0) sm.ngl[0] = 0;
+    __syncthreads();
+    const uint32_t ptot = smem_excl_scan<kFT, kSubBuckets / kFT + 1>(P, nb, sm.w32);
+    const uint32_t ncnt = ptot >> 14;
+    if (tid == 0) P[nb] = ptot;
+    for (uint32_t i = tid; i < ncnt; i += kFT) cnt[i] = 0;
+    __syncthreads();
+    LTRACE(1);
+    uint32_t it[kLocalItems];  // counter index | order within the sub-bucket << 15
+#pragma unroll
+    for (int u = 0; u < kLocalItems; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        it[u] = 0;
+        if (i < rn) {
+            const uint32_t J = bucket_of(k[u], c, half);
+            const uint32_t p0 = P[J - j_lo], p1 = P[J - j_lo + 1];
+            const uint32_t m = (p1 & 0x3fffu) - (p0 & 0x3fffu);
+            const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
+            const uint32_t idx = (p0 >> 14) + sub_digit(k[u], J, db, c, half, lg_cap);
+            it[u] = idx | (atomicAdd(&cnt[idx], 1u) << 15);
+        }
+    }
+    __syncthreads();
+    (void)smem_excl_scan<kFT, 2 * kKcap / kFT + 1>(cnt, ncnt, sm.w32);
+    LTRACE(2);
+    // initial placement: sub-bucket start + arrival order; keep (start, size)
+#pragma unroll
+    for (int u = 0; u < kLocalItems; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        if (i < rn) {
+            const uint32_t idx = it[u] & 0x7fffu;
+            const uint32_t st = cnt[idx], e = idx + 1u < ncnt ? cnt[idx + 1] : rn;
+            A[st + (it[u] >> 15)] = k[u];
+            it[u] = st | ((e - st) << 14);
+        }
+    }
+    __syncthreads();
+    // rank inside sub-buckets of <= kMaxRankM keys; list the bigger ones
+#pragma unroll
+    for (int u = 0; u < kLocalItems; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        if (i < rn) {
+            const uint32_t st = it[u] & 0x3fffu, m2 = it[u] >> 14;
+            if (m2 <= kMaxRankM) {
+                uint32_t r = 0;
+                for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k[u] ? 1u : 0u;
+                it[u] = (st + r) | 0x80000000u;
+            } else {
+                it[u] = 0;
+                if (A[st] == k[u]) {
+                    const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
+                    if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m2; }
+                }
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kLocalItems; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        if (i < rn && (it[u] >> 31)) A[it[u] & 0x7fffffffu] = k[u];
+    }
+    __syncthreads();
+    LTRACE(3);
+    bool full_lsd = false;
+    if (sm.ngl[0]) full_lsd = refine_groups(sm, A, sm.b, nullptr);
+    if (full_lsd) {
+        unsigned long long o, an;
+        block_or_and(sm, A, rn, o, an);
+        const uint64_t* r = local_lsd(sm, A, sm.b, rn, o ^ an);
+        if (r != A)
+            for (uint32_t i = tid; i < rn; i += kFT) A[i] = r[i];
+        __syncthreads();
+    }
+    if (tr && tid == 0) { tr[5] = full_lsd ? 1000u : sm.ngl[0]; }
     LTRACE(4);
 #undef LTRACE
 }
@@ -641,27 +785,31 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     uint32_t final_buf, passes;
     if (!fallback) {
         const uint32_t rn = r_hi - r_lo;
-        for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
-        TRACE(13);
-        // starving keys come first; sort the two parts separately (each with the bits that
-        // vary inside it), so the starving flag does not take the MSD digit
-        const uint32_t key_top = c.SB + c.IB;
-        uint32_t ns = 0;
-        for (uint32_t i = tid; i < rn; i += kFT) ns += ((sm.l.a[i] >> key_top) & 1ull) ? 0u : 1u;
-        {
-            uint32_t tot;
-            (void)block_excl_scan_u32<kFT>(ns, sm.l.w32, &tot);
-            ns = tot;
-        }
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
         if (tr && tid == 0) {
-            tr[30] = rn; tr[31] = ns;
+            tr[30] = rn; tr[31] = j_hi - j_lo;
             for (int q = 32; q < 64; q++) tr[q] = 0;
         }
-        // buckets [0, half) hold the starving keys
-        local_sort(sm.l, sm.l.a, sm.l.b, ns, T, j_lo, min(j_hi, half), tr ? tr + 16 : nullptr);
-        local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr,
-                   tr ? tr + 32 : nullptr);
+        if (j_hi - j_lo < (uint32_t)kSubBuckets) {
+            TRACE(13);
+            range_sort(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half, tr ? tr + 16 : nullptr);
+        } else {  // a sparse range over very many buckets: sort the two parts by bucket runs
+            for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
+            TRACE(13);
+            // starving keys come first; sort the two parts separately (buckets [0, half)
+            // hold the starving keys)
+            const uint32_t key_top = c.SB + c.IB;
+            uint32_t ns = 0;
+            for (uint32_t i = tid; i < rn; i += kFT) ns += ((sm.l.a[i] >> key_top) & 1ull) ? 0u : 1u;
+            {
+                uint32_t tot;
+                (void)block_excl_scan_u32<kFT>(ns, sm.l.w32, &tot);
+                ns = tot;
+            }
+            local_sort(sm.l, sm.l.a, sm.l.b, ns, T, j_lo, min(j_hi, half), tr ? tr + 16 : nullptr);
+            local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr,
+                       tr ? tr + 32 : nullptr);
+        }
         TRACE(14);
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;

@@ -70,39 +70,32 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
     return before + x - v;
 }
 
-// Exclusive scan of arr[0..L) in shared memory by all NT threads, L <= R*32*NT/32.
-// Warp w owns the contiguous chunk [w*R*32, (w+1)*R*32), lane-strided (no bank
-// conflicts); its R rounds are scanned in parallel (ILP) instead of one after the
-// other.  Returns the total; `add` (optional) receives arr[j] + exclusive(j).
+// Exclusive scan of arr[0..L) in shared memory by all NT threads, L <= R*NT.
+// Raking: thread t owns the R consecutive words [t*R, t*R+R) (R odd => the lanes
+// of a warp hit distinct banks), sums them serially, one warp scan of the thread
+// sums, one scan of the warp sums, then rewrites its words.  ~2R shared-memory
+// accesses + 10 shuffles per thread.  Returns the total; `add` (optional)
+// receives arr[j] + exclusive(j).
 template <int NT, int R>
 __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, uint32_t* w32,
                                                    uint32_t* add = nullptr) {
     constexpr int NW = NT / 32;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t j0 = warp * (uint32_t)(R * 32);
-    uint32_t v[R], x[R];
+    const uint32_t j0 = threadIdx.x * (uint32_t)R;
+    uint32_t v[R];
+    uint32_t s = 0;
 #pragma unroll
     for (int r = 0; r < R; r++) {
-        const uint32_t j = j0 + r * 32 + lane;
-        v[r] = j < L ? arr[j] : 0u;
-        x[r] = v[r];
+        v[r] = j0 + r < L ? arr[j0 + r] : 0u;
+        s += v[r];
     }
+    uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x[r], o);
-            if (lane >= (uint32_t)o) x[r] += y;
-        }
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
     }
-    uint32_t carry = 0;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const uint32_t t = __shfl_sync(0xffffffffu, x[r], 31);
-        x[r] = carry + x[r] - v[r];
-        carry += t;
-    }
-    if (lane == 0) w32[warp] = carry;
+    if (lane == 31) w32[warp] = x;
     __syncthreads();
     if (warp == 0) {
         const uint32_t t = lane < (uint32_t)NW ? w32[lane] : 0u;
@@ -116,14 +109,15 @@ __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, ui
         if (lane == NW - 1) w32[NW] = y;
     }
     __syncthreads();
-    const uint32_t off = w32[warp], total = w32[NW];
+    uint32_t run = w32[warp] + x - s;
+    const uint32_t total = w32[NW];
 #pragma unroll
     for (int r = 0; r < R; r++) {
-        const uint32_t j = j0 + r * 32 + lane;
-        if (j < L) {
-            arr[j] = x[r] + off;
-            if (add) add[j] += x[r] + off;
+        if (j0 + r < L) {
+            arr[j0 + r] = run;
+            if (add) add[j0 + r] += run;
         }
+        run += v[r];
     }
     __syncthreads();
     return total;
