@@ -3,23 +3,21 @@
 // share of keys fits in shared memory (capacity <= #SM * kKcap).
 //
 //   S  score: each CTA scores its contiguous range of slots (A0 fused, A1, A2,
-//      A3, key) and keeps its keys in shared memory
-//   H  bucket histogram of its keys; the bucket is an exact monotone function
-//      of the key, (starving, bit length of the score, next kBucketM score
-//      bits) -- "float-like" buckets adapt to the dynamic range of the scores
+//      A3, key) and keeps its keys in shared memory, with a histogram over
+//      "float-like" buckets of the key, (starving, bit length of the score, next
+//      kBucketM score bits): an exact monotone function of the key
+//   H  the CTA adds its bucket counts to the step's global totals with atomics;
+//      the returned old values are its offsets inside the buckets
 //   -- barrier --
-//   T  transposed count exchange: CTA c scans buckets j = c (mod G) over all
-//      CTAs (exclusive prefix per CTA, total per bucket)
-//   -- barrier --
-//   X  bucket bases (scan of the totals) and scatter of the keys into bucket
+//   X  bucket starts (scan of the totals) and scatter of the keys into bucket
 //      order in global memory; every CTA derives the bucket-aligned key range
 //      it will sort
 //   -- barrier --
-//   L  each CTA loads its range (<= kKcap keys) into shared memory and LSD
-//      radix-sorts it there (8-bit digits over the bits that vary within the
-//      range, stable warp multisplit); writes the final ranked keys.  If any
-//      range exceeds kKcap (a huge bucket of near-equal scores) every CTA runs
-//      the grid-synchronous global LSD sort instead (sort_dev.cuh).
+//   L  each CTA sorts its range (<= kKcap keys) on chip: keys in registers, one
+//      counting pass by a per-bucket digit, rank-by-comparison inside the
+//      sub-buckets (range_sort).  If any range exceeds kKcap (a huge bucket of
+//      near-equal scores) every CTA runs the grid-synchronous global LSD sort
+//      instead (sort_dev.cuh).
 //   A  CTA 0 admits (A5) as soon as the head of the order it needs is sorted.
 #include "sort_dev.cuh"
 #include "step_dev.cuh"
@@ -556,8 +554,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const uint32_t G = gridDim.x, bid = blockIdx.x;
     const uint32_t half = (c.SB <= (uint32_t)kBucketM) ? (1u << c.SB) : ((c.SB - kBucketM + 1u) << kBucketM);
     const uint32_t NB = 2u * half;
-    uint32_t* H = b.blocksum;  // [G][NB] bucket counts -> exclusive prefix over CTAs
-    uint32_t* T = b.blocksum + (size_t)G * NB;  // [NB] bucket totals
+    uint32_t* T = b.btot + (a.parity ? kMaxBuckets : 0);  // [NB] bucket totals of this step
+    {   // the other parity's totals are zeroed for the next step
+        uint32_t* Tn = b.btot + (a.parity ? 0 : kMaxBuckets);
+        for (uint32_t j = bid * kFT + tid; j < NB; j += G * kFT) Tn[j] = 0;
+    }
 
     TRACE(0);
     // ---------------- S: score this CTA's slots, keys into shared memory.  The seven SoA
@@ -657,83 +658,49 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         b.kmask[G + bid] = n;
     }
     TRACE(1);
-    // ---------------- H: publish this CTA's bucket counts
-    for (uint32_t j = tid; j < NB; j += kFT) H[(size_t)bid * NB + j] = sm.s.cnt[j];
+    // ---------------- H: add this CTA's bucket counts to the totals; the returned old
+    // value is this CTA's offset inside the bucket (the CTAs' order inside a bucket is
+    // free: the range sort orders every bucket completely)
+    {
+        constexpr int kU = 8;
+        for (uint32_t j0 = 0; j0 < NB; j0 += kU * kFT) {
+            uint32_t v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const uint32_t j = j0 + (uint32_t)u * kFT + tid;
+                v[u] = j < NB ? sm.s.cnt[j] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; u++)
+                if (v[u]) v[u] = atomicAdd(&T[j0 + (uint32_t)u * kFT + tid], v[u]);
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const uint32_t j = j0 + (uint32_t)u * kFT + tid;
+                if (j < NB) sm.s.cnt[j] = v[u];
+            }
+        }
+    }
     TRACE(2);
     uint32_t bar = a.step * kBarPerStep;
     grid_barrier(b.flags, G, ++bar);
     TRACE(3);
-
-    // ---------------- T: CTA bid owns buckets [jb0, jb1): it loads that column block of
-    // the count matrix (coalesced row segments) into shared memory, scans each column
-    // down the CTAs (exclusive prefix per CTA, total per bucket) and writes it back.
-    {
-        const uint32_t jb0 = (NB * bid) / G, jb1 = (NB * (bid + 1)) / G;
-        const uint32_t w = jb1 - jb0;
-        uint32_t* tile = sm.s.cnt;  // G x w (the bucket counts are already published)
-        const uint32_t nt = G * w;
-        for (uint32_t q0 = 0; q0 < nt; q0 += 8 * kFT) {  // 8 loads in flight per thread
-            uint32_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint32_t q = q0 + (uint32_t)u * kFT + tid;
-                v[u] = q < nt ? __ldcg(&H[(size_t)(q / w) * NB + jb0 + q % w]) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint32_t q = q0 + (uint32_t)u * kFT + tid;
-                if (q < nt) tile[q] = v[u];
-            }
-        }
-        __syncthreads();
-        for (uint32_t j = warp; j < w; j += kFW) {  // one warp per column, lanes over CTAs (ILP over rows)
-            uint32_t v[kTRows], x[kTRows];
-#pragma unroll
-            for (int i = 0; i < kTRows; i++) {
-                const uint32_t r = 32u * i + lane;
-                v[i] = r < G ? tile[r * w + j] : 0u;
-                x[i] = v[i];
-            }
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-                for (int i = 0; i < kTRows; i++) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x[i], o);
-                    if (lane >= (uint32_t)o) x[i] += y;
-                }
-            }
-            uint32_t carry = 0;
-#pragma unroll
-            for (int i = 0; i < kTRows; i++) {
-                const uint32_t r = 32u * i + lane;
-                const uint32_t t = __shfl_sync(0xffffffffu, x[i], 31);
-                if (r < G) tile[r * w + j] = carry + x[i] - v[i];
-                carry += t;
-            }
-            if (lane == 0) T[jb0 + j] = carry;
-        }
-        __syncthreads();
-        for (uint32_t q = tid; q < nt; q += kFT) H[(size_t)(q / w) * NB + jb0 + q % w] = tile[q];
-    }
     TRACE(4);
-    grid_barrier(b.flags, G, ++bar);
     TRACE(5);
 
     // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
-    // bucket order; cursor(j) = start(j) + keys of bucket j in the CTAs before this one
+    // bucket order; cursor(j) = start(j) + this CTA's offset inside bucket j
     {
         constexpr int kPer = (kMaxBuckets + kFT - 1) / kFT;  // 15
-        uint32_t tv[kPer], hv[kPer];
+        uint32_t tv[kPer];
 #pragma unroll
         for (int u = 0; u < kPer; u++) {
             const uint32_t j = tid + (uint32_t)u * kFT;
             tv[u] = j < NB ? __ldcg(&T[j]) : 0u;
-            hv[u] = j < NB ? __ldcg(&H[(size_t)bid * NB + j]) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < kPer; u++) {
             const uint32_t j = tid + (uint32_t)u * kFT;
-            if (j < NB) { sm.s.start[j] = tv[u]; sm.s.cnt[j] = hv[u]; }
+            if (j < NB) sm.s.start[j] = tv[u];
         }
     }
     __syncthreads();

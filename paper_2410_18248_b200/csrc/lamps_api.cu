@@ -177,8 +177,8 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_pin = L.take((size_t)gmax * 8);
     size_t o_flags = L.take((size_t)32 * 4 * (2 + 16));  // grid barrier: release word, 16 group counters, root
     const size_t bsum_lsd = (size_t)2 * gmax * kBins * 4;
-    const size_t bsum_fused = h->fused ? ((size_t)h->fused_grid + 1) * fused_max_buckets() * 4 : 0;
-    size_t o_bsum = L.take(std::max(bsum_lsd, bsum_fused));
+    size_t o_bsum = L.take(bsum_lsd);
+    size_t o_btot = h->fused ? L.take((size_t)2 * fused_max_buckets() * 4) : 0;
     size_t o_ctl = L.take(sizeof(Ctl));
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
     size_t o_ai0 = L.take((size_t)mb * 8), o_ai1 = L.take((size_t)mb * 8);
@@ -207,6 +207,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.pin_part = reinterpret_cast<unsigned long long*>(base + o_pin);
     h->b.flags = reinterpret_cast<uint32_t*>(base + o_flags);
     h->b.blocksum = reinterpret_cast<uint32_t*>(base + o_bsum);
+    h->b.btot = h->fused ? reinterpret_cast<uint32_t*>(base + o_btot) : nullptr;
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;
     h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);

@@ -73,7 +73,9 @@ struct Bufs {
     Ctl* ctl;
     unsigned long long* kmask;   // [2][max(score_grid, sort_grid)] per-block OR / AND of keys
     unsigned long long* pin_part;  // [sort_grid] per-CTA pinned sums (fused kernel)
-    uint32_t* blocksum;      // LSD: [2][grid][kBins] digit counts; fused: [grid+1][buckets]
+    uint32_t* blocksum;      // LSD: [2][grid][kBins] digit counts
+    uint32_t* btot;          // fused: [2][buckets] bucket totals by step parity; the other
+                             // parity's array is zeroed during the step (zero at init)
     uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity
