@@ -224,6 +224,9 @@ def run_ours(args, rank, world, local):
             s.step_async(kv)
         torch.cuda.synchronize()
     r0 = s.result()
+    # timed steps start from the snapshot again, so the measured state is snapshot + k steps
+    # (the warm-up / burn steps would otherwise age the pool: starvation counters grow)
+    s.import_pool(snap, snap["id_base"], snap["next_id"])
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
@@ -257,6 +260,7 @@ def run_ours(args, rank, world, local):
           flush.zero_()
           sp.step_async(kv)
       sp.timing()
+      sp.import_pool(snap, snap["id_base"], snap["next_id"])  # same states as the timed steps above
       traces = []
       for _ in range(args.steps):
           flush.zero_()

@@ -55,11 +55,12 @@ if os.environ.get("TRACE"):
     ms, nst = st.timing() if False else (None, None)
     if os.environ.get("PERCTA"):
         t0 = acc[-1]
-        print("cta  keys  starving  Lsort_us  Lstarv_refine  Lnon_refine  big_s big_n  end_us")
+        print("cta  keys buckets  Lsort_us  [P+zero  count+scan  place+rank  refine]  big  score_us  Xscatter_us")
         for cta in range(t0.shape[0]):
             r = t0[cta]
-            print(f"{cta:3d} {r[30]:6d} {r[31]:6d} {(r[14]-r[13])/1965:8.2f} {(r[19]-r[18])/1965 if r[18] else 0:8.2f} "
-                  f"{(r[27]-r[26])/1965 if r[26] else 0:8.2f} {r[21]:5d} {r[29]:5d} {(r[8]-t0[:,0].min())/1965:8.2f}")
+            sub = [(r[17 + i] - r[16 + i]) / 1965 for i in range(4)]
+            print(f"{cta:3d} {r[30]:6d} {r[31]:6d} {(r[14]-r[13])/1965:8.2f}  " + " ".join(f"{x:6.2f}" for x in sub) +
+                  f"  {r[21]:4d} {(r[1]-r[0])/1965:7.2f} {(r[12]-r[11])/1965:7.2f}")
     if os.environ.get("LEVELS"):
         t0 = acc[-1]
         print("cta  keys  per-level (us, groups) of the non-starving part; level-0 substeps or/and,count,scan,scatter,final")
