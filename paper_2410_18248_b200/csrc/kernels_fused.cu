@@ -684,6 +684,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     uint32_t bar = a.step * kBarPerStep;
     grid_barrier(b.flags, G, ++bar);
     TRACE(3);
+    // CTA 0, warp 0: the pinned total (A5's budget) is final now; kept in registers
+    unsigned long long pinned_all = 0;
+    if (bid == 0 && warp == 0) {
+        for (uint32_t r = lane; r < G; r += 32) pinned_all += __ldcg(&b.pin_part[r]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pinned_all += __shfl_xor_sync(0xffffffffu, pinned_all, o);
+    }
     TRACE(4);
     TRACE(5);
 
@@ -725,9 +732,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now: key boundaries
     uint32_t* jb = rb + (G + 1);                             // and bucket boundaries of the ranges
     if (tid <= G) {
-        // CTA 0 sorts only the head (about 2 * max_batch keys) so it can start the
-        // admission early; the other CTAs share the rest evenly
-        const uint32_t head = min(n, max(2u * a.max_batch, n / (4u * G)));
+        // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
+        // end of their bucket) so it can start the admission early; the other CTAs share
+        // the rest evenly
+        const uint32_t head = min(n, a.max_batch + 32u);
         const uint32_t q = tid == 0 ? 0u : head + (uint32_t)(((uint64_t)(tid - 1) * (n - head)) / (G - 1 ? G - 1 : 1));
         uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
         while (lo < hi) {
@@ -794,13 +802,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const bool wait = fallback || r_end0 < need;
     if (wait) grid_barrier(b.flags, G, ++bar);
     if (bid != 0) return;
-    unsigned long long pinned_all;
-    {
-        unsigned long long v = tid < G ? __ldcg(&b.pin_part[tid]) : 0ull;
-        unsigned long long tot;
-        (void)block_excl_scan_u64<kFT>(v, sm.l.adm.w64, &tot);
-        pinned_all = tot;
-    }
+    if (tid == 0) sm.l.adm.w64[0] = pinned_all;
+    __syncthreads();
+    pinned_all = sm.l.adm.w64[0];
+    __syncthreads();
     if (tid == 0) {
         ctl->n_passes = passes;
         ctl->final_buf = final_buf;
@@ -835,7 +840,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         TRACE(9);
         return;
     }
-    admit_cta(b, c, a, head, n, pinned_all, sm.l.adm);
+    // the preempted check probes a hash table of the admitted slots in shared memory
+    // (sm.l.b is free once the range is sorted); very large batches stamp P.stamp
+    uint32_t hs = 1024;
+    while (hs < 2u * a.max_batch) hs <<= 1;
+    const bool use_h = !wait && hs * 4u <= sizeof(sm.l.b);
+    admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? reinterpret_cast<uint32_t*>(sm.l.b) : nullptr,
+              use_h ? hs : 0u);
     TRACE(9);
 }
 

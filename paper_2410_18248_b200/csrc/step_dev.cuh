@@ -241,10 +241,16 @@ struct AdmitSmem {
     uint32_t w32[32];
 };
 
+// htab (optional, shared memory, >= 2 * max_batch u32 entries, power of two hsize):
+// admitted slots are inserted into an open-addressing table and the preempted check
+// probes it, instead of stamping P.stamp and re-reading it from global memory.
+__device__ __forceinline__ uint32_t slot_hash(uint32_t s, uint32_t mask) { return (s * 2654435761u >> 7) & mask; }
+
 __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const StepArgs& a,
                                           const uint64_t* keys, uint64_t n_elig, uint64_t pinned,
-                                          AdmitSmem& sm) {
+                                          AdmitSmem& sm, uint32_t* htab = nullptr, uint32_t hsize = 0) {
     constexpr int NT = 1024;
+    constexpr uint32_t kEmpty = 0xffffffffu;
     Ctl* ctl = b.ctl;
     const Pool& P = b.pool;
     const uint32_t tid = threadIdx.x;
@@ -254,35 +260,46 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
     if (budget < Wn) Wn = budget;
     const uint64_t idmask = (1ull << c.IB) - 1ull;
     const uint32_t par = a.parity, prev = par ^ 1u;
+    const uint32_t hmask = hsize - 1u;
+    if (htab)
+        for (uint32_t i = tid; i < hsize; i += NT) htab[i] = kEmpty;
 
     // prefetch the previous admitted list (independent of the ranking)
     uint32_t pslot = 0, pw = 0;
+    uint64_t pid = 0;
     if (tid < n_prev) {
         pslot = b.adm_slot[prev][tid];
+        pid = b.adm_id[prev][tid];
         pw = P.sfc[pslot];
     }
     unsigned long long carry = 0;
     uint32_t cut = 0;
     for (uint32_t base = 0; base < Wn; base += NT) {
         const uint32_t k = base + tid;
-        uint32_t slot = 0;
+        uint32_t slot = 0, w = 0;
         uint64_t idoff = 0;
         unsigned long long dem = 0;
         if (k < Wn) {
             idoff = keys[k] & idmask;
             slot = (uint32_t)((a.id_base + idoff) & c.cap_mask);
-            dem = blk((uint64_t)P.ctx[slot] + 1u, c);
+            const uint32_t ctx = P.ctx[slot];
+            w = P.sfc[slot];
+            dem = blk((uint64_t)ctx + 1u, c);
         }
         unsigned long long tot;
         const unsigned long long incl = carry + block_excl_scan_u64<NT>(dem, sm.w64, &tot) + dem;
         const bool fit = k < Wn && incl <= budget;
         const uint32_t nfit = (uint32_t)__syncthreads_count(fit);
         if (fit) {
-            const uint32_t w = P.sfc[slot];
             b.adm_slot[par][k] = slot;
             b.adm_id[par][k] = a.id_base + idoff;
             b.adm_strat[par][k] = (uint8_t)sfc_strat(w);
-            P.stamp[slot] = a.step;
+            if (htab) {
+                uint32_t h = slot_hash(slot, hmask);
+                while (atomicCAS(&htab[h], kEmpty, slot) != kEmpty) h = (h + 1u) & hmask;
+            } else {
+                P.stamp[slot] = a.step;
+            }
             P.sfc[slot] = (w & 0xffffu) | SFC_RAN;  // StarvationCnt <- 0; runs this iteration
             if (k == base + nfit - 1) ctl->budget_used = incl;
         }
@@ -299,14 +316,24 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
     for (uint32_t base = 0; base < n_prev; base += NT) {
         const uint32_t k = base + tid;
         uint32_t f = 0;
+        uint64_t id = 0;
         if (k < n_prev) {
             const uint32_t s = base ? b.adm_slot[prev][k] : pslot;
             const uint32_t w = base ? P.sfc[s] : pw;
-            f = (sfc_state(w) == ST_READY && P.stamp[s] != a.step) ? 1u : 0u;
+            id = base ? b.adm_id[prev][k] : pid;
+            bool now;
+            if (htab) {
+                uint32_t h = slot_hash(s, hmask), v;
+                while ((v = htab[h]) != s && v != kEmpty) h = (h + 1u) & hmask;
+                now = v == s;
+            } else {
+                now = P.stamp[s] == a.step;
+            }
+            f = (sfc_state(w) == ST_READY && !now) ? 1u : 0u;
         }
         uint32_t tot;
         const uint32_t pos = block_excl_scan_u32<NT>(f, sm.w32, &tot);
-        if (f) b.pre_id[npre + pos] = b.adm_id[prev][k];
+        if (f) b.pre_id[npre + pos] = id;
         npre += tot;
     }
     if (tid == 0) {
