@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     while (hs < 2u * a.max_batch) hs <<= 1;
     const bool use_h = !wait && hs * 4u <= sizeof(sm.l.b);
     admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? reinterpret_cast<uint32_t*>(sm.l.b) : nullptr,
-              use_h ? hs : 0u);
+              use_h ? hs : 0u, b.trace ? b.trace + 40 : nullptr);
     TRACE(9);
 }
 

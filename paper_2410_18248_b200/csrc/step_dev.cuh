@@ -248,7 +248,9 @@ __device__ __forceinline__ uint32_t slot_hash(uint32_t s, uint32_t mask) { retur
 
 __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const StepArgs& a,
                                           const uint64_t* keys, uint64_t n_elig, uint64_t pinned,
-                                          AdmitSmem& sm, uint32_t* htab = nullptr, uint32_t hsize = 0) {
+                                          AdmitSmem& sm, uint32_t* htab = nullptr, uint32_t hsize = 0,
+                                          unsigned long long* tr = nullptr) {
+#define ATRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     constexpr int NT = 1024;
     constexpr uint32_t kEmpty = 0xffffffffu;
     Ctl* ctl = b.ctl;
@@ -261,6 +263,7 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
     const uint64_t idmask = (1ull << c.IB) - 1ull;
     const uint32_t par = a.parity, prev = par ^ 1u;
     const uint32_t hmask = hsize - 1u;
+    ATRACE(0);
     if (htab)
         for (uint32_t i = tid; i < hsize; i += NT) htab[i] = kEmpty;
 
@@ -286,10 +289,12 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
             w = P.sfc[slot];
             dem = blk((uint64_t)ctx + 1u, c);
         }
+        if (base == 0) ATRACE(1);
         unsigned long long tot;
         const unsigned long long incl = carry + block_excl_scan_u64<NT>(dem, sm.w64, &tot) + dem;
         const bool fit = k < Wn && incl <= budget;
         const uint32_t nfit = (uint32_t)__syncthreads_count(fit);
+        if (base == 0) ATRACE(2);
         if (fit) {
             b.adm_slot[par][k] = slot;
             b.adm_id[par][k] = a.id_base + idoff;
@@ -310,6 +315,7 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
     }
     if (tid == 0 && cut == 0) ctl->budget_used = 0;
     __syncthreads();
+    ATRACE(3);
 
     // preempted: admitted last step, still READY, not admitted now (previous rank order)
     uint32_t npre = 0;
@@ -346,6 +352,8 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
         ctl->n_elig = 0;  // accumulators of the next step
         ctl->pinned = 0;
     }
+    ATRACE(4);
+#undef ATRACE
 }
 
 }  // namespace lamps

@@ -77,3 +77,7 @@ if os.environ.get("TRACE"):
                 b = [r[0], r[16], r[17], r[18], r[19], r[20]]
                 ss = " sub " + ",".join(f"{(b[i+1]-b[i]) / 1965:.2f}" for i in range(5)) + f" cut {r[21]} keys {r[22]}"
             print(f"{cta:3d} {t0[cta,30]:6d} " + " ".join(lv) + ss)
+    if os.environ.get("ADMIT"):
+        r = acc[-1][0, 40:45]
+        print("admit substeps us (init+loads, scan+count, writes+hash, preempted):",
+              [round((r[i + 1] - r[i]) / 1965, 2) for i in range(4)])
