@@ -439,9 +439,20 @@ __device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t d
 // range) indexed by sub_digit, so the sub-buckets hold ~1 key; keys of sub-buckets
 // of <= kMaxRankM keys are ranked by comparison, bigger ones (many near-equal keys)
 // go to refine_groups, and an LSD of the whole range is the last resort.
-__device__ __forceinline__ void range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
+//
+// Head range (pool != nullptr, rn <= kHeadPre): the admission's per-key loads (ctx for
+// the demand blk(ctx+1), the state word) are issued with the key loads and land in
+// shared memory in sorted order (kHeadD / kHeadW words of sm.b), so A5 needs no
+// dependent global round trip.  Returns whether those arrays are valid (not after a
+// refinement pass, which moves keys).
+constexpr uint32_t kHeadPre = 2560;
+constexpr uint32_t kHeadTC = 2 * kKcap / 2, kHeadTW = kHeadTC + kHeadPre;   // unsorted ctx / state
+constexpr uint32_t kHeadD = kHeadTW + kHeadPre, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
+static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
+__device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
                                            const uint32_t* T, uint32_t j_lo, uint32_t j_hi, const Cost& c,
-                                           uint32_t half, unsigned long long* tr) {
+                                           uint32_t half, unsigned long long* tr, const Pool* pool = nullptr,
+                                           uint32_t id_base_mod = 0) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x;
     const uint32_t nb = j_hi - j_lo;
@@ -456,6 +467,21 @@ __device__ __forceinline__ void range_sort(PhaseL& sm, const uint64_t* __restric
         const uint32_t i = tid + (uint32_t)u * kFT;
         k[u] = i < rn ? __ldcg(src + i) : 0ull;
     }
+    uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
+    constexpr int kHU = (kHeadPre + kFT - 1) / kFT;
+    uint32_t hc[kHU], hw[kHU];
+    if (pool) {
+#pragma unroll
+        for (int u = 0; u < kHU; u++) {
+            const uint32_t i = tid + (uint32_t)u * kFT;
+            hc[u] = hw[u] = 0;
+            if (i < rn) {
+                const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
+                hc[u] = __ldcg(&pool->ctx[slot]);
+                hw[u] = __ldcg(&pool->sfc[slot]);
+            }
+        }
+    }
     for (uint32_t j = tid; j < nb; j += kFT) {
         const uint32_t m = __ldcg(&T[j_lo + j]);
         const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
@@ -467,6 +493,13 @@ __device__ __forceinline__ void range_sort(PhaseL& sm, const uint64_t* __restric
     const uint32_t ncnt = ptot >> 14;
     if (tid == 0) P[nb] = ptot;
     for (uint32_t i = tid; i < ncnt; i += kFT) cnt[i] = 0;
+    if (pool) {
+#pragma unroll
+        for (int u = 0; u < kHU; u++) {
+            const uint32_t i = tid + (uint32_t)u * kFT;
+            if (i < rn) { b32[kHeadTC + i] = hc[u]; b32[kHeadTW + i] = hw[u]; }
+        }
+    }
     __syncthreads();
     LTRACE(1);
     uint32_t it[kLocalItems];  // counter index | order within the sub-bucket << 15
@@ -521,7 +554,14 @@ __device__ __forceinline__ void range_sort(PhaseL& sm, const uint64_t* __restric
 #pragma unroll
     for (int u = 0; u < kLocalItems; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
-        if (i < rn && (it[u] >> 31)) A[it[u] & 0x7fffffffu] = k[u];
+        if (i < rn && (it[u] >> 31)) {
+            const uint32_t pos = it[u] & 0x7fffffffu;
+            A[pos] = k[u];
+            if (pool) {
+                b32[kHeadD + pos] = (uint32_t)blk((uint64_t)b32[kHeadTC + i] + 1u, c);
+                b32[kHeadW + pos] = b32[kHeadTW + i];
+            }
+        }
     }
     __syncthreads();
     LTRACE(3);
@@ -535,9 +575,11 @@ __device__ __forceinline__ void range_sort(PhaseL& sm, const uint64_t* __restric
             for (uint32_t i = tid; i < rn; i += kFT) A[i] = r[i];
         __syncthreads();
     }
+    const bool dw_ok = pool != nullptr && sm.ngl[0] == 0;
     if (tr && tid == 0) { tr[5] = full_lsd ? 1000u : sm.ngl[0]; }
     LTRACE(4);
 #undef LTRACE
+    return dw_ok;
 }
 
 #define TRACE(k)                                                                         \
@@ -758,6 +800,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
 
     // ---------------- L: sort the key ranges
     uint32_t final_buf, passes;
+    bool head_dw = false;  // CTA 0: demands / state words of its head in sm.l.b (sorted order)
     if (!fallback) {
         const uint32_t rn = r_hi - r_lo;
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
@@ -767,7 +810,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         }
         if (j_hi - j_lo < (uint32_t)kSubBuckets) {
             TRACE(13);
-            range_sort(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half, tr ? tr + 16 : nullptr);
+            const bool pre = bid == 0 && rn <= kHeadPre;
+            head_dw = range_sort(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half, tr ? tr + 16 : nullptr,
+                                 pre ? &b.pool : nullptr, a.id_base_mod);
         } else {  // a sparse range over very many buckets: sort the two parts by bucket runs
             for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
             TRACE(13);
@@ -813,6 +858,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     }
     TRACE(15);
     const uint64_t* head = wait ? b.keys[final_buf] : sm.l.a;  // CTA 0 holds [0, need) itself unless it waited
+    const bool dw = head_dw && !wait;
     if (a.flags & kStepMerge) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
         const uint32_t K = a.max_batch, nv = min(n, K);
@@ -824,7 +870,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             MergeRec r;
             r.sk = k >> c.IB;
             r.gid = lid * a.world + a.rank;
-            r.demand = (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
+            r.demand = dw ? reinterpret_cast<const uint32_t*>(sm.l.b)[kHeadD + i]
+                          : (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
             r.slot = slot;
             r.pad = 0;
             b.xsend[1 + i] = r;
@@ -844,9 +891,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // (sm.l.b is free once the range is sorted); very large batches stamp P.stamp
     uint32_t hs = 1024;
     while (hs < 2u * a.max_batch) hs <<= 1;
-    const bool use_h = !wait && hs * 4u <= sizeof(sm.l.b);
+    const bool use_h = !wait && hs <= kHeadTC;
+    const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);
     admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? reinterpret_cast<uint32_t*>(sm.l.b) : nullptr,
-              use_h ? hs : 0u, b.trace ? b.trace + 40 : nullptr);
+              use_h ? hs : 0u, b.trace ? b.trace + 40 : nullptr, dw ? b32 + kHeadD : nullptr,
+              dw ? b32 + kHeadW : nullptr);
     TRACE(9);
 }
 

@@ -249,7 +249,8 @@ __device__ __forceinline__ uint32_t slot_hash(uint32_t s, uint32_t mask) { retur
 __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const StepArgs& a,
                                           const uint64_t* keys, uint64_t n_elig, uint64_t pinned,
                                           AdmitSmem& sm, uint32_t* htab = nullptr, uint32_t hsize = 0,
-                                          unsigned long long* tr = nullptr) {
+                                          unsigned long long* tr = nullptr, const uint32_t* dsm = nullptr,
+                                          const uint32_t* wsm = nullptr) {
 #define ATRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     constexpr int NT = 1024;
     constexpr uint32_t kEmpty = 0xffffffffu;
@@ -285,9 +286,14 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
         if (k < Wn) {
             idoff = keys[k] & idmask;
             slot = (uint32_t)((a.id_base + idoff) & c.cap_mask);
-            const uint32_t ctx = P.ctx[slot];
-            w = P.sfc[slot];
-            dem = blk((uint64_t)ctx + 1u, c);
+            if (dsm) {  // demand and state word staged on chip by the range sort
+                dem = dsm[k];
+                w = wsm[k];
+            } else {
+                const uint32_t ctx = P.ctx[slot];
+                w = P.sfc[slot];
+                dem = blk((uint64_t)ctx + 1u, c);
+            }
         }
         if (base == 0) ATRACE(1);
         unsigned long long tot;
