@@ -446,9 +446,12 @@ __device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t d
 // dependent global round trip.  Returns whether those arrays are valid (not after a
 // refinement pass, which moves keys).
 constexpr uint32_t kHeadPre = 2560;
-constexpr uint32_t kHeadTC = 2 * kKcap / 2, kHeadTW = kHeadTC + kHeadPre;   // unsorted ctx / state
-constexpr uint32_t kHeadD = kHeadTW + kHeadPre, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
+constexpr uint32_t kHeadTC = 2 * kKcap / 2;               // hash table limit (words of sm.b)
+constexpr uint32_t kHeadD = kHeadTC, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
 static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
+// NI = keys per thread (kLocalItems; 3 for the head range, whose loads for the
+// admission stay in flight in registers for the whole sort)
+template <int NI, bool HEAD>
 __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
                                            const uint32_t* T, uint32_t j_lo, uint32_t j_hi, const Cost& c,
                                            uint32_t half, unsigned long long* tr, const Pool* pool = nullptr,
@@ -461,16 +464,17 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);     // <= 2 * kKcap counters
     uint64_t* A = sm.a;
     LTRACE(0);
-    uint64_t k[kLocalItems];
+    static_assert(!HEAD || NI * kFT >= (int)kHeadPre, "head items");
+    uint64_t k[NI];
 #pragma unroll
-    for (int u = 0; u < kLocalItems; u++) {
+    for (int u = 0; u < NI; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
         k[u] = i < rn ? __ldcg(src + i) : 0ull;
     }
     uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
-    constexpr int kHU = (kHeadPre + kFT - 1) / kFT;
+    constexpr int kHU = HEAD ? NI : 1;
     uint32_t hc[kHU], hw[kHU];
-    if (pool) {
+    if (HEAD) {
 #pragma unroll
         for (int u = 0; u < kHU; u++) {
             const uint32_t i = tid + (uint32_t)u * kFT;
@@ -493,18 +497,11 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     const uint32_t ncnt = ptot >> 14;
     if (tid == 0) P[nb] = ptot;
     for (uint32_t i = tid; i < ncnt; i += kFT) cnt[i] = 0;
-    if (pool) {
-#pragma unroll
-        for (int u = 0; u < kHU; u++) {
-            const uint32_t i = tid + (uint32_t)u * kFT;
-            if (i < rn) { b32[kHeadTC + i] = hc[u]; b32[kHeadTW + i] = hw[u]; }
-        }
-    }
     __syncthreads();
     LTRACE(1);
-    uint32_t it[kLocalItems];  // counter index | order within the sub-bucket << 15
+    uint32_t it[NI];  // counter index | order within the sub-bucket << 15
 #pragma unroll
-    for (int u = 0; u < kLocalItems; u++) {
+    for (int u = 0; u < NI; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
         it[u] = 0;
         if (i < rn) {
@@ -517,11 +514,11 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
         }
     }
     __syncthreads();
-    (void)smem_excl_scan<kFT, 2 * kKcap / kFT + 1>(cnt, ncnt, sm.w32);
+    (void)smem_excl_scan<kFT, 2 * NI + 1>(cnt, ncnt, sm.w32);
     LTRACE(2);
     // initial placement: sub-bucket start + arrival order; keep (start, size)
 #pragma unroll
-    for (int u = 0; u < kLocalItems; u++) {
+    for (int u = 0; u < NI; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
         if (i < rn) {
             const uint32_t idx = it[u] & 0x7fffu;
@@ -533,7 +530,7 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     __syncthreads();
     // rank inside sub-buckets of <= kMaxRankM keys; list the bigger ones
 #pragma unroll
-    for (int u = 0; u < kLocalItems; u++) {
+    for (int u = 0; u < NI; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
         if (i < rn) {
             const uint32_t st = it[u] & 0x3fffu, m2 = it[u] >> 14;
@@ -552,14 +549,14 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < kLocalItems; u++) {
+    for (int u = 0; u < NI; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
         if (i < rn && (it[u] >> 31)) {
             const uint32_t pos = it[u] & 0x7fffffffu;
             A[pos] = k[u];
-            if (pool) {
-                b32[kHeadD + pos] = (uint32_t)blk((uint64_t)b32[kHeadTC + i] + 1u, c);
-                b32[kHeadW + pos] = b32[kHeadTW + i];
+            if (HEAD) {
+                b32[kHeadD + pos] = (uint32_t)blk((uint64_t)hc[u] + 1u, c);
+                b32[kHeadW + pos] = hw[u];
             }
         }
     }
@@ -575,7 +572,7 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
             for (uint32_t i = tid; i < rn; i += kFT) A[i] = r[i];
         __syncthreads();
     }
-    const bool dw_ok = pool != nullptr && sm.ngl[0] == 0;
+    const bool dw_ok = HEAD && sm.ngl[0] == 0;
     if (tr && tid == 0) { tr[5] = full_lsd ? 1000u : sm.ngl[0]; }
     LTRACE(4);
 #undef LTRACE
@@ -810,9 +807,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         }
         if (j_hi - j_lo < (uint32_t)kSubBuckets) {
             TRACE(13);
-            const bool pre = bid == 0 && rn <= kHeadPre;
-            head_dw = range_sort(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half, tr ? tr + 16 : nullptr,
-                                 pre ? &b.pool : nullptr, a.id_base_mod);
+            if (bid == 0 && rn <= kHeadPre)
+                head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c,
+                                                                      half, tr ? tr + 16 : nullptr, &b.pool,
+                                                                      a.id_base_mod);
+            else
+                (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
+                                                     tr ? tr + 16 : nullptr);
         } else {  // a sparse range over very many buckets: sort the two parts by bucket runs
             for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
             TRACE(13);
