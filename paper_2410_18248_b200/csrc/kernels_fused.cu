@@ -474,22 +474,21 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
     constexpr int kHU = HEAD ? NI : 1;
     uint32_t hc[kHU], hw[kHU];
-    if (HEAD) {
+    if (HEAD) {  // L2 prefetch of what the admission reads (no registers held in flight)
 #pragma unroll
         for (int u = 0; u < kHU; u++) {
             const uint32_t i = tid + (uint32_t)u * kFT;
-            hc[u] = hw[u] = 0;
             if (i < rn) {
                 const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
-                hc[u] = __ldcg(&pool->ctx[slot]);
-                hw[u] = __ldcg(&pool->sfc[slot]);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->ctx + slot));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->sfc + slot));
             }
         }
     }
     for (uint32_t j = tid; j < nb; j += kFT) {
         const uint32_t m = __ldcg(&T[j_lo + j]);
         const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
-        P[j] = m | ((1u << db) << 14);
+        P[j] = m | ((m ? 1u << db : 0u) << 14);  // empty buckets take no counters: ncnt < 2 rn
     }
     if (tid == 0) sm.ngl[0] = 0;
     __syncthreads();
@@ -528,6 +527,18 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
         }
     }
     __syncthreads();
+    if (HEAD) {  // the admission's loads (L2 hits by now), consumed after the ranking
+#pragma unroll
+        for (int u = 0; u < kHU; u++) {
+            const uint32_t i = tid + (uint32_t)u * kFT;
+            hc[u] = hw[u] = 0;
+            if (i < rn) {
+                const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
+                hc[u] = __ldcg(&pool->ctx[slot]);
+                hw[u] = __ldcg(&pool->sfc[slot]);
+            }
+        }
+    }
     // rank inside sub-buckets of <= kMaxRankM keys; list the bigger ones
 #pragma unroll
     for (int u = 0; u < NI; u++) {
@@ -720,6 +731,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         }
     }
     TRACE(2);
+    if (bid == 0) {  // while waiting for the other CTAs: L2 prefetch of the previous admitted list
+        const uint32_t np = ctl->n_admitted, prv = a.parity ^ 1u;
+        for (uint32_t i = tid; i < np; i += kFT) {
+            const uint32_t ps = __ldcg(&b.adm_slot[prv][i]);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(b.pool.sfc + ps));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(b.adm_id[prv] + i));
+        }
+    }
     uint32_t bar = a.step * kBarPerStep;
     grid_barrier(b.flags, G, ++bar);
     TRACE(3);
