@@ -446,6 +446,10 @@ __device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t d
 // dependent global round trip.  Returns whether those arrays are valid (not after a
 // refinement pass, which moves keys).
 constexpr uint32_t kHeadPre = 2560;
+// range_sort ranks sub-buckets of up to this many keys by comparison (one thread per
+// key, O(size) shared-memory reads): cheaper than a refinement pass for the few
+// sub-buckets of near-equal keys (e.g. saturated scores) a range may hold
+constexpr uint32_t kRangeRankM = 256;
 constexpr uint32_t kHeadTC = 2 * kKcap / 2;               // hash table limit (words of sm.b)
 constexpr uint32_t kHeadD = kHeadTC, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
 static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
@@ -545,8 +549,9 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
         const uint32_t i = tid + (uint32_t)u * kFT;
         if (i < rn) {
             const uint32_t st = it[u] & 0x3fffu, m2 = it[u] >> 14;
-            if (m2 <= kMaxRankM) {
+            if (m2 <= kRangeRankM) {
                 uint32_t r = 0;
+#pragma unroll 4
                 for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k[u] ? 1u : 0u;
                 it[u] = (st + r) | 0x80000000u;
             } else {
