@@ -59,7 +59,7 @@ struct PhaseL {                  // L
             uint32_t scan[kFW];
         };
         struct {                         // local MSD + rank
-            uint32_t pos[kSubBuckets];   // 32 KB: counts -> starts -> ends
+            uint32_t pos[kKcap > kSubBuckets ? kKcap : kSubBuckets];  // 40 KB: counts -> starts; sbi
             uint32_t w32[kFW + 1];
             uint32_t nbig;
         };
@@ -450,8 +450,8 @@ constexpr uint32_t kHeadPre = 2560;
 // key, O(size) shared-memory reads): cheaper than a refinement pass for the few
 // sub-buckets of near-equal keys (e.g. saturated scores) a range may hold
 constexpr uint32_t kRangeRankM = 256;
-constexpr uint32_t kHeadTC = 2 * kKcap / 2;               // hash table limit (words of sm.b)
-constexpr uint32_t kHeadD = kHeadTC, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
+constexpr uint32_t kHeadTC = 2 * kKcap / 2, kHeadTW = kHeadTC + kHeadPre;  // by initial position
+constexpr uint32_t kHeadD = kHeadTW + kHeadPre, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
 static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
 // NI = keys per thread (kLocalItems; 3 for the head range, whose loads for the
 // admission stay in flight in registers for the whole sort)
@@ -477,7 +477,6 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     }
     uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
     constexpr int kHU = HEAD ? NI : 1;
-    uint32_t hc[kHU], hw[kHU];
     if (HEAD) {  // L2 prefetch of what the admission reads (no registers held in flight)
 #pragma unroll
         for (int u = 0; u < kHU; u++) {
@@ -519,60 +518,58 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     __syncthreads();
     (void)smem_excl_scan<kFT, 2 * NI + 1>(cnt, ncnt, sm.w32);
     LTRACE(2);
-    // initial placement: sub-bucket start + arrival order; keep (start, size)
+    // initial placement: sub-bucket start + arrival order; per position its sub-bucket's
+    // (start, size) in sbi (P is dead after the count pass)
+    uint32_t* sbi = sm.pos;
 #pragma unroll
     for (int u = 0; u < NI; u++) {
         const uint32_t i = tid + (uint32_t)u * kFT;
         if (i < rn) {
             const uint32_t idx = it[u] & 0x7fffu;
             const uint32_t st = cnt[idx], e = idx + 1u < ncnt ? cnt[idx + 1] : rn;
-            A[st + (it[u] >> 15)] = k[u];
-            it[u] = st | ((e - st) << 14);
-        }
-    }
-    __syncthreads();
-    if (HEAD) {  // the admission's loads (L2 hits by now), consumed after the ranking
-#pragma unroll
-        for (int u = 0; u < kHU; u++) {
-            const uint32_t i = tid + (uint32_t)u * kFT;
-            hc[u] = hw[u] = 0;
-            if (i < rn) {
+            const uint32_t p = st + (it[u] >> 15);
+            A[p] = k[u];
+            sbi[p] = st | ((e - st) << 14);
+            if (HEAD) {  // the admission's loads (L2 hits by now), by position
                 const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
-                hc[u] = __ldcg(&pool->ctx[slot]);
-                hw[u] = __ldcg(&pool->sfc[slot]);
+                b32[kHeadTC + p] = __ldcg(&pool->ctx[slot]);
+                b32[kHeadTW + p] = __ldcg(&pool->sfc[slot]);
             }
         }
     }
-    // rank inside sub-buckets of <= kMaxRankM keys; list the bigger ones
+    __syncthreads();
+    // rank inside sub-buckets of <= kRangeRankM keys by comparison; list the bigger ones.
+    // Thread t takes positions t + u*kFT: a sub-bucket's keys are contiguous, so the lanes
+    // of a warp mostly share a sub-bucket and the loop trip counts agree
 #pragma unroll
     for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        if (i < rn) {
-            const uint32_t st = it[u] & 0x3fffu, m2 = it[u] >> 14;
+        const uint32_t p = tid + (uint32_t)u * kFT;
+        it[u] = 0;
+        if (p < rn) {
+            k[u] = A[p];
+            const uint32_t inf = sbi[p];
+            const uint32_t st = inf & 0x3fffu, m2 = inf >> 14;
             if (m2 <= kRangeRankM) {
                 uint32_t r = 0;
 #pragma unroll 4
                 for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k[u] ? 1u : 0u;
                 it[u] = (st + r) | 0x80000000u;
-            } else {
-                it[u] = 0;
-                if (A[st] == k[u]) {
-                    const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
-                    if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m2; }
-                }
+            } else if (p == st) {
+                const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
+                if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m2; }
             }
         }
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        if (i < rn && (it[u] >> 31)) {
+        const uint32_t p = tid + (uint32_t)u * kFT;
+        if (p < rn && (it[u] >> 31)) {
             const uint32_t pos = it[u] & 0x7fffffffu;
             A[pos] = k[u];
             if (HEAD) {
-                b32[kHeadD + pos] = (uint32_t)blk((uint64_t)hc[u] + 1u, c);
-                b32[kHeadW + pos] = hw[u];
+                b32[kHeadD + pos] = (uint32_t)blk((uint64_t)b32[kHeadTC + p] + 1u, c);
+                b32[kHeadW + pos] = b32[kHeadTW + p];
             }
         }
     }
