@@ -41,6 +41,7 @@ struct PhaseS {                  // S, H, T, X
     uint32_t w32[kFW + 1];
     unsigned long long red[3][kFW];
     uint32_t nk, base;
+    unsigned long long mbar[2];  // S: TMA completion barriers of the two stage buffers
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -614,38 +615,52 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
 
     TRACE(0);
     // ---------------- S: score this CTA's slots, keys into shared memory.  The seven SoA
-    // words of each chunk of 1024 slots are staged by cp.async (double buffered) while
+    // words of each chunk of 1024 slots are staged by TMA bulk copies (one thread issues
+    // seven 1-D copies per chunk; an mbarrier counts the bytes), double buffered, while
     // the previous chunk is scored, one slot per thread.
-    if (tid == 0) sm.s.nk = 0;
-    for (uint32_t i = tid; i < NB; i += kFT) sm.s.cnt[i] = 0;
     const uint32_t ngroups = (c.cap + 3u) >> 2;
     const uint32_t gpc = (ngroups + G - 1) / G;
     const uint32_t s_lo = 4u * min(ngroups, bid * gpc), s_hi = 4u * min(ngroups, bid * gpc + gpc);
     const uint32_t nchunk = (s_hi - s_lo + kChunk - 1) / kChunk;
     uint32_t* stage = sm.s.start;  // [2][7][kChunk] words
-    auto issue = [&](uint32_t ch) {
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&sm.s.mbar[0]);
+    auto issue = [&](uint32_t ch) {  // thread 0
         const uint32_t base = s_lo + ch * kChunk, buf = ch & 1u;
-        for (uint32_t q = tid; q < 7u * (kChunk / 4); q += kFT) {
-            const uint32_t ai = q / (kChunk / 4), p4 = 4u * (q % (kChunk / 4));
-            if (base + p4 < s_hi) {
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&stage[(buf * 7u + ai) * kChunk + p4]);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(b.pool.sfc + (size_t)ai * b.pool.stride + base + p4) : "memory");
-            }
+        const uint32_t bytes = min((uint32_t)kChunk, s_hi - base) * 4u;  // multiple of 16: s_lo, s_hi are 4-aligned
+        const uint32_t mb = mb0 + 8u * buf;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(7u * bytes) : "memory");
+#pragma unroll
+        for (uint32_t ai = 0; ai < 7u; ai++) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&stage[(buf * 7u + ai) * kChunk]);
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(dst), "l"(b.pool.sfc + (size_t)ai * b.pool.stride + base), "r"(bytes), "r"(mb)
+                         : "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (nchunk) issue(0);
+    if (tid == 0) {
+        sm.s.nk = 0;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (nchunk) issue(0);
+    }
+    for (uint32_t i = tid; i < NB; i += kFT) sm.s.cnt[i] = 0;
     __syncthreads();
     unsigned long long pinned = 0, kor = 0, kand = ~0ull;
     const uint32_t lt_mask = (1u << lane) - 1u;
     for (uint32_t ch = 0; ch < nchunk; ch++) {
-        if (ch + 1 < nchunk) {
+        if (tid == 0 && ch + 1 < nchunk) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer reads done (barrier below)
             issue(ch + 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        __syncthreads();
+        {   // wait for this chunk's bytes: phase parity = use count of the buffer & 1
+            const uint32_t mb = mb0 + 8u * (ch & 1u), par = (ch >> 1) & 1u;
+            asm volatile(
+                "{\n.reg .pred p;\nWAIT_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra WAIT_%=;\n}\n" ::"r"(mb), "r"(par) : "memory");
+        }
         const uint32_t slot = s_lo + ch * kChunk + tid;
         const uint32_t* sw = stage + (ch & 1u) * 7u * kChunk + tid;
         bool have = false;
@@ -683,6 +698,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             }
         }
         __syncthreads();
+    }
+    if (tid == 0) {  // the barrier words are reused as plain shared memory after S
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0 + 8u) : "memory");
     }
     __syncthreads();
     const uint32_t nk_cta = sm.s.nk;

@@ -141,9 +141,10 @@ __device__ __forceinline__ uint64_t t_swap_fast(uint32_t x, const Cost& c) {
     return x ? (c.S0 + wide32((uint32_t)c.S1, x)) >> c.SH : 0ull;
 }
 // F(n) = sum_{j=1..n} ceil(j/B) = B Q(Q+1)/2 + R(Q+1), n = Q B + R
+// = (Q+1)(QB + 2R)/2 = (Q+1)(n+R)/2 (the product is even: QB even for B >= 2, Q(Q+1) for B = 1)
 __device__ __forceinline__ uint64_t ramp_fast(uint32_t n, const Cost& c) {
     const uint32_t Q = n >> c.lgB, R = n & (c.B - 1u);
-    return ((wide32(Q, Q + 1u) >> 1) << c.lgB) + wide32(R, Q + 1u);
+    return wide32(Q + 1u, n + R) >> 1;
 }
 
 // strategy (A1) and score (A2) of one READY slot on the fast path
