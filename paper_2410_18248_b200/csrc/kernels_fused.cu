@@ -809,50 +809,17 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         }
     }
     if (planned) {  // region cursors, then the keys straight into their range's region
-        // dc[d] = this CTA's keys for range d; local layout: keys grouped by range in the
-        // (now free) stage buffer, so each (CTA, range) run is written contiguously
-        uint64_t* kb2 = reinterpret_cast<uint64_t*>(sm.s.start);
-        // (the local tables live above the buckets in use: cnt has kMaxBuckets words)
-        const bool grouped = nk_cta <= (uint32_t)(sizeof(sm.s.start) / 8) &&
-                             NB + 2u * kFusedMaxGrid + 1u <= (uint32_t)kMaxBuckets;
-        uint32_t* lst = sm.s.cnt + NB;  // [G + 1] local starts
         __syncthreads();
-        if (grouped) {
-            uint32_t v = tid < G ? sm.s.dc[tid] : 0u, tot;
-            const uint32_t ex = block_excl_scan_u32<kFT>(v, sm.s.w32, &tot);
-            if (tid < G) lst[tid] = ex;
-            if (tid == G) lst[G] = tot;
-        }
         if (tid < G) {
             const uint32_t cd = sm.s.dc[tid];
-            sm.s.dc[tid] = tid * (uint32_t)kKcap + (cd ? atomicAdd(&dcur[tid], cd) : 0u);  // global start
+            sm.s.dc[tid] = tid * (uint32_t)kKcap + (cd ? atomicAdd(&dcur[tid], cd) : 0u);
         }
         __syncthreads();
-        if (grouped) {
-            uint32_t* lcur = sm.s.cnt + NB + kFusedMaxGrid + 1;  // [G] local cursors
-            if (tid < G) lcur[tid] = lst[tid];
-            __syncthreads();
-            for (uint32_t i = tid; i < nk_cta; i += kFT) {
-                const uint64_t k = sm.s.kbuf[i];
-                kb2[atomicAdd(&lcur[sm.s.rng[bucket_of(k, c, half)]], 1u)] = k;
-            }
-            __syncthreads();
-            for (uint32_t i = tid; i < nk_cta; i += kFT) {  // range of local position i: last d with lst[d] <= i
-                uint32_t lo = 0, hi = G;
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (lst[mid] <= i) lo = mid; else hi = mid;
-                }
-                const uint32_t pos = sm.s.dc[lo] + (i - lst[lo]);
-                if (pos < (lo + 1u) * (uint32_t)kKcap) b.keys[0][pos] = kb2[i];  // else: overflow
-            }
-        } else {
-            for (uint32_t i = tid; i < nk_cta; i += kFT) {
-                const uint64_t k = sm.s.kbuf[i];
-                const uint32_t d = sm.s.rng[bucket_of(k, c, half)];
-                const uint32_t pos = atomicAdd(&sm.s.dc[d], 1u);
-                if (pos < (d + 1u) * (uint32_t)kKcap) b.keys[0][pos] = k;  // else: overflow, discovery path
-            }
+        for (uint32_t i = tid; i < nk_cta; i += kFT) {
+            const uint64_t k = sm.s.kbuf[i];
+            const uint32_t d = sm.s.rng[bucket_of(k, c, half)];
+            const uint32_t pos = atomicAdd(&sm.s.dc[d], 1u);
+            if (pos < (d + 1u) * (uint32_t)kKcap) b.keys[0][pos] = k;  // else: overflow, discovery path
         }
     }
     TRACE(2);
