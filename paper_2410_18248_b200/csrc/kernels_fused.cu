@@ -42,12 +42,6 @@ struct PhaseS {                  // S, H, T, X
     unsigned long long red[3][kFW];
     uint32_t nk, base;
     unsigned long long mbar[2];  // S: TMA completion barriers of the two stage buffers
-    // planned ranges (the previous step's range plan): bucket -> range, the plan's
-    // boundaries, per-range key counts -> global cursors, and the validated totals
-    uint8_t rng[kMaxBuckets];
-    uint32_t pl[kFusedMaxGrid + 1];
-    uint32_t dc[kFusedMaxGrid];
-    uint32_t pl_n, pl_base, pl_rn, pl_r0, pl_ok;
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -452,16 +446,6 @@ __device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t d
 // shared memory in sorted order (kHeadD / kHeadW words of sm.b), so A5 needs no
 // dependent global round trip.  Returns whether those arrays are valid (not after a
 // refinement pass, which moves keys).
-// Where a planned range writes the next step's range plan: for each target position q_k
-// inside [base, base + rn) (k = 1..G-1), the first bucket whose start is >= q_k.
-struct PlanOut {
-    uint32_t* out;
-    uint32_t base, n, head, G;
-};
-__device__ __forceinline__ uint32_t plan_target(uint32_t k, uint32_t n, uint32_t head, uint32_t G) {
-    return k == 0 ? 0u : head + (uint32_t)(((uint64_t)(k - 1) * (n - head)) / (G - 1 ? G - 1 : 1));
-}
-
 constexpr uint32_t kHeadPre = 2560;
 // range_sort ranks sub-buckets of up to this many keys by comparison (one thread per
 // key, O(size) shared-memory reads): cheaper than a refinement pass for the few
@@ -476,7 +460,7 @@ template <int NI, bool HEAD>
 __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
                                            const uint32_t* T, uint32_t j_lo, uint32_t j_hi, const Cost& c,
                                            uint32_t half, unsigned long long* tr, const Pool* pool = nullptr,
-                                           uint32_t id_base_mod = 0, const PlanOut* po = nullptr) {
+                                           uint32_t id_base_mod = 0) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x;
     const uint32_t nb = j_hi - j_lo;
@@ -517,17 +501,6 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     if (tid == 0) P[nb] = ptot;
     for (uint32_t i = tid; i < ncnt; i += kFT) cnt[i] = 0;
     __syncthreads();
-    if (po && tid >= 1 && tid < po->G) {  // next step's plan entries that fall in this range
-        const uint32_t q = plan_target(tid, po->n, po->head, po->G);
-        if (q >= po->base && q < po->base + rn) {
-            uint32_t lo = 0, hi = nb;  // first bucket with start >= q (nb: the next range's first)
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if ((P[mid] & 0x3fffu) + po->base >= q) hi = mid; else lo = mid + 1;
-            }
-            po->out[tid] = j_lo + lo;
-        }
-    }
     LTRACE(1);
     uint32_t it[NI];  // counter index | order within the sub-bucket << 15
 #pragma unroll
@@ -635,35 +608,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const uint32_t half = (c.SB <= (uint32_t)kBucketM) ? (1u << c.SB) : ((c.SB - kBucketM + 1u) << kBucketM);
     const uint32_t NB = 2u * half;
     uint32_t* T = b.btot + (a.parity ? kMaxBuckets : 0);  // [NB] bucket totals of this step
-    uint32_t* dcur = b.dcur + (a.parity ? kFusedMaxGrid : 0);  // planned-range cursors of this step
-    {   // the other parity's totals / cursors are zeroed for the next step
+    {   // the other parity's totals are zeroed for the next step
         uint32_t* Tn = b.btot + (a.parity ? 0 : kMaxBuckets);
         for (uint32_t j = bid * kFT + tid; j < NB; j += G * kFT) Tn[j] = 0;
-        if (bid == 0 && tid < G) b.dcur[(a.parity ? 0 : kFusedMaxGrid) + tid] = 0;
-    }
-    // Range plan: the bucket boundaries of the ranges, computed by the previous step from its
-    // totals.  With a plan the keys go straight to their range's region of keys[0] before the
-    // first barrier (no global bucket scan, no second barrier); a range that overflows its
-    // kKcap region sends every CTA down the discovery path (X) instead.
-    const uint32_t* plan_in = b.plan + (a.parity ? 0 : kPlanWords);  // written by the previous step
-    uint32_t* plan_out = b.plan + (a.parity ? kPlanWords : 0);
-    bool planned = __ldcg(&plan_in[kPlanOk]) == 1u && !(a.flags & kStepForceFallback);
-    if (planned) {
-        for (uint32_t r = tid; r <= G; r += kFT) sm.s.pl[r] = __ldcg(&plan_in[r]);
-        for (uint32_t r = tid; r < G; r += kFT) sm.s.dc[r] = 0;
-        __syncthreads();
-        bool sparse = false;  // the plan's ranges must suit range_sort (< kSubBuckets buckets)
-        for (uint32_t r = tid; r < G; r += kFT) sparse |= sm.s.pl[r + 1] - sm.s.pl[r] >= (uint32_t)kSubBuckets;
-        planned = !__syncthreads_or(sparse);
-        if (planned)
-            for (uint32_t j = tid; j < NB; j += kFT) {  // range of bucket j: last r with pl[r] <= j
-                uint32_t lo = 0, hi = G;
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (sm.s.pl[mid] <= j) lo = mid; else hi = mid;
-                }
-                sm.s.rng[j] = (uint8_t)lo;
-            }
     }
 
     TRACE(0);
@@ -796,30 +743,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             }
 #pragma unroll
             for (int u = 0; u < kU; u++)
-                if (v[u]) {
-                    const uint32_t j = j0 + (uint32_t)u * kFT + tid;
-                    if (planned) atomicAdd(&sm.s.dc[sm.s.rng[j]], v[u]);
-                    v[u] = atomicAdd(&T[j], v[u]);
-                }
+                if (v[u]) v[u] = atomicAdd(&T[j0 + (uint32_t)u * kFT + tid], v[u]);
 #pragma unroll
             for (int u = 0; u < kU; u++) {
                 const uint32_t j = j0 + (uint32_t)u * kFT + tid;
                 if (j < NB) sm.s.cnt[j] = v[u];
             }
-        }
-    }
-    if (planned) {  // region cursors, then the keys straight into their range's region
-        __syncthreads();
-        if (tid < G) {
-            const uint32_t cd = sm.s.dc[tid];
-            sm.s.dc[tid] = tid * (uint32_t)kKcap + (cd ? atomicAdd(&dcur[tid], cd) : 0u);
-        }
-        __syncthreads();
-        for (uint32_t i = tid; i < nk_cta; i += kFT) {
-            const uint64_t k = sm.s.kbuf[i];
-            const uint32_t d = sm.s.rng[bucket_of(k, c, half)];
-            const uint32_t pos = atomicAdd(&sm.s.dc[d], 1u);
-            if (pos < (d + 1u) * (uint32_t)kKcap) b.keys[0][pos] = k;  // else: overflow, discovery path
         }
     }
     TRACE(2);
@@ -842,114 +771,69 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         for (int o = 16; o; o >>= 1) pinned_all += __shfl_xor_sync(0xffffffffu, pinned_all, o);
     }
     TRACE(4);
-    if (planned) {  // every range within its region?  totals, this range's base and size
-        if (warp == 0) {
-            uint32_t tot = 0, before = 0, mx = 0;
-            for (uint32_t r = lane; r < G; r += 32) {
-                const uint32_t v = __ldcg(&dcur[r]);
-                tot += v;
-                before += r < bid ? v : 0u;
-                mx = max(mx, v);
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                tot += __shfl_xor_sync(0xffffffffu, tot, o);
-                before += __shfl_xor_sync(0xffffffffu, before, o);
-                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            }
-            if (lane == 0) {
-                sm.s.pl_n = tot;
-                sm.s.pl_base = before;
-                sm.s.pl_ok = mx <= (uint32_t)kKcap ? 1u : 0u;
-                sm.s.pl_rn = __ldcg(&dcur[bid]);
-                sm.s.pl_r0 = __ldcg(&dcur[0]);
-            }
-        }
-        __syncthreads();
-        planned = sm.s.pl_ok != 0;
-    }
     TRACE(5);
-    uint32_t n, r_lo, r_hi, r_end0, j_lo, j_hi, src_off;
-    bool fallback;
-    if (planned) {
-        n = sm.s.pl_n;
-        r_lo = sm.s.pl_base;
-        r_hi = r_lo + sm.s.pl_rn;
-        r_end0 = sm.s.pl_r0;
-        j_lo = sm.s.pl[bid];
-        j_hi = sm.s.pl[bid + 1];
-        src_off = bid * (uint32_t)kKcap;
-        fallback = false;
-        TRACE(10); TRACE(11); TRACE(12); TRACE(6);
-        __syncthreads();  // the PhaseS fields above are read before L reuses the memory
-        TRACE(7);
-    } else {
-        // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
-        // bucket order; cursor(j) = start(j) + this CTA's offset inside bucket j
-        {
-            constexpr int kPer = (kMaxBuckets + kFT - 1) / kFT;  // 15
-            uint32_t tv[kPer];
-    #pragma unroll
-            for (int u = 0; u < kPer; u++) {
-                const uint32_t j = tid + (uint32_t)u * kFT;
-                tv[u] = j < NB ? __ldcg(&T[j]) : 0u;
-            }
-    #pragma unroll
-            for (int u = 0; u < kPer; u++) {
-                const uint32_t j = tid + (uint32_t)u * kFT;
-                if (j < NB) sm.s.start[j] = tv[u];
-            }
+
+    // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
+    // bucket order; cursor(j) = start(j) + this CTA's offset inside bucket j
+    {
+        constexpr int kPer = (kMaxBuckets + kFT - 1) / kFT;  // 15
+        uint32_t tv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; u++) {
+            const uint32_t j = tid + (uint32_t)u * kFT;
+            tv[u] = j < NB ? __ldcg(&T[j]) : 0u;
         }
-        __syncthreads();
-        TRACE(10);
-        // bucket starts = exclusive scan of the totals; scatter cursors = starts + this CTA's prefix
-        {
-            const uint32_t tot = smem_excl_scan<kFT, (kMaxBuckets + kFT - 1) / kFT>(sm.s.start, NB, sm.s.w32, sm.s.cnt);
-            if (tid == 0) sm.s.base = tot;  // total number of keys
+#pragma unroll
+        for (int u = 0; u < kPer; u++) {
+            const uint32_t j = tid + (uint32_t)u * kFT;
+            if (j < NB) sm.s.start[j] = tv[u];
         }
-        __syncthreads();
-        TRACE(11);
-        n = sm.s.base;
-        for (uint32_t i = tid; i < nk_cta; i += kFT) {
-            const uint64_t k = sm.s.kbuf[i];
-            const uint32_t pos = atomicAdd(&sm.s.cnt[bucket_of(k, c, half)], 1u);  // order within a bucket is free
-            b.keys[0][pos] = k;
-        }
-        __syncthreads();
-        TRACE(12);
-        // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
-        // bucket with start >= q_r by binary search; the largest range decides the fallback
-        uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now: key boundaries
-        uint32_t* jb = rb + (G + 1);                             // and bucket boundaries of the ranges
-        if (tid <= G) {
-            // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
-            // end of their bucket) so it can start the admission early; the other CTAs share
-            // the rest evenly
-            const uint32_t head = min(n, a.max_batch + 32u);
-            const uint32_t q = plan_target(tid, n, head, G);
-            uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
-            }
-            rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
-            jb[tid] = tid == G ? NB : lo;
-        }
-        __syncthreads();
-        uint32_t mx = 0;
-        if (tid < G) mx = rb[tid + 1] - rb[tid];
-        fallback = (a.flags & kStepForceFallback) || __syncthreads_or(mx > (uint32_t)kKcap);
-        r_lo = rb[bid]; r_hi = rb[bid + 1]; r_end0 = rb[1];
-        j_lo = jb[bid]; j_hi = jb[bid + 1];
-        src_off = r_lo;
-        if (bid == 0) {  // the range plan of the next step: these ranges
-            if (tid <= G) plan_out[tid] = jb[tid];
-            if (tid == 0) plan_out[kPlanOk] = 1u;
-        }
-        TRACE(6);
-        grid_barrier(b.flags, G, ++bar);
-        TRACE(7);
     }
+    __syncthreads();
+    TRACE(10);
+    // bucket starts = exclusive scan of the totals; scatter cursors = starts + this CTA's prefix
+    {
+        const uint32_t tot = smem_excl_scan<kFT, (kMaxBuckets + kFT - 1) / kFT>(sm.s.start, NB, sm.s.w32, sm.s.cnt);
+        if (tid == 0) sm.s.base = tot;  // total number of keys
+    }
+    __syncthreads();
+    TRACE(11);
+    const uint32_t n = sm.s.base;
+    for (uint32_t i = tid; i < nk_cta; i += kFT) {
+        const uint64_t k = sm.s.kbuf[i];
+        const uint32_t pos = atomicAdd(&sm.s.cnt[bucket_of(k, c, half)], 1u);  // order within a bucket is free
+        b.keys[0][pos] = k;
+    }
+    __syncthreads();
+    TRACE(12);
+    // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
+    // bucket with start >= q_r by binary search; the largest range decides the fallback
+    uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now: key boundaries
+    uint32_t* jb = rb + (G + 1);                             // and bucket boundaries of the ranges
+    if (tid <= G) {
+        // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
+        // end of their bucket) so it can start the admission early; the other CTAs share
+        // the rest evenly
+        const uint32_t head = min(n, a.max_batch + 32u);
+        const uint32_t q = tid == 0 ? 0u : head + (uint32_t)(((uint64_t)(tid - 1) * (n - head)) / (G - 1 ? G - 1 : 1));
+        uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
+        }
+        rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
+        jb[tid] = tid == G ? NB : lo;
+    }
+    __syncthreads();
+    uint32_t mx = 0;
+    if (tid < G) mx = rb[tid + 1] - rb[tid];
+    const bool fallback = (a.flags & kStepForceFallback) ||
+                          __syncthreads_or(mx > (uint32_t)kKcap);
+    const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
+    const uint32_t j_lo = jb[bid], j_hi = jb[bid + 1];
+    TRACE(6);
+    grid_barrier(b.flags, G, ++bar);
+    TRACE(7);
 
     // ---------------- L: sort the key ranges
     uint32_t final_buf, passes;
@@ -961,23 +845,17 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             tr[30] = rn; tr[31] = j_hi - j_lo;
             for (int q = 32; q < 64; q++) tr[q] = 0;
         }
-        const uint32_t head = min(n, a.max_batch + 32u);
-        const PlanOut po{plan_out, r_lo, n, head, G};
-        if (planned && bid == 0) {  // plan entries no range holds; the plan is complete when the step ends
-            if (tid >= 1 && tid < G && plan_target(tid, n, head, G) >= n) plan_out[tid] = NB;
-            if (tid == 0) { plan_out[0] = 0; plan_out[G] = NB; plan_out[kPlanOk] = 1u; }
-        }
         if (j_hi - j_lo < (uint32_t)kSubBuckets) {
             TRACE(13);
             if (bid == 0 && rn <= kHeadPre)
-                head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, b.keys[0] + src_off, rn, T, j_lo, j_hi,
-                                                                      c, half, tr ? tr + 16 : nullptr, &b.pool,
-                                                                      a.id_base_mod, planned ? &po : nullptr);
+                head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c,
+                                                                      half, tr ? tr + 16 : nullptr, &b.pool,
+                                                                      a.id_base_mod);
             else
-                (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + src_off, rn, T, j_lo, j_hi, c, half,
-                                                     tr ? tr + 16 : nullptr, nullptr, 0u, planned ? &po : nullptr);
-        } else {  // a sparse range over very many buckets (discovery path only): bucket runs
-            for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][src_off + i]);
+                (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
+                                                     tr ? tr + 16 : nullptr);
+        } else {  // a sparse range over very many buckets: sort the two parts by bucket runs
+            for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
             TRACE(13);
             // starving keys come first; sort the two parts separately (buckets [0, half)
             // hold the starving keys)

@@ -170,9 +170,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     Layout L;
     size_t o_soa[8];
     for (int i = 0; i < 8; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
-    // keys[0] also holds the planned ranges of the fused kernel: kFusedKcap keys per CTA
-    const size_t k0 = std::max((size_t)cap_pad + kSortTile, h->fused ? (size_t)h->fused_grid * kFusedKcap : 0);
-    size_t o_keys0 = L.take(k0 * 8);
+    size_t o_keys0 = L.take(((size_t)cap_pad + kSortTile) * 8);
     size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
     const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
     size_t o_kmask = L.take((size_t)2 * gmax * 8);
@@ -181,8 +179,6 @@ size_t carve(lamps_t* h, uint8_t* base) {
     const size_t bsum_lsd = (size_t)2 * gmax * kBins * 4;
     size_t o_bsum = L.take(bsum_lsd);
     size_t o_btot = h->fused ? L.take((size_t)2 * fused_max_buckets() * 4) : 0;
-    size_t o_plan = h->fused ? L.take((size_t)2 * kPlanWords * 4) : 0;
-    size_t o_dcur = h->fused ? L.take((size_t)2 * kFusedMaxGrid * 4) : 0;
     size_t o_ctl = L.take(sizeof(Ctl));
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
     size_t o_ai0 = L.take((size_t)mb * 8), o_ai1 = L.take((size_t)mb * 8);
@@ -212,8 +208,6 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.flags = reinterpret_cast<uint32_t*>(base + o_flags);
     h->b.blocksum = reinterpret_cast<uint32_t*>(base + o_bsum);
     h->b.btot = h->fused ? reinterpret_cast<uint32_t*>(base + o_btot) : nullptr;
-    h->b.plan = h->fused ? reinterpret_cast<uint32_t*>(base + o_plan) : nullptr;
-    h->b.dcur = h->fused ? reinterpret_cast<uint32_t*>(base + o_dcur) : nullptr;
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;
     h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);
@@ -250,7 +244,7 @@ void grids(lamps_t* h, bool query_device) {
         const uint32_t groups = (h->cap + 3) / 4;
         const uint32_t gpc = (groups + h->fused_grid - 1) / h->fused_grid;
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && gpc * 4u <= (uint32_t)kFusedKcap && fused_occ >= 1 &&
-                   h->fused_grid <= (uint32_t)kFusedMaxGrid;
+                   h->fused_grid <= 256u;  // count exchange covers up to 256 CTAs
     }
     if (!query_device) {  // size query: assume the fused path may be chosen
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && h->cap <= 148u * (uint32_t)kFusedKcap;

@@ -18,9 +18,6 @@ constexpr int kScoreThreads = 256;  // K1 CTA
 constexpr int kAdmitThreads = 1024; // K3 (single CTA)
 constexpr int kMaxBatch = 16384;
 constexpr int kFusedKcap = 10240;    // keys per SM kept in shared memory by the fused step kernel
-constexpr int kFusedMaxGrid = 256;   // fused kernel: CTAs (range plan / cursor arrays)
-constexpr int kPlanWords = kFusedMaxGrid + 4;  // [0..G] range bucket boundaries, [kPlanOk] valid flag
-constexpr int kPlanOk = kFusedMaxGrid + 3;
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
 constexpr uint32_t kStepMerge = 2u;          // StepArgs.flags: emit top-K records, no local admission
 constexpr uint32_t kMergeMaxRecords = 8192;  // world * max_batch limit of the merge kernel
@@ -79,9 +76,6 @@ struct Bufs {
     uint32_t* blocksum;      // LSD: [2][grid][kBins] digit counts
     uint32_t* btot;          // fused: [2][buckets] bucket totals by step parity; the other
                              // parity's array is zeroed during the step (zero at init)
-    uint32_t* plan;          // fused: [2][kPlanWords] range plan (bucket boundaries) written by
-                             // step s into parity s & 1, read by step s + 1
-    uint32_t* dcur;          // fused: [2][kFusedMaxGrid] planned-range key cursors by parity
     uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity
