@@ -80,5 +80,5 @@ def lib_config(cname: str, **over) -> dict:
              ticks_per_second=p["ticks_per_second"],
              starvation_threshold=c["starvation_threshold"], max_batch=c["max_batch"],
              kv_capacity_blocks=max(c["kv_total"], 1 << 20), score_bits=c["score_bits"],
-             id_bits=c["id_bits"])
+             id_bits=c["id_bits"], policy=c.get("policy", 0), score_interval=c.get("score_interval", 0))
     return d

@@ -24,6 +24,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 OK, EINVAL, ENOSPC, ENOENT = 0, -1, -2, -3
 FREE, READY, PAUSED_P, PAUSED_D, PAUSED_S = 0, 1, 2, 3, 4
 P, D, S, NONE = 0, 1, 2, 3
+POL_LAMPS, POL_FCFS, POL_SJF, POL_SJF_TOTAL = 0, 1, 2, 3
 EV_API_CALL, EV_FINISHED = 1, 2
 
 
@@ -44,7 +45,7 @@ class OCfg(ctypes.Structure):
         ("c_other", ctypes.c_uint64), ("ticks_per_second", ctypes.c_double),
         ("starvation_threshold", ctypes.c_uint32), ("max_batch", ctypes.c_uint32),
         ("kv_capacity_blocks", ctypes.c_uint64), ("score_bits", ctypes.c_uint32),
-        ("id_bits", ctypes.c_uint32),
+        ("id_bits", ctypes.c_uint32), ("policy", ctypes.c_uint32), ("score_interval", ctypes.c_uint32),
     ]
 
 
@@ -62,7 +63,10 @@ REQ_DTYPE = np.dtype([
     ("starving", np.uint32), ("strategy", np.uint32), ("cnt", np.uint32),
     ("ctx", np.uint32), ("pre_rem", np.uint32), ("api_ticks", np.uint32),
     ("resp_len", np.uint32), ("post_len", np.uint32), ("pending", np.uint32),
+    ("age", np.uint32), ("dirty", np.uint32), ("cached_score", np.uint64),
 ], align=True)
+# snapshot fields that may be absent (defaults: a fresh pool, every score to be computed)
+REQ_DEFAULTS = {"age": 0, "dirty": 1, "cached_score": 0}
 
 EVENT_DTYPE = np.dtype([("id", np.uint64), ("kind", np.uint32), ("reserved", np.uint32)], align=True)
 
@@ -90,6 +94,7 @@ def lib():
         L.o_wastes.restype = None; L.o_wastes.argtypes = [vp, u64, u64, u64, vp]
         L.o_argmin3.restype = u32; L.o_argmin3.argtypes = [vp]
         L.o_score.restype = u64; L.o_score.argtypes = [vp, vp, u32]
+        L.o_policy_score.restype = u64; L.o_policy_score.argtypes = [vp, vp]
         L.o_submit.restype = ctypes.c_int
         L.o_submit.argtypes = [vp, vp, ctypes.POINTER(u64), vp, u32, vp]
         L.o_api_return.restype = ctypes.c_int
@@ -114,7 +119,7 @@ def make_cfg(d: dict) -> OCfg:
     """Build the oracle's config struct from a plain dict of integers."""
     c = OCfg()
     for name, _ in OCfg._fields_:
-        setattr(c, name, d[name])
+        setattr(c, name, d.get(name, 0) if name in ("policy", "score_interval") else d[name])
     return c
 
 
@@ -161,6 +166,13 @@ def score(cfg: OCfg, *, ctx, pre_rem, api_ticks=0, resp_len=0, post_len=0, pendi
     return int(lib().o_score(ctypes.byref(cfg), _ptr(r), strategy))
 
 
+def policy_score(cfg: OCfg, *, pre_rem, post_len=0, api_ticks=0, has_api=1) -> int:
+    r = np.zeros(1, REQ_DTYPE)
+    r["pre_rem"], r["post_len"], r["api_ticks"], r["has_api"] = pre_rem, post_len, api_ticks, has_api
+    r["state"] = READY
+    return int(lib().o_policy_score(ctypes.byref(cfg), _ptr(r)))
+
+
 def segments(rows) -> np.ndarray:
     """rows: iterable of dicts/tuples (prompt_len, pre_len, resp_len, post_len, api_seconds, has_api)."""
     rows = list(rows)
@@ -193,7 +205,8 @@ class OraclePool:
     def load(self, fields: dict, next_id: int, prev_admitted=None):
         """Load a per-slot snapshot (dict of arrays, length capacity, incl. 'id')."""
         for f in REQ_DTYPE.names:
-            self.pool[f] = np.asarray(fields[f]).astype(REQ_DTYPE[f])
+            v = fields[f] if f in fields else REQ_DEFAULTS[f]
+            self.pool[f] = np.asarray(v).astype(REQ_DTYPE[f])
         self.next_id = int(next_id)
         self.prev_adm = np.asarray(prev_admitted if prev_admitted is not None else [], np.uint64)
 

@@ -19,6 +19,8 @@
  *   - Algorithm 1: sort, fill running batch, starvation counter . P:957-1028
  *   - starvation threshold, sticky tag, counter reset ........... P:1085
  *   - prefill cost shape k1*n^2*d ............................... P:1580
+ *   - baseline rank keys FCFS / SJF / SJF by total length ....... P:818-822
+ *   - selective score update (cached scores, refresh interval) .. P:1080
  *
  * Everything is computed with plain loops, exact 128-bit intermediates and
  * explicit clamps; sums are done by explicit summation (no closed forms), the
@@ -58,6 +60,13 @@ typedef unsigned __int128 u128;
 
 #define O_INGEST_LIMIT (1u << 24) /* reading R21: max tokens per request ingest */
 
+/* rank policies (P:818-822 baselines, P:1078 LAMPS; reading R25) */
+#define O_POL_LAMPS 0u
+#define O_POL_FCFS 1u
+#define O_POL_SJF 2u
+#define O_POL_SJF_TOTAL 3u
+#define O_MAX_INTERVAL 127u /* selective score update: refresh interval limit (R26) */
+
 typedef struct {
     uint32_t capacity;      /* pool slots */
     uint32_t block_tokens;  /* B: tokens per KV block (paged KV) */
@@ -72,6 +81,8 @@ typedef struct {
     uint64_t kv_capacity_blocks;
     uint32_t score_bits;    /* scores clamp at 2^score_bits - 1 (R22) */
     uint32_t id_bits;
+    uint32_t policy;        /* O_POL_* (R25) */
+    uint32_t score_interval; /* LAMPS selective score update: refresh every k steps (R26); 0, 1 = always */
 } ocfg;
 
 typedef struct {
@@ -83,6 +94,9 @@ typedef struct {
     uint32_t resp_len;  /* predicted API response tokens */
     uint32_t post_len;  /* predicted decode tokens after the API */
     uint32_t pending;   /* ticks of prefill / swap-in owed */
+    uint32_t age;       /* steps since the cached score was computed (R26) */
+    uint32_t dirty;     /* segment changed since (submit / API return): recompute (R26) */
+    uint64_t cached_score;
 } oreq;
 
 typedef struct {
@@ -152,6 +166,9 @@ int o_validate_cfg(const ocfg* c) {
     if (c->score_bits == 0 || c->id_bits == 0) return O_EINVAL;
     if (c->score_bits + c->id_bits + 1 > 64) return O_EINVAL;
     if (((uint64_t)1 << c->id_bits) < c->capacity) return O_EINVAL;
+    if (c->policy > O_POL_SJF_TOTAL) return O_EINVAL;
+    if (c->policy == O_POL_SJF_TOTAL && c->tau == 0) return O_EINVAL;
+    if (c->score_interval > O_MAX_INTERVAL) return O_EINVAL;
     return O_OK;
 }
 
@@ -249,6 +266,29 @@ uint64_t o_score(const ocfg* cfg, const oreq* r, uint32_t strategy) {
     return (uint64_t)(area < maxs ? area : maxs);
 }
 
+/* Baseline rank keys (reading R25), lower = earlier, clamped to 2^score_bits - 1:
+ *   FCFS      : 0 for every request, so the order is the request id, i.e. arrival
+ *               ("determines their order based on request ID")
+ *   SJF       : remaining output (decode) tokens of the current segment,
+ *               pre_rem + post_len ("based only on length")
+ *   SJF_TOTAL : SJF + the API duration in decode iterations, ceil(api_ticks / tau)
+ *               ("output length plus API duration")
+ * LAMPS is o_score. */
+uint64_t o_policy_score(const ocfg* cfg, const oreq* r) {
+    uint64_t v = 0;
+    if (cfg->policy == O_POL_SJF || cfg->policy == O_POL_SJF_TOTAL) {
+        v = r->pre_rem;
+        if (r->has_api) v = v + r->post_len;
+    }
+    if (cfg->policy == O_POL_SJF_TOTAL && r->has_api) {
+        uint64_t it = r->api_ticks / cfg->tau;
+        if (r->api_ticks % cfg->tau != 0) it = it + 1;
+        v = v + it;
+    }
+    uint64_t maxs = (cfg->score_bits >= 64) ? UINT64_MAX : (((uint64_t)1 << cfg->score_bits) - 1);
+    return v < maxs ? v : maxs;
+}
+
 /* ------------------------------------------------------------------ */
 /* ingest: submit (Alg.1) and API return (Alg.1)  */
 /* ------------------------------------------------------------------ */
@@ -303,6 +343,7 @@ int o_submit(const ocfg* cfg, oreq* pool, uint64_t* next_id, const oseg* segs, u
         r->post_len = segs[k].has_api ? segs[k].post_len : 0;
         uint64_t pf = o_t_fwd(cfg, r->ctx);
         r->pending = pf > 0xffffffffull ? 0xffffffffu : (uint32_t)pf;
+        r->dirty = 1; /* a new segment: its score is computed at the next step (R26) */
         if (ids_out) ids_out[k] = id;
     }
     *next_id += n;
@@ -367,6 +408,7 @@ int o_api_return(const ocfg* cfg, oreq* pool, const uint64_t* ids, const uint32_
         r->resp_len = next[k].has_api ? next[k].resp_len : 0;
         r->post_len = next[k].has_api ? next[k].post_len : 0;
         r->state = O_READY;
+        r->dirty = 1; /* a new segment: recompute its score (R26) */
     }
     free(ticks);
     return O_OK;
@@ -479,16 +521,31 @@ int o_step(const ocfg* cfg, oreq* pool, const uint64_t* prev_adm, uint32_t n_pre
         if (r->state == O_PAUSED_P) pinned += o_blk(r->ctx, B);
         if (r->state != O_READY) continue;
 
-        /* A1 */
+        /* A1 + A2.  LAMPS with selective score update (reading R26):
+         * a READY request keeps the strategy and score of its last computation
+         * unless its segment changed or that computation is score_interval steps
+         * old.  Baseline policies (R25) rank by their own key, always fresh; their
+         * strategy is still the argmin of Eq. (1)-(3). */
         uint64_t W[3] = {0, 0, 0};
         uint32_t strat = O_NONE;
-        if (r->has_api) {
-            o_wastes(cfg, r->ctx, r->pre_rem, r->api_ticks, W);
-            strat = o_argmin3(W);
+        uint64_t sc;
+        int fresh = cfg->policy != O_POL_LAMPS || cfg->score_interval <= 1 || r->dirty ||
+                    r->age + 1 >= cfg->score_interval;
+        if (fresh) {
+            if (r->has_api) {
+                o_wastes(cfg, r->ctx, r->pre_rem, r->api_ticks, W);
+                strat = o_argmin3(W);
+            }
+            r->strategy = strat;
+            sc = cfg->policy == O_POL_LAMPS ? o_score(cfg, r, strat) : o_policy_score(cfg, r);
+            r->cached_score = sc;
+            r->age = 0;
+            r->dirty = 0;
+        } else {
+            strat = r->strategy;
+            sc = r->cached_score;
+            r->age = r->age + 1;
         }
-        r->strategy = strat;
-        /* A2 */
-        uint64_t sc = o_score(cfg, r, strat);
         /* A3 */
         if (r->cnt >= cfg->starvation_threshold) r->starving = 1;
 
@@ -561,3 +618,4 @@ uint32_t o_sizeof_req(void) { return (uint32_t)sizeof(oreq); }
 uint32_t o_sizeof_cfg(void) { return (uint32_t)sizeof(ocfg); }
 uint32_t o_sizeof_seg(void) { return (uint32_t)sizeof(oseg); }
 uint32_t o_sizeof_summary(void) { return (uint32_t)sizeof(osummary); }
+uint32_t o_sizeof_event(void) { return (uint32_t)sizeof(oevent); }
