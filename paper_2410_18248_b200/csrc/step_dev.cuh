@@ -208,7 +208,7 @@ __device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, ui
 // One slot given its seven SoA words (A0 default update already applied by the
 // caller).  Returns true and the key if the slot is READY; updates *w (sfc).
 // exact 128-bit path (rare: large contexts or constants), kept out of line
-__device__ __forceinline__ uint32_t strategy_score_exact(uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
+static __device__ __noinline__ uint32_t strategy_score_exact(uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
                                                       uint32_t post, uint32_t pend, uint32_t has, const Cost& c,
                                                       uint64_t* sc, uint64_t* wp, uint64_t* wd, uint64_t* ws) {
     *wp = *wd = *ws = 0;
