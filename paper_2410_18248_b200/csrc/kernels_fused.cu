@@ -99,7 +99,7 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint3
 // warps: warp w owns the contiguous segment [w*32*ipt, (w+1)*32*ipt), item j of
 // lane l is position w*32*ipt + j*32 + l, so (warp, j, lane) order is array
 // order (stability).  Ranks come from a ballot multisplit (digit_peers).
-__device__ __noinline__ uint64_t* local_lsd(PhaseL& sm, uint64_t* src, uint64_t* dst, uint32_t n,
+__device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint64_t* src, uint64_t* dst, uint32_t n,
                                                unsigned long long vary) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t ipt = (n + kFT - 1) / kFT;  // items per lane, <= kLocalItems
@@ -194,7 +194,7 @@ __device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint
 // positions; sub-groups still bigger than kMaxRankM go to the next pass.  Returns
 // true if the lists overflowed or kMaxLevels passes did not finish (the caller
 // then sorts the whole part by LSD).
-__device__ __noinline__ bool refine_groups(PhaseL& sm, uint64_t* A, uint64_t* Bf, unsigned long long* xtr) {
+__device__ __forceinline__ bool refine_groups(PhaseL& sm, uint64_t* A, uint64_t* Bf, unsigned long long* xtr) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     uint32_t cur = 0;
     bool full_lsd = false;
@@ -351,7 +351,7 @@ __device__ __noinline__ bool refine_groups(PhaseL& sm, uint64_t* A, uint64_t* Bf
 // its own; one scan over the blocks of a batch gives positions; sub-groups
 // still bigger than kMaxRankM go to the next pass.  After kMaxLevels passes (or
 // if the group tables overflow) the stable LSD finishes the part.
-__device__ __noinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
+__device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
                                            const uint32_t* T, uint32_t j0, uint32_t j1,
                                            unsigned long long* tr, unsigned long long* xtr = nullptr) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)

@@ -147,7 +147,7 @@ __device__ __forceinline__ void scatter_tile(uint64_t* __restrict__ out, uint32_
 // B  each CTA reads the counts of all CTAs (digit totals) and of the CTAs
 // before it (its offsets);  C  keys are staged digit-sorted in shared memory
 // and written in coalesced runs;  grid barrier.
-static __device__ __noinline__ uint32_t lsd_sort_global(const Bufs& b, uint32_t n,
+__device__ __forceinline__ uint32_t lsd_sort_global(const Bufs& b, uint32_t n,
                                                     const unsigned long long* kmask, uint32_t nmask,
                                                     SortSmem& sm, uint32_t& bar) {
     const uint32_t tid = threadIdx.x;

@@ -207,17 +207,6 @@ __device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, ui
 
 // One slot given its seven SoA words (A0 default update already applied by the
 // caller).  Returns true and the key if the slot is READY; updates *w (sfc).
-// exact 128-bit path (rare: large contexts or constants), kept out of line
-static __device__ __noinline__ uint32_t strategy_score_exact(uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
-                                                      uint32_t post, uint32_t pend, uint32_t has, const Cost& c,
-                                                      uint64_t* sc, uint64_t* wp, uint64_t* wd, uint64_t* ws) {
-    *wp = *wd = *ws = 0;
-    uint32_t strat = STR_NONE;
-    if (has) strat = strategy_of(ctx, pre, api, c, wp, wd, ws);
-    *sc = score_of(ctx, pre, api, resp, post, pend, has, strat, c);
-    return strat;
-}
-
 template <bool DBG>
 __device__ __forceinline__ bool score_slot(const Cost& c, uint32_t id_base_mod, unsigned long long* dbg,
                                            uint32_t slot, uint32_t& w, uint32_t ctx, uint32_t pre,
@@ -230,7 +219,10 @@ __device__ __forceinline__ bool score_slot(const Cost& c, uint32_t id_base_mod, 
     if (c.fast && span < kFastCtxLimit) {
         strat = strategy_score_fast(ctx, pre, api, resp, post, pend, has, c, &sc, &wp, &wd, &ws);
     } else {
-        strat = strategy_score_exact(ctx, pre, api, resp, post, pend, has, c, &sc, &wp, &wd, &ws);
+        wp = wd = ws = 0;
+        strat = STR_NONE;
+        if (has) strat = strategy_of(ctx, pre, api, c, &wp, &wd, &ws);
+        sc = score_of(ctx, pre, api, resp, post, pend, has, strat, c);
     }
     const uint32_t cnt = sfc_cnt(w);
     const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
