@@ -126,7 +126,19 @@ typedef struct {
     uint32_t transport;               /* LAMPS_XPORT_NCCL or LAMPS_XPORT_LOOPBACK */
     const void* nccl_id;              /* 128-byte ncclUniqueId (all ranks the same; from
                                          lamps_nccl_unique_id on one rank) */
+    /* ---- rank policy ---------------------------------------- */
+    uint32_t policy;                  /* LAMPS_POLICY_*: the score field of the key (R25) */
+    uint32_t score_interval;          /* LAMPS only: selective score update (P:1080, P:1113,
+                                         R26).  0 or 1 = every step; k <= 127 = a READY
+                                         request keeps its strategy and score for k steps
+                                         unless its segment changes (submit / API return) */
 } lamps_config;
+
+/* rank policies (R25): lower key = earlier; starving requests first under all of them */
+#define LAMPS_POLICY_LAMPS 0u     /* memory-over-time area */
+#define LAMPS_POLICY_FCFS 1u      /* request id = arrival */
+#define LAMPS_POLICY_SJF 2u       /* remaining decode tokens of the segment */
+#define LAMPS_POLICY_SJF_TOTAL 3u /* + API duration in decode iterations, ceil(ticks / tau) */
 
 #define LAMPS_XPORT_NCCL 0u     /* one ncclAllGather per step over NVLink (libnccl.so.2) */
 #define LAMPS_XPORT_LOOPBACK 1u /* all shards in this process on one device: lamps_group_step */
@@ -159,7 +171,10 @@ typedef struct {
  * capacity, caller-owned host memory).  Used by lamps_pool_import /
  * lamps_pool_export for tests, benches and checkpoints.
  * dbg_w (3 per slot: W_P, W_D, W_S) and dbg_score are export-only and need
- * LAMPS_DEBUG_OUT; they hold the values of the last step for READY slots.
+ * LAMPS_DEBUG_OUT; they hold the values of the last step for READY slots (W
+ * are 0 where a cached score was reused).  age / dirty / cached_score are the
+ * selective-update state (R26); on import NULL means a fresh pool (every score
+ * computed at the next step: age 0, dirty 1, cached_score 0).
  */
 typedef struct {
     uint64_t* id;
@@ -167,6 +182,9 @@ typedef struct {
     uint32_t *ctx, *pre_rem, *api_ticks, *resp_len, *post_len, *pending;
     uint64_t* dbg_w;     /* may be NULL */
     uint64_t* dbg_score; /* may be NULL */
+    uint32_t* age;       /* may be NULL; steps since the cached score was computed, <= 127 */
+    uint32_t* dirty;     /* may be NULL; 1 = segment changed, recompute */
+    uint64_t* cached_score; /* may be NULL */
 } lamps_pool_io;
 
 /*

@@ -538,7 +538,7 @@ int o_step(const ocfg* cfg, oreq* pool, const uint64_t* prev_adm, uint32_t n_pre
             }
             r->strategy = strat;
             sc = cfg->policy == O_POL_LAMPS ? o_score(cfg, r, strat) : o_policy_score(cfg, r);
-            r->cached_score = sc;
+            if (cfg->policy == O_POL_LAMPS && cfg->score_interval > 1) r->cached_score = sc; /* the cache exists only then */
             r->age = 0;
             r->dirty = 0;
         } else {

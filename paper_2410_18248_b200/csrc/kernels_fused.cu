@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             const uint32_t st = sfc_state(w);
             if (st == ST_PP) pinned += blk(ctx, c);
             if (st == ST_READY) {
-                have = score_slot<DBG>(c, a.id_base_mod, b.dbg, slot, w, ctx, pre, sw[3 * kChunk],
+                have = score_slot<DBG>(b.pool, c, a.id_base_mod, b.dbg, slot, w, ctx, pre, sw[3 * kChunk],
                                        sw[4 * kChunk], sw[5 * kChunk], pend, key);
                 b.pool.sfc[slot] = w;
             }

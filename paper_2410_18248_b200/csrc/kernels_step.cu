@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_events(Bufs b, Cost c, StepArgs a) {
     P.pend[s] = 0u;
     const uint32_t st = strategy_of(ctx, 0, P.api[s], c);
     const uint32_t starv = sfc_starv(w);
-    P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u);
+    P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u) | (w & SFC_META);
 }
 
 // ---------------------------------------------------------------------------
@@ -142,7 +142,7 @@ __global__ void k_submit(Pool P, Cost c, const SubmitRec* rec, uint32_t n) {
     P.post[s] = r.post;
     const uint64_t f = t_fwd(r.ctx, c);  // prefill owed
     P.pend[s] = f > 0xffffffffull ? 0xffffffffu : (uint32_t)f;
-    P.sfc[s] = sfc_pack(ST_READY, r.has, 0, STR_NONE, 0);
+    P.sfc[s] = sfc_pack(ST_READY, r.has, 0, STR_NONE, 0) | SFC_DIRTY;  // a new segment (R26)
 }
 
 __global__ void k_api_return(Pool P, Cost c, const ReturnRec* rec, uint32_t n) {
@@ -171,7 +171,8 @@ __global__ void k_api_return(Pool P, Cost c, const ReturnRec* rec, uint32_t n) {
     P.api[s] = r.api;
     P.resp[s] = r.resp;
     P.post[s] = r.post;
-    P.sfc[s] = sfc_pack(ST_READY, r.has, sfc_starv(w), sfc_strat(w), sfc_cnt(w));  // RAN clear
+    // RAN clear; a new segment: its score is recomputed at the next step (R26)
+    P.sfc[s] = sfc_pack(ST_READY, r.has, sfc_starv(w), sfc_strat(w), sfc_cnt(w)) | (w & SFC_AGE_MASK) | SFC_DIRTY;
 }
 
 __global__ void k_gather_u32(const uint32_t* src, const uint32_t* slots, uint32_t* out, uint32_t n) {

@@ -149,6 +149,9 @@ const char* validate_cfg(const lamps_config* c) {
     if (c->score_bits == 0 || c->id_bits == 0 || c->score_bits + c->id_bits + 1 > 64)
         return "need score_bits, id_bits >= 1 and score_bits + id_bits + 1 <= 64";
     if (c->id_bits < 64 && (1ull << c->id_bits) < c->capacity) return "2^id_bits must be >= capacity";
+    if (c->policy > LAMPS_POLICY_SJF_TOTAL) return "unknown policy";
+    if (c->policy == LAMPS_POLICY_SJF_TOTAL && c->tau == 0) return "SJF_TOTAL needs tau >= 1";
+    if (c->score_interval > 127) return "score_interval must be <= 127";
     if (c->world > 1 || (c->flags & LAMPS_MERGE)) {
         if (c->world > 32 || c->rank >= (c->world > 1 ? c->world : 1u)) return "need rank < world <= 32";
         if ((uint64_t)c->world * c->max_batch > kMergeMaxRecords) return "world * max_batch must be <= 8192";
@@ -168,8 +171,8 @@ size_t carve(lamps_t* h, uint8_t* base) {
     const uint32_t cap_pad = h->cap_pad;
     const uint32_t mb = h->cfg.max_batch;
     Layout L;
-    size_t o_soa[8];
-    for (int i = 0; i < 8; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
+    size_t o_soa[10];  // sfc, ctx, pre, api, resp, post, pend, stamp, score cache lo / hi
+    for (int i = 0; i < 10; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
     size_t o_keys0 = L.take(((size_t)cap_pad + kSortTile) * 8);
     size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
     const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
@@ -196,9 +199,9 @@ size_t carve(lamps_t* h, uint8_t* base) {
     if (!base) return L.off;
     h->b.xsend = merge ? reinterpret_cast<MergeRec*>(base + o_xs) : nullptr;
     h->b.xrecv = merge ? reinterpret_cast<MergeRec*>(base + o_xr) : nullptr;
-    uint32_t* soa[8];
-    for (int i = 0; i < 8; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
-    h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7], cap_pad};
+    uint32_t* soa[10];
+    for (int i = 0; i < 10; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
+    h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7], soa[8], soa[9], cap_pad};
     for (int i = 1; i < 8; i++)
         if (soa[i] != soa[0] + (size_t)i * cap_pad) return 0;  // layout invariant used by the kernels
     h->b.keys[0] = reinterpret_cast<uint64_t*>(base + o_keys0);
@@ -494,6 +497,9 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     c.score_max = (cfg->score_bits >= 64) ? ~0ull : ((1ull << cfg->score_bits) - 1ull);
     c.cap = cfg->capacity; c.cap_mask = cfg->capacity - 1u;
     c.fast = fast_bounds_ok(*cfg) ? 1u : 0u;
+    c.policy = cfg->policy;
+    c.interval = cfg->score_interval;
+    c.cache = (cfg->policy == LAMPS_POLICY_LAMPS && cfg->score_interval > 1) ? 1u : 0u;
     h->hstate.assign(h->cap, H_FREE);
     auto cleanup = [&](int code, const char*) { lamps_free(h); return code; };
     if (cudaMemsetAsync(h->ws, 0, need, h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "memset");
@@ -745,9 +751,11 @@ int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uin
         const uint64_t id = io->id[s];
         if (id < id_base || id >= next_id || (id & h->cost.cap_mask) != s)
             return fail(h, LAMPS_EINVAL, "import: id outside the window or in the wrong slot");
-        if (io->has_api[s] > 1 || io->starving[s] > 1 || io->strategy[s] > 3 || io->cnt[s] > 65535)
+        if (io->has_api[s] > 1 || io->starving[s] > 1 || io->strategy[s] > 3 || io->cnt[s] > 65535 ||
+            (io->age && io->age[s] > 127) || (io->dirty && io->dirty[s] > 1))
             return fail(h, LAMPS_EINVAL, "import: field out of range");
-        sfc[s] = sfc_pack(st, io->has_api[s], io->starving[s], io->strategy[s], io->cnt[s]);
+        sfc[s] = sfc_pack(st, io->has_api[s], io->starving[s], io->strategy[s], io->cnt[s]) |
+                 ((io->age ? io->age[s] : 0u) << SFC_AGE_SHIFT) | ((io->dirty ? io->dirty[s] : 1u) ? SFC_DIRTY : 0u);
         hs[s] = st == LAMPS_READY ? H_READY : H_PAUSED;
     }
     const Pool& P = h->b.pool;
@@ -759,6 +767,14 @@ int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uin
     for (int f = 0; f < 6; f++) {
         for (uint32_t s = 0; s < cap; s++) tmp[s] = io->state[s] == LAMPS_FREE ? 0u : src[f][s];
         CU(h, cudaMemcpyAsync(dst[f], tmp.data(), (size_t)cp * 4, cudaMemcpyHostToDevice, h->stream));
+        CU(h, cudaStreamSynchronize(h->stream));
+    }
+    for (int half = 0; half < 2; half++) {  // cached scores (R26)
+        for (uint32_t s = 0; s < cap; s++) {
+            const uint64_t v = (io->cached_score && io->state[s] != LAMPS_FREE) ? io->cached_score[s] : 0ull;
+            tmp[s] = half ? (uint32_t)(v >> 32) : (uint32_t)v;
+        }
+        CU(h, cudaMemcpyAsync(half ? P.schi : P.sclo, tmp.data(), (size_t)cp * 4, cudaMemcpyHostToDevice, h->stream));
         CU(h, cudaStreamSynchronize(h->stream));
     }
     CU(h, cudaMemsetAsync(P.stamp, 0, (size_t)cp * 4, h->stream));
@@ -794,9 +810,17 @@ int lamps_pool_export(lamps_t* h, lamps_pool_io* io) {
         if (io->starving) io->starving[s] = sfc_starv(w);
         if (io->strategy) io->strategy[s] = sfc_strat(w);
         if (io->cnt) io->cnt[s] = sfc_cnt(w);
+        if (io->age) io->age[s] = sfc_age(w);
+        if (io->dirty) io->dirty[s] = (w & SFC_DIRTY) ? 1u : 0u;
         if (io->id)
             io->id[s] = sfc_state(w) == LAMPS_FREE ? 0ull
                                                     : h->id_base + ((s - h->id_base) & h->cost.cap_mask);
+    }
+    if (io->cached_score) {
+        std::vector<uint32_t> lo(cap), hi(cap);
+        CU(h, cudaMemcpy(lo.data(), P.sclo, (size_t)cap * 4, cudaMemcpyDeviceToHost));
+        CU(h, cudaMemcpy(hi.data(), P.schi, (size_t)cap * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t s = 0; s < cap; s++) io->cached_score[s] = ((uint64_t)hi[s] << 32) | lo[s];
     }
     if (io->dbg_w || io->dbg_score) {
         std::vector<unsigned long long> d((size_t)cap * 4);

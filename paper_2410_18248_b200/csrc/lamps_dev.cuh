@@ -31,6 +31,14 @@ __host__ __device__ __forceinline__ uint32_t sfc_pack(uint32_t st, uint32_t has,
 }
 
 constexpr uint32_t SFC_RAN = 1u << 7;  // admitted by the previous step (A0 pending)
+// selective score update (R26): steps since the cached score was computed, and
+// "segment changed" (set by submit / API return)
+constexpr uint32_t SFC_AGE_SHIFT = 8, SFC_AGE_MASK = 0x7fu << SFC_AGE_SHIFT;
+constexpr uint32_t SFC_DIRTY = 1u << 15;
+constexpr uint32_t SFC_META = SFC_AGE_MASK | SFC_DIRTY;
+__host__ __device__ __forceinline__ uint32_t sfc_age(uint32_t w) { return (w >> SFC_AGE_SHIFT) & 0x7fu; }
+// rank policies (R25)
+constexpr uint32_t POL_LAMPS = 0, POL_FCFS = 1, POL_SJF = 2, POL_SJF_TOTAL = 3;
 
 // Per-handle constants, passed by value as a kernel parameter (constant bank).
 struct Cost {
@@ -39,6 +47,9 @@ struct Cost {
     uint32_t SH, lgB, B, T;
     uint32_t SB, IB, cap_mask, cap;
     uint32_t fast;       // constants satisfy the 64-bit fast-path bounds (host-checked)
+    uint32_t policy;     // POL_* (R25)
+    uint32_t interval;   // selective score update interval (R26)
+    uint32_t cache;      // policy == LAMPS && interval > 1: the score cache is in use
 };
 
 // Per-slot bound of the fast path (see strategy_score_fast): ctx+pre+resp+post < 2^20.
@@ -48,6 +59,7 @@ constexpr uint64_t kFastCtxLimit = 1ull << 20;
 struct Pool {
     uint32_t *sfc, *ctx, *pre, *api, *resp, *post, *pend;
     uint32_t* stamp;  // step number at which the slot was last admitted
+    uint32_t *sclo, *schi;  // cached score (R26), low / high word
     uint32_t stride;  // words between consecutive SoA arrays (ctx == sfc + stride, ...)
 };
 

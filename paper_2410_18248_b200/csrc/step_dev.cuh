@@ -123,6 +123,52 @@ __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, ui
     return total;
 }
 
+// Baseline rank keys (R25): FCFS 0 (order = id), SJF remaining decode tokens of
+// the segment, SJF by total length + the API duration in iterations.
+__device__ __forceinline__ uint64_t policy_score(const Cost& c, uint32_t has, uint32_t pre, uint32_t post,
+                                                 uint32_t api) {
+    uint64_t v = 0;
+    if (c.policy == POL_SJF || c.policy == POL_SJF_TOTAL) v = (uint64_t)pre + (has ? post : 0u);
+    if (c.policy == POL_SJF_TOTAL && has) v += ((uint64_t)api + c.tau - 1u) / c.tau;
+    return v < c.score_max ? v : c.score_max;
+}
+
+// A1 + A2 of one READY slot under the configured policy and the selective score
+// update (R25, R26): a cached (strategy, score) is reused unless the segment
+// changed or it is `interval` steps old.  meta = the slot's new age / dirty bits.
+__device__ __forceinline__ uint32_t strategy_score(const Pool& P, const Cost& c, uint32_t slot, uint32_t w,
+                                                   uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
+                                                   uint32_t post, uint32_t pend, uint64_t& sc, uint64_t& wp,
+                                                   uint64_t& wd, uint64_t& ws, uint32_t& meta) {
+    if (c.cache) {
+        const uint32_t age = sfc_age(w);
+        if (!(w & SFC_DIRTY) && age + 1u < c.interval) {
+            sc = ((uint64_t)P.schi[slot] << 32) | P.sclo[slot];
+            wp = wd = ws = 0;
+            meta = (age + 1u) << SFC_AGE_SHIFT;
+            return sfc_strat(w);
+        }
+    }
+    const uint32_t has = sfc_has(w);
+    uint32_t strat;
+    const uint64_t span = (uint64_t)ctx + pre + (has ? (uint64_t)resp + post : 0ull);
+    if (c.fast && span < kFastCtxLimit) {
+        strat = strategy_score_fast(ctx, pre, api, resp, post, pend, has, c, &sc, &wp, &wd, &ws);
+    } else {
+        wp = wd = ws = 0;
+        strat = STR_NONE;
+        if (has) strat = strategy_of(ctx, pre, api, c, &wp, &wd, &ws);
+        sc = score_of(ctx, pre, api, resp, post, pend, has, strat, c);
+    }
+    if (c.policy != POL_LAMPS) sc = policy_score(c, has, pre, post, api);
+    if (c.cache) {
+        P.sclo[slot] = (uint32_t)sc;
+        P.schi[slot] = (uint32_t)(sc >> 32);
+    }
+    meta = 0;
+    return strat;
+}
+
 // One group of four consecutive slots g*4..g*4+3 (128-bit loads of the SoA).
 // A0 (fused): slots admitted by the previous step (SFC_RAN) generated one
 // token: ctx += 1, pre_rem -= 1 (floor 0), pending = 0.
@@ -173,22 +219,15 @@ __device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, ui
         if (st != ST_READY) continue;
         any_ready = true;
         const uint32_t has = sfc_has(w);
+        const uint32_t slot = 4u * g + (uint32_t)j;
         uint64_t wp, wd, ws, sc;
-        uint32_t strat;
-        const uint64_t span = (uint64_t)cv[j] + prv[j] + (has ? (uint64_t)rsv[j] + pov[j] : 0ull);
-        if (c.fast && span < kFastCtxLimit) {
-            strat = strategy_score_fast(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, c, &sc, &wp, &wd, &ws);
-        } else {
-            wp = wd = ws = 0;
-            strat = STR_NONE;
-            if (has) strat = strategy_of(cv[j], prv[j], apv[j], c, &wp, &wd, &ws);
-            sc = score_of(cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], has, strat, c);
-        }
+        uint32_t meta;
+        const uint32_t strat = strategy_score(P, c, slot, w, cv[j], prv[j], apv[j], rsv[j], pov[j], pev[j], sc,
+                                              wp, wd, ws, meta);
         const uint32_t cnt = sfc_cnt(w);
         const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
         const uint32_t cnt2 = cnt < 65535u ? cnt + 1u : 65535u;
-        wv[j] = sfc_pack(ST_READY, has, starv, strat, cnt2);
-        const uint32_t slot = 4u * g + (uint32_t)j;
+        wv[j] = sfc_pack(ST_READY, has, starv, strat, cnt2) | meta;
         const uint32_t idoff = (slot - id_base_mod) & c.cap_mask;
         // keys are packed to the front of key[] in slot order (predicated, no dynamic index)
         const uint64_t k = ((uint64_t)(starv ^ 1u) << key_top) | (sc << c.IB) | idoff;
@@ -208,25 +247,17 @@ __device__ __forceinline__ uint32_t score_group(const Pool& P, const Cost& c, ui
 // One slot given its seven SoA words (A0 default update already applied by the
 // caller).  Returns true and the key if the slot is READY; updates *w (sfc).
 template <bool DBG>
-__device__ __forceinline__ bool score_slot(const Cost& c, uint32_t id_base_mod, unsigned long long* dbg,
-                                           uint32_t slot, uint32_t& w, uint32_t ctx, uint32_t pre,
-                                           uint32_t api, uint32_t resp, uint32_t post, uint32_t pend,
-                                           uint64_t& key) {
+__device__ __forceinline__ bool score_slot(const Pool& P, const Cost& c, uint32_t id_base_mod,
+                                           unsigned long long* dbg, uint32_t slot, uint32_t& w, uint32_t ctx,
+                                           uint32_t pre, uint32_t api, uint32_t resp, uint32_t post,
+                                           uint32_t pend, uint64_t& key) {
     const uint32_t has = sfc_has(w);
     uint64_t wp, wd, ws, sc;
-    uint32_t strat;
-    const uint64_t span = (uint64_t)ctx + pre + (has ? (uint64_t)resp + post : 0ull);
-    if (c.fast && span < kFastCtxLimit) {
-        strat = strategy_score_fast(ctx, pre, api, resp, post, pend, has, c, &sc, &wp, &wd, &ws);
-    } else {
-        wp = wd = ws = 0;
-        strat = STR_NONE;
-        if (has) strat = strategy_of(ctx, pre, api, c, &wp, &wd, &ws);
-        sc = score_of(ctx, pre, api, resp, post, pend, has, strat, c);
-    }
+    uint32_t meta;
+    const uint32_t strat = strategy_score(P, c, slot, w, ctx, pre, api, resp, post, pend, sc, wp, wd, ws, meta);
     const uint32_t cnt = sfc_cnt(w);
     const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
-    w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u);
+    w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u) | meta;
     key = ((uint64_t)(starv ^ 1u) << (c.SB + c.IB)) | (sc << c.IB) | ((slot - id_base_mod) & c.cap_mask);
     if (DBG) {
         unsigned long long* d = dbg + 4ull * slot;

@@ -19,6 +19,7 @@ LAMPS_FREE, LAMPS_READY, LAMPS_PAUSED_P, LAMPS_PAUSED_D, LAMPS_PAUSED_S = 0, 1, 
 LAMPS_PRESERVE, LAMPS_DISCARD, LAMPS_SWAP, LAMPS_NONE = 0, 1, 2, 3
 LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
 LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE, LAMPS_MERGE = 1, 2, 4, 8, 16, 32
+LAMPS_POLICY_LAMPS, LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL = 0, 1, 2, 3
 LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK = 0, 1
 
 u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
@@ -39,7 +40,7 @@ class lamps_config(ctypes.Structure):
                 ("ticks_per_second", dbl), ("starvation_threshold", u32), ("max_batch", u32),
                 ("kv_capacity_blocks", u64), ("score_bits", u32), ("id_bits", u32),
                 ("stream", vp), ("flags", u32), ("world", u32), ("rank", u32), ("transport", u32),
-                ("nccl_id", vp)]
+                ("nccl_id", vp), ("policy", u32), ("score_interval", u32)]
 
 
 class lamps_step_out(ctypes.Structure):
@@ -54,7 +55,8 @@ class lamps_step_out(ctypes.Structure):
 class lamps_pool_io(ctypes.Structure):
     _fields_ = [("id", vp), ("state", vp), ("has_api", vp), ("starving", vp), ("strategy", vp),
                 ("cnt", vp), ("ctx", vp), ("pre_rem", vp), ("api_ticks", vp), ("resp_len", vp),
-                ("post_len", vp), ("pending", vp), ("dbg_w", vp), ("dbg_score", vp)]
+                ("post_len", vp), ("pending", vp), ("dbg_w", vp), ("dbg_score", vp),
+                ("age", vp), ("dirty", vp), ("cached_score", vp)]
 
 
 SEGMENT_DTYPE = np.dtype([("prompt_len", np.uint32), ("pre_len", np.uint32), ("resp_len", np.uint32),
@@ -322,14 +324,20 @@ class Scheduler:
         keep = {"id": np.ascontiguousarray(np.asarray(fields["id"])[:cap], np.uint64)}
         for f in POOL_U32_FIELDS:
             keep[f] = np.ascontiguousarray(np.asarray(fields[f])[:cap], np.uint32)
+        for f in ("age", "dirty"):  # selective-update state (optional: a fresh pool)
+            if f in fields:
+                keep[f] = np.ascontiguousarray(np.asarray(fields[f])[:cap], np.uint32)
+        if "cached_score" in fields:
+            keep["cached_score"] = np.ascontiguousarray(np.asarray(fields["cached_score"])[:cap], np.uint64)
         io = lamps_pool_io(**{k: _p(v) for k, v in keep.items()})
         self._check(lib().lamps_pool_import(self.h, ctypes.byref(io), int(id_base), int(next_id)))
 
     def export_pool(self, debug: bool = False) -> dict:
         cap = self.capacity
         out = {"id": np.zeros(cap, np.uint64)}
-        for f in POOL_U32_FIELDS:
+        for f in POOL_U32_FIELDS + ("age", "dirty"):
             out[f] = np.zeros(cap, np.uint32)
+        out["cached_score"] = np.zeros(cap, np.uint64)
         io = lamps_pool_io(**{k: _p(v) for k, v in out.items()})
         if debug:
             out["dbg_w"] = np.zeros(3 * cap, np.uint64)

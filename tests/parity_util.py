@@ -5,7 +5,7 @@ import gen
 import oracle as O
 
 FIELDS = ("state", "has_api", "starving", "strategy", "cnt", "ctx", "pre_rem", "api_ticks",
-          "resp_len", "post_len", "pending")
+          "resp_len", "post_len", "pending", "age", "dirty")
 
 
 PATH_FLAGS = {"fused": 0, "multi": 4, "fallback": 8}  # LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK
@@ -61,6 +61,8 @@ def compare_state(s, o, r=None, where=""):
             raise AssertionError(f"{where}: field {f} differs at live slots {np.nonzero(live)[0][bad]}: "
                                  f"gpu {a[bad]} oracle {b[bad]}")
     assert np.array_equal(e["id"][live], P["id"][live]), where
+    if o.cfg.policy == O.POL_LAMPS and o.cfg.score_interval > 1:  # the score cache (R26)
+        assert np.array_equal(e["cached_score"][live], P["cached_score"][live]), (where, "cached_score")
     if r is not None and "W_P" in r:
         ready = P["state"] == O.READY
         for f in ("W_P", "W_D", "W_S", "score"):
@@ -72,7 +74,9 @@ def compare_state(s, o, r=None, where=""):
 
 
 def snapshot_step_parity(cname, seed=0, id_base=0, steps=3, debug=True, path="fused", **over):
-    cfg = gen.lib_config(cname, **{k: v for k, v in over.items() if k in ("max_batch", "starvation_threshold", "score_bits", "id_bits")})
+    cfg = gen.lib_config(cname, **{k: v for k, v in over.items()
+                                   if k in ("max_batch", "starvation_threshold", "score_bits", "id_bits", "policy",
+                                            "score_interval")})
     snap = gen.snapshot(cname, seed=seed, id_base=id_base,
                         **{k: v for k, v in over.items() if k in ("n", "capacity")})
     if "capacity" in over:
