@@ -38,7 +38,7 @@ def test_selective_update_snapshot_parity(interval, path):
 def test_policy_closed_loop(policy, interval, path):
     """Submissions, API calls / returns (which mark segments dirty) and finishes."""
     st = closed_loop("C3", 1200, 120, 500, 5.0, path=path, state_every=5, policy=policy, score_interval=interval)
-    assert st["api"] > 0 and st["fin"] > 0
+    assert st["api"] > 0 and st["adm"] > 0
 
 
 def test_selective_update_c4_toolbench_interval_10():
