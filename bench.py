@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-variants", action="store_true", help="skip the policy / selective-update variants")
     ap.add_argument("--merge", action="store_true",
                     help="N=1: run the multi-shard exchange + merge over a 1-rank NCCL communicator")
     return ap.parse_args()
@@ -325,6 +326,38 @@ def run_ours(args, rank, world, local):
         dt_e2e, ne_e2e = float(mx.item()), float(sm.item())
     e2e_value = ne_e2e / dt_e2e
 
+    # ---- variants: the same pool and timing under the selective score
+    # update (interval 10, the paper's ToolBench setting) and the baseline keys
+    variants = []
+    if world == 1 and not args.no_variants:
+        from paper_2410_18248_b200.lamps import LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL
+        for name, over in (("lamps_interval_10", dict(score_interval=10)),
+                           ("sjf", dict(policy=LAMPS_POLICY_SJF)),
+                           ("sjf_total", dict(policy=LAMPS_POLICY_SJF_TOTAL)),
+                           ("fcfs", dict(policy=LAMPS_POLICY_FCFS))):
+            vcfg = dict(cfg); vcfg.update(over)
+            sv = Scheduler(vcfg, stream=stream)
+            sv.import_pool(snap, snap["id_base"], snap["next_id"])
+            for _ in range(args.warmup):
+                flush.zero_()
+                sv.step_async(kv)
+            sv.import_pool(snap, snap["id_base"], snap["next_id"])
+            nsteps = max(args.steps, 10)
+            ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
+            ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
+            torch.cuda.synchronize()
+            for k in range(nsteps):
+                flush.zero_()
+                ev0[k].record(stream)
+                sv.step_async(kv)
+                ev1[k].record(stream)
+            torch.cuda.synchronize()
+            vms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1)) / nsteps
+            vres = sv.result()
+            variants.append({"name": name, **over, "us_per_step": vms * 1e3,
+                             "decisions_per_s": vres["n_eligible"] / (vms / 1e3), "steps": nsteps})
+            sv.close()
+
     if rank == 0:
         peak, peak_src = measured_peak_hbm()
         # algorithmic bytes of one step: the SoA is read once (28 B/slot),
@@ -383,6 +416,8 @@ def run_ours(args, rank, world, local):
                     "ms_per_step": 1e3 * dt_e2e / e2e_steps,
                     "path": "lamps_api_return + lamps_schedule_step + lamps_submit (host buffers)"},
         }
+        if variants:
+            line["variants"] = variants
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(cname)
         print(json.dumps(line), flush=True)
