@@ -73,6 +73,11 @@ extern "C" {
 #define LAMPS_MERGE 32u         /* world <= 1: still run the multi-shard exchange + merge over a 1-rank
                                    NCCL communicator (transport NCCL, nccl_id required); tests the
                                    NCCL path on one GPU */
+#define LAMPS_HEAD_ONLY 64u     /* top-K fast path: rank only the head of the order the
+                                   admission can reach (>= min(n_eligible, max_batch) keys, to the end
+                                   of a bucket).  Admitted set, preempted list, counters and pool
+                                   state are those of the full pass; lamps_ranked_keys returns the
+                                   head only.  Fused path; the 3-kernel path ranks everything */
 
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 
@@ -262,7 +267,8 @@ int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uin
 /* lamps_pool_export -- copy the pool (and debug values if requested) to io. */
 int lamps_pool_export(lamps_t* h, lamps_pool_io* io);
 
-/* Copy the last step's ranked keys (n_eligible of them) to host memory. */
+/* Copy the last step's ranked keys (n_eligible of them, or the head only under
+ * LAMPS_HEAD_ONLY; *n_out receives the count) to host memory. */
 int lamps_ranked_keys(lamps_t* h, uint64_t* host_out, uint64_t max_keys, uint64_t* n_out);
 
 /*

@@ -42,6 +42,7 @@ struct PhaseS {                  // S, H, T, X
     unsigned long long red[3][kFW];
     uint32_t nk, base;
     unsigned long long mbar[2];  // S: TMA completion barriers of the two stage buffers
+    uint32_t hb_j, hb_r;         // head-only mode: first bucket past the head, its start
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -799,9 +800,29 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     __syncthreads();
     TRACE(11);
     const uint32_t n = sm.s.base;
+    // head-only mode (F3): only the buckets of CTA 0's range -- the head the admission can
+    // reach -- are scattered and sorted; the other CTAs are done after the next barrier
+    bool head_only = false;
+    if (a.flags & kStepHeadOnly) {
+        if (tid == 0) {
+            const uint32_t head = min(n, a.max_batch + 32u);
+            uint32_t lo = 0, hi = NB;  // first bucket with start >= head
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sm.s.start[mid] >= head) hi = mid; else lo = mid + 1;
+            }
+            sm.s.hb_j = lo;
+            sm.s.hb_r = lo == NB ? n : sm.s.start[lo];
+        }
+        __syncthreads();
+        head_only = sm.s.hb_r <= (uint32_t)kKcap && !(a.flags & kStepForceFallback);
+    }
+    const uint32_t jcut = head_only ? sm.s.hb_j : NB;
     for (uint32_t i = tid; i < nk_cta; i += kFT) {
         const uint64_t k = sm.s.kbuf[i];
-        const uint32_t pos = atomicAdd(&sm.s.cnt[bucket_of(k, c, half)], 1u);  // order within a bucket is free
+        const uint32_t j = bucket_of(k, c, half);
+        if (j >= jcut) continue;
+        const uint32_t pos = atomicAdd(&sm.s.cnt[j], 1u);  // order within a bucket is free
         b.keys[0][pos] = k;
     }
     __syncthreads();
@@ -810,7 +831,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // bucket with start >= q_r by binary search; the largest range decides the fallback
     uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now: key boundaries
     uint32_t* jb = rb + (G + 1);                             // and bucket boundaries of the ranges
-    if (tid <= G) {
+    if (head_only) {  // one range: [0, hb_r) in buckets [0, hb_j), sorted by CTA 0
+        if (tid <= G) {
+            rb[tid] = tid == 0 ? 0u : sm.s.hb_r;
+            jb[tid] = tid == 0 ? 0u : sm.s.hb_j;
+        }
+    } else if (tid <= G) {
         // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
         // end of their bucket) so it can start the admission early; the other CTAs share
         // the rest evenly
@@ -896,6 +922,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         ctl->n_passes = passes;
         ctl->final_buf = final_buf;
         ctl->fallbacks += fallback ? 1u : 0u;
+        ctl->n_ranked = head_only ? r_end0 : n;  // head-only: keys [0, hb_r) are ranked
     }
     TRACE(15);
     const uint64_t* head = wait ? b.keys[final_buf] : sm.l.a;  // CTA 0 holds [0, need) itself unless it waited

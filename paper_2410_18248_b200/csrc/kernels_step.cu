@@ -123,8 +123,10 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Bufs b, Cost c, StepArg
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kAdmitThreads) k_admit(Bufs b, Cost c, StepArgs a) {
     __shared__ AdmitSmem sm;
-    const Ctl* ctl = b.ctl;
-    admit_cta(b, c, a, b.keys[ctl->final_buf & 1u], ctl->n_elig, ctl->pinned, sm);
+    Ctl* ctl = b.ctl;
+    const uint32_t n = ctl->n_elig;
+    admit_cta(b, c, a, b.keys[ctl->final_buf & 1u], n, ctl->pinned, sm);
+    if (threadIdx.x == 0) ctl->n_ranked = n;  // the 3-kernel path ranks everything
 }
 
 // ---------------------------------------------------------------------------

@@ -335,6 +335,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.world = h->world;
     a.rank = h->rank;
     if (h->merge) a.flags |= kStepMerge;
+    if (h->cfg.flags & LAMPS_HEAD_ONLY) a.flags |= kStepHeadOnly;
     return a;
 }
 
@@ -838,7 +839,7 @@ int lamps_ranked_keys(lamps_t* h, uint64_t* host_out, uint64_t max_keys, uint64_
     if (!h || !n_out) return LAMPS_EINVAL;
     CU(h, cudaMemcpyAsync(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
-    const uint64_t n = h->h_ctl->n_elig_out;
+    const uint64_t n = h->h_ctl->n_ranked;  // n_eligible, or the head only (LAMPS_HEAD_ONLY)
     *n_out = n;
     if (host_out && max_keys) {
         const uint64_t m = std::min(n, max_keys);

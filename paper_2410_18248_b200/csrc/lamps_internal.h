@@ -20,6 +20,7 @@ constexpr int kMaxBatch = 16384;
 constexpr int kFusedKcap = 10240;    // keys per SM kept in shared memory by the fused step kernel
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
 constexpr uint32_t kStepMerge = 2u;          // StepArgs.flags: emit top-K records, no local admission
+constexpr uint32_t kStepHeadOnly = 4u;       // StepArgs.flags: rank only the admission head (F3)
 constexpr uint32_t kMergeMaxRecords = 8192;  // world * max_batch limit of the merge kernel
 
 // multi-GPU exchange: per rank one header followed by K records (32 B each)
@@ -53,6 +54,8 @@ struct Ctl {
     uint32_t n_admitted, n_preempted, blocked_head, n_prev;
     unsigned long long budget, budget_used;
     unsigned long long n_elig_out, pinned_out;
+    uint32_t n_ranked;               // keys of the ranked order available in keys[final_buf]
+    uint32_t pad1;
 };
 
 struct StepArgs {
@@ -64,7 +67,7 @@ struct StepArgs {
     uint32_t n_ev;
     uint32_t max_batch;
     uint32_t parity;        // admitted list buffer written this step
-    uint32_t flags;         // kStepForceFallback, kStepMerge
+    uint32_t flags;         // kStepForceFallback, kStepMerge, kStepHeadOnly
     uint32_t world, rank;   // multi-GPU shards
 };
 

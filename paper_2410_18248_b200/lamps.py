@@ -19,6 +19,7 @@ LAMPS_FREE, LAMPS_READY, LAMPS_PAUSED_P, LAMPS_PAUSED_D, LAMPS_PAUSED_S = 0, 1, 
 LAMPS_PRESERVE, LAMPS_DISCARD, LAMPS_SWAP, LAMPS_NONE = 0, 1, 2, 3
 LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
 LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE, LAMPS_MERGE = 1, 2, 4, 8, 16, 32
+LAMPS_HEAD_ONLY = 64
 LAMPS_POLICY_LAMPS, LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL = 0, 1, 2, 3
 LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK = 0, 1
 

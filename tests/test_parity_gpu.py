@@ -16,7 +16,7 @@ from parity_util import (compare_outputs, compare_state, load_both, make_pair, s
 pytestmark = pytest.mark.gpu
 
 
-PATHS = ["fused", "multi", "fallback"]
+PATHS = ["fused", "multi", "fallback", "head"]
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -29,7 +29,7 @@ def test_snapshot_parity(cname, seed, id_base, path):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("path", ["fused", "multi"])
+@pytest.mark.parametrize("path", ["fused", "multi", "head"])
 def test_c5_full_size_parity(path):
     # BASELINE.json's 1M-request pool in the launch configuration bench.py times
     snapshot_step_parity("C5", seed=0, id_base=(1 << 20) * 7 + 99, steps=2, path=path)
@@ -49,7 +49,7 @@ def test_tiny_capacity(cap, path):
     snapshot_step_parity("C1", seed=cap, n=cap, capacity=cap, steps=3, path=path)
 
 
-@pytest.mark.parametrize("path", ["fused", "multi"])
+@pytest.mark.parametrize("path", ["fused", "multi", "head"])
 def test_equal_scores_large_bucket(path):
     # 40000 identical requests: one bucket far larger than a shared-memory range,
     # so the fused kernel must take its in-kernel global LSD fallback; order = ids
