@@ -331,12 +331,15 @@ def run_ours(args, rank, world, local):
     variants = []
     if world == 1 and not args.no_variants:
         from paper_2410_18248_b200.lamps import LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL
-        for name, over in (("lamps_interval_10", dict(score_interval=10)),
+        from paper_2410_18248_b200 import LAMPS_HEAD_ONLY
+        for name, over in (("head_only", dict(flags=LAMPS_HEAD_ONLY)),
+                           ("head_only_interval_10", dict(flags=LAMPS_HEAD_ONLY, score_interval=10)),
+                           ("lamps_interval_10", dict(score_interval=10)),
                            ("sjf", dict(policy=LAMPS_POLICY_SJF)),
                            ("sjf_total", dict(policy=LAMPS_POLICY_SJF_TOTAL)),
                            ("fcfs", dict(policy=LAMPS_POLICY_FCFS))):
-            vcfg = dict(cfg); vcfg.update(over)
-            sv = Scheduler(vcfg, stream=stream)
+            vcfg = dict(cfg); vcfg.update({k: v for k, v in over.items() if k != "flags"})
+            sv = Scheduler(vcfg, flags=over.get("flags", 0), stream=stream)
             sv.import_pool(snap, snap["id_base"], snap["next_id"])
             for _ in range(args.warmup):
                 flush.zero_()
