@@ -82,15 +82,20 @@ union FusedSmem {
     SortSmem g;
 };
 
+// Bucket of a key: (starving flag, bit length e of v = the key's score|id bits, the
+// next kBucketM bits of v) -- a float-like, exact monotone function of the key.  Over
+// v rather than the score alone, so keys whose scores are equal or small (FCFS: all 0)
+// still spread by id.
 __device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint32_t half) {
-    const uint32_t ns = (uint32_t)(key >> (c.SB + c.IB)) & 1u;  // 1 = not starving
-    const uint64_t sc = (key >> c.IB) & c.score_max;
-    const uint32_t e = 64u - (uint32_t)__clzll((long long)sc);  // bit length
+    const uint32_t vb = c.SB + c.IB;
+    const uint32_t ns = (uint32_t)(key >> vb) & 1u;  // 1 = not starving
+    const uint64_t v = key & ((1ull << vb) - 1ull);
+    const uint32_t e = 64u - (uint32_t)__clzll((long long)v);  // bit length
     uint32_t fb;
     if (e <= (uint32_t)kBucketM)
-        fb = (uint32_t)sc;
+        fb = (uint32_t)v;
     else
-        fb = ((e - kBucketM) << kBucketM) + (uint32_t)((sc >> (e - 1 - kBucketM)) & ((1u << kBucketM) - 1));
+        fb = ((e - kBucketM) << kBucketM) + (uint32_t)((v >> (e - 1 - kBucketM)) & ((1u << kBucketM) - 1));
     return ns * half + fb;
 }
 
@@ -423,13 +428,17 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
 __device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t db, const Cost& c,
                                               uint32_t half, uint32_t lg_cap) {
     const uint32_t fb = J >= half ? J - half : J;
+    if (fb < (1u << kBucketM)) return 0u;  // exact bucket: one key
+    const uint32_t ls = (fb >> kBucketM) - 1u;  // varying low bits of v: e - 1 - kBucketM
     const uint64_t idoff = k & (uint64_t)c.cap_mask;
-    uint64_t v = idoff;
-    uint32_t wv = lg_cap;
-    if (fb >= (1u << kBucketM)) {
-        const uint32_t ls = (fb >> kBucketM) - 1u;  // e - 1 - kBucketM, e = (fb >> kBucketM) + kBucketM
-        v |= ((k >> c.IB) & ((1ull << ls) - 1ull)) << lg_cap;
-        wv += ls;
+    uint64_t v;
+    uint32_t wv;
+    if (ls > c.IB) {  // varying score bits, then the id offset packed into lg_cap bits
+        v = (((k >> c.IB) & ((1ull << (ls - c.IB)) - 1ull)) << lg_cap) | idoff;
+        wv = ls - c.IB + lg_cap;
+    } else {          // id bits only; those above lg_cap are always 0
+        wv = ls < lg_cap ? ls : lg_cap;
+        v = idoff & ((1ull << wv) - 1ull);
     }
     return wv >= db ? (uint32_t)(v >> (wv - db)) : (uint32_t)(v << (db - wv));
 }
@@ -606,7 +615,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     Ctl* ctl = b.ctl;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t G = gridDim.x, bid = blockIdx.x;
-    const uint32_t half = (c.SB <= (uint32_t)kBucketM) ? (1u << c.SB) : ((c.SB - kBucketM + 1u) << kBucketM);
+    const uint32_t vbits = c.SB + c.IB;  // buckets over the key's score|id bits (bucket_of)
+    const uint32_t half = (vbits <= (uint32_t)kBucketM) ? (1u << vbits) : ((vbits - kBucketM + 1u) << kBucketM);
     const uint32_t NB = 2u * half;
     uint32_t* T = b.btot + (a.parity ? kMaxBuckets : 0);  // [NB] bucket totals of this step
     {   // the other parity's totals are zeroed for the next step
