@@ -177,3 +177,28 @@ def requests(cname: str, n: int, seed: int = 0, **over) -> list:
             segs.append((int(10 * rng.integers(0, 50) + 5), d, int(resp[k])))
         out.append(dict(prompt=int(prompt[k]), segs=segs, final=int(rng.integers(1, 201))))
     return out
+
+
+def truths(cname: str, n: int, seed: int = 0, bins: bool = False, key0: int = 0, **over) -> dict:
+    """Measured values of n first segments for the predictor ingest (row F4), as plain
+    arrays (the caller packs them into its own record type): prompt, pre_len (or the
+    predictor's bin b with pre_len = 0 when bins=True), resp_len, post_len, api_ticks
+    (quantised measured duration, 1 us ticks), has_api, key = key0 + index."""
+    c = dict(CONFIGS[cname]); c.update(over)
+    rng = rng_for(cname, 104729 + seed)
+    med, sig, lo, hi = c["prompt"]
+    prompt = _lognormal_clip(rng, n, med, sig, lo, hi)
+    b = rng.integers(0, 50, n)
+    ci, dur_s, resp, num = _class_arrays(rng, n, c["classes"])
+    has = (rng.random(n) >= 0.1).astype(np.int64)
+    post = rng.integers(1, 201, n)
+    return {
+        "key": key0 + np.arange(n, dtype=np.int64),
+        "prompt_len": prompt,
+        "pre_len": np.zeros(n, np.int64) if bins else 10 * b + 5 + rng.integers(-4, 5, n),
+        "pre_bin": b if bins else np.full(n, 0xFFFFFFFF, np.int64),
+        "resp_len": np.where(has == 1, resp, 0),
+        "post_len": np.where(has == 1, post, 0),
+        "api_ticks": np.where(has == 1, np.rint(dur_s * 1e6).astype(np.int64), 0),
+        "has_api": has,
+    }

@@ -322,6 +322,65 @@ int lamps_nccl_unique_id(void* out128);
 int lamps_group_step(lamps_t* const* h, uint32_t world, const lamps_event* const* ev,
                      const uint32_t* n_ev, const uint64_t* kv_total, lamps_step_out* out);
 
+/* ---- predictor ingest and error injection ---------------- */
+
+#define LAMPS_NO_BIN 0xffffffffu
+#define LAMPS_BIN_TOKENS 10u   /* predictor bins of 10 tokens */
+#define LAMPS_MAX_BIN 49u      /* 50 bins */
+
+/*
+ * What is known about one segment before prediction: the measured values of
+ * a trace (the INFERCEPT datasets carry them) or, for the length,
+ * the length predictor's bin (the classifier itself -- OPT-125M +
+ * a linear head -- needs trained weights and is out of scope).
+ */
+typedef struct {
+    uint64_t key;        /* RNG stream of this record (e.g. the trace index); < 2^57 */
+    uint32_t prompt_len; /* copied to the output */
+    uint32_t pre_len;    /* measured decode tokens before the API (or in total) */
+    uint32_t pre_bin;    /* LAMPS_NO_BIN, or the predictor's bin b <= LAMPS_MAX_BIN:
+                            the length is the bin's midpoint 10 b + 5 */
+    uint32_t resp_len;   /* API response tokens (has_api), copied */
+    uint32_t post_len;   /* measured decode tokens after the API (has_api) */
+    uint32_t api_ticks;  /* measured API duration in ticks, already quantised (R22) (has_api) */
+    uint32_t has_api;    /* 0 or 1 */
+    uint32_t reserved;   /* must be 0 */
+} lamps_truth;
+
+/*
+ * Error injection of the paper's prediction study:
+ * predicted = measured + error, error ~ N(0, p * measured), applied to the
+ * output lengths (pre_len and post_len, p = len_error_ppm / 1e6) and to the API
+ * duration (p = api_error_ppm / 1e6), clamped at 0 (reading R27).  The normal
+ * draw is integer and counter-based, so it is reproducible bit for bit:
+ *   w_k = splitmix64 output number n = (key*4 + field)*32 + k + 1 from `seed`
+ *         (state seed + n * 0x9E3779B97F4A7C15, the standard finaliser),
+ *         field 0 = pre_len, 1 = post_len, 2 = api_ticks, k = 0..16;
+ *   X = sum_{k<16} popcount(w_k)  (Binomial(1024, 1/2): mean 512, sd 16);
+ *   Z = (X - 512) * 2^16 + (w_16 >> 48) - 2^15   (z = Z / 2^20, sd ~ 1; the low
+ *       term is a uniform dither across one binomial step);
+ *   error = round-half-away(p_ppm * m * Z / (1e6 * 2^20)), exact 128-bit;
+ *   predicted = min(max(m + error, 0), 2^24 (lengths) or 2^32 - 1 (ticks)).
+ */
+typedef struct {
+    uint64_t seed;
+    uint32_t len_error_ppm;  /* p for pre_len / post_len, parts per million, <= 10^7 */
+    uint32_t api_error_ppm;  /* p for the API duration, parts per million, <= 10^7 */
+} lamps_noise;
+
+/*
+ * lamps_predict -- turn n truths (host array) into predicted segments (host
+ * array out[n], ready for lamps_submit / lamps_api_return).  Bin-to-length,
+ * the normal draws and the rounding run on the GPU (k_predict) on the handle's
+ * stream; out[k].api_seconds = api_ticks / ticks_per_second, which lamps_submit
+ * quantises back to exactly api_ticks.  noise == NULL means no error (p = 0).
+ * Synchronous.  Errors: EINVAL (NULL arrays with n > 0, has_api > 1, reserved
+ * != 0, pre_bin out of range, key >= 2^57, ppm > 10^7), ECUDA.  The pool is
+ * not touched.
+ */
+int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_noise* noise,
+                  lamps_segment* out);
+
 /* Library version (major << 16 | minor). */
 uint32_t lamps_version(void);
 

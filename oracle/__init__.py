@@ -101,6 +101,10 @@ def lib():
         L.o_api_return.argtypes = [vp, vp, vp, vp, vp, u32]
         L.o_step.restype = ctypes.c_int
         L.o_step.argtypes = [vp, vp, vp, u32, vp, u32, u64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.o_splitmix_output.restype = u64; L.o_splitmix_output.argtypes = [u64, u64]
+        L.o_normal_q20.restype = ctypes.c_int64; L.o_normal_q20.argtypes = [u64, u64, u32]
+        L.o_perturb.restype = u32; L.o_perturb.argtypes = [u32, u32, ctypes.c_int64, u64]
+        L.o_predict.restype = ctypes.c_int; L.o_predict.argtypes = [vp, u32, u64, u32, u32, vp]
         for n in ("o_sizeof_req", "o_sizeof_cfg", "o_sizeof_seg", "o_sizeof_summary"):
             getattr(L, n).restype = u32
         assert L.o_sizeof_req() == REQ_DTYPE.itemsize
@@ -185,6 +189,35 @@ def segments(rows) -> np.ndarray:
             (a[k]["prompt_len"], a[k]["pre_len"], a[k]["resp_len"], a[k]["post_len"],
              a[k]["api_seconds"], a[k]["has_api"]) = r
     return a
+
+
+# ---------------------------------------------------------------- F4 ingest
+TRUTH_DTYPE = np.dtype([("key", np.uint64), ("prompt_len", np.uint32), ("pre_len", np.uint32),
+                        ("pre_bin", np.uint32), ("resp_len", np.uint32), ("post_len", np.uint32),
+                        ("api_ticks", np.uint32), ("has_api", np.uint32), ("reserved", np.uint32)], align=True)
+PRED_DTYPE = np.dtype([("pre_len", np.uint32), ("resp_len", np.uint32), ("post_len", np.uint32),
+                       ("api_ticks", np.uint32)])
+NO_BIN = 0xFFFFFFFF
+
+
+def splitmix_output(seed: int, n: int) -> int:
+    return int(lib().o_splitmix_output(seed, n))
+
+
+def normal_q20(seed: int, key: int, field: int) -> int:
+    return int(lib().o_normal_q20(seed, key, field))
+
+
+def perturb(m: int, ppm: int, Z: int, hi: int) -> int:
+    return int(lib().o_perturb(m, ppm, Z, hi))
+
+
+def predict(truth: np.ndarray, seed: int = 0, len_error_ppm: int = 0, api_error_ppm: int = 0):
+    """Truths (TRUTH_DTYPE) -> (rc, predictions PRED_DTYPE)."""
+    truth = np.ascontiguousarray(truth, TRUTH_DTYPE)
+    out = np.zeros(max(len(truth), 1), PRED_DTYPE)
+    rc = int(lib().o_predict(_ptr(truth), len(truth), seed, len_error_ppm, api_error_ppm, _ptr(out)))
+    return rc, out[:len(truth)]
 
 
 # ---------------------------------------------------------------- pool

@@ -21,6 +21,8 @@
  *   - prefill cost shape k1*n^2*d ............................... P:1580
  *   - baseline rank keys FCFS / SJF / SJF by total length ....... P:818-822
  *   - selective score update (cached scores, refresh interval) .. P:1080
+ *   - predictor bins (50 x 10 tokens) ........................... P:1115
+ *   - error injection error ~ N(0, p*m) ......................... P:1450-1451
  *
  * Everything is computed with plain loops, exact 128-bit intermediates and
  * explicit clamps; sums are done by explicit summation (no closed forms), the
@@ -610,6 +612,106 @@ int o_step(const ocfg* cfg, oreq* pool, const uint64_t* prev_adm, uint32_t n_pre
     out->n_preempted = n_pre;
     out->blocked_head = (n_e > 0 && n_adm == 0) ? 1u : 0u;
     free(E);
+    return O_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Predictor ingest and error injection (row F4, reading R27)         */
+/* ------------------------------------------------------------------ */
+
+typedef struct {
+    uint64_t key;
+    uint32_t prompt_len, pre_len, pre_bin, resp_len, post_len, api_ticks, has_api, reserved;
+} otruth;
+
+typedef struct {
+    uint32_t pre_len, resp_len, post_len, api_ticks;
+} opred;
+
+#define O_NO_BIN 0xffffffffu
+
+/* splitmix64 (Steele, Lea, Flood 2014; Vigna's reference C): the generator's
+ * state advances by the golden gamma before every output, so output number n
+ * (1-based) of the generator seeded with `seed` is next() called on the state
+ * seed + (n - 1) * gamma. */
+static uint64_t o_splitmix_next(uint64_t* state) {
+    uint64_t z = (*state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint64_t o_splitmix_output(uint64_t seed, uint64_t n) {
+    uint64_t state = seed + (n - 1) * 0x9E3779B97F4A7C15ull;
+    return o_splitmix_next(&state);
+}
+
+/* number of one bits, bit by bit */
+static uint32_t o_popcount(uint64_t w) {
+    uint32_t c = 0;
+    for (int b = 0; b < 64; b++)
+        if ((w >> b) & 1ull) c = c + 1;
+    return c;
+}
+
+/* The normal draw of reading R27 for (key, field), in units of 2^-20:
+ * X = number of one bits in the 16 words n0 .. n0+15, Binomial(1024, 1/2)
+ * (mean 512, standard deviation sqrt(1024/4) = 16), standardised and scaled:
+ * (X - 512) / 16 * 2^20 = (X - 512) * 2^16; plus the top 16 bits of word
+ * n0+16 centred, a uniform dither across one binomial step (1/16). */
+int64_t o_normal_q20(uint64_t seed, uint64_t key, uint32_t field) {
+    const uint64_t n0 = (key * 4 + field) * 32 + 1;
+    uint32_t X = 0;
+    for (uint32_t k = 0; k < 16; k++) X += o_popcount(o_splitmix_output(seed, n0 + k));
+    const int64_t U = (int64_t)(o_splitmix_output(seed, n0 + 16) >> 48);
+    return ((int64_t)X - 512) * 65536 + (U - 32768);
+}
+
+/* predicted = measured + error, error = p * m * z with
+ * p = ppm / 10^6 and z = Z / 2^20, rounded half away from zero, then clamped
+ * at 0 and at `hi` (reading R27). */
+uint32_t o_perturb(uint32_t m, uint32_t ppm, int64_t Z, uint64_t hi) {
+    const u128 num_mag = (u128)ppm * m * (u128)(Z < 0 ? -Z : Z);
+    const u128 den = (u128)1000000 * 1048576;
+    u128 q = num_mag / den;
+    const u128 r = num_mag % den;
+    if (2 * r >= den) q = q + 1; /* half away from zero (on the magnitude) */
+    int64_t v = (int64_t)m;
+    if (Z < 0) v = v - (int64_t)q;
+    else v = v + (int64_t)q;
+    if (v < 0) v = 0;
+    if ((uint64_t)v > hi) v = (int64_t)hi;
+    return (uint32_t)v;
+}
+
+/* Truths -> predicted segment fields.  pre_len comes from the bin midpoint
+ * 10 b + 5 when a bin is given (50 bins of 10 tokens); the output
+ * lengths (pre, post) get p = len_ppm, the API duration p = api_ppm; the
+ * response length is passed through. */
+int o_predict(const otruth* t, uint32_t n, uint64_t seed, uint32_t len_ppm, uint32_t api_ppm, opred* out) {
+    if (len_ppm > 10000000u || api_ppm > 10000000u) return O_EINVAL;
+    for (uint32_t k = 0; k < n; k++) {
+        if (t[k].has_api > 1 || t[k].reserved != 0) return O_EINVAL;
+        if (t[k].pre_bin != O_NO_BIN && t[k].pre_bin > 49) return O_EINVAL;
+        if ((t[k].key >> 57) != 0) return O_EINVAL;
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        uint32_t pre = t[k].pre_len;
+        if (t[k].pre_bin != O_NO_BIN) pre = 10 * t[k].pre_bin + 5;
+        opred r = {0, 0, 0, 0};
+        r.pre_len = pre;
+        if (len_ppm != 0) r.pre_len = o_perturb(pre, len_ppm, o_normal_q20(seed, t[k].key, 0), O_INGEST_LIMIT);
+        if (t[k].has_api) {
+            r.resp_len = t[k].resp_len;
+            r.post_len = t[k].post_len;
+            r.api_ticks = t[k].api_ticks;
+            if (len_ppm != 0)
+                r.post_len = o_perturb(t[k].post_len, len_ppm, o_normal_q20(seed, t[k].key, 1), O_INGEST_LIMIT);
+            if (api_ppm != 0)
+                r.api_ticks = o_perturb(t[k].api_ticks, api_ppm, o_normal_q20(seed, t[k].key, 2), 4294967295ull);
+        }
+        out[k] = r;
+    }
     return O_OK;
 }
 

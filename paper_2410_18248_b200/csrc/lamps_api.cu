@@ -583,6 +583,54 @@ int lamps_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, uint64_t* id
     return LAMPS_OK;
 }
 
+int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_noise* noise,
+                  lamps_segment* out) {
+    if (!h) return LAMPS_EINVAL;
+    if (n && (!truth || !out)) return fail(h, LAMPS_EINVAL, "NULL argument");
+    const uint64_t seed = noise ? noise->seed : 0ull;
+    const uint32_t lp = noise ? noise->len_error_ppm : 0u, ap = noise ? noise->api_error_ppm : 0u;
+    if (lp > 10000000u || ap > 10000000u) return fail(h, LAMPS_EINVAL, "error ppm above 10^7");
+    for (uint32_t k = 0; k < n; k++) {
+        const lamps_truth& t = truth[k];
+        if (t.has_api > 1 || t.reserved)
+            return fail(h, LAMPS_EINVAL, "predict[" + std::to_string(k) + "]: has_api > 1 or reserved != 0");
+        if (t.pre_bin != LAMPS_NO_BIN && t.pre_bin > LAMPS_MAX_BIN)
+            return fail(h, LAMPS_EINVAL, "predict[" + std::to_string(k) + "]: pre_bin out of range");
+        if (t.key >> 57) return fail(h, LAMPS_EINVAL, "predict[" + std::to_string(k) + "]: key >= 2^57");
+    }
+    constexpr uint32_t kChunk = kIngestChunk / 2;  // truths + predictions fit the staging buffer
+    static_assert((size_t)kChunk * (sizeof(TruthRec) + sizeof(PredRec)) <= (size_t)kIngestChunk * sizeof(SubmitRec),
+                  "predict staging");
+    TruthRec* tin = static_cast<TruthRec*>(h->h_ingest);
+    PredRec* pout = reinterpret_cast<PredRec*>(tin + kChunk);
+    TruthRec* d_in = static_cast<TruthRec*>(h->d_ingest);
+    PredRec* d_out = reinterpret_cast<PredRec*>(d_in + kChunk);
+    for (uint32_t k0 = 0; k0 < n; k0 += kChunk) {
+        const uint32_t m = std::min(kChunk, n - k0);
+        for (uint32_t i = 0; i < m; i++) {
+            const lamps_truth& t = truth[k0 + i];
+            tin[i] = TruthRec{t.key, t.pre_len, t.pre_bin, t.resp_len, t.post_len, t.api_ticks, t.has_api};
+        }
+        CU(h, cudaMemcpyAsync(d_in, tin, (size_t)m * sizeof(TruthRec), cudaMemcpyHostToDevice, h->stream));
+        CU(h, launch_predict(d_in, d_out, m, seed, lp, ap, h->stream));
+        CU(h, cudaMemcpyAsync(pout, d_out, (size_t)m * sizeof(PredRec), cudaMemcpyDeviceToHost, h->stream));
+        CU(h, cudaStreamSynchronize(h->stream));
+        for (uint32_t i = 0; i < m; i++) {
+            lamps_segment& s = out[k0 + i];
+            const PredRec& r = pout[i];
+            s.prompt_len = truth[k0 + i].prompt_len;
+            s.pre_len = r.pre;
+            s.resp_len = r.resp;
+            s.post_len = r.post;
+            s.has_api = truth[k0 + i].has_api;
+            // |ticks/tps * tps - ticks| <= 2^-52 * 2^32 << 1/2: quantises back to r.api exactly
+            s.api_seconds = (double)r.api / h->cfg.ticks_per_second;
+            s.reserved = 0;
+        }
+    }
+    return LAMPS_OK;
+}
+
 int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_resp_len,
                      const lamps_segment* next, uint32_t n) {
     if (!h) return LAMPS_EINVAL;

@@ -120,4 +120,16 @@ cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* d_slots, uint
 cudaError_t launch_api_return(const Pool& p, const Cost& c, const ReturnRec* d_rec, uint32_t n,
                               cudaStream_t s);
 
+// predictor ingest (kernels_ingest.cu, row F4): truth records in, predicted segments out
+struct TruthRec {
+    unsigned long long key;
+    uint32_t pre, pre_bin, resp, post, api, has;
+};
+struct PredRec {
+    uint32_t pre, resp, post, api;
+};
+static_assert(sizeof(TruthRec) == 32 && sizeof(PredRec) == 16, "ingest records");
+cudaError_t launch_predict(const TruthRec* d_in, PredRec* d_out, uint32_t n, uint64_t seed, uint32_t len_ppm,
+                           uint32_t api_ppm, cudaStream_t s);
+
 }  // namespace lamps

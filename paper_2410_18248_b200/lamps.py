@@ -63,6 +63,16 @@ class lamps_pool_io(ctypes.Structure):
 SEGMENT_DTYPE = np.dtype([("prompt_len", np.uint32), ("pre_len", np.uint32), ("resp_len", np.uint32),
                           ("post_len", np.uint32), ("api_seconds", np.float64), ("has_api", np.uint32),
                           ("reserved", np.uint32)], align=True)
+TRUTH_DTYPE = np.dtype([("key", np.uint64), ("prompt_len", np.uint32), ("pre_len", np.uint32),
+                        ("pre_bin", np.uint32), ("resp_len", np.uint32), ("post_len", np.uint32),
+                        ("api_ticks", np.uint32), ("has_api", np.uint32), ("reserved", np.uint32)], align=True)
+LAMPS_NO_BIN = 0xFFFFFFFF
+
+
+class lamps_noise(ctypes.Structure):
+    _fields_ = [("seed", u64), ("len_error_ppm", u32), ("api_error_ppm", u32)]
+
+
 EVENT_DTYPE = np.dtype([("id", np.uint64), ("kind", np.uint32), ("reserved", np.uint32)], align=True)
 POOL_U32_FIELDS = ("state", "has_api", "starving", "strategy", "cnt", "ctx", "pre_rem", "api_ticks",
                    "resp_len", "post_len", "pending")
@@ -97,6 +107,7 @@ def lib() -> ctypes.CDLL:
             "lamps_nccl_unique_id": (c_int, [vp]),
             "lamps_group_step": (c_int, [vp, u32, vp, vp, vp, vp]),
             "lamps_version": (u32, []),
+            "lamps_predict": (c_int, [vp, vp, u32, P(lamps_noise), vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -224,6 +235,20 @@ class Scheduler:
         segs = np.ascontiguousarray(segs, SEGMENT_DTYPE)
         ids = np.zeros(max(len(segs), 1), np.uint64)
         return lamps_submit(self.h, segs, ids), ids[:len(segs)]
+
+    def predict_rc(self, truth: np.ndarray, seed: int = 0, len_error_ppm: int = 0, api_error_ppm: int = 0,
+                   noise: bool = True):
+        """lamps_predict: truths (TRUTH_DTYPE) -> predicted segments (SEGMENT_DTYPE), row F4."""
+        truth = np.ascontiguousarray(truth, TRUTH_DTYPE)
+        out = np.zeros(max(len(truth), 1), SEGMENT_DTYPE)
+        nz = lamps_noise(seed, len_error_ppm, api_error_ppm)
+        rc = lib().lamps_predict(self.h, _p(truth), len(truth), ctypes.byref(nz) if noise else None, _p(out))
+        return rc, out[:len(truth)]
+
+    def predict(self, truth: np.ndarray, seed: int = 0, len_error_ppm: int = 0, api_error_ppm: int = 0):
+        rc, out = self.predict_rc(truth, seed, len_error_ppm, api_error_ppm)
+        self._check(rc)
+        return out
 
     def api_return_rc(self, ids, actual, nxt) -> int:
         return lamps_api_return(self.h, np.ascontiguousarray(ids, np.uint64),
