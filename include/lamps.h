@@ -142,7 +142,8 @@ typedef struct {
 /* rank policies (R25): lower key = earlier; starving requests first under all of them */
 #define LAMPS_POLICY_LAMPS 0u     /* memory-over-time area */
 #define LAMPS_POLICY_FCFS 1u      /* request id = arrival */
-#define LAMPS_POLICY_SJF 2u       /* remaining decode tokens of the segment */
+#define LAMPS_POLICY_SJF 2u       /* remaining iterations of the segment: decode tokens + owed
+                                     prefill / swap-in ceil(pending / tau) */
 #define LAMPS_POLICY_SJF_TOTAL 3u /* + API duration in decode iterations, ceil(ticks / tau) */
 
 #define LAMPS_XPORT_NCCL 0u     /* one ncclAllGather per step over NVLink (libnccl.so.2) */

@@ -170,9 +170,10 @@ def score(cfg: OCfg, *, ctx, pre_rem, api_ticks=0, resp_len=0, post_len=0, pendi
     return int(lib().o_score(ctypes.byref(cfg), _ptr(r), strategy))
 
 
-def policy_score(cfg: OCfg, *, pre_rem, post_len=0, api_ticks=0, has_api=1) -> int:
+def policy_score(cfg: OCfg, *, pre_rem, post_len=0, api_ticks=0, has_api=1, pending=0) -> int:
     r = np.zeros(1, REQ_DTYPE)
     r["pre_rem"], r["post_len"], r["api_ticks"], r["has_api"] = pre_rem, post_len, api_ticks, has_api
+    r["pending"] = pending
     r["state"] = READY
     return int(lib().o_policy_score(ctypes.byref(cfg), _ptr(r)))
 

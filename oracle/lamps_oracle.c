@@ -169,7 +169,7 @@ int o_validate_cfg(const ocfg* c) {
     if (c->score_bits + c->id_bits + 1 > 64) return O_EINVAL;
     if (((uint64_t)1 << c->id_bits) < c->capacity) return O_EINVAL;
     if (c->policy > O_POL_SJF_TOTAL) return O_EINVAL;
-    if (c->policy == O_POL_SJF_TOTAL && c->tau == 0) return O_EINVAL;
+    if ((c->policy == O_POL_SJF || c->policy == O_POL_SJF_TOTAL) && c->tau == 0) return O_EINVAL;
     if (c->score_interval > O_MAX_INTERVAL) return O_EINVAL;
     return O_OK;
 }
@@ -271,22 +271,27 @@ uint64_t o_score(const ocfg* cfg, const oreq* r, uint32_t strategy) {
 /* Baseline rank keys (reading R25), lower = earlier, clamped to 2^score_bits - 1:
  *   FCFS      : 0 for every request, so the order is the request id, i.e. arrival
  *               ("determines their order based on request ID")
- *   SJF       : remaining output (decode) tokens of the current segment,
- *               pre_rem + post_len ("based only on length")
+ *   SJF       : remaining length of the current segment in decode iterations:
+ *               pre_rem + post_len + the owed prefill / swap-in, ceil(pending / tau)
+ *               ("based only on length"; "a post-API part of length 2
+ *               (including recomputation)")
  *   SJF_TOTAL : SJF + the API duration in decode iterations, ceil(api_ticks / tau)
  *               ("output length plus API duration")
  * LAMPS is o_score. */
+static uint64_t ceil_div(uint64_t a, uint64_t b) {
+    uint64_t q = a / b;
+    if (a % b != 0) q = q + 1;
+    return q;
+}
+
 uint64_t o_policy_score(const ocfg* cfg, const oreq* r) {
     uint64_t v = 0;
     if (cfg->policy == O_POL_SJF || cfg->policy == O_POL_SJF_TOTAL) {
         v = r->pre_rem;
         if (r->has_api) v = v + r->post_len;
+        v = v + ceil_div(r->pending, cfg->tau);
     }
-    if (cfg->policy == O_POL_SJF_TOTAL && r->has_api) {
-        uint64_t it = r->api_ticks / cfg->tau;
-        if (r->api_ticks % cfg->tau != 0) it = it + 1;
-        v = v + it;
-    }
+    if (cfg->policy == O_POL_SJF_TOTAL && r->has_api) v = v + ceil_div(r->api_ticks, cfg->tau);
     uint64_t maxs = (cfg->score_bits >= 64) ? UINT64_MAX : (((uint64_t)1 << cfg->score_bits) - 1);
     return v < maxs ? v : maxs;
 }

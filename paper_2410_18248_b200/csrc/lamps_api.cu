@@ -150,7 +150,8 @@ const char* validate_cfg(const lamps_config* c) {
         return "need score_bits, id_bits >= 1 and score_bits + id_bits + 1 <= 64";
     if (c->id_bits < 64 && (1ull << c->id_bits) < c->capacity) return "2^id_bits must be >= capacity";
     if (c->policy > LAMPS_POLICY_SJF_TOTAL) return "unknown policy";
-    if (c->policy == LAMPS_POLICY_SJF_TOTAL && c->tau == 0) return "SJF_TOTAL needs tau >= 1";
+    if ((c->policy == LAMPS_POLICY_SJF || c->policy == LAMPS_POLICY_SJF_TOTAL) && c->tau == 0)
+        return "SJF and SJF_TOTAL need tau >= 1";
     if (c->score_interval > 127) return "score_interval must be <= 127";
     if (c->world > 1 || (c->flags & LAMPS_MERGE)) {
         if (c->world > 32 || c->rank >= (c->world > 1 ? c->world : 1u)) return "need rank < world <= 32";

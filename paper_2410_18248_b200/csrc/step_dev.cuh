@@ -123,12 +123,15 @@ __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, ui
     return total;
 }
 
-// Baseline rank keys (R25): FCFS 0 (order = id), SJF remaining decode tokens of
-// the segment, SJF by total length + the API duration in iterations.
+// Baseline rank keys (R25): FCFS 0 (order = id), SJF the remaining iterations of
+// the segment (decode tokens + owed prefill / swap-in, ceil(pending / tau): "a
+// post-API part of length 2 (including recomputation)"), SJF by total
+// length + the API duration in iterations.
 __device__ __forceinline__ uint64_t policy_score(const Cost& c, uint32_t has, uint32_t pre, uint32_t post,
-                                                 uint32_t api) {
+                                                 uint32_t api, uint32_t pend) {
     uint64_t v = 0;
-    if (c.policy == POL_SJF || c.policy == POL_SJF_TOTAL) v = (uint64_t)pre + (has ? post : 0u);
+    if (c.policy == POL_SJF || c.policy == POL_SJF_TOTAL)
+        v = (uint64_t)pre + (has ? post : 0u) + ((uint64_t)pend + c.tau - 1u) / c.tau;
     if (c.policy == POL_SJF_TOTAL && has) v += ((uint64_t)api + c.tau - 1u) / c.tau;
     return v < c.score_max ? v : c.score_max;
 }
@@ -160,7 +163,7 @@ __device__ __forceinline__ uint32_t strategy_score(const Pool& P, const Cost& c,
         if (has) strat = strategy_of(ctx, pre, api, c, &wp, &wd, &ws);
         sc = score_of(ctx, pre, api, resp, post, pend, has, strat, c);
     }
-    if (c.policy != POL_LAMPS) sc = policy_score(c, has, pre, post, api);
+    if (c.policy != POL_LAMPS) sc = policy_score(c, has, pre, post, api, pend);
     if (c.cache) {
         P.sclo[slot] = (uint32_t)sc;
         P.schi[slot] = (uint32_t)(sc >> 32);

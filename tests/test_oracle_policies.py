@@ -53,6 +53,12 @@ def test_policy_score_closed_forms():
     assert O.policy_score(sjf, pre_rem=7, post_len=5, api_ticks=99) == 12
     fcfs = O.make_cfg(unit_cfg(O.POL_FCFS))
     assert O.policy_score(fcfs, pre_rem=7, post_len=5, api_ticks=99) == 0
+    # owed prefill / swap-in counts in iterations ("a post-API part of length 2
+    # (including recomputation)"): ceil(pending / tau)
+    sjf10 = O.make_cfg(unit_cfg(O.POL_SJF, tau=10))
+    for pend, it in ((0, 0), (1, 1), (10, 1), (11, 2)):
+        assert O.policy_score(sjf10, pre_rem=1, post_len=0, has_api=0, pending=pend) == 1 + it
+        assert O.policy_score(cfg, pre_rem=4, post_len=3, api_ticks=25, pending=pend) == 4 + 3 + 3 + it
     small = O.make_cfg(unit_cfg(O.POL_SJF, score_bits=3))
     assert O.policy_score(small, pre_rem=100, post_len=0) == 7  # clamp 2^SB - 1
 
@@ -60,7 +66,8 @@ def test_policy_score_closed_forms():
 def test_policy_validation():
     assert O.validate_cfg(O.make_cfg(unit_cfg(4))) == O.EINVAL
     assert O.validate_cfg(O.make_cfg(unit_cfg(O.POL_SJF_TOTAL, tau=0))) == O.EINVAL
-    assert O.validate_cfg(O.make_cfg(unit_cfg(O.POL_SJF, tau=0))) == O.OK
+    assert O.validate_cfg(O.make_cfg(unit_cfg(O.POL_SJF, tau=0))) == O.EINVAL  # ceil(pending / tau)
+    assert O.validate_cfg(O.make_cfg(unit_cfg(O.POL_FCFS, tau=0))) == O.OK
     assert O.validate_cfg(O.make_cfg(unit_cfg(O.POL_LAMPS, score_interval=127))) == O.OK
     assert O.validate_cfg(O.make_cfg(unit_cfg(O.POL_LAMPS, score_interval=128))) == O.EINVAL
 
@@ -93,8 +100,9 @@ def test_sjf_sorted_by_remaining_tokens(seed):
     r = o.step(kv_total=640)
     P = o.pool
     slot = {int(i): k for k, i in enumerate(P["id"])}
+    tau = cfg["tau"]
     rem = [int(P["pre_rem"][slot[int(i)]]) + (int(P["post_len"][slot[int(i)]]) if P["has_api"][slot[int(i)]] else 0)
-           for i in r["ranked_id"]]
+           + -(-int(P["pending"][slot[int(i)]]) // tau) for i in r["ranked_id"]]
     assert [int(x) for x in r["ranked_score"]] == rem
     keys = _ranked_keys(r)
     assert keys == sorted(keys)

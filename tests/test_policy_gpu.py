@@ -74,7 +74,8 @@ def test_cached_state_roundtrip_through_import():
 
 def test_policy_config_validation():
     from paper_2410_18248_b200 import Scheduler, LampsError
-    for bad in (dict(policy=4), dict(policy=O.POL_SJF_TOTAL, tau=0), dict(score_interval=128)):
+    for bad in (dict(policy=4), dict(policy=O.POL_SJF_TOTAL, tau=0), dict(policy=O.POL_SJF, tau=0),
+                dict(score_interval=128)):
         cfg = gen.lib_config("C1")
         cfg.update(bad)
         with pytest.raises(LampsError):
