@@ -1,0 +1,103 @@
+"""SURVEY row F2 (part 1): the worked example (Table 1) replayed mechanically
+by the unit-model engine (sim/unit.py) with the CPU oracle as the ranker.  The paper's
+four average completion times (Fig. example caption) are reproduced: FCFS
+35/3, SJF 31/3, SJF by total length 11, "Preferred*" 10 -- and the literal integral
+order of reading R16 gives 29/3."""
+from fractions import Fraction
+
+import pytest
+
+from sim import StaticRanker, average_jct, simulate_unit
+from sim_util import OracleRanker, table1_cfg, table1_specs
+
+PAPER = {"FCFS": (1, "fcfs"), "SJF": (2, "sjf"), "SJF_TOTAL": (3, "sjf_total")}
+# completion times of R1, R2, R3 in the paper's figure (SURVEY App. A hand traces)
+DONE = {"FCFS": [8, 15, 12], "SJF": [12, 14, 5], "SJF_TOTAL": [11, 18, 4], "PREFERRED": [12, 14, 4],
+        "LAMPS": [14, 10, 5]}
+
+
+def run(golden, fx, policy, static=None):
+    cfg = table1_cfg(golden, fx, policy)
+    rk = OracleRanker(cfg)
+    if static is not None:
+        rk = StaticRanker(static, rk)
+    return simulate_unit(table1_specs(golden), rk, budget=6, max_running=1, tau=cfg["tau"])
+
+
+@pytest.mark.parametrize("fx", ["a", "b"])
+@pytest.mark.parametrize("pol", list(PAPER))
+def test_worked_example_average_jct(golden, fx, pol):
+    code, key = PAPER[pol]
+    reqs, _ = run(golden, fx, code)
+    assert average_jct(reqs) == Fraction(golden["table1"]["average_jct_units"][key])
+    assert [r.done_at for r in reqs] == DONE[pol]
+    # handling labels at the API call are the paper's (Table 1 row "Memory action")
+    assert ["PDS"[r.api_label] for r in reqs] == [r["label"] for r in golden["table1"]["requests"].values()]
+
+
+@pytest.mark.parametrize("fx", ["a", "b"])
+def test_worked_example_preferred_order(golden, fx):
+    """the preferred schedule runs R3, then R2, then R1 (static order): 10 units."""
+    reqs, tl = run(golden, fx, 0, static=[2, 1, 0])
+    assert average_jct(reqs) == Fraction(golden["table1"]["average_jct_units"]["preferred"]) == 10
+    assert [r.done_at for r in reqs] == DONE["PREFERRED"]
+    # "the post-API part of R2 becomes ready at time unit 10, but due to memory
+    # constraints, it waits until R1 finishes"
+    assert all(1 not in tl[t] for t in (10, 11)) and 0 in tl[11]
+
+
+@pytest.mark.parametrize("fx", ["a", "b"])
+def test_worked_example_literal_lamps(golden, fx):
+    """Reading R16: the literal memory-over-time integral orders R2 < R3 < R1; replayed
+    under the same engine it averages 29/3 -- below the paper's "Preferred*" 10."""
+    reqs, _ = run(golden, fx, 0)
+    assert average_jct(reqs) == Fraction(29, 3)
+    assert [r.done_at for r in reqs] == DONE["LAMPS"]
+
+
+def test_fcfs_narrative_details(golden):
+    """FCFS runs R2's pre-API part during R1's API call (it is discarded
+    after one unit), but not R3's (it would not release memory before R1 resumes)."""
+    reqs, tl = run(golden, "a", 1)
+    assert tl[5] == [1]          # R2 pre during R1's API (5-7)
+    assert tl[6] == []           # R3 blocked
+    assert tl[7] == [0]          # R1 resumes
+
+
+def test_sjf_narrative_details(golden):
+    """at t = 8 R2 returns with 2 units left (including recomputation), ties the
+    running R1 (2 left) and waits; at t = 9 R1 holds 5 units in its API call and R2
+    cannot start until R1 finishes."""
+    reqs, tl = run(golden, "a", 2)
+    assert tl[8] == [0] and tl[9] == [] and tl[10] == [] and tl[11] == [0]
+    assert tl[12] == [1] and tl[13] == [1]
+
+
+# ---------------------------------------------------------------- scale engine (sim/engine.py)
+import gen  # noqa: E402
+from sim import engine  # noqa: E402
+from sim_util import OracleBackend  # noqa: E402
+
+
+def test_engine_runs_to_completion_and_is_deterministic():
+    cfg = gen.lib_config("C3")
+    a = engine.run("C3", 120, 3.0, OracleBackend(cfg), seed=2)
+    b = engine.run("C3", 120, 3.0, OracleBackend(cfg), seed=2)
+    assert a["finished"] == 120 and a == b
+    assert a["jct_p99_s"] >= a["jct_median_s"] > 0
+
+
+def test_engine_zero_error_equals_exact_predictions():
+    """p = 0 through the predictor ingest is the exact-prediction run."""
+    cfg = gen.lib_config("C2")
+    a = engine.run("C2", 150, 5.0, OracleBackend(cfg), seed=4, len_error_ppm=0, api_error_ppm=0)
+    b = engine.run("C2", 150, 5.0, OracleBackend(cfg), seed=4, len_error_ppm=0, api_error_ppm=0, noise_seed=99)
+    assert a["done_step"] == b["done_step"]
+
+
+def test_engine_survives_large_mispredictions():
+    """p = 50 % on lengths and durations: requests that run past their predicted length
+    (pre_rem clamped at 0, R24) or stop short still finish."""
+    cfg = gen.lib_config("C3")
+    m = engine.run("C3", 120, 3.0, OracleBackend(cfg), seed=5, len_error_ppm=500_000, api_error_ppm=500_000)
+    assert m["finished"] == 120
