@@ -12,7 +12,8 @@ import gen  # noqa: E402
 from sim import engine  # noqa: E402
 
 N = int(os.environ.get("N", "600"))
-RATE = float(os.environ.get("RATE", "3.0"))
+RATE = float(os.environ.get("RATE", "4.0"))
+KV = int(os.environ.get("KV", "1000"))
 SEEDS = [int(x) for x in os.environ.get("SEEDS", "0,1,2").split(",")]
 
 
@@ -42,8 +43,8 @@ def sweep(cname, profile, kv, label, cases, **fixed):
 
 res = {
     "workload": f"{N} requests per run, Poisson {RATE} req/s, seeds {SEEDS}; Multi-API classes (gen.requests C3), "
-                "GPT-J profile, KV budget 3000 blocks; one step = one decode iteration (tau = 12 ms)",
-    "starvation": sweep("C3", "gptj", 3000, "T", [{"T": t} for t in (10, 50, 100, 200, 1000, 65535)]),
-    "error_injection": sweep("C3", "gptj", 3000, "p", [{"p": p} for p in (0, 50_000, 100_000, 300_000, 500_000)]),
+                f"GPT-J profile, KV budget {KV} blocks; one step = one decode iteration (tau = 12 ms)",
+    "starvation": sweep("C3", "gptj", KV, "T", [{"T": t} for t in (10, 50, 100, 200, 1000, 65535)]),
+    "error_injection": sweep("C3", "gptj", KV, "p", [{"p": p} for p in (0, 50_000, 100_000, 300_000, 500_000)]),
 }
 print(json.dumps(res, indent=1))
