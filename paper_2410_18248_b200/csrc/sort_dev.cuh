@@ -20,35 +20,29 @@ struct SortSmem {
     uint32_t n_pass;
 };
 
-// Grid barrier for a cooperative launch (all CTAs resident), two-level: CTAs
-// arrive on one of kBarGroups group counters (separate 128-byte lines, so
-// same-address atomics serialize only within a group); the last arriver of a
-// group arrives on the root counter; the last root arriver publishes the
-// barrier value with a release store that every CTA polls (acquire).  Values
-// grow monotonically across barriers and steps; counters self-reset.
-constexpr uint32_t kBarGroups = 16;
+// Grid barrier for a cooperative launch (all CTAs resident), flat: thread 0 of
+// every CTA adds 1 to a 64-bit counter that only grows (acq_rel atomic); the
+// arrivals of one barrier are G consecutive counter values, so the CTA whose add
+// returned `old` waits until the counter reaches (old / G + 1) * G (acquire
+// polls).  The counter is a multiple of G between barriers; kernels with
+// different grid sizes use different counter lines (G mod 16).  Measured on B200
+// with 148 x 1024 threads: 1.16 us per barrier, vs 2.57 us for a two-level tree
+// (scripts/micro/barrier.cu).  `value` is unused (kept for the call sites'
+// bookkeeping of barriers per step).
 __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks, uint32_t value) {
+    (void)value;
     __syncthreads();
     if (threadIdx.x == 0) {
-        const uint32_t g = blockIdx.x % kBarGroups;
-        const uint32_t gsize = nblocks / kBarGroups + (g < nblocks % kBarGroups ? 1u : 0u);
-        const uint32_t ngroups = nblocks < kBarGroups ? nblocks : kBarGroups;
-        uint32_t* gcnt = bar + 32u * (1u + g);  // group counters, 128 B apart
-        uint32_t* root = bar + 32u * (1u + kBarGroups);
-        uint32_t old;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(gcnt) : "memory");
-        if (old == gsize - 1) {
-            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(gcnt) : "memory");
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(root) : "memory");
-            if (old == ngroups - 1) {
-                asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(root) : "memory");
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(value) : "memory");
-            }
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar + 32u * (1u + (nblocks & 15u)));
+        unsigned long long old;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(cnt) : "memory");
+        const unsigned long long target = (old / nblocks + 1ull) * nblocks;
+        if (old + 1ull != target) {
+            unsigned long long cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(cnt) : "memory");
+            } while (cur < target);
         }
-        uint32_t cur;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
-        } while ((int)(cur - value) < 0);
     }
     __syncthreads();
 }
