@@ -33,6 +33,7 @@ constexpr int kBucketM = 7;                 // score bits per octave
 constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
 constexpr int kLocalItems = kKcap / kFT;    // 10
 constexpr int kTRows = 8;                   // count exchange: up to 256 CTAs
+constexpr int kMaxCtas = 256;               // range weights: grid size limit
 
 struct PhaseS {                  // S, H, T, X
     uint64_t kbuf[kKcap];        // 96 KB: this CTA's keys
@@ -43,6 +44,9 @@ struct PhaseS {                  // S, H, T, X
     uint32_t nk, base;
     unsigned long long mbar[2];  // S: TMA completion barriers of the two stage buffers
     uint32_t hb_j, hb_r;         // head-only mode: first bucket past the head, its start
+    float ccost[kMaxCtas];       // range-sort cycles per key of each CTA (previous steps)
+    uint32_t rb[kMaxCtas + 1], jb[kMaxCtas + 1];  // X: key / bucket boundaries of the ranges
+    float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -620,11 +624,18 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const uint32_t NB = 2u * half;
     uint32_t* T = b.btot + (a.parity ? kMaxBuckets : 0);  // [NB] bucket totals of this step
     {   // the other parity's totals are zeroed for the next step
-        uint32_t* Tn = b.btot + (a.parity ? 0 : kMaxBuckets);
-        for (uint32_t j = bid * kFT + tid; j < NB; j += G * kFT) Tn[j] = 0;
+        uint4* Tn = reinterpret_cast<uint4*>(b.btot + (a.parity ? 0 : kMaxBuckets));
+        for (uint32_t j = bid * kFT + tid; j < (NB + 3u) / 4u; j += G * kFT) Tn[j] = make_uint4(0, 0, 0, 0);
     }
 
     TRACE(0);
+    // the CTAs' measured range-sort costs (previous steps) -> shared memory by cp.async, so
+    // the L2 latency hides behind the score phase; they weight the key ranges (X)
+    if (tid < G && tid < (uint32_t)kMaxCtas) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.s.ccost[tid]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\ncp.async.commit_group;" ::"r"(dst),
+                     "l"(b.cta_cost + tid) : "memory");
+    }
     // ---------------- S: score this CTA's slots, keys into shared memory.  The seven SoA
     // words of each chunk of 1024 slots are staged by TMA bulk copies (one thread issues
     // seven 1-D copies per chunk; an mbarrier counts the bytes), double buffered, while
@@ -656,9 +667,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (nchunk) issue(0);
     }
-    for (uint32_t i = tid; i < NB; i += kFT) sm.s.cnt[i] = 0;
+    for (uint32_t i = tid; i < (NB + 3u) / 4u; i += kFT) reinterpret_cast<uint4*>(sm.s.cnt)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    unsigned long long pinned = 0, kor = 0, kand = ~0ull;
+    unsigned long long pinned = 0;
     const uint32_t lt_mask = (1u << lane) - 1u;
     for (uint32_t ch = 0; ch < nchunk; ch++) {
         if (tid == 0 && ch + 1 < nchunk) {
@@ -703,13 +714,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             base = __shfl_sync(0xffffffffu, base, leader);
             if (have) {
                 sm.s.kbuf[base + __popc(m & lt_mask)] = key;
-                kor |= key;
-                kand &= key;
                 atomicAdd(&sm.s.cnt[bucket_of(key, c, half)], 1u);
             }
         }
         __syncthreads();
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // ccost (read after the barrier below)
     if (tid == 0) {  // the barrier words are reused as plain shared memory after S
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0) : "memory");
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0 + 8u) : "memory");
@@ -717,27 +727,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     __syncthreads();
     const uint32_t nk_cta = sm.s.nk;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
-        kor |= __shfl_xor_sync(0xffffffffu, kor, o);
-        kand &= __shfl_xor_sync(0xffffffffu, kand, o);
-    }
-    if (lane == 0) {
-        sm.s.red[0][warp] = pinned;
-        sm.s.red[1][warp] = kor;
-        sm.s.red[2][warp] = kand;
-    }
+    for (int o = 16; o; o >>= 1) pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
+    if (lane == 0) sm.s.red[0][warp] = pinned;
     __syncthreads();
     if (tid == 0) {
-        unsigned long long t = 0, o = 0, n = ~0ull;
-        for (int w = 0; w < kFW; w++) {
-            t += sm.s.red[0][w];
-            o |= sm.s.red[1][w];
-            n &= sm.s.red[2][w];
-        }
+        unsigned long long t = 0;
+        for (int w = 0; w < kFW; w++) t += sm.s.red[0][w];
         b.pin_part[bid] = t;
-        b.kmask[bid] = o;
-        b.kmask[G + bid] = n;
     }
     TRACE(1);
     // ---------------- H: add this CTA's bucket counts to the totals; the returned old
@@ -785,24 +781,25 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     TRACE(5);
 
     // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
-    // bucket order; cursor(j) = start(j) + this CTA's offset inside bucket j
+    // bucket order; cursor(j) = start(j) + this CTA's offset inside bucket j.  The totals
+    // are loaded coalesced (uint4) into shared memory, then scanned in place by raking.
     {
-        constexpr int kPer = (kMaxBuckets + kFT - 1) / kFT;  // 15
-        uint32_t tv[kPer];
+        constexpr int kPer4 = (kMaxBuckets / 4 + kFT - 1) / kFT;  // 4
+        uint4 tv[kPer4];
+        const uint32_t nb4 = (NB + 3u) / 4u;
 #pragma unroll
-        for (int u = 0; u < kPer; u++) {
+        for (int u = 0; u < kPer4; u++) {
             const uint32_t j = tid + (uint32_t)u * kFT;
-            tv[u] = j < NB ? __ldcg(&T[j]) : 0u;
+            tv[u] = j < nb4 ? __ldcg(reinterpret_cast<const uint4*>(T) + j) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < kPer; u++) {
+        for (int u = 0; u < kPer4; u++) {
             const uint32_t j = tid + (uint32_t)u * kFT;
-            if (j < NB) sm.s.start[j] = tv[u];
+            if (j < nb4) reinterpret_cast<uint4*>(sm.s.start)[j] = tv[u];
         }
     }
     __syncthreads();
     TRACE(10);
-    // bucket starts = exclusive scan of the totals; scatter cursors = starts + this CTA's prefix
     {
         const uint32_t tot = smem_excl_scan<kFT, (kMaxBuckets + kFT - 1) / kFT>(sm.s.start, NB, sm.s.w32, sm.s.cnt);
         if (tid == 0) sm.s.base = tot;  // total number of keys
@@ -828,38 +825,92 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         head_only = sm.s.hb_r <= (uint32_t)kKcap && !(a.flags & kStepForceFallback);
     }
     const uint32_t jcut = head_only ? sm.s.hb_j : NB;
-    for (uint32_t i = tid; i < nk_cta; i += kFT) {
-        const uint64_t k = sm.s.kbuf[i];
-        const uint32_t j = bucket_of(k, c, half);
-        if (j >= jcut) continue;
-        const uint32_t pos = atomicAdd(&sm.s.cnt[j], 1u);  // order within a bucket is free
-        b.keys[0][pos] = k;
+    // The first kRW warps compute the range boundaries while the other warps scatter the
+    // keys (both only read the bucket starts).  CTA r sorts the buckets whose start lies
+    // in [q_r, q_{r+1}); thread r finds the first bucket with start >= q_r by binary
+    // search; the largest range decides the fallback.
+    uint32_t* rb = sm.s.rb;  // key boundaries of the ranges
+    uint32_t* jb = sm.s.jb;  // bucket boundaries of the ranges
+    const uint32_t kRW = (G + 1u + 31u) / 32u;
+    if (warp < kRW) {
+        if (head_only) {  // one range: [0, hb_r) in buckets [0, hb_j), sorted by CTA 0
+            if (tid <= G) {
+                rb[tid] = tid == 0 ? 0u : sm.s.hb_r;
+                jb[tid] = tid == 0 ? 0u : sm.s.hb_j;
+            }
+        } else {
+            // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
+            // end of their bucket) so it can start the admission early; the other CTAs share
+            // the rest in proportion to their measured speed (cycles per key of the previous
+            // steps' range sorts: some SMs of a B200 run this phase markedly slower), weight
+            // mean/cost capped at 1.25; below 0.4 the CTA gets no range (G <= 255)
+            float* wx = sm.s.wx;  // [G + 1] exclusive weight prefix
+            if (warp == 0) {
+                constexpr int kW = kMaxCtas / 32;
+                float cst[kW];
+                float ksum = 0.f, kcnt = 0.f;
+#pragma unroll
+                for (int u = 0; u < kW; u++) {
+                    const uint32_t r = lane * kW + (uint32_t)u;
+                    cst[u] = (r >= 1 && r < G) ? sm.s.ccost[r] : 0.f;
+                    if (cst[u] > 0.f) { ksum += cst[u]; kcnt += 1.f; }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+                    kcnt += __shfl_xor_sync(0xffffffffu, kcnt, o);
+                }
+                const float mean = kcnt > 0.f ? __fdividef(ksum, kcnt) : 1.f;
+                float w[kW], run = 0.f;
+#pragma unroll
+                for (int u = 0; u < kW; u++) {
+                    const uint32_t r = lane * kW + (uint32_t)u;
+                    w[u] = 0.f;
+                    if (r >= 1 && r < G) {
+                        const float rel = cst[u] > 0.f ? __fdividef(mean, cst[u]) : 1.f;
+                        w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.25f);
+                    }
+                    run += w[u];
+                }
+                float x = run;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
+                }
+                float e = x - run;
+#pragma unroll
+                for (int u = 0; u < kW; u++) {
+                    const uint32_t r = lane * kW + (uint32_t)u;
+                    if (r <= G) wx[r] = e;  // r = G: the total
+                    e += w[u];
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(kRW * 32u) : "memory");  // the kRW warps only
+            if (tid <= G) {
+                const uint32_t head = min(n, a.max_batch + 32u);
+                const float wt = wx[G];
+                const float f = tid == 0 ? 0.f : (wt > 0.f ? fminf(__fdividef(wx[tid], wt), 1.f) : 0.f);
+                const uint32_t q = tid == 0 ? 0u : head + min(n - head, (uint32_t)(f * (float)(n - head)));
+                uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
+                }
+                rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
+                jb[tid] = tid == G ? NB : lo;
+            }
+        }
+    } else {
+        for (uint32_t i = tid - kRW * 32u; i < nk_cta; i += kFT - kRW * 32u) {
+            const uint64_t k = sm.s.kbuf[i];
+            const uint32_t j = bucket_of(k, c, half);
+            if (j >= jcut) continue;
+            const uint32_t pos = atomicAdd(&sm.s.cnt[j], 1u);  // order within a bucket is free
+            b.keys[0][pos] = k;
+        }
     }
-    __syncthreads();
     TRACE(12);
-    // CTA r sorts the buckets whose start lies in [r n/G, (r+1) n/G): thread r finds the first
-    // bucket with start >= q_r by binary search; the largest range decides the fallback
-    uint32_t* rb = reinterpret_cast<uint32_t*>(sm.s.kbuf);  // kbuf is dead now: key boundaries
-    uint32_t* jb = rb + (G + 1);                             // and bucket boundaries of the ranges
-    if (head_only) {  // one range: [0, hb_r) in buckets [0, hb_j), sorted by CTA 0
-        if (tid <= G) {
-            rb[tid] = tid == 0 ? 0u : sm.s.hb_r;
-            jb[tid] = tid == 0 ? 0u : sm.s.hb_j;
-        }
-    } else if (tid <= G) {
-        // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
-        // end of their bucket) so it can start the admission early; the other CTAs share
-        // the rest evenly
-        const uint32_t head = min(n, a.max_batch + 32u);
-        const uint32_t q = tid == 0 ? 0u : head + (uint32_t)(((uint64_t)(tid - 1) * (n - head)) / (G - 1 ? G - 1 : 1));
-        uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
-        }
-        rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
-        jb[tid] = tid == G ? NB : lo;
-    }
     __syncthreads();
     uint32_t mx = 0;
     if (tid < G) mx = rb[tid + 1] - rb[tid];
@@ -876,9 +927,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     bool head_dw = false;  // CTA 0: demands / state words of its head in sm.l.b (sorted order)
     if (!fallback) {
         const uint32_t rn = r_hi - r_lo;
+        const long long l_t0 = clock64();
+        unsigned long long g_t0 = 0;
+        if (b.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
         if (tr && tid == 0) {
             tr[30] = rn; tr[31] = j_hi - j_lo;
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            tr[28] = smid;  // diagnostics: SM of this CTA
             for (int q = 32; q < 64; q++) tr[q] = 0;
         }
         if (j_hi - j_lo < (uint32_t)kSubBuckets) {
@@ -908,10 +965,44 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                        tr ? tr + 32 : nullptr);
         }
         TRACE(14);
+        if (b.trace && tid == 0) {
+            unsigned long long g_t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t1));
+            b.trace[(size_t)bid * kTraceSlots + 26] = g_t0;
+            b.trace[(size_t)bid * kTraceSlots + 27] = g_t1;
+        }
+        if (tid == 0 && bid != 0 && rn >= 1024u && !head_only) {
+            // this CTA's range-sort cycles per key, for the next steps' range weights (EMA;
+            // the CTA -> SM placement of the cooperative launch is stable in practice)
+            const float cst = __fdividef((float)(clock64() - l_t0), (float)rn);
+            const float old = b.cta_cost[bid];
+            b.cta_cost[bid] = old > 0.f ? 0.75f * old + 0.25f * cst : cst;
+        }
         for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
         final_buf = 1;
         passes = 1;
     } else {
+        {   // OR / AND of the keys (the LSD skips digit positions that never vary)
+            unsigned long long o = 0, an = ~0ull;
+            for (uint32_t i = bid * kFT + tid; i < n; i += G * kFT) {
+                const uint64_t k = __ldcg(&b.keys[0][i]);
+                o |= k;
+                an &= k;
+            }
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                o |= __shfl_xor_sync(0xffffffffu, o, s);
+                an &= __shfl_xor_sync(0xffffffffu, an, s);
+            }
+            if (lane == 0) { sm.s.red[1][warp] = o; sm.s.red[2][warp] = an; }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 0; w < kFW; w++) { o |= sm.s.red[1][w]; an &= sm.s.red[2][w]; }
+                b.kmask[bid] = o;
+                b.kmask[G + bid] = an;
+            }
+            grid_barrier(b.flags, G, ++bar);
+        }
         passes = lsd_sort_global(b, n, b.kmask, G, sm.g, bar);
         final_buf = passes & 1u;
     }

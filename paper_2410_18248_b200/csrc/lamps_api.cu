@@ -184,6 +184,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_bsum = L.take(bsum_lsd);
     size_t o_btot = h->fused ? L.take((size_t)2 * fused_max_buckets() * 4) : 0;
     size_t o_ctl = L.take(sizeof(Ctl));
+    size_t o_ctasm = L.take((size_t)gmax * 4);
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
     size_t o_ai0 = L.take((size_t)mb * 8), o_ai1 = L.take((size_t)mb * 8);
     size_t o_at0 = L.take(mb), o_at1 = L.take(mb);
@@ -215,6 +216,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;
     h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);
+    h->b.cta_cost = reinterpret_cast<float*>(base + o_ctasm);
     h->b.adm_slot[0] = reinterpret_cast<uint32_t*>(base + o_as0);
     h->b.adm_slot[1] = reinterpret_cast<uint32_t*>(base + o_as1);
     h->b.adm_id[0] = reinterpret_cast<uint64_t*>(base + o_ai0);
@@ -248,7 +250,7 @@ void grids(lamps_t* h, bool query_device) {
         const uint32_t groups = (h->cap + 3) / 4;
         const uint32_t gpc = (groups + h->fused_grid - 1) / h->fused_grid;
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && gpc * 4u <= (uint32_t)kFusedKcap && fused_occ >= 1 &&
-                   h->fused_grid <= 256u;  // count exchange covers up to 256 CTAs
+                   h->fused_grid <= 255u;  // range weights (kMaxCtas) cover up to 255 CTAs
     }
     if (!query_device) {  // size query: assume the fused path may be chosen
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && h->cap <= 148u * (uint32_t)kFusedKcap;

@@ -89,6 +89,8 @@ struct Bufs {
     unsigned long long* dbg; // [cap][4] W_P, W_D, W_S, score (LAMPS_DEBUG_OUT) or null
     unsigned long long* trace;  // [grid][16] clock64 at phase boundaries (LAMPS_TRACE) or null
     uint32_t* flags;         // grid barrier words (see sort_dev.cuh)
+    float* cta_cost;         // fused: [grid] measured range-sort cycles per key of each CTA
+                             // (EMA over steps; 0 = not measured): weights the key ranges
     MergeRec* xsend;         // [1 + K] header + top-K records of this rank (world > 1)
     MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
 };

@@ -60,7 +60,8 @@ if os.environ.get("TRACE"):
             r = t0[cta]
             sub = [(r[17 + i] - r[16 + i]) / 1965 for i in range(4)]
             print(f"{cta:3d} {r[30]:6d} {r[31]:6d} {(r[14]-r[13])/1965:8.2f}  " + " ".join(f"{x:6.2f}" for x in sub) +
-                  f"  {r[21]:4d} {(r[1]-r[0])/1965:7.2f} {(r[12]-r[11])/1965:7.2f}")
+                  f"  {r[21]:4d} {(r[1]-r[0])/1965:7.2f} {(r[12]-r[11])/1965:7.2f} {r[28]:4d}"
+                  f" {(r[27]-r[26])/1000:7.2f} {(r[26]-t0[:,26].min())/1000:7.2f} {r[24]/1000:7.2f} {r[25]/1965:7.2f}")
     if os.environ.get("LEVELS"):
         t0 = acc[-1]
         print("cta  keys  per-level (us, groups) of the non-starving part; level-0 substeps or/and,count,scan,scatter,final")
