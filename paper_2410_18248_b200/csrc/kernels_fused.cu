@@ -659,6 +659,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                          : "memory");
         }
     };
+    if (a.n_ev) {  // A0 for the engine's events on this CTA's slots, before they are staged
+        for (uint32_t e = tid; e < a.n_ev; e += kFT) {
+            const DevEvent E = static_cast<const DevEvent*>(b.events)[e];
+            const uint32_t s = (uint32_t)E.id & c.cap_mask;
+            if (s >= s_lo && s < s_hi) apply_event(b.pool, c, E);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+        __syncthreads();
+    }
     if (tid == 0) {
         sm.s.nk = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kMT) k_merge(Bufs b, Cost c, StepArgs a) {
         ctl->budget_used = used;
         ctl->blocked_head = (total_valid > 0 && cut == 0) ? 1u : 0u;
         ctl->pinned_out = pin_local;
+        publish_host_result(b);
     }
 }
 

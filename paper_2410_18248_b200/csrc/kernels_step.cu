@@ -18,21 +18,7 @@ namespace {
 __global__ void __launch_bounds__(256) k_events(Bufs b, Cost c, StepArgs a) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= a.n_ev) return;
-    const Pool& P = b.pool;
-    const DevEvent E = static_cast<const DevEvent*>(b.events)[e];
-    const uint32_t s = (uint32_t)E.id & c.cap_mask;
-    const uint32_t w = P.sfc[s];
-    if (E.kind == EV_FINISHED) {
-        P.sfc[s] = 0u;
-        return;
-    }
-    const uint32_t ctx = P.ctx[s] + ((w & SFC_RAN) ? 1u : 0u);  // this iteration's token
-    P.ctx[s] = ctx;
-    P.pre[s] = 0u;
-    P.pend[s] = 0u;
-    const uint32_t st = strategy_of(ctx, 0, P.api[s], c);
-    const uint32_t starv = sfc_starv(w);
-    P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u) | (w & SFC_META);
+    apply_event(b.pool, c, static_cast<const DevEvent*>(b.events)[e]);
 }
 
 // ---------------------------------------------------------------------------

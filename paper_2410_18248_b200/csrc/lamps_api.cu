@@ -95,6 +95,14 @@ struct lamps_s {
     uint32_t* d_gather = nullptr;
     // host shadow
     std::vector<uint8_t> hstate;
+    std::vector<uint32_t> hctx;  // host shadow of each slot's context length (ingest checks
+                                 // without a device round trip): submit, +1 per admission
+                                 // (applied by the next step's A0), + response at API return
+    bool shadow_ok = true;       // false once a step's admitted list went unread (async use)
+    std::vector<uint32_t> adm_mark;  // per slot: step that last admitted it (event validation)
+    std::vector<uint32_t> ev_mark;   // per slot: tag of the last event batch naming it
+    uint32_t ev_tag = 0;
+    uint32_t fetched_step = 0;   // last step whose admitted list entered the shadow
     uint64_t next_id = 0, id_base = 0;
     uint32_t step = 0;
     std::vector<uint64_t> prev_adm;
@@ -109,6 +117,12 @@ struct lamps_s {
     uint8_t* h_adm_strat = nullptr;
     uint64_t* h_pre_ids = nullptr;
     bool have_result = false;
+    // mapped pinned result block (written by the admission kernel)
+    void* h_res = nullptr;
+    HostRes* hres = nullptr;
+    // staging reuse: the last host-to-device copy out of h_ingest
+    cudaEvent_t ing_ev = nullptr;
+    bool ing_pending = false;
     // timing ring
     std::vector<cudaEvent_t> tev;
     uint32_t t_count = 0, t_head = 0;
@@ -346,11 +360,12 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
 int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     const bool timing = (h->cfg.flags & LAMPS_TIMING) != 0;
     if (timing && h->t_count == kTimingRing) return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
+    if (h->have_result && h->fetched_step != h->step) h->shadow_ok = false;  // an unread admitted list
     h->step++;
     const StepArgs a = make_args(h, kv_total, n_ev);
     h->last_id_base = h->id_base;
     record_timing(h, 0);
-    CU(h, launch_events(h->b, h->cost, a, h->stream));
+    if (!h->fused) CU(h, launch_events(h->b, h->cost, a, h->stream));  // fused: in the kernel's prologue
     record_timing(h, 1);
     if (h->fused) {
         CU(h, launch_fused(h->b, h->cost, a, h->fused_grid, h->stream));
@@ -363,7 +378,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         record_timing(h, 3);
         CU(h, launch_admit(h->b, h->cost, a, h->stream));
     }
-    h->last_kernels = (h->fused ? 1 : 3) + (n_ev ? 1 : 0);
+    h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);
     return LAMPS_OK;
 }
 
@@ -399,38 +414,69 @@ int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
 }
 
 int fetch_result(lamps_t* h, lamps_step_out* out) {
-    CU(h, cudaMemcpyAsync(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    // the admission kernel wrote the summary and the lists into mapped host memory
     CU(h, cudaStreamSynchronize(h->stream));
-    const Ctl& C = *h->h_ctl;
+    const HostRes& R = *h->hres;
     const uint32_t par = h->step & 1u;
-    if (C.n_admitted) {
-        CU(h, cudaMemcpyAsync(h->h_adm_ids, h->b.adm_id[par], (size_t)C.n_admitted * 8,
-                              cudaMemcpyDeviceToHost, h->stream));
-        CU(h, cudaMemcpyAsync(h->h_adm_strat, h->b.adm_strat[par], C.n_admitted,
-                              cudaMemcpyDeviceToHost, h->stream));
+    const uint64_t* adm = h->h_adm_ids;
+    h->prev_adm.assign(adm, adm + R.n_admitted);
+    if (h->fetched_step != h->step) {
+        for (uint32_t k = 0; k < R.n_admitted; k++) {
+            const uint32_t sl = (uint32_t)(adm[k] & h->cost.cap_mask);
+            h->hctx[sl] += 1u;  // the next step's A0
+            h->adm_mark[sl] = h->step;
+        }
+        h->fetched_step = h->step;
     }
-    if (C.n_preempted)
-        CU(h, cudaMemcpyAsync(h->h_pre_ids, h->b.pre_id, (size_t)C.n_preempted * 8,
-                              cudaMemcpyDeviceToHost, h->stream));
-    CU(h, cudaStreamSynchronize(h->stream));
-    h->prev_adm.assign(h->h_adm_ids, h->h_adm_ids + C.n_admitted);
     h->prev_known = true;
     if (out) {
         std::memset(out, 0, sizeof(*out));
-        out->n_eligible = C.n_elig_out;
-        out->pinned = C.pinned_out;
-        out->budget = C.budget;
-        out->budget_used = C.budget_used;
-        out->n_admitted = C.n_admitted;
-        out->n_preempted = C.n_preempted;
-        out->blocked_head = C.blocked_head;
+        out->n_eligible = R.n_elig;
+        out->pinned = R.pinned;
+        out->budget = R.budget;
+        out->budget_used = R.budget_used;
+        out->n_admitted = R.n_admitted;
+        out->n_preempted = R.n_preempted;
+        out->blocked_head = R.blocked_head;
         out->id_base = h->last_id_base;
         out->admitted_ids = h->h_adm_ids;
         out->admitted_strategy = h->h_adm_strat;
         out->preempted_ids = h->h_pre_ids;
-        out->d_ranked_keys = h->b.keys[C.final_buf & 1u];
+        out->d_ranked_keys = h->b.keys[R.final_buf & 1u];
         out->d_admitted_slots = h->b.adm_slot[par];
     }
+    return LAMPS_OK;
+}
+
+// Rebuild the context shadow from the device (after async steps whose admitted lists the
+// host never read): the device ctx plus the pending A0 of the last step's admitted slots.
+int resync_shadow(lamps_t* h) {
+    CU(h, cudaStreamSynchronize(h->stream));
+    CU(h, cudaMemcpy(h->hctx.data(), h->b.pool.ctx, (size_t)h->cap * 4, cudaMemcpyDeviceToHost));
+    if (h->have_result) {
+        CU(h, cudaMemcpy(h->h_ctl, h->b.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+        const uint32_t n = h->h_ctl->n_admitted;
+        std::vector<uint32_t> slots(n);
+        if (n) CU(h, cudaMemcpy(slots.data(), h->b.adm_slot[h->step & 1u], (size_t)n * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t k = 0; k < n; k++) h->hctx[slots[k]] += 1u;
+    }
+    h->fetched_step = h->step;
+    h->shadow_ok = true;
+    return LAMPS_OK;
+}
+
+// the pinned ingest staging may be rewritten once its last host-to-device copy is done
+int staging_wait(lamps_t* h) {
+    if (h->ing_pending) {
+        CU(h, cudaEventSynchronize(h->ing_ev));
+        h->ing_pending = false;
+    }
+    return LAMPS_OK;
+}
+
+int staging_copied(lamps_t* h) {
+    CU(h, cudaEventRecord(h->ing_ev, h->stream));
+    h->ing_pending = true;
     return LAMPS_OK;
 }
 
@@ -510,10 +556,30 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     if (cudaHostAlloc(&h->h_ingest, (size_t)kIngestChunk * sizeof(SubmitRec), cudaHostAllocDefault) ||
         cudaHostAlloc((void**)&h->h_ev, (size_t)cfg->max_batch * sizeof(lamps_event), cudaHostAllocDefault) ||
         cudaHostAlloc((void**)&h->h_ctl, sizeof(Ctl), cudaHostAllocDefault) ||
-        cudaHostAlloc((void**)&h->h_adm_ids, (size_t)cfg->max_batch * 8, cudaHostAllocDefault) ||
-        cudaHostAlloc((void**)&h->h_adm_strat, cfg->max_batch, cudaHostAllocDefault) ||
-        cudaHostAlloc((void**)&h->h_pre_ids, (size_t)cfg->max_batch * 8, cudaHostAllocDefault))
+        cudaHostAlloc(&h->h_res, sizeof(HostRes) + (size_t)cfg->max_batch * 17, cudaHostAllocMapped) ||
+        cudaEventCreateWithFlags(&h->ing_ev, cudaEventDisableTiming))
         return cleanup(LAMPS_ECUDA, "cudaHostAlloc");
+    {   // result block: summary | admitted ids | preempted ids | admitted strategies
+        uint8_t* hb = static_cast<uint8_t*>(h->h_res);
+        uint8_t* db = nullptr;
+        if (cudaHostGetDevicePointer((void**)&db, h->h_res, 0) != cudaSuccess)
+            return cleanup(LAMPS_ECUDA, "cudaHostGetDevicePointer");
+        const size_t o_adm = sizeof(HostRes), o_pre = o_adm + (size_t)cfg->max_batch * 8,
+                     o_str = o_pre + (size_t)cfg->max_batch * 8;
+        h->hres = reinterpret_cast<HostRes*>(hb);
+        h->h_adm_ids = reinterpret_cast<uint64_t*>(hb + o_adm);
+        h->h_pre_ids = reinterpret_cast<uint64_t*>(hb + o_pre);
+        h->h_adm_strat = hb + o_str;
+        std::memset(hb, 0, o_str + cfg->max_batch);
+        h->b.hres = reinterpret_cast<HostRes*>(db);
+        h->b.h_adm_id = reinterpret_cast<unsigned long long*>(db + o_adm);
+        h->b.h_pre_id = reinterpret_cast<unsigned long long*>(db + o_pre);
+        h->b.h_adm_strat = db + o_str;
+    }
+    h->hctx.assign(h->cap, 0u);
+    h->adm_mark.assign(h->cap, 0u);
+    h->ev_mark.assign(h->cap, 0u);
+
     if (cfg->flags & LAMPS_TIMING) {
         h->tev.resize((size_t)kTimingRing * 5);
         for (auto& e : h->tev)
@@ -540,9 +606,8 @@ int lamps_free(lamps_t* h) {
     if (h->h_ingest) cudaFreeHost(h->h_ingest);
     if (h->h_ev) cudaFreeHost(h->h_ev);
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
-    if (h->h_adm_ids) cudaFreeHost(h->h_adm_ids);
-    if (h->h_adm_strat) cudaFreeHost(h->h_adm_strat);
-    if (h->h_pre_ids) cudaFreeHost(h->h_pre_ids);
+    if (h->h_res) cudaFreeHost(h->h_res);
+    if (h->ing_ev) cudaEventDestroy(h->ing_ev);
     delete h;
     return LAMPS_OK;
 }
@@ -562,6 +627,7 @@ int lamps_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, uint64_t* id
     SubmitRec* rec = static_cast<SubmitRec*>(h->h_ingest);
     for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
         const uint32_t m = std::min(kIngestChunk, n - k0);
+        if (int rc = staging_wait(h)) return rc;
         for (uint32_t i = 0; i < m; i++) {
             const lamps_segment& s = segs[k0 + i];
             SubmitRec& r = rec[i];
@@ -575,11 +641,12 @@ int lamps_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, uint64_t* id
             r.pad = 0;
         }
         CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(SubmitRec), cudaMemcpyHostToDevice, h->stream));
+        if (int rc = staging_copied(h)) return rc;
         CU(h, launch_submit(h->b.pool, h->cost, static_cast<const SubmitRec*>(h->d_ingest), m, h->stream));
-        CU(h, cudaStreamSynchronize(h->stream));  // staging reuse
     }
     for (uint32_t k = 0; k < n; k++) {
         h->hstate[(h->next_id + k) & h->cost.cap_mask] = H_READY;
+        h->hctx[(h->next_id + k) & h->cost.cap_mask] = segs[k].prompt_len;
         if (ids_out) ids_out[k] = h->next_id + k;
     }
     h->next_id += n;
@@ -610,6 +677,7 @@ int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_
     PredRec* d_out = reinterpret_cast<PredRec*>(d_in + kChunk);
     for (uint32_t k0 = 0; k0 < n; k0 += kChunk) {
         const uint32_t m = std::min(kChunk, n - k0);
+        if (int rc = staging_wait(h)) return rc;
         for (uint32_t i = 0; i < m; i++) {
             const lamps_truth& t = truth[k0 + i];
             tin[i] = TruthRec{t.key, t.pre_len, t.pre_bin, t.resp_len, t.post_len, t.api_ticks, t.has_api};
@@ -649,17 +717,12 @@ int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_res
             return fail(h, LAMPS_EINVAL, "api_return: duplicate id");
     }
     std::vector<uint32_t> ticks(n), ctx(n);
-    // current context of each request (device state) for the ingest checks
-    uint32_t* slots = static_cast<uint32_t*>(h->h_ingest);
-    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
-        const uint32_t m = std::min(kIngestChunk, n - k0);
-        for (uint32_t i = 0; i < m; i++) slots[i] = (uint32_t)(ids[k0 + i] & h->cost.cap_mask);
-        CU(h, cudaMemcpyAsync(h->d_ingest, slots, (size_t)m * 4, cudaMemcpyHostToDevice, h->stream));
-        CU(h, launch_gather_u32(h->b.pool.ctx, static_cast<const uint32_t*>(h->d_ingest), h->d_gather, m,
-                                h->stream));
-        CU(h, cudaMemcpyAsync(ctx.data() + k0, h->d_gather, (size_t)m * 4, cudaMemcpyDeviceToHost, h->stream));
-        CU(h, cudaStreamSynchronize(h->stream));
+    // current context of each request, from the host shadow
+    if (!h->shadow_ok) {
+        const int rc = resync_shadow(h);
+        if (rc) return rc;
     }
+    for (uint32_t k = 0; k < n; k++) ctx[k] = h->hctx[ids[k] & h->cost.cap_mask];
     for (uint32_t k = 0; k < n; k++) {
         if (const char* m = check_segment(h, (uint64_t)ctx[k] + actual_resp_len[k], next[k], &ticks[k]))
             return fail(h, LAMPS_EINVAL, std::string("api_return[") + std::to_string(k) + "]: " + m);
@@ -667,6 +730,7 @@ int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_res
     ReturnRec* rec = static_cast<ReturnRec*>(h->h_ingest);
     for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
         const uint32_t m = std::min(kIngestChunk, n - k0);
+        if (int rc = staging_wait(h)) return rc;
         for (uint32_t i = 0; i < m; i++) {
             const lamps_segment& s = next[k0 + i];
             ReturnRec& r = rec[i];
@@ -680,10 +744,13 @@ int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_res
             r.pad = 0;
         }
         CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(ReturnRec), cudaMemcpyHostToDevice, h->stream));
+        if (int rc = staging_copied(h)) return rc;
         CU(h, launch_api_return(h->b.pool, h->cost, static_cast<const ReturnRec*>(h->d_ingest), m, h->stream));
-        CU(h, cudaStreamSynchronize(h->stream));
     }
-    for (uint32_t k = 0; k < n; k++) h->hstate[ids[k] & h->cost.cap_mask] = H_READY;
+    for (uint32_t k = 0; k < n; k++) {
+        h->hstate[ids[k] & h->cost.cap_mask] = H_READY;
+        h->hctx[ids[k] & h->cost.cap_mask] = ctx[k] + actual_resp_len[k];
+    }
     return LAMPS_OK;
 }
 
@@ -699,20 +766,18 @@ int prepare_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_t
             if (rc) return rc;
         }
         if (n_ev > h->prev_adm.size()) return fail(h, LAMPS_EINVAL, "more events than admitted requests");
-        std::vector<uint64_t> prev(h->prev_adm);
-        std::sort(prev.begin(), prev.end());
-        std::vector<uint64_t> seen;
-        seen.reserve(n_ev);
+        // O(n_ev): a valid event names a live id whose slot the previous step admitted,
+        // at most once (per-slot marks; the live id of a slot is unique)
+        const uint32_t tag = ++h->ev_tag;
         for (uint32_t e = 0; e < n_ev; e++) {
             if (ev[e].kind != LAMPS_EV_API_CALL && ev[e].kind != LAMPS_EV_FINISHED)
                 return fail(h, LAMPS_EINVAL, "unknown event kind");
-            if (!std::binary_search(prev.begin(), prev.end(), ev[e].id))
+            const uint32_t sl = (uint32_t)(ev[e].id & h->cost.cap_mask);
+            if (!id_live(h, ev[e].id) || h->adm_mark[sl] != h->step || h->fetched_step != h->step)
                 return fail(h, LAMPS_EINVAL, "event for a request not admitted by the previous step");
-            seen.push_back(ev[e].id);
+            if (h->ev_mark[sl] == tag) return fail(h, LAMPS_EINVAL, "duplicate event id");
+            h->ev_mark[sl] = tag;
         }
-        std::sort(seen.begin(), seen.end());
-        if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
-            return fail(h, LAMPS_EINVAL, "duplicate event id");
         std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
         CU(h, cudaMemcpyAsync(const_cast<void*>(h->b.events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
                               cudaMemcpyHostToDevice, h->stream));
@@ -833,6 +898,10 @@ int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uin
     CU(h, cudaMemsetAsync(h->b.ctl, 0, sizeof(Ctl), h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
     h->hstate.swap(hs);
+    for (uint32_t s2 = 0; s2 < cap; s2++) h->hctx[s2] = io->state[s2] == LAMPS_FREE ? 0u : io->ctx[s2];
+    h->shadow_ok = true;
+    h->fetched_step = h->step;
+    std::fill(h->adm_mark.begin(), h->adm_mark.end(), 0u);  // previous admitted list cleared
     h->id_base = id_base;
     h->next_id = next_id;
     advance_id_base(h);

@@ -58,6 +58,13 @@ struct Ctl {
     uint32_t pad1;
 };
 
+// Step result delivered straight into mapped pinned host memory by the admission (one
+// stream synchronisation per step, no device-to-host copies): summary, then the lists.
+struct HostRes {
+    unsigned long long n_elig, pinned, budget, budget_used;
+    uint32_t n_admitted, n_preempted, blocked_head, final_buf;
+};
+
 struct StepArgs {
     uint64_t kv_total;
     uint64_t id_base;       // ids of this step's keys are id_base + offset
@@ -91,6 +98,10 @@ struct Bufs {
     uint32_t* flags;         // grid barrier words (see sort_dev.cuh)
     float* cta_cost;         // fused: [grid] measured range-sort cycles per key of each CTA
                              // (EMA over steps; 0 = not measured): weights the key ranges
+    HostRes* hres;           // mapped pinned host memory (device pointer): step summary
+    unsigned long long* h_adm_id;  // mapped: admitted ids [max_batch]
+    unsigned long long* h_pre_id;  // mapped: preempted ids [max_batch]
+    uint8_t* h_adm_strat;          // mapped: admitted strategies [max_batch]
     MergeRec* xsend;         // [1 + K] header + top-K records of this rank (world > 1)
     MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
 };

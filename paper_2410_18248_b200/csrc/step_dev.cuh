@@ -11,6 +11,26 @@ struct DevEvent {
     uint32_t kind, reserved;
 };
 
+// A0 for one engine event about a request admitted by the previous step (K0, or the
+// fused kernel's prologue): API_CALL routes it to P/D/S by argmin waste at C_i = ctx
+// (Alg.1) and resets its counter unless starving; FINISHED frees
+// the slot.  The token of this iteration is counted (SFC_RAN).
+__device__ __forceinline__ void apply_event(const Pool& P, const Cost& c, const DevEvent E) {
+    const uint32_t s = (uint32_t)E.id & c.cap_mask;
+    const uint32_t w = P.sfc[s];
+    if (E.kind == EV_FINISHED) {
+        P.sfc[s] = 0u;
+        return;
+    }
+    const uint32_t ctx = P.ctx[s] + ((w & SFC_RAN) ? 1u : 0u);  // this iteration's token
+    P.ctx[s] = ctx;
+    P.pre[s] = 0u;
+    P.pend[s] = 0u;
+    const uint32_t st = strategy_of(ctx, 0, P.api[s], c);
+    const uint32_t starv = sfc_starv(w);
+    P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u) | (w & SFC_META);
+}
+
 // block-wide exclusive scans (all NT threads call; totals in *tot)
 template <int NT>
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh_warp, uint32_t* tot) {
@@ -269,6 +289,20 @@ __device__ __forceinline__ bool score_slot(const Pool& P, const Cost& c, uint32_
     return true;
 }
 
+// The step summary into mapped host memory (one thread, after the Ctl fields are final).
+__device__ __forceinline__ void publish_host_result(const Bufs& b) {
+    const Ctl* ctl = b.ctl;
+    HostRes* r = b.hres;
+    r->n_elig = ctl->n_elig_out;
+    r->pinned = ctl->pinned_out;
+    r->budget = ctl->budget;
+    r->budget_used = *(volatile const unsigned long long*)&ctl->budget_used;
+    r->n_admitted = ctl->n_admitted;
+    r->n_preempted = ctl->n_preempted;
+    r->blocked_head = ctl->blocked_head;
+    r->final_buf = ctl->final_buf;
+}
+
 // A5 admission by one 1024-thread CTA over the ranked keys (see k_admit).
 struct AdmitSmem {
     unsigned long long w64[32];
@@ -339,6 +373,8 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
             b.adm_slot[par][k] = slot;
             b.adm_id[par][k] = a.id_base + idoff;
             b.adm_strat[par][k] = (uint8_t)sfc_strat(w);
+            b.h_adm_id[k] = a.id_base + idoff;  // the host's copy (mapped memory)
+            b.h_adm_strat[k] = (uint8_t)sfc_strat(w);
             if (htab) {
                 uint32_t h = slot_hash(slot, hmask);
                 while (atomicCAS(&htab[h], kEmpty, slot) != kEmpty) h = (h + 1u) & hmask;
@@ -379,7 +415,10 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
         }
         uint32_t tot;
         const uint32_t pos = block_excl_scan_u32<NT>(f, sm.w32, &tot);
-        if (f) b.pre_id[npre + pos] = id;
+        if (f) {
+            b.pre_id[npre + pos] = id;
+            b.h_pre_id[npre + pos] = id;
+        }
         npre += tot;
     }
     if (tid == 0) {
@@ -391,6 +430,7 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
         ctl->pinned_out = pinned;
         ctl->n_elig = 0;  // accumulators of the next step
         ctl->pinned = 0;
+        publish_host_result(b);
     }
     ATRACE(4);
 #undef ATRACE

@@ -100,5 +100,5 @@ def test_nccl_one_rank_merge_path():
         assert list(g["preempted_id"]) == list(ro["preempted_id"]), t
         assert g["budget"] == ro["budget"] and g["budget_used"] == ro["budget_used"], t
         prev = np.asarray(g["admitted_id"], np.int64)
-    assert s.stats()[0] == 2 + 1  # events + fused + merge
+    assert s.stats()[0] == 1 + 1  # fused (events in its prologue) + merge
     s.close()
