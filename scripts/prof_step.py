@@ -13,6 +13,8 @@ s = Scheduler(cfg, flags=LAMPS_TIMING if os.environ.get("TIMING") else 0)
 s.import_pool(snap, snap["id_base"], snap["next_id"])
 kv = gen.CONFIGS[cname]["kv_total"]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+if os.environ.get("NOFLUSH"):
+    flush = torch.empty(16, dtype=torch.uint8, device="cuda")
 for _ in range(steps):
     flush.zero_()
     s.step_async(kv)
