@@ -102,12 +102,15 @@ __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, ui
     constexpr int NW = NT / 32;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t j0 = threadIdx.x * (uint32_t)R;
+    const bool mine = j0 < L;  // threads past the end skip their (predicated) R words
     uint32_t v[R];
     uint32_t s = 0;
+    if (mine) {
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-        v[r] = j0 + r < L ? arr[j0 + r] : 0u;
-        s += v[r];
+        for (int r = 0; r < R; r++) {
+            v[r] = j0 + r < L ? arr[j0 + r] : 0u;
+            s += v[r];
+        }
     }
     uint32_t x = s;
 #pragma unroll
@@ -131,13 +134,15 @@ __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, ui
     __syncthreads();
     uint32_t run = w32[warp] + x - s;
     const uint32_t total = w32[NW];
+    if (mine) {
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-        if (j0 + r < L) {
-            arr[j0 + r] = run;
-            if (add) add[j0 + r] += run;
+        for (int r = 0; r < R; r++) {
+            if (j0 + r < L) {
+                arr[j0 + r] = run;
+                if (add) add[j0 + r] += run;
+            }
+            run += v[r];
         }
-        run += v[r];
     }
     __syncthreads();
     return total;
