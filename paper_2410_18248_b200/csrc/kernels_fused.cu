@@ -953,6 +953,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                 head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c,
                                                                       half, tr ? tr + 16 : nullptr, &b.pool,
                                                                       a.id_base_mod);
+            else if (rn <= 3u * kFT)  // fewer keys per thread: less code on the executed path
+                (void)range_sort<3, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
+                                           tr ? tr + 16 : nullptr);
+            else if (rn <= 7u * kFT)
+                (void)range_sort<7, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
+                                           tr ? tr + 16 : nullptr);
             else
                 (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
                                                      tr ? tr + 16 : nullptr);
