@@ -46,7 +46,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-variants", action="store_true", help="skip the policy / selective-update variants")
     ap.add_argument("--merge", action="store_true",
-                    help="N=1: run the multi-shard exchange + merge over a 1-rank NCCL communicator")
+                    help="N=1: run the multi-shard exchange + merge path with one rank")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-shard exchange: p2p = peer stores + merge inside the step kernel "
+                         "(CUDA IPC over NVLink), nccl = ncclAllGather + merge kernel")
     return ap.parse_args()
 
 
@@ -194,16 +197,44 @@ def run_ours(args, rank, world, local):
     snap = gen.snapshot(cname, seed=rank, id_base=id_base)
     stream = torch.cuda.current_stream()
 
+    from paper_2410_18248_b200.lamps import LAMPS_XPORT_NCCL, LAMPS_XPORT_P2P
     nccl_id, mflags = None, 0
-    if world > 1:  # one NCCL all-gather per step for the global admission merge
-        obj = [Scheduler.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    elif args.merge:
-        from paper_2410_18248_b200 import LAMPS_MERGE
-        nccl_id, mflags = Scheduler.nccl_unique_id(), LAMPS_MERGE
     merged = world > 1 or args.merge
-    s = Scheduler(cfg, flags=mflags, stream=stream, world=world, rank=rank, nccl_id=nccl_id)
+    transport = args.transport if merged else None
+    if merged and world == 1:
+        from paper_2410_18248_b200 import LAMPS_MERGE
+        mflags = LAMPS_MERGE
+    s = None
+    if merged and transport == "p2p":
+        # peer-memory exchange: every rank maps every rank's exchange buffer (CUDA IPC);
+        # falls back to NCCL if the mapping is not possible on this machine
+        try:
+            s = Scheduler(cfg, flags=mflags, stream=stream, world=world, rank=rank, transport=LAMPS_XPORT_P2P)
+            if world > 1:
+                hs = [None] * world
+                dist.all_gather_object(hs, s.p2p_handle())
+                s.p2p_connect(hs)
+        except Exception as e:  # noqa: BLE001
+            print(f"p2p transport unavailable ({e}); using NCCL", file=sys.stderr)
+            if s is not None:
+                s.close()
+            s, transport = None, "nccl"
+        if world > 1:  # every rank must agree on the transport
+            flag = torch.tensor([1 if transport == "p2p" else 0], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if transport == "p2p" and int(flag.item()) == 0:
+                s.close()
+                s, transport = None, "nccl"
+    if merged and transport == "nccl":
+        if world > 1:
+            obj = [Scheduler.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+        else:
+            nccl_id = Scheduler.nccl_unique_id()
+    if s is None:
+        s = Scheduler(cfg, flags=mflags, stream=stream, world=world, rank=rank, nccl_id=nccl_id,
+                      transport=LAMPS_XPORT_NCCL)
     s.import_pool(snap, snap["id_base"], snap["next_id"])
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device="cuda")
@@ -241,7 +272,7 @@ def run_ours(args, rank, world, local):
     res = s.result()
     n_elig = res["n_eligible"]
     kernels, passes = s.stats()
-    fused = kernels == (2 if merged else 1)
+    fused = kernels == (2 if merged and transport == "nccl" else 1)
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     ne_t = torch.tensor([float(n_elig)], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -367,7 +398,7 @@ def run_ours(args, rank, world, local):
         # the state word written once (4 B/slot), and the keys written and read once (16 B/key)
         step_bytes = 32 * cap + 16 * n_elig
         if phase is None:  # multi-GPU: whole step (fused kernel + all-gather + merge), max over ranks
-            dom = "k_fused+merge"
+            dom = "k_fused+merge" if transport == "nccl" else "k_fused"
             kernels_tbl = {dom: {"ms": ms_max, "bytes": step_bytes, "GBps": step_bytes / (ms_max * 1e6)}}
         elif fused:
             dom = "k_fused"
@@ -392,6 +423,8 @@ def run_ours(args, rank, world, local):
                 traffic = json.load(open(tp)).get(dom)
             except Exception:
                 traffic = None
+        xdesc = ("peer stores into every rank's buffer + merge inside the step kernel" if transport == "p2p"
+                 else "NCCL all-gather + merge kernel")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "us_per_step": ms_max * 1e3,
@@ -402,15 +435,15 @@ def run_ours(args, rank, world, local):
                        "kv_total_blocks": kv, "max_batch": cfg["max_batch"],
                        "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
                        "l2": "flushed before every timed step (256 MiB write)",
-                       "parallelism": (f"{world} shards x 1M, one NCCL all-gather of the top-{cfg['max_batch']} "
-                                       f"per step for the global admission") if world > 1 else
-                                      ("1 shard, exchange + merge over a 1-rank NCCL communicator" if merged
+                       "parallelism": (f"{world} shards x 1M, one exchange of the top-{cfg['max_batch']} per "
+                                       f"step for the global admission ({xdesc})") if world > 1 else
+                                      (f"1 shard, exchange + merge with one rank ({xdesc})" if merged
                                        else "1 shard")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak if ach else None, "traffic": traffic,
                          "peak_source": peak_src},
             "kernels": kernels_tbl,
-            "path": ("fused cooperative step kernel" + (" + NCCL all-gather + merge kernel" if merged else "")) if fused else "3-kernel path",
+            "path": ("fused cooperative step kernel" + (f" ({xdesc})" if merged else "")) if fused else "3-kernel path",
             "sort_passes": passes,
             "gpu_launches": kernels * args.steps,
             "clocks": clk.summary(),

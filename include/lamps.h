@@ -79,6 +79,10 @@ extern "C" {
                                    state are those of the full pass; lamps_ranked_keys returns the
                                    head only.  Fused path; the 3-kernel path ranks everything */
 
+#define LAMPS_SHARE_DEVICE 128u /* P2P ranks co-resident on ONE device (lamps_p2p_connect_local, tests):
+                                   the step kernel uses #SM / world CTAs so all ranks' kernels run
+                                   at once; each rank needs its own stream */
+
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 
 typedef struct lamps_s lamps_t;
@@ -148,6 +152,12 @@ typedef struct {
 
 #define LAMPS_XPORT_NCCL 0u     /* one ncclAllGather per step over NVLink (libnccl.so.2) */
 #define LAMPS_XPORT_LOOPBACK 1u /* all shards in this process on one device: lamps_group_step */
+#define LAMPS_XPORT_P2P 2u      /* no library collective: inside the step kernel, CTA 0 stores its
+                                   records straight into every rank's exchange buffer (CUDA IPC
+                                   mappings over NVLink / NVSwitch), raises a flag on each, waits
+                                   for all ranks' flags and merges + admits -- one kernel per step.
+                                   Needs lamps_p2p_handle / lamps_p2p_connect after lamps_init
+                                   (world 1: self-exchange, no connect needed) */
 
 /*
  * Result of one step.  Host arrays are owned by the handle and stay valid until
@@ -381,6 +391,20 @@ typedef struct {
  */
 int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_noise* noise,
                   lamps_segment* out);
+
+/*
+ * Peer-memory transport (LAMPS_XPORT_P2P).  lamps_p2p_handle writes this rank's 64-byte
+ * cudaIpcMemHandle of its exchange buffer (library-allocated, p2p layout) to out64;
+ * the caller all-gathers the handles (e.g. torch.distributed) and passes them to
+ * lamps_p2p_connect (world * 64 bytes, rank order), which maps every peer's buffer
+ * (cudaIpcOpenMemHandle).  lamps_p2p_connect_local connects `world` handles of this
+ * process that share one device (LAMPS_SHARE_DEVICE; the buffers are used directly).
+ * Every rank must then call lamps_schedule_step the same number of times (the step
+ * kernels wait for each other).  Errors: EINVAL (wrong transport / sizes), ECUDA.
+ */
+int lamps_p2p_handle(lamps_t* h, void* out64);
+int lamps_p2p_connect(lamps_t* h, const void* handles, size_t n_bytes);
+int lamps_p2p_connect_local(lamps_t* const* hs, uint32_t world);
 
 /* Library version (major << 16 | minor). */
 uint32_t lamps_version(void);

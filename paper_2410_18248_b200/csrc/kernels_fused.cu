@@ -19,6 +19,7 @@
 //      near-equal scores) every CTA runs the grid-synchronous global LSD sort
 //      instead (sort_dev.cuh).
 //   A  CTA 0 admits (A5) as soon as the head of the order it needs is sorted.
+#include "merge_dev.cuh"
 #include "sort_dev.cuh"
 #include "step_dev.cuh"
 
@@ -47,6 +48,7 @@ struct PhaseS {                  // S, H, T, X
     float ccost[kMaxCtas];       // range-sort cycles per key of each CTA (previous steps)
     uint32_t rb[kMaxCtas + 1], jb[kMaxCtas + 1];  // X: key / bucket boundaries of the ranges
     float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
+    uint32_t jtrim[2];           // X: this CTA's range, non-empty buckets [jtrim[0], jtrim[1])
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -85,6 +87,15 @@ union FusedSmem {
     PhaseL l;
     SortSmem g;
 };
+// After the union, untouched by every phase: the peer-memory exchange's state (peer
+// buffer pointers, prefetched at kernel start) and the in-kernel merge's small structures.
+struct SmemTail {
+    MergeRec* xp[32];
+    AdmitSmem adm;
+    uint32_t nv[32];
+    unsigned long long hsum[2];
+};
+constexpr size_t kFusedSmemBytes = sizeof(FusedSmem) + ((sizeof(SmemTail) + 127) & ~(size_t)127);
 
 // Bucket of a key: (starving flag, bit length e of v = the key's score|id bits, the
 // next kBucketM bits of v) -- a float-like, exact monotone function of the key.  Over
@@ -631,6 +642,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     TRACE(0);
     // the CTAs' measured range-sort costs (previous steps) -> shared memory by cp.async, so
     // the L2 latency hides behind the score phase; they weight the key ranges (X)
+    SmemTail& tail = *reinterpret_cast<SmemTail*>(smem_raw + sizeof(FusedSmem));
+    if ((a.flags & kStepP2P) && tid < a.world) {  // the peers' exchange buffers
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tail.xp[tid]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;" ::"r"(dst),
+                     "l"(b.xpeers + tid) : "memory");
+    }
     if (tid < G && tid < (uint32_t)kMaxCtas) {
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.s.ccost[tid]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\ncp.async.commit_group;" ::"r"(dst),
@@ -852,7 +869,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             // end of their bucket) so it can start the admission early; the other CTAs share
             // the rest in proportion to their measured speed (cycles per key of the previous
             // steps' range sorts: some SMs of a B200 run this phase markedly slower), weight
-            // mean/cost capped at 1.25; below 0.4 the CTA gets no range (G <= 255)
+            // mean/cost capped at 1.15 (keeps a range within 7 keys per thread); below 0.4 the CTA gets no range (G <= 255)
             float* wx = sm.s.wx;  // [G + 1] exclusive weight prefix
             if (warp == 0) {
                 constexpr int kW = kMaxCtas / 32;
@@ -877,7 +894,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                     w[u] = 0.f;
                     if (r >= 1 && r < G) {
                         const float rel = cst[u] > 0.f ? __fdividef(mean, cst[u]) : 1.f;
-                        w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.25f);
+                        w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.15f);
                     }
                     run += w[u];
                 }
@@ -925,8 +942,28 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     if (tid < G) mx = rb[tid + 1] - rb[tid];
     const bool fallback = (a.flags & kStepForceFallback) ||
                           __syncthreads_or(mx > (uint32_t)kKcap);
+    // trim this range's bucket interval to its non-empty buckets (leading / trailing empty
+    // buckets share the boundary's start): the first bucket is the last one starting at
+    // r_lo, the end is the first bucket starting at r_hi.  Keeps the head range and the
+    // ranges next to the starving / non-starving split from spanning thousands of buckets.
+    if (tid == 0) {
+        const uint32_t rl = rb[bid], rh = rb[bid + 1];
+        auto first_ge = [&](uint32_t x) {
+            uint32_t lo = 0, hi = NB;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sm.s.start[mid] >= x) hi = mid; else lo = mid + 1;
+            }
+            return lo;
+        };
+        const uint32_t jh = first_ge(rh);
+        const uint32_t jl = rl < rh ? first_ge(rl + 1u) - 1u : jh;
+        sm.s.jtrim[0] = jl;
+        sm.s.jtrim[1] = jh;
+    }
+    __syncthreads();
     const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
-    const uint32_t j_lo = jb[bid], j_hi = jb[bid + 1];
+    const uint32_t j_lo = sm.s.jtrim[0], j_hi = sm.s.jtrim[1];
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
     TRACE(7);
@@ -1047,27 +1084,85 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
         const uint32_t K = a.max_batch, nv = min(n, K);
         const uint64_t idmask = (1ull << c.IB) - 1ull;
-        for (uint32_t i = tid; i < nv; i += kFT) {
-            const uint64_t k = head[i];
-            const uint64_t lid = a.id_base + (k & idmask);
-            const uint32_t slot = (uint32_t)(lid & c.cap_mask);
+        const bool p2p = (a.flags & kStepP2P) != 0;
+        const uint32_t W = a.world, par = a.xseq & 1u;
+        // peer-memory transport: record i of this rank goes to every peer's receive area
+        // [par][rank] by NVLink stores (the one-shot all-gather), then flags, then the merge
+        const size_t slot0 = ((size_t)par * W + a.rank) * (K + 1);
+        for (uint32_t i = tid; i <= nv; i += kFT) {
             MergeRec r;
-            r.sk = k >> c.IB;
-            r.gid = lid * a.world + a.rank;
-            r.demand = dw ? reinterpret_cast<const uint32_t*>(sm.l.b)[kHeadD + i]
-                          : (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
-            r.slot = slot;
-            r.pad = 0;
-            b.xsend[1 + i] = r;
+            if (i == 0) {
+                MergeHdr* h = reinterpret_cast<MergeHdr*>(&r);
+                h->pinned = pinned_all;
+                h->kv_total = a.kv_total;
+                h->n_valid = nv;
+                h->n_local = n;
+                h->pad = 0;
+            } else {
+                const uint64_t k = head[i - 1];
+                const uint64_t lid = a.id_base + (k & idmask);
+                const uint32_t slot = (uint32_t)(lid & c.cap_mask);
+                r.sk = k >> c.IB;
+                r.gid = lid * a.world + a.rank;
+                r.demand = dw ? reinterpret_cast<const uint32_t*>(sm.l.b)[kHeadD + i - 1]
+                              : (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
+                r.slot = slot;
+                r.pad = 0;
+            }
+            if (p2p) {
+                for (uint32_t p = 0; p < W; p++) tail.xp[p][slot0 + i] = r;
+            } else {
+                b.xsend[i] = r;
+            }
         }
+        if (!p2p) {
+            TRACE(9);
+            return;
+        }
+        unsigned long long* xtr = b.trace ? b.trace + 48 : nullptr;  // CTA 0's slots 48..55
+        if (xtr && tid == 0) xtr[0] = clock64();
+        __syncthreads();
+        const size_t nrec = p2p_rec_count(W, K);
+        // the CTA's records (ordered before by the barrier) before the flags: system scope
+        // when the peers are other GPUs, device scope when every rank shares this device
+        const bool sys = (a.flags & kStepP2PSys) != 0;
         if (tid == 0) {
-            MergeHdr* h = reinterpret_cast<MergeHdr*>(b.xsend);
-            h->pinned = pinned_all;
-            h->kv_total = a.kv_total;
-            h->n_valid = nv;
-            h->n_local = n;
-            h->pad = 0;
+            if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+            else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (uint32_t p = 0; p < W; p++) {
+                uint32_t* pf = reinterpret_cast<uint32_t*>(tail.xp[p] + nrec) + par * 32u + a.rank;
+                if (sys) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(pf), "r"(a.xseq) : "memory");
+                else asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(pf), "r"(a.xseq) : "memory");
+            }
+            if (xtr) xtr[1] = clock64();
         }
+        if (tid < W) {
+            const uint32_t* of = reinterpret_cast<const uint32_t*>(b.xown + nrec) + par * 32u + tid;
+            uint32_t v;
+            do {
+                if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(of) : "memory");
+                else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(of) : "memory");
+            } while (v != a.xseq);
+        }
+        __syncthreads();
+        TRACE(15);
+        // merge scratch over sm.l.a (the head keys are no longer needed there: the admission
+        // reads this rank's keys from b.keys), small structures at the end of shared memory.
+        // While the scratch stays inside sm.l.a the admission keeps the preempted-check hash
+        // table (start of sm.l.b) and, below the staged head arrays, their demand / state words
+        const size_t mb = merge_smem_bytes(W, K);
+        AdmitSmem& madm = tail.adm;
+        uint32_t* mnv = tail.nv;
+        unsigned long long* mhs = tail.hsum;
+        uint32_t hs = 1024;
+        while (hs < 2u * K) hs <<= 1;
+        const bool in_a = mb <= sizeof(sm.l.a) && !wait;
+        const bool use_h = in_a && hs <= kHeadTC;
+        const bool use_d = dw && mb <= (size_t)kHeadD * 4u + sizeof(sm.l.a);
+        uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.l.b);
+        merge_admit_cta(b, c, a, b.xown + (size_t)par * W * (K + 1), smem_raw, madm, mnv, mhs,
+                        use_h ? b32 : nullptr, use_h ? hs : 0u, use_d ? b32 + kHeadD : nullptr,
+                        use_d ? b32 + kHeadW : nullptr, xtr ? xtr + 2 : nullptr);
         TRACE(9);
         return;
     }
@@ -1085,14 +1180,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
 
 }  // namespace
 
-static_assert(sizeof(FusedSmem) <= 232448, "fused kernel shared memory exceeds 227 KB");
-size_t fused_smem_bytes() { return sizeof(FusedSmem); }
+static_assert(kFusedSmemBytes <= 232448, "fused kernel shared memory exceeds 227 KB");
+size_t fused_smem_bytes() { return sizeof(FusedSmem); }  // the union (in-kernel merge scratch limit)
 
 int fused_blocks_per_sm() {
     int nb = 0;
-    cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
-    cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused<false>, kFT, sizeof(FusedSmem));
+    cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmemBytes);
+    cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused<false>, kFT, kFusedSmemBytes);
     return nb;
 }
 
@@ -1104,7 +1199,7 @@ cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32
     StepArgs aa = a;
     void* args[] = {&bb, &cc, &aa};
     const void* fn = b.dbg ? (const void*)k_fused<true> : (const void*)k_fused<false>;
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFT), args, sizeof(FusedSmem), s);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFT), args, kFusedSmemBytes, s);
 }
 
 }  // namespace lamps

@@ -88,6 +88,12 @@ struct lamps_s {
     bool fused = false;
     uint32_t world = 1, rank = 0;
     bool merge = false;  // merge_mode(cfg)
+    // peer-memory transport
+    MergeRec* xbuf = nullptr;            // own exchange buffer (cudaMalloc, IPC-exportable)
+    MergeRec** d_peers = nullptr;        // device table of the world ranks' buffers
+    std::vector<void*> peer_open;        // IPC mappings to close
+    bool p2p_ready = false;
+    uint32_t xseq = 0;
     nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
@@ -170,9 +176,13 @@ const char* validate_cfg(const lamps_config* c) {
     if (c->world > 1 || (c->flags & LAMPS_MERGE)) {
         if (c->world > 32 || c->rank >= (c->world > 1 ? c->world : 1u)) return "need rank < world <= 32";
         if ((uint64_t)c->world * c->max_batch > kMergeMaxRecords) return "world * max_batch must be <= 8192";
-        if (c->transport > LAMPS_XPORT_LOOPBACK) return "unknown transport";
+        if (c->transport > LAMPS_XPORT_P2P) return "unknown transport";
         if (c->transport == LAMPS_XPORT_NCCL && !c->nccl_id) return "NCCL transport needs nccl_id";
-        if (c->world <= 1 && c->transport != LAMPS_XPORT_NCCL) return "LAMPS_MERGE at world 1 needs the NCCL transport";
+        if (c->world <= 1 && c->transport == LAMPS_XPORT_LOOPBACK)
+            return "LAMPS_MERGE at world 1 needs the NCCL or P2P transport";
+        if (c->transport == LAMPS_XPORT_P2P &&
+            merge_smem_bytes(c->world > 1 ? c->world : 1u, c->max_batch) + 1024 > fused_smem_bytes())
+            return "P2P transport: world * max_batch too large for the in-kernel merge";
     }
     return nullptr;
 }
@@ -260,6 +270,8 @@ void grids(lamps_t* h, bool query_device) {
         fused_occ = fused_blocks_per_sm();
     }
     h->fused_grid = (uint32_t)std::max(1, sms * std::max(fused_occ, 1));
+    if ((h->cfg.flags & LAMPS_SHARE_DEVICE) && h->cfg.world > 1)  // co-resident ranks split the SMs
+        h->fused_grid = std::max<uint32_t>(1u, h->fused_grid / h->cfg.world);
     {
         const uint32_t groups = (h->cap + 3) / 4;
         const uint32_t gpc = (groups + h->fused_grid - 1) / h->fused_grid;
@@ -352,6 +364,11 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.world = h->world;
     a.rank = h->rank;
     if (h->merge) a.flags |= kStepMerge;
+    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
+        a.flags |= kStepP2P;
+        if (h->world > 1 && !(h->cfg.flags & LAMPS_SHARE_DEVICE)) a.flags |= kStepP2PSys;
+        a.xseq = h->xseq;
+    }
     if (h->cfg.flags & LAMPS_HEAD_ONLY) a.flags |= kStepHeadOnly;
     return a;
 }
@@ -359,6 +376,10 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
 // phase 1: events, scoring, ranking (and, single shard, admission)
 int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     const bool timing = (h->cfg.flags & LAMPS_TIMING) != 0;
+    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
+        if (!h->p2p_ready) return fail(h, LAMPS_EINVAL, "P2P transport: call lamps_p2p_connect first");
+        h->xseq++;  // every rank steps in lockstep, so the sequence numbers agree
+    }
     if (timing && h->t_count == kTimingRing) return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
     if (h->have_result && h->fetched_step != h->step) h->shadow_ok = false;  // an unread admitted list
     h->step++;
@@ -378,13 +399,13 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         record_timing(h, 3);
         CU(h, launch_admit(h->b, h->cost, a, h->stream));
     }
-    h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);
+    h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);  // P2P: the exchange and merge are in k_fused
     return LAMPS_OK;
 }
 
 // phase 2 (world > 1): exchange the top-K records, merge, admit this rank's share
 int enqueue_phase2(lamps_t* h, uint64_t kv_total, uint32_t n_ev, bool exchange) {
-    if (h->merge) {
+    if (h->merge && h->cfg.transport != LAMPS_XPORT_P2P) {  // P2P: exchanged and merged in k_fused
         const StepArgs a = make_args(h, kv_total, n_ev);
         if (exchange) {
             const size_t bytes = ((size_t)h->cfg.max_batch + 1) * sizeof(MergeRec);
@@ -406,8 +427,10 @@ int enqueue_phase2(lamps_t* h, uint64_t kv_total, uint32_t n_ev, bool exchange) 
 }
 
 int enqueue_step(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
-    if (h->world > 1 && h->cfg.transport != LAMPS_XPORT_NCCL)
+    if (h->world > 1 && h->cfg.transport == LAMPS_XPORT_LOOPBACK)
         return fail(h, LAMPS_EINVAL, "loopback shards step together: use lamps_group_step");
+    if (h->world > 1 && (h->cfg.flags & LAMPS_SHARE_DEVICE))
+        return fail(h, LAMPS_EINVAL, "ranks sharing one device step together: use lamps_group_step");
     int rc = enqueue_phase1(h, kv_total, n_ev);
     if (rc) return rc;
     return enqueue_phase2(h, kv_total, n_ev, true);
@@ -586,6 +609,20 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
             if (cudaEventCreate(&e) != cudaSuccess) return cleanup(LAMPS_ECUDA, "event");
     }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "sync");
+    if (h->merge && cfg->transport == LAMPS_XPORT_P2P) {
+        const size_t xb = p2p_bytes(h->world, cfg->max_batch);
+        if (cudaMalloc((void**)&h->xbuf, xb) != cudaSuccess ||
+            cudaMalloc((void**)&h->d_peers, (size_t)h->world * sizeof(MergeRec*)) != cudaSuccess ||
+            cudaMemset(h->xbuf, 0, xb) != cudaSuccess)
+            return cleanup(LAMPS_ECUDA, "P2P exchange buffer");
+        h->b.xown = h->xbuf;
+        h->b.xpeers = h->d_peers;
+        if (h->world == 1) {  // self-exchange: the same kernel path with one rank
+            if (cudaMemcpy(h->d_peers, &h->xbuf, sizeof(MergeRec*), cudaMemcpyHostToDevice) != cudaSuccess)
+                return cleanup(LAMPS_ECUDA, "P2P table");
+            h->p2p_ready = true;
+        }
+    }
     if (h->merge && cfg->transport == LAMPS_XPORT_NCCL) {
         if (!g_nccl.load()) return cleanup(LAMPS_ENCCL, "libnccl.so.2 not loadable");
         NcclId id;
@@ -600,6 +637,9 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
 int lamps_free(lamps_t* h) {
     if (!h) return LAMPS_EINVAL;
     cudaStreamSynchronize(h->stream);
+    for (void* p : h->peer_open) cudaIpcCloseMemHandle(p);
+    if (h->d_peers) cudaFree(h->d_peers);
+    if (h->xbuf) cudaFree(h->xbuf);
     if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
     for (auto& e : h->tev)
         if (e) cudaEventDestroy(e);
@@ -801,10 +841,15 @@ int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64
 int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* const* ev, const uint32_t* n_ev,
                      const uint64_t* kv_total, lamps_step_out* out) {
     if (!hs || !n_ev || !kv_total || world < 2 || world > 32) return LAMPS_EINVAL;
+    const bool p2p = hs[0] && hs[0]->cfg.transport == LAMPS_XPORT_P2P;
     for (uint32_t r = 0; r < world; r++) {
-        if (!hs[r] || hs[r]->world != world || hs[r]->rank != r || hs[r]->cfg.transport != LAMPS_XPORT_LOOPBACK ||
-            hs[r]->cfg.max_batch != hs[0]->cfg.max_batch || hs[r]->stream != hs[0]->stream)
-            return fail(hs[0], LAMPS_EINVAL, "group: handles must be loopback ranks 0..world-1 on one stream");
+        if (!hs[r] || hs[r]->world != world || hs[r]->rank != r || hs[r]->cfg.max_batch != hs[0]->cfg.max_batch)
+            return fail(hs[0], LAMPS_EINVAL, "group: handles must be ranks 0..world-1");
+        if (!p2p && (hs[r]->cfg.transport != LAMPS_XPORT_LOOPBACK || hs[r]->stream != hs[0]->stream))
+            return fail(hs[0], LAMPS_EINVAL, "group: loopback handles on one stream");
+        if (p2p && (hs[r]->cfg.transport != LAMPS_XPORT_P2P || !(hs[r]->cfg.flags & LAMPS_SHARE_DEVICE) ||
+                    (r && hs[r]->stream == hs[0]->stream)))
+            return fail(hs[0], LAMPS_EINVAL, "group: P2P handles need LAMPS_SHARE_DEVICE and one stream each");
     }
     for (uint32_t r = 0; r < world; r++) {
         int rc = prepare_step(hs[r], ev ? ev[r] : nullptr, n_ev[r], kv_total[r]);
@@ -815,7 +860,7 @@ int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* cons
         if (rc) return rc;
     }
     const size_t bytes = ((size_t)hs[0]->cfg.max_batch + 1) * sizeof(MergeRec);
-    for (uint32_t d = 0; d < world; d++)
+    for (uint32_t d = 0; d < world && !p2p; d++)
         for (uint32_t r = 0; r < world; r++)
             CU(hs[d], cudaMemcpyAsync(reinterpret_cast<uint8_t*>(hs[d]->b.xrecv) + r * bytes, hs[r]->b.xsend, bytes,
                                       cudaMemcpyDeviceToDevice, hs[d]->stream));
@@ -826,6 +871,46 @@ int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* cons
     for (uint32_t r = 0; r < world; r++) {
         int rc = fetch_result(hs[r], out ? &out[r] : nullptr);
         if (rc) return rc;
+    }
+    return LAMPS_OK;
+}
+
+int lamps_p2p_handle(lamps_t* h, void* out64) {
+    if (!h || !out64) return LAMPS_EINVAL;
+    if (!h->xbuf) return fail(h, LAMPS_EINVAL, "not a P2P-transport handle");
+    CU(h, cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(out64), h->xbuf));
+    return LAMPS_OK;
+}
+
+int lamps_p2p_connect(lamps_t* h, const void* handles, size_t n_bytes) {
+    if (!h || !handles) return LAMPS_EINVAL;
+    if (!h->xbuf) return fail(h, LAMPS_EINVAL, "not a P2P-transport handle");
+    if (n_bytes != (size_t)h->world * sizeof(cudaIpcMemHandle_t)) return fail(h, LAMPS_EINVAL, "need world handles");
+    std::vector<MergeRec*> tab(h->world);
+    for (uint32_t r = 0; r < h->world; r++) {
+        if (r == h->rank) { tab[r] = h->xbuf; continue; }
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(hd), sizeof(hd));
+        void* p = nullptr;
+        CU(h, cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+        h->peer_open.push_back(p);
+        tab[r] = static_cast<MergeRec*>(p);
+    }
+    CU(h, cudaMemcpy(h->d_peers, tab.data(), tab.size() * sizeof(MergeRec*), cudaMemcpyHostToDevice));
+    h->p2p_ready = true;
+    return LAMPS_OK;
+}
+
+int lamps_p2p_connect_local(lamps_t* const* hs, uint32_t world) {
+    if (!hs || world < 1 || world > 32) return LAMPS_EINVAL;
+    std::vector<MergeRec*> tab(world);
+    for (uint32_t r = 0; r < world; r++) {
+        if (!hs[r] || !hs[r]->xbuf || hs[r]->world != world || hs[r]->rank != r) return LAMPS_EINVAL;
+        tab[r] = hs[r]->xbuf;
+    }
+    for (uint32_t r = 0; r < world; r++) {
+        CU(hs[r], cudaMemcpy(hs[r]->d_peers, tab.data(), tab.size() * sizeof(MergeRec*), cudaMemcpyHostToDevice));
+        hs[r]->p2p_ready = true;
     }
     return LAMPS_OK;
 }

@@ -21,6 +21,8 @@ constexpr int kFusedKcap = 10240;    // keys per SM kept in shared memory by the
 constexpr uint32_t kStepForceFallback = 1u;  // StepArgs.flags: fused kernel takes the global LSD
 constexpr uint32_t kStepMerge = 2u;          // StepArgs.flags: emit top-K records, no local admission
 constexpr uint32_t kStepHeadOnly = 4u;       // StepArgs.flags: rank only the admission head (F3)
+constexpr uint32_t kStepP2P = 8u;            // StepArgs.flags: exchange by peer stores + merge in k_fused
+constexpr uint32_t kStepP2PSys = 16u;        // StepArgs.flags: the peers are other GPUs (system scope)
 constexpr uint32_t kMergeMaxRecords = 8192;  // world * max_batch limit of the merge kernel
 
 // multi-GPU exchange: per rank one header followed by K records (32 B each)
@@ -36,6 +38,12 @@ struct MergeRec {
     unsigned long long pad;
 };
 static_assert(sizeof(MergeHdr) == 32 && sizeof(MergeRec) == 32, "exchange records are 32 B");
+// Peer-memory exchange buffer of one rank: records [2 parities][world][K + 1] (header +
+// K records from each source rank), then flags [2][32] u32 (source rank's sequence number).
+__host__ __device__ inline size_t p2p_rec_count(uint32_t world, uint32_t K) { return 2ull * world * (K + 1ull); }
+__host__ __device__ inline size_t p2p_bytes(uint32_t world, uint32_t K) {
+    return p2p_rec_count(world, K) * sizeof(MergeRec) + 2 * 32 * 4;
+}
 constexpr int kTraceSlots = 64;
 constexpr uint32_t kBarPerStep = 64;  // grid-barrier values reserved per step
 
@@ -76,6 +84,7 @@ struct StepArgs {
     uint32_t parity;        // admitted list buffer written this step
     uint32_t flags;         // kStepForceFallback, kStepMerge, kStepHeadOnly
     uint32_t world, rank;   // multi-GPU shards
+    uint32_t xseq;          // peer-memory exchange: sequence number of this step's exchange
 };
 
 struct Bufs {
@@ -102,6 +111,9 @@ struct Bufs {
     unsigned long long* h_adm_id;  // mapped: admitted ids [max_batch]
     unsigned long long* h_pre_id;  // mapped: preempted ids [max_batch]
     uint8_t* h_adm_strat;          // mapped: admitted strategies [max_batch]
+    MergeRec* const* xpeers; // peer-memory transport: [world] exchange buffers (device pointers,
+                             // peers' mapped through CUDA IPC), layout p2p_* below
+    MergeRec* xown;          // this rank's exchange buffer (the receive side)
     MergeRec* xsend;         // [1 + K] header + top-K records of this rank (world > 1)
     MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
 };
@@ -117,6 +129,11 @@ int fused_blocks_per_sm();
 uint32_t fused_max_buckets();
 cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t grid, cudaStream_t s);
 cudaError_t launch_merge(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
+// merge scratch: sk, gid (8 B) and demand (4 B) per record of the W runs, 3 index arrays of K
+__host__ __device__ inline size_t merge_smem_bytes(uint32_t world, uint32_t K) {
+    const size_t R = (size_t)world * K;
+    return R * 8 * 2 + R * 4 + (size_t)K * 4 * 3;
+}
 cudaError_t launch_admit(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 
 // ingest records (host -> device staging)

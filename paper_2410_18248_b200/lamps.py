@@ -21,7 +21,8 @@ LAMPS_EV_API_CALL, LAMPS_EV_FINISHED = 1, 2
 LAMPS_DEBUG_OUT, LAMPS_TIMING, LAMPS_MULTI_KERNEL, LAMPS_FORCE_FALLBACK, LAMPS_TRACE, LAMPS_MERGE = 1, 2, 4, 8, 16, 32
 LAMPS_HEAD_ONLY = 64
 LAMPS_POLICY_LAMPS, LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL = 0, 1, 2, 3
-LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK = 0, 1
+LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK, LAMPS_XPORT_P2P = 0, 1, 2
+LAMPS_SHARE_DEVICE = 128
 
 u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 
@@ -108,6 +109,9 @@ def lib() -> ctypes.CDLL:
             "lamps_group_step": (c_int, [vp, u32, vp, vp, vp, vp]),
             "lamps_version": (u32, []),
             "lamps_predict": (c_int, [vp, vp, u32, P(lamps_noise), vp]),
+            "lamps_p2p_handle": (c_int, [vp, vp]),
+            "lamps_p2p_connect": (c_int, [vp, vp, ctypes.c_size_t]),
+            "lamps_p2p_connect_local": (c_int, [vp, u32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -343,6 +347,26 @@ class Scheduler:
         if rc != LAMPS_OK:
             raise LampsError(rc, lamps_last_error(shards[0].h))
         return [shards[r]._result(outs[r]) for r in range(W)]
+
+    # ---- peer-memory transport (LAMPS_XPORT_P2P)
+    def p2p_handle(self) -> bytes:
+        """This rank's 64-byte CUDA IPC handle of its exchange buffer."""
+        buf = ctypes.create_string_buffer(64)
+        self._check(lib().lamps_p2p_handle(self.h, buf))
+        return buf.raw
+
+    def p2p_connect(self, handles: list):
+        """Map every rank's exchange buffer (handles in rank order, from p2p_handle)."""
+        blob = b"".join(handles)
+        self._check(lib().lamps_p2p_connect(self.h, blob, len(blob)))
+
+    @staticmethod
+    def p2p_connect_local(shards):
+        """Connect P2P ranks that live in this process on one device (LAMPS_SHARE_DEVICE)."""
+        hs = (vp * len(shards))(*[s.h for s in shards])
+        rc = lib().lamps_p2p_connect_local(hs, len(shards))
+        if rc != LAMPS_OK:
+            raise LampsError(rc, lamps_last_error(shards[0].h))
 
     # ---- snapshots
     def import_pool(self, fields: dict, id_base: int, next_id: int):

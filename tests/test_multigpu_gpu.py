@@ -12,14 +12,19 @@ from shard_util import FIELDS, restrict, split_kv, union_and_shards
 pytestmark = pytest.mark.gpu
 
 
-def run(cname, world, cap_l, n_union, kv_union, steps=3, seed=0, **over):
+def run(cname, world, cap_l, n_union, kv_union, steps=3, seed=0, p2p=False, **over):
     from paper_2410_18248_b200 import Scheduler
-    from paper_2410_18248_b200.lamps import LAMPS_XPORT_LOOPBACK
+    from paper_2410_18248_b200.lamps import LAMPS_SHARE_DEVICE, LAMPS_XPORT_LOOPBACK, LAMPS_XPORT_P2P
     import torch
     cfg_l, cfg_u, u, shards = union_and_shards(cname, world, cap_l, n_union, seed=seed, **over)
-    stream = torch.cuda.current_stream()
-    S = [Scheduler(cfg_l, world=world, rank=r, transport=LAMPS_XPORT_LOOPBACK, stream=stream)
-         for r in range(world)]
+    if p2p:  # peer-memory exchange inside the step kernel; ranks co-resident on this device
+        S = [Scheduler(cfg_l, world=world, rank=r, transport=LAMPS_XPORT_P2P, flags=LAMPS_SHARE_DEVICE,
+                       stream=torch.cuda.Stream()) for r in range(world)]
+        Scheduler.p2p_connect_local(S)
+    else:
+        stream = torch.cuda.current_stream()
+        S = [Scheduler(cfg_l, world=world, rank=r, transport=LAMPS_XPORT_LOOPBACK, stream=stream)
+             for r in range(world)]
     for r in range(world):
         S[r].import_pool(shards[r], shards[r]["id_base"], shards[r]["next_id"])
     o = O.OraclePool(cfg_u)
@@ -102,3 +107,38 @@ def test_nccl_one_rank_merge_path():
         prev = np.asarray(g["admitted_id"], np.int64)
     assert s.stats()[0] == 1 + 1  # fused (events in its prologue) + merge
     s.close()
+
+
+# ---- peer-memory transport: records stored into every rank's buffer, flags, merge and
+# admission inside the fused step kernel (one kernel per rank per step)
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_merge_c2(world):
+    run("C2", world, 2048, 1800, 3000, max_batch=256, p2p=True, steps=4)
+
+
+def test_p2p_merge_c4():
+    run("C4", 2, 65536, 100000, 10000, max_batch=1024, p2p=True)
+
+
+def test_p2p_merge_tight_budget_and_small_k():
+    run("C3", 4, 1024, 3000, 80, max_batch=7, p2p=True, steps=5)
+
+
+def test_p2p_self_exchange_world1():
+    """world 1 over the peer-memory path: identical to the plain single-shard step."""
+    from paper_2410_18248_b200 import Scheduler
+    from paper_2410_18248_b200.lamps import LAMPS_XPORT_P2P
+    cfg = gen.lib_config("C3")
+    snap = gen.snapshot("C3", seed=2, id_base=77)
+    a = Scheduler(cfg)
+    b = Scheduler(cfg, transport=LAMPS_XPORT_P2P, flags=32)  # LAMPS_MERGE
+    for s in (a, b):
+        s.import_pool(snap, snap["id_base"], snap["next_id"])
+    for t in range(4):
+        ga, gb = a.step(kv_total=640), b.step(kv_total=640)
+        for k in ("n_eligible", "budget", "budget_used", "n_admitted", "n_preempted", "blocked_head"):
+            assert ga[k] == gb[k], (t, k)
+        assert np.array_equal(ga["admitted_id"], gb["admitted_id"])
+        assert np.array_equal(ga["preempted_id"], gb["preempted_id"])
+    assert b.stats()[0] == 1  # one kernel: exchange and merge inside k_fused
+    a.close(); b.close()
