@@ -48,7 +48,7 @@ struct PhaseS {                  // S, H, T, X
     float ccost[kMaxCtas];       // range-sort cycles per key of each CTA (previous steps)
     uint32_t rb[kMaxCtas + 1], jb[kMaxCtas + 1];  // X: key / bucket boundaries of the ranges
     float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
-    uint32_t jtrim[2];           // X: this CTA's range, non-empty buckets [jtrim[0], jtrim[1])
+    uint32_t jlo[kMaxCtas], jhi[kMaxCtas];  // X: each range's non-empty buckets [jlo, jhi)
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             // end of their bucket) so it can start the admission early; the other CTAs share
             // the rest in proportion to their measured speed (cycles per key of the previous
             // steps' range sorts: some SMs of a B200 run this phase markedly slower), weight
-            // mean/cost capped at 1.15 (keeps a range within 7 keys per thread); below 0.4 the CTA gets no range (G <= 255)
+            // mean/cost capped at 1.15 (keeps a range within 8 keys per thread); below 0.4 the CTA gets no range (G <= 255)
             float* wx = sm.s.wx;  // [G + 1] exclusive weight prefix
             if (warp == 0) {
                 constexpr int kW = kMaxCtas / 32;
@@ -895,6 +895,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                     if (r >= 1 && r < G) {
                         const float rel = cst[u] > 0.f ? __fdividef(mean, cst[u]) : 1.f;
                         w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.15f);
+                        if (a.tune & 1u) w[u] = 1.f;
                     }
                     run += w[u];
                 }
@@ -923,9 +924,34 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                     const uint32_t mid = (lo + hi) >> 1;
                     if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
                 }
+                // boundaries after the head snap to the NEAREST bucket start (a range overshoots
+                // its target by at most half a bucket); the head's end stays >= its target
+                if (tid >= 2 && tid < G && lo > 0 && !(a.tune & 2u)) {
+                    const uint32_t above = lo == NB ? n : sm.s.start[lo], below = sm.s.start[lo - 1];
+                    if (q - below < above - q) lo = lo - 1;
+                }
                 rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
                 jb[tid] = tid == G ? NB : lo;
             }
+        }
+        // trim each range's bucket interval to its non-empty buckets (leading / trailing
+        // empty buckets share the boundary's start): the first bucket is the last one starting
+        // at rb[r], the end is the first bucket starting at rb[r+1].  Keeps the head range and
+        // the ranges next to the starving / non-starving split from spanning thousands of buckets
+        asm volatile("bar.sync 1, %0;" ::"r"(kRW * 32u) : "memory");
+        if (tid < G) {
+            const uint32_t rl = rb[tid], rh = rb[tid + 1];
+            auto first_ge = [&](uint32_t x) {
+                uint32_t lo = 0, hi = NB;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (sm.s.start[mid] >= x) hi = mid; else lo = mid + 1;
+                }
+                return lo;
+            };
+            const uint32_t jh = first_ge(rh);
+            sm.s.jlo[tid] = rl < rh ? first_ge(rl + 1u) - 1u : jh;
+            sm.s.jhi[tid] = jh;
         }
     } else {
         for (uint32_t i = tid - kRW * 32u; i < nk_cta; i += kFT - kRW * 32u) {
@@ -942,28 +968,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     if (tid < G) mx = rb[tid + 1] - rb[tid];
     const bool fallback = (a.flags & kStepForceFallback) ||
                           __syncthreads_or(mx > (uint32_t)kKcap);
-    // trim this range's bucket interval to its non-empty buckets (leading / trailing empty
-    // buckets share the boundary's start): the first bucket is the last one starting at
-    // r_lo, the end is the first bucket starting at r_hi.  Keeps the head range and the
-    // ranges next to the starving / non-starving split from spanning thousands of buckets.
-    if (tid == 0) {
-        const uint32_t rl = rb[bid], rh = rb[bid + 1];
-        auto first_ge = [&](uint32_t x) {
-            uint32_t lo = 0, hi = NB;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (sm.s.start[mid] >= x) hi = mid; else lo = mid + 1;
-            }
-            return lo;
-        };
-        const uint32_t jh = first_ge(rh);
-        const uint32_t jl = rl < rh ? first_ge(rl + 1u) - 1u : jh;
-        sm.s.jtrim[0] = jl;
-        sm.s.jtrim[1] = jh;
-    }
-    __syncthreads();
     const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
-    const uint32_t j_lo = sm.s.jtrim[0], j_hi = sm.s.jtrim[1];
+    const uint32_t j_lo = sm.s.jlo[bid], j_hi = sm.s.jhi[bid];
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
     TRACE(7);
@@ -993,8 +999,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             else if (rn <= 3u * kFT)  // fewer keys per thread: less code on the executed path
                 (void)range_sort<3, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
                                            tr ? tr + 16 : nullptr);
-            else if (rn <= 7u * kFT)
-                (void)range_sort<7, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
+            else if (rn <= 8u * kFT)
+                (void)range_sort<8, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
                                            tr ? tr + 16 : nullptr);
             else
                 (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -94,6 +95,7 @@ struct lamps_s {
     std::vector<void*> peer_open;        // IPC mappings to close
     bool p2p_ready = false;
     uint32_t xseq = 0;
+    uint32_t tune = 0;  // StepArgs.tune, from env LAMPS_TUNE (A/B measurements)
     nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
@@ -363,6 +365,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.flags = (h->cfg.flags & LAMPS_FORCE_FALLBACK) ? kStepForceFallback : 0u;
     a.world = h->world;
     a.rank = h->rank;
+    a.tune = h->tune;
     if (h->merge) a.flags |= kStepMerge;
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
         a.flags |= kStepP2P;
@@ -551,6 +554,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
         delete h;
         return LAMPS_ENOTSUP;
     }
+    if (const char* tv = std::getenv("LAMPS_TUNE")) h->tune = (uint32_t)std::strtoul(tv, nullptr, 0);
     h->world = cfg->world > 1 ? cfg->world : 1;
     h->rank = cfg->world > 1 ? cfg->rank : 0;
     h->merge = merge_mode(*cfg);

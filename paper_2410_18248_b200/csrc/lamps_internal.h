@@ -85,6 +85,9 @@ struct StepArgs {
     uint32_t flags;         // kStepForceFallback, kStepMerge, kStepHeadOnly
     uint32_t world, rank;   // multi-GPU shards
     uint32_t xseq;          // peer-memory exchange: sequence number of this step's exchange
+    uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
+                            // bit 0 uniform key ranges (no speed weights), bit 1 first-boundary
+                            // instead of nearest-boundary snapping
 };
 
 struct Bufs {
