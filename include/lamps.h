@@ -248,6 +248,32 @@ int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_res
 int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev,
                         uint64_t kv_total_blocks, lamps_step_out* out);
 
+/*
+ * lamps_iterate -- one engine iteration in one call: the API returns, then one
+ * scheduling step with the engine's events, then the new arrivals, i.e. exactly
+ *   lamps_api_return(returns); lamps_schedule_step(events); lamps_submit(arrivals)
+ * but with one host synchronisation: every part is validated before any is applied
+ * (on error nothing is applied), the returns and events are applied inside the step
+ * kernel, and the arrivals are enqueued behind the step without waiting (they are
+ * ranked from the next step on).  Arrival ids go to arrival_ids_out (may be NULL).
+ * Errors: those of the three calls; EINVAL if more than 65536 returns.
+ */
+typedef struct {
+    const lamps_event* events;        /* reports on the previous step's batch */
+    uint32_t n_events;
+    uint32_t n_returns;
+    const uint64_t* return_ids;       /* PAUSED requests whose API returned */
+    const uint32_t* return_resp;      /* actual response tokens */
+    const lamps_segment* return_next; /* predictions of their next segment */
+    const lamps_segment* arrivals;    /* new requests, in arrival order */
+    uint32_t n_arrivals;
+    uint32_t reserved;
+    uint64_t* arrival_ids_out;
+    uint64_t kv_total_blocks;
+} lamps_iteration;
+
+int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out);
+
 /* lamps_free -- release the handle (not the caller's workspace). */
 int lamps_free(lamps_t* h);
 

@@ -676,7 +676,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                          : "memory");
         }
     };
-    if (a.n_ev) {  // A0 for the engine's events on this CTA's slots, before they are staged
+    if (a.n_ev | a.n_ret) {  // API returns and A0 for the engine's events on this CTA's slots,
+                             // before they are staged (the two touch disjoint requests)
+        for (uint32_t e = tid; e < a.n_ret; e += kFT) {
+            const ReturnRec R = static_cast<const ReturnRec*>(b.returns)[e];
+            if (R.slot >= s_lo && R.slot < s_hi) apply_return(b.pool, c, R);
+        }
         for (uint32_t e = tid; e < a.n_ev; e += kFT) {
             const DevEvent E = static_cast<const DevEvent*>(b.events)[e];
             const uint32_t s = (uint32_t)E.id & c.cap_mask;

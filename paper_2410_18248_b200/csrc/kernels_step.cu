@@ -136,31 +136,7 @@ __global__ void k_submit(Pool P, Cost c, const SubmitRec* rec, uint32_t n) {
 __global__ void k_api_return(Pool P, Cost c, const ReturnRec* rec, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const ReturnRec r = rec[i];
-    const uint32_t s = r.slot;
-    const uint32_t w = P.sfc[s];
-    const uint64_t ci = P.ctx[s];
-    const uint64_t c1 = ci + r.actual;
-    const uint64_t f1 = t_fwd(c1, c), f0 = t_fwd(ci, c);
-    const uint64_t inc = f1 - f0;  // T_fwd is non-decreasing
-    uint64_t owed;
-    const uint32_t st = sfc_state(w);
-    if (st == ST_PD) {
-        owed = f1;  // discarded: recompute everything
-    } else if (st == ST_PS) {
-        const uint64_t sw = t_swap(ci, c);
-        owed = sw + inc < sw ? ~0ull : sw + inc;  // swap-in + prefill of the response
-    } else {
-        owed = inc;  // preserved: prefill of the response
-    }
-    P.pend[s] = owed > 0xffffffffull ? 0xffffffffu : (uint32_t)owed;
-    P.ctx[s] = (uint32_t)c1;
-    P.pre[s] = r.pre;
-    P.api[s] = r.api;
-    P.resp[s] = r.resp;
-    P.post[s] = r.post;
-    // RAN clear; a new segment: its score is recomputed at the next step (R26)
-    P.sfc[s] = sfc_pack(ST_READY, r.has, sfc_starv(w), sfc_strat(w), sfc_cnt(w)) | (w & SFC_AGE_MASK) | SFC_DIRTY;
+    apply_return(P, c, rec[i]);
 }
 
 __global__ void k_gather_u32(const uint32_t* src, const uint32_t* slots, uint32_t* out, uint32_t n) {

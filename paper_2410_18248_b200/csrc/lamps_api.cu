@@ -96,6 +96,7 @@ struct lamps_s {
     bool p2p_ready = false;
     uint32_t xseq = 0;
     uint32_t tune = 0;  // StepArgs.tune, from env LAMPS_TUNE (A/B measurements)
+    uint32_t ret_pending = 0;  // API returns staged for the next fused step's prologue
     nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
@@ -252,6 +253,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.pre_id = reinterpret_cast<uint64_t*>(base + o_pre);
     h->b.events = base + o_ev;
     h->d_ingest = base + o_ing;
+    h->b.returns = h->d_ingest;
     h->d_gather = reinterpret_cast<uint32_t*>(base + o_gat);
     h->b.dbg = (h->cfg.flags & LAMPS_DEBUG_OUT) ? reinterpret_cast<unsigned long long*>(base + o_dbg)
                                                   : nullptr;
@@ -366,6 +368,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.world = h->world;
     a.rank = h->rank;
     a.tune = h->tune;
+    a.n_ret = h->fused ? h->ret_pending : 0u;
     if (h->merge) a.flags |= kStepMerge;
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
         a.flags |= kStepP2P;
@@ -403,6 +406,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         CU(h, launch_admit(h->b, h->cost, a, h->stream));
     }
     h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);  // P2P: the exchange and merge are in k_fused
+    h->ret_pending = 0;
     return LAMPS_OK;
 }
 
@@ -504,6 +508,172 @@ int staging_copied(lamps_t* h) {
     CU(h, cudaEventRecord(h->ing_ev, h->stream));
     h->ing_pending = true;
     return LAMPS_OK;
+}
+
+// ---- validation and staging shared by the single calls and lamps_iterate ----------
+
+// submit: the segments (pure checks; ticks out)
+int check_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, std::vector<uint32_t>& ticks) {
+    if (n && !segs) return fail(h, LAMPS_EINVAL, "segs is NULL");
+    ticks.assign(n, 0u);
+    for (uint32_t k = 0; k < n; k++) {
+        if (const char* m = check_segment(h, segs[k].prompt_len, segs[k], &ticks[k]))
+            return fail(h, LAMPS_EINVAL, std::string("submit[") + std::to_string(k) + "]: " + m);
+    }
+    return LAMPS_OK;
+}
+
+// submit: the id window and free slots, counting the slots in freed[0..nf) (sorted) as free
+int window_submit(lamps_t* h, uint32_t n, const uint32_t* freed, uint32_t nf) {
+    auto is_free = [&](uint32_t sl) {
+        return h->hstate[sl] == H_FREE || (nf && std::binary_search(freed, freed + nf, sl));
+    };
+    uint64_t base = h->id_base;
+    while (nf && base < h->next_id && is_free((uint32_t)(base & h->cost.cap_mask))) base++;
+    if (h->next_id + n - base > h->cap) return fail(h, LAMPS_ENOSPC, "pool full (id window)");
+    for (uint32_t k = 0; k < n; k++)
+        if (!is_free((uint32_t)((h->next_id + k) & h->cost.cap_mask)))
+            return fail(h, LAMPS_ENOSPC, "pool full (slot occupied)");
+    return LAMPS_OK;
+}
+
+int do_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, const std::vector<uint32_t>& ticks,
+              uint64_t* ids_out) {
+    SubmitRec* rec = static_cast<SubmitRec*>(h->h_ingest);
+    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
+        const uint32_t m = std::min(kIngestChunk, n - k0);
+        if (int rc = staging_wait(h)) return rc;
+        for (uint32_t i = 0; i < m; i++) {
+            const lamps_segment& s = segs[k0 + i];
+            SubmitRec& r = rec[i];
+            r.slot = (uint32_t)((h->next_id + k0 + i) & h->cost.cap_mask);
+            r.ctx = s.prompt_len;
+            r.pre = s.pre_len;
+            r.has = s.has_api;
+            r.api = s.has_api ? ticks[k0 + i] : 0u;
+            r.resp = s.has_api ? s.resp_len : 0u;
+            r.post = s.has_api ? s.post_len : 0u;
+            r.pad = 0;
+        }
+        CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(SubmitRec), cudaMemcpyHostToDevice, h->stream));
+        if (int rc = staging_copied(h)) return rc;
+        CU(h, launch_submit(h->b.pool, h->cost, static_cast<const SubmitRec*>(h->d_ingest), m, h->stream));
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        h->hstate[(h->next_id + k) & h->cost.cap_mask] = H_READY;
+        h->hctx[(h->next_id + k) & h->cost.cap_mask] = segs[k].prompt_len;
+        if (ids_out) ids_out[k] = h->next_id + k;
+    }
+    h->next_id += n;
+    return LAMPS_OK;
+}
+
+// API returns: ids PAUSED, distinct, segments valid against the context shadow
+int check_returns(lamps_t* h, const uint64_t* ids, const uint32_t* actual, const lamps_segment* next, uint32_t n,
+                  std::vector<uint32_t>& ticks, std::vector<uint32_t>& ctx) {
+    if (n && (!ids || !actual || !next)) return fail(h, LAMPS_EINVAL, "NULL argument");
+    for (uint32_t k = 0; k < n; k++) {
+        if (!id_live(h, ids[k]) || h->hstate[ids[k] & h->cost.cap_mask] != H_PAUSED)
+            return fail(h, LAMPS_ENOENT, "api_return: id unknown or not paused");
+    }
+    {
+        std::vector<uint64_t> s(ids, ids + n);
+        std::sort(s.begin(), s.end());
+        if (std::adjacent_find(s.begin(), s.end()) != s.end())
+            return fail(h, LAMPS_EINVAL, "api_return: duplicate id");
+    }
+    ticks.assign(n, 0u);
+    ctx.assign(n, 0u);
+    if (!h->shadow_ok) {
+        const int rc = resync_shadow(h);
+        if (rc) return rc;
+    }
+    for (uint32_t k = 0; k < n; k++) ctx[k] = h->hctx[ids[k] & h->cost.cap_mask];
+    for (uint32_t k = 0; k < n; k++) {
+        if (const char* m = check_segment(h, (uint64_t)ctx[k] + actual[k], next[k], &ticks[k]))
+            return fail(h, LAMPS_EINVAL, std::string("api_return[") + std::to_string(k) + "]: " + m);
+    }
+    return LAMPS_OK;
+}
+
+// API returns: staged to the device; applied by k_api_return now, or (prologue, one
+// chunk) by the next fused step kernel before it scores
+int do_returns(lamps_t* h, const uint64_t* ids, const uint32_t* actual, const lamps_segment* next, uint32_t n,
+               const std::vector<uint32_t>& ticks, const std::vector<uint32_t>& ctx, bool prologue) {
+    ReturnRec* rec = static_cast<ReturnRec*>(h->h_ingest);
+    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
+        const uint32_t m = std::min(kIngestChunk, n - k0);
+        if (int rc = staging_wait(h)) return rc;
+        for (uint32_t i = 0; i < m; i++) {
+            const lamps_segment& s = next[k0 + i];
+            ReturnRec& r = rec[i];
+            r.slot = (uint32_t)(ids[k0 + i] & h->cost.cap_mask);
+            r.actual = actual[k0 + i];
+            r.pre = s.pre_len;
+            r.has = s.has_api;
+            r.api = s.has_api ? ticks[k0 + i] : 0u;
+            r.resp = s.has_api ? s.resp_len : 0u;
+            r.post = s.has_api ? s.post_len : 0u;
+            r.pad = 0;
+        }
+        CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(ReturnRec), cudaMemcpyHostToDevice, h->stream));
+        if (int rc = staging_copied(h)) return rc;
+        if (prologue)
+            h->ret_pending = m;  // the caller guarantees n <= kIngestChunk
+        else
+            CU(h, launch_api_return(h->b.pool, h->cost, static_cast<const ReturnRec*>(h->d_ingest), m, h->stream));
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        h->hstate[ids[k] & h->cost.cap_mask] = H_READY;
+        h->hctx[ids[k] & h->cost.cap_mask] = ctx[k] + actual[k];
+    }
+    return LAMPS_OK;
+}
+
+// events: valid against the previous admitted list (pure checks)
+int check_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks) {
+    if (n_ev && !ev) return fail(h, LAMPS_EINVAL, "events is NULL");
+    if (kv_total_blocks > h->cfg.kv_capacity_blocks)
+        return fail(h, LAMPS_EINVAL, "kv_total_blocks exceeds kv_capacity_blocks");
+    if (n_ev) {
+        if (!h->prev_known) {  // previous step ran async: fetch its admitted list
+            int rc = fetch_result(h, nullptr);
+            if (rc) return rc;
+        }
+        if (n_ev > h->prev_adm.size()) return fail(h, LAMPS_EINVAL, "more events than admitted requests");
+        // O(n_ev): a valid event names a live id whose slot the previous step admitted,
+        // at most once (per-slot marks; the live id of a slot is unique)
+        const uint32_t tag = ++h->ev_tag;
+        for (uint32_t e = 0; e < n_ev; e++) {
+            if (ev[e].kind != LAMPS_EV_API_CALL && ev[e].kind != LAMPS_EV_FINISHED)
+                return fail(h, LAMPS_EINVAL, "unknown event kind");
+            const uint32_t sl = (uint32_t)(ev[e].id & h->cost.cap_mask);
+            if (!id_live(h, ev[e].id) || h->adm_mark[sl] != h->step || h->fetched_step != h->step)
+                return fail(h, LAMPS_EINVAL, "event for a request not admitted by the previous step");
+            if (h->ev_mark[sl] == tag) return fail(h, LAMPS_EINVAL, "duplicate event id");
+            h->ev_mark[sl] = tag;
+        }
+    }
+    return LAMPS_OK;
+}
+
+// events: staged to the device, liveness shadow updated
+int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
+    if (!n_ev) return LAMPS_OK;
+    std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
+    CU(h, cudaMemcpyAsync(const_cast<void*>(h->b.events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
+                          cudaMemcpyHostToDevice, h->stream));
+    for (uint32_t e = 0; e < n_ev; e++)
+        h->hstate[ev[e].id & h->cost.cap_mask] = ev[e].kind == LAMPS_EV_FINISHED ? H_FREE : H_PAUSED;
+    advance_id_base(h);
+    return LAMPS_OK;
+}
+
+// host-side part of a step: validate the events against the previous admitted
+// list, stage them to the device, update the liveness shadow (state unchanged on error)
+int prepare_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks) {
+    if (int rc = check_events(h, ev, n_ev, kv_total_blocks)) return rc;
+    return stage_events(h, ev, n_ev);
 }
 
 }  // namespace
@@ -658,43 +828,10 @@ int lamps_free(lamps_t* h) {
 
 int lamps_submit(lamps_t* h, const lamps_segment* segs, uint32_t n, uint64_t* ids_out) {
     if (!h) return LAMPS_EINVAL;
-    if (n && !segs) return fail(h, LAMPS_EINVAL, "segs is NULL");
-    std::vector<uint32_t> ticks(n);
-    for (uint32_t k = 0; k < n; k++) {
-        if (const char* m = check_segment(h, segs[k].prompt_len, segs[k], &ticks[k]))
-            return fail(h, LAMPS_EINVAL, std::string("submit[") + std::to_string(k) + "]: " + m);
-    }
-    if (h->next_id + n - h->id_base > h->cap) return fail(h, LAMPS_ENOSPC, "pool full (id window)");
-    for (uint32_t k = 0; k < n; k++)
-        if (h->hstate[(h->next_id + k) & h->cost.cap_mask] != H_FREE)
-            return fail(h, LAMPS_ENOSPC, "pool full (slot occupied)");
-    SubmitRec* rec = static_cast<SubmitRec*>(h->h_ingest);
-    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
-        const uint32_t m = std::min(kIngestChunk, n - k0);
-        if (int rc = staging_wait(h)) return rc;
-        for (uint32_t i = 0; i < m; i++) {
-            const lamps_segment& s = segs[k0 + i];
-            SubmitRec& r = rec[i];
-            r.slot = (uint32_t)((h->next_id + k0 + i) & h->cost.cap_mask);
-            r.ctx = s.prompt_len;
-            r.pre = s.pre_len;
-            r.has = s.has_api;
-            r.api = s.has_api ? ticks[k0 + i] : 0u;
-            r.resp = s.has_api ? s.resp_len : 0u;
-            r.post = s.has_api ? s.post_len : 0u;
-            r.pad = 0;
-        }
-        CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(SubmitRec), cudaMemcpyHostToDevice, h->stream));
-        if (int rc = staging_copied(h)) return rc;
-        CU(h, launch_submit(h->b.pool, h->cost, static_cast<const SubmitRec*>(h->d_ingest), m, h->stream));
-    }
-    for (uint32_t k = 0; k < n; k++) {
-        h->hstate[(h->next_id + k) & h->cost.cap_mask] = H_READY;
-        h->hctx[(h->next_id + k) & h->cost.cap_mask] = segs[k].prompt_len;
-        if (ids_out) ids_out[k] = h->next_id + k;
-    }
-    h->next_id += n;
-    return LAMPS_OK;
+    std::vector<uint32_t> ticks;
+    if (int rc = check_submit(h, segs, n, ticks)) return rc;
+    if (int rc = window_submit(h, n, nullptr, 0)) return rc;
+    return do_submit(h, segs, n, ticks, ids_out);
 }
 
 int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_noise* noise,
@@ -749,87 +886,9 @@ int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_
 int lamps_api_return(lamps_t* h, const uint64_t* ids, const uint32_t* actual_resp_len,
                      const lamps_segment* next, uint32_t n) {
     if (!h) return LAMPS_EINVAL;
-    if (n && (!ids || !actual_resp_len || !next)) return fail(h, LAMPS_EINVAL, "NULL argument");
-    for (uint32_t k = 0; k < n; k++) {
-        if (!id_live(h, ids[k]) || h->hstate[ids[k] & h->cost.cap_mask] != H_PAUSED)
-            return fail(h, LAMPS_ENOENT, "api_return: id unknown or not paused");
-    }
-    {
-        std::vector<uint64_t> s(ids, ids + n);
-        std::sort(s.begin(), s.end());
-        if (std::adjacent_find(s.begin(), s.end()) != s.end())
-            return fail(h, LAMPS_EINVAL, "api_return: duplicate id");
-    }
-    std::vector<uint32_t> ticks(n), ctx(n);
-    // current context of each request, from the host shadow
-    if (!h->shadow_ok) {
-        const int rc = resync_shadow(h);
-        if (rc) return rc;
-    }
-    for (uint32_t k = 0; k < n; k++) ctx[k] = h->hctx[ids[k] & h->cost.cap_mask];
-    for (uint32_t k = 0; k < n; k++) {
-        if (const char* m = check_segment(h, (uint64_t)ctx[k] + actual_resp_len[k], next[k], &ticks[k]))
-            return fail(h, LAMPS_EINVAL, std::string("api_return[") + std::to_string(k) + "]: " + m);
-    }
-    ReturnRec* rec = static_cast<ReturnRec*>(h->h_ingest);
-    for (uint32_t k0 = 0; k0 < n; k0 += kIngestChunk) {
-        const uint32_t m = std::min(kIngestChunk, n - k0);
-        if (int rc = staging_wait(h)) return rc;
-        for (uint32_t i = 0; i < m; i++) {
-            const lamps_segment& s = next[k0 + i];
-            ReturnRec& r = rec[i];
-            r.slot = (uint32_t)(ids[k0 + i] & h->cost.cap_mask);
-            r.actual = actual_resp_len[k0 + i];
-            r.pre = s.pre_len;
-            r.has = s.has_api;
-            r.api = s.has_api ? ticks[k0 + i] : 0u;
-            r.resp = s.has_api ? s.resp_len : 0u;
-            r.post = s.has_api ? s.post_len : 0u;
-            r.pad = 0;
-        }
-        CU(h, cudaMemcpyAsync(h->d_ingest, rec, (size_t)m * sizeof(ReturnRec), cudaMemcpyHostToDevice, h->stream));
-        if (int rc = staging_copied(h)) return rc;
-        CU(h, launch_api_return(h->b.pool, h->cost, static_cast<const ReturnRec*>(h->d_ingest), m, h->stream));
-    }
-    for (uint32_t k = 0; k < n; k++) {
-        h->hstate[ids[k] & h->cost.cap_mask] = H_READY;
-        h->hctx[ids[k] & h->cost.cap_mask] = ctx[k] + actual_resp_len[k];
-    }
-    return LAMPS_OK;
-}
-
-// host-side part of a step: validate the events against the previous admitted
-// list, stage them to the device, update the liveness shadow (state unchanged on error)
-int prepare_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks) {
-    if (n_ev && !ev) return fail(h, LAMPS_EINVAL, "events is NULL");
-    if (kv_total_blocks > h->cfg.kv_capacity_blocks)
-        return fail(h, LAMPS_EINVAL, "kv_total_blocks exceeds kv_capacity_blocks");
-    if (n_ev) {
-        if (!h->prev_known) {  // previous step ran async: fetch its admitted list
-            int rc = fetch_result(h, nullptr);
-            if (rc) return rc;
-        }
-        if (n_ev > h->prev_adm.size()) return fail(h, LAMPS_EINVAL, "more events than admitted requests");
-        // O(n_ev): a valid event names a live id whose slot the previous step admitted,
-        // at most once (per-slot marks; the live id of a slot is unique)
-        const uint32_t tag = ++h->ev_tag;
-        for (uint32_t e = 0; e < n_ev; e++) {
-            if (ev[e].kind != LAMPS_EV_API_CALL && ev[e].kind != LAMPS_EV_FINISHED)
-                return fail(h, LAMPS_EINVAL, "unknown event kind");
-            const uint32_t sl = (uint32_t)(ev[e].id & h->cost.cap_mask);
-            if (!id_live(h, ev[e].id) || h->adm_mark[sl] != h->step || h->fetched_step != h->step)
-                return fail(h, LAMPS_EINVAL, "event for a request not admitted by the previous step");
-            if (h->ev_mark[sl] == tag) return fail(h, LAMPS_EINVAL, "duplicate event id");
-            h->ev_mark[sl] = tag;
-        }
-        std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
-        CU(h, cudaMemcpyAsync(const_cast<void*>(h->b.events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
-                              cudaMemcpyHostToDevice, h->stream));
-        for (uint32_t e = 0; e < n_ev; e++)
-            h->hstate[ev[e].id & h->cost.cap_mask] = ev[e].kind == LAMPS_EV_FINISHED ? H_FREE : H_PAUSED;
-        advance_id_base(h);
-    }
-    return LAMPS_OK;
+    std::vector<uint32_t> ticks, ctx;
+    if (int rc = check_returns(h, ids, actual_resp_len, next, n, ticks, ctx)) return rc;
+    return do_returns(h, ids, actual_resp_len, next, n, ticks, ctx, false);
 }
 
 int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks,
@@ -840,6 +899,33 @@ int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64
     rc = enqueue_step(h, kv_total_blocks, n_ev);
     if (rc) return rc;
     return fetch_result(h, out);
+}
+
+int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
+    if (!h || !it) return LAMPS_EINVAL;
+    if (h->world > 1 && h->cfg.transport == LAMPS_XPORT_LOOPBACK)
+        return fail(h, LAMPS_EINVAL, "loopback shards step together: use lamps_group_step");
+    const uint32_t nr = it->n_returns, ne = it->n_events, na = it->n_arrivals;
+    if (h->fused && nr > kIngestChunk) return fail(h, LAMPS_EINVAL, "more than 65536 API returns in one iteration");
+    // 1. everything is validated before anything is applied
+    std::vector<uint32_t> rticks, rctx, aticks;
+    if (int rc = check_returns(h, it->return_ids, it->return_resp, it->return_next, nr, rticks, rctx)) return rc;
+    if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
+    if (int rc = check_submit(h, it->arrivals, na, aticks)) return rc;
+    {   // the arrivals' slots, counting the slots this iteration's FINISHED events free
+        std::vector<uint32_t> freed;
+        for (uint32_t e = 0; e < ne; e++)
+            if (it->events[e].kind == LAMPS_EV_FINISHED) freed.push_back((uint32_t)(it->events[e].id & h->cost.cap_mask));
+        std::sort(freed.begin(), freed.end());
+        if (int rc = window_submit(h, na, freed.data(), (uint32_t)freed.size())) return rc;
+    }
+    // 2. API returns (in the fused kernel's prologue), events, the step, its result
+    if (int rc = do_returns(h, it->return_ids, it->return_resp, it->return_next, nr, rticks, rctx, h->fused)) return rc;
+    if (int rc = stage_events(h, it->events, ne)) return rc;
+    if (int rc = enqueue_step(h, it->kv_total_blocks, ne)) return rc;
+    if (int rc = fetch_result(h, out)) return rc;
+    // 3. arrivals, enqueued behind the step (no wait): they are ranked from the next step on
+    return do_submit(h, it->arrivals, na, aticks, it->arrival_ids_out);
 }
 
 int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* const* ev, const uint32_t* n_ev,

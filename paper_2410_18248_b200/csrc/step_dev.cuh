@@ -31,6 +31,36 @@ __device__ __forceinline__ void apply_event(const Pool& P, const Cost& c, const 
     P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u) | (w & SFC_META);
 }
 
+// API return of one PAUSED request (Alg.1, R10): ctx grows by the actual
+// response; the owed prefill / swap-in by its handling strategy; the next segment's
+// predictions; READY (K_api_return, or the fused kernel's prologue).
+__device__ __forceinline__ void apply_return(const Pool& P, const Cost& c, const ReturnRec r) {
+    const uint32_t s = r.slot;
+    const uint32_t w = P.sfc[s];
+    const uint64_t ci = P.ctx[s];
+    const uint64_t c1 = ci + r.actual;
+    const uint64_t f1 = t_fwd(c1, c), f0 = t_fwd(ci, c);
+    const uint64_t inc = f1 - f0;  // T_fwd is non-decreasing
+    uint64_t owed;
+    const uint32_t st = sfc_state(w);
+    if (st == ST_PD) {
+        owed = f1;  // discarded: recompute everything
+    } else if (st == ST_PS) {
+        const uint64_t sw = t_swap(ci, c);
+        owed = sw + inc < sw ? ~0ull : sw + inc;  // swap-in + prefill of the response
+    } else {
+        owed = inc;  // preserved: prefill of the response
+    }
+    P.pend[s] = owed > 0xffffffffull ? 0xffffffffu : (uint32_t)owed;
+    P.ctx[s] = (uint32_t)c1;
+    P.pre[s] = r.pre;
+    P.api[s] = r.api;
+    P.resp[s] = r.resp;
+    P.post[s] = r.post;
+    // RAN clear; a new segment: its score is recomputed at the next step (R26)
+    P.sfc[s] = sfc_pack(ST_READY, r.has, sfc_starv(w), sfc_strat(w), sfc_cnt(w)) | (w & SFC_AGE_MASK) | SFC_DIRTY;
+}
+
 // block-wide exclusive scans (all NT threads call; totals in *tot)
 template <int NT>
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh_warp, uint32_t* tot) {

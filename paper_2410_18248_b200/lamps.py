@@ -70,6 +70,12 @@ TRUTH_DTYPE = np.dtype([("key", np.uint64), ("prompt_len", np.uint32), ("pre_len
 LAMPS_NO_BIN = 0xFFFFFFFF
 
 
+class lamps_iteration(ctypes.Structure):
+    _fields_ = [("events", vp), ("n_events", u32), ("n_returns", u32), ("return_ids", vp),
+                ("return_resp", vp), ("return_next", vp), ("arrivals", vp), ("n_arrivals", u32),
+                ("reserved", u32), ("arrival_ids_out", vp), ("kv_total_blocks", u64)]
+
+
 class lamps_noise(ctypes.Structure):
     _fields_ = [("seed", u64), ("len_error_ppm", u32), ("api_error_ppm", u32)]
 
@@ -110,6 +116,7 @@ def lib() -> ctypes.CDLL:
             "lamps_version": (u32, []),
             "lamps_predict": (c_int, [vp, vp, u32, P(lamps_noise), vp]),
             "lamps_p2p_handle": (c_int, [vp, vp]),
+            "lamps_iterate": (c_int, [vp, P(lamps_iteration), P(lamps_step_out)]),
             "lamps_p2p_connect": (c_int, [vp, vp, ctypes.c_size_t]),
             "lamps_p2p_connect_local": (c_int, [vp, u32]),
         }
@@ -282,6 +289,36 @@ class Scheduler:
     def step(self, events=None, kv_total: int = 0) -> dict:
         self._check(self.step_rc(events, kv_total))
         return self._result(self._out)
+
+    def iterate_rc(self, events=None, ret_ids=None, ret_resp=None, ret_next=None, arrivals=None,
+                   kv_total: int = 0):
+        """lamps_iterate: API returns, one step with the events, arrivals -- one sync.
+        Returns (rc, result dict or None, arrival ids)."""
+        it = lamps_iteration()
+        keep = []
+        if events is not None and len(events):
+            ev = np.ascontiguousarray(events, EVENT_DTYPE); keep.append(ev)
+            it.events, it.n_events = _p(ev), len(ev)
+        if ret_ids is not None and len(ret_ids):
+            ri = np.ascontiguousarray(ret_ids, np.uint64)
+            rr = np.ascontiguousarray(ret_resp, np.uint32)
+            rn = np.ascontiguousarray(ret_next, SEGMENT_DTYPE)
+            keep += [ri, rr, rn]
+            it.return_ids, it.return_resp, it.return_next, it.n_returns = _p(ri), _p(rr), _p(rn), len(ri)
+        ids = np.zeros(0, np.uint64)
+        if arrivals is not None and len(arrivals):
+            ar = np.ascontiguousarray(arrivals, SEGMENT_DTYPE)
+            ids = np.zeros(len(ar), np.uint64)
+            keep += [ar, ids]
+            it.arrivals, it.n_arrivals, it.arrival_ids_out = _p(ar), len(ar), _p(ids)
+        it.kv_total_blocks = int(kv_total)
+        rc = lib().lamps_iterate(self.h, ctypes.byref(it), ctypes.byref(self._out))
+        return rc, (self._result(self._out) if rc == LAMPS_OK else None), ids
+
+    def iterate(self, events=None, ret_ids=None, ret_resp=None, ret_next=None, arrivals=None, kv_total: int = 0):
+        rc, out, ids = self.iterate_rc(events, ret_ids, ret_resp, ret_next, arrivals, kv_total)
+        self._check(rc)
+        return out, ids
 
     def step_async(self, kv_total: int):
         self._check(lib().lamps_schedule_step_async(self.h, int(kv_total)))
