@@ -48,7 +48,6 @@ struct PhaseS {                  // S, H, T, X
     float ccost[kMaxCtas];       // range-sort cycles per key of each CTA (previous steps)
     uint32_t rb[kMaxCtas + 1], jb[kMaxCtas + 1];  // X: key / bucket boundaries of the ranges
     float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
-    uint32_t jlo[kMaxCtas], jhi[kMaxCtas];  // X: each range's non-empty buckets [jlo, jhi)
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -623,7 +622,9 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
         if (b.trace && threadIdx.x == 0) b.trace[blockIdx.x * kTraceSlots + (k)] = clock64(); \
     } while (0)
 
-template <bool DBG>
+// P2P: the peer-memory exchange + in-kernel merge instance (its code and shared-memory
+// tail are left out of the plain instance)
+template <bool DBG, bool P2P>
 __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     // the CTAs' measured range-sort costs (previous steps) -> shared memory by cp.async, so
     // the L2 latency hides behind the score phase; they weight the key ranges (X)
     SmemTail& tail = *reinterpret_cast<SmemTail*>(smem_raw + sizeof(FusedSmem));
-    if ((a.flags & kStepP2P) && tid < a.world) {  // the peers' exchange buffers
+    if (P2P && tid < a.world) {  // the peers' exchange buffers
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tail.xp[tid]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;" ::"r"(dst),
                      "l"(b.xpeers + tid) : "memory");
@@ -874,7 +875,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             // end of their bucket) so it can start the admission early; the other CTAs share
             // the rest in proportion to their measured speed (cycles per key of the previous
             // steps' range sorts: some SMs of a B200 run this phase markedly slower), weight
-            // mean/cost capped at 1.15 (keeps a range within 8 keys per thread); below 0.4 the CTA gets no range (G <= 255)
+            // mean/cost capped at 1.25; below 0.4 the CTA gets no range (G <= 255)
             float* wx = sm.s.wx;  // [G + 1] exclusive weight prefix
             if (warp == 0) {
                 constexpr int kW = kMaxCtas / 32;
@@ -899,7 +900,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                     w[u] = 0.f;
                     if (r >= 1 && r < G) {
                         const float rel = cst[u] > 0.f ? __fdividef(mean, cst[u]) : 1.f;
-                        w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.15f);
+                        w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.25f);
                         if (a.tune & 1u) w[u] = 1.f;
                     }
                     run += w[u];
@@ -929,34 +930,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                     const uint32_t mid = (lo + hi) >> 1;
                     if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
                 }
-                // boundaries after the head snap to the NEAREST bucket start (a range overshoots
-                // its target by at most half a bucket); the head's end stays >= its target
-                if (tid >= 2 && tid < G && lo > 0 && !(a.tune & 2u)) {
+                // (LAMPS_TUNE bit 1) boundaries after the head snap to the NEAREST bucket start;
+                // default: the first bucket start >= the target; the head's end stays >= its target
+                if (tid >= 2 && tid < G && lo > 0 && (a.tune & 2u)) {
                     const uint32_t above = lo == NB ? n : sm.s.start[lo], below = sm.s.start[lo - 1];
                     if (q - below < above - q) lo = lo - 1;
                 }
                 rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
                 jb[tid] = tid == G ? NB : lo;
             }
-        }
-        // trim each range's bucket interval to its non-empty buckets (leading / trailing
-        // empty buckets share the boundary's start): the first bucket is the last one starting
-        // at rb[r], the end is the first bucket starting at rb[r+1].  Keeps the head range and
-        // the ranges next to the starving / non-starving split from spanning thousands of buckets
-        asm volatile("bar.sync 1, %0;" ::"r"(kRW * 32u) : "memory");
-        if (tid < G) {
-            const uint32_t rl = rb[tid], rh = rb[tid + 1];
-            auto first_ge = [&](uint32_t x) {
-                uint32_t lo = 0, hi = NB;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (sm.s.start[mid] >= x) hi = mid; else lo = mid + 1;
-                }
-                return lo;
-            };
-            const uint32_t jh = first_ge(rh);
-            sm.s.jlo[tid] = rl < rh ? first_ge(rl + 1u) - 1u : jh;
-            sm.s.jhi[tid] = jh;
         }
     } else {
         for (uint32_t i = tid - kRW * 32u; i < nk_cta; i += kFT - kRW * 32u) {
@@ -974,7 +956,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     const bool fallback = (a.flags & kStepForceFallback) ||
                           __syncthreads_or(mx > (uint32_t)kKcap);
     const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
-    const uint32_t j_lo = sm.s.jlo[bid], j_hi = sm.s.jhi[bid];
+    const uint32_t j_lo = jb[bid], j_hi = jb[bid + 1];
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
     TRACE(7);
@@ -1004,8 +986,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             else if (rn <= 3u * kFT)  // fewer keys per thread: less code on the executed path
                 (void)range_sort<3, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
                                            tr ? tr + 16 : nullptr);
-            else if (rn <= 8u * kFT)
-                (void)range_sort<8, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
+            else if (rn <= 7u * kFT)
+                (void)range_sort<7, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
                                            tr ? tr + 16 : nullptr);
             else
                 (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
@@ -1095,7 +1077,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
         const uint32_t K = a.max_batch, nv = min(n, K);
         const uint64_t idmask = (1ull << c.IB) - 1ull;
-        const bool p2p = (a.flags & kStepP2P) != 0;
+        constexpr bool p2p = P2P;
         const uint32_t W = a.world, par = a.xseq & 1u;
         // peer-memory transport: record i of this rank goes to every peer's receive area
         // [par][rank] by NVLink stores (the one-shot all-gather), then flags, then the merge
@@ -1196,9 +1178,11 @@ size_t fused_smem_bytes() { return sizeof(FusedSmem); }  // the union (in-kernel
 
 int fused_blocks_per_sm() {
     int nb = 0;
-    cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmemBytes);
-    cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmemBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused<false>, kFT, kFusedSmemBytes);
+    cudaFuncSetAttribute(k_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
+    cudaFuncSetAttribute(k_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
+    cudaFuncSetAttribute(k_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmemBytes);
+    cudaFuncSetAttribute(k_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused<false, true>, kFT, kFusedSmemBytes);
     return nb;
 }
 
@@ -1209,8 +1193,10 @@ cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32
     Cost cc = c;
     StepArgs aa = a;
     void* args[] = {&bb, &cc, &aa};
-    const void* fn = b.dbg ? (const void*)k_fused<true> : (const void*)k_fused<false>;
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFT), args, kFusedSmemBytes, s);
+    const bool p2p = (a.flags & kStepP2P) != 0;
+    const void* fn = p2p ? (b.dbg ? (const void*)k_fused<true, true> : (const void*)k_fused<false, true>)
+                         : (b.dbg ? (const void*)k_fused<true, false> : (const void*)k_fused<false, false>);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFT), args, p2p ? kFusedSmemBytes : sizeof(FusedSmem), s);
 }
 
 }  // namespace lamps

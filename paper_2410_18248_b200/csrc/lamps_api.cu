@@ -742,6 +742,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     c.T = cfg->starvation_threshold;
     c.SB = cfg->score_bits; c.IB = cfg->id_bits;
     c.score_max = (cfg->score_bits >= 64) ? ~0ull : ((1ull << cfg->score_bits) - 1ull);
+    c.nsbit = 1ull << (cfg->score_bits + cfg->id_bits);  // <= 2^63 (SB + IB + 1 <= 64)
     c.cap = cfg->capacity; c.cap_mask = cfg->capacity - 1u;
     c.fast = fast_bounds_ok(*cfg) ? 1u : 0u;
     c.policy = cfg->policy;

@@ -44,6 +44,7 @@ constexpr uint32_t POL_LAMPS = 0, POL_FCFS = 1, POL_SJF = 2, POL_SJF_TOTAL = 3;
 struct Cost {
     uint64_t tau, A1, A2, S0, S1, c_other;
     uint64_t score_max;  // 2^SB - 1
+    uint64_t nsbit;      // 1 << (SB + IB): the key's "not starving" bit
     uint32_t SH, lgB, B, T;
     uint32_t SB, IB, cap_mask, cap;
     uint32_t fast;       // constants satisfy the 64-bit fast-path bounds (host-checked)

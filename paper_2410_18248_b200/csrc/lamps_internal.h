@@ -87,8 +87,8 @@ struct StepArgs {
     uint32_t xseq;          // peer-memory exchange: sequence number of this step's exchange
     uint32_t n_ret;         // fused path: API returns staged at Bufs::returns, applied in the prologue
     uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
-                            // bit 0 uniform key ranges (no speed weights), bit 1 first-boundary
-                            // instead of nearest-boundary snapping
+                            // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
+                            // instead of first-boundary snapping of the range ends
 };
 
 struct Bufs {

@@ -209,8 +209,11 @@ __device__ __forceinline__ uint32_t strategy_score(const Pool& P, const Cost& c,
     }
     const uint32_t has = sfc_has(w);
     uint32_t strat;
-    const uint64_t span = (uint64_t)ctx + pre + (has ? (uint64_t)resp + post : 0ull);
-    if (c.fast && span < kFastCtxLimit) {
+    // fast path iff the slot's lengths sum below 2^20; checked in 32 bits: all four below
+    // 2^18 (so the sum cannot wrap) and the sum below 2^20 (a rarer slot with one length in
+    // [2^18, 2^20) takes the exact path, which gives the same result)
+    const uint32_t rp = has ? resp : 0u, pp = has ? post : 0u;
+    if (c.fast && (ctx | pre | rp | pp) < (1u << 18) && ctx + pre + rp + pp < (uint32_t)kFastCtxLimit) {
         strat = strategy_score_fast(ctx, pre, api, resp, post, pend, has, c, &sc, &wp, &wd, &ws);
     } else {
         wp = wd = ws = 0;
@@ -316,7 +319,7 @@ __device__ __forceinline__ bool score_slot(const Pool& P, const Cost& c, uint32_
     const uint32_t cnt = sfc_cnt(w);
     const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
     w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u) | meta;
-    key = ((uint64_t)(starv ^ 1u) << (c.SB + c.IB)) | (sc << c.IB) | ((slot - id_base_mod) & c.cap_mask);
+    key = (starv ? 0ull : c.nsbit) | (sc << c.IB) | ((slot - id_base_mod) & c.cap_mask);
     if (DBG) {
         unsigned long long* d = dbg + 4ull * slot;
         d[0] = wp; d[1] = wd; d[2] = ws; d[3] = sc;

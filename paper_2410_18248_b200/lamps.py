@@ -91,8 +91,8 @@ def lib() -> ctypes.CDLL:
     """Load liblamps.so (building it first if it is missing or stale)."""
     global _L
     if _L is None:
-        path = _build.LIB
-        if not os.path.exists(path) or _build.stale():
+        path = os.environ.get("LAMPS_LIB") or _build.LIB  # LAMPS_LIB: another build (A/B runs)
+        if path == _build.LIB and (not os.path.exists(path) or _build.stale()):
             _build.build()
         L = ctypes.CDLL(path)
         c_int, P = ctypes.c_int, ctypes.POINTER
@@ -121,6 +121,8 @@ def lib() -> ctypes.CDLL:
             "lamps_p2p_connect_local": (c_int, [vp, u32]),
         }
         for name, (res, args) in sig.items():
+            if path != _build.LIB and not hasattr(L, name):
+                continue  # an older build loaded for an A/B run
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
         _L = L
