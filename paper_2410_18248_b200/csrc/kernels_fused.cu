@@ -42,6 +42,7 @@ struct PhaseS {                  // S, H, T, X
     uint32_t start[kMaxBuckets]; // 58 KB: bucket totals -> bucket start positions
     uint32_t w32[kFW + 1];
     unsigned long long red[3][kFW];
+    uint32_t vmask[kKcap / 32];  // S: which kbuf positions (slots) hold keys
     uint32_t nk, base;
     unsigned long long mbar[2];  // S: TMA completion barriers of the two stage buffers
     uint32_t hb_j, hb_r;         // head-only mode: first bucket past the head, its start
@@ -474,7 +475,10 @@ constexpr uint32_t kHeadPre = 2560;
 // range_sort ranks sub-buckets of up to this many keys by comparison (one thread per
 // key, O(size) shared-memory reads): cheaper than a refinement pass for the few
 // sub-buckets of near-equal keys (e.g. saturated scores) a range may hold
-constexpr uint32_t kRangeRankM = 256;
+#ifndef LAMPS_RANK_M  // A/B builds: scripts/build_variant.sh out.so -DLAMPS_RANK_M=...
+#define LAMPS_RANK_M 256
+#endif
+constexpr uint32_t kRangeRankM = LAMPS_RANK_M;
 constexpr uint32_t kHeadTC = 2 * kKcap / 2, kHeadTW = kHeadTC + kHeadPre;  // by initial position
 constexpr uint32_t kHeadD = kHeadTW + kHeadPre, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
 static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
@@ -737,17 +741,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                 b.pool.sfc[slot] = w;
             }
         }
-        // warp-aggregated compaction (the order of keys in kbuf does not matter)
+        // keys stay at their slot's position in kbuf (no compaction: a CTA's slot range fits
+        // kbuf); which positions hold keys is one ballot word per warp
         const uint32_t m = __ballot_sync(0xffffffffu, have);
-        if (m) {
-            const uint32_t leader = __ffs(m) - 1u;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(&sm.s.nk, (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (have) {
-                sm.s.kbuf[base + __popc(m & lt_mask)] = key;
-                atomicAdd(&sm.s.cnt[bucket_of(key, c, half)], 1u);
-            }
+        if (lane == 0) sm.s.vmask[(ch * kChunk + tid) >> 5] = m;
+        if (have) {
+            sm.s.kbuf[ch * kChunk + tid] = key;
+            atomicAdd(&sm.s.cnt[bucket_of(key, c, half)], 1u);
         }
         __syncthreads();
     }
@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0 + 8u) : "memory");
     }
     __syncthreads();
-    const uint32_t nk_cta = sm.s.nk;
+    const uint32_t nk_cta = s_hi - s_lo;  // kbuf positions (slots of this CTA), vmask = which hold keys
 #pragma unroll
     for (int o = 16; o; o >>= 1) pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
     if (lane == 0) sm.s.red[0][warp] = pinned;
@@ -942,6 +942,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
         }
     } else {
         for (uint32_t i = tid - kRW * 32u; i < nk_cta; i += kFT - kRW * 32u) {
+            if (!((sm.s.vmask[i >> 5] >> (i & 31u)) & 1u)) continue;
             const uint64_t k = sm.s.kbuf[i];
             const uint32_t j = bucket_of(k, c, half);
             if (j >= jcut) continue;
