@@ -328,9 +328,9 @@ def run_ours(args, rank, world, local):
     t0 = time.perf_counter()
     ne_e2e = 0
     for k in range(e2e_steps):
-        # one engine iteration through lamps_iterate: the engine's report on the previous
-        # batch (2 finish, 2 call their API), API returns of requests paused earlier, the
-        # step, and 2 new arrivals into the freed slots -- one host synchronisation
+        # one engine iteration through lamps_iterate: API returns of requests paused earlier,
+        # 2 new arrivals, and the step with the engine's report on the previous batch (2
+        # finish, 2 call their API) -- one staging copy, one kernel, one host synchronisation
         ev = np.zeros(min(4, len(prev)), EVENT_DTYPE)
         for j in range(len(ev)):
             ev[j]["id"], ev[j]["kind"] = prev[j], 2 if j < 2 else 1
@@ -452,7 +452,7 @@ def run_ours(args, rank, world, local):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                     "d2h_bytes_per_step": d2h / e2e_steps,
                     "ms_per_step": 1e3 * dt_e2e / e2e_steps,
-                    "path": "lamps_iterate per engine iteration: API returns + events + step + arrivals "
+                    "path": "lamps_iterate per engine iteration: API returns + arrivals + events + step "
                             "(host buffers; results by mapped memory)"},
         }
         if variants:

@@ -249,14 +249,15 @@ int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev,
                         uint64_t kv_total_blocks, lamps_step_out* out);
 
 /*
- * lamps_iterate -- one engine iteration in one call: the API returns, then one
- * scheduling step with the engine's events, then the new arrivals, i.e. exactly
- *   lamps_api_return(returns); lamps_schedule_step(events); lamps_submit(arrivals)
- * but with one host synchronisation: every part is validated before any is applied
- * (on error nothing is applied), the returns and events are applied inside the step
- * kernel, and the arrivals are enqueued behind the step without waiting (they are
- * ranked from the next step on).  Arrival ids go to arrival_ids_out (may be NULL).
- * Errors: those of the three calls; EINVAL if more than 65536 returns.
+ * lamps_iterate -- one engine iteration in one call: the API returns, the new arrivals,
+ * then one scheduling step with the engine's events, i.e. exactly
+ *   lamps_api_return(returns); lamps_submit(arrivals); lamps_schedule_step(events)
+ * but with one host synchronisation: every part is validated before any is applied (on
+ * error nothing is applied), and on the fused path the returns, arrivals and events are
+ * applied inside the step kernel's prologue (one staging copy, one kernel).  Arrivals are
+ * ranked in this step; they cannot reuse the slots this iteration's FINISHED events free
+ * (those are free from the next call on).  Arrival ids go to arrival_ids_out (may be NULL).
+ * Errors: those of the three calls.
  */
 typedef struct {
     const lamps_event* events;        /* reports on the previous step's batch */

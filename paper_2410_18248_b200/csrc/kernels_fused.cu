@@ -681,11 +681,16 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                          : "memory");
         }
     };
-    if (a.n_ev | a.n_ret) {  // API returns and A0 for the engine's events on this CTA's slots,
-                             // before they are staged (the two touch disjoint requests)
+    if (a.n_ev | a.n_ret | a.n_sub) {  // API returns, arrivals and A0 for the engine's events on
+                                       // this CTA's slots, before they are staged (the three touch
+                                       // disjoint slots: PAUSED, FREE, admitted last step)
         for (uint32_t e = tid; e < a.n_ret; e += kFT) {
             const ReturnRec R = static_cast<const ReturnRec*>(b.returns)[e];
             if (R.slot >= s_lo && R.slot < s_hi) apply_return(b.pool, c, R);
+        }
+        for (uint32_t e = tid; e < a.n_sub; e += kFT) {
+            const SubmitRec R = static_cast<const SubmitRec*>(b.arrivals)[e];
+            if (R.slot >= s_lo && R.slot < s_hi) apply_submit(b.pool, c, R);
         }
         for (uint32_t e = tid; e < a.n_ev; e += kFT) {
             const DevEvent E = static_cast<const DevEvent*>(b.events)[e];

@@ -121,16 +121,7 @@ __global__ void __launch_bounds__(kAdmitThreads) k_admit(Bufs b, Cost c, StepArg
 __global__ void k_submit(Pool P, Cost c, const SubmitRec* rec, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const SubmitRec r = rec[i];
-    const uint32_t s = r.slot;
-    P.ctx[s] = r.ctx;
-    P.pre[s] = r.pre;
-    P.api[s] = r.api;
-    P.resp[s] = r.resp;
-    P.post[s] = r.post;
-    const uint64_t f = t_fwd(r.ctx, c);  // prefill owed
-    P.pend[s] = f > 0xffffffffull ? 0xffffffffu : (uint32_t)f;
-    P.sfc[s] = sfc_pack(ST_READY, r.has, 0, STR_NONE, 0) | SFC_DIRTY;  // a new segment (R26)
+    apply_submit(P, c, rec[i]);
 }
 
 __global__ void k_api_return(Pool P, Cost c, const ReturnRec* rec, uint32_t n) {

@@ -97,6 +97,7 @@ struct lamps_s {
     uint32_t xseq = 0;
     uint32_t tune = 0;  // StepArgs.tune, from env LAMPS_TUNE (A/B measurements)
     uint32_t ret_pending = 0;  // API returns staged for the next fused step's prologue
+    uint32_t sub_pending = 0;  // arrivals staged for the next fused step's prologue
     nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
@@ -369,6 +370,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.rank = h->rank;
     a.tune = h->tune;
     a.n_ret = h->fused ? h->ret_pending : 0u;
+    a.n_sub = h->fused ? h->sub_pending : 0u;
     if (h->merge) a.flags |= kStepMerge;
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
         a.flags |= kStepP2P;
@@ -407,6 +409,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     }
     h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);  // P2P: the exchange and merge are in k_fused
     h->ret_pending = 0;
+    h->sub_pending = 0;
     return LAMPS_OK;
 }
 
@@ -907,26 +910,70 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     if (h->world > 1 && h->cfg.transport == LAMPS_XPORT_LOOPBACK)
         return fail(h, LAMPS_EINVAL, "loopback shards step together: use lamps_group_step");
     const uint32_t nr = it->n_returns, ne = it->n_events, na = it->n_arrivals;
-    if (h->fused && nr > kIngestChunk) return fail(h, LAMPS_EINVAL, "more than 65536 API returns in one iteration");
     // 1. everything is validated before anything is applied
     std::vector<uint32_t> rticks, rctx, aticks;
     if (int rc = check_returns(h, it->return_ids, it->return_resp, it->return_next, nr, rticks, rctx)) return rc;
-    if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
     if (int rc = check_submit(h, it->arrivals, na, aticks)) return rc;
-    {   // the arrivals' slots, counting the slots this iteration's FINISHED events free
-        std::vector<uint32_t> freed;
-        for (uint32_t e = 0; e < ne; e++)
-            if (it->events[e].kind == LAMPS_EV_FINISHED) freed.push_back((uint32_t)(it->events[e].id & h->cost.cap_mask));
-        std::sort(freed.begin(), freed.end());
-        if (int rc = window_submit(h, na, freed.data(), (uint32_t)freed.size())) return rc;
+    if (int rc = window_submit(h, na, nullptr, 0)) return rc;
+    if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
+    // 2. API returns and arrivals: on the fused path staged together (one copy) and applied in
+    //    the step kernel's prologue; otherwise by their own kernels before the step
+    if (h->fused && (uint64_t)nr + na <= kIngestChunk) {
+        if (int rc = staging_wait(h)) return rc;
+        ReturnRec* rr = static_cast<ReturnRec*>(h->h_ingest);
+        SubmitRec* sr = reinterpret_cast<SubmitRec*>(rr + nr);
+        static_assert(sizeof(ReturnRec) == sizeof(SubmitRec), "one staging layout");
+        for (uint32_t i = 0; i < nr; i++) {
+            const lamps_segment& sg = it->return_next[i];
+            ReturnRec& r = rr[i];
+            r.slot = (uint32_t)(it->return_ids[i] & h->cost.cap_mask);
+            r.actual = it->return_resp[i];
+            r.pre = sg.pre_len;
+            r.has = sg.has_api;
+            r.api = sg.has_api ? rticks[i] : 0u;
+            r.resp = sg.has_api ? sg.resp_len : 0u;
+            r.post = sg.has_api ? sg.post_len : 0u;
+            r.pad = 0;
+        }
+        for (uint32_t i = 0; i < na; i++) {
+            const lamps_segment& sg = it->arrivals[i];
+            SubmitRec& r = sr[i];
+            r.slot = (uint32_t)((h->next_id + i) & h->cost.cap_mask);
+            r.ctx = sg.prompt_len;
+            r.pre = sg.pre_len;
+            r.has = sg.has_api;
+            r.api = sg.has_api ? aticks[i] : 0u;
+            r.resp = sg.has_api ? sg.resp_len : 0u;
+            r.post = sg.has_api ? sg.post_len : 0u;
+            r.pad = 0;
+        }
+        if (nr + na) {
+            CU(h, cudaMemcpyAsync(h->d_ingest, rr, (size_t)(nr + na) * sizeof(ReturnRec), cudaMemcpyHostToDevice,
+                                  h->stream));
+            if (int rc = staging_copied(h)) return rc;
+        }
+        h->ret_pending = nr;
+        h->sub_pending = na;
+        h->b.arrivals = static_cast<const ReturnRec*>(h->d_ingest) + nr;
+        for (uint32_t k = 0; k < nr; k++) {
+            h->hstate[it->return_ids[k] & h->cost.cap_mask] = H_READY;
+            h->hctx[it->return_ids[k] & h->cost.cap_mask] = rctx[k] + it->return_resp[k];
+        }
+        for (uint32_t k = 0; k < na; k++) {
+            h->hstate[(h->next_id + k) & h->cost.cap_mask] = H_READY;
+            h->hctx[(h->next_id + k) & h->cost.cap_mask] = it->arrivals[k].prompt_len;
+            if (it->arrival_ids_out) it->arrival_ids_out[k] = h->next_id + k;
+        }
+        h->next_id += na;
+    } else {
+        if (int rc = do_returns(h, it->return_ids, it->return_resp, it->return_next, nr, rticks, rctx, false))
+            return rc;
+        if (int rc = do_submit(h, it->arrivals, na, aticks, it->arrival_ids_out)) return rc;
     }
-    // 2. API returns (in the fused kernel's prologue), events, the step, its result
-    if (int rc = do_returns(h, it->return_ids, it->return_resp, it->return_next, nr, rticks, rctx, h->fused)) return rc;
+    // 3. the step with the events, its result (the one host synchronisation)
     if (int rc = stage_events(h, it->events, ne)) return rc;
     if (int rc = enqueue_step(h, it->kv_total_blocks, ne)) return rc;
-    if (int rc = fetch_result(h, out)) return rc;
-    // 3. arrivals, enqueued behind the step (no wait): they are ranked from the next step on
-    return do_submit(h, it->arrivals, na, aticks, it->arrival_ids_out);
+    return fetch_result(h, out);
 }
 
 int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* const* ev, const uint32_t* n_ev,

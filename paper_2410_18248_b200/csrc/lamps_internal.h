@@ -86,6 +86,7 @@ struct StepArgs {
     uint32_t world, rank;   // multi-GPU shards
     uint32_t xseq;          // peer-memory exchange: sequence number of this step's exchange
     uint32_t n_ret;         // fused path: API returns staged at Bufs::returns, applied in the prologue
+    uint32_t n_sub;         // fused path: arrivals staged at Bufs::arrivals, applied in the prologue
     uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
                             // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
                             // instead of first-boundary snapping of the range ends
@@ -107,6 +108,7 @@ struct Bufs {
     uint64_t* pre_id;        // preempted ids
     const void* events;      // lamps_event[max_batch] (device)
     const void* returns;     // ReturnRec[] staged by lamps_iterate (device, the ingest staging)
+    const void* arrivals;    // SubmitRec[] staged by lamps_iterate (device, after the returns)
     unsigned long long* dbg; // [cap][4] W_P, W_D, W_S, score (LAMPS_DEBUG_OUT) or null
     unsigned long long* trace;  // [grid][16] clock64 at phase boundaries (LAMPS_TRACE) or null
     uint32_t* flags;         // grid barrier words (see sort_dev.cuh)

@@ -31,6 +31,20 @@ __device__ __forceinline__ void apply_event(const Pool& P, const Cost& c, const 
     P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u) | (w & SFC_META);
 }
 
+// Intake of one new request (Alg.1): READY, ctx = prompt, the prefill owed
+// T_fwd(prompt), a new segment (k_submit, or the fused kernel's prologue).
+__device__ __forceinline__ void apply_submit(const Pool& P, const Cost& c, const SubmitRec r) {
+    const uint32_t s = r.slot;
+    P.ctx[s] = r.ctx;
+    P.pre[s] = r.pre;
+    P.api[s] = r.api;
+    P.resp[s] = r.resp;
+    P.post[s] = r.post;
+    const uint64_t f = t_fwd(r.ctx, c);  // prefill owed
+    P.pend[s] = f > 0xffffffffull ? 0xffffffffu : (uint32_t)f;
+    P.sfc[s] = sfc_pack(ST_READY, r.has, 0, STR_NONE, 0) | SFC_DIRTY;  // a new segment (R26)
+}
+
 // API return of one PAUSED request (Alg.1, R10): ctx grows by the actual
 // response; the owed prefill / swap-in by its handling strategy; the next segment's
 // predictions; READY (K_api_return, or the fused kernel's prologue).

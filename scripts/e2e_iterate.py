@@ -37,8 +37,8 @@ def run(mode):
         else:
             if len(ids):
                 s.api_return(ids, resp, nxt)
-            out = s.step(ev, kv)
             s.submit_rc(segs)
+            out = s.step(ev, kv)
         t2 = time.perf_counter()
         T["build"] += t1 - t0; T["call"] += t2 - t1
         paused += [int(x) for x in ev["id"][2:]]

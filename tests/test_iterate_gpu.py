@@ -1,7 +1,8 @@
-"""lamps_iterate (one engine iteration in one call: API returns, the step with its events,
-arrivals) against the oracle running the same iteration as three separate calls, on closed
+"""lamps_iterate (one engine iteration in one call: API returns, arrivals, the step with its
+events) against the oracle running the same iteration as three separate calls, on closed
 loops -- every step's outputs and, periodically, the whole pool state bit-exact -- on the
-fused path (returns and events applied in the kernel's prologue) and the 3-kernel path."""
+fused path (returns, arrivals and events applied in the kernel's prologue) and the 3-kernel
+path."""
 import numpy as np
 import pytest
 
@@ -18,30 +19,24 @@ def loop(cname, n_req, steps, initial, per_step, path="fused", seed=0, state_eve
     s, o = make_pair(cfg, debug=False, path=path)
     reqs = gen.requests(cname, n_req, seed=seed)
     drv = gen.ClosedLoop(reqs, gen.PROFILES[gen.CONFIGS[cname]["profile"]]["tau"], initial, per_step, seed)
-    # the first arrivals before any step
-    idx, rows = drv.arrivals(0)
-    a, b = seg_rows_to_arrays(rows)
-    ids = s.submit(a)
-    rc, ido = o.submit(b)
-    assert rc == 0 and np.array_equal(ids, ido)
-    drv.on_submitted(idx, ids)
     prev = []
     seen = dict(ret=0, ev=0, arr=0)
     for t in range(steps):
         rids, resp, rrows = drv.api_returns(t)
+        idx, arows = drv.arrivals(t)
         ev = drv.events(t, prev)
-        idx, arows = drv.arrivals(t + 1)
         ra, rb = seg_rows_to_arrays(rrows)
         aa, ab = seg_rows_to_arrays(arows)
         g, gids = s.iterate(events=ev, ret_ids=rids, ret_resp=resp, ret_next=ra, arrivals=aa, kv_total=kv)
+        # the oracle runs the same iteration as three calls
         if rids:
             assert o.api_return(rids, resp, rb) == 0
-        r = o.step(ev, kv)
-        compare_outputs(s, g, r, where=f"{cname} t={t}")
         if len(arows):
             rc, oids = o.submit(ab)
             assert rc == 0 and np.array_equal(gids, oids), t
             drv.on_submitted(idx, gids)
+        r = o.step(ev, kv)
+        compare_outputs(s, g, r, where=f"{cname} t={t}")
         if t % state_every == 0 or t == steps - 1:
             compare_state(s, o, where=f"{cname} t={t}")
         prev = g["admitted_id"]
