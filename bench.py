@@ -364,17 +364,19 @@ def run_ours(args, rank, world, local):
     variants = []
     if world == 1 and not args.no_variants:
         from paper_2410_18248_b200.lamps import LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL
-        from paper_2410_18248_b200 import LAMPS_HEAD_ONLY
-        for name, over in (("head_only", dict(flags=LAMPS_HEAD_ONLY)),
+        from paper_2410_18248_b200 import LAMPS_HEAD_ONLY, LAMPS_MERGE
+        for name, over in (("p2p_exchange_merge_world1", dict(flags=LAMPS_MERGE, transport=LAMPS_XPORT_P2P)),
+                           ("head_only", dict(flags=LAMPS_HEAD_ONLY)),
                            ("head_only_interval_10", dict(flags=LAMPS_HEAD_ONLY, score_interval=10)),
                            ("lamps_interval_10", dict(score_interval=10)),
                            ("sjf", dict(policy=LAMPS_POLICY_SJF)),
                            ("sjf_total", dict(policy=LAMPS_POLICY_SJF_TOTAL)),
                            ("fcfs", dict(policy=LAMPS_POLICY_FCFS))):
-            vcfg = dict(cfg); vcfg.update({k: v for k, v in over.items() if k != "flags"})
-            sv = Scheduler(vcfg, flags=over.get("flags", 0), stream=stream)
+            vcfg = dict(cfg); vcfg.update({k: v for k, v in over.items() if k not in ("flags", "transport")})
+            sv = Scheduler(vcfg, flags=over.get("flags", 0), stream=stream,
+                           transport=over.get("transport", LAMPS_XPORT_NCCL))
             sv.import_pool(snap, snap["id_base"], snap["next_id"])
-            for _ in range(args.warmup):
+            for _ in range(max(args.warmup, 100)):  # the range weights settle (burn-in)
                 flush.zero_()
                 sv.step_async(kv)
             sv.import_pool(snap, snap["id_base"], snap["next_id"])
