@@ -1073,7 +1073,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     if (tid == 0) {
         ctl->n_passes = passes;
         ctl->final_buf = final_buf;
-        ctl->fallbacks += fallback ? 1u : 0u;
+        if (fallback) atomicAdd(&ctl->fallbacks, 1u);  // a reduction, no load on the path
         ctl->n_ranked = head_only ? r_end0 : n;  // head-only: keys [0, hb_r) are ranked
     }
     TRACE(15);

@@ -61,16 +61,23 @@ __device__ __forceinline__ void merge_admit_cta(const Bufs& b, const Cost& c, co
     uint32_t* run = tmp + K;  // K indices of the run being merged
     const uint32_t tid = threadIdx.x;
 
-    if (tid < W) nv[tid] = reinterpret_cast<const MergeHdr*>(xrecv + (size_t)tid * (K + 1))->n_valid;
-    if (tid == 0) {
+    if (tid < 32) {  // the W headers in parallel (warp 0), sums by shuffles
         unsigned long long kv = 0, pin = 0;
-        for (uint32_t r = 0; r < W; r++) {
-            const MergeHdr* h = reinterpret_cast<const MergeHdr*>(xrecv + (size_t)r * (K + 1));
-            kv += h->kv_total;
-            pin += h->pinned;
+        if (tid < W) {
+            const MergeHdr h = *reinterpret_cast<const MergeHdr*>(xrecv + (size_t)tid * (K + 1));
+            nv[tid] = h.n_valid;
+            kv = h.kv_total;
+            pin = h.pinned;
         }
-        hsum[0] = kv;
-        hsum[1] = pin;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            kv += __shfl_xor_sync(0xffffffffu, kv, o);
+            pin += __shfl_xor_sync(0xffffffffu, pin, o);
+        }
+        if (tid == 0) {
+            hsum[0] = kv;
+            hsum[1] = pin;
+        }
     }
     __syncthreads();
     for (uint32_t f = tid; f < R; f += kMT) {
