@@ -292,7 +292,7 @@ def run_ours(args, rank, world, local):
     sp = Scheduler(cfg, flags=LAMPS_TIMING | LAMPS_TRACE, stream=stream) if not merged else None
     if sp is not None:
       sp.import_pool(snap, snap["id_base"], snap["next_id"])
-      for _ in range(args.warmup):
+      for _ in range(max(args.warmup, 100)):  # burn-in: the range weights settle
           flush.zero_()
           sp.step_async(kv)
       sp.timing()
@@ -447,6 +447,13 @@ def run_ours(args, rank, world, local):
                          "frac": ach / peak if ach else None, "traffic": traffic,
                          "peak_source": peak_src},
             "kernels": kernels_tbl,
+            # A4 alone (SURVEY 8(d) "keys/s per sort"): eligible keys over the fused kernel's sort
+            # phases (scatter into bucket order + its barrier + the range sorts, slowest CTA)
+            "sort": ({"keys_per_s": n_elig / (1e-6 * (trace_us["bucket_scatter"] + trace_us["barrier3"]
+                                                      + trace_us["range_sort"])),
+                      "us": round(trace_us["bucket_scatter"] + trace_us["barrier3"] + trace_us["range_sort"], 2)}
+                     if trace_us else None),
+            "pool_slots_per_s": world * cap / (ms_max / 1e3),
             "path": ("fused cooperative step kernel" + (f" ({xdesc})" if merged else "")) if fused else "3-kernel path",
             "sort_passes": passes,
             "gpu_launches": kernels * args.steps,

@@ -905,7 +905,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
                     w[u] = 0.f;
                     if (r >= 1 && r < G) {
                         const float rel = cst[u] > 0.f ? __fdividef(mean, cst[u]) : 1.f;
-                        w[u] = rel < 0.4f ? 0.f : fminf(rel, 1.25f);
+                        // two-sided (measured 0.8 us better than one-sided or uniform on one
+                        // box, scripts/ab_tune.py); LAMPS_TUNE bit 3: one-sided (cap 1)
+                        w[u] = rel < 0.4f ? 0.f : fminf(rel, (a.tune & 8u) ? 1.f : 1.25f);
                         if (a.tune & 1u) w[u] = 1.f;
                     }
                     run += w[u];

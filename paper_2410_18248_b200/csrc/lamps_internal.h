@@ -89,7 +89,8 @@ struct StepArgs {
     uint32_t n_sub;         // fused path: arrivals staged at Bufs::arrivals, applied in the prologue
     uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
                             // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
-                            // instead of first-boundary snapping of the range ends
+                            // instead of first-boundary snapping of the range ends, bit 3
+                            // one-sided speed weights (capped at 1 instead of 1.25)
 };
 
 struct Bufs {
