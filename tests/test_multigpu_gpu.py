@@ -12,13 +12,14 @@ from shard_util import FIELDS, restrict, split_kv, union_and_shards
 pytestmark = pytest.mark.gpu
 
 
-def run(cname, world, cap_l, n_union, kv_union, steps=3, seed=0, p2p=False, **over):
+def run(cname, world, cap_l, n_union, kv_union, steps=3, seed=0, p2p=False, head_only=False, **over):
     from paper_2410_18248_b200 import Scheduler
     from paper_2410_18248_b200.lamps import LAMPS_SHARE_DEVICE, LAMPS_XPORT_LOOPBACK, LAMPS_XPORT_P2P
     import torch
     cfg_l, cfg_u, u, shards = union_and_shards(cname, world, cap_l, n_union, seed=seed, **over)
     if p2p:  # peer-memory exchange inside the step kernel; ranks co-resident on this device
-        S = [Scheduler(cfg_l, world=world, rank=r, transport=LAMPS_XPORT_P2P, flags=LAMPS_SHARE_DEVICE,
+        S = [Scheduler(cfg_l, world=world, rank=r, transport=LAMPS_XPORT_P2P,
+                       flags=LAMPS_SHARE_DEVICE | (64 if head_only else 0),  # 64 = LAMPS_HEAD_ONLY
                        stream=torch.cuda.Stream()) for r in range(world)]
         Scheduler.p2p_connect_local(S)
     else:
@@ -41,12 +42,15 @@ def run(cname, world, cap_l, n_union, kv_union, steps=3, seed=0, p2p=False, **ov
             assert list(g["preempted_id"]) == list(restrict(ro["preempted_id"], world, r)), where
             assert g["budget"] == ro["budget"] and g["budget_used"] == ro["budget_used"], where
             assert g["blocked_head"] == ro["blocked_head"], where
-            # local ranked order == global order restricted to the shard
+            # local ranked order == global order restricted to the shard (a prefix of it when
+            # only the head is ranked)
             ids, score, starv = S[r].decode_keys(S[r].ranked_keys(), g["id_base"])
             mine = ro["ranked_id"] % world == r
-            assert np.array_equal(ids, ro["ranked_id"][mine] // world), where
-            assert np.array_equal(score, ro["ranked_score"][mine]), where
-            assert np.array_equal(starv, ro["ranked_starving"][mine]), where
+            m = len(ids)
+            assert head_only or m == int(mine.sum()), where
+            assert np.array_equal(ids, (ro["ranked_id"][mine] // world)[:m]), where
+            assert np.array_equal(score, ro["ranked_score"][mine][:m]), where
+            assert np.array_equal(starv, ro["ranked_starving"][mine][:m]), where
             # whole shard state == union state restricted
             e = S[r].export_pool()
             P = o.pool
@@ -142,3 +146,8 @@ def test_p2p_self_exchange_world1():
         assert np.array_equal(ga["preempted_id"], gb["preempted_id"])
     assert b.stats()[0] == 1  # one kernel: exchange and merge inside k_fused
     a.close(); b.close()
+
+
+def test_p2p_merge_head_only():
+    """F3 head-only ranking on every rank + the peer-memory exchange: the same global batch."""
+    run("C2", 2, 2048, 1800, 3000, max_batch=256, p2p=True, head_only=True, steps=4)
