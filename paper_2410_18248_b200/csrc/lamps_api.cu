@@ -277,6 +277,8 @@ void grids(lamps_t* h, bool query_device) {
     h->fused_grid = (uint32_t)std::max(1, sms * std::max(fused_occ, 1));
     if ((h->cfg.flags & LAMPS_SHARE_DEVICE) && h->cfg.world > 1)  // co-resident ranks split the SMs
         h->fused_grid = std::max<uint32_t>(1u, h->fused_grid / h->cfg.world);
+    if (const char* gv = std::getenv("LAMPS_FUSED_GRID"))  // measurements: a smaller step grid
+        h->fused_grid = std::max<uint32_t>(1u, std::min<uint32_t>(h->fused_grid, (uint32_t)std::strtoul(gv, nullptr, 0)));
     {
         const uint32_t groups = (h->cap + 3) / 4;
         const uint32_t gpc = (groups + h->fused_grid - 1) / h->fused_grid;
