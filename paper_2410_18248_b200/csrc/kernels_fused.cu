@@ -33,7 +33,6 @@ constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
 constexpr int kBucketM = 7;                 // score bits per octave
 constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
 constexpr int kLocalItems = kKcap / kFT;    // 10
-constexpr int kTRows = 8;                   // count exchange: up to 256 CTAs
 constexpr int kMaxCtas = 256;               // range weights: grid size limit
 
 struct PhaseS {                  // S, H, T, X
@@ -711,7 +710,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     for (uint32_t i = tid; i < (NB + 3u) / 4u; i += kFT) reinterpret_cast<uint4*>(sm.s.cnt)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     unsigned long long pinned = 0;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     for (uint32_t ch = 0; ch < nchunk; ch++) {
         if (tid == 0 && ch + 1 < nchunk) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer reads done (barrier below)
