@@ -272,15 +272,28 @@ class Scheduler:
         self._check(self.api_return_rc(ids, actual, nxt))
 
     # ---- step
+    def _views(self, out: lamps_step_out):
+        """numpy views of the handle's result lists (fixed host buffers), made once."""
+        key = (ctypes.addressof(out.admitted_ids.contents) if out.admitted_ids else 0,
+               ctypes.addressof(out.preempted_ids.contents) if out.preempted_ids else 0)
+        if getattr(self, "_vkey", None) != key:
+            mb = int(self.cfg.max_batch)
+            self._vkey = key
+            self._vadm = np.ctypeslib.as_array(out.admitted_ids, (mb,)) if key[0] else None
+            self._vstr = np.ctypeslib.as_array(out.admitted_strategy, (mb,)) if key[0] else None
+            self._vpre = np.ctypeslib.as_array(out.preempted_ids, (mb,)) if key[1] else None
+        return self._vadm, self._vstr, self._vpre
+
     def _result(self, out: lamps_step_out) -> dict:
         na, npr = out.n_admitted, out.n_preempted
+        va, vs, vp_ = self._views(out)
         return {
             "rc": 0, "n_eligible": int(out.n_eligible), "pinned": int(out.pinned),
             "budget": int(out.budget), "budget_used": int(out.budget_used), "n_admitted": int(na),
             "n_preempted": int(npr), "blocked_head": int(out.blocked_head), "id_base": int(out.id_base),
-            "admitted_id": np.ctypeslib.as_array(out.admitted_ids, (na,)).copy() if na else np.zeros(0, np.uint64),
-            "admitted_strategy": np.ctypeslib.as_array(out.admitted_strategy, (na,)).copy() if na else np.zeros(0, np.uint8),
-            "preempted_id": np.ctypeslib.as_array(out.preempted_ids, (npr,)).copy() if npr else np.zeros(0, np.uint64),
+            "admitted_id": va[:na].copy() if na else np.zeros(0, np.uint64),
+            "admitted_strategy": vs[:na].copy() if na else np.zeros(0, np.uint8),
+            "preempted_id": vp_[:npr].copy() if npr else np.zeros(0, np.uint64),
         }
 
     def step_rc(self, events=None, kv_total: int = 0):
