@@ -30,7 +30,10 @@ namespace {
 constexpr int kFT = 1024;                   // threads per CTA
 constexpr int kFW = kFT / 32;               // warps
 constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
-constexpr int kBucketM = 7;                 // score bits per octave
+#ifndef LAMPS_BUCKET_M  // A/B builds: scripts/build_variant.sh out.so -DLAMPS_BUCKET_M=...
+#define LAMPS_BUCKET_M 7
+#endif
+constexpr int kBucketM = LAMPS_BUCKET_M;                 // score bits per octave
 constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
 constexpr int kLocalItems = kKcap / kFT;    // 10
 constexpr int kMaxCtas = 256;               // range weights: grid size limit
@@ -620,6 +623,50 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     return dw_ok;
 }
 
+// A small range (rn <= kSmallSort keys): ranked by comparison against all its keys (the
+// keys are unique, so the rank is the count of smaller keys; the few hundred keys are read
+// as shared-memory broadcasts), no bucket table.  A small pool's head range can span
+// thousands of sparse buckets (starving keys first, over the whole score range), where
+// the table dominates.  HEAD (CTA 0): the admission's per-key loads by sorted position into
+// the staged head arrays, prefetched to L2 while ranking.
+constexpr uint32_t kSmallSort = 384;
+template <bool HEAD>
+__device__ __forceinline__ void small_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn, const Cost& c,
+                                           const Pool* pool, uint32_t id_base_mod) {
+    const uint32_t tid = threadIdx.x;
+    uint64_t* A = sm.a;
+    uint64_t* Bq = sm.b;  // scratch [0, rn): below the staged head arrays
+    uint64_t k = 0;
+    if (tid < rn) {
+        k = __ldcg(src + tid);
+        A[tid] = k;
+        if (HEAD) {
+            const uint32_t slot = (id_base_mod + (uint32_t)(k & c.cap_mask)) & c.cap_mask;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->ctx + slot));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->sfc + slot));
+        }
+    }
+    __syncthreads();
+    if (tid < rn) {
+        uint32_t r = 0;
+#pragma unroll 8
+        for (uint32_t q = 0; q < rn; q++) r += A[q] < k ? 1u : 0u;
+        Bq[r] = k;
+    }
+    __syncthreads();
+    if (tid < rn) {
+        const uint64_t x = Bq[tid];
+        A[tid] = x;
+        if (HEAD) {
+            uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
+            const uint32_t slot = (id_base_mod + (uint32_t)(x & c.cap_mask)) & c.cap_mask;
+            b32[kHeadD + tid] = (uint32_t)blk((uint64_t)__ldcg(&pool->ctx[slot]) + 1u, c);
+            b32[kHeadW + tid] = __ldcg(&pool->sfc[slot]);
+        }
+    }
+    __syncthreads();
+}
+
 #define TRACE(k)                                                                         \
     do {                                                                                 \
         if (b.trace && threadIdx.x == 0) b.trace[blockIdx.x * kTraceSlots + (k)] = clock64(); \
@@ -983,7 +1030,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             tr[28] = smid;  // diagnostics: SM of this CTA
             for (int q = 32; q < 64; q++) tr[q] = 0;
         }
-        if (j_hi - j_lo < (uint32_t)kSubBuckets) {
+        if (rn <= kSmallSort && !(a.tune & 4u)) {
+            TRACE(13);
+            if (bid == 0) {
+                small_sort<true>(sm.l, b.keys[0] + r_lo, rn, c, &b.pool, a.id_base_mod);
+                head_dw = true;
+            } else {
+                small_sort<false>(sm.l, b.keys[0] + r_lo, rn, c, nullptr, 0u);
+            }
+        } else if (j_hi - j_lo < (uint32_t)kSubBuckets) {
             TRACE(13);
             if (bid == 0 && rn <= kHeadPre)
                 head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c,

@@ -90,7 +90,8 @@ struct StepArgs {
     uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
                             // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
                             // instead of first-boundary snapping of the range ends, bit 3
-                            // one-sided speed weights (capped at 1 instead of 1.25)
+                            // one-sided speed weights (capped at 1 instead of 1.25), bit 2 the
+                            // bucket range sort also for ranges of <= 384 keys
 };
 
 struct Bufs {

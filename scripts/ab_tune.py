@@ -7,9 +7,10 @@ import torch
 import gen
 from paper_2410_18248_b200 import Scheduler
 
-cfg = gen.lib_config("C5")
-snap = gen.snapshot("C5", seed=0, id_base=(1 << 20) * 7 + 99)
-kv = gen.CONFIGS["C5"]["kv_total"]
+CN = os.environ.get("CFG", "C5")
+cfg = gen.lib_config(CN)
+snap = gen.snapshot(CN, seed=0, id_base=(1 << 20) * 7 + 99)
+kv = gen.CONFIGS[CN]["kv_total"]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 settings = [int(x, 0) for x in os.environ.get("TUNES", "0,1,2,3").split(",")]
 res = {t: [] for t in settings}
