@@ -667,6 +667,99 @@ __device__ __forceinline__ void small_sort(PhaseL& sm, const uint64_t* __restric
     __syncthreads();
 }
 
+// CTA 0's head range when its buckets are sparse (nb > 2 rn: the head's starving keys span
+// a wide score range): a counting sort over the OCCUPIED buckets only -- a bitmap of the
+// keys' buckets, their compact index by popcount prefix -- then rank by comparison inside
+// each bucket (a bucket holds ~1 key here), then the admission's per-key loads by sorted
+// position (prefetched to L2 at the start).  No bucket table over the whole interval.
+// Returns false (nothing written) if a bucket holds more than kRangeRankM keys; the caller
+// then uses range_sort.
+__device__ __forceinline__ bool head_sparse_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
+                                                 const Cost& c, uint32_t half, uint32_t j_lo, uint32_t nb,
+                                                 const Pool& pool, uint32_t id_base_mod) {
+    constexpr int NI = (kHeadPre + kFT - 1) / kFT;  // 3
+    const uint32_t tid = threadIdx.x;
+    uint32_t* bm = sm.pos;            // bucket bitmap, nw <= 1024 words
+    uint32_t* wp = sm.pos + 1024;     // exclusive popcount prefix per word
+    uint32_t* cnt = sm.pos + 2048;    // per occupied bucket: count -> start
+    uint32_t* sbi = sm.pos + 4608;    // per position: bucket start | size << 14
+    uint64_t* A = sm.a;
+    uint64_t* Bq = sm.b;              // [0, rn): below the staged head arrays
+    const uint32_t nw = (nb + 31u) >> 5;
+    for (uint32_t w = tid; w < nw; w += kFT) bm[w] = 0u;
+    __syncthreads();
+    uint64_t k[NI];
+    uint32_t J[NI], ci[NI];
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        k[u] = 0;
+        J[u] = 0;
+        if (i < rn) {
+            k[u] = __ldcg(src + i);
+            J[u] = bucket_of(k[u], c, half) - j_lo;
+            atomicOr(&bm[J[u] >> 5], 1u << (J[u] & 31u));
+            const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool.ctx + slot));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool.sfc + slot));
+        }
+    }
+    __syncthreads();
+    for (uint32_t w = tid; w < nw; w += kFT) wp[w] = __popc(bm[w]);
+    __syncthreads();
+    const uint32_t nocc = smem_excl_scan<kFT, 1>(wp, nw, sm.w32);
+    for (uint32_t q = tid; q < nocc; q += kFT) cnt[q] = 0u;
+    __syncthreads();
+    uint32_t ord[NI];
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        ci[u] = 0;
+        ord[u] = 0;
+        if (i < rn) {
+            const uint32_t w = J[u] >> 5;
+            ci[u] = wp[w] + __popc(bm[w] & ((1u << (J[u] & 31u)) - 1u));
+            ord[u] = atomicAdd(&cnt[ci[u]], 1u);
+        }
+    }
+    __syncthreads();
+    uint32_t big = 0;
+    for (uint32_t q = tid; q < nocc; q += kFT) big |= cnt[q] > kRangeRankM ? 1u : 0u;
+    if (__syncthreads_or(big)) return false;
+    (void)smem_excl_scan<kFT, 3>(cnt, nocc, sm.w32);
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        if (i < rn) {
+            const uint32_t st = cnt[ci[u]], e = ci[u] + 1u < nocc ? cnt[ci[u] + 1u] : rn;
+            const uint32_t p = st + ord[u];
+            A[p] = k[u];
+            sbi[p] = st | ((e - st) << 14);
+        }
+    }
+    __syncthreads();
+    uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        const uint32_t p = tid + (uint32_t)u * kFT;
+        if (p < rn) {
+            const uint64_t x = A[p];
+            const uint32_t inf = sbi[p], st = inf & 0x3fffu, m = inf >> 14;
+            uint32_t r = 0;
+            for (uint32_t q = 0; q < m; q++) r += A[st + q] < x ? 1u : 0u;
+            const uint32_t fp = st + r;
+            Bq[fp] = x;
+            const uint32_t slot = (id_base_mod + (uint32_t)(x & c.cap_mask)) & c.cap_mask;
+            b32[kHeadD + fp] = (uint32_t)blk((uint64_t)__ldcg(&pool.ctx[slot]) + 1u, c);
+            b32[kHeadW + fp] = __ldcg(&pool.sfc[slot]);
+        }
+    }
+    __syncthreads();
+    for (uint32_t p = tid; p < rn; p += kFT) A[p] = Bq[p];
+    __syncthreads();
+    return true;
+}
+
 #define TRACE(k)                                                                         \
     do {                                                                                 \
         if (b.trace && threadIdx.x == 0) b.trace[blockIdx.x * kTraceSlots + (k)] = clock64(); \
@@ -1038,6 +1131,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
             } else {
                 small_sort<false>(sm.l, b.keys[0] + r_lo, rn, c, nullptr, 0u);
             }
+        } else if (bid == 0 && rn <= kHeadPre && j_hi - j_lo > 2u * rn && j_hi - j_lo <= 32768u &&
+                   !(a.tune & 16u) &&
+                   head_sparse_sort(sm.l, b.keys[0] + r_lo, rn, c, half, j_lo, j_hi - j_lo, b.pool,
+                                    a.id_base_mod)) {
+            TRACE(13);
+            head_dw = true;
         } else if (j_hi - j_lo < (uint32_t)kSubBuckets) {
             TRACE(13);
             if (bid == 0 && rn <= kHeadPre)

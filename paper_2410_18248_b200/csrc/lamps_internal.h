@@ -91,7 +91,8 @@ struct StepArgs {
                             // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
                             // instead of first-boundary snapping of the range ends, bit 3
                             // one-sided speed weights (capped at 1 instead of 1.25), bit 2 the
-                            // bucket range sort also for ranges of <= 384 keys
+                            // bucket range sort also for ranges of <= 384 keys, bit 4 no
+                            // sparse-bucket sort for the head range
 };
 
 struct Bufs {
