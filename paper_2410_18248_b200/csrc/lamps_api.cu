@@ -102,6 +102,7 @@ struct lamps_s {
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
     void* d_ingest = nullptr;
+    const void* d_events = nullptr;
     uint32_t* d_gather = nullptr;
     // host shadow
     std::vector<uint8_t> hstate;
@@ -253,6 +254,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.adm_strat[1] = base + o_at1;
     h->b.pre_id = reinterpret_cast<uint64_t*>(base + o_pre);
     h->b.events = base + o_ev;
+    h->d_events = h->b.events;
     h->d_ingest = base + o_ing;
     h->b.returns = h->d_ingest;
     h->d_gather = reinterpret_cast<uint32_t*>(base + o_gat);
@@ -662,15 +664,22 @@ int check_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_t
     return LAMPS_OK;
 }
 
-// events: staged to the device, liveness shadow updated
-int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
-    if (!n_ev) return LAMPS_OK;
-    std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
-    CU(h, cudaMemcpyAsync(const_cast<void*>(h->b.events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
-                          cudaMemcpyHostToDevice, h->stream));
+// events: liveness shadow updated (the events already staged)
+void events_staged(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
+    if (!n_ev) return;
     for (uint32_t e = 0; e < n_ev; e++)
         h->hstate[ev[e].id & h->cost.cap_mask] = ev[e].kind == LAMPS_EV_FINISHED ? H_FREE : H_PAUSED;
     advance_id_base(h);
+}
+
+// events: staged to the device, liveness shadow updated
+int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
+    h->b.events = h->d_events;
+    if (!n_ev) return LAMPS_OK;
+    std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
+    CU(h, cudaMemcpyAsync(const_cast<void*>(h->d_events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
+                          cudaMemcpyHostToDevice, h->stream));
+    events_staged(h, ev, n_ev);
     return LAMPS_OK;
 }
 
@@ -918,9 +927,12 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     if (int rc = check_submit(h, it->arrivals, na, aticks)) return rc;
     if (int rc = window_submit(h, na, nullptr, 0)) return rc;
     if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
-    // 2. API returns and arrivals: on the fused path staged together (one copy) and applied in
-    //    the step kernel's prologue; otherwise by their own kernels before the step
-    if (h->fused && (uint64_t)nr + na <= kIngestChunk) {
+    // 2. API returns, arrivals and the events: on the fused path staged together (one copy)
+    //    and applied in the step kernel's prologue; otherwise returns and arrivals by their own
+    //    kernels before the step
+    const size_t rbytes = (size_t)(nr + na) * sizeof(ReturnRec), ebytes = (size_t)ne * sizeof(lamps_event);
+    bool ev_staged = false;
+    if (h->fused && rbytes + ebytes <= (size_t)kIngestChunk * sizeof(SubmitRec)) {
         if (int rc = staging_wait(h)) return rc;
         ReturnRec* rr = static_cast<ReturnRec*>(h->h_ingest);
         SubmitRec* sr = reinterpret_cast<SubmitRec*>(rr + nr);
@@ -949,11 +961,13 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
             r.post = sg.has_api ? sg.post_len : 0u;
             r.pad = 0;
         }
-        if (nr + na) {
-            CU(h, cudaMemcpyAsync(h->d_ingest, rr, (size_t)(nr + na) * sizeof(ReturnRec), cudaMemcpyHostToDevice,
-                                  h->stream));
+        if (ne) std::memcpy(reinterpret_cast<uint8_t*>(rr) + rbytes, it->events, ebytes);  // 16 B aligned
+        if (rbytes + ebytes) {
+            CU(h, cudaMemcpyAsync(h->d_ingest, rr, rbytes + ebytes, cudaMemcpyHostToDevice, h->stream));
             if (int rc = staging_copied(h)) return rc;
         }
+        h->b.events = static_cast<const uint8_t*>(h->d_ingest) + rbytes;
+        ev_staged = true;
         h->ret_pending = nr;
         h->sub_pending = na;
         h->b.arrivals = static_cast<const ReturnRec*>(h->d_ingest) + nr;
@@ -973,7 +987,10 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
         if (int rc = do_submit(h, it->arrivals, na, aticks, it->arrival_ids_out)) return rc;
     }
     // 3. the step with the events, its result (the one host synchronisation)
-    if (int rc = stage_events(h, it->events, ne)) return rc;
+    if (ev_staged)
+        events_staged(h, it->events, ne);
+    else if (int rc = stage_events(h, it->events, ne))
+        return rc;
     if (int rc = enqueue_step(h, it->kv_total_blocks, ne)) return rc;
     return fetch_result(h, out);
 }
