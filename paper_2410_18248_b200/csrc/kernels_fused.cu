@@ -768,7 +768,7 @@ __device__ __forceinline__ bool head_sparse_sort(PhaseL& sm, const uint64_t* __r
 // P2P: the peer-memory exchange + in-kernel merge instance (its code and shared-memory
 // tail are left out of the plain instance)
 template <bool DBG, bool P2P>
-__global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
+__global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, const __grid_constant__ InlineStage inl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
     Ctl* ctl = b.ctl;
@@ -823,16 +823,23 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a) {
     if (a.n_ev | a.n_ret | a.n_sub) {  // API returns, arrivals and A0 for the engine's events on
                                        // this CTA's slots, before they are staged (the three touch
                                        // disjoint slots: PAUSED, FREE, admitted last step)
+        const ReturnRec* rets = a.inl ? reinterpret_cast<const ReturnRec*>(inl.bytes)
+                                      : static_cast<const ReturnRec*>(b.returns);
+        const SubmitRec* subs = a.inl ? reinterpret_cast<const SubmitRec*>(inl.bytes) + a.n_ret
+                                      : static_cast<const SubmitRec*>(b.arrivals);
+        const DevEvent* evs = a.inl ? reinterpret_cast<const DevEvent*>(reinterpret_cast<const SubmitRec*>(inl.bytes) +
+                                                                        a.n_ret + a.n_sub)
+                                    : static_cast<const DevEvent*>(b.events);
         for (uint32_t e = tid; e < a.n_ret; e += kFT) {
-            const ReturnRec R = static_cast<const ReturnRec*>(b.returns)[e];
+            const ReturnRec R = rets[e];
             if (R.slot >= s_lo && R.slot < s_hi) apply_return(b.pool, c, R);
         }
         for (uint32_t e = tid; e < a.n_sub; e += kFT) {
-            const SubmitRec R = static_cast<const SubmitRec*>(b.arrivals)[e];
+            const SubmitRec R = subs[e];
             if (R.slot >= s_lo && R.slot < s_hi) apply_submit(b.pool, c, R);
         }
         for (uint32_t e = tid; e < a.n_ev; e += kFT) {
-            const DevEvent E = static_cast<const DevEvent*>(b.events)[e];
+            const DevEvent E = evs[e];
             const uint32_t s = (uint32_t)E.id & c.cap_mask;
             if (s >= s_lo && s < s_hi) apply_event(b.pool, c, E);
         }
@@ -1348,11 +1355,13 @@ int fused_blocks_per_sm() {
 
 uint32_t fused_max_buckets() { return kMaxBuckets; }
 
-cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t grid, cudaStream_t s) {
+cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t grid,
+                         cudaStream_t s) {
+    static const InlineStage kNone{};
     Bufs bb = b;
     Cost cc = c;
     StepArgs aa = a;
-    void* args[] = {&bb, &cc, &aa};
+    void* args[] = {&bb, &cc, &aa, const_cast<InlineStage*>(inl ? inl : &kNone)};
     const bool p2p = (a.flags & kStepP2P) != 0;
     const void* fn = p2p ? (b.dbg ? (const void*)k_fused<true, true> : (const void*)k_fused<false, true>)
                          : (b.dbg ? (const void*)k_fused<true, false> : (const void*)k_fused<false, false>);

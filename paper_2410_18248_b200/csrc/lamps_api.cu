@@ -98,6 +98,8 @@ struct lamps_s {
     uint32_t tune = 0;  // StepArgs.tune, from env LAMPS_TUNE (A/B measurements)
     uint32_t ret_pending = 0;  // API returns staged for the next fused step's prologue
     uint32_t sub_pending = 0;  // arrivals staged for the next fused step's prologue
+    bool inl_pending = false;  // ... staged in `inl` (the kernel's parameter block)
+    InlineStage inl{};
     nccl_comm_t comm = nullptr;
     uint8_t* ws = nullptr;
     // device ingest staging (inside the workspace)
@@ -375,6 +377,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.tune = h->tune;
     a.n_ret = h->fused ? h->ret_pending : 0u;
     a.n_sub = h->fused ? h->sub_pending : 0u;
+    a.inl = h->fused && h->inl_pending ? 1u : 0u;
     if (h->merge) a.flags |= kStepMerge;
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
         a.flags |= kStepP2P;
@@ -401,7 +404,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     if (!h->fused) CU(h, launch_events(h->b, h->cost, a, h->stream));  // fused: in the kernel's prologue
     record_timing(h, 1);
     if (h->fused) {
-        CU(h, launch_fused(h->b, h->cost, a, h->fused_grid, h->stream));
+        CU(h, launch_fused(h->b, h->cost, a, a.inl ? &h->inl : nullptr, h->fused_grid, h->stream));
         record_timing(h, 2);
         record_timing(h, 3);
     } else {
@@ -414,6 +417,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);  // P2P: the exchange and merge are in k_fused
     h->ret_pending = 0;
     h->sub_pending = 0;
+    h->inl_pending = false;
     return LAMPS_OK;
 }
 
@@ -676,6 +680,12 @@ void events_staged(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
 int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
     h->b.events = h->d_events;
     if (!n_ev) return LAMPS_OK;
+    if (h->fused && !h->ret_pending && !h->sub_pending && (size_t)n_ev * sizeof(lamps_event) <= kInlineStage) {
+        std::memcpy(h->inl.bytes, ev, (size_t)n_ev * sizeof(lamps_event));  // the kernel's parameters
+        h->inl_pending = true;
+        events_staged(h, ev, n_ev);
+        return LAMPS_OK;
+    }
     std::memcpy(h->h_ev, ev, (size_t)n_ev * sizeof(lamps_event));
     CU(h, cudaMemcpyAsync(const_cast<void*>(h->d_events), h->h_ev, (size_t)n_ev * sizeof(lamps_event),
                           cudaMemcpyHostToDevice, h->stream));
@@ -927,14 +937,19 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     if (int rc = check_submit(h, it->arrivals, na, aticks)) return rc;
     if (int rc = window_submit(h, na, nullptr, 0)) return rc;
     if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
-    // 2. API returns, arrivals and the events: on the fused path staged together (one copy)
-    //    and applied in the step kernel's prologue; otherwise returns and arrivals by their own
+    // 2. API returns, arrivals and the events: on the fused path staged together and applied
+    //    in the step kernel's prologue -- up to kInlineStage bytes inside the kernel's parameter
+    //    block (no copy), else with one copy; otherwise returns and arrivals by their own
     //    kernels before the step
     const size_t rbytes = (size_t)(nr + na) * sizeof(ReturnRec), ebytes = (size_t)ne * sizeof(lamps_event);
     bool ev_staged = false;
+    h->inl_pending = false;
     if (h->fused && rbytes + ebytes <= (size_t)kIngestChunk * sizeof(SubmitRec)) {
-        if (int rc = staging_wait(h)) return rc;
-        ReturnRec* rr = static_cast<ReturnRec*>(h->h_ingest);
+        const bool inl = rbytes + ebytes <= kInlineStage;
+        if (!inl) {
+            if (int rc = staging_wait(h)) return rc;
+        }
+        ReturnRec* rr = inl ? reinterpret_cast<ReturnRec*>(h->inl.bytes) : static_cast<ReturnRec*>(h->h_ingest);
         SubmitRec* sr = reinterpret_cast<SubmitRec*>(rr + nr);
         static_assert(sizeof(ReturnRec) == sizeof(SubmitRec), "one staging layout");
         for (uint32_t i = 0; i < nr; i++) {
@@ -962,7 +977,8 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
             r.pad = 0;
         }
         if (ne) std::memcpy(reinterpret_cast<uint8_t*>(rr) + rbytes, it->events, ebytes);  // 16 B aligned
-        if (rbytes + ebytes) {
+        h->inl_pending = inl;
+        if (!inl && rbytes + ebytes) {
             CU(h, cudaMemcpyAsync(h->d_ingest, rr, rbytes + ebytes, cudaMemcpyHostToDevice, h->stream));
             if (int rc = staging_copied(h)) return rc;
         }

@@ -87,12 +87,21 @@ struct StepArgs {
     uint32_t xseq;          // peer-memory exchange: sequence number of this step's exchange
     uint32_t n_ret;         // fused path: API returns staged at Bufs::returns, applied in the prologue
     uint32_t n_sub;         // fused path: arrivals staged at Bufs::arrivals, applied in the prologue
+    uint32_t inl;           // fused path: returns, arrivals, events read from the kernel's
+                            // InlineStage parameter (records in that order) instead of Bufs
     uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
                             // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
                             // instead of first-boundary snapping of the range ends, bit 3
                             // one-sided speed weights (capped at 1 instead of 1.25), bit 2 the
                             // bucket range sort also for ranges of <= 384 keys, bit 4 no
                             // sparse-bucket sort for the head range
+};
+
+// A small iteration's staging (API returns, arrivals, events) carried in the fused kernel's
+// parameter block: no copy operation before the launch.
+constexpr uint32_t kInlineStage = 2048;
+struct InlineStage {
+    alignas(16) unsigned char bytes[kInlineStage];
 };
 
 struct Bufs {
@@ -137,7 +146,8 @@ int sort_blocks_per_sm();  // occupancy of the persistent sort kernel
 size_t fused_smem_bytes();
 int fused_blocks_per_sm();
 uint32_t fused_max_buckets();
-cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, uint32_t grid, cudaStream_t s);
+cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t grid,
+                         cudaStream_t s);
 cudaError_t launch_merge(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 // merge scratch: sk, gid (8 B) and demand (4 B) per record of the W runs, 3 index arrays of K
 __host__ __device__ inline size_t merge_smem_bytes(uint32_t world, uint32_t K) {
