@@ -73,3 +73,60 @@ def test_iterate_rejects_atomically():
     for f in ("state", "ctx", "pre_rem", "cnt", "pending"):
         assert np.array_equal(before[f], after[f]), f
     s.close()
+
+
+def _segs(n, has_api=1, seed=0):
+    """n arrival segments in both record types (library, oracle), lengths varied by seed."""
+    rows = [dict(prompt_len=60 + (7 * k + seed) % 90, pre_len=3 + (5 * k + seed) % 11, has_api=has_api,
+                 api_seconds=0.25 + 0.125 * ((k + seed) % 5), resp_len=4 + k % 9, post_len=2 + (3 * k) % 7)
+            for k in range(n)]
+    return seg_rows_to_arrays(rows)
+
+
+# (API returns, arrivals, events) around the 2 KB staging carried in the kernel's parameter
+# block (32 B per return / arrival, 16 B per event): exactly 2048 B and one record more
+# (the copy path), each kind alone and mixed
+@pytest.mark.parametrize("n_ret,n_arr,n_ev", [(0, 64, 0), (0, 65, 0), (0, 0, 128), (0, 0, 129),
+                                              (30, 30, 8), (30, 30, 9), (64, 0, 0), (65, 0, 0), (1, 1, 1)])
+def test_iterate_staging_sizes(n_ret, n_arr, n_ev):
+    from paper_2410_18248_b200.lamps import EVENT_DTYPE
+    cfg = gen.lib_config("C3")
+    kv = 1 << 19  # every eligible request fits: admitted lists of up to max_batch (256)
+    s, o = make_pair(cfg, debug=False)
+    # 300 requests that call an API after a few tokens
+    a, b = _segs(300)
+    g, gids = s.iterate(arrivals=a, kv_total=kv)
+    rc, oids = o.submit(b)
+    assert rc == 0 and np.array_equal(gids, oids)
+    compare_outputs(s, g, o.step(None, kv), where="t0")
+    prev = g["admitted_id"]
+    # the first 100 admitted call their API (paused), the rest keep decoding
+    ev = np.zeros(100, EVENT_DTYPE)
+    ev["id"], ev["kind"] = prev[:100], 1
+    g, _ = s.iterate(events=ev, kv_total=kv)
+    compare_outputs(s, g, o.step(ev, kv), where="t1")
+    paused = [int(x) for x in ev["id"]]
+    prev = g["admitted_id"]
+    assert len(prev) >= n_ev
+    # the iteration under test: n_ret returns (next segment without an API), n_arr
+    # arrivals, n_ev finished requests of the previous batch
+    ret_ids = np.asarray(paused[:n_ret], np.uint64)
+    ra, rb = _segs(n_ret, has_api=0, seed=3)
+    resp = np.full(n_ret, 6, np.uint32)
+    aa, ab = _segs(n_arr, seed=5)
+    ev = np.zeros(n_ev, EVENT_DTYPE)
+    ev["id"], ev["kind"] = prev[:n_ev], 2
+    g, gids = s.iterate(events=ev, ret_ids=ret_ids, ret_resp=resp, ret_next=ra, arrivals=aa, kv_total=kv)
+    if n_ret:
+        assert o.api_return(ret_ids, resp, rb) == 0
+    if n_arr:
+        rc, oids = o.submit(ab)
+        assert rc == 0 and np.array_equal(gids, oids)
+    compare_outputs(s, g, o.step(ev, kv), where="t2")
+    compare_state(s, o, where="t2")
+    # and a plain step with events of the same size class (lamps_schedule_step)
+    ev2 = np.zeros(min(n_ev, len(g["admitted_id"])), EVENT_DTYPE)
+    ev2["id"], ev2["kind"] = g["admitted_id"][:len(ev2)], 2
+    compare_outputs(s, s.step(ev2, kv), o.step(ev2, kv), where="t3")
+    compare_state(s, o, where="t3")
+    s.close()
