@@ -268,7 +268,8 @@ def run_ours(args, rank, world, local):
         s.step_async(kv)
         ends[k].record(stream)
     barrier()
-    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+    per_step_ms = sorted(a.elapsed_time(b) for a, b in zip(starts, ends))
+    ms = sum(per_step_ms) / args.steps
     # the clock sampler (an nvidia-smi process) covered warm-up and the timed steps; it is
     # stopped here because its driver queries stall host-side CUDA calls, which the
     # host-timed e2e loop below would otherwise absorb
@@ -454,6 +455,11 @@ def run_ours(args, rank, world, local):
                       "us": round(trace_us["bucket_scatter"] + trace_us["barrier3"] + trace_us["range_sort"], 2)}
                      if trace_us else None),
             "pool_slots_per_s": world * cap / (ms_max / 1e3),
+            # this rank's per-step distribution (median and p99 of the step time)
+            "step_us": {"min": round(per_step_ms[0] * 1e3, 2),
+                        "median": round(per_step_ms[len(per_step_ms) // 2] * 1e3, 2),
+                        "p99": round(per_step_ms[min(len(per_step_ms) - 1, int(0.99 * len(per_step_ms)))] * 1e3, 2),
+                        "max": round(per_step_ms[-1] * 1e3, 2)},
             "path": ("fused cooperative step kernel" + (f" ({xdesc})" if merged else "")) if fused else "3-kernel path",
             "sort_passes": passes,
             "gpu_launches": kernels * args.steps,
