@@ -428,6 +428,10 @@ int lamps_predict(lamps_t* h, const lamps_truth* truth, uint32_t n, const lamps_
  * process that share one device (LAMPS_SHARE_DEVICE; the buffers are used directly).
  * Every rank must then call lamps_schedule_step the same number of times (the step
  * kernels wait for each other).  Errors: EINVAL (wrong transport / sizes), ECUDA.
+ * A step whose peers' records do not all arrive within LAMPS_P2P_TIMEOUT_MS milliseconds
+ * (environment variable read at lamps_init; default 10000) ends without admitting and
+ * returns LAMPS_ENCCL ("peer exchange timed out"): the ranks are out of lockstep (a peer
+ * died or stopped stepping) and the handles should be freed.
  */
 int lamps_p2p_handle(lamps_t* h, void* out64);
 int lamps_p2p_connect(lamps_t* h, const void* handles, size_t n_bytes);

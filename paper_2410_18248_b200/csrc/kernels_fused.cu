@@ -1296,15 +1296,32 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
             }
             if (xtr) xtr[1] = clock64();
         }
+        bool late = false;  // bounded wait: a peer that never steps must not hang the GPU
         if (tid < W) {
             const uint32_t* of = reinterpret_cast<const uint32_t*>(b.xown + nrec) + par * 32u + tid;
-            uint32_t v;
-            do {
+            unsigned long long t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            const unsigned long long lim = (unsigned long long)a.xtimeout_ms * 1000000ull;
+            for (uint32_t it = 1;; it++) {
+                uint32_t v;
                 if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(of) : "memory");
                 else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(of) : "memory");
-            } while (v != a.xseq);
+                if (v == a.xseq) break;
+                if (!(it & 255u)) {
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (t - t0 > lim) {
+                        late = true;
+                        break;
+                    }
+                }
+            }
         }
-        __syncthreads();
+        late = __syncthreads_or(late);
+        if (tid == 0) b.hres->xfail = late ? 1u : 0u;
+        if (late) {
+            TRACE(9);
+            return;
+        }
         TRACE(15);
         // merge scratch over sm.l.a (the head keys are no longer needed there: the admission
         // reads this rank's keys from b.keys), small structures at the end of shared memory.

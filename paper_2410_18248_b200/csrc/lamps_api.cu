@@ -95,6 +95,7 @@ struct lamps_s {
     std::vector<void*> peer_open;        // IPC mappings to close
     bool p2p_ready = false;
     uint32_t xseq = 0;
+    uint32_t xtimeout_ms = 10000;  // P2P: longest wait for the peers (env LAMPS_P2P_TIMEOUT_MS)
     uint32_t tune = 0;  // StepArgs.tune, from env LAMPS_TUNE (A/B measurements)
     uint32_t ret_pending = 0;  // API returns staged for the next fused step's prologue
     uint32_t sub_pending = 0;  // arrivals staged for the next fused step's prologue
@@ -383,6 +384,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         a.flags |= kStepP2P;
         if (h->world > 1 && !(h->cfg.flags & LAMPS_SHARE_DEVICE)) a.flags |= kStepP2PSys;
         a.xseq = h->xseq;
+        a.xtimeout_ms = h->xtimeout_ms;
     }
     if (h->cfg.flags & LAMPS_HEAD_ONLY) a.flags |= kStepHeadOnly;
     return a;
@@ -458,6 +460,8 @@ int fetch_result(lamps_t* h, lamps_step_out* out) {
     // the admission kernel wrote the summary and the lists into mapped host memory
     CU(h, cudaStreamSynchronize(h->stream));
     const HostRes& R = *h->hres;
+    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P && R.xfail)
+        return fail(h, LAMPS_ENCCL, "peer exchange timed out: a rank did not step (ranks out of lockstep)");
     const uint32_t par = h->step & 1u;
     const uint64_t* adm = h->h_adm_ids;
     h->prev_adm.assign(adm, adm + R.n_admitted);
@@ -749,6 +753,8 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
         return LAMPS_ENOTSUP;
     }
     if (const char* tv = std::getenv("LAMPS_TUNE")) h->tune = (uint32_t)std::strtoul(tv, nullptr, 0);
+    if (const char* xv = std::getenv("LAMPS_P2P_TIMEOUT_MS"))
+        h->xtimeout_ms = std::max<uint32_t>(1u, (uint32_t)std::strtoul(xv, nullptr, 0));
     h->world = cfg->world > 1 ? cfg->world : 1;
     h->rank = cfg->world > 1 ? cfg->rank : 0;
     h->merge = merge_mode(*cfg);

@@ -71,6 +71,7 @@ struct Ctl {
 struct HostRes {
     unsigned long long n_elig, pinned, budget, budget_used;
     uint32_t n_admitted, n_preempted, blocked_head, final_buf;
+    uint32_t xfail, pad;  // P2P: 1 = the peers' records did not arrive in time (no admission)
 };
 
 struct StepArgs {
@@ -85,6 +86,7 @@ struct StepArgs {
     uint32_t flags;         // kStepForceFallback, kStepMerge, kStepHeadOnly
     uint32_t world, rank;   // multi-GPU shards
     uint32_t xseq;          // peer-memory exchange: sequence number of this step's exchange
+    uint32_t xtimeout_ms;   // peer-memory exchange: longest wait for the peers' flags
     uint32_t n_ret;         // fused path: API returns staged at Bufs::returns, applied in the prologue
     uint32_t n_sub;         // fused path: arrivals staged at Bufs::arrivals, applied in the prologue
     uint32_t inl;           // fused path: returns, arrivals, events read from the kernel's

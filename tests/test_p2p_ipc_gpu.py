@@ -73,3 +73,57 @@ def test_p2p_two_processes():
     for p in ps:
         p.join(timeout=30)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def _worker_dead_peer(rank, world, port, q):
+    """Rank 1 connects but never steps: rank 0's step must end (bounded wait) with
+    LAMPS_ENCCL instead of hanging the GPU."""
+    try:
+        import time
+
+        import torch
+        import torch.distributed as dist
+
+        os.environ["LAMPS_P2P_TIMEOUT_MS"] = "300"
+        from paper_2410_18248_b200 import Scheduler
+        from paper_2410_18248_b200.lamps import LAMPS_ENCCL, LAMPS_XPORT_P2P
+        from shard_util import union_and_shards
+
+        dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        cfg_l, _, _, shards = union_and_shards("C2", world, 2048, 1800, max_batch=256)
+        s = Scheduler(cfg_l, world=world, rank=rank, transport=LAMPS_XPORT_P2P)
+        hs = [None] * world
+        dist.all_gather_object(hs, s.p2p_handle())
+        s.p2p_connect(hs)
+        s.import_pool(shards[rank], shards[rank]["id_base"], shards[rank]["next_id"])
+        if rank == 0:
+            t0 = time.time()
+            rc = s.step_rc(kv_total=1500)
+            dt = time.time() - t0
+            assert rc == LAMPS_ENCCL, rc
+            assert dt < 30, dt
+        dist.barrier()
+        s.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except BaseException as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.timeout(300)
+def test_p2p_dead_peer_times_out():
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    os.environ["PYTHONPATH"] = os.pathsep.join([here, os.path.dirname(here), os.environ.get("PYTHONPATH", "")])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_dead_peer, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=280) for _ in ps)
+    for p in ps:
+        p.join(timeout=30)
+    assert res == {0: "ok", 1: "ok"}, res
