@@ -214,6 +214,11 @@ def run_ours(args, rank, world, local):
                 hs = [None] * world
                 dist.all_gather_object(hs, s.p2p_handle())
                 s.p2p_connect(hs)
+                # one trial exchange (empty pool): the peers' stores must arrive (bounded
+                # wait in the kernel, LAMPS_ENCCL on timeout)
+                rc = s.step_rc(kv_total=0)
+                if rc != 0:
+                    raise RuntimeError(f"trial exchange failed ({rc})")
         except Exception as e:  # noqa: BLE001
             print(f"p2p transport unavailable ({e}); using NCCL", file=sys.stderr)
             if s is not None:
