@@ -186,9 +186,18 @@ def run_ours(args, rank, world, local):
     from paper_2410_18248_b200 import LAMPS_TIMING, Scheduler
     from paper_2410_18248_b200.lamps import EVENT_DTYPE, SEGMENT_DTYPE
 
+    # LAMPS_BENCH_OVERSUBSCRIBE=1 (testing the N > 1 code path on a one-GPU box): ranks share
+    # the devices and talk over gloo; the ranks' kernels are time-sliced, so times are not
+    # meaningful
+    oversub = os.environ.get("LAMPS_BENCH_OVERSUBSCRIBE") == "1"
+    if oversub:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cname = args.config
     cfg = gen.lib_config(cname)
     kv = gen.CONFIGS[cname]["kv_total"]
