@@ -342,25 +342,33 @@ def run_ours(args, rank, world, local):
     barrier()
     t0 = time.perf_counter()
     ne_e2e = 0
+    # the engine's buffers, reused every iteration (as a serving engine would)
+    ev_buf = np.zeros(4, EVENT_DTYPE)
+    ev_buf["kind"] = [2, 2, 1, 1]
+    ids_buf = np.zeros(2, np.uint64)
+    nxt = np.zeros(2, SEGMENT_DTYPE)
+    nxt["pre_len"], nxt["has_api"] = 50, 0
+    resp = np.full(2, 16, np.uint32)
+    segs = np.zeros(2, SEGMENT_DTYPE)
+    segs["prompt_len"], segs["pre_len"], segs["has_api"], segs["api_seconds"] = 300, 100, 1, 1.5
+    segs["resp_len"], segs["post_len"] = 64, 50
     for k in range(e2e_steps):
         # one engine iteration through lamps_iterate: API returns of requests paused earlier,
         # 2 new arrivals, and the step with the engine's report on the previous batch (2
-        # finish, 2 call their API) -- one staging copy, one kernel, one host synchronisation
-        ev = np.zeros(min(4, len(prev)), EVENT_DTYPE)
-        for j in range(len(ev)):
-            ev[j]["id"], ev[j]["kind"] = prev[j], 2 if j < 2 else 1
-        ids = np.asarray(paused[:2], np.uint64)
-        nxt = np.zeros(len(ids), SEGMENT_DTYPE)
-        nxt["pre_len"], nxt["has_api"] = 50, 0
-        resp = np.full(len(ids), 16, np.uint32)
-        paused = paused[2:]
-        segs = np.zeros(2, SEGMENT_DTYPE)
-        segs["prompt_len"], segs["pre_len"], segs["has_api"], segs["api_seconds"] = 300, 100, 1, 1.5
-        segs["resp_len"], segs["post_len"] = 64, 50
-        rc, out, _ = s.iterate_rc(events=ev, ret_ids=ids, ret_resp=resp, ret_next=nxt, arrivals=segs, kv_total=kv)
+        # finish, 2 call their API) -- staging in the kernel's parameter block, one kernel,
+        # one host synchronisation
+        ne = min(4, len(prev))
+        ev = ev_buf[:ne]
+        ev["id"] = prev[:ne]
+        nr = min(2, len(paused))
+        ids = ids_buf[:nr]
+        ids[:] = paused[:nr]
+        paused = paused[nr:]
+        rc, out, _ = s.iterate_rc(events=ev, ret_ids=ids, ret_resp=resp[:nr], ret_next=nxt[:nr], arrivals=segs,
+                                  kv_total=kv)
         if rc != 0:
             raise RuntimeError(f"lamps_iterate failed ({rc})")
-        h2d += ev.nbytes + ids.nbytes + resp.nbytes + nxt.nbytes + segs.nbytes
+        h2d += ev.nbytes + ids.nbytes + resp[:nr].nbytes + nxt[:nr].nbytes + segs.nbytes
         paused += [int(x) for x in ev["id"][2:]]
         d2h += 64 + 9 * out["n_admitted"] + 8 * out["n_preempted"]
         ne_e2e += out["n_eligible"]

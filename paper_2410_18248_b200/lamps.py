@@ -76,6 +76,10 @@ class lamps_iteration(ctypes.Structure):
                 ("reserved", u32), ("arrival_ids_out", vp), ("kv_total_blocks", u64)]
 
 
+_NO_IDS = np.zeros(0, np.uint64)
+_NO_IDS.flags.writeable = False
+
+
 class lamps_noise(ctypes.Structure):
     _fields_ = [("seed", u64), ("len_error_ppm", u32), ("api_error_ppm", u32)]
 
@@ -136,7 +140,8 @@ class LampsError(RuntimeError):
 
 
 def _p(a):
-    return None if a is None else a.ctypes.data_as(vp)
+    # the raw address (the caller keeps the array alive across the call)
+    return None if a is None else a.ctypes.data
 
 
 # ---- thin wrappers with the C names (return codes, no exceptions) ----------
@@ -212,6 +217,7 @@ class Scheduler:
             raise LampsError(rc, "lamps_init failed")
         self.h = h
         self._out = lamps_step_out()
+        self._it = lamps_iteration()
 
     def _check(self, rc):
         if rc != LAMPS_OK:
@@ -309,23 +315,30 @@ class Scheduler:
                    kv_total: int = 0):
         """lamps_iterate: API returns, one step with the events, arrivals -- one sync.
         Returns (rc, result dict or None, arrival ids)."""
-        it = lamps_iteration()
+        it = self._it  # one struct per handle, every field set on each call
         keep = []
         if events is not None and len(events):
             ev = np.ascontiguousarray(events, EVENT_DTYPE); keep.append(ev)
             it.events, it.n_events = _p(ev), len(ev)
+        else:
+            it.events, it.n_events = None, 0
         if ret_ids is not None and len(ret_ids):
             ri = np.ascontiguousarray(ret_ids, np.uint64)
             rr = np.ascontiguousarray(ret_resp, np.uint32)
             rn = np.ascontiguousarray(ret_next, SEGMENT_DTYPE)
             keep += [ri, rr, rn]
             it.return_ids, it.return_resp, it.return_next, it.n_returns = _p(ri), _p(rr), _p(rn), len(ri)
-        ids = np.zeros(0, np.uint64)
+        else:
+            it.return_ids = it.return_resp = it.return_next = None
+            it.n_returns = 0
+        ids = _NO_IDS
         if arrivals is not None and len(arrivals):
             ar = np.ascontiguousarray(arrivals, SEGMENT_DTYPE)
             ids = np.zeros(len(ar), np.uint64)
             keep += [ar, ids]
             it.arrivals, it.n_arrivals, it.arrival_ids_out = _p(ar), len(ar), _p(ids)
+        else:
+            it.arrivals, it.n_arrivals, it.arrival_ids_out = None, 0, None
         it.kv_total_blocks = int(kv_total)
         rc = lib().lamps_iterate(self.h, ctypes.byref(it), ctypes.byref(self._out))
         return rc, (self._result(self._out) if rc == LAMPS_OK else None), ids
