@@ -683,6 +683,7 @@ void events_staged(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
 // events: staged to the device, liveness shadow updated
 int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
     h->b.events = h->d_events;
+    if (!h->ret_pending && !h->sub_pending) h->inl_pending = false;  // no stale inline staging
     if (!n_ev) return LAMPS_OK;
     if (h->fused && !h->ret_pending && !h->sub_pending && (size_t)n_ev * sizeof(lamps_event) <= kInlineStage) {
         std::memcpy(h->inl.bytes, ev, (size_t)n_ev * sizeof(lamps_event));  // the kernel's parameters
@@ -697,10 +698,21 @@ int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
     return LAMPS_OK;
 }
 
+// the step's own preconditions, checked before anything is staged (so that a rejected
+// step leaves the handle unchanged; after staging only a CUDA error can fail it)
+int step_precheck(lamps_t* h) {
+    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P && !h->p2p_ready)
+        return fail(h, LAMPS_EINVAL, "P2P transport: call lamps_p2p_connect first");
+    if ((h->cfg.flags & LAMPS_TIMING) && h->t_count == kTimingRing)
+        return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
+    return LAMPS_OK;
+}
+
 // host-side part of a step: validate the events against the previous admitted
 // list, stage them to the device, update the liveness shadow (state unchanged on error)
 int prepare_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64_t kv_total_blocks) {
     if (int rc = check_events(h, ev, n_ev, kv_total_blocks)) return rc;
+    if (int rc = step_precheck(h)) return rc;
     return stage_events(h, ev, n_ev);
 }
 
@@ -943,6 +955,7 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     if (int rc = check_submit(h, it->arrivals, na, aticks)) return rc;
     if (int rc = window_submit(h, na, nullptr, 0)) return rc;
     if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
+    if (int rc = step_precheck(h)) return rc;  // once staged, the ingest must launch
     // 2. API returns, arrivals and the events: on the fused path staged together and applied
     //    in the step kernel's prologue -- up to kInlineStage bytes inside the kernel's parameter
     //    block (no copy), else with one copy; otherwise returns and arrivals by their own

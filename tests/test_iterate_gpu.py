@@ -130,3 +130,43 @@ def test_iterate_staging_sizes(n_ret, n_arr, n_ev):
     compare_outputs(s, s.step(ev2, kv), o.step(ev2, kv), where="t3")
     compare_state(s, o, where="t3")
     s.close()
+
+
+def test_rejected_step_leaves_handle_unchanged():
+    """A step refused for its own preconditions (here: the timing ring is full) is refused
+    before anything is staged: the pool and the host shadow are unchanged, and the same
+    iteration then runs exactly as on a twin handle that never saw the refusal (the inline
+    staging of the refused call must not leak into the next one)."""
+    from paper_2410_18248_b200 import LAMPS_TIMING, Scheduler
+    from paper_2410_18248_b200.lamps import EVENT_DTYPE, LAMPS_EINVAL
+    cfg = gen.lib_config("C2")
+    snap = gen.snapshot("C2", seed=4, id_base=11)
+    kv = 1 << 19  # full batches (max_batch admitted), so 200 events exceed the 2 KB inline staging
+    s, t = Scheduler(cfg, flags=LAMPS_TIMING), Scheduler(cfg)
+    for h in (s, t):
+        h.import_pool(snap, snap["id_base"], snap["next_id"])
+    g = s.step(kv_total=kv)
+    assert np.array_equal(g["admitted_id"], t.step(kv_total=kv)["admitted_id"])
+    for _ in range(4095):  # fill the timing ring (4096 entries)
+        s.step_async(kv)
+        t.step_async(kv)
+    gs, gt = s.result(), t.result()
+    assert np.array_equal(gs["admitted_id"], gt["admitted_id"])
+    before = s.export_pool()
+    small = np.zeros(2, EVENT_DTYPE)
+    small["id"], small["kind"] = gs["admitted_id"][:2], 2
+    assert s.step_rc(small, kv) == LAMPS_EINVAL  # ring full
+    rc, _, _ = s.iterate_rc(events=small, kv_total=kv)
+    assert rc == LAMPS_EINVAL
+    after = s.export_pool()
+    for f in ("state", "ctx", "pre_rem", "cnt", "pending"):
+        assert np.array_equal(before[f], after[f]), f
+    s.timing()  # drain
+    assert len(gs["admitted_id"]) >= 200
+    big = np.zeros(200, EVENT_DTYPE)  # 3200 B > 2 KB: the copy path
+    big["id"], big["kind"] = gs["admitted_id"][:len(big)], 1
+    a, b = s.step(big, kv), t.step(big, kv)
+    for k in ("n_eligible", "n_admitted", "n_preempted", "budget_used"):
+        assert a[k] == b[k], k
+    assert np.array_equal(a["admitted_id"], b["admitted_id"])
+    s.close(); t.close()
