@@ -393,11 +393,11 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
 // phase 1: events, scoring, ranking (and, single shard, admission)
 int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     const bool timing = (h->cfg.flags & LAMPS_TIMING) != 0;
-    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
-        if (!h->p2p_ready) return fail(h, LAMPS_EINVAL, "P2P transport: call lamps_p2p_connect first");
-        h->xseq++;  // every rank steps in lockstep, so the sequence numbers agree
-    }
+    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P && !h->p2p_ready)
+        return fail(h, LAMPS_EINVAL, "P2P transport: call lamps_p2p_connect first");
     if (timing && h->t_count == kTimingRing) return fail(h, LAMPS_EINVAL, "timing ring full: call lamps_timing_read");
+    // after every check: every rank steps in lockstep, so the sequence numbers agree
+    if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) h->xseq++;
     if (h->have_result && h->fetched_step != h->step) h->shadow_ok = false;  // an unread admitted list
     h->step++;
     const StepArgs a = make_args(h, kv_total, n_ev);
@@ -700,7 +700,11 @@ int stage_events(lamps_t* h, const lamps_event* ev, uint32_t n_ev) {
 
 // the step's own preconditions, checked before anything is staged (so that a rejected
 // step leaves the handle unchanged; after staging only a CUDA error can fail it)
-int step_precheck(lamps_t* h) {
+int step_precheck(lamps_t* h, bool group = false) {
+    if (!group && h->world > 1 && h->cfg.transport == LAMPS_XPORT_LOOPBACK)
+        return fail(h, LAMPS_EINVAL, "loopback shards step together: use lamps_group_step");
+    if (!group && h->world > 1 && (h->cfg.flags & LAMPS_SHARE_DEVICE))
+        return fail(h, LAMPS_EINVAL, "ranks sharing one device step together: use lamps_group_step");
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P && !h->p2p_ready)
         return fail(h, LAMPS_EINVAL, "P2P transport: call lamps_p2p_connect first");
     if ((h->cfg.flags & LAMPS_TIMING) && h->t_count == kTimingRing)
@@ -946,8 +950,7 @@ int lamps_schedule_step(lamps_t* h, const lamps_event* ev, uint32_t n_ev, uint64
 
 int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     if (!h || !it) return LAMPS_EINVAL;
-    if (h->world > 1 && h->cfg.transport == LAMPS_XPORT_LOOPBACK)
-        return fail(h, LAMPS_EINVAL, "loopback shards step together: use lamps_group_step");
+    if (int rc = step_precheck(h)) return rc;  // world > 1 refusals etc. before any host work
     const uint32_t nr = it->n_returns, ne = it->n_events, na = it->n_arrivals;
     // 1. everything is validated before anything is applied
     std::vector<uint32_t> rticks, rctx, aticks;
@@ -955,7 +958,6 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     if (int rc = check_submit(h, it->arrivals, na, aticks)) return rc;
     if (int rc = window_submit(h, na, nullptr, 0)) return rc;
     if (int rc = check_events(h, it->events, ne, it->kv_total_blocks)) return rc;
-    if (int rc = step_precheck(h)) return rc;  // once staged, the ingest must launch
     // 2. API returns, arrivals and the events: on the fused path staged together and applied
     //    in the step kernel's prologue -- up to kInlineStage bytes inside the kernel's parameter
     //    block (no copy), else with one copy; otherwise returns and arrivals by their own
@@ -1043,9 +1045,15 @@ int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* cons
                     (r && hs[r]->stream == hs[0]->stream)))
             return fail(hs[0], LAMPS_EINVAL, "group: P2P handles need LAMPS_SHARE_DEVICE and one stream each");
     }
+    // two passes: every shard is validated before any shard is staged, so a refused shard
+    // leaves every handle unchanged (staging itself can fail only on a CUDA error)
     for (uint32_t r = 0; r < world; r++) {
-        int rc = prepare_step(hs[r], ev ? ev[r] : nullptr, n_ev[r], kv_total[r]);
-        if (rc) return rc;  // earlier shards were validated and staged only (no kernel ran yet)
+        if (int rc = check_events(hs[r], ev ? ev[r] : nullptr, n_ev[r], kv_total[r])) return rc;
+        if (int rc = step_precheck(hs[r], true)) return rc;
+    }
+    for (uint32_t r = 0; r < world; r++) {
+        int rc = stage_events(hs[r], ev ? ev[r] : nullptr, n_ev[r]);
+        if (rc) return rc;
     }
     for (uint32_t r = 0; r < world; r++) {
         int rc = enqueue_phase1(hs[r], kv_total[r], n_ev[r]);
@@ -1117,6 +1125,7 @@ int lamps_schedule_step_async(lamps_t* h, uint64_t kv_total_blocks) {
     if (!h) return LAMPS_EINVAL;
     if (kv_total_blocks > h->cfg.kv_capacity_blocks)
         return fail(h, LAMPS_EINVAL, "kv_total_blocks exceeds kv_capacity_blocks");
+    if (int rc0 = step_precheck(h)) return rc0;  // before enqueue_phase1 bumps the exchange sequence
     int rc = enqueue_step(h, kv_total_blocks, 0);
     if (rc) return rc;
     h->prev_known = false;
@@ -1152,6 +1161,11 @@ int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uin
                  ((io->age ? io->age[s] : 0u) << SFC_AGE_SHIFT) | ((io->dirty ? io->dirty[s] : 1u) ? SFC_DIRTY : 0u);
         hs[s] = st == LAMPS_READY ? H_READY : H_PAUSED;
     }
+    // ingest staged by a failed lamps_iterate must not reach the imported pool
+    if (int rc = staging_wait(h)) return rc;
+    h->ret_pending = 0;
+    h->sub_pending = 0;
+    h->inl_pending = false;
     const Pool& P = h->b.pool;
     const uint32_t* src[6] = {io->ctx, io->pre_rem, io->api_ticks, io->resp_len, io->post_len, io->pending};
     uint32_t* dst[6] = {P.ctx, P.pre, P.api, P.resp, P.post, P.pend};

@@ -151,3 +151,80 @@ def test_p2p_self_exchange_world1():
 def test_p2p_merge_head_only():
     """F3 head-only ranking on every rank + the peer-memory exchange: the same global batch."""
     run("C2", 2, 2048, 1800, 3000, max_batch=256, p2p=True, head_only=True, steps=4)
+
+
+def _p2p_group(cfg, world):
+    import torch
+    from paper_2410_18248_b200 import Scheduler
+    from paper_2410_18248_b200.lamps import LAMPS_SHARE_DEVICE, LAMPS_XPORT_P2P
+    S = [Scheduler(cfg, world=world, rank=r, transport=LAMPS_XPORT_P2P, flags=LAMPS_SHARE_DEVICE,
+                   stream=torch.cuda.Stream()) for r in range(world)]
+    Scheduler.p2p_connect_local(S)
+    return S
+
+
+def test_shared_device_rank_iterate_refused_before_staging():
+    """lamps_iterate on a world>1 LAMPS_SHARE_DEVICE rank is refused before any
+    return / arrival is staged -- pool, id window and the next group step are unchanged."""
+    from paper_2410_18248_b200.lamps import LAMPS_EINVAL
+    cfg_l, cfg_u, u, shards = union_and_shards("C2", 2, 2048, 1800)
+    S, T = _p2p_group(cfg_l, 2), _p2p_group(cfg_l, 2)
+    for G in (S, T):
+        for r in range(2):
+            G[r].import_pool(shards[r], shards[r]["id_base"], shards[r]["next_id"])
+    kvs = split_kv(3000, 2)
+    before = S[0].export_pool()
+    arr = S[0].segments([dict(prompt_len=50, pre_len=10, resp_len=5, post_len=7, api_seconds=0.5,
+                              has_api=1)] * 3)
+    rc, out, ids = S[0].iterate_rc(arrivals=arr, kv_total=kvs[0])
+    assert rc == LAMPS_EINVAL and out is None
+    after = S[0].export_pool()
+    for f in FIELDS:
+        assert np.array_equal(before[f], after[f]), f
+    a = type(S[0]).group_step(S, None, kvs)
+    b = type(S[0]).group_step(T, None, kvs)
+    for r in range(2):
+        assert np.array_equal(a[r]["admitted_id"], b[r]["admitted_id"])
+    # the id window did not move: the next arrivals get the same ids on both groups
+    sa = S[0].submit(arr)
+    sb = T[0].submit(arr)
+    assert np.array_equal(sa, sb)
+    for s in S + T:
+        s.close()
+
+
+def test_group_step_refused_shard_stages_nothing():
+    """a group step in which one shard's events are invalid is refused before any
+    shard is staged; the same group then steps exactly like a twin that never saw the call."""
+    from paper_2410_18248_b200 import Scheduler
+    from paper_2410_18248_b200.lamps import EVENT_DTYPE, LampsError, LAMPS_XPORT_LOOPBACK
+    import torch
+    cfg_l, cfg_u, u, shards = union_and_shards("C2", 2, 2048, 1800)
+    stream = torch.cuda.current_stream()
+    G = [[Scheduler(cfg_l, world=2, rank=r, transport=LAMPS_XPORT_LOOPBACK, stream=stream) for r in range(2)]
+         for _ in range(2)]
+    for S in G:
+        for r in range(2):
+            S[r].import_pool(shards[r], shards[r]["id_base"], shards[r]["next_id"])
+    kvs = split_kv(3000, 2)
+    first = [Scheduler.group_step(S, None, kvs) for S in G]
+    ev = []
+    for r in range(2):
+        e = np.zeros(2, EVENT_DTYPE)
+        e["id"], e["kind"] = first[0][r]["admitted_id"][:2], 2  # FINISHED
+        ev.append(e)
+    bad = [ev[0], ev[1].copy()]
+    bad[1]["id"][0] = 1 << 40  # not admitted by shard 1's previous step
+    with pytest.raises(LampsError):
+        Scheduler.group_step(G[0], bad, kvs)
+    for S in G:  # shard 0's FINISHED events must not have been half-applied
+        out = Scheduler.group_step(S, ev, kvs)
+        S.append(out)
+    for r in range(2):
+        assert np.array_equal(G[0][2][r]["admitted_id"], G[1][2][r]["admitted_id"])
+        e0, e1 = G[0][r].export_pool(), G[1][r].export_pool()
+        for f in FIELDS:
+            assert np.array_equal(e0[f], e1[f]), (r, f)
+    for S in G:
+        for s in S[:2]:
+            s.close()
