@@ -19,6 +19,8 @@
 //      near-equal scores) every CTA runs the grid-synchronous global LSD sort
 //      instead (sort_dev.cuh).
 //   A  CTA 0 admits (A5) as soon as the head of the order it needs is sorted.
+#include <algorithm>
+
 #include "merge_dev.cuh"
 #include "sort_dev.cuh"
 #include "step_dev.cuh"
@@ -30,27 +32,30 @@ namespace {
 constexpr int kFT = 1024;                   // threads per CTA
 constexpr int kFW = kFT / 32;               // warps
 constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
-#ifndef LAMPS_BUCKET_M  // A/B builds: scripts/build_variant.sh out.so -DLAMPS_BUCKET_M=...
-#define LAMPS_BUCKET_M 7
-#endif
-constexpr int kBucketM = LAMPS_BUCKET_M;                 // score bits per octave
-constexpr int kMaxBuckets = 2 * (64 - kBucketM + 1) << kBucketM;  // 14848
+constexpr int kMaxBuckets = 14848;          // bucket table capacity (bucket_t, bt_update)
+constexpr int kTabW = 136;                  // bucket table: [0, 130) octave entries, [130] bucket count
+constexpr uint32_t kTabNB = 130;
 constexpr int kLocalItems = kKcap / kFT;    // 10
 constexpr int kMaxCtas = 256;               // range weights: grid size limit
+// splitters in shared memory: entry i at i + i / 16 (no bank conflicts in the binary search,
+// whose steps read the odd multiples of 128, 64, ... -- same banks without the padding)
+constexpr int kSplPad = kMaxCtas + 1 + (kMaxCtas + 1) / 16 + 1;
+__host__ __device__ constexpr uint32_t spl_pos(uint32_t i) { return i + (i >> 4); }
+constexpr int kSplG = 264;  // global splitters per parity: [0, 256) splitters, [256] the largest key
 
-struct PhaseS {                  // S, H, T, X
-    uint64_t kbuf[kKcap];        // 96 KB: this CTA's keys
-    uint32_t cnt[kMaxBuckets];   // 58 KB: bucket counts -> scatter cursors
-    uint32_t start[kMaxBuckets]; // 58 KB: bucket totals -> bucket start positions
+struct PhaseS {                  // S, H, X (cold), R
+    uint64_t kbuf[kKcap];        // 80 KB: this CTA's keys (compacted, in no particular order)
+    uint32_t cnt[kMaxBuckets];   // 58 KB: bucket counts (cold); R: with start, the keys sorted by range
+    uint32_t start[kMaxBuckets]; // 58 KB: bucket totals -> bucket start positions (cold)
     uint32_t w32[kFW + 1];
     unsigned long long red[3][kFW];
-    uint32_t vmask[kKcap / 32];  // S: which kbuf positions (slots) hold keys
     uint32_t nk, base;
-    unsigned long long mbar[2];  // S: TMA completion barriers of the two stage buffers
-    uint32_t hb_j, hb_r;         // head-only mode: first bucket past the head, its start
+    uint32_t vmask[kKcap / 32];  // S: which kbuf positions hold keys
     float ccost[kMaxCtas];       // range-sort cycles per key of each CTA (previous steps)
     uint32_t rb[kMaxCtas + 1], jb[kMaxCtas + 1];  // X: key / bucket boundaries of the ranges
     float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
+    alignas(16) unsigned long long spl[kSplPad];  // R: range r = keys in [spl[P(r)], spl[P(r + 1)]), P = spl_pos
+    uint32_t lcnt[kMaxCtas + 1], lst[kMaxCtas + 1], gbase[kMaxCtas];  // R: this CTA's run per range
 };
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
@@ -83,11 +88,15 @@ struct PhaseL {                  // L
     unsigned long long gor[kMaxBig / 4], gand[kMaxBig / 4];
     unsigned long long red[2][kFW];
     AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
+    uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size (bit 31: overflow) and position
 };
-union FusedSmem {
-    PhaseS s;
-    PhaseL l;
-    SortSmem g;
+struct FusedSmem {
+    union {
+        PhaseS s;
+        PhaseL l;
+        SortSmem g;
+    };
+    alignas(16) uint32_t btab[kTabW];  // this step's bucket table (bucket_t), every phase
 };
 // After the union, untouched by every phase: the peer-memory exchange's state (peer
 // buffer pointers, prefetched at kernel start) and the in-kernel merge's small structures.
@@ -100,20 +109,62 @@ struct SmemTail {
 constexpr size_t kFusedSmemBytes = sizeof(FusedSmem) + ((sizeof(SmemTail) + 127) & ~(size_t)127);
 
 // Bucket of a key: (starving flag, bit length e of v = the key's score|id bits, the
-// next kBucketM bits of v) -- a float-like, exact monotone function of the key.  Over
-// v rather than the score alone, so keys whose scores are equal or small (FCFS: all 0)
-// still spread by id.
-__device__ __forceinline__ uint32_t bucket_of(uint64_t key, const Cost& c, uint32_t half) {
-    const uint32_t vb = c.SB + c.IB;
-    const uint32_t ns = (uint32_t)(key >> vb) & 1u;  // 1 = not starving
+// next m_e bits of v) -- a float-like, exact monotone function of the key whose
+// resolution m_e per octave (ns, e) comes from a table: entry ns*65+e = base | s << 16 |
+// m << 24 (s = e-1-m: the low bits of v the bucket leaves free), bucket = base + the m
+// bits of v below its leading one.  Over v rather than the score alone, so keys whose
+// scores are equal or small (FCFS: all 0) still spread by id.  The table adapts to the
+// key distribution: every step writes the next step's table from its own octave counts
+// (bt_update), so buckets hold about the same number of keys; any valid table gives the
+// same order (only the balance of the ranges depends on it).
+__device__ __forceinline__ uint32_t bucket_t(uint64_t key, const uint32_t* tab, uint32_t vb, uint32_t& sv) {
+    const uint32_t ns = (uint32_t)(key >> vb) & 1u;
     const uint64_t v = key & ((1ull << vb) - 1ull);
     const uint32_t e = 64u - (uint32_t)__clzll((long long)v);  // bit length
-    uint32_t fb;
-    if (e <= (uint32_t)kBucketM)
-        fb = (uint32_t)v;
-    else
-        fb = ((e - kBucketM) << kBucketM) + (uint32_t)((v >> (e - 1 - kBucketM)) & ((1u << kBucketM) - 1));
-    return ns * half + fb;
+    const uint32_t t = tab[ns * 65u + e];
+    sv = (t >> 16) & 63u;
+    return (t & 0xffffu) + ((uint32_t)(v >> sv) & ((1u << (t >> 24)) - 1u));
+}
+
+// Next step's table from this step's bucket starts (exclusive scan `start` over the NB
+// buckets of the current table `tab`, n keys): octave o gets 2^m' buckets with
+// m' = floor(log2(n_o * kTabTarget / n)) (at least 1 bucket, at most 2^min(14, e-1)),
+// empty octaves 2 buckets; bases are the prefix of the spans in (ns, e) order.  The
+// total stays <= kTabTarget + 2 * 130 <= kMaxBuckets.  One warp.
+constexpr uint32_t kTabTarget = 12288;
+__device__ __forceinline__ void bt_update(const uint32_t* tab, const uint32_t* start, uint32_t n, uint32_t vb,
+                                          uint32_t* out) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t NB = tab[kTabNB];
+    uint32_t carry = 0;
+    for (uint32_t o0 = 0; o0 < kTabNB; o0 += 32) {
+        const uint32_t o = o0 + lane;
+        const uint32_t e = o % 65u;
+        const bool valid = o < kTabNB && e <= vb;
+        uint32_t span = 0, mq = 0;
+        if (valid) {
+            const uint32_t t = tab[o], base = t & 0xffffu, sp0 = 1u << (t >> 24);
+            const uint32_t s0 = base < NB ? start[base] : n, s1 = base + sp0 < NB ? start[base + sp0] : n;
+            const uint32_t no = s1 - s0, cap_m = e >= 1u ? min(14u, e - 1u) : 0u;
+            if (no == 0) {
+                mq = min(cap_m, 1u);
+            } else {
+                const uint64_t want = (uint64_t)no * kTabTarget / (n ? n : 1u);
+                mq = want <= 1 ? 0u : min(cap_m, 63u - (uint32_t)__clzll((long long)want));
+            }
+            span = 1u << mq;
+        }
+        uint32_t x = span;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= (uint32_t)d) x += y;
+        }
+        const uint32_t base = carry + x - span;
+        if (o < kTabNB) out[o] = valid ? (base | ((e >= 1u ? e - 1u - mq : 0u) << 16) | (mq << 24)) : base;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) out[kTabNB] = carry;
 }
 
 // Stable LSD sort of the n (<= kKcap) keys at src[0..n) in shared memory over the
@@ -435,26 +486,21 @@ __device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf
 #undef LTRACE
 }
 
-// Digit of key k inside its bucket J: the top db bits of the bits below those the
-// bucket fixes.  A bucket with exponent e > kBucketM fixes the score's top
-// kBucketM + 1 bits, so the varying part is (low e-1-kBucketM score bits, id
-// offset); an exact bucket (score < 2^kBucketM) varies only in the id offset.  The
-// id offset (id - id_base, the key's low bits) is < cap = 2^lg_cap, so it is packed
-// into lg_cap bits (not IB) and its top bits carry information.  Monotone in the key
-// within a bucket, so (bucket, digit) order is key order.
-__device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t db, const Cost& c,
-                                              uint32_t half, uint32_t lg_cap) {
-    const uint32_t fb = J >= half ? J - half : J;
-    if (fb < (1u << kBucketM)) return 0u;  // exact bucket: one key
-    const uint32_t ls = (fb >> kBucketM) - 1u;  // varying low bits of v: e - 1 - kBucketM
+// Digit of key k inside its bucket: the top db bits of the sv low bits of v the bucket
+// leaves free (sv from bucket_t), i.e. (low score bits, id offset).  The id offset
+// (id - id_base, the key's low IB bits) is < cap = 2^lg_cap, so it is packed into lg_cap
+// bits (not IB) and its top bits carry information.  Monotone in the key within a
+// bucket, so (bucket, digit) order is key order.
+__device__ __forceinline__ uint32_t sub_digit_t(uint64_t k, uint32_t sv, uint32_t db, const Cost& c,
+                                                uint32_t lg_cap) {
     const uint64_t idoff = k & (uint64_t)c.cap_mask;
     uint64_t v;
     uint32_t wv;
-    if (ls > c.IB) {  // varying score bits, then the id offset packed into lg_cap bits
-        v = (((k >> c.IB) & ((1ull << (ls - c.IB)) - 1ull)) << lg_cap) | idoff;
-        wv = ls - c.IB + lg_cap;
+    if (sv > c.IB) {  // varying score bits, then the id offset packed into lg_cap bits
+        v = (((k >> c.IB) & ((1ull << (sv - c.IB)) - 1ull)) << lg_cap) | idoff;
+        wv = sv - c.IB + lg_cap;
     } else {          // id bits only; those above lg_cap are always 0
-        wv = ls < lg_cap ? ls : lg_cap;
+        wv = sv < lg_cap ? sv : lg_cap;
         v = idoff & ((1ull << wv) - 1ull);
     }
     return wv >= db ? (uint32_t)(v >> (wv - db)) : (uint32_t)(v << (db - wv));
@@ -474,6 +520,7 @@ __device__ __forceinline__ uint32_t sub_digit(uint64_t k, uint32_t J, uint32_t d
 // dependent global round trip.  Returns whether those arrays are valid (not after a
 // refinement pass, which moves keys).
 constexpr uint32_t kHeadPre = 2560;
+constexpr uint32_t kHeadMargin = 128;   // the head range: max_batch + this many keys of the previous order
 // range_sort ranks sub-buckets of up to this many keys by comparison (one thread per
 // key, O(size) shared-memory reads): cheaper than a refinement pass for the few
 // sub-buckets of near-equal keys (e.g. saturated scores) a range may hold
@@ -488,8 +535,8 @@ static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
 // admission stay in flight in registers for the whole sort)
 template <int NI, bool HEAD>
 __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
-                                           const uint32_t* T, uint32_t j_lo, uint32_t j_hi, const Cost& c,
-                                           uint32_t half, unsigned long long* tr, const Pool* pool = nullptr,
+                                           uint32_t j_lo, uint32_t j_hi, const Cost& c,
+                                           const uint32_t* tab, unsigned long long* tr, const Pool* pool = nullptr,
                                            uint32_t id_base_mod = 0) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x;
@@ -519,12 +566,29 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
             }
         }
     }
+    // the bucket of every key (kept in registers: J - j_lo | sv << 16) and the range's own
+    // bucket counts (a bucket may straddle two ranges)
+    for (uint32_t j = tid; j <= nb; j += kFT) P[j] = 0;
+    if (tid == 0) sm.ngl[0] = 0;
+    __syncthreads();
+    uint32_t jv[NI];
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        const uint32_t i = tid + (uint32_t)u * kFT;
+        jv[u] = 0;
+        if (i < rn) {
+            uint32_t sv;
+            const uint32_t J = bucket_t(k[u], tab, c.SB + c.IB, sv) - j_lo;
+            jv[u] = J | (sv << 16);
+            atomicAdd(&P[J], 1u);
+        }
+    }
+    __syncthreads();
     for (uint32_t j = tid; j < nb; j += kFT) {
-        const uint32_t m = __ldcg(&T[j_lo + j]);
+        const uint32_t m = P[j];
         const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
         P[j] = m | ((m ? 1u << db : 0u) << 14);  // empty buckets take no counters: ncnt < 2 rn
     }
-    if (tid == 0) sm.ngl[0] = 0;
     __syncthreads();
     const uint32_t ptot = smem_excl_scan<kFT, kSubBuckets / kFT + 1>(P, nb, sm.w32);
     const uint32_t ncnt = ptot >> 14;
@@ -538,11 +602,11 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
         const uint32_t i = tid + (uint32_t)u * kFT;
         it[u] = 0;
         if (i < rn) {
-            const uint32_t J = bucket_of(k[u], c, half);
-            const uint32_t p0 = P[J - j_lo], p1 = P[J - j_lo + 1];
+            const uint32_t J = jv[u] & 0xffffu, sv = jv[u] >> 16;
+            const uint32_t p0 = P[J], p1 = P[J + 1];
             const uint32_t m = (p1 & 0x3fffu) - (p0 & 0x3fffu);
             const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
-            const uint32_t idx = (p0 >> 14) + sub_digit(k[u], J, db, c, half, lg_cap);
+            const uint32_t idx = (p0 >> 14) + sub_digit_t(k[u], sv, db, c, lg_cap);
             it[u] = idx | (atomicAdd(&cnt[idx], 1u) << 15);
         }
     }
@@ -623,6 +687,94 @@ __device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restric
     return dw_ok;
 }
 
+// Sort of a CTA's key range (rn <= kKcap keys at src, global) into sm.a with one counting
+// pass on a LINEAR digit of the key, d = (k - kmin) >> sh, over 2^ceil(log2 rn) counters
+// spanning [kmin, kmax] of the range's own keys: a range between two quantiles of the order
+// holds keys of about one octave, spread about evenly, so a counter holds ~1 key.  Keys of a
+// counter are ranked by comparison (<= kRangeRankM keys; unique keys: rank = number of
+// smaller keys), bigger groups are refined (refine_groups), an LSD of the range is the last
+// resort -- any key distribution gives the exact order.  Keys stay in registers (NI per thread).
+// Code space of the linear digit: the key's (starving flag, bit length e of v, the 40 bits of v
+// below its leading one) -- monotone in the key, linear in v inside an octave, so a range
+// spanning several octaves (or the starving / not-starving boundary) still spreads evenly.
+__device__ __forceinline__ unsigned long long key_code(uint64_t k, uint32_t vb) {
+    const uint64_t v = k & ((1ull << vb) - 1ull);
+    const uint32_t e = 64u - (uint32_t)__clzll((long long)v);
+    const uint64_t mant = e ? ((v << (64u - e)) << 1) >> 24 : 0ull;
+    return ((unsigned long long)(((uint32_t)(k >> vb) << 6) | e) << 40) | mant;
+}
+// Sort of a CTA's key range (rn <= kKcap keys at src, global, L2-resident) straight into its
+// place in the ranked order (out, global), in compact loops (this code runs once per step and
+// is fetched cold, so no per-thread item arrays): one counting pass on a linear digit of the
+// key code between the range's bounds lo..hi (the splitters: quantiles of the previous
+// order, so ~2 counters per key), d = (code(k) - code(lo)) >> sh clamped to the counters;
+// placement by digit into sm.a; then every key's rank inside its counter by comparison
+// (<= kRangeRankM keys; unique keys: the number of smaller keys) gives its final position.
+// Returns false if a counter held more keys: sm.a then holds the range (placed by digit)
+// and the caller sorts it otherwise.
+__device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
+                                                uint64_t* __restrict__ out, unsigned long long lo,
+                                                unsigned long long hi, uint32_t vb, unsigned long long* tr) {
+#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
+    const uint32_t tid = threadIdx.x;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);  // <= 2^14 + 1 counters
+    uint32_t* dv = sm.pos;                              // per key: digit | order << 14
+    uint64_t* A = sm.a;
+    LTRACE(0);
+    const unsigned long long cmn = key_code(lo, vb), cmx = key_code(hi, vb);
+    const unsigned long long span = cmx > cmn ? cmx - cmn : 0ull;
+    const uint32_t cb = min(rn > 1u ? 33u - (uint32_t)__clz(rn - 1u) : 0u, 14u);  // ~2 counters per key
+    const uint32_t nbits = 64u - (uint32_t)__clzll((long long)span);
+    const uint32_t sh = nbits > cb ? nbits - cb : 0u;
+    const uint32_t ncnt = (uint32_t)min(span >> sh, (unsigned long long)((1u << cb) - 1u)) + 1u;
+    auto digit = [&](uint64_t k) -> uint32_t {
+        const unsigned long long c = key_code(k, vb);
+        const unsigned long long d = (c > cmn ? c - cmn : 0ull) >> sh;
+        return (uint32_t)min(d, (unsigned long long)(ncnt - 1u));
+    };
+    for (uint32_t i = tid; i <= ncnt; i += kFT) cnt[i] = 0u;
+    __syncthreads();
+    LTRACE(1);
+    for (uint32_t i = tid; i < rn; i += kFT) {
+        const uint32_t d = digit(__ldcg(src + i));
+        dv[i] = d | (atomicAdd(&cnt[d], 1u) << 14);
+    }
+    __syncthreads();
+    LTRACE(2);
+    (void)smem_excl_scan<kFT, (1 << 14) / kFT + 1>(cnt, ncnt, sm.w32);
+    if (tid == 0) cnt[ncnt] = rn;
+    LTRACE(3);
+    for (uint32_t i = tid; i < rn; i += kFT) {
+        const uint32_t v = dv[i];
+        A[cnt[v & 0x3fffu] + (v >> 14)] = __ldcg(src + i);
+    }
+    __syncthreads();
+    LTRACE(4);
+    bool big = false;
+    for (uint32_t p = tid; p < rn; p += kFT) {
+        const uint64_t k = A[p];
+        const uint32_t d = digit(k), st = cnt[d], m2 = cnt[d + 1] - st;
+        uint32_t r = 0;
+        if (m2 <= 4u) {  // the common case: straight-line, predicated compares
+            if (m2 > 1u) {
+                r += A[st] < k ? 1u : 0u;
+                r += A[st + 1] < k ? 1u : 0u;
+                if (m2 > 2u) r += A[st + 2] < k ? 1u : 0u;
+                if (m2 > 3u) r += A[st + 3] < k ? 1u : 0u;
+            }
+        } else if (m2 <= kRangeRankM) {
+            for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k ? 1u : 0u;
+        } else {
+            big = true;
+            continue;
+        }
+        out[st + r] = k;
+    }
+    LTRACE(5);
+#undef LTRACE
+    return !__syncthreads_or(big);
+}
+
 // A small range (rn <= kSmallSort keys): ranked by comparison against all its keys (the
 // keys are unique, so the rank is the count of smaller keys; the few hundred keys are read
 // as shared-memory broadcasts), no bucket table.  A small pool's head range can span
@@ -675,7 +827,7 @@ __device__ __forceinline__ void small_sort(PhaseL& sm, const uint64_t* __restric
 // Returns false (nothing written) if a bucket holds more than kRangeRankM keys; the caller
 // then uses range_sort.
 __device__ __forceinline__ bool head_sparse_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
-                                                 const Cost& c, uint32_t half, uint32_t j_lo, uint32_t nb,
+                                                 const Cost& c, const uint32_t* tab, uint32_t j_lo, uint32_t nb,
                                                  const Pool& pool, uint32_t id_base_mod) {
     constexpr int NI = (kHeadPre + kFT - 1) / kFT;  // 3
     const uint32_t tid = threadIdx.x;
@@ -697,7 +849,8 @@ __device__ __forceinline__ bool head_sparse_sort(PhaseL& sm, const uint64_t* __r
         J[u] = 0;
         if (i < rn) {
             k[u] = __ldcg(src + i);
-            J[u] = bucket_of(k[u], c, half) - j_lo;
+            uint32_t sv;
+            J[u] = bucket_t(k[u], tab, c.SB + c.IB, sv) - j_lo;
             atomicOr(&bm[J[u] >> 5], 1u << (J[u] & 31u));
             const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
             asm volatile("prefetch.global.L2 [%0];" ::"l"(pool.ctx + slot));
@@ -768,60 +921,65 @@ __device__ __forceinline__ bool head_sparse_sort(PhaseL& sm, const uint64_t* __r
 // P2P: the peer-memory exchange + in-kernel merge instance (its code and shared-memory
 // tail are left out of the plain instance)
 template <bool DBG, bool P2P>
-__global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, const __grid_constant__ InlineStage inl) {
+__global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b, const __grid_constant__ Cost c, StepArgs a,
+                                                  const __grid_constant__ InlineStage inl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
     Ctl* ctl = b.ctl;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t G = gridDim.x, bid = blockIdx.x;
-    const uint32_t vbits = c.SB + c.IB;  // buckets over the key's score|id bits (bucket_of)
-    const uint32_t half = (vbits <= (uint32_t)kBucketM) ? (1u << vbits) : ((vbits - kBucketM + 1u) << kBucketM);
-    const uint32_t NB = 2u * half;
-    uint32_t* T = b.btot + (a.parity ? kMaxBuckets : 0);  // [NB] bucket totals of this step
-    {   // the other parity's totals are zeroed for the next step
-        uint4* Tn = reinterpret_cast<uint4*>(b.btot + (a.parity ? 0 : kMaxBuckets));
-        for (uint32_t j = bid * kFT + tid; j < (NB + 3u) / 4u; j += G * kFT) Tn[j] = make_uint4(0, 0, 0, 0);
+    const uint32_t vb = c.SB + c.IB;  // buckets over the key's score|id bits (bucket_t)
+    // this CTA's slots; all of their SoA words are requested into L2 at once (bulk
+    // prefetches, no shared memory), so the score phase's double-buffered TMA copies below
+    // hit L2 and HBM sees the whole pool's reads in flight
+    const uint32_t ngroups = (c.cap + 3u) >> 2;
+    const uint32_t gpc = (ngroups + G - 1) / G;
+    const uint32_t s_lo = 4u * min(ngroups, bid * gpc), s_hi = 4u * min(ngroups, bid * gpc + gpc);
+    if (warp == 0) {
+        const uint32_t npf = 7u * ((s_hi - s_lo + kChunk - 1) / kChunk);
+        for (uint32_t q = lane; q < npf; q += 32u) {
+            const uint32_t ai = q % 7u, base = s_lo + (q / 7u) * kChunk;
+            const uint32_t bytes = min((uint32_t)kChunk, s_hi - base) * 4u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b.pool.sfc + (size_t)ai * b.pool.stride + base),
+                         "r"(bytes) : "memory");
+        }
     }
+    uint32_t* T = b.btot + (a.parity ? kMaxBuckets : 0);  // [NB] bucket totals of this step (cold steps)
+    {   // the other parity's totals are zeroed for the next step (whose table may be larger)
+        uint4* Tn = reinterpret_cast<uint4*>(b.btot + (a.parity ? 0 : kMaxBuckets));
+        for (uint32_t j = bid * kFT + tid; j < (uint32_t)kMaxBuckets / 4u; j += G * kFT) Tn[j] = make_uint4(0, 0, 0, 0);
+    }
+    uint32_t* rcur = b.rcur + (a.parity ? kMaxCtas : 0);  // [G] keys written to each range
+    if (bid == 0 && tid < (uint32_t)kMaxCtas) b.rcur[(a.parity ? 0 : kMaxCtas) + tid] = 0u;  // the next step's
+    // the bucket table and (warm steps) the splitters the previous step wrote -> shared memory
+    // by cp.async: read only after the score phase, so their latency hides behind it
+    if (tid < (uint32_t)kTabW / 4u) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.btab[4 * tid]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\ncp.async.commit_group;" ::"r"(dst),
+                     "l"(b.btab + (size_t)a.parity * kTabW + 4 * tid) : "memory");
+    }
+    if (!a.cold && tid < (uint32_t)kMaxCtas) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.s.spl[spl_pos(tid)]);  // + the max below
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;" ::"r"(dst),
+                     "l"(b.spl + (size_t)a.parity * kSplG + tid) : "memory");
+    }
+    if (!a.cold && tid == 0) sm.s.spl[spl_pos(kMaxCtas)] = __ldcg(b.spl + (size_t)a.parity * kSplG + kMaxCtas);
 
     TRACE(0);
-    // the CTAs' measured range-sort costs (previous steps) -> shared memory by cp.async, so
-    // the L2 latency hides behind the score phase; they weight the key ranges (X)
     SmemTail& tail = *reinterpret_cast<SmemTail*>(smem_raw + sizeof(FusedSmem));
     if (P2P && tid < a.world) {  // the peers' exchange buffers
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tail.xp[tid]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;" ::"r"(dst),
                      "l"(b.xpeers + tid) : "memory");
     }
-    if (tid < G && tid < (uint32_t)kMaxCtas) {
+    // cold steps: the CTAs' measured range-sort costs (previous steps) weight the key ranges (X)
+    if (a.cold && tid < G && tid < (uint32_t)kMaxCtas) {
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.s.ccost[tid]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\ncp.async.commit_group;" ::"r"(dst),
                      "l"(b.cta_cost + tid) : "memory");
     }
-    // ---------------- S: score this CTA's slots, keys into shared memory.  The seven SoA
-    // words of each chunk of 1024 slots are staged by TMA bulk copies (one thread issues
-    // seven 1-D copies per chunk; an mbarrier counts the bytes), double buffered, while
-    // the previous chunk is scored, one slot per thread.
-    const uint32_t ngroups = (c.cap + 3u) >> 2;
-    const uint32_t gpc = (ngroups + G - 1) / G;
-    const uint32_t s_lo = 4u * min(ngroups, bid * gpc), s_hi = 4u * min(ngroups, bid * gpc + gpc);
-    const uint32_t nchunk = (s_hi - s_lo + kChunk - 1) / kChunk;
-    uint32_t* stage = sm.s.start;  // [2][7][kChunk] words
-    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&sm.s.mbar[0]);
-    auto issue = [&](uint32_t ch) {  // thread 0
-        const uint32_t base = s_lo + ch * kChunk, buf = ch & 1u;
-        const uint32_t bytes = min((uint32_t)kChunk, s_hi - base) * 4u;  // multiple of 16: s_lo, s_hi are 4-aligned
-        const uint32_t mb = mb0 + 8u * buf;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(7u * bytes) : "memory");
-#pragma unroll
-        for (uint32_t ai = 0; ai < 7u; ai++) {
-            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&stage[(buf * 7u + ai) * kChunk]);
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(dst), "l"(b.pool.sfc + (size_t)ai * b.pool.stride + base), "r"(bytes), "r"(mb)
-                         : "memory");
-        }
-    };
     if (a.n_ev | a.n_ret | a.n_sub) {  // API returns, arrivals and A0 for the engine's events on
-                                       // this CTA's slots, before they are staged (the three touch
+                                       // this CTA's slots, before they are scored (the three touch
                                        // disjoint slots: PAUSED, FREE, admitted last step)
         const ReturnRec* rets = a.inl ? reinterpret_cast<const ReturnRec*>(inl.bytes)
                                       : static_cast<const ReturnRec*>(b.returns);
@@ -843,189 +1001,163 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
             const uint32_t s = (uint32_t)E.id & c.cap_mask;
             if (s >= s_lo && s < s_hi) apply_event(b.pool, c, E);
         }
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
         __syncthreads();
     }
-    if (tid == 0) {
-        sm.s.nk = 0;
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (nchunk) issue(0);
-    }
-    for (uint32_t i = tid; i < (NB + 3u) / 4u; i += kFT) reinterpret_cast<uint4*>(sm.s.cnt)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    unsigned long long pinned = 0;
-    for (uint32_t ch = 0; ch < nchunk; ch++) {
-        if (tid == 0 && ch + 1 < nchunk) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer reads done (barrier below)
-            issue(ch + 1);
-        }
-        {   // wait for this chunk's bytes: phase parity = use count of the buffer & 1
-            const uint32_t mb = mb0 + 8u * (ch & 1u), par = (ch >> 1) & 1u;
-            asm volatile(
-                "{\n.reg .pred p;\nWAIT_%=:\n"
-                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-                "@!p bra WAIT_%=;\n}\n" ::"r"(mb), "r"(par) : "memory");
-        }
-        const uint32_t slot = s_lo + ch * kChunk + tid;
-        const uint32_t* sw = stage + (ch & 1u) * 7u * kChunk + tid;
-        bool have = false;
-        uint64_t key = 0;
-        if (slot < s_hi) {
-            uint32_t w = sw[0], ctx = sw[kChunk], pre = sw[2 * kChunk], pend = sw[6 * kChunk];
-            if (w & SFC_RAN) {  // A0: the previous batch generated one token
-                ctx += 1u;
-                pre = pre ? pre - 1u : 0u;
-                pend = 0u;
-                b.pool.ctx[slot] = ctx;
-                b.pool.pre[slot] = pre;
-                b.pool.pend[slot] = 0u;
-            }
-            const uint32_t st = sfc_state(w);
-            if (st == ST_PP) pinned += blk(ctx, c);
-            if (st == ST_READY) {
-                have = score_slot<DBG>(b.pool, c, a.id_base_mod, b.dbg, slot, w, ctx, pre, sw[3 * kChunk],
-                                       sw[4 * kChunk], sw[5 * kChunk], pend, key);
-                b.pool.sfc[slot] = w;
-            }
-        }
-        // keys stay at their slot's position in kbuf (no compaction: a CTA's slot range fits
-        // kbuf); which positions hold keys is one ballot word per warp
-        const uint32_t m = __ballot_sync(0xffffffffu, have);
-        if (lane == 0) sm.s.vmask[(ch * kChunk + tid) >> 5] = m;
-        if (have) {
-            sm.s.kbuf[ch * kChunk + tid] = key;
-            atomicAdd(&sm.s.cnt[bucket_of(key, c, half)], 1u);
-        }
-        __syncthreads();
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");  // ccost (read after the barrier below)
-    if (tid == 0) {  // the barrier words are reused as plain shared memory after S
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0) : "memory");
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb0 + 8u) : "memory");
+    if (tid < (uint32_t)kMaxCtas) sm.s.lcnt[tid] = 0u;  // R's per-range counts
+    if (a.cold) {
+        for (uint32_t i = tid; i < (uint32_t)kMaxBuckets / 4u; i += kFT)
+            reinterpret_cast<uint4*>(sm.s.cnt)[i] = make_uint4(0, 0, 0, 0);
+        asm volatile("cp.async.wait_all;" ::: "memory");  // the bucket table (histogram below)
     }
     __syncthreads();
-    const uint32_t nk_cta = s_hi - s_lo;  // kbuf positions (slots of this CTA), vmask = which hold keys
+    // ---------------- S: score this CTA's slots, two per thread per round (64-bit loads of the
+    // seven SoA words, L2 hits after the bulk prefetch above); keys compacted into kbuf (warp-
+    // aggregated: one shared-memory atomic per warp); cold steps also count the keys' buckets
+    uint32_t pinned = 0, nmine = 0;  // this thread's pinned blocks (< 2^32: <= 8 slots of < 2^16) and keys
+    auto score1 = [&](uint32_t slot, uint32_t w, uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
+                      uint32_t post, uint32_t pend, uint64_t& key) -> bool {
+        if (w & SFC_RAN) {  // A0: the previous batch generated one token
+            ctx += 1u;
+            pre = pre ? pre - 1u : 0u;
+            pend = 0u;
+            b.pool.ctx[slot] = ctx;
+            b.pool.pre[slot] = pre;
+            b.pool.pend[slot] = 0u;
+        }
+        const uint32_t st = sfc_state(w);
+        if (st == ST_PP) pinned += (ctx + c.B - 1u) >> c.lgB;
+        if (st != ST_READY) return false;
+        const uint32_t has = sfc_has(w), rp = has ? resp : 0u, pp = has ? post : 0u;
+        // fast check: all four below 2^18, so their sum is below 2^20 (kFastCtxLimit)
+        if (c.lean && (ctx | pre | rp | pp) < (1u << 18)) {
+            // A1 + A2 (score_lean), A3: starvation, counter, key
+            uint64_t sc, wp, wd, ws;
+            const uint32_t strat = score_lean(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws);
+            const uint32_t cnt = sfc_cnt(w);
+            const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
+            w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u);
+            key = (starv ? 0ull : c.nsbit) | (sc << c.IB) | ((slot - a.id_base_mod) & c.cap_mask);
+            if (DBG) {
+                unsigned long long* d = b.dbg + 4ull * slot;
+                d[0] = wp; d[1] = wd; d[2] = ws; d[3] = sc;
+            }
+        } else {
+            const ColdOut o = score_slot_cold<DBG>(b.pool, c, a.id_base_mod, b.dbg, slot, w, ctx, pre, api, resp,
+                                                   post, pend);
+            key = o.key;
+            w = o.w;
+        }
+        b.pool.sfc[slot] = w;
+        nmine++;
+        return true;
+    };
+    // keys stay at their slot's position in kbuf (position = slot - s_lo); which positions hold
+    // keys: one ballot word per warp and slot parity (vmask[2 * (q >> 5) + j], q = pair index)
+    {
+        const uint32_t p_lo = s_lo >> 1, p_hi = s_hi >> 1;  // slot pairs
+        const uint2* S2 = reinterpret_cast<const uint2*>(b.pool.sfc);
+        const uint32_t st2 = b.pool.stride >> 1;
+        for (uint32_t p0 = p_lo + (tid & ~31u); p0 < p_hi; p0 += kFT) {  // warp-uniform bound
+            const uint32_t pr = p0 + lane;
+            uint64_t k0 = 0, k1 = 0;
+            bool h0 = false, h1 = false;
+            if (pr < p_hi) {
+                const uint2 w = __ldcg(S2 + pr), cx = __ldcg(S2 + st2 + pr), pe = __ldcg(S2 + 2 * st2 + pr),
+                            ap = __ldcg(S2 + 3 * st2 + pr), rs = __ldcg(S2 + 4 * st2 + pr),
+                            po = __ldcg(S2 + 5 * st2 + pr), pd = __ldcg(S2 + 6 * st2 + pr);
+                h0 = score1(2u * pr, w.x, cx.x, pe.x, ap.x, rs.x, po.x, pd.x, k0);
+                h1 = score1(2u * pr + 1u, w.y, cx.y, pe.y, ap.y, rs.y, po.y, pd.y, k1);
+                reinterpret_cast<ulonglong2*>(sm.s.kbuf)[pr - p_lo] = make_ulonglong2(k0, k1);
+                if (a.cold) {
+                    uint32_t sv;
+                    if (h0) atomicAdd(&sm.s.cnt[bucket_t(k0, sm.btab, vb, sv)], 1u);
+                    if (h1) atomicAdd(&sm.s.cnt[bucket_t(k1, sm.btab, vb, sv)], 1u);
+                }
+            }
+            const uint32_t m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+            if (lane == 0) {
+                const uint32_t wq = (p0 - p_lo) >> 5;
+                sm.s.vmask[2 * wq] = m0;
+                sm.s.vmask[2 * wq + 1] = m1;
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // table, splitters, costs, peer pointers
+    const uint32_t npos = s_hi - s_lo;  // kbuf positions (slots of this CTA)
+    const uint32_t NB = sm.btab[kTabNB];  // buckets of this step's table
+    unsigned long long pin64 = pinned;
+    uint32_t nk_cta = nmine;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) pinned += __shfl_xor_sync(0xffffffffu, pinned, o);
-    if (lane == 0) sm.s.red[0][warp] = pinned;
+    for (int o = 16; o; o >>= 1) {
+        pin64 += __shfl_xor_sync(0xffffffffu, pin64, o);
+        nk_cta += __shfl_xor_sync(0xffffffffu, nk_cta, o);
+    }
+    if (lane == 0) { sm.s.red[0][warp] = pin64; sm.s.red[1][warp] = nk_cta; }
     __syncthreads();
+    {
+        uint32_t t = 0;
+#pragma unroll 8
+        for (int w = 0; w < kFW; w++) t += (uint32_t)sm.s.red[1][w];
+        nk_cta = t;  // keys of this CTA
+    }
     if (tid == 0) {
         unsigned long long t = 0;
         for (int w = 0; w < kFW; w++) t += sm.s.red[0][w];
         b.pin_part[bid] = t;
+        b.nk_part[bid] = nk_cta;
     }
     TRACE(1);
-    // ---------------- H: add this CTA's bucket counts to the totals; the returned old
-    // value is this CTA's offset inside the bucket (the CTAs' order inside a bucket is
-    // free: the range sort orders every bucket completely)
-    {
-        constexpr int kU = 8;
-        for (uint32_t j0 = 0; j0 < NB; j0 += kU * kFT) {
-            uint32_t v[kU];
-#pragma unroll
-            for (int u = 0; u < kU; u++) {
-                const uint32_t j = j0 + (uint32_t)u * kFT + tid;
-                v[u] = j < NB ? sm.s.cnt[j] : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < kU; u++)
-                if (v[u]) v[u] = atomicAdd(&T[j0 + (uint32_t)u * kFT + tid], v[u]);
-#pragma unroll
-            for (int u = 0; u < kU; u++) {
-                const uint32_t j = j0 + (uint32_t)u * kFT + tid;
-                if (j < NB) sm.s.cnt[j] = v[u];
-            }
-        }
-    }
-    TRACE(2);
-    if (bid == 0) {  // while waiting for the other CTAs: L2 prefetch of the previous admitted list
-        const uint32_t np = ctl->n_admitted, prv = a.parity ^ 1u;
-        for (uint32_t i = tid; i < np; i += kFT) {
-            const uint32_t ps = __ldcg(&b.adm_slot[prv][i]);
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(b.pool.sfc + ps));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(b.adm_id[prv] + i));
-        }
-    }
     uint32_t bar = a.step * kBarPerStep;
-    grid_barrier(b.flags, G, ++bar);
-    TRACE(3);
-    // CTA 0, warp 0: the pinned total (A5's budget) is final now; kept in registers
-    unsigned long long pinned_all = 0;
-    if (bid == 0 && warp == 0) {
-        for (uint32_t r = lane; r < G; r += 32) pinned_all += __ldcg(&b.pin_part[r]);
+    const bool head_mode = (a.flags & kStepHeadOnly) != 0;
+    if (a.cold) {
+        // ---------------- cold step (no splitters from a previous step): bucket histogram ->
+        // totals -> bucket-aligned key ranges -> splitters = the ranges' lowest bucket keys
+        {   // H: this CTA's bucket counts into the totals
+            constexpr int kU = 8;
+            for (uint32_t j0 = 0; j0 < NB; j0 += kU * kFT) {
 #pragma unroll
-        for (int o = 16; o; o >>= 1) pinned_all += __shfl_xor_sync(0xffffffffu, pinned_all, o);
-    }
-    TRACE(4);
-    TRACE(5);
-
-    // ---------------- X: bucket starts (scan of the totals, in shared memory), scatter into
-    // bucket order; cursor(j) = start(j) + this CTA's offset inside bucket j.  The totals
-    // are loaded coalesced (uint4) into shared memory, then scanned in place by raking.
-    {
-        constexpr int kPer4 = (kMaxBuckets / 4 + kFT - 1) / kFT;  // 4
-        uint4 tv[kPer4];
-        const uint32_t nb4 = (NB + 3u) / 4u;
-#pragma unroll
-        for (int u = 0; u < kPer4; u++) {
-            const uint32_t j = tid + (uint32_t)u * kFT;
-            tv[u] = j < nb4 ? __ldcg(reinterpret_cast<const uint4*>(T) + j) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < kPer4; u++) {
-            const uint32_t j = tid + (uint32_t)u * kFT;
-            if (j < nb4) reinterpret_cast<uint4*>(sm.s.start)[j] = tv[u];
-        }
-    }
-    __syncthreads();
-    TRACE(10);
-    {
-        const uint32_t tot = smem_excl_scan<kFT, (kMaxBuckets + kFT - 1) / kFT>(sm.s.start, NB, sm.s.w32, sm.s.cnt);
-        if (tid == 0) sm.s.base = tot;  // total number of keys
-    }
-    __syncthreads();
-    TRACE(11);
-    const uint32_t n = sm.s.base;
-    // head-only mode (F3): only the buckets of CTA 0's range -- the head the admission can
-    // reach -- are scattered and sorted; the other CTAs are done after the next barrier
-    bool head_only = false;
-    if (a.flags & kStepHeadOnly) {
-        if (tid == 0) {
-            const uint32_t head = min(n, a.max_batch + 32u);
-            uint32_t lo = 0, hi = NB;  // first bucket with start >= head
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (sm.s.start[mid] >= head) hi = mid; else lo = mid + 1;
+                for (int u = 0; u < kU; u++) {
+                    const uint32_t j = j0 + (uint32_t)u * kFT + tid;
+                    const uint32_t v = j < NB ? sm.s.cnt[j] : 0u;
+                    if (v) atomicAdd(&T[j], v);
+                }
             }
-            sm.s.hb_j = lo;
-            sm.s.hb_r = lo == NB ? n : sm.s.start[lo];
+        }
+        TRACE(2);
+        grid_barrier(b.flags, G, ++bar);
+        TRACE(3);
+        {   // X: bucket starts (the totals loaded coalesced, scanned in place by raking)
+            constexpr int kPer4 = (kMaxBuckets / 4 + kFT - 1) / kFT;  // 4
+            uint4 tv[kPer4];
+            const uint32_t nb4 = (NB + 3u) / 4u;
+#pragma unroll
+            for (int u = 0; u < kPer4; u++) {
+                const uint32_t j = tid + (uint32_t)u * kFT;
+                tv[u] = j < nb4 ? __ldcg(reinterpret_cast<const uint4*>(T) + j) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kPer4; u++) {
+                const uint32_t j = tid + (uint32_t)u * kFT;
+                if (j < nb4) reinterpret_cast<uint4*>(sm.s.start)[j] = tv[u];
+            }
         }
         __syncthreads();
-        head_only = sm.s.hb_r <= (uint32_t)kKcap && !(a.flags & kStepForceFallback);
-    }
-    const uint32_t jcut = head_only ? sm.s.hb_j : NB;
-    // The first kRW warps compute the range boundaries while the other warps scatter the
-    // keys (both only read the bucket starts).  CTA r sorts the buckets whose start lies
-    // in [q_r, q_{r+1}); thread r finds the first bucket with start >= q_r by binary
-    // search; the largest range decides the fallback.
-    uint32_t* rb = sm.s.rb;  // key boundaries of the ranges
-    uint32_t* jb = sm.s.jb;  // bucket boundaries of the ranges
-    const uint32_t kRW = (G + 1u + 31u) / 32u;
-    if (warp < kRW) {
-        if (head_only) {  // one range: [0, hb_r) in buckets [0, hb_j), sorted by CTA 0
-            if (tid <= G) {
-                rb[tid] = tid == 0 ? 0u : sm.s.hb_r;
-                jb[tid] = tid == 0 ? 0u : sm.s.hb_j;
-            }
-        } else {
-            // CTA 0 sorts only the head (the max_batch keys the admission may take, to the
-            // end of their bucket) so it can start the admission early; the other CTAs share
-            // the rest in proportion to their measured speed (cycles per key of the previous
-            // steps' range sorts: some SMs of a B200 run this phase markedly slower), weight
-            // mean/cost capped at 1.25; below 0.4 the CTA gets no range (G <= 255)
+        TRACE(10);
+        {
+            const uint32_t tot = smem_excl_scan<kFT, (kMaxBuckets + kFT - 1) / kFT>(sm.s.start, NB, sm.s.w32);
+            if (tid == 0) sm.s.base = tot;  // total number of keys
+        }
+        __syncthreads();
+        TRACE(11);
+        const uint32_t n0 = sm.s.base;
+        // the next step's bucket table from this step's octave counts (one warp of the last CTA)
+        if (bid == G - 1u && warp == kFW - 1) bt_update(sm.btab, sm.s.start, n0, vb, b.btab + (size_t)(a.parity ^ 1u) * kTabW);
+        // CTA 0 sorts only the head (the max_batch keys the admission may take, to the end of
+        // their bucket) so it can start the admission early; the other CTAs share the rest in
+        // proportion to their measured speed (cycles per key of the previous steps' range
+        // sorts), weight mean/cost capped at 1.25; below 0.4 the CTA gets no range (G <= 255)
+        const uint32_t kRW = (G + 1u + 31u) / 32u;
+        if (warp < kRW) {
             float* wx = sm.s.wx;  // [G + 1] exclusive weight prefix
             if (warp == 0) {
                 constexpr int kW = kMaxCtas / 32;
@@ -1050,8 +1182,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
                     w[u] = 0.f;
                     if (r >= 1 && r < G) {
                         const float rel = cst[u] > 0.f ? __fdividef(mean, cst[u]) : 1.f;
-                        // two-sided (measured 0.8 us better than one-sided or uniform on one
-                        // box, scripts/ab_tune.py); LAMPS_TUNE bit 3: one-sided (cap 1)
                         w[u] = rel < 0.4f ? 0.f : fminf(rel, (a.tune & 8u) ? 1.f : 1.25f);
                         if (a.tune & 1u) w[u] = 1.f;
                     }
@@ -1073,52 +1203,159 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
             }
             asm volatile("bar.sync 1, %0;" ::"r"(kRW * 32u) : "memory");  // the kRW warps only
             if (tid <= G) {
-                const uint32_t head = min(n, a.max_batch + 32u);
+                const uint32_t head = min(n0, a.max_batch + 32u);
                 const float wt = wx[G];
                 const float f = tid == 0 ? 0.f : (wt > 0.f ? fminf(__fdividef(wx[tid], wt), 1.f) : 0.f);
-                const uint32_t q = tid == 0 ? 0u : head + min(n - head, (uint32_t)(f * (float)(n - head)));
+                const uint32_t q = tid == 0 ? 0u : head + min(n0 - head, (uint32_t)(f * (float)(n0 - head)));
                 uint32_t lo = 0, hi = NB;  // first j with start(j) >= q
                 while (lo < hi) {
                     const uint32_t mid = (lo + hi) >> 1;
                     if (sm.s.start[mid] >= q) hi = mid; else lo = mid + 1;
                 }
-                // (LAMPS_TUNE bit 1) boundaries after the head snap to the NEAREST bucket start;
-                // default: the first bucket start >= the target; the head's end stays >= its target
-                if (tid >= 2 && tid < G && lo > 0 && (a.tune & 2u)) {
-                    const uint32_t above = lo == NB ? n : sm.s.start[lo], below = sm.s.start[lo - 1];
-                    if (q - below < above - q) lo = lo - 1;
-                }
-                rb[tid] = (tid == G || lo == NB) ? n : sm.s.start[lo];
-                jb[tid] = tid == G ? NB : lo;
+                sm.s.jb[tid] = tid == G ? NB : lo;
             }
         }
-    } else {
-        for (uint32_t i = tid - kRW * 32u; i < nk_cta; i += kFT - kRW * 32u) {
-            if (!((sm.s.vmask[i >> 5] >> (i & 31u)) & 1u)) continue;
+        __syncthreads();
+        // splitter r = the lowest key of bucket jb[r] (octave (ns, e) found by binary search
+        // over the table's bases; key = ns | (2^m + mantissa) << s); none past the last bucket.
+        // Entry kMaxCtas: the largest key's bound (the last nonempty bucket's highest key).
+        auto bucket_key = [&](uint32_t j, bool high) -> unsigned long long {
+            uint32_t lo = 0, hi = kTabNB - 1u;  // last octave with base <= j and a nonzero span
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1u) >> 1;
+                if ((sm.btab[mid] & 0xffffu) <= j) lo = mid; else hi = mid - 1u;
+            }
+            while (lo > 0 && (sm.btab[lo] & 0xffffu) == (lo + 1u < kTabNB ? sm.btab[lo + 1] & 0xffffu : NB)) lo--;
+            const uint32_t t = sm.btab[lo], e = lo % 65u, ns = lo / 65u;
+            const uint32_t sv = (t >> 16) & 63u, m = t >> 24, mm = j - (t & 0xffffu);
+            unsigned long long v = e == 0u ? 0ull : ((unsigned long long)((1u << m) | mm) << sv);
+            if (high) v |= (1ull << sv) - 1ull;
+            return ((unsigned long long)ns << vb) | v;
+        };
+        if (tid < (uint32_t)kMaxCtas + 1u) {
+            unsigned long long sk = ~0ull;
+            if (tid == 0) {
+                sk = 0ull;
+            } else if (tid < G && sm.s.jb[tid] < NB) {
+                sk = bucket_key(sm.s.jb[tid], false);
+            } else if (tid == (uint32_t)kMaxCtas && n0) {
+                uint32_t lo = 0, hi = NB;  // first j with start(j) >= n0; the last nonempty is before it
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (sm.s.start[mid] >= n0) hi = mid; else lo = mid + 1;
+                }
+                sk = bucket_key(lo - 1u, true);
+            }
+            sm.s.spl[spl_pos(tid)] = sk;
+            if (bid == G - 1u) b.spl[(size_t)a.parity * kSplG + tid] = sk;  // head-only keeps them
+        }
+        __syncthreads();
+    }
+    else if (bid == G - 1u && tid < (uint32_t)kTabW) {
+        b.btab[(size_t)(a.parity ^ 1u) * kTabW + tid] = sm.btab[tid];  // warm step: the table carries over
+    }
+    // ---------------- R: every key to its range, range r = keys in [spl[r], spl[r+1]) (a
+    // binary search over the splitters), written into the range's region keys0[r * kKcap ...]:
+    // per range this CTA's keys form one run (a local counting sort), whose offset inside
+    // the region one global atomic per range gives, so the stores are contiguous
+    // (compact loops, no per-thread item arrays: the kernel runs once per step and its code is
+    // fetched cold -- straight-line unrolled code costs more in instruction fetch than it saves)
+    uint32_t* const kr = reinterpret_cast<uint32_t*>(sm.s.cnt);          // scratch over cnt + start
+    uint64_t* const kb2 = reinterpret_cast<uint64_t*>(kr);                 // [kKcap] keys by range
+    uint8_t* const rr = reinterpret_cast<uint8_t*>(kr) + 8u * kKcap;       // [kKcap] their range
+    uint8_t* const rv = rr + kKcap;                                        // [kKcap] range by position
+    {
+        const unsigned long long* spl = sm.s.spl;
+        for (uint32_t i = tid; i < npos; i += kFT) {
+            const uint32_t q = i >> 1;
+            if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
             const uint64_t k = sm.s.kbuf[i];
-            const uint32_t j = bucket_of(k, c, half);
-            if (j >= jcut) continue;
-            const uint32_t pos = atomicAdd(&sm.s.cnt[j], 1u);  // order within a bucket is free
-            b.keys[0][pos] = k;
+            uint32_t r = 0;
+#pragma unroll
+            for (uint32_t st = kMaxCtas / 2u; st; st >>= 1) r = k >= spl[spl_pos(r + st)] ? r + st : r;
+            r = min(r, G - 1u);
+            rv[i] = (uint8_t)r;
+            atomicAdd(&sm.s.lcnt[r], 1u);
         }
     }
-    TRACE(12);
     __syncthreads();
-    uint32_t mx = 0;
-    if (tid < G) mx = rb[tid + 1] - rb[tid];
-    const bool fallback = (a.flags & kStepForceFallback) ||
-                          __syncthreads_or(mx > (uint32_t)kKcap);
-    const uint32_t r_lo = rb[bid], r_hi = rb[bid + 1], r_end0 = rb[1];
-    const uint32_t j_lo = jb[bid], j_hi = jb[bid + 1];
+    TRACE(4);
+    if (tid < G) {
+        const uint32_t m = sm.s.lcnt[tid];
+        sm.s.gbase[tid] = m ? atomicAdd(&rcur[tid], m) : 0u;
+    }
+    if (tid < (uint32_t)kMaxCtas) sm.s.lst[tid] = sm.s.lcnt[tid];
+    __syncthreads();
+    (void)smem_excl_scan<kFT, 1>(sm.s.lst, kMaxCtas, sm.s.w32);
+    if (tid < (uint32_t)kMaxCtas) sm.s.lcnt[tid] = sm.s.lst[tid];  // run cursors
+    __syncthreads();
+    TRACE(5);
+    for (uint32_t i = tid; i < npos; i += kFT) {
+        const uint32_t q = i >> 1;
+        if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
+        const uint32_t r = rv[i], lp = atomicAdd(&sm.s.lcnt[r], 1u);  // order within a run is free
+        kb2[lp] = sm.s.kbuf[i];
+        rr[lp] = (uint8_t)r;
+    }
+    __syncthreads();
+    TRACE(12);
+    for (uint32_t i = tid; i < nk_cta; i += kFT) {
+        const uint32_t r = rr[i], pos = sm.s.gbase[r] + (i - sm.s.lst[r]);
+        if (pos < (uint32_t)kKcap) b.keys[0][(size_t)r * kKcap + pos] = kb2[i];  // else: overflow -> fallback
+    }
+    // this CTA's range: its splitters and bucket span (shared memory is reused after the barrier)
+    const unsigned long long spl_lo = sm.s.spl[spl_pos(bid)], spl_hi = bid + 1u < G ? sm.s.spl[spl_pos(bid + 1)] : ~0ull;
+    // the range's key bounds for its digit: [spl_lo, spl_hi - 1], or the previous order's
+    // largest key for the last nonempty range (keys outside are clamped into the end counters)
+    const unsigned long long key_hi = spl_hi == ~0ull ? sm.s.spl[spl_pos(kMaxCtas)] : spl_hi - 1ull;
+    uint32_t j_lo = 0, j_hi = 0;
+    {
+        uint32_t sv;
+        j_lo = bucket_t(spl_lo, sm.btab, vb, sv);
+        j_hi = (bid + 1u >= G || spl_hi == ~0ull) ? NB : bucket_t(spl_hi - 1ull, sm.btab, vb, sv) + 1u;
+        if (spl_hi <= spl_lo) j_hi = j_lo;
+    }
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
     TRACE(7);
+    // ranges' sizes (prefix: where each sorted range goes) and the CTAs' key counts (n)
+    uint32_t rsz = 0, rpre = 0, n = 0;
+    bool fallback = (a.flags & kStepForceFallback) != 0;
+    {
+        const uint32_t v = tid < G ? __ldcg(&rcur[tid]) : 0u, q = tid < G ? __ldcg(&b.nk_part[tid]) : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_u32<kFT>(v, sm.l.w32, &tot);
+        if (tid < G) sm.l.rsz[tid] = v | (v > (uint32_t)kKcap ? 0x80000000u : 0u);
+        if (tid < G) sm.l.rpre[tid] = ex;
+        uint32_t nn;
+        (void)block_excl_scan_u32<kFT>(q, sm.l.w32, &nn);
+        n = nn;
+        fallback = __syncthreads_or(fallback || v > (uint32_t)kKcap) != 0;
+        rsz = sm.l.rsz[bid] & 0x7fffffffu;
+        rpre = sm.l.rpre[bid];
+    }
+    const uint32_t r_end0 = sm.l.rsz[0] & 0x7fffffffu;
+    // head-only mode (F3): CTA 0 ranks the head; the others stop here, unless the head range
+    // does not hold the keys the admission needs (then every range is sorted)
+    const bool head_only = head_mode && !fallback && r_end0 >= min(n, a.max_batch + 32u);
+    // positions of the next step's splitters in this step's order: the head (range 0) ends
+    // at max_batch + kHeadMargin keys, the other ranges share the rest evenly
+    const uint32_t q1 = min(n, a.max_batch + kHeadMargin);
+    auto qpos = [&](uint32_t s) -> uint32_t {  // s = 1 .. G-1
+        return q1 + (uint32_t)(((uint64_t)(s - 1u) * (uint64_t)(n - q1)) / (uint64_t)max(G - 1u, 1u));
+    };
+    unsigned long long* spl_next = b.spl + (size_t)(a.parity ^ 1u) * kSplG;
+    if (head_only && bid == G - 1u)  // the splitters are kept: the other ranges were not sorted
+        for (uint32_t s2 = tid; s2 <= (uint32_t)kMaxCtas; s2 += kFT)
+            spl_next[s2] = __ldcg(&b.spl[(size_t)a.parity * kSplG + s2]);
 
     // ---------------- L: sort the key ranges
     uint32_t final_buf, passes;
     bool head_dw = false;  // CTA 0: demands / state words of its head in sm.l.b (sorted order)
-    if (!fallback) {
-        const uint32_t rn = r_hi - r_lo;
+    bool written = false;  // the range sort wrote the sorted range to keys1 itself
+    if (!fallback && (!head_only || bid == 0)) {
+        const uint32_t rn = rsz;
+        const uint64_t* src = b.keys[0] + (size_t)bid * kKcap;
         const long long l_t0 = clock64();
         unsigned long long g_t0 = 0;
         if (b.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
@@ -1133,48 +1370,49 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
         if (rn <= kSmallSort && !(a.tune & 4u)) {
             TRACE(13);
             if (bid == 0) {
-                small_sort<true>(sm.l, b.keys[0] + r_lo, rn, c, &b.pool, a.id_base_mod);
+                small_sort<true>(sm.l, src, rn, c, &b.pool, a.id_base_mod);
                 head_dw = true;
             } else {
-                small_sort<false>(sm.l, b.keys[0] + r_lo, rn, c, nullptr, 0u);
+                small_sort<false>(sm.l, src, rn, c, nullptr, 0u);
             }
-        } else if (bid == 0 && rn <= kHeadPre && j_hi - j_lo > 2u * rn && j_hi - j_lo <= 32768u &&
-                   !(a.tune & 16u) &&
-                   head_sparse_sort(sm.l, b.keys[0] + r_lo, rn, c, half, j_lo, j_hi - j_lo, b.pool,
-                                    a.id_base_mod)) {
+        } else if (bid != 0) {  // an ordinary range: linear-digit counting sort, straight to the output
+            TRACE(13);
+            written = range_sort_loop(sm.l, src, rn, b.keys[1] + rpre, spl_lo, key_hi, vb, tr ? tr + 32 : nullptr);
+            if (!written) {  // a counter held too many keys: sort the placed range by LSD
+                unsigned long long o, an;
+                block_or_and(sm.l, sm.l.a, rn, o, an);
+                const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
+                if (r != sm.l.a)
+                    for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
+                __syncthreads();
+            }
+        } else if (rn <= kHeadPre && j_hi - j_lo > 2u * rn && j_hi - j_lo <= 32768u && !(a.tune & 16u) &&
+                   head_sparse_sort(sm.l, src, rn, c, sm.btab, j_lo, j_hi - j_lo, b.pool, a.id_base_mod)) {
             TRACE(13);
             head_dw = true;
-        } else if (j_hi - j_lo < (uint32_t)kSubBuckets) {
+        } else if (j_hi - j_lo < (uint32_t)kSubBuckets) {  // CTA 0's head: bucket sort, admission loads staged
             TRACE(13);
-            if (bid == 0 && rn <= kHeadPre)
-                head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c,
-                                                                      half, tr ? tr + 16 : nullptr, &b.pool,
-                                                                      a.id_base_mod);
-            else if (rn <= 3u * kFT)  // fewer keys per thread: less code on the executed path
-                (void)range_sort<3, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
-                                           tr ? tr + 16 : nullptr);
-            else if (rn <= 7u * kFT)
-                (void)range_sort<7, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
-                                           tr ? tr + 16 : nullptr);
-            else
-                (void)range_sort<kLocalItems, false>(sm.l, b.keys[0] + r_lo, rn, T, j_lo, j_hi, c, half,
-                                                     tr ? tr + 16 : nullptr);
-        } else {  // a sparse range over very many buckets: sort the two parts by bucket runs
-            for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][r_lo + i]);
-            TRACE(13);
-            // starving keys come first; sort the two parts separately (buckets [0, half)
-            // hold the starving keys)
-            const uint32_t key_top = c.SB + c.IB;
-            uint32_t ns = 0;
-            for (uint32_t i = tid; i < rn; i += kFT) ns += ((sm.l.a[i] >> key_top) & 1ull) ? 0u : 1u;
-            {
-                uint32_t tot;
-                (void)block_excl_scan_u32<kFT>(ns, sm.l.w32, &tot);
-                ns = tot;
+            if (rn <= kHeadPre)
+                head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, src, rn, j_lo, j_hi, c, sm.btab,
+                                                                      tr ? tr + 16 : nullptr, &b.pool, a.id_base_mod);
+            else if (!(written = range_sort_loop(sm.l, src, rn, b.keys[1] + rpre, spl_lo, key_hi, vb, nullptr))) {
+                unsigned long long o, an;  // a counter held too many keys: sort the placed range by LSD
+                block_or_and(sm.l, sm.l.a, rn, o, an);
+                const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
+                if (r != sm.l.a)
+                    for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
+                __syncthreads();
             }
-            local_sort(sm.l, sm.l.a, sm.l.b, ns, T, j_lo, min(j_hi, half), tr ? tr + 16 : nullptr);
-            local_sort(sm.l, sm.l.a + ns, sm.l.b + ns, rn - ns, T, max(j_lo, half), j_hi, tr ? tr + 24 : nullptr,
-                       tr ? tr + 32 : nullptr);
+        } else {  // a sparse range over very many buckets: stable LSD over the varying digits
+            for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&src[i]);
+            __syncthreads();
+            TRACE(13);
+            unsigned long long o, an;
+            block_or_and(sm.l, sm.l.a, rn, o, an);
+            const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
+            if (r != sm.l.a)
+                for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
+            __syncthreads();
         }
         TRACE(14);
         if (b.trace && tid == 0) {
@@ -1183,17 +1421,38 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
             b.trace[(size_t)bid * kTraceSlots + 26] = g_t0;
             b.trace[(size_t)bid * kTraceSlots + 27] = g_t1;
         }
-        if (tid == 0 && bid != 0 && rn >= 1024u && !head_only) {
-            // this CTA's range-sort cycles per key, for the next steps' range weights (EMA;
+        if (tid == 0 && bid != 0 && rn >= 1024u) {
+            // this CTA's range-sort cycles per key, for the cold steps' range weights (EMA;
             // the CTA -> SM placement of the cooperative launch is stable in practice)
             const float cst = __fdividef((float)(clock64() - l_t0), (float)rn);
             const float old = b.cta_cost[bid];
             b.cta_cost[bid] = old > 0.f ? 0.75f * old + 0.25f * cst : cst;
         }
-        for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][r_lo + i] = sm.l.a[i];
+        if (!written)
+            for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][rpre + i] = sm.l.a[i];
+        __syncthreads();  // the range's keys are in place (visible to this CTA's threads)
+        // the next step's splitters that fall in this range, and the largest key
+        if (!head_only && tid >= 1u && tid < G) {
+            const uint32_t q = qpos(tid);
+            if (q >= rpre && q < rpre + rn) spl_next[tid] = __ldcg(&b.keys[1][q]);
+        }
+        if (!head_only && tid == (uint32_t)kMaxCtas && rn && rpre + rn == n) spl_next[kMaxCtas] = __ldcg(&b.keys[1][n - 1u]);
         final_buf = 1;
         passes = 1;
-    } else {
+    } else if (fallback) {
+        {   // the keys compacted into keys0 (this CTA's at the prefix of the CTAs' key counts)
+            uint32_t off = 0;
+            {
+                const uint32_t q = tid < bid ? __ldcg(&b.nk_part[tid]) : 0u;
+                uint32_t tot;
+                (void)block_excl_scan_u32<kFT>(q, sm.l.w32, &tot);
+                off = tot;
+            }
+            // kb2 (this CTA's keys, compacted by R) is intact: since the barrier only PhaseL's
+            // small arrays past sm.l.b (w32, rsz, rpre) were written
+            for (uint32_t i = tid; i < nk_cta; i += kFT) b.keys[0][off + i] = kb2[i];
+            grid_barrier(b.flags, G, ++bar);
+        }
         {   // OR / AND of the keys (the LSD skips digit positions that never vary)
             unsigned long long o = 0, an = ~0ull;
             for (uint32_t i = bid * kFT + tid; i < n; i += G * kFT) {
@@ -1217,15 +1476,32 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
         }
         passes = lsd_sort_global(b, n, b.kmask, G, sm.g, bar);
         final_buf = passes & 1u;
+    } else {
+        final_buf = 1;  // head-only: CTA 0 ranked the head; this CTA is done
+        passes = 1;
+    }
+    // the next step's splitters past the last key, and (after the LSD) all of them
+    if (bid == 0 && tid < (uint32_t)kMaxCtas && !head_only) {
+        if (tid == 0) spl_next[0] = 0ull;
+        else if (tid >= G || qpos(tid) >= n) spl_next[tid] = ~0ull;
+    }
+    unsigned long long pinned_all = 0;
+    if (bid == 0 && warp == 0) {  // A5's budget: the pinned total
+        for (uint32_t r = lane; r < G; r += 32) pinned_all += __ldcg(&b.pin_part[r]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pinned_all += __shfl_xor_sync(0xffffffffu, pinned_all, o);
     }
 
     TRACE(8);
     // ---------------- A: admission by CTA 0
     // CTA 0 may start as soon as the head it needs is sorted: without the fallback
-    // the keys [0, rb[1]) are sorted by CTA 0 itself.
+    // the keys [0, rsz[0]) are sorted by CTA 0 itself.
     const uint32_t need = min(n, a.max_batch);  // the admission (or the merge records) reads keys [0, need)
     const bool wait = fallback || r_end0 < need;
     if (wait) grid_barrier(b.flags, G, ++bar);
+    if (fallback && bid == 0 && tid >= 1u && tid < G && qpos(tid) < n)
+        spl_next[tid] = __ldcg(&b.keys[final_buf][qpos(tid)]);
+    if (fallback && bid == 0 && tid == (uint32_t)kMaxCtas && n) spl_next[kMaxCtas] = __ldcg(&b.keys[final_buf][n - 1u]);
     if (bid != 0) return;
     if (tid == 0) sm.l.adm.w64[0] = pinned_all;
     __syncthreads();
@@ -1238,7 +1514,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
         ctl->n_ranked = head_only ? r_end0 : n;  // head-only: keys [0, hb_r) are ranked
     }
     TRACE(15);
-    const uint64_t* head = wait ? b.keys[final_buf] : sm.l.a;  // CTA 0 holds [0, need) itself unless it waited
+    // CTA 0 holds [0, need) in shared memory unless it waited (or its range sort wrote them out)
+    const uint64_t* head = (wait || written) ? b.keys[final_buf] : sm.l.a;
     const bool dw = head_dw && !wait;
     if (a.flags & kStepMerge) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
@@ -1358,7 +1635,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(Bufs b, Cost c, StepArgs a, co
 }  // namespace
 
 static_assert(kFusedSmemBytes <= 232448, "fused kernel shared memory exceeds 227 KB");
-size_t fused_smem_bytes() { return sizeof(FusedSmem); }  // the union (in-kernel merge scratch limit)
+size_t fused_smem_bytes() { return offsetof(FusedSmem, btab); }  // the union (in-kernel merge scratch limit)
 
 int fused_blocks_per_sm() {
     int nb = 0;
@@ -1371,6 +1648,22 @@ int fused_blocks_per_sm() {
 }
 
 uint32_t fused_max_buckets() { return kMaxBuckets; }
+
+// The initial bucket table (before any step has measured the key distribution): every
+// octave (ns, e) of v's bit length gets 2^min(7, e-1) buckets -- the fixed float-like
+// buckets of 7 mantissa bits.  bt_update replaces it after the first step.
+void fused_default_table(uint32_t vb, uint32_t* out) {
+    uint32_t base = 0;
+    for (uint32_t o = 0; o < kTabNB; o++) {
+        const uint32_t e = o % 65u;
+        if (e > vb) { out[o] = base; continue; }
+        const uint32_t m = e >= 1u ? std::min(7u, e - 1u) : 0u;
+        out[o] = base | ((e >= 1u ? e - 1u - m : 0u) << 16) | (m << 24);
+        base += 1u << m;
+    }
+    out[kTabNB] = base;
+    for (uint32_t o = kTabNB + 1; o < (uint32_t)kTabW; o++) out[o] = 0;
+}
 
 cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t grid,
                          cudaStream_t s) {

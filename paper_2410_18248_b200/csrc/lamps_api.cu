@@ -87,6 +87,7 @@ struct lamps_s {
     Bufs b{};
     uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
     bool fused = false;
+    bool cold = true;     // fused: no splitters yet (StepArgs.cold); a fused step writes the next's
     uint32_t world = 1, rank = 0;
     bool merge = false;  // merge_mode(cfg)
     // peer-memory transport
@@ -206,7 +207,8 @@ size_t carve(lamps_t* h, uint8_t* base) {
     Layout L;
     size_t o_soa[10];  // sfc, ctx, pre, api, resp, post, pend, stamp, score cache lo / hi
     for (int i = 0; i < 10; i++) o_soa[i] = L.take((size_t)cap_pad * 4);
-    size_t o_keys0 = L.take(((size_t)cap_pad + kSortTile) * 8);
+    // keys0: in the fused kernel, range r's keys are written to [r * kFusedKcap, ...)
+    size_t o_keys0 = L.take(std::max((size_t)cap_pad + kSortTile, h->fused ? (size_t)h->fused_grid * kFusedKcap : 0) * 8);
     size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
     const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
     size_t o_kmask = L.take((size_t)2 * gmax * 8);
@@ -215,6 +217,10 @@ size_t carve(lamps_t* h, uint8_t* base) {
     const size_t bsum_lsd = (size_t)2 * gmax * kBins * 4;
     size_t o_bsum = L.take(bsum_lsd);
     size_t o_btot = h->fused ? L.take((size_t)2 * fused_max_buckets() * 4) : 0;
+    size_t o_btab = h->fused ? L.take((size_t)2 * 136 * 4) : 0;
+    size_t o_spl = h->fused ? L.take((size_t)2 * 264 * 8) : 0;
+    size_t o_rcur = h->fused ? L.take((size_t)2 * 256 * 4) : 0;
+    size_t o_nkp = L.take((size_t)gmax * 4);
     size_t o_ctl = L.take(sizeof(Ctl));
     size_t o_ctasm = L.take((size_t)gmax * 4);
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
@@ -245,6 +251,10 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.flags = reinterpret_cast<uint32_t*>(base + o_flags);
     h->b.blocksum = reinterpret_cast<uint32_t*>(base + o_bsum);
     h->b.btot = h->fused ? reinterpret_cast<uint32_t*>(base + o_btot) : nullptr;
+    h->b.btab = h->fused ? reinterpret_cast<uint32_t*>(base + o_btab) : nullptr;
+    h->b.spl = h->fused ? reinterpret_cast<unsigned long long*>(base + o_spl) : nullptr;
+    h->b.rcur = h->fused ? reinterpret_cast<uint32_t*>(base + o_rcur) : nullptr;
+    h->b.nk_part = reinterpret_cast<uint32_t*>(base + o_nkp);
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;
     h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);
@@ -379,6 +389,7 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     a.n_ret = h->fused ? h->ret_pending : 0u;
     a.n_sub = h->fused ? h->sub_pending : 0u;
     a.inl = h->fused && h->inl_pending ? 1u : 0u;
+    a.cold = h->cold ? 1u : 0u;
     if (h->merge) a.flags |= kStepMerge;
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
         a.flags |= kStepP2P;
@@ -407,6 +418,7 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     record_timing(h, 1);
     if (h->fused) {
         CU(h, launch_fused(h->b, h->cost, a, a.inl ? &h->inl : nullptr, h->fused_grid, h->stream));
+        h->cold = false;  // the kernel wrote the next step's splitters
         record_timing(h, 2);
         record_timing(h, 3);
     } else {
@@ -794,6 +806,7 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
     c.policy = cfg->policy;
     c.interval = cfg->score_interval;
     c.cache = (cfg->policy == LAMPS_POLICY_LAMPS && cfg->score_interval > 1) ? 1u : 0u;
+    c.lean = (c.fast && c.lgB >= 1 && cfg->policy == LAMPS_POLICY_LAMPS && !c.cache) ? 1u : 0u;
     h->hstate.assign(h->cap, H_FREE);
     auto cleanup = [&](int code, const char*) { lamps_free(h); return code; };
     if (cudaMemsetAsync(h->ws, 0, need, h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "memset");
@@ -828,6 +841,13 @@ int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lam
         h->tev.resize((size_t)kTimingRing * 5);
         for (auto& e : h->tev)
             if (cudaEventCreate(&e) != cudaSuccess) return cleanup(LAMPS_ECUDA, "event");
+    }
+    if (h->fused) {  // both parities' bucket tables start as the default (kernels_fused.cu)
+        uint32_t* tab = static_cast<uint32_t*>(h->h_ingest);
+        fused_default_table(cfg->score_bits + cfg->id_bits, tab);
+        std::memcpy(tab + 136, tab, 136 * 4);
+        if (cudaMemcpyAsync(h->b.btab, tab, 2 * 136 * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+            return cleanup(LAMPS_ECUDA, "bucket table");
     }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(LAMPS_ECUDA, "sync");
     if (h->merge && cfg->transport == LAMPS_XPORT_P2P) {
@@ -1166,6 +1186,7 @@ int lamps_pool_import(lamps_t* h, const lamps_pool_io* io, uint64_t id_base, uin
     h->ret_pending = 0;
     h->sub_pending = 0;
     h->inl_pending = false;
+    h->cold = true;  // the imported pool's distribution is unknown: bucket-histogram ranges first
     const Pool& P = h->b.pool;
     const uint32_t* src[6] = {io->ctx, io->pre_rem, io->api_ticks, io->resp_len, io->post_len, io->pending};
     uint32_t* dst[6] = {P.ctx, P.pre, P.api, P.resp, P.post, P.pend};

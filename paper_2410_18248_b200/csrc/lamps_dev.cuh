@@ -51,6 +51,7 @@ struct Cost {
     uint32_t policy;     // POL_* (R25)
     uint32_t interval;   // selective score update interval (R26)
     uint32_t cache;      // policy == LAMPS && interval > 1: the score cache is in use
+    uint32_t lean;       // fast && B >= 2 && LAMPS policy && !cache: score_lean applies (per-slot check)
 };
 
 // Per-slot bound of the fast path (see strategy_score_fast): ctx+pre+resp+post < 2^20.
@@ -188,6 +189,47 @@ __device__ __forceinline__ uint32_t strategy_score_fast(uint32_t ctx, uint32_t p
     *score = s > c.score_max ? c.score_max : s;
     *wp_o = wp; *wd_o = wd; *ws_o = ws;
     return strat;
+}
+
+// ---------------------------------------------------------------------------
+// Lean fast path (the fused kernel's score phase): the same values as
+// strategy_score_fast, computed branch-free with fewer instructions.  Valid
+// when Cost::lean (fast bounds, B >= 2, LAMPS policy, no score cache) and the
+// slot passes the per-slot fast check.  rp / pp = resp / post if has_api, else 0.
+//   * F(n) = (Q+1)(n+R)/2 = (Q+1) * ((n+R) >> 1): n+R = QB+2R is even for even B
+//   * the two ramps share one multiply by tau:
+//       tau*(F(ci)-F(ctx)) + tau*(F(ce)-F(cr)) = tau*((F(ci)+F(ce)) - (F(ctx)+F(cr)))
+//     (without an API rp = pp = 0, so ce = cr = ci and the second ramp vanishes)
+//   * the three API-phase areas are all formed and the argmin selects one (no
+//     divergence between lanes of different strategies); each is bounded by the
+//     host's proof (fast_bounds_ok bounds the largest of the three)
+// a*b for a < 2^32 and any b whose product stays < 2^64 (two IMADs)
+__device__ __forceinline__ uint64_t mul32x64(uint32_t a, uint64_t b) {
+    return wide32(a, (uint32_t)b) + (wide32(a, (uint32_t)(b >> 32)) << 32);
+}
+__device__ __forceinline__ uint32_t score_lean(uint32_t ctx, uint32_t pre, uint32_t api, uint32_t rp, uint32_t pp,
+                                               uint32_t pend, uint32_t has, const Cost& c, uint64_t& sc,
+                                               uint64_t& wp, uint64_t& wd, uint64_t& ws) {
+    const uint32_t Bm1 = c.B - 1u, lg = c.lgB;
+    const uint32_t ci = ctx + pre, cr = ci + rp, ce = cr + pp;
+    auto F = [&](uint32_t n) { return wide32((n >> lg) + 1u, (n + (n & Bm1)) >> 1); };
+    const uint64_t D = (F(ci) + F(ce)) - (F(ctx) + F(cr));
+    uint64_t s = wide32((ctx + Bm1) >> lg, pend) + mul32x64((uint32_t)c.tau, D);
+    const uint32_t A1 = (uint32_t)c.A1, A2 = (uint32_t)c.A2;
+    const uint64_t tf = (wide32(A1, ci) + mul32x64(A2, wide32(ci, ci))) >> c.SH;   // T_fwd(C_i)
+    const uint64_t ts = ci ? (c.S0 + wide32((uint32_t)c.S1, ci)) >> c.SH : 0ull;  // T_swap(C_i)
+    const uint32_t cb = ci + (uint32_t)c.c_other;
+    wp = wide32(api, ci);           // Eq. (1)
+    wd = mul32x64(cb, tf);          // Eq. (2)
+    ws = mul32x64(cb, ts) << 1;     // Eq. (3)
+    const uint32_t strat = (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
+    const uint32_t bci = (ci + Bm1) >> lg, bcr = (cr + Bm1) >> lg;
+    const uint64_t tfr = (wide32(A1, cr) + mul32x64(A2, wide32(cr, cr))) >> c.SH;  // T_fwd(C_i + resp)
+    const uint64_t aP = wide32(bci, api), aD = mul32x64(bcr, tfr), aS = mul32x64(bci, ts) << 1;
+    s += has ? (strat == STR_P ? aP : (strat == STR_D ? aD : aS)) : 0ull;
+    sc = s > c.score_max ? c.score_max : s;
+    if (!has) wp = wd = ws = 0;
+    return has ? strat : STR_NONE;
 }
 
 // Lanes of the warp holding the same 8-bit digit d (0..255; 256 = empty lane),

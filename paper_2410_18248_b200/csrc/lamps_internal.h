@@ -91,6 +91,8 @@ struct StepArgs {
     uint32_t n_sub;         // fused path: arrivals staged at Bufs::arrivals, applied in the prologue
     uint32_t inl;           // fused path: returns, arrivals, events read from the kernel's
                             // InlineStage parameter (records in that order) instead of Bufs
+    uint32_t cold;          // fused: no splitters from a previous step (first step after init /
+                            // import): ranges from a bucket histogram instead
     uint32_t tune;          // A/B knobs of the fused kernel (env LAMPS_TUNE at init; 0 = defaults):
                             // bit 0 uniform key ranges (no speed weights), bit 1 nearest-
                             // instead of first-boundary snapping of the range ends, bit 3
@@ -114,6 +116,12 @@ struct Bufs {
     uint32_t* blocksum;      // LSD: [2][grid][kBins] digit counts
     uint32_t* btot;          // fused: [2][buckets] bucket totals by step parity; the other
                              // parity's array is zeroed during the step (zero at init)
+    uint32_t* btab;          // fused: [2][136] bucket tables by step parity (kernels_fused.cu
+                             // bucket_t); each cold step writes the next step's (bt_update)
+    unsigned long long* spl; // fused: [2][256] range splitters by step parity; each step writes
+                             // the next step's from its own sorted order
+    uint32_t* rcur;          // fused: [2][256] keys written to each range, by step parity
+    uint32_t* nk_part;       // fused: [grid] keys of each CTA
     uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity
@@ -148,6 +156,7 @@ int sort_blocks_per_sm();  // occupancy of the persistent sort kernel
 size_t fused_smem_bytes();
 int fused_blocks_per_sm();
 uint32_t fused_max_buckets();
+void fused_default_table(uint32_t vb, uint32_t* out136);  // the initial bucket table
 cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t grid,
                          cudaStream_t s);
 cudaError_t launch_merge(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);

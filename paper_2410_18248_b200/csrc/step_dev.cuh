@@ -143,19 +143,15 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
 template <int NT, int R>
 __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, uint32_t* w32,
                                                    uint32_t* add = nullptr) {
+    // the R words are read twice from shared memory (sum, then rewrite) instead of being
+    // held in registers: no spills for large R
     constexpr int NW = NT / 32;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t j0 = threadIdx.x * (uint32_t)R;
-    const bool mine = j0 < L;  // threads past the end skip their (predicated) R words
-    uint32_t v[R];
+    const uint32_t jn = j0 < L ? min((uint32_t)R, L - j0) : 0u;  // words of this thread
     uint32_t s = 0;
-    if (mine) {
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            v[r] = j0 + r < L ? arr[j0 + r] : 0u;
-            s += v[r];
-        }
-    }
+#pragma unroll 4
+    for (uint32_t r = 0; r < jn; r++) s += arr[j0 + r];
     uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -178,15 +174,12 @@ __device__ __forceinline__ uint32_t smem_excl_scan(uint32_t* arr, uint32_t L, ui
     __syncthreads();
     uint32_t run = w32[warp] + x - s;
     const uint32_t total = w32[NW];
-    if (mine) {
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-            if (j0 + r < L) {
-                arr[j0 + r] = run;
-                if (add) add[j0 + r] += run;
-            }
-            run += v[r];
-        }
+#pragma unroll 4
+    for (uint32_t r = 0; r < jn; r++) {
+        const uint32_t v = arr[j0 + r];
+        arr[j0 + r] = run;
+        if (add) add[j0 + r] += run;
+        run += v;
     }
     __syncthreads();
     return total;
@@ -339,6 +332,23 @@ __device__ __forceinline__ bool score_slot(const Pool& P, const Cost& c, uint32_
         d[0] = wp; d[1] = wd; d[2] = ws; d[3] = sc;
     }
     return true;
+}
+
+// score_slot out of line: the fused kernel's score phase inlines only score_lean and
+// calls this for the slots (or configurations) the lean path does not cover
+// (exact 128-bit path, baseline policies, score cache).
+struct ColdOut {
+    unsigned long long key;
+    uint32_t w;
+};
+template <bool DBG>
+__device__ __noinline__ ColdOut score_slot_cold(const Pool& P, const Cost& c, uint32_t id_base_mod,
+                                                unsigned long long* dbg, uint32_t slot, uint32_t w, uint32_t ctx,
+                                                uint32_t pre, uint32_t api, uint32_t resp, uint32_t post,
+                                                uint32_t pend) {
+    uint64_t key = 0;
+    (void)score_slot<DBG>(P, c, id_base_mod, dbg, slot, w, ctx, pre, api, resp, post, pend, key);
+    return ColdOut{key, w};
 }
 
 // The step summary into mapped host memory (one thread, after the Ctl fields are final).

@@ -36,10 +36,11 @@ if os.environ.get("TRACE"):
         if it >= 3:
             acc.append(t)
     t = np.stack(acc)  # steps x cta x 16
-    segs = [("score", 0, 1), ("publish", 1, 2), ("barrier1", 2, 3), ("exchange", 3, 4), ("barrier2", 4, 5),
-            ("X load T/H", 5, 10), ("X starts", 10, 11), ("X scatter", 11, 12), ("X ranges", 12, 6),
-            ("barrier3", 6, 7), ("L load", 7, 13), ("L sort", 13, 14), ("L store", 14, 8),
-            ("A pinned", 8, 15), ("A admit", 15, 9)]
+    # warm steps: S, R (range counting sort + run stores), barrier, L, A
+    segs = [("score", 0, 1), ("R search+count", 1, 4), ("R run offsets", 4, 5), ("R local place", 5, 12),
+            ("R store", 12, 6), ("barrier", 6, 7),
+            ("L prep", 7, 13), ("L sort", 13, 14), ("L store+spl", 14, 8),
+            ("A wait/pinned", 8, 15), ("A admit", 15, 9)]
     print("phase durations us (median over steps of max / mean over CTAs):")
     for nm, a0, a1 in segs:
         d = (t[:, :, a1] - t[:, :, a0]) / 1.965e3
@@ -57,13 +58,13 @@ if os.environ.get("TRACE"):
     ms, nst = st.timing() if False else (None, None)
     if os.environ.get("PERCTA"):
         t0 = acc[-1]
-        print("cta  keys buckets  Lsort_us  [P+zero  count+scan  place+rank  refine]  big  score_us  Xscatter_us")
+        print("cta  sm  keys  score  R   barr  Lsort [load+minmax zero count scan place rank final]  store")
         for cta in range(t0.shape[0]):
             r = t0[cta]
-            sub = [(r[17 + i] - r[16 + i]) / 1965 for i in range(4)]
-            print(f"{cta:3d} {r[30]:6d} {r[31]:6d} {(r[14]-r[13])/1965:8.2f}  " + " ".join(f"{x:6.2f}" for x in sub) +
-                  f"  {r[21]:4d} {(r[1]-r[0])/1965:7.2f} {(r[12]-r[11])/1965:7.2f} {r[28]:4d}"
-                  f" {(r[27]-r[26])/1000:7.2f} {(r[26]-t0[:,26].min())/1000:7.2f} {r[24]/1000:7.2f} {r[25]/1965:7.2f}")
+            d = lambda a, b: (r[b] - r[a]) / 1965
+            sub = [(r[33 + i] - r[32 + i]) / 1965 if r[32 + i] and r[33 + i] else 0.0 for i in range(7)]
+            print(f"{cta:3d} {r[28]:4d} {r[30]:6d} {d(0,1):6.2f} {d(1,6):5.2f} {d(6,7):5.2f} {d(13,14):6.2f} [" +
+                  " ".join(f"{x:5.2f}" for x in sub) + f"] {d(14,8):5.2f}")
     if os.environ.get("LEVELS"):
         t0 = acc[-1]
         print("cta  keys  per-level (us, groups) of the non-starving part; level-0 substeps or/and,count,scan,scatter,final")

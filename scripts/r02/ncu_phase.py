@@ -56,3 +56,7 @@ for nm, a in sorted(agg.items(), key=lambda x: -x[1][0]):
 if "--lines" in sys.argv:
     for (f, l), d in sorted(per.items(), key=lambda x: -x[1][0])[:40]:
         print(f"{f}:{l} {100*d[0]/ts:5.1f}% {d[1]}")
+if "--stalls" in sys.argv:
+    for (f, l), d in sorted(per.items(), key=lambda x: -x[1][0])[:25]:
+        top = ", ".join(f"{k} {100*v/max(d[0],1):.0f}%" for k, v in d[2].most_common(4))
+        print(f"{f}:{l} {100*d[0]/ts:5.1f}% inst {d[1]:8d}  {top}")
