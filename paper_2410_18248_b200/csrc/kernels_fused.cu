@@ -41,7 +41,11 @@ constexpr int kMaxCtas = 256;               // range weights: grid size limit
 // whose steps read the odd multiples of 128, 64, ... -- same banks without the padding)
 constexpr int kSplPad = kMaxCtas + 1 + (kMaxCtas + 1) / 16 + 1;
 __host__ __device__ constexpr uint32_t spl_pos(uint32_t i) { return i + (i >> 4); }
-constexpr int kSplG = 264;  // global splitters per parity: [0, 256) splitters, [256] the largest key
+// Global splitter grid per parity (written by each step for the next): fine[f], f = 0 .. 16 G;
+// range r = keys in [fine[16 r], fine[16 r + 16]), the 15 entries between are its quantiles
+// (the range sort's piecewise-linear digit); fine[16 G] = the largest key
+constexpr int kSeg = 16;
+constexpr int kSplG = kSeg * kMaxCtas + 16;
 
 struct PhaseS {                  // S, H, X (cold), R
     uint64_t kbuf[kKcap];        // 80 KB: this CTA's keys (compacted, in no particular order)
@@ -88,7 +92,9 @@ struct PhaseL {                  // L
     unsigned long long gor[kMaxBig / 4], gand[kMaxBig / 4];
     unsigned long long red[2][kFW];
     AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
-    uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size (bit 31: overflow) and position
+    uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size and position in the order
+    unsigned long long fine[kSeg + 1], fcode[kSeg + 1];  // this range's grid entries, their key codes
+    uint32_t shs[kSeg];                                  // range sort: per segment, the digit's shift
 };
 struct FusedSmem {
     union {
@@ -705,55 +711,87 @@ __device__ __forceinline__ unsigned long long key_code(uint64_t k, uint32_t vb) 
 }
 // Sort of a CTA's key range (rn <= kKcap keys at src, global, L2-resident) straight into its
 // place in the ranked order (out, global), in compact loops (this code runs once per step and
-// is fetched cold, so no per-thread item arrays): one counting pass on a linear digit of the
-// key code between the range's bounds lo..hi (the splitters: quantiles of the previous
-// order, so ~2 counters per key), d = (code(k) - code(lo)) >> sh clamped to the counters;
-// placement by digit into sm.a; then every key's rank inside its counter by comparison
-// (<= kRangeRankM keys; unique keys: the number of smaller keys) gives its final position.
-// Returns false if a counter held more keys: sm.a then holds the range (placed by digit)
-// and the caller sorts it otherwise.
+// is fetched cold, so no per-thread item arrays).  One counting pass on a piecewise-linear
+// digit: the range's 16 segments between its grid entries sm.fine[0..16] (quantiles of the
+// previous step's order, so each segment holds ~1/16 of the keys) get W counters each, a key's
+// counter is seg * W + (code(k) - code(fine[seg])) >> shift(seg), clamped -- monotone in the
+// key, ~2 counters per key whatever the density inside the range.  Placement by digit into
+// sm.a, then each key's rank inside its counter by comparison (<= kRangeRankM keys; unique keys:
+// the number of smaller keys) gives its final position.  Returns false if a counter held more
+// keys: sm.a then holds the range (placed by digit) and the caller sorts it otherwise.
+// CTA 0 (pool != nullptr, head staging): the admission's per-key loads (ctx for the demand
+// blk(ctx + 1), the state word) are issued in the rank pass and land in dsm / wsm (shared
+// memory) by final position, and the ranked keys stay in sm.b: A5 then needs no global round
+// trip for its head.
 __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
-                                                uint64_t* __restrict__ out, unsigned long long lo,
-                                                unsigned long long hi, uint32_t vb, unsigned long long* tr) {
+                                                uint64_t* __restrict__ out, uint32_t vb, unsigned long long* tr,
+                                                const Pool* pool = nullptr, uint32_t id_base_mod = 0,
+                                                const Cost* cc = nullptr, uint32_t* dsm = nullptr,
+                                                uint32_t* wsm = nullptr) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);  // <= 2^14 + 1 counters
-    uint32_t* dv = sm.pos;                              // per key: digit | order << 14
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);                      // <= 2^13 + 1 counters
+    uint16_t* dp = reinterpret_cast<uint16_t*>(sm.b) + 2u * ((1u << 13) + 4u);  // per position: digit
+    uint32_t* dv = sm.pos;                                                   // per key: digit | order << 13
     uint64_t* A = sm.a;
     LTRACE(0);
-    const unsigned long long cmn = key_code(lo, vb), cmx = key_code(hi, vb);
-    const unsigned long long span = cmx > cmn ? cmx - cmn : 0ull;
-    const uint32_t cb = min(rn > 1u ? 33u - (uint32_t)__clz(rn - 1u) : 0u, 14u);  // ~2 counters per key
-    const uint32_t nbits = 64u - (uint32_t)__clzll((long long)span);
-    const uint32_t sh = nbits > cb ? nbits - cb : 0u;
-    const uint32_t ncnt = (uint32_t)min(span >> sh, (unsigned long long)((1u << cb) - 1u)) + 1u;
-    auto digit = [&](uint64_t k) -> uint32_t {
-        const unsigned long long c = key_code(k, vb);
-        const unsigned long long d = (c > cmn ? c - cmn : 0ull) >> sh;
-        return (uint32_t)min(d, (unsigned long long)(ncnt - 1u));
-    };
+    const uint32_t cb = max(min(rn > 1u ? 33u - (uint32_t)__clz(rn - 1u) : 0u, 13u), 4u);  // ~2-4 counters per key
+    const uint32_t lw = cb - 4u, W = 1u << lw, ncnt = (uint32_t)kSeg * W;  // W counters per segment
+    uint32_t* shs = sm.shs;  // per segment: shift of the code difference
+    if (tid < (uint32_t)kSeg) {
+        const unsigned long long d = sm.fcode[tid + 1] > sm.fcode[tid] ? sm.fcode[tid + 1] - sm.fcode[tid] : 0ull;
+        const uint32_t nb = 64u - (uint32_t)__clzll((long long)d);
+        shs[tid] = nb > lw ? nb - lw : 0u;
+    }
     for (uint32_t i = tid; i <= ncnt; i += kFT) cnt[i] = 0u;
     __syncthreads();
+    auto digit = [&](uint64_t k) -> uint32_t {
+        uint32_t sg = 0;
+#pragma unroll
+        for (uint32_t st = kSeg / 2; st; st >>= 1) sg = k >= sm.fine[sg + st] ? sg + st : sg;
+        const unsigned long long c = key_code(k, vb), c0 = sm.fcode[sg];
+        const unsigned long long d = (c > c0 ? c - c0 : 0ull) >> shs[sg];
+        return sg * W + (uint32_t)min(d, (unsigned long long)(W - 1u));
+    };
     LTRACE(1);
-    for (uint32_t i = tid; i < rn; i += kFT) {
-        const uint32_t d = digit(__ldcg(src + i));
-        dv[i] = d | (atomicAdd(&cnt[d], 1u) << 14);
+    for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {  // four loads in flight per thread
+        uint64_t kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) kk[u] = i0 + (uint32_t)u * kFT < rn ? __ldcg(src + i0 + (uint32_t)u * kFT) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t i = i0 + (uint32_t)u * kFT;
+            if (i < rn) {
+                const uint32_t d = digit(kk[u]);
+                dv[i] = d | (atomicAdd(&cnt[d], 1u) << 13);
+            }
+        }
     }
     __syncthreads();
     LTRACE(2);
-    (void)smem_excl_scan<kFT, (1 << 14) / kFT + 1>(cnt, ncnt, sm.w32);
+    (void)smem_excl_scan<kFT, (1 << 13) / kFT + 1>(cnt, ncnt, sm.w32);
     if (tid == 0) cnt[ncnt] = rn;
     LTRACE(3);
-    for (uint32_t i = tid; i < rn; i += kFT) {
-        const uint32_t v = dv[i];
-        A[cnt[v & 0x3fffu] + (v >> 14)] = __ldcg(src + i);
+    for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
+        uint64_t kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) kk[u] = i0 + (uint32_t)u * kFT < rn ? __ldcg(src + i0 + (uint32_t)u * kFT) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t i = i0 + (uint32_t)u * kFT;
+            if (i < rn) {
+                const uint32_t v = dv[i], d = v & 0x1fffu, p = cnt[d] + (v >> 13);
+                A[p] = kk[u];
+                dp[p] = (uint16_t)d;
+            }
+        }
     }
     __syncthreads();
     LTRACE(4);
     bool big = false;
     for (uint32_t p = tid; p < rn; p += kFT) {
         const uint64_t k = A[p];
-        const uint32_t d = digit(k), st = cnt[d], m2 = cnt[d + 1] - st;
+        const uint32_t d = dp[p], st = cnt[d], m2 = cnt[d + 1] - st;
         uint32_t r = 0;
         if (m2 <= 4u) {  // the common case: straight-line, predicated compares
             if (m2 > 1u) {
@@ -768,11 +806,40 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
             big = true;
             continue;
         }
-        out[st + r] = k;
+        dv[p] = st + r;  // final position (dv is free after the placement)
     }
     LTRACE(5);
+    if (__syncthreads_or(big)) return false;
+    // the ranked keys gathered in shared memory (sm.b: the counters are dead), then written out
+    // whole lines at a time (scattered 8-byte stores to lines not in L2 stall the store path)
+    uint64_t* B2 = sm.b;
+    for (uint32_t p = tid; p < rn; p += kFT) B2[dv[p]] = A[p];
+    __syncthreads();
+    if (dsm) {  // CTA 0: the admission's loads (L2 hits: the score phase read them), all in flight at once
+        for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
+            uint32_t cx[4], w[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t i = i0 + (uint32_t)u * kFT;
+                const uint32_t slot = i < rn ? (id_base_mod + (uint32_t)(B2[i] & cc->cap_mask)) & cc->cap_mask : 0u;
+                cx[u] = i < rn ? __ldcg(&pool->ctx[slot]) : 0u;
+                w[u] = i < rn ? __ldcg(&pool->sfc[slot]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t i = i0 + (uint32_t)u * kFT;
+                if (i < rn) {
+                    dsm[i] = (uint32_t)blk((uint64_t)cx[u] + 1u, *cc);
+                    wsm[i] = w[u];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    for (uint32_t i = tid; i < rn; i += kFT) out[i] = B2[i];
+    LTRACE(6);
 #undef LTRACE
-    return !__syncthreads_or(big);
+    return true;
 }
 
 // A small range (rn <= kSmallSort keys): ranked by comparison against all its keys (the
@@ -958,12 +1025,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\ncp.async.commit_group;" ::"r"(dst),
                      "l"(b.btab + (size_t)a.parity * kTabW + 4 * tid) : "memory");
     }
-    if (!a.cold && tid < (uint32_t)kMaxCtas) {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.s.spl[spl_pos(tid)]);  // + the max below
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;" ::"r"(dst),
-                     "l"(b.spl + (size_t)a.parity * kSplG + tid) : "memory");
+    if (!a.cold && tid <= (uint32_t)kMaxCtas) {  // the range splitters fine[16 r] (r < G), the largest key
+        if (tid < G || tid == (uint32_t)kMaxCtas) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.s.spl[spl_pos(tid)]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;" ::"r"(dst),
+                         "l"(b.spl + (size_t)a.parity * kSplG + kSeg * min(tid, G)) : "memory");
+        } else {
+            sm.s.spl[spl_pos(tid)] = ~0ull;
+        }
     }
-    if (!a.cold && tid == 0) sm.s.spl[spl_pos(kMaxCtas)] = __ldcg(b.spl + (size_t)a.parity * kSplG + kMaxCtas);
 
     TRACE(0);
     SmemTail& tail = *reinterpret_cast<SmemTail*>(smem_raw + sizeof(FusedSmem));
@@ -1247,9 +1317,22 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
                 sk = bucket_key(lo - 1u, true);
             }
             sm.s.spl[spl_pos(tid)] = sk;
-            if (bid == G - 1u) b.spl[(size_t)a.parity * kSplG + tid] = sk;  // head-only keeps them
         }
         __syncthreads();
+        // this step's grid (every CTA: its own range's quantiles are read back after the
+        // barrier; head-only steps keep the grid): splitters, and between two of them
+        // entries interpolated linearly in key space (no quantiles known yet)
+        for (uint32_t f = bid * kFT + tid; f <= kSeg * G; f += G * kFT) {
+            const uint32_t r = f / kSeg, j = f % kSeg;
+            const unsigned long long lo = sm.s.spl[spl_pos(r == G ? kMaxCtas : r)];
+            unsigned long long v = lo;
+            if (r < G && j) {
+                const unsigned long long hi = r + 1u < G ? sm.s.spl[spl_pos(r + 1u)] : sm.s.spl[spl_pos(kMaxCtas)];
+                const unsigned long long h2 = hi == ~0ull ? sm.s.spl[spl_pos(kMaxCtas)] : hi;
+                v = h2 > lo ? lo + (h2 - lo) / kSeg * j : lo;
+            }
+            b.spl[(size_t)a.parity * kSplG + f] = v;
+        }
     }
     else if (bid == G - 1u && tid < (uint32_t)kTabW) {
         b.btab[(size_t)(a.parity ^ 1u) * kTabW + tid] = sm.btab[tid];  // warm step: the table carries over
@@ -1266,16 +1349,29 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     uint8_t* const rv = rr + kKcap;                                        // [kKcap] range by position
     {
         const unsigned long long* spl = sm.s.spl;
-        for (uint32_t i = tid; i < npos; i += kFT) {
-            const uint32_t q = i >> 1;
-            if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
-            const uint64_t k = sm.s.kbuf[i];
-            uint32_t r = 0;
+        for (uint32_t i0 = tid; i0 < npos; i0 += 2u * kFT) {  // two searches advanced together
+            uint64_t k[2];
+            bool ok[2];
+            uint32_t r[2];
 #pragma unroll
-            for (uint32_t st = kMaxCtas / 2u; st; st >>= 1) r = k >= spl[spl_pos(r + st)] ? r + st : r;
-            r = min(r, G - 1u);
-            rv[i] = (uint8_t)r;
-            atomicAdd(&sm.s.lcnt[r], 1u);
+            for (int u = 0; u < 2; u++) {
+                const uint32_t i = i0 + (uint32_t)u * kFT, q = i >> 1;
+                ok[u] = i < npos && ((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u);
+                k[u] = ok[u] ? sm.s.kbuf[i] : 0ull;
+                r[u] = 0;
+            }
+#pragma unroll
+            for (uint32_t st = kMaxCtas / 2u; st; st >>= 1) {
+#pragma unroll
+                for (int u = 0; u < 2; u++) r[u] = k[u] >= spl[spl_pos(r[u] + st)] ? r[u] + st : r[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                if (!ok[u]) continue;
+                const uint32_t rg = min(r[u], G - 1u);
+                rv[i0 + (uint32_t)u * kFT] = (uint8_t)rg;
+                atomicAdd(&sm.s.lcnt[rg], 1u);
+            }
         }
     }
     __syncthreads();
@@ -1303,56 +1399,78 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         const uint32_t r = rr[i], pos = sm.s.gbase[r] + (i - sm.s.lst[r]);
         if (pos < (uint32_t)kKcap) b.keys[0][(size_t)r * kKcap + pos] = kb2[i];  // else: overflow -> fallback
     }
-    // this CTA's range: its splitters and bucket span (shared memory is reused after the barrier)
-    const unsigned long long spl_lo = sm.s.spl[spl_pos(bid)], spl_hi = bid + 1u < G ? sm.s.spl[spl_pos(bid + 1)] : ~0ull;
-    // the range's key bounds for its digit: [spl_lo, spl_hi - 1], or the previous order's
-    // largest key for the last nonempty range (keys outside are clamped into the end counters)
-    const unsigned long long key_hi = spl_hi == ~0ull ? sm.s.spl[spl_pos(kMaxCtas)] : spl_hi - 1ull;
-    uint32_t j_lo = 0, j_hi = 0;
-    {
-        uint32_t sv;
-        j_lo = bucket_t(spl_lo, sm.btab, vb, sv);
-        j_hi = (bid + 1u >= G || spl_hi == ~0ull) ? NB : bucket_t(spl_hi - 1ull, sm.btab, vb, sv) + 1u;
-        if (spl_hi <= spl_lo) j_hi = j_lo;
-    }
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
     TRACE(7);
     // ranges' sizes (prefix: where each sorted range goes) and the CTAs' key counts (n)
     uint32_t rsz = 0, rpre = 0, n = 0;
     bool fallback = (a.flags & kStepForceFallback) != 0;
-    {
-        const uint32_t v = tid < G ? __ldcg(&rcur[tid]) : 0u, q = tid < G ? __ldcg(&b.nk_part[tid]) : 0u;
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan_u32<kFT>(v, sm.l.w32, &tot);
-        if (tid < G) sm.l.rsz[tid] = v | (v > (uint32_t)kKcap ? 0x80000000u : 0u);
-        if (tid < G) sm.l.rpre[tid] = ex;
-        uint32_t nn;
-        (void)block_excl_scan_u32<kFT>(q, sm.l.w32, &nn);
-        n = nn;
-        fallback = __syncthreads_or(fallback || v > (uint32_t)kKcap) != 0;
-        rsz = sm.l.rsz[bid] & 0x7fffffffu;
-        rpre = sm.l.rpre[bid];
+    if (warp == 0) {  // one round trip: 8 ranges and 8 CTAs per lane, a warp scan
+        uint32_t v[kMaxCtas / 32], tot = 0, nq = 0, big = 0;
+#pragma unroll
+        for (int j = 0; j < kMaxCtas / 32; j++) {
+            const uint32_t r = lane * (kMaxCtas / 32) + (uint32_t)j;
+            v[j] = r < G ? __ldcg(&rcur[r]) : 0u;
+            nq += r < G ? __ldcg(&b.nk_part[r]) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxCtas / 32; j++) { tot += v[j]; big |= v[j] > (uint32_t)kKcap ? 1u : 0u; }
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        uint32_t run = x - tot;
+#pragma unroll
+        for (int j = 0; j < kMaxCtas / 32; j++) {
+            const uint32_t r = lane * (kMaxCtas / 32) + (uint32_t)j;
+            sm.l.rsz[r] = v[j];
+            sm.l.rpre[r] = run;
+            run += v[j];
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) nq += __shfl_xor_sync(0xffffffffu, nq, o);
+        big = __any_sync(0xffffffffu, big != 0u) ? 1u : 0u;
+        if (lane == 0) { sm.l.w32[0] = nq; sm.l.w32[1] = big; }
     }
-    const uint32_t r_end0 = sm.l.rsz[0] & 0x7fffffffu;
+    __syncthreads();
+    n = sm.l.w32[0];
+    fallback = fallback || sm.l.w32[1] != 0u;
+    rsz = sm.l.rsz[bid];
+    rpre = sm.l.rpre[bid];
+    const uint32_t r_end0 = sm.l.rsz[0];
     // head-only mode (F3): CTA 0 ranks the head; the others stop here, unless the head range
     // does not hold the keys the admission needs (then every range is sorted)
     const bool head_only = head_mode && !fallback && r_end0 >= min(n, a.max_batch + 32u);
     // positions of the next step's splitters in this step's order: the head (range 0) ends
     // at max_batch + kHeadMargin keys, the other ranges share the rest evenly
-    const uint32_t q1 = min(n, a.max_batch + kHeadMargin);
-    auto qpos = [&](uint32_t s) -> uint32_t {  // s = 1 .. G-1
-        return q1 + (uint32_t)(((uint64_t)(s - 1u) * (uint64_t)(n - q1)) / (uint64_t)max(G - 1u, 1u));
+    const uint32_t q1 = G > 1u ? min(n, a.max_batch + kHeadMargin) : n;
+    // position of grid entry f (0 .. 16 G) in this step's order: range 0's 16 segments over
+    // [0, q1), the other ranges' over [q1, n) evenly (past the last key: the last key)
+    auto qf = [&](uint32_t f) -> uint32_t {
+        const uint64_t p = f <= (uint32_t)kSeg
+                               ? (uint64_t)q1 * f / kSeg
+                               : q1 + (uint64_t)(f - kSeg) * (uint64_t)(n - q1) / ((uint64_t)kSeg * (G - 1u));
+        return n ? (uint32_t)min(p, (uint64_t)(n - 1u)) : 0u;
     };
     unsigned long long* spl_next = b.spl + (size_t)(a.parity ^ 1u) * kSplG;
-    if (head_only && bid == G - 1u)  // the splitters are kept: the other ranges were not sorted
-        for (uint32_t s2 = tid; s2 <= (uint32_t)kMaxCtas; s2 += kFT)
-            spl_next[s2] = __ldcg(&b.spl[(size_t)a.parity * kSplG + s2]);
+    if (head_only && bid == G - 1u)  // the grid is kept: the other ranges were not sorted
+        for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = __ldcg(&b.spl[(size_t)a.parity * kSplG + f]);
+    // this range's grid entries fine[16 bid .. 16 bid + 16]: key codes and per-segment shifts of
+    // the range sort's piecewise-linear digit (segment j: keys in [fine[j], fine[j + 1]))
+    if (warp == 1 && lane <= (uint32_t)kSeg) {
+        const unsigned long long fk = __ldcg(&b.spl[(size_t)a.parity * kSplG + kSeg * bid + lane]);
+        sm.l.fine[lane] = fk;
+        sm.l.fcode[lane] = key_code(fk, vb);
+    }
 
+    __syncthreads();  // the grid entries
     // ---------------- L: sort the key ranges
     uint32_t final_buf, passes;
     bool head_dw = false;  // CTA 0: demands / state words of its head in sm.l.b (sorted order)
     bool written = false;  // the range sort wrote the sorted range to keys1 itself
+    bool head_loop = false;  // CTA 0: head keys in sm.l.b, demands / states in sm.l.pos (range_sort_loop)
     if (!fallback && (!head_only || bid == 0)) {
         const uint32_t rn = rsz;
         const uint64_t* src = b.keys[0] + (size_t)bid * kKcap;
@@ -1361,7 +1479,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         if (b.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_t0));
         unsigned long long* tr = b.trace ? b.trace + (size_t)bid * kTraceSlots : nullptr;
         if (tr && tid == 0) {
-            tr[30] = rn; tr[31] = j_hi - j_lo;
+            tr[30] = rn; tr[31] = 0;
             uint32_t smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             tr[28] = smid;  // diagnostics: SM of this CTA
@@ -1375,9 +1493,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             } else {
                 small_sort<false>(sm.l, src, rn, c, nullptr, 0u);
             }
-        } else if (bid != 0) {  // an ordinary range: linear-digit counting sort, straight to the output
+        } else {  // linear-digit counting sort, straight to the output (CTA 0: the head)
             TRACE(13);
-            written = range_sort_loop(sm.l, src, rn, b.keys[1] + rpre, spl_lo, key_hi, vb, tr ? tr + 32 : nullptr);
+            // CTA 0 (single shard): head + admission loads on chip
+            const bool stage = bid == 0 && rn <= kHeadPre && !(a.flags & kStepMerge);
+            written = range_sort_loop(sm.l, src, rn, b.keys[1] + rpre, vb, tr ? tr + 32 : nullptr, &b.pool,
+                                      a.id_base_mod, &c, stage ? sm.l.pos + kHeadPre : nullptr,
+                                      stage ? sm.l.pos + 2u * kHeadPre : nullptr);
+            head_loop = stage && written;
             if (!written) {  // a counter held too many keys: sort the placed range by LSD
                 unsigned long long o, an;
                 block_or_and(sm.l, sm.l.a, rn, o, an);
@@ -1386,33 +1509,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
                     for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
                 __syncthreads();
             }
-        } else if (rn <= kHeadPre && j_hi - j_lo > 2u * rn && j_hi - j_lo <= 32768u && !(a.tune & 16u) &&
-                   head_sparse_sort(sm.l, src, rn, c, sm.btab, j_lo, j_hi - j_lo, b.pool, a.id_base_mod)) {
-            TRACE(13);
-            head_dw = true;
-        } else if (j_hi - j_lo < (uint32_t)kSubBuckets) {  // CTA 0's head: bucket sort, admission loads staged
-            TRACE(13);
-            if (rn <= kHeadPre)
-                head_dw = range_sort<(kHeadPre + kFT - 1) / kFT, true>(sm.l, src, rn, j_lo, j_hi, c, sm.btab,
-                                                                      tr ? tr + 16 : nullptr, &b.pool, a.id_base_mod);
-            else if (!(written = range_sort_loop(sm.l, src, rn, b.keys[1] + rpre, spl_lo, key_hi, vb, nullptr))) {
-                unsigned long long o, an;  // a counter held too many keys: sort the placed range by LSD
-                block_or_and(sm.l, sm.l.a, rn, o, an);
-                const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
-                if (r != sm.l.a)
-                    for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
-                __syncthreads();
-            }
-        } else {  // a sparse range over very many buckets: stable LSD over the varying digits
-            for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = __ldcg(&src[i]);
-            __syncthreads();
-            TRACE(13);
-            unsigned long long o, an;
-            block_or_and(sm.l, sm.l.a, rn, o, an);
-            const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
-            if (r != sm.l.a)
-                for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
-            __syncthreads();
         }
         TRACE(14);
         if (b.trace && tid == 0) {
@@ -1431,12 +1527,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         if (!written)
             for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][rpre + i] = sm.l.a[i];
         __syncthreads();  // the range's keys are in place (visible to this CTA's threads)
-        // the next step's splitters that fall in this range, and the largest key
-        if (!head_only && tid >= 1u && tid < G) {
-            const uint32_t q = qpos(tid);
-            if (q >= rpre && q < rpre + rn) spl_next[tid] = __ldcg(&b.keys[1][q]);
-        }
-        if (!head_only && tid == (uint32_t)kMaxCtas && rn && rpre + rn == n) spl_next[kMaxCtas] = __ldcg(&b.keys[1][n - 1u]);
+        // the next step's grid entries that fall in this range
+        if (!head_only && rn)
+            for (uint32_t f = tid; f <= kSeg * G; f += kFT) {
+                const uint32_t q = qf(f);
+                if (q >= rpre && q < rpre + rn) spl_next[f] = __ldcg(&b.keys[1][q]);
+            }
         final_buf = 1;
         passes = 1;
     } else if (fallback) {
@@ -1481,10 +1577,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         passes = 1;
     }
     // the next step's splitters past the last key, and (after the LSD) all of them
-    if (bid == 0 && tid < (uint32_t)kMaxCtas && !head_only) {
-        if (tid == 0) spl_next[0] = 0ull;
-        else if (tid >= G || qpos(tid) >= n) spl_next[tid] = ~0ull;
-    }
+    if (bid == 0 && !head_only && n == 0)  // no keys: an empty grid
+        for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = 0ull;
     unsigned long long pinned_all = 0;
     if (bid == 0 && warp == 0) {  // A5's budget: the pinned total
         for (uint32_t r = lane; r < G; r += 32) pinned_all += __ldcg(&b.pin_part[r]);
@@ -1499,9 +1593,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     const uint32_t need = min(n, a.max_batch);  // the admission (or the merge records) reads keys [0, need)
     const bool wait = fallback || r_end0 < need;
     if (wait) grid_barrier(b.flags, G, ++bar);
-    if (fallback && bid == 0 && tid >= 1u && tid < G && qpos(tid) < n)
-        spl_next[tid] = __ldcg(&b.keys[final_buf][qpos(tid)]);
-    if (fallback && bid == 0 && tid == (uint32_t)kMaxCtas && n) spl_next[kMaxCtas] = __ldcg(&b.keys[final_buf][n - 1u]);
+    if (fallback && bid == 0 && n)
+        for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = __ldcg(&b.keys[final_buf][qf(f)]);
     if (bid != 0) return;
     if (tid == 0) sm.l.adm.w64[0] = pinned_all;
     __syncthreads();
@@ -1515,7 +1608,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     }
     TRACE(15);
     // CTA 0 holds [0, need) in shared memory unless it waited (or its range sort wrote them out)
-    const uint64_t* head = (wait || written) ? b.keys[final_buf] : sm.l.a;
+    const bool hl = head_loop && !wait;  // head keys in sm.l.b, demands / states in sm.l.pos
+    const uint64_t* head = wait ? b.keys[final_buf]
+                                : (hl ? reinterpret_cast<const uint64_t*>(sm.l.b) : (written ? b.keys[final_buf] : sm.l.a));
     const bool dw = head_dw && !wait;
     if (a.flags & kStepMerge) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
@@ -1626,9 +1721,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     while (hs < 2u * a.max_batch) hs <<= 1;
     const bool use_h = !wait && hs <= kHeadTC;
     const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);
-    admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? reinterpret_cast<uint32_t*>(sm.l.b) : nullptr,
-              use_h ? hs : 0u, b.trace ? b.trace + 40 : nullptr, dw ? b32 + kHeadD : nullptr,
-              dw ? b32 + kHeadW : nullptr);
+    uint32_t* htab = hl ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
+    admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? htab : nullptr, use_h ? hs : 0u,
+              b.trace ? b.trace + 40 : nullptr,
+              hl ? sm.l.pos + kHeadPre : (dw ? b32 + kHeadD : nullptr),
+              hl ? sm.l.pos + 2u * kHeadPre : (dw ? b32 + kHeadW : nullptr));
     TRACE(9);
 }
 

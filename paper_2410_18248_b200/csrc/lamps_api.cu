@@ -218,7 +218,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_bsum = L.take(bsum_lsd);
     size_t o_btot = h->fused ? L.take((size_t)2 * fused_max_buckets() * 4) : 0;
     size_t o_btab = h->fused ? L.take((size_t)2 * 136 * 4) : 0;
-    size_t o_spl = h->fused ? L.take((size_t)2 * 264 * 8) : 0;
+    size_t o_spl = h->fused ? L.take((size_t)2 * (16 * 256 + 16) * 8) : 0;  // kernels_fused.cu kSplG
     size_t o_rcur = h->fused ? L.take((size_t)2 * 256 * 4) : 0;
     size_t o_nkp = L.take((size_t)gmax * 4);
     size_t o_ctl = L.take(sizeof(Ctl));
