@@ -60,6 +60,64 @@ def dist_env():
     return rank, world, local
 
 
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without torchrun: re-launch this command under
+    torch.distributed.run with N ranks on this node (rank r -> cuda:r), rendezvous on
+    127.0.0.1; rank 0 prints the JSON line.  NCCL_DEBUG=INFO unless set, so the
+    communicator's rank count is in the log."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def cpu_info():
+    """(host cores, CPU model) for the oracle baseline's "1 core of N"."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
+class PinnedCore:
+    """Run the oracle on one host core (the `taskset -c <core>` of BASELINE.md 4, applied to
+    this process with sched_setaffinity; the oracle is single-threaded C called in-process)."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
+
+
+def n_ready(snap):
+    return int((snap["state"] == 1).sum())  # READY (gen.pools)
+
+
+def config_dict(cname, cfg, kv, n_elig, world, parallelism):
+    """The workload description; identical in both arms (same pool, same keys)."""
+    return {"workload": f"{cname}: 1M-request pool (2^20 slots), GPT-J profile, {n_elig} READY per shard"
+                        if cname == "C5" else f"{cname}: {cfg['capacity']}-slot pool, {n_elig} READY per shard",
+            "slots_per_gpu": cfg["capacity"], "eligible_per_gpu": n_elig, "kv_total_blocks": kv,
+            "max_batch": cfg["max_batch"], "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
+            "l2": "flushed before every timed step (256 MiB write)", "parallelism": parallelism,
+            "n_shards": world}
+
+
 def measured_peak_hbm():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -130,25 +188,31 @@ def run_reference(args, rank, world):
     if not full:  # bounded sample: a 2^18-slot pool of the same workload
         cfg["capacity"] = 1 << 18
         snap = gen.snapshot(cname, seed=0, n=1 << 18, capacity=1 << 18)
+    merged = world > 1 or args.merge
+    conf = config_dict(cname, gen.lib_config(cname), kv, n_ready(gen.snapshot(cname, seed=0, id_base=(1 << 20) * 7 + 99)),
+                       world, parallelism(world, merged, args.transport if merged else None, gen.lib_config(cname)))
     p = O.OraclePool(cfg)
     p.load(snap, snap["next_id"])
-    for _ in range(args.warmup):
-        p.step(kv_total=kv)
-    t0 = time.perf_counter()
-    ne = 0
-    for _ in range(args.steps):
-        r = p.step(kv_total=kv)
-        ne += r["n_eligible"]
-    dt = time.perf_counter() - t0
+    ncores, model = cpu_info()
+    with PinnedCore() as pc:
+        for _ in range(args.warmup):
+            p.step(kv_total=kv)
+        t0 = time.perf_counter()
+        ne = 0
+        for _ in range(args.steps):
+            r = p.step(kv_total=kv)
+            ne += r["n_eligible"]
+        dt = time.perf_counter() - t0
     v = ne / dt
     sample = (f"full {cname} pool ({cfg['capacity']} slots)" if full else
-              f"{cname} workload, 2^18-slot sample") + f", {args.steps} oracle steps"
+              f"{cname} workload, 2^18-slot sample") + f", {args.steps} oracle steps, pinned to core {pc.core}"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic", "config": {"workload": f"{cname}: 1M-request pool" if full else cname,
-                                            "slots": cfg["capacity"]},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": conf,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "cores_total": ncores,
+                             "cores_desc": f"1 core of {ncores}", "cpu_model": model, "kind": "oracle",
+                             "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -163,18 +227,30 @@ def cpu_baseline(cname, seconds=12.0):
     p = O.OraclePool(cfg)
     p.load(snap, snap["next_id"])
     kv = gen.CONFIGS[cname]["kv_total"]
-    t0 = time.perf_counter()
-    n, ne = 0, 0
-    while True:
-        r = p.step(kv_total=kv)
-        n += 1
-        ne += r["n_eligible"]
-        if time.perf_counter() - t0 > seconds:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": ne / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    ncores, model = cpu_info()
+    with PinnedCore() as pc:
+        t0 = time.perf_counter()
+        n, ne = 0, 0
+        while True:
+            r = p.step(kv_total=kv)
+            n += 1
+            ne += r["n_eligible"]
+            if time.perf_counter() - t0 > seconds:
+                break
+        dt = time.perf_counter() - t0
+    return {"value": ne / dt, "unit": UNIT, "cores": 1, "cores_total": ncores, "cores_desc": f"1 core of {ncores}",
+            "cpu_model": model, "kind": "oracle",
             "sample": f"{n} oracle steps over the full {cname} pool ({cfg['capacity']} slots), "
-                      f"{1e3 * dt / n:.0f} ms/step, single-threaded C"}
+                      f"{1e3 * dt / n:.0f} ms/step, single-threaded C pinned to core {pc.core}"}
+
+
+def parallelism(world, merged, transport, cfg):
+    xdesc = ("peer stores into every rank's buffer + merge inside the step kernel" if transport == "p2p"
+             else "NCCL all-gather + merge kernel")
+    if world > 1:
+        return (f"{world} shards x 1M, one exchange of the top-{cfg['max_batch']} per step for the global "
+                f"admission ({xdesc})")
+    return f"1 shard, exchange + merge with one rank ({xdesc})" if merged else "1 shard"
 
 
 def run_ours(args, rank, world, local):
@@ -290,6 +366,12 @@ def run_ours(args, rank, world, local):
     clk.__exit__(None, None, None)
     res = s.result()
     n_elig = res["n_eligible"]
+    # the P/D/S mix of the eligible requests after the timed steps (Table 2's API
+    # classes), from the pool's state words
+    ex = s.export_pool()
+    rd = ex["state"] == 1
+    mix = {"P": int(((ex["strategy"] == 0) & rd).sum()), "D": int(((ex["strategy"] == 1) & rd).sum()),
+           "S": int(((ex["strategy"] == 2) & rd).sum()), "none": int(((ex["strategy"] == 3) & rd).sum())}
     kernels, passes = s.stats()
     fused = kernels == (2 if merged and transport == "nccl" else 1)
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -457,15 +539,9 @@ def run_ours(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms_max, "us_per_step": ms_max * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
-            "config": {"workload": f"{cname}: 1M-request pool (2^20 slots), GPT-J profile, "
-                                   f"{n_elig} READY per shard", "slots_per_gpu": cap, "eligible_per_gpu": n_elig,
-                       "kv_total_blocks": kv, "max_batch": cfg["max_batch"],
-                       "key_bits": 1 + cfg["score_bits"] + cfg["id_bits"],
-                       "l2": "flushed before every timed step (256 MiB write)",
-                       "parallelism": (f"{world} shards x 1M, one exchange of the top-{cfg['max_batch']} per "
-                                       f"step for the global admission ({xdesc})") if world > 1 else
-                                      (f"1 shard, exchange + merge with one rank ({xdesc})" if merged
-                                       else "1 shard")},
+            "config": config_dict(cname, cfg, kv, n_ready(snap), world, parallelism(world, merged, transport, cfg)),
+            "transport": transport if merged else None, "ranks_connected": world,
+            "strategy_mix": mix,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak if ach else None, "traffic": traffic,
                          "peak_source": peak_src},
@@ -505,7 +581,11 @@ def run_ours(args, rank, world, local):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     rank, world, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; using {world} ranks", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

@@ -47,6 +47,17 @@ if os.environ.get("TRACE"):
         if a0 >= 8 and a1 in (15, 9):
             d = d[:, :1]
         print(f"  {nm:12s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
+    # critical path: every CTA leaves the barrier at about the same time, so the step is
+    # max(pre-barrier) + barrier + max(post-barrier); CTA 0's post includes the admission
+    pre = (t[:, :, 6] - t[:, :, 0]) / 1.965e3
+    post = (t[:, :, 8] - t[:, :, 7]) / 1.965e3
+    post[:, 0] = (t[:, 0, 9] - t[:, 0, 7]) / 1.965e3
+    print(f"  pre-barrier max {np.median(pre.max(axis=1)):6.2f} (cta {int(np.median(pre.argmax(axis=1)))})  "
+          f"post-barrier max {np.median(post.max(axis=1)):6.2f} (cta {int(np.median(post.argmax(axis=1)))}), "
+          f"cta0 post {np.median(post[:, 0]):6.2f}, others' mean {np.median(post[:, 1:].mean(axis=1)):6.2f}")
+    lp = (t[:, 0, 13] - t[:, 0, 7]) / 1.965e3
+    print(f"  cta0: L prep {np.median(lp):5.2f} sort {np.median((t[:, 0, 14] - t[:, 0, 13]) / 1.965e3):5.2f} "
+          f"store {np.median((t[:, 0, 8] - t[:, 0, 14]) / 1.965e3):5.2f} admit {np.median((t[:, 0, 9] - t[:, 0, 8]) / 1.965e3):5.2f}")
     for base, part in ((16, "starving"), (24, "nonstarv")):
         for nm, a0, a1 in (("bucket starts", 0, 1), ("rank level1", 1, 2), ("refine", 2, 3), ("lsd fallback", 3, 4)):
             d = (t[:, :, base + a1] - t[:, :, base + a0]) / 1.965e3

@@ -60,3 +60,11 @@ if "--stalls" in sys.argv:
     for (f, l), d in sorted(per.items(), key=lambda x: -x[1][0])[:25]:
         top = ", ".join(f"{k} {100*v/max(d[0],1):.0f}%" for k, v in d[2].most_common(4))
         print(f"{f}:{l} {100*d[0]/ts:5.1f}% inst {d[1]:8d}  {top}")
+if "--range" in sys.argv:  # per-line instructions / samples of file:lo-hi
+    spec_r = sys.argv[sys.argv.index("--range") + 1]
+    f0, rng = spec_r.split(":")
+    lo, hi = map(int, rng.split("-"))
+    for (f, l), d in sorted(per.items(), key=lambda x: (x[0][0], x[0][1] or 0)):
+        if f == f0 and l is not None and lo <= l <= hi and (d[0] or d[1]):
+            top = ", ".join(f"{k} {100*v/max(d[0],1):.0f}%" for k, v in d[2].most_common(3))
+            print(f"{f}:{l:5d} smp {d[0]:5d} inst {d[1]:9d}  {top}")

@@ -44,3 +44,17 @@ def test_reference_arm_torchrun_world2():
     lines = [x for x in r.stdout.splitlines() if x.strip().startswith("{")]
     assert len(lines) == 1, lines  # rank 0 alone prints
     _check(lines[0], 2, 1)
+
+
+def test_reference_arm_spawns_ranks_without_torchrun():
+    """`bench.py --gpus 2` with no torchrun launches the two ranks itself (rank 0 prints)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--config", "C2",
+                        "--steps", "1", "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=300,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.strip().startswith("{")]
+    assert len(lines) == 1, lines
+    _check(lines[0], 2, 1)
+    d = json.loads(lines[0])
+    assert d["cpu_baseline"]["cores_total"] >= 1 and "core" in d["cpu_baseline"]["sample"]
