@@ -83,6 +83,10 @@ extern "C" {
                                    the step kernel uses #SM / world CTAs so all ranks' kernels run
                                    at once; each rank needs its own stream */
 
+#define LAMPS_GRID_STEP 256u    /* pools the one-CTA small-pool step kernel covers (capacity <= 4096,
+                                   one shard) take the grid-wide fused step kernel instead (tests,
+                                   measurements) */
+
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 
 typedef struct lamps_s lamps_t;

@@ -87,6 +87,7 @@ struct lamps_s {
     Bufs b{};
     uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
     bool fused = false;
+    bool small = false;   // fused family: the one-CTA small-pool step kernel (k_small)
     bool cold = true;     // fused: no splitters yet (StepArgs.cold); a fused step writes the next's
     uint32_t world = 1, rank = 0;
     bool merge = false;  // merge_mode(cfg)
@@ -184,7 +185,8 @@ const char* validate_cfg(const lamps_config* c) {
     if (c->score_interval > 127) return "score_interval must be <= 127";
     if (c->world > 1 || (c->flags & LAMPS_MERGE)) {
         if (c->world > 32 || c->rank >= (c->world > 1 ? c->world : 1u)) return "need rank < world <= 32";
-        if ((uint64_t)c->world * c->max_batch > kMergeMaxRecords) return "world * max_batch must be <= 8192";
+        if (c->transport == LAMPS_XPORT_P2P && (uint64_t)c->world * c->max_batch > kMergeMaxRecords)
+            return "P2P transport: world * max_batch must be <= 8192 (the in-kernel merge); NCCL / loopback merge any";
         if (c->transport > LAMPS_XPORT_P2P) return "unknown transport";
         if (c->transport == LAMPS_XPORT_NCCL && !c->nccl_id) return "NCCL transport needs nccl_id";
         if (c->world <= 1 && c->transport == LAMPS_XPORT_LOOPBACK)
@@ -236,9 +238,14 @@ size_t carve(lamps_t* h, uint8_t* base) {
     const bool merge = merge_mode(h->cfg);
     size_t o_xs = merge ? L.take(((size_t)mb + 1) * sizeof(MergeRec)) : 0;
     size_t o_xr = merge ? L.take((size_t)world * ((size_t)mb + 1) * sizeof(MergeRec)) : 0;
+    const bool large = merge && merge_is_large(world, mb);
+    size_t o_xc = large ? L.take((size_t)world * world * mb * 4) : 0;
+    size_t o_xo = large ? L.take((size_t)mb * 4) : 0;
     if (!base) return L.off;
     h->b.xsend = merge ? reinterpret_cast<MergeRec*>(base + o_xs) : nullptr;
     h->b.xrecv = merge ? reinterpret_cast<MergeRec*>(base + o_xr) : nullptr;
+    h->b.xcnt = large ? reinterpret_cast<uint32_t*>(base + o_xc) : nullptr;
+    h->b.xorder = large ? reinterpret_cast<uint32_t*>(base + o_xo) : nullptr;
     uint32_t* soa[10];
     for (int i = 0; i < 10; i++) soa[i] = reinterpret_cast<uint32_t*>(base + o_soa[i]);
     h->b.pool = Pool{soa[0], soa[1], soa[2], soa[3], soa[4], soa[5], soa[6], soa[7], soa[8], soa[9], cap_pad};
@@ -300,6 +307,9 @@ void grids(lamps_t* h, bool query_device) {
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && gpc * 4u <= (uint32_t)kFusedKcap && fused_occ >= 1 &&
                    h->fused_grid <= 255u;  // range weights (kMaxCtas) cover up to 255 CTAs
     }
+    // small pools: the whole step in one CTA (k_small), no grid barriers
+    h->small = h->fused && h->cap <= small_max_cap() && !merge_mode(h->cfg) && !(h->cfg.flags & LAMPS_GRID_STEP) &&
+               !((h->cfg.flags & LAMPS_SHARE_DEVICE) && h->cfg.world > 1);
     if (!query_device) {  // size query: assume the fused path may be chosen
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && h->cap <= 148u * (uint32_t)kFusedKcap;
         h->fused_grid = std::max<uint32_t>(h->fused_grid, 296u);
@@ -417,7 +427,10 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     if (!h->fused) CU(h, launch_events(h->b, h->cost, a, h->stream));  // fused: in the kernel's prologue
     record_timing(h, 1);
     if (h->fused) {
-        CU(h, launch_fused(h->b, h->cost, a, a.inl ? &h->inl : nullptr, h->fused_grid, h->stream));
+        if (h->small)
+            CU(h, launch_small(h->b, h->cost, a, a.inl ? &h->inl : nullptr, h->stream));
+        else
+            CU(h, launch_fused(h->b, h->cost, a, a.inl ? &h->inl : nullptr, h->fused_grid, h->stream));
         h->cold = false;  // the kernel wrote the next step's splitters
         record_timing(h, 2);
         record_timing(h, 3);
@@ -447,7 +460,7 @@ int enqueue_phase2(lamps_t* h, uint64_t kv_total, uint32_t n_ev, bool exchange) 
                                                 (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
         }
         CU(h, launch_merge(h->b, h->cost, a, h->stream));
-        h->last_kernels += 1;
+        h->last_kernels += merge_is_large(h->world, h->cfg.max_batch) ? 3 : 1;
     }
     record_timing(h, 4);
     if (h->cfg.flags & LAMPS_TIMING) {

@@ -23,7 +23,8 @@ constexpr uint32_t kStepMerge = 2u;          // StepArgs.flags: emit top-K recor
 constexpr uint32_t kStepHeadOnly = 4u;       // StepArgs.flags: rank only the admission head (F3)
 constexpr uint32_t kStepP2P = 8u;            // StepArgs.flags: exchange by peer stores + merge in k_fused
 constexpr uint32_t kStepP2PSys = 16u;        // StepArgs.flags: the peers are other GPUs (system scope)
-constexpr uint32_t kMergeMaxRecords = 8192;  // world * max_batch limit of the merge kernel
+constexpr uint32_t kMergeMaxRecords = 8192;  // world * max_batch of the in-kernel (P2P) merge's records
+constexpr size_t kMergeSmemMax = 232448 - 4096;  // above: the grid-wide merge by rank (k_merge_count/place/cut)
 
 // multi-GPU exchange: per rank one header followed by K records (32 B each)
 struct MergeHdr {
@@ -145,6 +146,8 @@ struct Bufs {
     MergeRec* xown;          // this rank's exchange buffer (the receive side)
     MergeRec* xsend;         // [1 + K] header + top-K records of this rank (world > 1)
     MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
+    uint32_t* xcnt;          // large merges: [world][world * K] counts of smaller records per other run
+    uint32_t* xorder;        // large merges: [K] the merged order's first K records (xrecv indices)
 };
 
 // launchers (kernels_step.cu / kernels_sort.cu)
@@ -159,7 +162,10 @@ uint32_t fused_max_buckets();
 void fused_default_table(uint32_t vb, uint32_t* out136);  // the initial bucket table
 cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t grid,
                          cudaStream_t s);
+uint32_t small_max_cap();  // the one-CTA small-pool step kernel's capacity limit
+cudaError_t launch_small(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, cudaStream_t s);
 cudaError_t launch_merge(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
+bool merge_is_large(uint32_t world, uint32_t K);  // world * K records beyond one CTA's shared memory
 // merge scratch: sk, gid (8 B) and demand (4 B) per record of the W runs, 3 index arrays of K
 __host__ __device__ inline size_t merge_smem_bytes(uint32_t world, uint32_t K) {
     const size_t R = (size_t)world * K;

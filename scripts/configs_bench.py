@@ -10,14 +10,17 @@ import torch  # noqa: E402
 
 import gen  # noqa: E402
 from paper_2410_18248_b200 import Scheduler  # noqa: E402
+from paper_2410_18248_b200.lamps import LAMPS_GRID_STEP  # noqa: E402
 
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush = torch.empty(256 << 20 if not os.environ.get("NOFLUSH") else 16, dtype=torch.uint8, device="cuda")
 out = []
-for cname in ("C1", "C2", "C3", "C4", "C5"):
+runs = [(c, 0) for c in ("C1", "C2", "C3", "C4", "C5")]
+runs += [(c, LAMPS_GRID_STEP) for c in ("C1", "C2", "C3")]  # small pools on the grid-wide kernel
+for cname, flags in runs:
     cfg = gen.lib_config(cname)
     snap = gen.snapshot(cname, seed=0, id_base=(1 << 20) * 7 + 99)
     kv = gen.CONFIGS[cname]["kv_total"]
-    s = Scheduler(cfg)
+    s = Scheduler(cfg, flags=flags)
     s.import_pool(snap, snap["id_base"], snap["next_id"])
     for _ in range(100):
         flush.zero_()
@@ -34,7 +37,8 @@ for cname in ("C1", "C2", "C3", "C4", "C5"):
     r = s.result()
     k, _ = s.stats()
     med = us[len(us) // 2]
-    out.append({"config": cname, "slots": cfg["capacity"], "live": int((snap["state"] != 0).sum()),
+    out.append({"config": cname, "kernel": "k_fused (grid)" if flags or cfg["capacity"] > 4096 else "k_small (one CTA)",
+                "slots": cfg["capacity"], "live": int((snap["state"] != 0).sum()),
                 "eligible": r["n_eligible"], "admitted": r["n_admitted"], "kernels_per_step": k,
                 "us_median": round(med, 2), "us_min": round(us[0], 2), "us_max": round(us[-1], 2),
                 "decisions_per_s": r["n_eligible"] / (med * 1e-6)})

@@ -8,8 +8,9 @@ FIELDS = ("state", "has_api", "starving", "strategy", "cnt", "ctx", "pre_rem", "
           "resp_len", "post_len", "pending", "age", "dirty")
 
 
-# fused step kernel; LAMPS_MULTI_KERNEL; LAMPS_FORCE_FALLBACK; LAMPS_HEAD_ONLY (F3 top-K fast path)
-PATH_FLAGS = {"fused": 0, "multi": 4, "fallback": 8, "head": 64}
+# fused step kernel (one-CTA k_small for capacity <= 4096); LAMPS_MULTI_KERNEL; LAMPS_FORCE_FALLBACK;
+# LAMPS_HEAD_ONLY (F3 top-K fast path); LAMPS_GRID_STEP (small pools on the grid-wide fused kernel)
+PATH_FLAGS = {"fused": 0, "multi": 4, "fallback": 8, "head": 64, "grid": 256, "grid_fallback": 256 | 8}
 
 
 def make_pair(cfg: dict, debug=True, path="fused"):

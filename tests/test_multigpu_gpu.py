@@ -73,6 +73,13 @@ def test_loopback_merge_c4(world, cap_l):
     run("C4", world, cap_l, 100000, 10000, max_batch=1024)
 
 
+@pytest.mark.parametrize("world,cap_l,K", [(4, 32768, 4096), (8, 16384, 8192)])
+def test_loopback_merge_large_k(world, cap_l, K):
+    # world * K records beyond one CTA's shared memory (global max_batch 8192
+    # over 8 shards): the grid-wide merge by rank (k_merge_count / k_merge_place / k_merge_cut)
+    run("C4", world, cap_l, 100000, 1_000_000, max_batch=K)
+
+
 def test_loopback_merge_tight_budget_and_small_k():
     run("C3", 4, 1024, 3000, 80, max_batch=7)
 
@@ -122,6 +129,11 @@ def test_p2p_merge_c2(world):
 
 def test_p2p_merge_c4():
     run("C4", 2, 65536, 100000, 10000, max_batch=1024, p2p=True)
+
+
+def test_p2p_merge_w4_k2048():
+    # 4 ranks x 2048 records: the largest exchange the in-kernel merge stages on chip
+    run("C4", 4, 32768, 100000, 200000, max_batch=2048, p2p=True)
 
 
 def test_p2p_merge_tight_budget_and_small_k():

@@ -16,7 +16,7 @@ from parity_util import (compare_outputs, compare_state, load_both, make_pair, s
 pytestmark = pytest.mark.gpu
 
 
-PATHS = ["fused", "multi", "fallback", "head"]
+PATHS = ["fused", "multi", "fallback", "head", "grid", "grid_fallback"]
 
 
 @pytest.mark.parametrize("path", PATHS)
