@@ -211,8 +211,12 @@ typedef struct {
  * lamps_init -- create a handle.  Two-phase: with d_workspace == NULL only
  * *ws_bytes is written (device bytes needed, 256-byte aligned).  Then call
  * again with a device buffer of at least that size (e.g. a torch uint8 CUDA
- * tensor) that the caller keeps alive until lamps_free.  The library never
- * allocates device memory itself; it allocates pinned host staging buffers.
+ * tensor) that the caller keeps alive until lamps_free.  All per-step device
+ * state lives in that workspace.  The library itself allocates pinned host
+ * staging / result buffers and, for the P2P transport only, the exchange
+ * buffer (cudaMalloc, 2 x world x (max_batch + 1) x 32 B + flags): CUDA IPC
+ * exports whole allocations, so it cannot be carved from the caller's buffer.
+ * Both are released by lamps_free.
  * Errors: EINVAL (NULL pointer, invalid config field), ECUDA.
  */
 int lamps_init(const lamps_config* cfg, void* d_workspace, size_t* ws_bytes, lamps_t** out);

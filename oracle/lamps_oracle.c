@@ -505,10 +505,15 @@ int o_step(const ocfg* cfg, oreq* pool, const uint64_t* prev_adm, uint32_t n_pre
         if (ev[e].kind == O_EV_FINISHED) {
             r->state = O_FREE;
         } else {
-            uint64_t W[3];
+            /* Alg.1: the request is routed by r.handling, the label of the ranking
+             * pass that admitted it (reading R11); a request without one (never ranked
+             * with an API ahead) takes the argmin of Eq. (1)-(3) at C_i = ctx */
             r->pre_rem = 0;
-            o_wastes(cfg, r->ctx, 0, r->api_ticks, W);
-            r->strategy = o_argmin3(W);
+            if (r->strategy == O_NONE) {
+                uint64_t W[3];
+                o_wastes(cfg, r->ctx, 0, r->api_ticks, W);
+                r->strategy = o_argmin3(W);
+            }
             r->state = O_PAUSED_P + r->strategy;
             if (!r->starving) r->cnt = 0;
         }

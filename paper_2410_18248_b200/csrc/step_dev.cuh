@@ -12,7 +12,7 @@ struct DevEvent {
 };
 
 // A0 for one engine event about a request admitted by the previous step (K0, or the
-// fused kernel's prologue): API_CALL routes it to P/D/S by argmin waste at C_i = ctx
+// fused kernel's prologue): API_CALL routes it to P/D/S by the label of the ranking pass
 // (Alg.1) and resets its counter unless starving; FINISHED frees
 // the slot.  The token of this iteration is counted (SFC_RAN).
 __device__ __forceinline__ void apply_event(const Pool& P, const Cost& c, const DevEvent E) {
@@ -26,7 +26,10 @@ __device__ __forceinline__ void apply_event(const Pool& P, const Cost& c, const 
     P.ctx[s] = ctx;
     P.pre[s] = 0u;
     P.pend[s] = 0u;
-    const uint32_t st = strategy_of(ctx, 0, P.api[s], c);
+    // routed by the label of the ranking pass that admitted it (Alg.1, R11); a
+    // request never ranked with an API ahead takes the argmin at C_i = ctx
+    const uint32_t lab = sfc_strat(w);
+    const uint32_t st = lab != STR_NONE ? lab : strategy_of(ctx, 0, P.api[s], c);
     const uint32_t starv = sfc_starv(w);
     P.sfc[s] = sfc_pack(ST_PP + st, sfc_has(w), starv, st, starv ? sfc_cnt(w) : 0u) | (w & SFC_META);
 }
