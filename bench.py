@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-shard exchange: p2p = peer stores + merge inside the step kernel "
                          "(CUDA IPC over NVLink), nccl = ncclAllGather + merge kernel")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: one 1M-request shard per GPU; strong: the 1M-request pool as --shards "
+                         "shards (8 x 131072) spread over the GPUs, all shards of a GPU co-resident")
+    ap.add_argument("--shards", type=int, default=8, help="strong scaling: shards of the 1M pool")
     return ap.parse_args()
 
 
@@ -579,6 +583,186 @@ def run_ours(args, rank, world, local):
     return 0
 
 
+def run_strong(args, rank, world, local):
+    """Strong scaling: the 1M-request pool as `shards` shards of 2^20 / shards
+    slots, shard g on GPU g // (shards / N); the shards of one GPU are co-resident step kernels
+    (#SM / S CTAs each, one stream each, launched together), every shard exchanges its top-K
+    records with all others by peer stores (same GPU: device memory; other GPUs: CUDA IPC over
+    NVLink) and admits its share of ONE global batch.  Time per step = device time from before
+    the first to after the last of this GPU's kernels, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    from paper_2410_18248_b200 import Scheduler
+    from paper_2410_18248_b200.lamps import EVENT_DTYPE, LAMPS_SHARE_DEVICE, LAMPS_XPORT_P2P
+    W = args.shards
+    if W % world:
+        raise SystemExit(f"--shards {W} must be a multiple of the rank count {world}")
+    S = W // world
+    oversub = os.environ.get("LAMPS_BENCH_OVERSUBSCRIBE") == "1"
+    if oversub:
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world > 1:
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cname = args.config
+    cfg = gen.lib_config(cname)
+    cap = cfg["capacity"] // W
+    cfg["capacity"] = cap
+    kv_all = gen.CONFIGS[cname]["kv_total"]
+    kvs_all = [kv_all // W + (kv_all - W * (kv_all // W) if g == 0 else 0) for g in range(W)]
+    mine = [rank * S + j for j in range(S)]
+    kvs = [kvs_all[g] for g in mine]
+    id_base = (1 << 17) * 7 + 99
+    streams = [torch.cuda.Stream() for _ in mine]
+    shards = [Scheduler(cfg, flags=LAMPS_SHARE_DEVICE, stream=streams[j], world=W, rank=g,
+                        transport=LAMPS_XPORT_P2P, local_ranks=S) for j, g in enumerate(mine)]
+    # each shard is 1/W of the 1M pool: its Preserve-paused KV is capped at 40% of ITS budget share
+    snaps = [gen.snapshot(cname, seed=g, n=cap, capacity=cap, id_base=id_base, kv_total=kvs_all[g]) for g in mine]
+    handles = [s.p2p_handle() for s in shards]
+    if world > 1:
+        allh = [None] * world
+        dist.all_gather_object(allh, handles)
+        flat = [h for hs in allh for h in hs]
+    else:
+        flat = handles
+    for s in shards:
+        s.p2p_connect(flat)
+    main = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def load():
+        for s, sn in zip(shards, snaps):
+            s.import_pool(sn, sn["id_base"], sn["next_id"])
+        barrier()
+
+    def enqueue(start=None, end=None):
+        # the GPU idles ~100 us (after the L2 flush) while the host enqueues the S launches, so
+        # the shards start together and the host's launch latency is not device time (as the
+        # flush hides it for the one launch of the single-shard step); e2e below includes it
+        torch.cuda._sleep(200_000)
+        e0 = torch.cuda.Event()
+        e0.record(main)
+        if start is not None:
+            start.record(main)
+        for st in streams:
+            st.wait_event(e0)
+        Scheduler.group_step_async(shards, kvs)
+        for st in streams:
+            e = torch.cuda.Event()
+            e.record(st)
+            main.wait_event(e)
+        if end is not None:
+            end.record(main)
+
+    load()
+    Scheduler.group_step_async(shards, [0] * S)  # trial exchange: every shard's records arrive
+    for s in shards:
+        s.result()
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device="cuda")
+    clk = ClockSampler(local).__enter__()
+    load()
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        enqueue()
+    t_w = time.perf_counter()
+    while time.perf_counter() - t_w < 0.4:  # let the clock sampler start
+        flush.zero_()
+        enqueue()
+        torch.cuda.synchronize()
+    barrier()
+    load()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()
+        enqueue(starts[k], ends[k])
+    barrier()
+    clk.__exit__(None, None, None)
+    per = sorted(a.elapsed_time(b) for a, b in zip(starts, ends))
+    ms = sum(per) / args.steps
+    res = [s.result() for s in shards]
+    ne_local = sum(r["n_eligible"] for r in res)
+    adm_local = sum(r["n_admitted"] for r in res)
+    t = torch.tensor([ms, float(ne_local), float(adm_local)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        mx = t[:1].clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm_ = t[1:].clone(); dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
+        ms_max, ne_all, adm_all = float(mx.item()), float(sm_[0].item()), float(sm_[1].item())
+    else:
+        ms_max, ne_all, adm_all = ms, float(ne_local), float(adm_local)
+    value = ne_all / (ms_max / 1e3)
+    # end to end: the engine's iteration through the public API (lamps_group_step with each
+    # shard's events about its previous batch: 2 finish), results to the host
+    load()
+    prev = [np.zeros(0, np.uint64) for _ in shards]
+    h2d = d2h = 0
+    e2e_steps = args.e2e_steps or max(args.steps, 100)
+    barrier()
+    t0 = time.perf_counter()
+    ne_e2e = 0
+    for k in range(e2e_steps):
+        evs = []
+        for p in prev:
+            e = np.zeros(min(2, len(p)), EVENT_DTYPE)
+            e["id"], e["kind"] = p[:len(e)], 2
+            evs.append(e)
+            h2d += e.nbytes
+        outs = Scheduler.group_step(shards, evs, kvs)
+        prev = [np.asarray(o["admitted_id"], np.uint64) for o in outs]
+        for o in outs:
+            d2h += 64 + 9 * o["n_admitted"] + 8 * o["n_preempted"]
+            ne_e2e += o["n_eligible"]
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt, float(ne_e2e)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        mx = t[:1].clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm_ = t[1:].clone(); dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
+        dt, ne_e2e = float(mx.item()), float(sm_.item())
+    if rank == 0:
+        peak, peak_src = measured_peak_hbm()
+        n_elig_gpu = ne_all / world
+        gpu_bytes = 32 * cap * S + 16 * n_elig_gpu  # this GPU's shards (DESIGN section 7)
+        ach = gpu_bytes / (ms_max * 1e6)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "us_per_step": ms_max * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{cname}: 1M-request pool as {W} shards x {cap} slots, {int(ne_all)} READY in all",
+                       "shards": W, "shards_per_gpu": S, "slots_per_shard": cap, "kv_total_blocks": kv_all,
+                       "max_batch": cfg["max_batch"], "l2": "flushed before every timed step (256 MiB write)",
+                       "parallelism": f"{W} shards over {world} GPU(s), {S} co-resident step kernels per GPU "
+                                      f"(#SM/{S} CTAs each); top-{cfg['max_batch']} records of every shard "
+                                      f"stored into every shard's buffer, merge + global cut in each kernel"},
+            "transport": "p2p", "ranks_connected": world, "admitted_per_step": adm_all,
+            "roofline": {"bound": "hbm", "kernel": f"k_fused x {S} (co-resident)", "achieved": ach, "peak": peak,
+                         "unit": "GB/s", "frac": ach / peak, "traffic": None, "peak_source": peak_src},
+            "step_us": {"min": round(per[0] * 1e3, 2), "median": round(per[len(per) // 2] * 1e3, 2),
+                        "max": round(per[-1] * 1e3, 2)},
+            "gpu_launches": S * args.steps, "clocks": clk.summary(),
+            "e2e": {"value": ne_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
+                    "d2h_bytes_per_step": d2h / e2e_steps, "ms_per_step": 1e3 * dt / e2e_steps,
+                    "path": "lamps_group_step per engine iteration (events in, results by mapped memory)"},
+        }
+        print(json.dumps(line), flush=True)
+    for s in shards:
+        s.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -588,6 +772,8 @@ def main():
         print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; using {world} ranks", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.scaling == "strong":
+        return run_strong(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
 

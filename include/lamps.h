@@ -145,6 +145,11 @@ typedef struct {
                                          R26).  0 or 1 = every step; k <= 127 = a READY
                                          request keeps its strategy and score for k steps
                                          unless its segment changes (submit / API return) */
+    /* ---- co-resident shards (appended) --------------------------------------- */
+    uint32_t local_ranks;             /* LAMPS_SHARE_DEVICE: shards co-resident on this
+                                         device (each step kernel takes #SM / local_ranks
+                                         CTAs); 0 = world.  Fewer than world: the other
+                                         shards are on other GPUs (system-scope exchange) */
 } lamps_config;
 
 /* rank policies (R25): lower key = earlier; starving requests first under all of them */
@@ -367,6 +372,17 @@ int lamps_nccl_unique_id(void* out128);
  */
 int lamps_group_step(lamps_t* const* h, uint32_t world, const lamps_event* const* ev,
                      const uint32_t* n_ev, const uint64_t* kv_total, lamps_step_out* out);
+
+/*
+ * lamps_group_step_async -- the co-resident P2P shards of this process (n handles,
+ * LAMPS_SHARE_DEVICE, one stream each, distinct ranks of one world; the other ranks may
+ * live in other processes / on other GPUs and step in lockstep): enqueue one step on
+ * every handle's stream without events and without waiting (results with
+ * lamps_step_result per handle).  Every handle is validated before any is enqueued.
+ * Errors: EINVAL (handles not such a group, kv_total > kv_capacity_blocks, pending
+ * results unread on a handle is allowed), ECUDA.
+ */
+int lamps_group_step_async(lamps_t* const* h, uint32_t n, const uint64_t* kv_total);
 
 /* ---- predictor ingest and error injection ---------------- */
 

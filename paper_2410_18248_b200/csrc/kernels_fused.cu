@@ -1084,6 +1084,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // seven SoA words, L2 hits after the bulk prefetch above); keys compacted into kbuf (warp-
     // aggregated: one shared-memory atomic per warp); cold steps also count the keys' buckets
     uint32_t pinned = 0, nmine = 0;  // this thread's pinned blocks (< 2^32: <= 8 slots of < 2^16) and keys
+    const bool fixed16 = c.SH == 16u && c.lgB == 4u;  // the workloads' profiles (gen/configs.py)
     auto score1 = [&](uint32_t slot, uint32_t w, uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
                       uint32_t post, uint32_t pend, uint64_t& key) -> bool {
         if (w & SFC_RAN) {  // A0: the previous batch generated one token
@@ -1095,14 +1096,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             b.pool.pend[slot] = 0u;
         }
         const uint32_t st = sfc_state(w);
-        if (st == ST_PP) pinned += (ctx + c.B - 1u) >> c.lgB;
+        pinned += st == ST_PP ? (ctx + c.B - 1u) >> c.lgB : 0u;
         if (st != ST_READY) return false;
         const uint32_t has = sfc_has(w), rp = has ? resp : 0u, pp = has ? post : 0u;
         // fast check: all four below 2^18, so their sum is below 2^20 (kFastCtxLimit)
         if (c.lean && (ctx | pre | rp | pp) < (1u << 18)) {
-            // A1 + A2 (score_lean), A3: starvation, counter, key
+            // A1 + A2 (score_lean; SH = 16, B = 16 with immediate shifts), A3: starvation, counter, key
             uint64_t sc, wp, wd, ws;
-            const uint32_t strat = score_lean(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws);
+            const uint32_t strat = fixed16 ? score_lean<16, 4>(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws)
+                                           : score_lean(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws);
             const uint32_t cnt = sfc_cnt(w);
             const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
             w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u);

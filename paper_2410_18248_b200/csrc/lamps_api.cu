@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "lamps.h"
@@ -68,6 +69,12 @@ NcclApi g_nccl;
 struct NcclId { char internal[128]; };  // ncclUniqueId is passed by value
 typedef int (*CommInitRankFn)(nccl_comm_t*, int, NcclId, int);
 constexpr int kNcclUint8 = 1;  // ncclUint8 in ncclDataType_t
+
+// Exchange buffers exported by this process: a handle of one of them is mapped to its own
+// pointer by lamps_p2p_connect (CUDA IPC cannot open a handle in the exporting process), so
+// co-resident shards of this process and shards in other processes connect the same way.
+std::mutex g_exp_mu;
+std::vector<std::pair<cudaIpcMemHandle_t, MergeRec*>> g_exported;
 
 struct Layout {
     size_t off = 0;
@@ -188,6 +195,7 @@ const char* validate_cfg(const lamps_config* c) {
         if (c->transport == LAMPS_XPORT_P2P && (uint64_t)c->world * c->max_batch > kMergeMaxRecords)
             return "P2P transport: world * max_batch must be <= 8192 (the in-kernel merge); NCCL / loopback merge any";
         if (c->transport > LAMPS_XPORT_P2P) return "unknown transport";
+        if (c->local_ranks > (c->world > 1 ? c->world : 1u)) return "local_ranks must be <= world";
         if (c->transport == LAMPS_XPORT_NCCL && !c->nccl_id) return "NCCL transport needs nccl_id";
         if (c->world <= 1 && c->transport == LAMPS_XPORT_LOOPBACK)
             return "LAMPS_MERGE at world 1 needs the NCCL or P2P transport";
@@ -297,8 +305,10 @@ void grids(lamps_t* h, bool query_device) {
         fused_occ = fused_blocks_per_sm();
     }
     h->fused_grid = (uint32_t)std::max(1, sms * std::max(fused_occ, 1));
-    if ((h->cfg.flags & LAMPS_SHARE_DEVICE) && h->cfg.world > 1)  // co-resident ranks split the SMs
-        h->fused_grid = std::max<uint32_t>(1u, h->fused_grid / h->cfg.world);
+    if ((h->cfg.flags & LAMPS_SHARE_DEVICE) && h->cfg.world > 1) {  // co-resident ranks split the SMs
+        const uint32_t lr = h->cfg.local_ranks ? std::min(h->cfg.local_ranks, h->cfg.world) : h->cfg.world;
+        h->fused_grid = std::max<uint32_t>(1u, h->fused_grid / lr);
+    }
     if (const char* gv = std::getenv("LAMPS_FUSED_GRID"))  // measurements: a smaller step grid
         h->fused_grid = std::max<uint32_t>(1u, std::min<uint32_t>(h->fused_grid, (uint32_t)std::strtoul(gv, nullptr, 0)));
     {
@@ -403,7 +413,10 @@ StepArgs make_args(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
     if (h->merge) a.flags |= kStepMerge;
     if (h->merge && h->cfg.transport == LAMPS_XPORT_P2P) {
         a.flags |= kStepP2P;
-        if (h->world > 1 && !(h->cfg.flags & LAMPS_SHARE_DEVICE)) a.flags |= kStepP2PSys;
+        // peers on other GPUs: system scope (co-resident shards only: device scope)
+        const bool all_local = (h->cfg.flags & LAMPS_SHARE_DEVICE) &&
+                               (h->cfg.local_ranks == 0 || h->cfg.local_ranks >= h->world);
+        if (h->world > 1 && !all_local) a.flags |= kStepP2PSys;
         a.xseq = h->xseq;
         a.xtimeout_ms = h->xtimeout_ms;
     }
@@ -893,6 +906,14 @@ int lamps_free(lamps_t* h) {
     cudaStreamSynchronize(h->stream);
     for (void* p : h->peer_open) cudaIpcCloseMemHandle(p);
     if (h->d_peers) cudaFree(h->d_peers);
+    if (h->xbuf) {
+        std::lock_guard<std::mutex> lk(g_exp_mu);
+        for (size_t i = 0; i < g_exported.size(); i++)
+            if (g_exported[i].second == h->xbuf) {
+                g_exported.erase(g_exported.begin() + (long)i);
+                break;
+            }
+    }
     if (h->xbuf) cudaFree(h->xbuf);
     if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
     for (auto& e : h->tev)
@@ -1065,13 +1086,28 @@ int lamps_iterate(lamps_t* h, const lamps_iteration* it, lamps_step_out* out) {
     return fetch_result(h, out);
 }
 
+// A step group: loopback handles are ranks 0..n-1 of a world of n; P2P handles are distinct
+// ranks of one world (n <= world: the other ranks step in other processes).
+int check_group(lamps_t* const* hs, uint32_t n, bool p2p) {
+    uint64_t seen = 0;
+    for (uint32_t r = 0; r < n; r++) {
+        if (!hs[r] || hs[r]->cfg.max_batch != hs[0]->cfg.max_batch || hs[r]->world != hs[0]->world)
+            return fail(hs[0], LAMPS_EINVAL, "group: handles of one world");
+        if (!p2p && (hs[r]->world != n || hs[r]->rank != r))
+            return fail(hs[0], LAMPS_EINVAL, "group: loopback handles must be ranks 0..world-1");
+        if (p2p && (hs[r]->rank >= hs[r]->world || (seen >> hs[r]->rank) & 1ull))
+            return fail(hs[0], LAMPS_EINVAL, "group: P2P handles must be distinct ranks");
+        seen |= 1ull << hs[r]->rank;
+    }
+    return LAMPS_OK;
+}
+
 int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* const* ev, const uint32_t* n_ev,
                      const uint64_t* kv_total, lamps_step_out* out) {
     if (!hs || !n_ev || !kv_total || world < 2 || world > 32) return LAMPS_EINVAL;
     const bool p2p = hs[0] && hs[0]->cfg.transport == LAMPS_XPORT_P2P;
+    if (int rc = check_group(hs, world, p2p)) return rc;
     for (uint32_t r = 0; r < world; r++) {
-        if (!hs[r] || hs[r]->world != world || hs[r]->rank != r || hs[r]->cfg.max_batch != hs[0]->cfg.max_batch)
-            return fail(hs[0], LAMPS_EINVAL, "group: handles must be ranks 0..world-1");
         if (!p2p && (hs[r]->cfg.transport != LAMPS_XPORT_LOOPBACK || hs[r]->stream != hs[0]->stream))
             return fail(hs[0], LAMPS_EINVAL, "group: loopback handles on one stream");
         if (p2p && (hs[r]->cfg.transport != LAMPS_XPORT_P2P || !(hs[r]->cfg.flags & LAMPS_SHARE_DEVICE) ||
@@ -1108,10 +1144,35 @@ int lamps_group_step(lamps_t* const* hs, uint32_t world, const lamps_event* cons
     return LAMPS_OK;
 }
 
+int lamps_group_step_async(lamps_t* const* hs, uint32_t n, const uint64_t* kv_total) {
+    if (!hs || !kv_total || n < 1 || n > 32 || !hs[0]) return LAMPS_EINVAL;
+    if (int rc = check_group(hs, n, true)) return rc;
+    for (uint32_t r = 0; r < n; r++) {
+        if (hs[r]->cfg.transport != LAMPS_XPORT_P2P || !(hs[r]->cfg.flags & LAMPS_SHARE_DEVICE) || hs[r]->world < 2 ||
+            (r && hs[r]->stream == hs[0]->stream))
+            return fail(hs[0], LAMPS_EINVAL, "group async: P2P handles with LAMPS_SHARE_DEVICE and one stream each");
+        if (int rc = check_events(hs[r], nullptr, 0, kv_total[r])) return rc;
+        if (int rc = step_precheck(hs[r], true)) return rc;
+    }
+    for (uint32_t r = 0; r < n; r++)
+        if (int rc = stage_events(hs[r], nullptr, 0)) return rc;
+    for (uint32_t r = 0; r < n; r++) {
+        if (int rc = enqueue_phase1(hs[r], kv_total[r], 0)) return rc;
+        if (int rc = enqueue_phase2(hs[r], kv_total[r], 0, false)) return rc;
+    }
+    return LAMPS_OK;
+}
+
 int lamps_p2p_handle(lamps_t* h, void* out64) {
     if (!h || !out64) return LAMPS_EINVAL;
     if (!h->xbuf) return fail(h, LAMPS_EINVAL, "not a P2P-transport handle");
-    CU(h, cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(out64), h->xbuf));
+    cudaIpcMemHandle_t hd;
+    CU(h, cudaIpcGetMemHandle(&hd, h->xbuf));
+    std::memcpy(out64, &hd, sizeof(hd));
+    std::lock_guard<std::mutex> lk(g_exp_mu);
+    for (auto& e : g_exported)
+        if (e.second == h->xbuf) return LAMPS_OK;
+    g_exported.emplace_back(hd, h->xbuf);
     return LAMPS_OK;
 }
 
@@ -1124,6 +1185,16 @@ int lamps_p2p_connect(lamps_t* h, const void* handles, size_t n_bytes) {
         if (r == h->rank) { tab[r] = h->xbuf; continue; }
         cudaIpcMemHandle_t hd;
         std::memcpy(&hd, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(hd), sizeof(hd));
+        MergeRec* own = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_exp_mu);
+            for (auto& e : g_exported)
+                if (!std::memcmp(&e.first, &hd, sizeof(hd))) own = e.second;
+        }
+        if (own) {  // exported by this process (a co-resident shard)
+            tab[r] = own;
+            continue;
+        }
         void* p = nullptr;
         CU(h, cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
         h->peer_open.push_back(p);

@@ -207,26 +207,33 @@ __device__ __forceinline__ uint32_t strategy_score_fast(uint32_t ctx, uint32_t p
 __device__ __forceinline__ uint64_t mul32x64(uint32_t a, uint64_t b) {
     return wide32(a, (uint32_t)b) + (wide32(a, (uint32_t)(b >> 32)) << 32);
 }
+// SHC / LGC: the fixed-point shift SH and log2 B as compile-time constants (0: the runtime
+// values); the fused kernel instantiates the common (16, 4) so the 64-bit shifts are immediate
+template <uint32_t SHC = 0, uint32_t LGC = 0>
 __device__ __forceinline__ uint32_t score_lean(uint32_t ctx, uint32_t pre, uint32_t api, uint32_t rp, uint32_t pp,
                                                uint32_t pend, uint32_t has, const Cost& c, uint64_t& sc,
                                                uint64_t& wp, uint64_t& wd, uint64_t& ws) {
-    const uint32_t Bm1 = c.B - 1u, lg = c.lgB;
+    const uint32_t lg = LGC ? LGC : c.lgB, Bm1 = (1u << lg) - 1u;
+    const uint32_t SHv = SHC ? SHC : c.SH;
     const uint32_t ci = ctx + pre, cr = ci + rp, ce = cr + pp;
     auto F = [&](uint32_t n) { return wide32((n >> lg) + 1u, (n + (n & Bm1)) >> 1); };
     const uint64_t D = (F(ci) + F(ce)) - (F(ctx) + F(cr));
     uint64_t s = wide32((ctx + Bm1) >> lg, pend) + mul32x64((uint32_t)c.tau, D);
     const uint32_t A1 = (uint32_t)c.A1, A2 = (uint32_t)c.A2;
-    const uint64_t tf = (wide32(A1, ci) + mul32x64(A2, wide32(ci, ci))) >> c.SH;   // T_fwd(C_i)
-    const uint64_t ts = ci ? (c.S0 + wide32((uint32_t)c.S1, ci)) >> c.SH : 0ull;  // T_swap(C_i)
+    const uint64_t tf = (wide32(A1, ci) + mul32x64(A2, wide32(ci, ci))) >> SHv;   // T_fwd(C_i)
+    const uint64_t ts = ci ? (c.S0 + wide32((uint32_t)c.S1, ci)) >> SHv : 0ull;  // T_swap(C_i)
     const uint32_t cb = ci + (uint32_t)c.c_other;
     wp = wide32(api, ci);           // Eq. (1)
     wd = mul32x64(cb, tf);          // Eq. (2)
     ws = mul32x64(cb, ts) << 1;     // Eq. (3)
     const uint32_t strat = (wp <= wd && wp <= ws) ? STR_P : (wd <= ws ? STR_D : STR_S);
     const uint32_t bci = (ci + Bm1) >> lg, bcr = (cr + Bm1) >> lg;
-    const uint64_t tfr = (wide32(A1, cr) + mul32x64(A2, wide32(cr, cr))) >> c.SH;  // T_fwd(C_i + resp)
+    const uint64_t tfr = (wide32(A1, cr) + mul32x64(A2, wide32(cr, cr))) >> SHv;  // T_fwd(C_i + resp)
     const uint64_t aP = wide32(bci, api), aD = mul32x64(bcr, tfr), aS = mul32x64(bci, ts) << 1;
-    s += has ? (strat == STR_P ? aP : (strat == STR_D ? aD : aS)) : 0ull;
+    // branch-free selection (predicated moves, no divergence between strategies)
+    uint64_t aX = strat == STR_D ? aD : aS;
+    aX = strat == STR_P ? aP : aX;
+    s += has ? aX : 0ull;
     sc = s > c.score_max ? c.score_max : s;
     if (!has) wp = wd = ws = 0;
     return has ? strat : STR_NONE;

@@ -43,7 +43,7 @@ class lamps_config(ctypes.Structure):
                 ("ticks_per_second", dbl), ("starvation_threshold", u32), ("max_batch", u32),
                 ("kv_capacity_blocks", u64), ("score_bits", u32), ("id_bits", u32),
                 ("stream", vp), ("flags", u32), ("world", u32), ("rank", u32), ("transport", u32),
-                ("nccl_id", vp), ("policy", u32), ("score_interval", u32)]
+                ("nccl_id", vp), ("policy", u32), ("score_interval", u32), ("local_ranks", u32)]
 
 
 class lamps_step_out(ctypes.Structure):
@@ -118,6 +118,7 @@ def lib() -> ctypes.CDLL:
             "lamps_trace_read": (c_int, [vp, vp, u32, P(u32)]),
             "lamps_nccl_unique_id": (c_int, [vp]),
             "lamps_group_step": (c_int, [vp, u32, vp, vp, vp, vp]),
+            "lamps_group_step_async": (c_int, [vp, u32, vp]),
             "lamps_version": (u32, []),
             "lamps_predict": (c_int, [vp, vp, u32, P(lamps_noise), vp]),
             "lamps_p2p_handle": (c_int, [vp, vp]),
@@ -190,7 +191,7 @@ class Scheduler:
     """
 
     def __init__(self, cfg: dict, flags: int = 0, stream=None, device=None, world: int = 1, rank: int = 0,
-                 transport: int = LAMPS_XPORT_NCCL, nccl_id: bytes = None):
+                 transport: int = LAMPS_XPORT_NCCL, nccl_id: bytes = None, local_ranks: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise LampsError(LAMPS_ECUDA, "no CUDA device: the LAMPS pass has no CPU fallback")
@@ -203,7 +204,7 @@ class Scheduler:
                 setattr(c, name, cfg[name])
         c.flags = flags
         c.stream = ctypes.c_void_p(self.stream.cuda_stream)
-        c.world, c.rank, c.transport = world, rank, transport
+        c.world, c.rank, c.transport, c.local_ranks = world, rank, transport, local_ranks
         self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         c.nccl_id = ctypes.cast(self._nccl_id, vp) if self._nccl_id is not None else None
         self.world, self.rank = world, rank
@@ -415,6 +416,18 @@ class Scheduler:
         return [shards[r]._result(outs[r]) for r in range(W)]
 
     # ---- peer-memory transport (LAMPS_XPORT_P2P)
+    @staticmethod
+    def group_step_async(shards, kv_totals):
+        """Enqueue one step on every co-resident P2P shard of this process (each on its own
+        stream; the other ranks of the world step in lockstep elsewhere), lamps_group_step_async.
+        Results: shard.result()."""
+        W = len(shards)
+        kv = (u64 * W)(*[int(x) for x in kv_totals])
+        hs = (vp * W)(*[s.h for s in shards])
+        rc = lib().lamps_group_step_async(hs, W, kv)
+        if rc != LAMPS_OK:
+            raise LampsError(rc, lamps_last_error(shards[0].h))
+
     def p2p_handle(self) -> bytes:
         """This rank's 64-byte CUDA IPC handle of its exchange buffer."""
         buf = ctypes.create_string_buffer(64)

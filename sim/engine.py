@@ -84,13 +84,17 @@ def _truth_rows(reqs, items, tps):
 
 def run(cname: str, n_req: int, rate: float, backend, *, seed: int = 0, kv_total: int | None = None,
         len_error_ppm: int = 0, api_error_ppm: int = 0, noise_seed: int = 1, max_steps: int = 200_000,
-        profile: str | None = None, reqs=None) -> dict:
-    """Run the closed loop until every request finished (or max_steps).  Returns metrics."""
+        profile: str | None = None, reqs=None, api_scale: float = 1.0) -> dict:
+    """Run the closed loop until every request finished (or max_steps).  Returns metrics.
+    api_scale multiplies every true API duration (regimes where queueing, not the API wait,
+    dominates the completion time)."""
     c = gen.CONFIGS[cname]
     prof = gen.PROFILES[profile or c["profile"]]
     tau, tps = prof["tau"], prof["ticks_per_second"]
     kv = c["kv_total"] if kv_total is None else kv_total
     reqs = gen.requests(cname, n_req, seed=seed) if reqs is None else reqs
+    if api_scale != 1.0:
+        reqs = [dict(r, segs=[(p, d * api_scale, resp) for (p, d, resp) in r["segs"]]) for r in reqs]
     rng = np.random.Generator(np.random.PCG64(0xF2 + seed))
     per_step = rate * tau / tps
     arrive = []

@@ -31,3 +31,18 @@ def test_bench_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.timeout(600)
+def test_bench_strong_scaling_line():
+    """--scaling strong at N=1: the 1M pool as 8 co-resident shards of 131072 slots exchanging
+    their top-K by peer stores; one line, scaling "strong", 8 step kernels per timed step."""
+    r = subprocess.run([sys.executable, "bench.py", "--scaling", "strong", "--steps", "3", "--warmup", "3",
+                        "--e2e-steps", "5"], cwd=ROOT, capture_output=True, text=True, timeout=580)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.strip().startswith("{")]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["scaling"] == "strong" and d["n_gpus"] == 1 and d["config"]["shards"] == 8
+    assert d["config"]["shards_per_gpu"] == 8 and d["gpu_launches"] == 8 * 3
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["admitted_per_step"] > 0
