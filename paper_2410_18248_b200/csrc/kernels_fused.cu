@@ -1,984 +1,10 @@
-// kernels_fused.cu -- the whole scheduling step (A0 default update .. A5) as
-// ONE cooperative kernel, one 1024-thread CTA per SM, for pools whose per-SM
-// share of keys fits in shared memory (capacity <= #SM * kKcap).
-//
-//   S  score: each CTA scores its contiguous range of slots (A0 fused, A1, A2,
-//      A3, key) and keeps its keys in shared memory, with a histogram over
-//      "float-like" buckets of the key, (starving, bit length of the score, next
-//      kBucketM score bits): an exact monotone function of the key
-//   H  the CTA adds its bucket counts to the step's global totals with atomics;
-//      the returned old values are its offsets inside the buckets
-//   -- barrier --
-//   X  bucket starts (scan of the totals) and scatter of the keys into bucket
-//      order in global memory; every CTA derives the bucket-aligned key range
-//      it will sort
-//   -- barrier --
-//   L  each CTA sorts its range (<= kKcap keys) on chip: keys in registers, one
-//      counting pass by a per-bucket digit, rank-by-comparison inside the
-//      sub-buckets (range_sort).  If any range exceeds kKcap (a huge bucket of
-//      near-equal scores) every CTA runs the grid-synchronous global LSD sort
-//      instead (sort_dev.cuh).
-//   A  CTA 0 admits (A5) as soon as the head of the order it needs is sorted.
-#include <algorithm>
-
-#include "merge_dev.cuh"
-#include "sort_dev.cuh"
-#include "step_dev.cuh"
+// kernels_fused.cu -- the whole scheduling step (A0 default update .. A5) as ONE cooperative
+// kernel, one 1024-thread CTA per SM (see fused_dev.cuh for the phases and the on-chip sorts).
+#include "fused_dev.cuh"
 
 namespace lamps {
 
 namespace {
-
-constexpr int kFT = 1024;                   // threads per CTA
-constexpr int kFW = kFT / 32;               // warps
-constexpr int kKcap = kFusedKcap;           // keys per CTA in shared memory
-constexpr int kMaxBuckets = 14848;          // bucket table capacity (bucket_t, bt_update)
-constexpr int kTabW = 136;                  // bucket table: [0, 130) octave entries, [130] bucket count
-constexpr uint32_t kTabNB = 130;
-constexpr int kLocalItems = kKcap / kFT;    // 10
-constexpr int kMaxCtas = 256;               // range weights: grid size limit
-// splitters in shared memory: entry i at i + i / 16 (no bank conflicts in the binary search,
-// whose steps read the odd multiples of 128, 64, ... -- same banks without the padding)
-constexpr int kSplPad = kMaxCtas + 1 + (kMaxCtas + 1) / 16 + 1;
-__host__ __device__ constexpr uint32_t spl_pos(uint32_t i) { return i + (i >> 4); }
-// Global splitter grid per parity (written by each step for the next): fine[f], f = 0 .. 16 G;
-// range r = keys in [fine[16 r], fine[16 r + 16]), the 15 entries between are its quantiles
-// (the range sort's piecewise-linear digit); fine[16 G] = the largest key
-constexpr int kSeg = 16;
-constexpr int kSplG = kSeg * kMaxCtas + 16;
-
-struct PhaseS {                  // S, H, X (cold), R
-    uint64_t kbuf[kKcap];        // 80 KB: this CTA's keys (compacted, in no particular order)
-    uint32_t cnt[kMaxBuckets];   // 58 KB: bucket counts (cold); R: with start, the keys sorted by range
-    uint32_t start[kMaxBuckets]; // 58 KB: bucket totals -> bucket start positions (cold)
-    uint32_t w32[kFW + 1];
-    unsigned long long red[3][kFW];
-    uint32_t nk, base;
-    uint32_t vmask[kKcap / 32];  // S: which kbuf positions hold keys
-    float ccost[kMaxCtas];       // range-sort cycles per key of each CTA (previous steps)
-    uint32_t rb[kMaxCtas + 1], jb[kMaxCtas + 1];  // X: key / bucket boundaries of the ranges
-    float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
-    alignas(16) unsigned long long spl[kSplPad];  // R: range r = keys in [spl[P(r)], spl[P(r + 1)]), P = spl_pos
-    uint32_t lcnt[kMaxCtas + 1], lst[kMaxCtas + 1], gbase[kMaxCtas];  // R: this CTA's run per range
-};
-constexpr int kSubBits = 13;                // local MSD digit
-constexpr int kSubBuckets = 1 << kSubBits;
-constexpr uint32_t kMaxRankM = 32;          // largest group ranked by comparison
-constexpr int kChunk = 1024;                // score phase: slots per cp.async chunk
-constexpr int kMaxBig = 1024;               // groups per refinement list (else full LSD)
-constexpr int kMaxLevels = 6;               // refinement passes before the LSD fallback
-struct PhaseL {                  // L
-    uint64_t a[kKcap];           // 96 KB
-    uint64_t b[kKcap];           // 96 KB
-    union {
-        struct {                         // local LSD (fallback)
-            uint16_t whist[kFW][kBins];  // 16 KB
-            uint32_t part[4][kBins];     // 4 KB
-            uint32_t texcl[kBins];
-            uint32_t scan[kFW];
-        };
-        struct {                         // local MSD + rank
-            uint32_t pos[kKcap > kSubBuckets ? kKcap : kSubBuckets];  // 40 KB: counts -> starts; sbi
-            uint32_t w32[kFW + 1];
-            uint32_t nbig;
-        };
-    };
-    // group refinement: lists of groups still to split (ping-pong), and per group of the
-    // current batch: key offset (prefix of sizes), digit shift / bits, counter base, OR / AND
-    uint16_t gl_lo[2][kMaxBig], gl_n[2][kMaxBig];
-    uint32_t ngl[2];
-    uint16_t gcum[kMaxBig], gbase[kMaxBig];
-    uint8_t gsh[kMaxBig], gdb[kMaxBig];
-    unsigned long long gor[kMaxBig / 4], gand[kMaxBig / 4];
-    unsigned long long red[2][kFW];
-    AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
-    uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size and position in the order
-    unsigned long long fine[kSeg + 1], fcode[kSeg + 1];  // this range's grid entries, their key codes
-    uint32_t shs[kSeg];                                  // range sort: per segment, the digit's shift
-};
-struct FusedSmem {
-    union {
-        PhaseS s;
-        PhaseL l;
-        SortSmem g;
-    };
-    alignas(16) uint32_t btab[kTabW];  // this step's bucket table (bucket_t), every phase
-};
-// After the union, untouched by every phase: the peer-memory exchange's state (peer
-// buffer pointers, prefetched at kernel start) and the in-kernel merge's small structures.
-struct SmemTail {
-    MergeRec* xp[32];
-    AdmitSmem adm;
-    uint32_t nv[32];
-    unsigned long long hsum[2];
-};
-constexpr size_t kFusedSmemBytes = sizeof(FusedSmem) + ((sizeof(SmemTail) + 127) & ~(size_t)127);
-
-// Bucket of a key: (starving flag, bit length e of v = the key's score|id bits, the
-// next m_e bits of v) -- a float-like, exact monotone function of the key whose
-// resolution m_e per octave (ns, e) comes from a table: entry ns*65+e = base | s << 16 |
-// m << 24 (s = e-1-m: the low bits of v the bucket leaves free), bucket = base + the m
-// bits of v below its leading one.  Over v rather than the score alone, so keys whose
-// scores are equal or small (FCFS: all 0) still spread by id.  The table adapts to the
-// key distribution: every step writes the next step's table from its own octave counts
-// (bt_update), so buckets hold about the same number of keys; any valid table gives the
-// same order (only the balance of the ranges depends on it).
-__device__ __forceinline__ uint32_t bucket_t(uint64_t key, const uint32_t* tab, uint32_t vb, uint32_t& sv) {
-    const uint32_t ns = (uint32_t)(key >> vb) & 1u;
-    const uint64_t v = key & ((1ull << vb) - 1ull);
-    const uint32_t e = 64u - (uint32_t)__clzll((long long)v);  // bit length
-    const uint32_t t = tab[ns * 65u + e];
-    sv = (t >> 16) & 63u;
-    return (t & 0xffffu) + ((uint32_t)(v >> sv) & ((1u << (t >> 24)) - 1u));
-}
-
-// Next step's table from this step's bucket starts (exclusive scan `start` over the NB
-// buckets of the current table `tab`, n keys): octave o gets 2^m' buckets with
-// m' = floor(log2(n_o * kTabTarget / n)) (at least 1 bucket, at most 2^min(14, e-1)),
-// empty octaves 2 buckets; bases are the prefix of the spans in (ns, e) order.  The
-// total stays <= kTabTarget + 2 * 130 <= kMaxBuckets.  One warp.
-constexpr uint32_t kTabTarget = 12288;
-__device__ __forceinline__ void bt_update(const uint32_t* tab, const uint32_t* start, uint32_t n, uint32_t vb,
-                                          uint32_t* out) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t NB = tab[kTabNB];
-    uint32_t carry = 0;
-    for (uint32_t o0 = 0; o0 < kTabNB; o0 += 32) {
-        const uint32_t o = o0 + lane;
-        const uint32_t e = o % 65u;
-        const bool valid = o < kTabNB && e <= vb;
-        uint32_t span = 0, mq = 0;
-        if (valid) {
-            const uint32_t t = tab[o], base = t & 0xffffu, sp0 = 1u << (t >> 24);
-            const uint32_t s0 = base < NB ? start[base] : n, s1 = base + sp0 < NB ? start[base + sp0] : n;
-            const uint32_t no = s1 - s0, cap_m = e >= 1u ? min(14u, e - 1u) : 0u;
-            if (no == 0) {
-                mq = min(cap_m, 1u);
-            } else {
-                const uint64_t want = (uint64_t)no * kTabTarget / (n ? n : 1u);
-                mq = want <= 1 ? 0u : min(cap_m, 63u - (uint32_t)__clzll((long long)want));
-            }
-            span = 1u << mq;
-        }
-        uint32_t x = span;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= (uint32_t)d) x += y;
-        }
-        const uint32_t base = carry + x - span;
-        if (o < kTabNB) out[o] = valid ? (base | ((e >= 1u ? e - 1u - mq : 0u) << 16) | (mq << 24)) : base;
-        carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) out[kTabNB] = carry;
-}
-
-// Stable LSD sort of the n (<= kKcap) keys at src[0..n) in shared memory over the
-// 8-bit digit positions where `vary` has bits, ping-ponging with dst[0..n);
-// returns the buffer holding the result.  Keys are spread evenly over the 32
-// warps: warp w owns the contiguous segment [w*32*ipt, (w+1)*32*ipt), item j of
-// lane l is position w*32*ipt + j*32 + l, so (warp, j, lane) order is array
-// order (stability).  Ranks come from a ballot multisplit (digit_peers).
-__device__ __forceinline__ uint64_t* local_lsd(PhaseL& sm, uint64_t* src, uint64_t* dst, uint32_t n,
-                                               unsigned long long vary) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t ipt = (n + kFT - 1) / kFT;  // items per lane, <= kLocalItems
-    const uint32_t seg = 32u * ipt;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int dpos = 0; dpos < kDigits; dpos++) {
-        if (!((vary >> (8 * dpos)) & 0xffull)) continue;
-        const uint32_t shift = 8u * dpos;
-        for (uint32_t i = tid; i < kFW * kBins; i += kFT) (&sm.whist[0][0])[i] = 0;
-        __syncthreads();
-        uint32_t pk[kLocalItems];  // digit << 16 | rank within the warp (digit 256 = empty)
-#pragma unroll
-        for (int j = 0; j < kLocalItems; j++) {
-            pk[j] = 256u << 16;
-            if ((uint32_t)j < ipt) {  // warp-uniform
-                const uint32_t li = warp * seg + j * 32 + lane;
-                const uint32_t d = li < n ? (uint32_t)(src[li] >> shift) & 0xffu : 256u;
-                const uint32_t peers = digit_peers(d);
-                const uint32_t leader = __ffs(peers) - 1u;
-                uint32_t prior = 0;
-                if (d < 256u && lane == leader) {
-                    prior = sm.whist[warp][d];
-                    sm.whist[warp][d] = (uint16_t)(prior + __popc(peers));
-                }
-                prior = __shfl_sync(0xffffffffu, prior, leader);
-                pk[j] = (d << 16) | (prior + __popc(peers & lt_mask));
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        {   // per digit: exclusive prefix over the 32 warps, 4 threads per digit (8 warps each)
-            const uint32_t d = tid & 255u, q = tid >> 8;
-            uint32_t run = 0;
-#pragma unroll
-            for (int w = 0; w < kFW / 4; w++) run += sm.whist[q * (kFW / 4) + w][d];
-            sm.part[q][d] = run;
-            __syncthreads();
-            uint32_t before = 0, tot = 0;
-#pragma unroll
-            for (int qq = 0; qq < 4; qq++) {
-                const uint32_t v = sm.part[qq][d];
-                before += (uint32_t)qq < q ? v : 0u;
-                tot += v;
-            }
-#pragma unroll
-            for (int w = 0; w < kFW / 4; w++) {
-                uint16_t& h = sm.whist[q * (kFW / 4) + w][d];
-                const uint32_t v = h;
-                h = (uint16_t)before;
-                before += v;
-            }
-            const uint32_t e = digit_excl_scan(sm.scan, tid < kBins ? tot : 0u);
-            if (tid < kBins) sm.texcl[tid] = e;
-            __syncthreads();
-        }
-#pragma unroll
-        for (int j = 0; j < kLocalItems; j++) {
-            const uint32_t d = pk[j] >> 16;
-            if (d < 256u) {
-                const uint32_t li = warp * seg + j * 32 + lane;
-                dst[sm.texcl[d] + sm.whist[warp][d] + (pk[j] & 0xffffu)] = src[li];
-            }
-        }
-        __syncthreads();
-        uint64_t* t = src; src = dst; dst = t;
-    }
-    return src;
-}
-
-__device__ __forceinline__ void block_or_and(PhaseL& sm, const uint64_t* x, uint32_t n,
-                                             unsigned long long& o, unsigned long long& an) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    o = 0; an = ~0ull;
-    for (uint32_t i = tid; i < n; i += kFT) { o |= x[i]; an &= x[i]; }
-#pragma unroll
-    for (int s = 16; s; s >>= 1) {
-        o |= __shfl_xor_sync(0xffffffffu, o, s);
-        an &= __shfl_xor_sync(0xffffffffu, an, s);
-    }
-    if (lane == 0) { sm.red[0][warp] = o; sm.red[1][warp] = an; }
-    __syncthreads();
-    o = 0; an = ~0ull;
-    for (int w = 0; w < kFW; w++) { o |= sm.red[0][w]; an &= sm.red[1][w]; }
-    __syncthreads();
-}
-
-// Refinement of the groups listed in sm.gl_lo[0] / gl_n[0] (sm.ngl[0] of them; keys
-// at A[lo, lo+n), Bf scratch at the same offsets) until every group is <= kMaxRankM
-// keys and ranked.  Each pass: per group a digit of its own top varying bits (db =
-// ceil(log2 size) bits, from the group's OR/AND), counted with shared-memory atomics
-// into a counter block of its own; one scan over the blocks of a batch gives
-// positions; sub-groups still bigger than kMaxRankM go to the next pass.  Returns
-// true if the lists overflowed or kMaxLevels passes did not finish (the caller
-// then sorts the whole part by LSD).
-__device__ __forceinline__ bool refine_groups(PhaseL& sm, uint64_t* A, uint64_t* Bf, unsigned long long* xtr) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    uint32_t cur = 0;
-    bool full_lsd = false;
-    for (int level = 0; !full_lsd && level < kMaxLevels; level++) {
-        const uint32_t ng = sm.ngl[cur];
-        if (xtr && tid == 0) { xtr[2 * level] = clock64(); xtr[2 * level + 1] = ng; }
-        if (ng == 0) break;
-        if (ng > (uint32_t)kMaxBig) { full_lsd = true; break; }
-        const uint32_t nxt = cur ^ 1u;
-        if (tid == 0) sm.ngl[nxt] = 0;
-        if (warp == 0) {  // key offsets: exclusive prefix of the group sizes
-            uint32_t cum = 0;
-            for (uint32_t g0 = 0; g0 < ng; g0 += 32) {
-                const uint32_t g = g0 + lane, mm = g < ng ? sm.gl_n[cur][g] : 0u;
-                uint32_t x = mm;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= (uint32_t)o) x += y;
-                }
-                if (g < ng) sm.gcum[g] = (uint16_t)(cum + x - mm);
-                cum += __shfl_sync(0xffffffffu, x, 31);
-            }
-            if (lane == 0) sm.w32[kFW] = cum;
-        }
-        __syncthreads();
-        const uint32_t K = sm.w32[kFW];
-        auto group_of = [&](uint32_t f, uint32_t g0, uint32_t g1) {
-            uint32_t lo_ = g0, hi_ = g1;
-            while (hi_ - lo_ > 1) {
-                const uint32_t mid = (lo_ + hi_) >> 1;
-                if (sm.gcum[mid] <= f) lo_ = mid; else hi_ = mid;
-            }
-            return lo_;
-        };
-        for (uint32_t gb = 0; gb < ng;) {  // batches: OR/AND slots and counter blocks must fit
-            const uint32_t ge = min(ng, gb + (uint32_t)(kMaxBig / 4));
-            // OR / AND of each group's keys: one warp per group, shuffle reduction (64-bit
-            // shared-memory atomicOr/And would be CAS loops on a handful of addresses)
-            for (uint32_t g = gb + warp; g < ge; g += kFW) {
-                const uint32_t lo_g = sm.gl_lo[cur][g], m = sm.gl_n[cur][g];
-                unsigned long long o = 0, an = ~0ull;
-                for (uint32_t i = lane; i < m; i += 32) {
-                    const uint64_t k = A[lo_g + i];
-                    o |= k;
-                    an &= k;
-                }
-#pragma unroll
-                for (int sh = 16; sh; sh >>= 1) {
-                    o |= __shfl_xor_sync(0xffffffffu, o, sh);
-                    an &= __shfl_xor_sync(0xffffffffu, an, sh);
-                }
-                if (lane == 0) { sm.gor[g - gb] = o; sm.gand[g - gb] = an; }
-            }
-            const uint32_t f0 = sm.gcum[gb];
-            __syncthreads();
-            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[16] = clock64();
-            if (warp == 0) {  // digit shift / bits, counter bases; cut the batch at kSubBuckets
-                uint32_t base = 0, cut = ge;
-                for (uint32_t g0 = gb; g0 < ge; g0 += 32) {
-                    const uint32_t g = g0 + lane;
-                    uint32_t sz = 0;
-                    if (g < ge) {
-                        const unsigned long long v = sm.gor[g - gb] ^ sm.gand[g - gb];  // != 0: unique keys
-                        const int h = 63 - __clzll((long long)v);
-                        uint32_t db = 32u - (uint32_t)__clz((uint32_t)sm.gl_n[cur][g] - 1u);  // ceil(log2 m)
-                        db = db > (uint32_t)kSubBits ? (uint32_t)kSubBits : db;
-                        sm.gsh[g] = (uint8_t)(h + 1 >= (int)db ? h + 1 - (int)db : 0);
-                        sm.gdb[g] = (uint8_t)db;
-                        sz = 1u << db;
-                    }
-                    uint32_t x = sz;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= (uint32_t)o) x += y;
-                    }
-                    if (g < ge) sm.gbase[g] = (uint16_t)min(base + x - sz, 65535u);
-                    const uint32_t ob = __ballot_sync(0xffffffffu, g < ge && base + x > (uint32_t)kSubBuckets);
-                    if (ob && cut == ge) cut = g0 + __ffs(ob) - 1;
-                    base += __shfl_sync(0xffffffffu, x, 31);
-                }
-                if (lane == 0) sm.w32[kFW - 1] = cut > gb ? cut : gb + 1;
-            }
-            __syncthreads();
-            const uint32_t gcut = sm.w32[kFW - 1];
-            const uint32_t fc = gcut < ng ? (uint32_t)sm.gcum[gcut] : K;
-            const uint32_t ncnt = (uint32_t)sm.gbase[gcut - 1] + (1u << sm.gdb[gcut - 1]);
-            for (uint32_t i = tid; i < ncnt; i += kFT) sm.pos[i] = 0;
-            __syncthreads();
-#define GDIGIT(k, g) (sm.gbase[g] + ((uint32_t)((k) >> sm.gsh[g]) & ((1u << sm.gdb[g]) - 1u)))
-            for (uint32_t f = f0 + tid; f < fc; f += kFT) {
-                const uint32_t g = group_of(f, gb, gcut);
-                atomicAdd(&sm.pos[GDIGIT(A[sm.gl_lo[cur][g] + (f - sm.gcum[g])], g)], 1u);
-            }
-            __syncthreads();
-            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[17] = clock64();
-            (void)smem_excl_scan<kFT, kSubBuckets / kFT + 1>(sm.pos, ncnt, sm.w32);
-            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[18] = clock64();
-            // group g's keys occupy [gcum_g - f0, gcum_g - f0 + m_g) of the batch's scan space
-            for (uint32_t f = f0 + tid; f < fc; f += kFT) {
-                const uint32_t g = group_of(f, gb, gcut);
-                const uint32_t lo_g = sm.gl_lo[cur][g], gz = sm.gcum[g] - f0;
-                const uint64_t k = A[lo_g + (f - sm.gcum[g])];
-                Bf[lo_g + atomicAdd(&sm.pos[GDIGIT(k, g)], 1u) - gz] = k;
-            }
-            __syncthreads();
-            if (xtr && tid == 0 && level == 0 && gb == 0) xtr[19] = clock64();
-            for (uint32_t f = f0 + tid; f < fc; f += kFT) {  // finish small sub-groups, list big ones
-                const uint32_t g = group_of(f, gb, gcut);
-                const uint32_t lo_g = sm.gl_lo[cur][g], gz = sm.gcum[g] - f0;
-                const uint32_t i = f - sm.gcum[g];
-                const uint64_t k = Bf[lo_g + i];
-                const uint32_t d = GDIGIT(k, g);
-                const uint32_t e = sm.pos[d] - gz;
-                const uint32_t st = (d > sm.gbase[g] ? sm.pos[d - 1] : sm.gcum[g] - f0 + gz * 0u) - gz;
-                const uint32_t stc = d > sm.gbase[g] ? st : 0u;
-                const uint32_t m2 = e - stc;
-                if (m2 > kMaxRankM) {
-                    A[lo_g + i] = k;
-                    if (i == stc) {
-                        const uint32_t t = atomicAdd(&sm.ngl[nxt], 1u);
-                        if (t < (uint32_t)kMaxBig) {
-                            sm.gl_lo[nxt][t] = (uint16_t)(lo_g + stc);
-                            sm.gl_n[nxt][t] = (uint16_t)m2;
-                        }
-                    }
-                    continue;
-                }
-                uint32_t r = 0;
-#pragma unroll 8
-                for (uint32_t q = stc; q < e; q++) r += Bf[lo_g + q] < k ? 1u : 0u;
-                A[lo_g + stc + r] = k;
-            }
-#undef GDIGIT
-            __syncthreads();
-            if (xtr && tid == 0 && level == 0 && gb == 0) { xtr[20] = clock64(); xtr[21] = gcut; xtr[22] = fc - f0; }
-            gb = gcut;
-        }
-        cur = nxt;
-        if (level + 1 == kMaxLevels && sm.ngl[cur]) full_lsd = true;
-    }
-    return full_lsd;
-}
-
-// Sort of the n keys at A[0..n) of one part of a range (same starving flag) in
-// shared memory; result in A, Bf is scratch.  The part arrives in global-bucket
-// order and its buckets [j0, j1) are known, so the buckets are the first-level
-// groups (sizes = the global totals T[j]; a bucket lies entirely in one range).
-// Groups of <= kMaxRankM keys are finished by rank-by-comparison (keys are
-// unique).  Bigger groups are refined in flat passes over all their keys: per
-// group a digit of its own top varying bits (db = ceil(log2 size) bits, from the
-// group's OR/AND), counted with shared-memory atomics into a counter block of
-// its own; one scan over the blocks of a batch gives positions; sub-groups
-// still bigger than kMaxRankM go to the next pass.  After kMaxLevels passes (or
-// if the group tables overflow) the stable LSD finishes the part.
-__device__ __forceinline__ void local_sort(PhaseL& sm, uint64_t* A, uint64_t* Bf, uint32_t n,
-                                           const uint32_t* T, uint32_t j0, uint32_t j1,
-                                           unsigned long long* tr, unsigned long long* xtr = nullptr) {
-#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
-    const uint32_t tid = threadIdx.x;
-    if (n <= 1) return;
-    LTRACE(0);
-    bool full_lsd = false;
-    // ---- level 1: bucket runs.  pos[0..nb] = starts of the part's buckets.
-    const uint32_t nb = j1 - j0;
-    if (nb + 1 > (uint32_t)kSubBuckets) {
-        full_lsd = true;
-    } else {
-        for (uint32_t j = tid; j < nb; j += kFT) sm.pos[j] = __ldcg(&T[j0 + j]);
-        if (tid == 0) { sm.ngl[0] = 0; sm.ngl[1] = 0; }
-        for (uint32_t i = tid; i < n; i += kFT) Bf[i] = A[i];
-        __syncthreads();
-        (void)smem_excl_scan<kFT, kSubBuckets / kFT + 1>(sm.pos, nb, sm.w32);
-        if (tid == 0) sm.pos[nb] = n;
-        __syncthreads();
-        LTRACE(1);
-        for (uint32_t i = tid; i < n; i += kFT) {
-            uint32_t lo_ = 0, hi_ = nb;  // last bucket with start <= i
-            while (hi_ - lo_ > 1) {
-                const uint32_t mid = (lo_ + hi_) >> 1;
-                if (sm.pos[mid] <= i) lo_ = mid; else hi_ = mid;
-            }
-            const uint32_t st = sm.pos[lo_], e = sm.pos[lo_ + 1], m = e - st;
-            const uint64_t k = Bf[i];
-            if (m > kMaxRankM) {
-                if (i == st) {
-                    const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
-                    if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m; }
-                }
-                continue;  // A[i] == k already
-            }
-            uint32_t r = 0;
-#pragma unroll 8
-            for (uint32_t q = st; q < e; q++) r += Bf[q] < k ? 1u : 0u;
-            A[st + r] = k;
-        }
-        __syncthreads();
-        LTRACE(2);
-    }
-    // ---- refinement passes over the big groups
-    if (!full_lsd) full_lsd = refine_groups(sm, A, Bf, xtr);
-    LTRACE(3);
-    if (xtr && tid == 0) xtr[14] = clock64();
-    if (full_lsd) {  // pathological distributions: stable LSD of the whole part
-        unsigned long long o, an;
-        block_or_and(sm, A, n, o, an);
-        const uint64_t* r = local_lsd(sm, A, Bf, n, o ^ an);
-        if (r != A)
-            for (uint32_t i = tid; i < n; i += kFT) A[i] = r[i];
-        __syncthreads();
-    }
-    if (tr && tid == 0) tr[5] = full_lsd ? 1000u : sm.ngl[0];
-    LTRACE(4);
-#undef LTRACE
-}
-
-// Digit of key k inside its bucket: the top db bits of the sv low bits of v the bucket
-// leaves free (sv from bucket_t), i.e. (low score bits, id offset).  The id offset
-// (id - id_base, the key's low IB bits) is < cap = 2^lg_cap, so it is packed into lg_cap
-// bits (not IB) and its top bits carry information.  Monotone in the key within a
-// bucket, so (bucket, digit) order is key order.
-__device__ __forceinline__ uint32_t sub_digit_t(uint64_t k, uint32_t sv, uint32_t db, const Cost& c,
-                                                uint32_t lg_cap) {
-    const uint64_t idoff = k & (uint64_t)c.cap_mask;
-    uint64_t v;
-    uint32_t wv;
-    if (sv > c.IB) {  // varying score bits, then the id offset packed into lg_cap bits
-        v = (((k >> c.IB) & ((1ull << (sv - c.IB)) - 1ull)) << lg_cap) | idoff;
-        wv = sv - c.IB + lg_cap;
-    } else {          // id bits only; those above lg_cap are always 0
-        wv = sv < lg_cap ? sv : lg_cap;
-        v = idoff & ((1ull << wv) - 1ull);
-    }
-    return wv >= db ? (uint32_t)(v >> (wv - db)) : (uint32_t)(v << (db - wv));
-}
-
-// Sort of a CTA's key range (rn <= kKcap keys in global src, buckets [j_lo, j_hi),
-// j_hi - j_lo < kSubBuckets) into sm.a.  Keys stay in registers (<= kLocalItems per
-// thread).  One counting pass: each bucket of m keys gets 2^ceil(log2 m) counters
-// (the bucket's exact size is the global total T[j]: a bucket lies entirely in one
-// range) indexed by sub_digit, so the sub-buckets hold ~1 key; keys of sub-buckets
-// of <= kMaxRankM keys are ranked by comparison, bigger ones (many near-equal keys)
-// go to refine_groups, and an LSD of the whole range is the last resort.
-//
-// Head range (pool != nullptr, rn <= kHeadPre): the admission's per-key loads (ctx for
-// the demand blk(ctx+1), the state word) are issued with the key loads and land in
-// shared memory in sorted order (kHeadD / kHeadW words of sm.b), so A5 needs no
-// dependent global round trip.  Returns whether those arrays are valid (not after a
-// refinement pass, which moves keys).
-constexpr uint32_t kHeadPre = 2560;
-constexpr uint32_t kHeadMargin = 128;   // the head range: max_batch + this many keys of the previous order
-// range_sort ranks sub-buckets of up to this many keys by comparison (one thread per
-// key, O(size) shared-memory reads): cheaper than a refinement pass for the few
-// sub-buckets of near-equal keys (e.g. saturated scores) a range may hold
-#ifndef LAMPS_RANK_M  // A/B builds: scripts/build_variant.sh out.so -DLAMPS_RANK_M=...
-#define LAMPS_RANK_M 256
-#endif
-constexpr uint32_t kRangeRankM = LAMPS_RANK_M;
-constexpr uint32_t kHeadTC = 2 * kKcap / 2, kHeadTW = kHeadTC + kHeadPre;  // by initial position
-constexpr uint32_t kHeadD = kHeadTW + kHeadPre, kHeadW = kHeadD + kHeadPre;  // sorted demand / state
-static_assert(kHeadW + kHeadPre <= 2 * kKcap, "head arrays exceed sm.b");
-// NI = keys per thread (kLocalItems; 3 for the head range, whose loads for the
-// admission stay in flight in registers for the whole sort)
-template <int NI, bool HEAD>
-__device__ __forceinline__ bool range_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
-                                           uint32_t j_lo, uint32_t j_hi, const Cost& c,
-                                           const uint32_t* tab, unsigned long long* tr, const Pool* pool = nullptr,
-                                           uint32_t id_base_mod = 0) {
-#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
-    const uint32_t tid = threadIdx.x;
-    const uint32_t nb = j_hi - j_lo;
-    const uint32_t lg_cap = 31u - (uint32_t)__clz(c.cap);
-    uint32_t* P = sm.pos;                                  // per bucket: start | counter base << 14
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);     // <= 2 * kKcap counters
-    uint64_t* A = sm.a;
-    LTRACE(0);
-    static_assert(!HEAD || NI * kFT >= (int)kHeadPre, "head items");
-    uint64_t k[NI];
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        k[u] = i < rn ? __ldcg(src + i) : 0ull;
-    }
-    uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
-    constexpr int kHU = HEAD ? NI : 1;
-    if (HEAD) {  // L2 prefetch of what the admission reads (no registers held in flight)
-#pragma unroll
-        for (int u = 0; u < kHU; u++) {
-            const uint32_t i = tid + (uint32_t)u * kFT;
-            if (i < rn) {
-                const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->ctx + slot));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->sfc + slot));
-            }
-        }
-    }
-    // the bucket of every key (kept in registers: J - j_lo | sv << 16) and the range's own
-    // bucket counts (a bucket may straddle two ranges)
-    for (uint32_t j = tid; j <= nb; j += kFT) P[j] = 0;
-    if (tid == 0) sm.ngl[0] = 0;
-    __syncthreads();
-    uint32_t jv[NI];
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        jv[u] = 0;
-        if (i < rn) {
-            uint32_t sv;
-            const uint32_t J = bucket_t(k[u], tab, c.SB + c.IB, sv) - j_lo;
-            jv[u] = J | (sv << 16);
-            atomicAdd(&P[J], 1u);
-        }
-    }
-    __syncthreads();
-    for (uint32_t j = tid; j < nb; j += kFT) {
-        const uint32_t m = P[j];
-        const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
-        P[j] = m | ((m ? 1u << db : 0u) << 14);  // empty buckets take no counters: ncnt < 2 rn
-    }
-    __syncthreads();
-    const uint32_t ptot = smem_excl_scan<kFT, kSubBuckets / kFT + 1>(P, nb, sm.w32);
-    const uint32_t ncnt = ptot >> 14;
-    if (tid == 0) P[nb] = ptot;
-    for (uint32_t i = tid; i < ncnt; i += kFT) cnt[i] = 0;
-    __syncthreads();
-    LTRACE(1);
-    uint32_t it[NI];  // counter index | order within the sub-bucket << 15
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        it[u] = 0;
-        if (i < rn) {
-            const uint32_t J = jv[u] & 0xffffu, sv = jv[u] >> 16;
-            const uint32_t p0 = P[J], p1 = P[J + 1];
-            const uint32_t m = (p1 & 0x3fffu) - (p0 & 0x3fffu);
-            const uint32_t db = m > 1u ? 32u - (uint32_t)__clz(m - 1u) : 0u;
-            const uint32_t idx = (p0 >> 14) + sub_digit_t(k[u], sv, db, c, lg_cap);
-            it[u] = idx | (atomicAdd(&cnt[idx], 1u) << 15);
-        }
-    }
-    __syncthreads();
-    (void)smem_excl_scan<kFT, 2 * NI + 1>(cnt, ncnt, sm.w32);
-    LTRACE(2);
-    // initial placement: sub-bucket start + arrival order; per position its sub-bucket's
-    // (start, size) in sbi (P is dead after the count pass)
-    uint32_t* sbi = sm.pos;
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        if (i < rn) {
-            const uint32_t idx = it[u] & 0x7fffu;
-            const uint32_t st = cnt[idx], e = idx + 1u < ncnt ? cnt[idx + 1] : rn;
-            const uint32_t p = st + (it[u] >> 15);
-            A[p] = k[u];
-            sbi[p] = st | ((e - st) << 14);
-            if (HEAD) {  // the admission's loads (L2 hits by now), by position
-                const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
-                b32[kHeadTC + p] = __ldcg(&pool->ctx[slot]);
-                b32[kHeadTW + p] = __ldcg(&pool->sfc[slot]);
-            }
-        }
-    }
-    __syncthreads();
-    // rank inside sub-buckets of <= kRangeRankM keys by comparison; list the bigger ones.
-    // Thread t takes positions t + u*kFT: a sub-bucket's keys are contiguous, so the lanes
-    // of a warp mostly share a sub-bucket and the loop trip counts agree
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t p = tid + (uint32_t)u * kFT;
-        it[u] = 0;
-        if (p < rn) {
-            k[u] = A[p];
-            const uint32_t inf = sbi[p];
-            const uint32_t st = inf & 0x3fffu, m2 = inf >> 14;
-            if (m2 <= kRangeRankM) {
-                uint32_t r = 0;
-#pragma unroll 4
-                for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k[u] ? 1u : 0u;
-                it[u] = (st + r) | 0x80000000u;
-            } else if (p == st) {
-                const uint32_t t = atomicAdd(&sm.ngl[0], 1u);
-                if (t < (uint32_t)kMaxBig) { sm.gl_lo[0][t] = (uint16_t)st; sm.gl_n[0][t] = (uint16_t)m2; }
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t p = tid + (uint32_t)u * kFT;
-        if (p < rn && (it[u] >> 31)) {
-            const uint32_t pos = it[u] & 0x7fffffffu;
-            A[pos] = k[u];
-            if (HEAD) {
-                b32[kHeadD + pos] = (uint32_t)blk((uint64_t)b32[kHeadTC + p] + 1u, c);
-                b32[kHeadW + pos] = b32[kHeadTW + p];
-            }
-        }
-    }
-    __syncthreads();
-    LTRACE(3);
-    bool full_lsd = false;
-    if (sm.ngl[0]) full_lsd = refine_groups(sm, A, sm.b, nullptr);
-    if (full_lsd) {
-        unsigned long long o, an;
-        block_or_and(sm, A, rn, o, an);
-        const uint64_t* r = local_lsd(sm, A, sm.b, rn, o ^ an);
-        if (r != A)
-            for (uint32_t i = tid; i < rn; i += kFT) A[i] = r[i];
-        __syncthreads();
-    }
-    const bool dw_ok = HEAD && sm.ngl[0] == 0;
-    if (tr && tid == 0) { tr[5] = full_lsd ? 1000u : sm.ngl[0]; }
-    LTRACE(4);
-#undef LTRACE
-    return dw_ok;
-}
-
-// Sort of a CTA's key range (rn <= kKcap keys at src, global) into sm.a with one counting
-// pass on a LINEAR digit of the key, d = (k - kmin) >> sh, over 2^ceil(log2 rn) counters
-// spanning [kmin, kmax] of the range's own keys: a range between two quantiles of the order
-// holds keys of about one octave, spread about evenly, so a counter holds ~1 key.  Keys of a
-// counter are ranked by comparison (<= kRangeRankM keys; unique keys: rank = number of
-// smaller keys), bigger groups are refined (refine_groups), an LSD of the range is the last
-// resort -- any key distribution gives the exact order.  Keys stay in registers (NI per thread).
-// Code space of the linear digit: the key's (starving flag, bit length e of v, the 40 bits of v
-// below its leading one) -- monotone in the key, linear in v inside an octave, so a range
-// spanning several octaves (or the starving / not-starving boundary) still spreads evenly.
-__device__ __forceinline__ unsigned long long key_code(uint64_t k, uint32_t vb) {
-    const uint64_t v = k & ((1ull << vb) - 1ull);
-    const uint32_t e = 64u - (uint32_t)__clzll((long long)v);
-    const uint64_t mant = e ? ((v << (64u - e)) << 1) >> 24 : 0ull;
-    return ((unsigned long long)(((uint32_t)(k >> vb) << 6) | e) << 40) | mant;
-}
-// Sort of a CTA's key range (rn <= kKcap keys at src, global, L2-resident) straight into its
-// place in the ranked order (out, global), in compact loops (this code runs once per step and
-// is fetched cold, so no per-thread item arrays).  One counting pass on a piecewise-linear
-// digit: the range's 16 segments between its grid entries sm.fine[0..16] (quantiles of the
-// previous step's order, so each segment holds ~1/16 of the keys) get W counters each, a key's
-// counter is seg * W + (code(k) - code(fine[seg])) >> shift(seg), clamped -- monotone in the
-// key, ~2 counters per key whatever the density inside the range.  Placement by digit into
-// sm.a, then each key's rank inside its counter by comparison (<= kRangeRankM keys; unique keys:
-// the number of smaller keys) gives its final position.  Returns false if a counter held more
-// keys: sm.a then holds the range (placed by digit) and the caller sorts it otherwise.
-// CTA 0 (pool != nullptr, head staging): the admission's per-key loads (ctx for the demand
-// blk(ctx + 1), the state word) are issued in the rank pass and land in dsm / wsm (shared
-// memory) by final position, and the ranked keys stay in sm.b: A5 then needs no global round
-// trip for its head.
-__device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
-                                                uint64_t* __restrict__ out, uint32_t vb, unsigned long long* tr,
-                                                const Pool* pool = nullptr, uint32_t id_base_mod = 0,
-                                                const Cost* cc = nullptr, uint32_t* dsm = nullptr,
-                                                uint32_t* wsm = nullptr) {
-#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
-    const uint32_t tid = threadIdx.x;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);                      // <= 2^13 + 1 counters
-    uint16_t* dp = reinterpret_cast<uint16_t*>(sm.b) + 2u * ((1u << 13) + 4u);  // per position: digit
-    uint32_t* dv = sm.pos;                                                   // per key: digit | order << 13
-    uint64_t* A = sm.a;
-    LTRACE(0);
-    const uint32_t cb = max(min(rn > 1u ? 33u - (uint32_t)__clz(rn - 1u) : 0u, 13u), 4u);  // ~2-4 counters per key
-    const uint32_t lw = cb - 4u, W = 1u << lw, ncnt = (uint32_t)kSeg * W;  // W counters per segment
-    uint32_t* shs = sm.shs;  // per segment: shift of the code difference
-    if (tid < (uint32_t)kSeg) {
-        const unsigned long long d = sm.fcode[tid + 1] > sm.fcode[tid] ? sm.fcode[tid + 1] - sm.fcode[tid] : 0ull;
-        const uint32_t nb = 64u - (uint32_t)__clzll((long long)d);
-        shs[tid] = nb > lw ? nb - lw : 0u;
-    }
-    for (uint32_t i = tid; i <= ncnt; i += kFT) cnt[i] = 0u;
-    __syncthreads();
-    auto digit = [&](uint64_t k) -> uint32_t {
-        uint32_t sg = 0;
-#pragma unroll
-        for (uint32_t st = kSeg / 2; st; st >>= 1) sg = k >= sm.fine[sg + st] ? sg + st : sg;
-        const unsigned long long c = key_code(k, vb), c0 = sm.fcode[sg];
-        const unsigned long long d = (c > c0 ? c - c0 : 0ull) >> shs[sg];
-        return sg * W + (uint32_t)min(d, (unsigned long long)(W - 1u));
-    };
-    LTRACE(1);
-    for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {  // four loads in flight per thread
-        uint64_t kk[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) kk[u] = i0 + (uint32_t)u * kFT < rn ? __ldcg(src + i0 + (uint32_t)u * kFT) : 0ull;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const uint32_t i = i0 + (uint32_t)u * kFT;
-            if (i < rn) {
-                const uint32_t d = digit(kk[u]);
-                dv[i] = d | (atomicAdd(&cnt[d], 1u) << 13);
-            }
-        }
-    }
-    __syncthreads();
-    LTRACE(2);
-    (void)smem_excl_scan<kFT, (1 << 13) / kFT + 1>(cnt, ncnt, sm.w32);
-    if (tid == 0) cnt[ncnt] = rn;
-    LTRACE(3);
-    for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
-        uint64_t kk[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) kk[u] = i0 + (uint32_t)u * kFT < rn ? __ldcg(src + i0 + (uint32_t)u * kFT) : 0ull;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const uint32_t i = i0 + (uint32_t)u * kFT;
-            if (i < rn) {
-                const uint32_t v = dv[i], d = v & 0x1fffu, p = cnt[d] + (v >> 13);
-                A[p] = kk[u];
-                dp[p] = (uint16_t)d;
-            }
-        }
-    }
-    __syncthreads();
-    LTRACE(4);
-    bool big = false;
-    for (uint32_t p = tid; p < rn; p += kFT) {
-        const uint64_t k = A[p];
-        const uint32_t d = dp[p], st = cnt[d], m2 = cnt[d + 1] - st;
-        uint32_t r = 0;
-        if (m2 <= 4u) {  // the common case: straight-line, predicated compares
-            if (m2 > 1u) {
-                r += A[st] < k ? 1u : 0u;
-                r += A[st + 1] < k ? 1u : 0u;
-                if (m2 > 2u) r += A[st + 2] < k ? 1u : 0u;
-                if (m2 > 3u) r += A[st + 3] < k ? 1u : 0u;
-            }
-        } else if (m2 <= kRangeRankM) {
-            for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k ? 1u : 0u;
-        } else {
-            big = true;
-            continue;
-        }
-        dv[p] = st + r;  // final position (dv is free after the placement)
-    }
-    LTRACE(5);
-    if (__syncthreads_or(big)) return false;
-    // the ranked keys gathered in shared memory (sm.b: the counters are dead), then written out
-    // whole lines at a time (scattered 8-byte stores to lines not in L2 stall the store path)
-    uint64_t* B2 = sm.b;
-    for (uint32_t p = tid; p < rn; p += kFT) B2[dv[p]] = A[p];
-    __syncthreads();
-    if (dsm) {  // CTA 0: the admission's loads (L2 hits: the score phase read them), all in flight at once
-        for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
-            uint32_t cx[4], w[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t i = i0 + (uint32_t)u * kFT;
-                const uint32_t slot = i < rn ? (id_base_mod + (uint32_t)(B2[i] & cc->cap_mask)) & cc->cap_mask : 0u;
-                cx[u] = i < rn ? __ldcg(&pool->ctx[slot]) : 0u;
-                w[u] = i < rn ? __ldcg(&pool->sfc[slot]) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t i = i0 + (uint32_t)u * kFT;
-                if (i < rn) {
-                    dsm[i] = (uint32_t)blk((uint64_t)cx[u] + 1u, *cc);
-                    wsm[i] = w[u];
-                }
-            }
-        }
-        __syncthreads();
-    }
-    for (uint32_t i = tid; i < rn; i += kFT) out[i] = B2[i];
-    LTRACE(6);
-#undef LTRACE
-    return true;
-}
-
-// A small range (rn <= kSmallSort keys): ranked by comparison against all its keys (the
-// keys are unique, so the rank is the count of smaller keys; the few hundred keys are read
-// as shared-memory broadcasts), no bucket table.  A small pool's head range can span
-// thousands of sparse buckets (starving keys first, over the whole score range), where
-// the table dominates.  HEAD (CTA 0): the admission's per-key loads by sorted position into
-// the staged head arrays, prefetched to L2 while ranking.
-constexpr uint32_t kSmallSort = 384;
-template <bool HEAD>
-__device__ __forceinline__ void small_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn, const Cost& c,
-                                           const Pool* pool, uint32_t id_base_mod) {
-    const uint32_t tid = threadIdx.x;
-    uint64_t* A = sm.a;
-    uint64_t* Bq = sm.b;  // scratch [0, rn): below the staged head arrays
-    uint64_t k = 0;
-    if (tid < rn) {
-        k = __ldcg(src + tid);
-        A[tid] = k;
-        if (HEAD) {
-            const uint32_t slot = (id_base_mod + (uint32_t)(k & c.cap_mask)) & c.cap_mask;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->ctx + slot));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool->sfc + slot));
-        }
-    }
-    __syncthreads();
-    if (tid < rn) {
-        uint32_t r = 0;
-#pragma unroll 8
-        for (uint32_t q = 0; q < rn; q++) r += A[q] < k ? 1u : 0u;
-        Bq[r] = k;
-    }
-    __syncthreads();
-    if (tid < rn) {
-        const uint64_t x = Bq[tid];
-        A[tid] = x;
-        if (HEAD) {
-            uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
-            const uint32_t slot = (id_base_mod + (uint32_t)(x & c.cap_mask)) & c.cap_mask;
-            b32[kHeadD + tid] = (uint32_t)blk((uint64_t)__ldcg(&pool->ctx[slot]) + 1u, c);
-            b32[kHeadW + tid] = __ldcg(&pool->sfc[slot]);
-        }
-    }
-    __syncthreads();
-}
-
-// CTA 0's head range when its buckets are sparse (nb > 2 rn: the head's starving keys span
-// a wide score range): a counting sort over the OCCUPIED buckets only -- a bitmap of the
-// keys' buckets, their compact index by popcount prefix -- then rank by comparison inside
-// each bucket (a bucket holds ~1 key here), then the admission's per-key loads by sorted
-// position (prefetched to L2 at the start).  No bucket table over the whole interval.
-// Returns false (nothing written) if a bucket holds more than kRangeRankM keys; the caller
-// then uses range_sort.
-__device__ __forceinline__ bool head_sparse_sort(PhaseL& sm, const uint64_t* __restrict__ src, uint32_t rn,
-                                                 const Cost& c, const uint32_t* tab, uint32_t j_lo, uint32_t nb,
-                                                 const Pool& pool, uint32_t id_base_mod) {
-    constexpr int NI = (kHeadPre + kFT - 1) / kFT;  // 3
-    const uint32_t tid = threadIdx.x;
-    uint32_t* bm = sm.pos;            // bucket bitmap, nw <= 1024 words
-    uint32_t* wp = sm.pos + 1024;     // exclusive popcount prefix per word
-    uint32_t* cnt = sm.pos + 2048;    // per occupied bucket: count -> start
-    uint32_t* sbi = sm.pos + 4608;    // per position: bucket start | size << 14
-    uint64_t* A = sm.a;
-    uint64_t* Bq = sm.b;              // [0, rn): below the staged head arrays
-    const uint32_t nw = (nb + 31u) >> 5;
-    for (uint32_t w = tid; w < nw; w += kFT) bm[w] = 0u;
-    __syncthreads();
-    uint64_t k[NI];
-    uint32_t J[NI], ci[NI];
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        k[u] = 0;
-        J[u] = 0;
-        if (i < rn) {
-            k[u] = __ldcg(src + i);
-            uint32_t sv;
-            J[u] = bucket_t(k[u], tab, c.SB + c.IB, sv) - j_lo;
-            atomicOr(&bm[J[u] >> 5], 1u << (J[u] & 31u));
-            const uint32_t slot = (id_base_mod + (uint32_t)(k[u] & c.cap_mask)) & c.cap_mask;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool.ctx + slot));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(pool.sfc + slot));
-        }
-    }
-    __syncthreads();
-    for (uint32_t w = tid; w < nw; w += kFT) wp[w] = __popc(bm[w]);
-    __syncthreads();
-    const uint32_t nocc = smem_excl_scan<kFT, 1>(wp, nw, sm.w32);
-    for (uint32_t q = tid; q < nocc; q += kFT) cnt[q] = 0u;
-    __syncthreads();
-    uint32_t ord[NI];
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        ci[u] = 0;
-        ord[u] = 0;
-        if (i < rn) {
-            const uint32_t w = J[u] >> 5;
-            ci[u] = wp[w] + __popc(bm[w] & ((1u << (J[u] & 31u)) - 1u));
-            ord[u] = atomicAdd(&cnt[ci[u]], 1u);
-        }
-    }
-    __syncthreads();
-    uint32_t big = 0;
-    for (uint32_t q = tid; q < nocc; q += kFT) big |= cnt[q] > kRangeRankM ? 1u : 0u;
-    if (__syncthreads_or(big)) return false;
-    (void)smem_excl_scan<kFT, 3>(cnt, nocc, sm.w32);
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t i = tid + (uint32_t)u * kFT;
-        if (i < rn) {
-            const uint32_t st = cnt[ci[u]], e = ci[u] + 1u < nocc ? cnt[ci[u] + 1u] : rn;
-            const uint32_t p = st + ord[u];
-            A[p] = k[u];
-            sbi[p] = st | ((e - st) << 14);
-        }
-    }
-    __syncthreads();
-    uint32_t* b32 = reinterpret_cast<uint32_t*>(sm.b);
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const uint32_t p = tid + (uint32_t)u * kFT;
-        if (p < rn) {
-            const uint64_t x = A[p];
-            const uint32_t inf = sbi[p], st = inf & 0x3fffu, m = inf >> 14;
-            uint32_t r = 0;
-            for (uint32_t q = 0; q < m; q++) r += A[st + q] < x ? 1u : 0u;
-            const uint32_t fp = st + r;
-            Bq[fp] = x;
-            const uint32_t slot = (id_base_mod + (uint32_t)(x & c.cap_mask)) & c.cap_mask;
-            b32[kHeadD + fp] = (uint32_t)blk((uint64_t)__ldcg(&pool.ctx[slot]) + 1u, c);
-            b32[kHeadW + fp] = __ldcg(&pool.sfc[slot]);
-        }
-    }
-    __syncthreads();
-    for (uint32_t p = tid; p < rn; p += kFT) A[p] = Bq[p];
-    __syncthreads();
-    return true;
-}
 
 #define TRACE(k)                                                                         \
     do {                                                                                 \
@@ -1084,7 +110,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // seven SoA words, L2 hits after the bulk prefetch above); keys compacted into kbuf (warp-
     // aggregated: one shared-memory atomic per warp); cold steps also count the keys' buckets
     uint32_t pinned = 0, nmine = 0;  // this thread's pinned blocks (< 2^32: <= 8 slots of < 2^16) and keys
-    const bool fixed16 = c.SH == 16u && c.lgB == 4u;  // the workloads' profiles (gen/configs.py)
+
     auto score1 = [&](uint32_t slot, uint32_t w, uint32_t ctx, uint32_t pre, uint32_t api, uint32_t resp,
                       uint32_t post, uint32_t pend, uint64_t& key) -> bool {
         if (w & SFC_RAN) {  // A0: the previous batch generated one token
@@ -1101,10 +127,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         const uint32_t has = sfc_has(w), rp = has ? resp : 0u, pp = has ? post : 0u;
         // fast check: all four below 2^18, so their sum is below 2^20 (kFastCtxLimit)
         if (c.lean && (ctx | pre | rp | pp) < (1u << 18)) {
-            // A1 + A2 (score_lean; SH = 16, B = 16 with immediate shifts), A3: starvation, counter, key
+            // A1 + A2 (score_lean), A3: starvation, counter, key.  (A second instance with the
+            // shifts as immediates was measured: the score phase gains 0.2 us, the step loses
+            // 2 us -- the step's code is fetched cold every step and grew)
             uint64_t sc, wp, wd, ws;
-            const uint32_t strat = fixed16 ? score_lean<16, 4>(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws)
-                                           : score_lean(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws);
+            const uint32_t strat = score_lean(ctx, pre, api, rp, pp, pend, has, c, sc, wp, wd, ws);
             const uint32_t cnt = sfc_cnt(w);
             const uint32_t starv = sfc_starv(w) | (cnt >= c.T ? 1u : 0u);
             w = sfc_pack(ST_READY, has, starv, strat, cnt < 65535u ? cnt + 1u : 65535u);
@@ -1731,175 +758,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     TRACE(9);
 }
 
-// ---------------------------------------------------------------------------
-// Small pools (capacity <= kSmallCap, BASELINE C1-C3): the whole step in ONE 1024-thread
-// CTA, a plain (non-cooperative) launch -- no grid barriers, no bucket tables, no
-// exchange of keys between CTAs.  The same device functions as the fused kernel:
-//   prologue  API returns, arrivals, A0 for the engine's events (apply_return /
-//             apply_submit / apply_event), then A0's default update and A1-A3 per slot
-//             (score_slot: strategy, score, starvation, key), keys compacted to keys[0]
-//   sort      range_sort_loop over all keys: one counting pass on a piecewise-linear digit
-//             over 16 segments whose ends are the previous step's quantiles (this step's
-//             smallest / largest key at the ends; cold steps: interpolated), rank by
-//             comparison inside counters, a local LSD as the last resort
-//   A5        admit_cta from the sorted keys on chip (demand / state staged by the sort)
-// The quantiles of this step's order are written for the next step.
-constexpr uint32_t kSmallCap = 4096;
-constexpr int kSmallPer = kSmallCap / kFT;  // slots per thread
-template <bool DBG>
-__global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b, const __grid_constant__ Cost c,
-                                                  StepArgs a, const __grid_constant__ InlineStage inl) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
-    Ctl* ctl = b.ctl;
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t vb = c.SB + c.IB;
-    const uint32_t cap = c.cap;
-    if (b.trace && tid == 0) b.trace[0] = clock64();
-    // the previous step's quantiles (warm steps), consumed after scoring
-    unsigned long long fk = 0;
-    if (!a.cold && tid <= (uint32_t)kSeg) fk = __ldcg(&b.spl[(size_t)a.parity * kSplG + tid]);
-    if (a.n_ev | a.n_ret | a.n_sub) {  // prologue, as the fused kernel's (disjoint slots)
-        const ReturnRec* rets = a.inl ? reinterpret_cast<const ReturnRec*>(inl.bytes)
-                                      : static_cast<const ReturnRec*>(b.returns);
-        const SubmitRec* subs = a.inl ? reinterpret_cast<const SubmitRec*>(inl.bytes) + a.n_ret
-                                      : static_cast<const SubmitRec*>(b.arrivals);
-        const DevEvent* evs = a.inl ? reinterpret_cast<const DevEvent*>(reinterpret_cast<const SubmitRec*>(inl.bytes) +
-                                                                        a.n_ret + a.n_sub)
-                                    : static_cast<const DevEvent*>(b.events);
-        for (uint32_t e = tid; e < a.n_ret; e += kFT) apply_return(b.pool, c, rets[e]);
-        for (uint32_t e = tid; e < a.n_sub; e += kFT) apply_submit(b.pool, c, subs[e]);
-        for (uint32_t e = tid; e < a.n_ev; e += kFT) apply_event(b.pool, c, evs[e]);
-        __syncthreads();
-    }
-    // ---- A0 default update, A1-A3 for this thread's slots (tid + u * kFT), keys in registers
-    const Pool& P = b.pool;
-    uint64_t key[kSmallPer];
-    uint32_t nk = 0, pinned = 0;
-    unsigned long long kmin = ~0ull, kmax = 0ull;
-#pragma unroll
-    for (int u = 0; u < kSmallPer; u++) {
-        const uint32_t slot = tid + (uint32_t)u * kFT;
-        key[u] = 0;
-        if (slot >= cap) continue;
-        // the seven SoA words in one round trip
-        uint32_t w = P.sfc[slot], ctx = P.ctx[slot], pre = P.pre[slot], pend = P.pend[slot];
-        const uint32_t api = P.api[slot], resp = P.resp[slot], post = P.post[slot];
-        if (w & SFC_RAN) {  // A0: the previous batch generated one token
-            ctx += 1u;
-            pre = pre ? pre - 1u : 0u;
-            pend = 0u;
-            P.ctx[slot] = ctx;
-            P.pre[slot] = pre;
-            P.pend[slot] = 0u;
-        }
-        const uint32_t st = sfc_state(w);
-        if (st == ST_PP) pinned += (ctx + c.B - 1u) >> c.lgB;
-        if (st != ST_READY) continue;
-        uint64_t k;
-        (void)score_slot<DBG>(P, c, a.id_base_mod, b.dbg, slot, w, ctx, pre, api, resp, post, pend, k);
-        P.sfc[slot] = w;
-#pragma unroll
-        for (int q = 0; q < kSmallPer; q++)  // packed to the front (no dynamic register index)
-            if (q == (int)nk) key[q] = k;
-        nk++;
-        kmin = min(kmin, (unsigned long long)k);
-        kmax = max(kmax, (unsigned long long)k);
-    }
-    // ---- compaction into keys[0] (block scan), the pinned total, this step's key bounds
-    uint32_t n;
-    const uint32_t pos = block_excl_scan_u32<kFT>(nk, sm.l.w32, &n);
-#pragma unroll
-    for (int q = 0; q < kSmallPer; q++)
-        if ((uint32_t)q < nk) b.keys[0][pos + q] = key[q];
-    unsigned long long pin64 = pinned;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        pin64 += __shfl_xor_sync(0xffffffffu, pin64, o);
-        kmin = min(kmin, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmin, o));
-        kmax = max(kmax, (unsigned long long)__shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if (lane == 0) { sm.l.red[0][warp] = kmin; sm.l.red[1][warp] = kmax; sm.l.adm.w64[warp] = pin64; }
-    __syncthreads();  // also orders the key stores before the sort's loads (same CTA)
-    if (warp == 0) {
-        unsigned long long lo = sm.l.red[0][lane], hi = sm.l.red[1][lane], pn = sm.l.adm.w64[lane];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            lo = min(lo, (unsigned long long)__shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, (unsigned long long)__shfl_xor_sync(0xffffffffu, hi, o));
-            pn += __shfl_xor_sync(0xffffffffu, pn, o);
-        }
-        if (lane == 0) { sm.l.red[0][0] = lo; sm.l.red[1][0] = hi; sm.l.red[0][1] = pn; }
-    }
-    __syncthreads();
-    const unsigned long long lo = sm.l.red[0][0], hi = sm.l.red[1][0];
-    const unsigned long long pinned_all = sm.l.red[0][1];
-    if (b.trace && tid == 0) b.trace[1] = clock64();
-    // ---- the digit's grid: ends = this step's bounds, inside = the previous step's quantiles
-    // clamped to them (cold steps: interpolated linearly in key space)
-    if (tid <= (uint32_t)kSeg) {
-        unsigned long long g;
-        if (tid == 0) g = lo;
-        else if (tid == (uint32_t)kSeg) g = hi;
-        else if (!a.cold) g = min(max((unsigned long long)fk, lo), hi);
-        else g = lo + (hi - lo) / kSeg * tid;
-        sm.l.fine[tid] = g;
-        sm.l.fcode[tid] = key_code(g, vb);
-    }
-    __syncthreads();
-    // ---- A4: sort (stages the admission's demand / state words when the keys fit the arrays)
-    const bool stage = n <= kHeadPre;
-    uint32_t* dsm = stage ? sm.l.pos + kHeadPre : nullptr;
-    uint32_t* wsm = stage ? sm.l.pos + 2u * kHeadPre : nullptr;
-    bool written = false, tiny = false;
-    if (n > 1u && n <= kSmallSort && !(a.flags & kStepForceFallback)) {
-        // a few hundred keys: rank of each by comparison against all (unique keys), the
-        // admission's per-key loads staged by sorted position (small_sort)
-        small_sort<true>(sm.l, b.keys[0], n, c, &b.pool, a.id_base_mod);
-        for (uint32_t i = tid; i < n; i += kFT) b.keys[1][i] = sm.l.a[i];
-        tiny = true;
-    } else if (n > 1u && !(a.flags & kStepForceFallback)) {
-        written = range_sort_loop(sm.l, b.keys[0], n, b.keys[1], vb, nullptr, &b.pool, a.id_base_mod, &c, dsm, wsm);
-    }
-    if (!written && !tiny) {  // a counter held too many keys (or the forced fallback): LSD of the whole pool
-        if (n <= 1u || (a.flags & kStepForceFallback))
-            for (uint32_t i = tid; i < n; i += kFT) sm.l.a[i] = __ldcg(&b.keys[0][i]);
-        __syncthreads();
-        if (n > 1u) {
-            unsigned long long o, an;
-            block_or_and(sm.l, sm.l.a, n, o, an);
-            const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, n, o ^ an);
-            if (r != sm.l.a)
-                for (uint32_t i = tid; i < n; i += kFT) sm.l.a[i] = r[i];
-            __syncthreads();
-        }
-        for (uint32_t i = tid; i < n; i += kFT) b.keys[1][i] = sm.l.a[i];
-    }
-    const uint64_t* srt = written ? reinterpret_cast<const uint64_t*>(sm.l.b) : sm.l.a;
-    // the next step's grid: the quantiles of this order
-    if (n && tid <= (uint32_t)kSeg) b.spl[(size_t)(a.parity ^ 1u) * kSplG + tid] = srt[min((uint32_t)((uint64_t)n * tid / kSeg), n - 1u)];
-    if (b.trace && tid == 0) b.trace[2] = clock64();
-    if (tid == 0) {
-        ctl->n_passes = 1;
-        ctl->final_buf = 1;
-        if (!written && !tiny && n > 1u) atomicAdd(&ctl->fallbacks, 1u);
-        ctl->n_ranked = n;
-    }
-    __syncthreads();
-    // ---- A5: admission from the sorted keys on chip; the preempted check's hash table in the
-    // other key buffer
-    uint32_t hs = 1024;
-    while (hs < 2u * a.max_batch) hs <<= 1;
-    const bool use_h = hs <= kHeadTC;
-    uint32_t* htab = written ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
-    const bool dw = written && stage;
-    const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);  // small_sort's staged arrays
-    static_assert(kHeadTC <= kHeadD, "small_sort's staged arrays lie past the hash table");
-    admit_cta(b, c, a, srt, n, pinned_all, sm.l.adm, use_h ? htab : nullptr, use_h ? hs : 0u, nullptr,
-              dw ? dsm : (tiny ? b32 + kHeadD : nullptr), dw ? wsm : (tiny ? b32 + kHeadW : nullptr));
-    if (b.trace && tid == 0) b.trace[3] = clock64();
-}
-
 }  // namespace
 
 static_assert(kFusedSmemBytes <= 232448, "fused kernel shared memory exceeds 227 KB");
@@ -1916,39 +774,6 @@ int fused_blocks_per_sm() {
 }
 
 uint32_t fused_max_buckets() { return kMaxBuckets; }
-uint32_t small_max_cap() { return kSmallCap; }
-
-cudaError_t launch_small(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
-        cudaFuncSetAttribute(k_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
-        attr = true;
-    }
-    static const InlineStage kNone{};
-    if (b.dbg)
-        k_small<true><<<1, kFT, sizeof(FusedSmem), s>>>(b, c, a, inl ? *inl : kNone);
-    else
-        k_small<false><<<1, kFT, sizeof(FusedSmem), s>>>(b, c, a, inl ? *inl : kNone);
-    return cudaGetLastError();
-}
-
-// The initial bucket table (before any step has measured the key distribution): every
-// octave (ns, e) of v's bit length gets 2^min(7, e-1) buckets -- the fixed float-like
-// buckets of 7 mantissa bits.  bt_update replaces it after the first step.
-void fused_default_table(uint32_t vb, uint32_t* out) {
-    uint32_t base = 0;
-    for (uint32_t o = 0; o < kTabNB; o++) {
-        const uint32_t e = o % 65u;
-        if (e > vb) { out[o] = base; continue; }
-        const uint32_t m = e >= 1u ? std::min(7u, e - 1u) : 0u;
-        out[o] = base | ((e >= 1u ? e - 1u - m : 0u) << 16) | (m << 24);
-        base += 1u << m;
-    }
-    out[kTabNB] = base;
-    for (uint32_t o = kTabNB + 1; o < (uint32_t)kTabW; o++) out[o] = 0;
-}
-
 cudaError_t launch_fused(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t grid,
                          cudaStream_t s) {
     static const InlineStage kNone{};

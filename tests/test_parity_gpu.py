@@ -29,7 +29,7 @@ def test_snapshot_parity(cname, seed, id_base, path):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("path", ["fused", "multi", "head"])
+@pytest.mark.parametrize("path", ["fused", "multi", "head", "fallback"])
 def test_c5_full_size_parity(path):
     # BASELINE.json's 1M-request pool in the launch configuration bench.py times
     snapshot_step_parity("C5", seed=0, id_base=(1 << 20) * 7 + 99, steps=2, path=path)
