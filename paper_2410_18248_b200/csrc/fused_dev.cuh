@@ -88,13 +88,6 @@ struct PhaseL {                  // L
             uint32_t nbig;
         };
     };
-    // group refinement: lists of groups still to split (ping-pong), and per group of the
-    // current batch: key offset (prefix of sizes), digit shift / bits, counter base, OR / AND
-    uint16_t gl_lo[2][kMaxBig], gl_n[2][kMaxBig];
-    uint32_t ngl[2];
-    uint16_t gcum[kMaxBig], gbase[kMaxBig];
-    uint8_t gsh[kMaxBig], gdb[kMaxBig];
-    unsigned long long gor[kMaxBig / 4], gand[kMaxBig / 4];
     unsigned long long red[2][kFW];
     AdmitSmem adm;                                // admission scratch (CTA 0, keys stay in a[])
     uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size and position in the order
@@ -431,6 +424,12 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
 #undef LTRACE
     return true;
 }
+
+// (Measured and not kept: range_sort_lean -- one L2 load, the digit recomputed
+// per pass -- and range_sort_cp -- cp.async staging, single-key loops: less code, but the
+// rank-by-comparison of clustered counters needs the unrolled loop; 53.2 / 56.1 vs 52.4 us.)
+#define LAMPS_RANGE_SORT range_sort_loop
+constexpr bool kSortedInA = false;  // where a successful range sort leaves the sorted keys (sm.b)
 
 // A small range (rn <= kSmallSort keys): ranked by comparison against all its keys (the
 // keys are unique, so the rank is the count of smaller keys; the few hundred keys are read

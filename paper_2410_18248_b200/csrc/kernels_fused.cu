@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             TRACE(13);
             // CTA 0 (single shard): head + admission loads on chip
             const bool stage = bid == 0 && rn <= kHeadPre && !(a.flags & kStepMerge);
-            written = range_sort_loop(sm.l, src, rn, b.keys[1] + rpre, vb, tr ? tr + 32 : nullptr, &b.pool,
+            written = LAMPS_RANGE_SORT(sm.l, src, rn, b.keys[1] + rpre, vb, tr ? tr + 32 : nullptr, &b.pool,
                                       a.id_base_mod, &c, stage ? sm.l.pos + kHeadPre : nullptr,
                                       stage ? sm.l.pos + 2u * kHeadPre : nullptr);
             head_loop = stage && written;
@@ -639,7 +639,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // CTA 0 holds [0, need) in shared memory unless it waited (or its range sort wrote them out)
     const bool hl = head_loop && !wait;  // head keys in sm.l.b, demands / states in sm.l.pos
     const uint64_t* head = wait ? b.keys[final_buf]
-                                : (hl ? reinterpret_cast<const uint64_t*>(sm.l.b) : (written ? b.keys[final_buf] : sm.l.a));
+                                : (hl ? (kSortedInA ? sm.l.a : reinterpret_cast<const uint64_t*>(sm.l.b))
+                                      : (written ? b.keys[final_buf] : sm.l.a));
     const bool dw = head_dw && !wait;
     if (a.flags & kStepMerge) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     while (hs < 2u * a.max_batch) hs <<= 1;
     const bool use_h = !wait && hs <= kHeadTC;
     const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);
-    uint32_t* htab = hl ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
+    uint32_t* htab = hl && !kSortedInA ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
     admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? htab : nullptr, use_h ? hs : 0u,
               b.trace ? b.trace + 40 : nullptr,
               hl ? sm.l.pos + kHeadPre : (dw ? b32 + kHeadD : nullptr),

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
         for (uint32_t i = tid; i < n; i += kFT) b.keys[1][i] = sm.l.a[i];
         tiny = true;
     } else if (n > 1u && !(a.flags & kStepForceFallback)) {
-        written = range_sort_loop(sm.l, b.keys[0], n, b.keys[1], vb, nullptr, &b.pool, a.id_base_mod, &c, dsm, wsm);
+        written = LAMPS_RANGE_SORT(sm.l, b.keys[0], n, b.keys[1], vb, nullptr, &b.pool, a.id_base_mod, &c, dsm, wsm);
     }
     if (!written && !tiny) {  // a counter held too many keys (or the forced fallback): LSD of the whole pool
         if (n <= 1u || (a.flags & kStepForceFallback))
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
         }
         for (uint32_t i = tid; i < n; i += kFT) b.keys[1][i] = sm.l.a[i];
     }
-    const uint64_t* srt = written ? reinterpret_cast<const uint64_t*>(sm.l.b) : sm.l.a;
+    const uint64_t* srt = written && !kSortedInA ? reinterpret_cast<const uint64_t*>(sm.l.b) : sm.l.a;
     // the next step's grid: the quantiles of this order
     if (n && tid <= (uint32_t)kSeg) b.spl[(size_t)(a.parity ^ 1u) * kSplG + tid] = srt[min((uint32_t)((uint64_t)n * tid / kSeg), n - 1u)];
     if (b.trace && tid == 0) b.trace[2] = clock64();
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
     uint32_t hs = 1024;
     while (hs < 2u * a.max_batch) hs <<= 1;
     const bool use_h = hs <= kHeadTC;
-    uint32_t* htab = written ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
+    uint32_t* htab = written && !kSortedInA ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
     const bool dw = written && stage;
     const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);  // small_sort's staged arrays
     static_assert(kHeadTC <= kHeadD, "small_sort's staged arrays lie past the hash table");
