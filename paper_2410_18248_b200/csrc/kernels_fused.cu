@@ -376,7 +376,19 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     uint64_t* const kb2 = reinterpret_cast<uint64_t*>(kr);                 // [kKcap] keys by range
     uint8_t* const rr = reinterpret_cast<uint8_t*>(kr) + 8u * kKcap;       // [kKcap] their range
     uint8_t* const rv = rr + kKcap;                                        // [kKcap] range by position
-    {
+    // warm head-only steps (F3): only the head matters -- range 0 = keys below the first
+    // splitter, every other key "range 1" (kept on chip for the fallback, never stored)
+    const bool hr = head_mode && !a.cold && G > 1u;
+    if (hr) {
+        const unsigned long long s1 = sm.s.spl[spl_pos(1)];
+        for (uint32_t i = tid; i < npos; i += kFT) {
+            const uint32_t q = i >> 1;
+            if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
+            const uint32_t rg = sm.s.kbuf[i] >= s1 ? 1u : 0u;
+            rv[i] = (uint8_t)rg;
+            atomicAdd(&sm.s.lcnt[rg], 1u);
+        }
+    } else {
         const unsigned long long* spl = sm.s.spl;
         for (uint32_t i0 = tid; i0 < npos; i0 += 2u * kFT) {  // two searches advanced together
             uint64_t k[2];
@@ -418,13 +430,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     for (uint32_t i = tid; i < npos; i += kFT) {
         const uint32_t q = i >> 1;
         if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
+        if (hr && rv[i]) continue;  // head-only: only the head is placed and stored
         const uint32_t r = rv[i], lp = atomicAdd(&sm.s.lcnt[r], 1u);  // order within a run is free
         kb2[lp] = sm.s.kbuf[i];
         rr[lp] = (uint8_t)r;
     }
     __syncthreads();
     TRACE(12);
-    for (uint32_t i = tid; i < nk_cta; i += kFT) {
+    for (uint32_t i = tid; i < (hr ? sm.s.lcnt[0] : nk_cta); i += kFT) {  // (head-only: run 0 = [0, lcnt[0]))
         const uint32_t r = rr[i], pos = sm.s.gbase[r] + (i - sm.s.lst[r]);
         if (pos < (uint32_t)kKcap) b.keys[0][(size_t)r * kKcap + pos] = kb2[i];  // else: overflow -> fallback
     }
@@ -443,7 +456,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             nq += r < G ? __ldcg(&b.nk_part[r]) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < kMaxCtas / 32; j++) { tot += v[j]; big |= v[j] > (uint32_t)kKcap ? 1u : 0u; }
+        for (int j = 0; j < kMaxCtas / 32; j++) {  // (head-only: "range 1" is every other key, not sorted)
+            tot += v[j];
+            big |= (v[j] > (uint32_t)kKcap && !(hr && lane * (kMaxCtas / 32) + (uint32_t)j > 0u)) ? 1u : 0u;
+        }
         uint32_t x = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -472,6 +488,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // head-only mode (F3): CTA 0 ranks the head; the others stop here, unless the head range
     // does not hold the keys the admission needs (then every range is sorted)
     const bool head_only = head_mode && !fallback && r_end0 >= min(n, a.max_batch + 32u);
+    if (hr && !head_only) fallback = true;  // head-only R placed only the head: the global LSD ranks the rest
     // positions of the next step's splitters in this step's order: the head (range 0) ends
     // at max_batch + kHeadMargin keys, the other ranges share the rest evenly
     const uint32_t q1 = G > 1u ? min(n, a.max_batch + kHeadMargin) : n;
@@ -484,8 +501,12 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         return n ? (uint32_t)min(p, (uint64_t)(n - 1u)) : 0u;
     };
     unsigned long long* spl_next = b.spl + (size_t)(a.parity ^ 1u) * kSplG;
-    if (head_only && bid == G - 1u)  // the grid is kept: the other ranges were not sorted
-        for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = __ldcg(&b.spl[(size_t)a.parity * kSplG + f]);
+    // head-only: the grid is kept (the other ranges were not sorted), except range 0's entries,
+    // which CTA 0 refreshes from its sorted head when it holds more than q1 keys
+    const bool hrefresh = head_only && r_end0 > q1;
+    if (head_only && bid == G - 1u)
+        for (uint32_t f = tid + (hrefresh ? kSeg + 1u : 0u); f <= kSeg * G; f += kFT)
+            spl_next[f] = __ldcg(&b.spl[(size_t)a.parity * kSplG + f]);
     // this range's grid entries fine[16 bid .. 16 bid + 16]: key codes and per-segment shifts of
     // the range sort's piecewise-linear digit (segment j: keys in [fine[j], fine[j + 1]))
     if (warp == 1 && lane <= (uint32_t)kSeg) {
@@ -562,6 +583,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
                 const uint32_t q = qf(f);
                 if (q >= rpre && q < rpre + rn) spl_next[f] = __ldcg(&b.keys[1][q]);
             }
+        if (hrefresh && bid == 0 && tid <= (uint32_t)kSeg) spl_next[tid] = __ldcg(&b.keys[1][qf(tid)]);
         final_buf = 1;
         passes = 1;
     } else if (fallback) {
@@ -574,8 +596,20 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
                 off = tot;
             }
             // kb2 (this CTA's keys, compacted by R) is intact: since the barrier only PhaseL's
-            // small arrays past sm.l.b (w32, rsz, rpre) were written
-            for (uint32_t i = tid; i < nk_cta; i += kFT) b.keys[0][off + i] = kb2[i];
+            // small arrays past sm.l.b (w32, rsz, rpre) were written.  Head-only R placed only
+            // the head in kb2: then the keys come from kbuf / vmask (intact likewise; any order)
+            if (hr) {
+                uint32_t* ctr = &sm.l.w32[kFW];
+                if (tid == 0) *ctr = 0u;
+                __syncthreads();
+                for (uint32_t i = tid; i < npos; i += kFT) {
+                    const uint32_t q = i >> 1;
+                    if ((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)
+                        b.keys[0][off + atomicAdd(ctr, 1u)] = sm.s.kbuf[i];
+                }
+            } else {
+                for (uint32_t i = tid; i < nk_cta; i += kFT) b.keys[0][off + i] = kb2[i];
+            }
             grid_barrier(b.flags, G, ++bar);
         }
         {   // OR / AND of the keys (the LSD skips digit positions that never vary)

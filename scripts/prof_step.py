@@ -26,7 +26,8 @@ if os.environ.get("TIMING"):
 if os.environ.get("TRACE"):
     import numpy as np
     from paper_2410_18248_b200 import LAMPS_TRACE
-    st = Scheduler(cfg, flags=LAMPS_TRACE)
+    from paper_2410_18248_b200 import LAMPS_HEAD_ONLY
+    st = Scheduler(cfg, flags=LAMPS_TRACE | (LAMPS_HEAD_ONLY if os.environ.get("HEAD") else 0))
     st.import_pool(snap, snap["id_base"], snap["next_id"])
     acc = []
     for it in range(10):
