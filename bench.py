@@ -31,6 +31,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# A4 (the sort) in the fused kernel: the keys to their ranges, the barrier, the range sorts
+SORT_SEGS = ("range_assign", "run_offsets", "run_place", "run_store", "barrier", "l_prep", "range_sort", "store_grid")
 METRIC = "scheduling decisions/s and µs per step at 1M-request pool; % HBM peak"
 UNIT = "decisions/s"
 
@@ -411,8 +413,10 @@ def run_ours(args, rank, world, local):
       trace_us = None
       if fused and traces:
           t = np.stack(traces)
-          segs = [("score", 0, 1), ("publish", 1, 2), ("barrier1", 2, 3), ("count_exchange", 3, 4),
-                  ("barrier2", 4, 5), ("bucket_scatter", 5, 6), ("barrier3", 6, 7), ("range_sort", 7, 8)]
+          # warm-step phase boundaries of k_fused (kernels_fused.cu TRACE points)
+          segs = [("score", 0, 1), ("range_assign", 1, 4), ("run_offsets", 4, 5), ("run_place", 5, 12),
+                  ("run_store", 12, 6), ("barrier", 6, 7), ("l_prep", 7, 13), ("range_sort", 13, 14),
+                  ("store_grid", 14, 8)]
           mhz = float(clk.summary().get("sm_mhz") or 1965.0)  # sampled during the timed steps
           trace_us = {nm: round(float(np.median((t[:, :, b1] - t[:, :, a1]).max(axis=1))) / mhz, 2)
                       for nm, a1, b1 in segs}
@@ -551,11 +555,10 @@ def run_ours(args, rank, world, local):
                          "peak_source": peak_src},
             "kernels": kernels_tbl,
             # A4 alone (SURVEY 8(d) "keys/s per sort"): eligible keys over the fused kernel's sort
-            # phases (scatter into bucket order + its barrier + the range sorts, slowest CTA)
-            "sort": ({"keys_per_s": n_elig / (1e-6 * (trace_us["bucket_scatter"] + trace_us["barrier3"]
-                                                      + trace_us["range_sort"])),
-                      "us": round(trace_us["bucket_scatter"] + trace_us["barrier3"] + trace_us["range_sort"], 2)}
-                     if trace_us else None),
+            # phases (keys to their ranges, the barrier, the range sorts; slowest CTA of each)
+            "sort": ({"keys_per_s": n_elig / (1e-6 * sum(trace_us[k] for k in SORT_SEGS)),
+                      "us": round(sum(trace_us[k] for k in SORT_SEGS), 2),
+                      "phases": list(SORT_SEGS)} if trace_us else None),
             "pool_slots_per_s": world * cap / (ms_max / 1e3),
             # this rank's per-step distribution (median and p99 of the step time)
             "step_us": {"min": round(per_step_ms[0] * 1e3, 2),

@@ -183,7 +183,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // table, splitters, costs, peer pointers
     const uint32_t npos = s_hi - s_lo;  // kbuf positions (slots of this CTA)
-    const uint32_t NB = sm.btab[kTabNB];  // buckets of this step's table
     unsigned long long pin64 = pinned;
     uint32_t nk_cta = nmine;
 #pragma unroll
@@ -206,6 +205,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         b.nk_part[bid] = nk_cta;
     }
     TRACE(1);
+    // (after the barrier above: the table was copied by other threads' cp.async)
+    const uint32_t NB = sm.btab[kTabNB];  // buckets of this step's table
     uint32_t bar = a.step * kBarPerStep;
     const bool head_mode = (a.flags & kStepHeadOnly) != 0;
     if (a.cold) {

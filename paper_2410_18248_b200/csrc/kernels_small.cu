@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
             hi = max(hi, (unsigned long long)__shfl_xor_sync(0xffffffffu, hi, o));
             pn += __shfl_xor_sync(0xffffffffu, pn, o);
         }
+        __syncwarp();  // every lane's reads above before lane 0 overwrites entries 0 / 1
         if (lane == 0) { sm.l.red[0][0] = lo; sm.l.red[1][0] = hi; sm.l.red[0][1] = pn; }
     }
     __syncthreads();

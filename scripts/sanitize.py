@@ -77,10 +77,41 @@ def c5(flags=0):
     s.close()
 
 
+def large_merge(world=4, K=4096):
+    """Loopback shards whose world * K records exceed one CTA's shared memory: the grid-wide
+    merge by rank (k_merge_count / k_merge_place / k_merge_cut)."""
+    cfg = gen.lib_config("C4", max_batch=K)
+    cfg["capacity"] = 32768
+    stream = torch.cuda.current_stream()
+    S = [Scheduler(cfg, world=world, rank=r, transport=L.LAMPS_XPORT_LOOPBACK, stream=stream) for r in range(world)]
+    for r, sh in enumerate(S):
+        snap = gen.snapshot("C4", seed=r, n=25000, capacity=32768, id_base=1000)
+        sh.import_pool(snap, snap["id_base"], snap["next_id"])
+    for _ in range(max(2, STEPS // 3)):
+        outs = Scheduler.group_step(S, None, [250_000] * world)
+    print(f"large_merge W={world} K={K}: {sum(o['n_admitted'] for o in outs)} admitted", flush=True)
+    for sh in S:
+        sh.close()
+
+
+def c4_head_only():
+    """The fused kernel's head-only ranking (warm steps place only the head) on C4."""
+    cfg = gen.lib_config("C4")
+    snap = gen.snapshot("C4", seed=0, id_base=77)
+    s = Scheduler(cfg, flags=L.LAMPS_HEAD_ONLY)
+    s.import_pool(snap, snap["id_base"], snap["next_id"])
+    for _ in range(STEPS):
+        g = s.step(kv_total=gen.CONFIGS["C4"]["kv_total"])
+    print(f"c4_head_only: {g['n_eligible']} eligible, {g['n_admitted']} admitted", flush=True)
+    s.close()
+
+
 MODES = {
-    "fused": lambda: closed_loop("fused"),
+    "fused": lambda: closed_loop("fused"),  # C3: the one-CTA small-pool kernel
+    "grid": lambda: closed_loop("grid", flags=L.LAMPS_GRID_STEP),  # C3 on the grid-wide fused kernel
+    "small_fallback": lambda: closed_loop("small_fallback", flags=L.LAMPS_FORCE_FALLBACK),
+    "grid_fallback": lambda: closed_loop("grid_fallback", flags=L.LAMPS_GRID_STEP | L.LAMPS_FORCE_FALLBACK),
     "multi": lambda: closed_loop("multi", flags=L.LAMPS_MULTI_KERNEL),
-    "fallback": lambda: closed_loop("fallback", flags=L.LAMPS_FORCE_FALLBACK),
     "head_only": lambda: closed_loop("head_only", flags=L.LAMPS_HEAD_ONLY),
     "interval10": lambda: closed_loop("interval10", score_interval=10),
     "sjf": lambda: closed_loop("sjf", policy=L.LAMPS_POLICY_SJF),
@@ -90,6 +121,8 @@ MODES = {
     "predict": predict,
     "c5": c5,
     "c5_head_only": lambda: c5(L.LAMPS_HEAD_ONLY),
+    "c4_head_only": c4_head_only,
+    "large_merge": large_merge,
 }
 
 if __name__ == "__main__":
