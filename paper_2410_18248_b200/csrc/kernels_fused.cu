@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     }
 
     TRACE(0);
+    if (b.trace && tid == 0) {  // diagnostics: the kernel's start on the global clock (slot 29)
+        unsigned long long g0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+        b.trace[(size_t)bid * kTraceSlots + 29] = g0;
+    }
     SmemTail& tail = *reinterpret_cast<SmemTail*>(smem_raw + sizeof(FusedSmem));
     if (P2P && tid < a.world) {  // the peers' exchange buffers
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tail.xp[tid]);
@@ -656,6 +661,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // the keys [0, rsz[0]) are sorted by CTA 0 itself.
     const uint32_t need = min(n, a.max_batch);  // the admission (or the merge records) reads keys [0, need)
     const bool wait = fallback || r_end0 < need;
+    if (b.trace && bid == 0 && tid == 0) {  // diagnostics: the head's size, whether CTA 0 waits
+        b.trace[56] = r_end0;
+        b.trace[57] = wait ? 1u : 0u;
+    }
     if (wait) grid_barrier(b.flags, G, ++bar);
     if (fallback && bid == 0 && n)
         for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = __ldcg(&b.keys[final_buf][qf(f)]);
@@ -686,30 +695,48 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         // peer-memory transport: record i of this rank goes to every peer's receive area
         // [par][rank] by NVLink stores (the one-shot all-gather), then flags, then the merge
         const size_t slot0 = ((size_t)par * W + a.rank) * (K + 1);
-        for (uint32_t i = tid; i <= nv; i += kFT) {
-            MergeRec r;
-            if (i == 0) {
-                MergeHdr* h = reinterpret_cast<MergeHdr*>(&r);
-                h->pinned = pinned_all;
-                h->kv_total = a.kv_total;
-                h->n_valid = nv;
-                h->n_local = n;
-                h->pad = 0;
-            } else {
+        if (b.trace && tid == 0) b.trace[58] = clock64();
+        for (uint32_t i = tid; i < ((nv + 32u) & ~31u); i += kFT) {  // whole warps (the shuffles below)
+            // the 32-B record as two 16-B vectors built in registers: a warp stores 1 KB of
+            // whole sectors per destination (a struct copied field by field through local
+            // memory made 4 partial-sector stores per record: 17 us for 8 x 1025 records)
+            ulonglong2 v0 = make_ulonglong2(0ull, 0ull), v1 = v0;
+            if (i > nv) {
+            } else if (i == 0) {  // MergeHdr {pinned, kv_total, n_valid | n_local << 32, pad}
+                v0 = make_ulonglong2(pinned_all, a.kv_total);
+                v1 = make_ulonglong2((unsigned long long)nv | ((unsigned long long)n << 32), 0ull);
+            } else {       // MergeRec {sk, gid, demand | slot << 32, pad}
                 const uint64_t k = head[i - 1];
                 const uint64_t lid = a.id_base + (k & idmask);
                 const uint32_t slot = (uint32_t)(lid & c.cap_mask);
-                r.sk = k >> c.IB;
-                r.gid = lid * a.world + a.rank;
-                r.demand = dw ? reinterpret_cast<const uint32_t*>(sm.l.b)[kHeadD + i - 1]
-                              : (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
-                r.slot = slot;
-                r.pad = 0;
+                const uint32_t dem = dw ? reinterpret_cast<const uint32_t*>(sm.l.b)[kHeadD + i - 1]
+                                        : (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
+                v0 = make_ulonglong2(k >> c.IB, lid * a.world + a.rank);
+                v1 = make_ulonglong2((unsigned long long)dem | ((unsigned long long)slot << 32), 0ull);
             }
             if (p2p) {
-                for (uint32_t p = 0; p < W; p++) tail.xp[p][slot0 + i] = r;
-            } else {
-                b.xsend[i] = r;
+                // the warp's 32 records are 64 consecutive 16-B chunks of each destination:
+                // two stores of 32 consecutive chunks (whole sectors) per destination, lane l
+                // of store h holding chunk 32 h + l = half (l & 1) of record 16 h + l / 2
+                const uint32_t i0 = i - lane;
+                ulonglong2 w[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const uint32_t sl = 16u * h + (lane >> 1);
+                    const unsigned long long a0 = __shfl_sync(0xffffffffu, v0.x, sl), a1 = __shfl_sync(0xffffffffu, v0.y, sl);
+                    const unsigned long long b0 = __shfl_sync(0xffffffffu, v1.x, sl), b1 = __shfl_sync(0xffffffffu, v1.y, sl);
+                    w[h] = (lane & 1u) ? make_ulonglong2(b0, b1) : make_ulonglong2(a0, a1);
+                }
+                for (uint32_t p = 0; p < W; p++) {
+                    ulonglong2* d = reinterpret_cast<ulonglong2*>(tail.xp[p] + slot0 + i0);
+#pragma unroll
+                    for (int h = 0; h < 2; h++)
+                        if (i0 + 16u * h + (lane >> 1) <= nv) d[32u * h + lane] = w[h];  // records <= nv only
+                }
+            } else if (i <= nv) {
+                ulonglong2* d = reinterpret_cast<ulonglong2*>(b.xsend + i);
+                d[0] = v0;
+                d[1] = v1;
             }
         }
         if (!p2p) {

@@ -169,7 +169,7 @@ bool merge_is_large(uint32_t world, uint32_t K);  // world * K records beyond on
 // merge scratch: sk, gid (8 B) and demand (4 B) per record of the W runs, 3 index arrays of K
 __host__ __device__ inline size_t merge_smem_bytes(uint32_t world, uint32_t K) {
     const size_t R = (size_t)world * K;
-    return R * 8 * 2 + R * 4 + (size_t)K * 4 * 3;
+    return R * 8 * 2 + R * 4 + ((size_t)(world + 1) / 2 + (world + 3) / 4 + 1) * K * 4;  // records; the tree's lists
 }
 cudaError_t launch_admit(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 

@@ -126,11 +126,35 @@ __device__ __forceinline__ void merge_cut_admit(const Bufs& b, const Cost& c, co
     }
 }
 
+// out[0..lim) = first lim elements of merge(A, B) where A(i) / B(j) give the record index of
+// element i / j (na / nb elements), by the T threads lt = 0..T-1 of a group (merge path:
+// each thread finds its co-rank by binary search, then merges its share sequentially).
+template <class FA, class FB>
+__device__ __forceinline__ void merge_path_grp(FA A, uint32_t na, FB B, uint32_t nb, uint32_t* out, uint32_t lim,
+                                               uint32_t lt, uint32_t T, const unsigned long long* sk,
+                                               const unsigned long long* gid) {
+    const uint32_t tot = min(na + nb, lim);
+    const uint32_t per = (tot + T - 1) / T;
+    const uint32_t k0 = min(tot, lt * per), k1 = min(tot, k0 + per);
+    if (k0 >= k1) return;
+    uint32_t lo = k0 > nb ? k0 - nb : 0u, hi = min(k0, na);
+    while (lo < hi) {
+        const uint32_t i = (lo + hi) >> 1;
+        if (rec_less(sk, gid, A(i), B(k0 - i - 1))) lo = i + 1; else hi = i;
+    }
+    uint32_t i = lo, j = k0 - lo;
+    for (uint32_t k = k0; k < k1; k++) {
+        const bool takeA = j >= nb || (i < na && rec_less(sk, gid, A(i), B(j)));
+        out[k] = takeA ? A(i++) : B(j++);
+    }
+}
+
 // Merge of the W runs in xrecv ([W][K+1]: header + records), global cut, and admission
 // of this rank's share, by one 1024-thread CTA.  smem_raw: merge_smem_bytes(W, K) bytes of
 // scratch; adm / nv[32] / hsum[2] small shared structures.  Used by k_merge (after the
 // NCCL all-gather or the loopback copies) and by the fused kernel's CTA 0 (after the
-// in-kernel peer-memory exchange).
+// in-kernel peer-memory exchange).  The runs are merged as a tree -- pairs in parallel, each
+// by its share of the CTA's threads, every output truncated to K -- ceil(log2 W) rounds.
 __device__ __forceinline__ void merge_admit_cta(const Bufs& b, const Cost& c, const StepArgs& a,
                                                 const MergeRec* __restrict__ xrecv, unsigned char* smem_raw,
                                                 AdmitSmem& adm, uint32_t* nv, unsigned long long* hsum,
@@ -141,37 +165,84 @@ __device__ __forceinline__ void merge_admit_cta(const Bufs& b, const Cost& c, co
     unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem_raw);
     unsigned long long* gid = sk + R;
     uint32_t* dem = reinterpret_cast<uint32_t*>(gid + R);
-    uint32_t* acc = dem + R;
-    uint32_t* tmp = acc + K;
-    uint32_t* run = tmp + K;  // K indices of the run being merged
+    uint32_t* X = dem + R;                   // [ceil(W/2)][K] lists of odd rounds
+    uint32_t* Y = X + ((W + 1) / 2) * K;     // [ceil(W/4) + 1][K] lists of even rounds
+    uint32_t* nl = reinterpret_cast<uint32_t*>(&adm.w32[0]);  // list lengths (adm is free until the cut)
     const uint32_t tid = threadIdx.x;
     merge_headers(xrecv, W, K, nv, hsum);
-    for (uint32_t f = tid; f < R; f += kMT) {
-        const uint32_t r = f / K, i = f % K;
-        if (i < nv[r]) {
-            const MergeRec rec = xrecv[(size_t)r * (K + 1) + 1 + i];
-            sk[f] = rec.sk;
-            gid[f] = rec.gid;
-            dem[f] = rec.demand;
+    {   // the records into shared memory: consecutive threads load consecutive 16-B halves of a
+        // run's records (whole sectors), four in flight per thread; half 0 = (sk, gid), half 1 =
+        // (demand, slot)
+        const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(xrecv);
+        const uint32_t Q = 2u * R;
+        for (uint32_t q0 = tid; q0 < Q; q0 += 4u * kMT) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t q = q0 + (uint32_t)u * kMT, r = q / (2u * K), cI = q % (2u * K), i = cI >> 1;
+                if (q < Q && i < nv[r]) v[u] = __ldcg(x2 + ((size_t)r * (K + 1) + 1 + i) * 2 + (cI & 1u));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t q = q0 + (uint32_t)u * kMT, r = q / (2u * K), cI = q % (2u * K), i = cI >> 1;
+                if (q < Q && i < nv[r]) {
+                    const uint32_t f = r * K + i;
+                    if (cI & 1u) {
+                        dem[f] = (uint32_t)v[u].x;
+                    } else {
+                        sk[f] = v[u].x;
+                        gid[f] = v[u].y;
+                    }
+                }
+            }
         }
     }
-    for (uint32_t i = tid; i < K; i += kMT) acc[i] = i;  // run 0
+    if (tid < W) nl[tid] = nv[tid];
     __syncthreads();
     if (tr && tid == 0) tr[0] = clock64();
-    uint32_t na = nv[0];
-    for (uint32_t r = 1; r < W; r++) {
-        for (uint32_t i = tid; i < K; i += kMT) run[i] = r * K + i;
+    // round 1 merges the runs (implicit lists r K + i) into X, later rounds X <-> Y
+    uint32_t nlist = W;
+    uint32_t* src = nullptr;  // nullptr: the runs themselves
+    uint32_t* dst = X;
+    while (nlist > 1) {
+        const uint32_t M = nlist / 2, T = kMT / M;  // pairs this round (an odd last list is copied)
+        const uint32_t g = tid / T, lt = tid % T;
+        const uint32_t la = g < M ? nl[2 * g] : 0u, lb = g < M ? nl[2 * g + 1] : 0u;
+        __syncthreads();  // every thread read nl before it is rewritten
+        if (g < M) {
+            uint32_t* o = dst + (size_t)g * K;
+            if (src == nullptr) {
+                const uint32_t ba = 2u * g * K, bb = (2u * g + 1u) * K;
+                merge_path_grp([&](uint32_t i) { return ba + i; }, la, [&](uint32_t j) { return bb + j; }, lb, o, K,
+                               lt, T, sk, gid);
+            } else {
+                const uint32_t* pa = src + (size_t)2 * g * K;
+                const uint32_t* pb = src + (size_t)(2 * g + 1) * K;
+                merge_path_grp([&](uint32_t i) { return pa[i]; }, la, [&](uint32_t j) { return pb[j]; }, lb, o, K,
+                               lt, T, sk, gid);
+            }
+            if (lt == 0) nl[g] = min(la + lb, K);
+        }
+        if (nlist & 1u) {  // the unpaired last list moves to position M
+            const uint32_t last = nlist - 1u, ln = nl[last];
+            uint32_t* o = dst + (size_t)M * K;
+            for (uint32_t i = tid; i < ln; i += kMT) o[i] = src ? src[(size_t)last * K + i] : last * K + i;
+            __syncthreads();
+            if (tid == 0) nl[M] = ln;
+        }
         __syncthreads();
-        merge_path(acc, na, run, nv[r], tmp, K, sk, gid);
-        na = min(na + nv[r], K);
-        for (uint32_t i = tid; i < na; i += kMT) acc[i] = tmp[i];
-        __syncthreads();
+        nlist = M + (nlist & 1u);
+        src = dst;
+        dst = dst == X ? Y : X;
     }
+    const uint32_t* acc = src;
+    const uint32_t na = src ? nl[0] : nv[0];
+    __syncthreads();
     if (tr && tid == 0) tr[1] = clock64();
-    merge_cut_admit(b, c, a, xrecv, na, [&](uint32_t k, unsigned long long& d, uint32_t& src) {
-        const uint32_t f = acc[k];
+    merge_cut_admit(b, c, a, xrecv, na, [&](uint32_t k, unsigned long long& d, uint32_t& srk) {
+        const uint32_t f = acc ? acc[k] : k;
         d = dem[f];
-        src = f / K;
+        srk = f / K;
     }, adm, nv, hsum, htab, hsize, dsm, wsm, tr);
 }
 
