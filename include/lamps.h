@@ -87,6 +87,9 @@ extern "C" {
                                    one shard) take the grid-wide fused step kernel instead (tests,
                                    measurements) */
 
+#define LAMPS_BIG_STEP 512u     /* take the large-pool path (k_big_score + k_big_sort, several ranges per
+                                   CTA; the default above #SM x 10240 slots) at any capacity (tests) */
+
 #define LAMPS_INGEST_LIMIT (1u << 24) /* max tokens of one request (R21) */
 
 typedef struct lamps_s lamps_t;

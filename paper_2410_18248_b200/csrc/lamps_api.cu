@@ -93,8 +93,10 @@ struct lamps_s {
     Cost cost{};
     Bufs b{};
     uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
+    uint32_t big_ranges = 0, big_grid = 0;
     bool fused = false;
     bool small = false;   // fused family: the one-CTA small-pool step kernel (k_small)
+    bool big = false;     // pools above the fused kernel's capacity: k_big_score + k_big_sort
     bool cold = true;     // fused: no splitters yet (StepArgs.cold); a fused step writes the next's
     uint32_t world = 1, rank = 0;
     bool merge = false;  // merge_mode(cfg)
@@ -220,7 +222,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     // keys0: in the fused kernel, range r's keys are written to [r * kFusedKcap, ...)
     size_t o_keys0 = L.take(std::max((size_t)cap_pad + kSortTile, h->fused ? (size_t)h->fused_grid * kFusedKcap : 0) * 8);
     size_t o_keys1 = L.take(((size_t)cap_pad + kSortTile) * 8);
-    const uint32_t gmax = std::max(h->score_grid, std::max(h->sort_grid, h->fused_grid));
+    const uint32_t gmax = std::max(std::max(h->score_grid, h->big_grid), std::max(h->sort_grid, h->fused_grid));
     size_t o_kmask = L.take((size_t)2 * gmax * 8);
     size_t o_pin = L.take((size_t)gmax * 8);
     size_t o_flags = L.take((size_t)32 * 4 * (2 + 16));  // grid barrier: release word, 16 group counters, root
@@ -231,6 +233,12 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_spl = h->fused ? L.take((size_t)2 * (16 * 256 + 16) * 8) : 0;  // kernels_fused.cu kSplG
     size_t o_rcur = h->fused ? L.take((size_t)2 * 256 * 4) : 0;
     size_t o_nkp = L.take((size_t)gmax * 4);
+    const size_t bigr = big_max_ranges();
+    size_t o_bspl = h->big ? L.take((size_t)2 * (16 * bigr + 16) * 8) : 0;
+    size_t o_brc = h->big ? L.take((size_t)2 * bigr * 4) : 0;
+    size_t o_bov = h->big ? L.take(64) : 0;
+    size_t o_bkr = h->big ? L.take((size_t)h->big_ranges * kFusedKcap * 8) : 0;
+    size_t o_bkc = h->big ? L.take((size_t)h->big_grid * big_slots_per_cta() * 8) : 0;
     size_t o_ctl = L.take(sizeof(Ctl));
     size_t o_ctasm = L.take((size_t)gmax * 4);
     size_t o_as0 = L.take((size_t)mb * 4), o_as1 = L.take((size_t)mb * 4);
@@ -270,6 +278,13 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.spl = h->fused ? reinterpret_cast<unsigned long long*>(base + o_spl) : nullptr;
     h->b.rcur = h->fused ? reinterpret_cast<uint32_t*>(base + o_rcur) : nullptr;
     h->b.nk_part = reinterpret_cast<uint32_t*>(base + o_nkp);
+    h->b.big_ranges = h->big_ranges;
+    h->b.big_grid = h->big_grid;
+    h->b.big_spl = h->big ? reinterpret_cast<unsigned long long*>(base + o_bspl) : nullptr;
+    h->b.big_rcur = h->big ? reinterpret_cast<uint32_t*>(base + o_brc) : nullptr;
+    h->b.big_over = h->big ? reinterpret_cast<uint32_t*>(base + o_bov) : nullptr;
+    h->b.big_keysr = h->big ? reinterpret_cast<uint64_t*>(base + o_bkr) : nullptr;
+    h->b.big_keysc = h->big ? reinterpret_cast<uint64_t*>(base + o_bkc) : nullptr;
     h->b.score_grid = h->score_grid;
     h->b.sort_grid = h->sort_grid;
     h->b.ctl = reinterpret_cast<Ctl*>(base + o_ctl);
@@ -323,6 +338,17 @@ void grids(lamps_t* h, bool query_device) {
     if (!query_device) {  // size query: assume the fused path may be chosen
         h->fused = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && h->cap <= 148u * (uint32_t)kFusedKcap;
         h->fused_grid = std::max<uint32_t>(h->fused_grid, 296u);
+    }
+    // pools above the fused kernel's capacity (or LAMPS_BIG_STEP): several ranges per CTA
+    h->big = !(h->cfg.flags & LAMPS_MULTI_KERNEL) && !merge_mode(h->cfg) &&
+             ((h->cfg.flags & LAMPS_BIG_STEP) || !h->fused) && fused_occ >= 1;
+    if (h->big) {
+        h->fused = false;
+        h->small = false;
+        const uint32_t G = std::max<uint32_t>(h->fused_grid, 1u);
+        const uint64_t per = (uint64_t)G * 7168u;  // ~6300 eligible keys per range at 88 % READY
+        h->big_ranges = (uint32_t)std::min<uint64_t>((uint64_t)G * ((h->cap + per - 1) / per), big_max_ranges());
+        h->big_grid = (h->cap + big_slots_per_cta() - 1) / big_slots_per_cta();
     }
     const uint32_t groups = (h->cap + 3) / 4;
     const uint32_t want = (groups + kScoreThreads - 1) / kScoreThreads;
@@ -447,14 +473,24 @@ int enqueue_phase1(lamps_t* h, uint64_t kv_total, uint32_t n_ev) {
         h->cold = false;  // the kernel wrote the next step's splitters
         record_timing(h, 2);
         record_timing(h, 3);
+    } else if (h->big && !h->cold) {  // warm large-pool step (events applied by k_events above)
+        StepArgs ab = a;
+        ab.n_ev = 0;
+        CU(h, launch_big(h->b, h->cost, ab, nullptr, h->fused_grid, h->stream));
+        record_timing(h, 2);
+        record_timing(h, 3);
     } else {
         CU(h, launch_score(h->b, h->cost, a, (int)h->score_grid, h->stream));
         record_timing(h, 2);
         CU(h, launch_sort(h->b, h->cost, a, h->stream));
         record_timing(h, 3);
         CU(h, launch_admit(h->b, h->cost, a, h->stream));
+        if (h->big) {  // cold large-pool step: the next step's grid from this order
+            CU(h, launch_big_grid(h->b, a, h->stream));
+            h->cold = false;
+        }
     }
-    h->last_kernels = h->fused ? 1 : 3 + (n_ev ? 1 : 0);  // P2P: the exchange and merge are in k_fused
+    h->last_kernels = (h->fused ? 1 : (h->big && a.cold == 0 ? 2 : 3 + (h->big ? 1 : 0))) + (!h->fused && n_ev ? 1 : 0);
     h->ret_pending = 0;
     h->sub_pending = 0;
     h->inl_pending = false;

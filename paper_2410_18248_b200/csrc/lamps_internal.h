@@ -146,6 +146,14 @@ struct Bufs {
     MergeRec* xown;          // this rank's exchange buffer (the receive side)
     MergeRec* xsend;         // [1 + K] header + top-K records of this rank (world > 1)
     MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
+    // pools above the fused kernel's capacity (kernels_big.cu): V ranges over the score CTAs
+    uint32_t big_ranges;     // V (a multiple of the sort grid)
+    uint32_t big_grid;       // k_big_score CTAs (kBigSlots slots each)
+    unsigned long long* big_spl;  // [2][16 * kBigMaxRanges + 16] splitter grid by step parity
+    uint32_t* big_rcur;      // [2][kBigMaxRanges] keys written to each range, by step parity
+    uint32_t* big_over;      // [2] a range's region overflowed (this step: global-LSD fallback)
+    uint64_t* big_keysr;     // [V][kFusedKcap] the range regions
+    uint64_t* big_keysc;     // [big_grid][kBigSlots] each score CTA's keys (the fallback's input)
     uint32_t* xcnt;          // large merges: [world][world * K] counts of smaller records per other run
     uint32_t* xorder;        // large merges: [K] the merged order's first K records (xrecv indices)
 };
@@ -166,6 +174,11 @@ uint32_t small_max_cap();  // the one-CTA small-pool step kernel's capacity limi
 cudaError_t launch_small(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, cudaStream_t s);
 cudaError_t launch_merge(const Bufs& b, const Cost& c, const StepArgs& a, cudaStream_t s);
 bool merge_is_large(uint32_t world, uint32_t K);  // world * K records beyond one CTA's shared memory
+uint32_t big_slots_per_cta();
+uint32_t big_max_ranges();
+cudaError_t launch_big(const Bufs& b, const Cost& c, const StepArgs& a, const InlineStage* inl, uint32_t sort_grid,
+                       cudaStream_t s);
+cudaError_t launch_big_grid(const Bufs& b, const StepArgs& a, cudaStream_t s);
 // merge scratch: sk, gid (8 B) and demand (4 B) per record of the W runs, 3 index arrays of K
 __host__ __device__ inline size_t merge_smem_bytes(uint32_t world, uint32_t K) {
     const size_t R = (size_t)world * K;

@@ -24,6 +24,7 @@ LAMPS_POLICY_LAMPS, LAMPS_POLICY_FCFS, LAMPS_POLICY_SJF, LAMPS_POLICY_SJF_TOTAL 
 LAMPS_XPORT_NCCL, LAMPS_XPORT_LOOPBACK, LAMPS_XPORT_P2P = 0, 1, 2
 LAMPS_SHARE_DEVICE = 128
 LAMPS_GRID_STEP = 256  # small pools: the grid-wide fused kernel instead of the one-CTA kernel
+LAMPS_BIG_STEP = 512  # the large-pool path (several ranges per CTA) at any capacity
 
 u32, u64, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 

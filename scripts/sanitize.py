@@ -123,6 +123,8 @@ MODES = {
     "c5_head_only": lambda: c5(L.LAMPS_HEAD_ONLY),
     "c4_head_only": c4_head_only,
     "large_merge": large_merge,
+    "big": lambda: closed_loop("big", flags=L.LAMPS_BIG_STEP),  # the large-pool path on C3
+    "big_fallback": lambda: closed_loop("big_fallback", flags=L.LAMPS_BIG_STEP | L.LAMPS_FORCE_FALLBACK),
 }
 
 if __name__ == "__main__":

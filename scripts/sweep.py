@@ -1,6 +1,7 @@
 """Pool-size sweep (BASELINE config C5: 2^10 .. 2^23 slots, GPT-J profile): device time per
-scheduling step (CUDA events, L2 flushed before every step) and the path taken (fused
-cooperative kernel up to #SM * 10240 slots, the 3-kernel path above).  JSON to stdout."""
+scheduling step (CUDA events, L2 flushed before every step) and the path taken (the one-CTA
+kernel up to 4096 slots, the fused cooperative kernel up to #SM * 10240, the large-pool path above;
+the untimed first step after the import builds the range grid).  JSON to stdout."""
 import json
 import os
 import sys
@@ -27,6 +28,8 @@ for lg in range(lo, hi + 1):
         flush.zero_()
         s.step_async(kv)
     s.import_pool(snap, snap["id_base"], snap["next_id"])
+    flush.zero_()
+    s.step_async(kv)  # the cold step after the import (builds the range grid), untimed
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(STEPS)]
     for a, b in ev:
         flush.zero_()
@@ -34,11 +37,14 @@ for lg in range(lo, hi + 1):
         s.step_async(kv)
         b.record()
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / STEPS
+    ts = sorted(a.elapsed_time(b) for a, b in ev)
+    ms = sum(ts) / STEPS
     r = s.result()
     k, _ = s.stats()
     row = {"slots": cap, "eligible": r["n_eligible"], "us_per_step": round(ms * 1e3, 2),
-           "decisions_per_s": r["n_eligible"] / (ms / 1e3), "path": "fused" if k == 1 else "3-kernel"}
+           "us_median": round(ts[len(ts) // 2] * 1e3, 2), "decisions_per_s": r["n_eligible"] / (ms / 1e3),
+           "path": ("k_small" if cap <= 4096 else "k_fused") if k == 1 else ("big (k_big_score + k_big_sort)"
+                                                                           if k == 2 else "3-kernel")}
     print(row, file=sys.stderr, flush=True)
     rows.append(row)
     s.close()

@@ -9,8 +9,10 @@ FIELDS = ("state", "has_api", "starving", "strategy", "cnt", "ctx", "pre_rem", "
 
 
 # fused step kernel (one-CTA k_small for capacity <= 4096); LAMPS_MULTI_KERNEL; LAMPS_FORCE_FALLBACK;
-# LAMPS_HEAD_ONLY (F3 top-K fast path); LAMPS_GRID_STEP (small pools on the grid-wide fused kernel)
-PATH_FLAGS = {"fused": 0, "multi": 4, "fallback": 8, "head": 64, "grid": 256, "grid_fallback": 256 | 8}
+# LAMPS_HEAD_ONLY (F3 top-K fast path); LAMPS_GRID_STEP (small pools on the grid-wide fused kernel);
+# LAMPS_BIG_STEP (the large-pool path -- several ranges per CTA -- at any capacity)
+PATH_FLAGS = {"fused": 0, "multi": 4, "fallback": 8, "head": 64, "grid": 256, "grid_fallback": 256 | 8,
+              "big": 512, "big_fallback": 512 | 8}
 
 
 def make_pair(cfg: dict, debug=True, path="fused"):

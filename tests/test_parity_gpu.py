@@ -16,7 +16,7 @@ from parity_util import (compare_outputs, compare_state, load_both, make_pair, s
 pytestmark = pytest.mark.gpu
 
 
-PATHS = ["fused", "multi", "fallback", "head", "grid", "grid_fallback"]
+PATHS = ["fused", "multi", "fallback", "head", "grid", "grid_fallback", "big", "big_fallback"]
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -33,6 +33,14 @@ def test_snapshot_parity(cname, seed, id_base, path):
 def test_c5_full_size_parity(path):
     # BASELINE.json's 1M-request pool in the launch configuration bench.py times
     snapshot_step_parity("C5", seed=0, id_base=(1 << 20) * 7 + 99, steps=2, path=path)
+
+
+@pytest.mark.slow
+def test_pool_above_fused_capacity_parity():
+    # 2^21 slots: above the fused kernel's 148 x 10240, the large-pool path (k_big_score +
+    # k_big_sort, two ranges per CTA); the first step is the cold 3-kernel one
+    snapshot_step_parity("C5", seed=1, n=1 << 21, capacity=1 << 21, id_base=(1 << 21) * 3 + 5, steps=3, id_bits=21,
+                         path="fused")
 
 
 @pytest.mark.parametrize("path", PATHS)
