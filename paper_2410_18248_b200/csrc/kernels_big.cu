@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kFT, 1) k_big_score(const __grid_constant__ Bu
     BigSmemA& sm = *reinterpret_cast<BigSmemA*>(smem_raw);
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, bid = blockIdx.x;
     const uint32_t V = b.big_ranges;
-    const uint32_t s_lo = bid * kBigSlots, s_hi = min(c.cap, s_lo + kBigSlots);
+    const uint32_t s_lo = bid * b.big_cta_slots, s_hi = min(c.cap, s_lo + b.big_cta_slots);  // <= kBigSlots
     const uint32_t npos = s_hi > s_lo ? s_hi - s_lo : 0u;
     if (warp == 0) {  // the CTA's seven SoA ranges into L2 (bulk prefetches)
         for (uint32_t q = lane; q < 7u * ((npos + 1023u) / 1024u); q += 32u) {

@@ -93,7 +93,7 @@ struct lamps_s {
     Cost cost{};
     Bufs b{};
     uint32_t cap = 0, cap_pad = 0, score_grid = 0, sort_grid = 0, fused_grid = 0;
-    uint32_t big_ranges = 0, big_grid = 0;
+    uint32_t big_ranges = 0, big_grid = 0, big_cta_slots = 0;
     bool fused = false;
     bool small = false;   // fused family: the one-CTA small-pool step kernel (k_small)
     bool big = false;     // pools above the fused kernel's capacity: k_big_score + k_big_sort
@@ -280,6 +280,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.nk_part = reinterpret_cast<uint32_t*>(base + o_nkp);
     h->b.big_ranges = h->big_ranges;
     h->b.big_grid = h->big_grid;
+    h->b.big_cta_slots = h->big_cta_slots;
     h->b.big_spl = h->big ? reinterpret_cast<unsigned long long*>(base + o_bspl) : nullptr;
     h->b.big_rcur = h->big ? reinterpret_cast<uint32_t*>(base + o_brc) : nullptr;
     h->b.big_over = h->big ? reinterpret_cast<uint32_t*>(base + o_bov) : nullptr;
@@ -348,7 +349,13 @@ void grids(lamps_t* h, bool query_device) {
         const uint32_t G = std::max<uint32_t>(h->fused_grid, 1u);
         const uint64_t per = (uint64_t)G * 7168u;  // ~6300 eligible keys per range at 88 % READY
         h->big_ranges = (uint32_t)std::min<uint64_t>((uint64_t)G * ((h->cap + per - 1) / per), big_max_ranges());
-        h->big_grid = (h->cap + big_slots_per_cta() - 1) / big_slots_per_cta();
+        // whole waves of one CTA per SM: the fewest waves whose CTAs hold <= 8192 slots each
+        const uint64_t sms_u = (uint64_t)std::max(sms, 1), mx = big_slots_per_cta();
+        const uint64_t waves = (h->cap + sms_u * mx - 1) / (sms_u * mx);
+        uint64_t spc = (h->cap + sms_u * waves - 1) / (sms_u * waves);
+        spc = std::min<uint64_t>((spc + 31) & ~31ull, mx);
+        h->big_cta_slots = (uint32_t)spc;
+        h->big_grid = (uint32_t)((h->cap + spc - 1) / spc);
     }
     const uint32_t groups = (h->cap + 3) / 4;
     const uint32_t want = (groups + kScoreThreads - 1) / kScoreThreads;

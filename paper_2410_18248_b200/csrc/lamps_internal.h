@@ -148,7 +148,8 @@ struct Bufs {
     MergeRec* xrecv;         // [world][1 + K] all ranks' send buffers after the all-gather
     // pools above the fused kernel's capacity (kernels_big.cu): V ranges over the score CTAs
     uint32_t big_ranges;     // V (a multiple of the sort grid)
-    uint32_t big_grid;       // k_big_score CTAs (kBigSlots slots each)
+    uint32_t big_grid;       // k_big_score CTAs
+    uint32_t big_cta_slots;  // slots per k_big_score CTA (<= kBigSlots; whole waves of #SM CTAs)
     unsigned long long* big_spl;  // [2][16 * kBigMaxRanges + 16] splitter grid by step parity
     uint32_t* big_rcur;      // [2][kBigMaxRanges] keys written to each range, by step parity
     uint32_t* big_over;      // [2] a range's region overflowed (this step: global-LSD fallback)
