@@ -105,3 +105,41 @@ def test_no_cpu_fallback_without_gpu(L):
         pytest.skip("GPU present")
     with pytest.raises(L.LampsError):
         L.Scheduler(dict(capacity=16, max_batch=4, id_bits=23, score_bits=40))
+
+
+def test_multi_shard_config_limits(L):
+    """The P2P in-kernel merge stages world x K records on chip (<= 8192); the NCCL and
+    loopback transports merge any exchange (the grid-wide merge by rank); local_ranks <= world."""
+    nid = ctypes.create_string_buffer(128)
+    n = ctypes.c_size_t(0)
+    big_p2p = _cfg(L, max_batch=8192, world=8, rank=0, transport=L.LAMPS_XPORT_P2P)
+    assert L.lib().lamps_init(ctypes.byref(big_p2p), None, ctypes.byref(n), None) == L.LAMPS_EINVAL
+    big_nccl = _cfg(L, max_batch=8192, world=8, rank=0, transport=L.LAMPS_XPORT_NCCL)
+    big_nccl.nccl_id = ctypes.cast(nid, ctypes.c_void_p)
+    assert L.lib().lamps_init(ctypes.byref(big_nccl), None, ctypes.byref(n), None) == L.LAMPS_OK
+    small = L.lamps_workspace_bytes(_cfg(L, max_batch=256, world=8, rank=0, transport=L.LAMPS_XPORT_LOOPBACK))
+    large = L.lamps_workspace_bytes(_cfg(L, max_batch=8192, world=8, rank=0, transport=L.LAMPS_XPORT_LOOPBACK))
+    assert large > small + 8 * 8 * 8192 * 4  # the merge-by-rank count matrix
+    over = _cfg(L, world=4, rank=0, transport=L.LAMPS_XPORT_P2P, local_ranks=5)
+    assert L.lib().lamps_init(ctypes.byref(over), None, ctypes.byref(n), None) == L.LAMPS_EINVAL
+    ok = _cfg(L, world=8, rank=3, transport=L.LAMPS_XPORT_P2P, local_ranks=4, flags=L.LAMPS_SHARE_DEVICE)
+    assert L.lib().lamps_init(ctypes.byref(ok), None, ctypes.byref(n), None) == L.LAMPS_OK
+
+
+def test_large_pool_workspace(L):
+    """Pools above the fused kernel's capacity carry the large-pool path's range regions."""
+    n21 = L.lamps_workspace_bytes(_cfg(L, capacity=1 << 21, id_bits=21, score_bits=35))
+    n20 = L.lamps_workspace_bytes(_cfg(L, capacity=1 << 20, id_bits=20, score_bits=35))
+    assert n21 > 2 * n20
+    forced = L.lamps_workspace_bytes(_cfg(L, flags=L.LAMPS_BIG_STEP))
+    plain = L.lamps_workspace_bytes(_cfg(L, flags=L.LAMPS_MULTI_KERNEL))  # the 3-kernel path alone
+    assert forced > plain + 148 * 10240 * 8  # V >= 148 range regions of 10240 keys
+
+
+def test_group_step_async_rejects_bad_groups(L):
+    """lamps_group_step_async validates before touching any handle (NULL / empty groups)."""
+    kv = (ctypes.c_uint64 * 1)(0)
+    assert L.lib().lamps_group_step_async(None, 1, kv) == L.LAMPS_EINVAL
+    hs = (ctypes.c_void_p * 1)(None)
+    assert L.lib().lamps_group_step_async(hs, 1, kv) == L.LAMPS_EINVAL
+    assert L.lib().lamps_group_step_async(hs, 0, kv) == L.LAMPS_EINVAL
