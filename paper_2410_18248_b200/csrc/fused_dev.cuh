@@ -310,7 +310,8 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
                                                 uint64_t* __restrict__ out, uint32_t vb, unsigned long long* tr,
                                                 const Pool* pool = nullptr, uint32_t id_base_mod = 0,
                                                 const Cost* cc = nullptr, uint32_t* dsm = nullptr,
-                                                uint32_t* wsm = nullptr) {
+                                                uint32_t* wsm = nullptr, const uint32_t* __restrict__ pd_src = nullptr,
+                                                const uint32_t* __restrict__ pw_src = nullptr) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.b);                      // <= 2^13 + 1 counters
@@ -355,6 +356,28 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
     (void)smem_excl_scan<kFT, (1 << 13) / kFT + 1>(cnt, ncnt, sm.w32);
     if (tid == 0) cnt[ncnt] = rn;
     LTRACE(3);
+    // CTA 0 with the head's payload (pd_src / pw_src beside the keys): placed with the keys
+    uint32_t* const Pd = sm.pos + 3u * kHeadPre;                         // [kHeadPre] by placed position
+    uint32_t* const Pw = reinterpret_cast<uint32_t*>(sm.b) + 14336u;     // [kHeadPre], past cnt / dp
+    if (pd_src) {  // rn <= kHeadPre: all loads in flight at once
+        constexpr int kPU = (kHeadPre + kFT - 1) / kFT;
+        uint32_t pdv[kPU], pwv[kPU];
+#pragma unroll
+        for (int u = 0; u < kPU; u++) {
+            const uint32_t i = tid + (uint32_t)u * kFT;
+            pdv[u] = i < rn ? __ldcg(pd_src + i) : 0u;
+            pwv[u] = i < rn ? __ldcg(pw_src + i) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPU; u++) {
+            const uint32_t i = tid + (uint32_t)u * kFT;
+            if (i < rn) {
+                const uint32_t v = dv[i], p = cnt[v & 0x1fffu] + (v >> 13);
+                Pd[p] = pdv[u];
+                Pw[p] = pwv[u];
+            }
+        }
+    }
     for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
         uint64_t kk[4];
 #pragma unroll
@@ -390,6 +413,10 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
             continue;
         }
         dv[p] = st + r;  // final position (dv is free after the placement)
+        if (pd_src) {
+            dsm[st + r] = Pd[p];
+            wsm[st + r] = Pw[p];
+        }
     }
     LTRACE(5);
     if (__syncthreads_or(big)) return false;
@@ -398,7 +425,7 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
     uint64_t* B2 = sm.b;
     for (uint32_t p = tid; p < rn; p += kFT) B2[dv[p]] = A[p];
     __syncthreads();
-    if (dsm) {  // CTA 0: the admission's loads (L2 hits: the score phase read them), all in flight at once
+    if (dsm && !pd_src) {  // CTA 0 without payload: the admission's loads (L2 hits), all in flight at once
         for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
             uint32_t cx[4], w[4];
 #pragma unroll

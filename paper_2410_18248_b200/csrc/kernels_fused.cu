@@ -443,9 +443,22 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     }
     __syncthreads();
     TRACE(12);
+    // warm steps: range 0's keys (the admission head; run 0 = kb2[0, lst[1])) get their payload
+    // -- demand blk(ctx + 1) and state word, this CTA's own slots (L2) -- stored beside them, so
+    // CTA 0 sorts the head with it instead of gathering it after its sort
+    const bool hpay = !a.cold && G > 1u && !(a.flags & kStepMerge);
+    const uint32_t n0 = sm.s.lst[1];
     for (uint32_t i = tid; i < (hr ? sm.s.lcnt[0] : nk_cta); i += kFT) {  // (head-only: run 0 = [0, lcnt[0]))
         const uint32_t r = rr[i], pos = sm.s.gbase[r] + (i - sm.s.lst[r]);
-        if (pos < (uint32_t)kKcap) b.keys[0][(size_t)r * kKcap + pos] = kb2[i];  // else: overflow -> fallback
+        if (pos < (uint32_t)kKcap) {  // else: overflow -> fallback
+            const uint64_t k = kb2[i];
+            b.keys[0][(size_t)r * kKcap + pos] = k;
+            if (hpay && i < n0) {
+                const uint32_t slot = (a.id_base_mod + (uint32_t)(k & c.cap_mask)) & c.cap_mask;
+                b.hd[pos] = (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
+                b.hw[pos] = b.pool.sfc[slot];
+            }
+        }
     }
     TRACE(6);
     grid_barrier(b.flags, G, ++bar);
@@ -553,9 +566,11 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             TRACE(13);
             // CTA 0 (single shard): head + admission loads on chip
             const bool stage = bid == 0 && rn <= kHeadPre && !(a.flags & kStepMerge);
+            const bool hpay0 = stage && !a.cold && G > 1u;  // (merge steps never stage)
             written = LAMPS_RANGE_SORT(sm.l, src, rn, b.keys[1] + rpre, vb, tr ? tr + 32 : nullptr, &b.pool,
                                       a.id_base_mod, &c, stage ? sm.l.pos + kHeadPre : nullptr,
-                                      stage ? sm.l.pos + 2u * kHeadPre : nullptr);
+                                      stage ? sm.l.pos + 2u * kHeadPre : nullptr, hpay0 ? b.hd : nullptr,
+                                      hpay0 ? b.hw : nullptr);
             head_loop = stage && written;
             if (!written) {  // a counter held too many keys: sort the placed range by LSD
                 unsigned long long o, an;

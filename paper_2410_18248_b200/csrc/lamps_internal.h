@@ -123,6 +123,9 @@ struct Bufs {
                              // the next step's from its own sorted order
     uint32_t* rcur;          // fused: [2][256] keys written to each range, by step parity
     uint32_t* nk_part;       // fused: [grid] keys of each CTA
+    uint32_t* hd;            // fused: [kFusedKcap] demand blk(ctx + 1) of range 0's keys (the admission
+                             // head), beside range 0's region of keys[0] (warm steps)
+    uint32_t* hw;            // fused: [kFusedKcap] their state words, likewise
     uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity
