@@ -65,7 +65,39 @@ struct PhaseS {                  // S, H, X (cold), R
     float wx[kMaxCtas + 1];      // X: exclusive prefix of the range weights
     alignas(16) unsigned long long spl[kSplPad];  // R: range r = keys in [spl[P(r)], spl[P(r + 1)]), P = spl_pos
     uint32_t lcnt[kMaxCtas + 1], lst[kMaxCtas + 1], gbase[kMaxCtas];  // R: this CTA's run per range
+    uint32_t novf, nmiss;        // binned R: keys in the overflow list, hint misses queued
+    alignas(8) unsigned long long hbar;  // binned R: the range hints' copy (mbarrier)
 };
+// Binned R: byte layout over sm.s.cnt + start (free in warm steps): range hints / ranges by
+// position (the copy starts at the 16-B boundary below the CTA's first slot), G bins of kBinCap
+// keys, the overflow list (position | index in the run << 14, every key of the CTA fits), the
+// queue of hint misses.
+constexpr uint32_t kBinCap = 48;
+constexpr uint32_t kRbBins = (kKcap + 32u + 63u) & ~63u;
+constexpr uint32_t kRbBinsMax = 148u * kBinCap * 8u;
+constexpr uint32_t kRbOvl = kRbBins + kRbBinsMax;
+constexpr uint32_t kRbMiss = kRbOvl + 4u * kKcap;
+constexpr uint32_t kMissCap = (sizeof(uint32_t) * 2u * kMaxBuckets - kRbMiss) / 2u;
+static_assert(kMissCap >= 2048u, "binned R: the miss queue is too small");
+__host__ __device__ constexpr bool bins_fit(uint32_t G) { return G <= 148u; }
+// thread 0 at kernel start: the hints of slots [s_lo, s_hi) (16-B aligned around them) -> dst
+__device__ __forceinline__ void range_hint_issue(unsigned long long& bar, uint8_t* dst, const uint8_t* hint,
+                                                 uint32_t s_lo, uint32_t s_hi) {
+    const uint32_t a0 = s_lo & ~15u, a1 = (s_hi + 15u) & ~15u;
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(a1 - a0) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)), "l"(hint + a0), "r"(a1 - a0), "r"(mb) : "memory");
+}
+__device__ __forceinline__ void range_hint_wait(unsigned long long& bar) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar);
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(mb) : "memory");
+}
 constexpr int kSubBits = 13;                // local MSD digit
 constexpr int kSubBuckets = 1 << kSubBits;
 constexpr uint32_t kMaxRankM = 32;          // largest group ranked by comparison
@@ -93,6 +125,8 @@ struct PhaseL {                  // L
     uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size and position in the order
     unsigned long long fine[kSeg + 1], fcode[kSeg + 1];  // this range's grid entries, their key codes
     uint32_t shs[kSeg];                                  // range sort: per segment, the digit's shift
+    alignas(8) unsigned long long mbar;                  // range_sort_tma: the staging copy's mbarrier
+    uint32_t gf[2];                                      // the next step's grid entries [gf0, gf1) in this range
 };
 struct FusedSmem {
     union {
@@ -450,6 +484,208 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
     LTRACE(6);
 #undef LTRACE
     return true;
+}
+
+// ---- The range sort staged by TMA (rn <= kTmaMax keys; every CTA, the head's too, runs this
+// same code, so its lines are fetched once for all SMs).  After the grid barrier one thread
+// requests the range's keys (the region the runs of all CTAs were stored into) into shared
+// memory with ONE bulk copy (cp.async.bulk, completion on an mbarrier; CTA 0 with the head's
+// payload: two more, the demand and state words R stored beside the head's keys).  Then the
+// counting pass on the piecewise-linear digit as in range_sort_loop, every pass over shared
+// memory, and the rank pass stores each key straight to its place in the output (a warp's
+// consecutive placed positions go to a few consecutive lines: the placement is the order up to
+// a counter's keys); with `keep` (CTA 0) also into shared memory for the admission, with the
+// payload by sorted position.
+// Layout (bytes): sm.a: A (placed keys) [0, 8 kTmaMax) | dp (u16 counter per placed position);
+// head payload placed: Pd [8 kHeadPre, 12 kHeadPre), Pw [12 kHeadPre, 16 kHeadPre) (rn <= kHeadPre).
+// From sm.b on (sm.b and the union after it): S (staged keys) [0, 8 kTmaMax) | cnt | dv;
+// head payload staged at [8 kHeadPre, 16 kHeadPre) of S's space; after the place pass the sorted
+// head goes to [0, 8 rn) (kept keys) and its payload to the staged payload's places (dsm / wsm).
+// Position of the next step's grid entry f (0 .. 16 G) in this step's order of n keys: range 0's
+// 16 segments over [0, q1), the other ranges' over [q1, n) evenly (past the last key: the last key).
+__device__ __forceinline__ uint32_t grid_q(uint32_t f, uint32_t q1, uint32_t n, uint32_t G) {
+    const uint64_t p = f <= (uint32_t)kSeg ? (uint64_t)q1 * f / kSeg
+                                           : q1 + (uint64_t)(f - kSeg) * (uint64_t)(n - q1) / ((uint64_t)kSeg * (G - 1u));
+    return n ? (uint32_t)min(p, (uint64_t)(n - 1u)) : 0u;
+}
+// The first f with grid_q(f) >= q (16 G + 1 if none), in closed form: for q <= q1 the head's
+// floor(q1 f / 16) >= q <=> f >= ceil(16 q / q1); past the head floor((f - 16) D / M) >= q - q1 <=>
+// f - 16 >= ceil((q - q1) M / D) (D = n - q1, M = 16 (G - 1)); the clamp at n - 1 only bites q >= n.
+__device__ __forceinline__ uint32_t grid_f(uint32_t q, uint32_t q1, uint32_t n, uint32_t G) {
+    if (q == 0u) return 0u;
+    if (q >= n) return (uint32_t)kSeg * G + 1u;
+    if (q <= q1) return (uint32_t)(((uint64_t)q * kSeg + q1 - 1u) / q1);
+    const uint64_t D = n - q1, num = (uint64_t)(q - q1) * kSeg * (G - 1u);
+    return kSeg + (uint32_t)((num + D - 1u) / D);
+}
+constexpr uint32_t kTmaMax = 7167;  // (the kept keys sit one key later when the range starts at an odd position)
+constexpr uint32_t kTsCnt = 8u * (kTmaMax + 1u);                         // byte offsets from sm.b
+constexpr uint32_t kTsDv = (kTsCnt + 4u * ((1u << 13) + 1u) + 15u) & ~15u;
+constexpr uint32_t kTsHd = 8u * kHeadPre, kTsHw = 12u * kHeadPre;        // head payload (sm.b / sm.a)
+static_assert(kTsHw + 4u * kHeadPre <= kTsCnt, "TMA range sort: head payload overlaps cnt");
+static_assert(kTsDv + 4u * kTmaMax <= 8u * kKcap + 4u * kKcap, "TMA range sort: S/cnt/dv exceed sm.b + sm.pos");
+static_assert(kTsCnt % 16u == 0u && kTsHd % 16u == 0u && kTsHw % 16u == 0u, "TMA staging offsets: 16-B aligned");
+static_assert(offsetof(PhaseL, b) + 8u * kKcap == offsetof(PhaseL, pos), "sm.pos must follow sm.b");
+static_assert(offsetof(PhaseL, w32) >= offsetof(PhaseL, b) + kTsDv + 4u * kTmaMax, "TMA range sort overlaps sm.w32");
+static_assert(8u * kTmaMax + 2u * kTmaMax <= 8u * kKcap, "TMA range sort: A + dp exceed sm.a");
+static_assert(kTsHw + 4u * kHeadPre <= 8u * kTmaMax, "TMA range sort: placed head payload overlaps dp");
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mb) : "memory");
+}
+// one thread, after the grid barrier: the range's keys [src, src + rn) -> sm.b, and (hd != null)
+// the head's demand / state words -> their staging places (16-B multiples: a few words past rn
+// may be copied, inside the regions)
+__device__ __forceinline__ void range_stage_issue(PhaseL& sm, const uint64_t* src, uint32_t rn,
+                                                  const uint32_t* hd = nullptr, const uint32_t* hw = nullptr) {
+    const uint32_t kb = ((rn + 1u) & ~1u) * 8u, pb = ((rn + 3u) & ~3u) * 4u;
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm.b);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the region was written by other CTAs' generic stores (ordered by the barrier's acquire),
+    // shared memory by this CTA's generic stores: both before the async proxy's copy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(kb + (hd ? 2u * pb : 0u)) : "memory");
+    bulk_g2s(dst, src, kb, mb);
+    if (hd) {
+        bulk_g2s(dst + kTsHd, hd, pb, mb);
+        bulk_g2s(dst + kTsHw, hw, pb, mb);
+    }
+}
+// every thread (after a __syncthreads that follows range_stage_issue): the copies have landed
+__device__ __forceinline__ void range_stage_wait(PhaseL& sm) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(mb) : "memory");
+}
+// the kept head (keep): sorted keys at sm.b, demand / state words by sorted position
+__device__ __forceinline__ uint32_t* tma_head_dem(PhaseL& sm) { return reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sm.b) + kTsHd); }
+__device__ __forceinline__ uint32_t* tma_head_st(PhaseL& sm) { return reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sm.b) + kTsHw); }
+
+// The sorted keys go to shared memory, sm.b + (o = the output position's parity) -- so that key i
+// and out[i] share their alignment -- and thread 0 stores them to out with one bulk copy (TMA,
+// its bulk group left open: the caller waits before the CTA exits or anyone reads out); the key
+// before the first and after the last 16-B pair of out by plain stores.  pay: the head payload
+// was staged; its words go to their sorted positions.  Returns false if a counter held more than
+// kRangeRankM keys (nothing stored): sm.a then holds the range placed by digit (the caller sorts
+// it otherwise).
+__device__ __forceinline__ bool range_sort_tma(PhaseL& sm, uint32_t rn, uint64_t* __restrict__ out, uint32_t o,
+                                               uint32_t vb, unsigned long long* tr, bool pay) {
+#define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
+    const uint32_t tid = threadIdx.x;
+    unsigned char* fb = reinterpret_cast<unsigned char*>(sm.b);
+    uint64_t* S = sm.b;                                          // staged keys, then (keep) the sorted head
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(fb + kTsCnt);    // <= 2^13 + 1 counters
+    uint32_t* dv = reinterpret_cast<uint32_t*>(fb + kTsDv);      // per staged key: digit | order << 13
+    uint32_t* Hd = reinterpret_cast<uint32_t*>(fb + kTsHd);      // head payload staged, then by sorted position
+    uint32_t* Hw = reinterpret_cast<uint32_t*>(fb + kTsHw);
+    uint64_t* A = sm.a;                                          // placed keys
+    uint16_t* dp = reinterpret_cast<uint16_t*>(sm.a + kTmaMax);  // per placed position: its counter
+    uint32_t* Pd = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sm.a) + kTsHd);  // payload placed
+    uint32_t* Pw = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sm.a) + kTsHw);
+    LTRACE(0);
+    const uint32_t cb = max(min(rn > 1u ? 33u - (uint32_t)__clz(rn - 1u) : 0u, 13u), 4u);  // ~2-4 counters per key
+    const uint32_t lw = cb - 4u, W = 1u << lw, ncnt = (uint32_t)kSeg * W;
+    uint32_t* shs = sm.shs;
+    if (tid < (uint32_t)kSeg) {
+        const unsigned long long d = sm.fcode[tid + 1] > sm.fcode[tid] ? sm.fcode[tid + 1] - sm.fcode[tid] : 0ull;
+        const uint32_t nb = 64u - (uint32_t)__clzll((long long)d);
+        shs[tid] = nb > lw ? nb - lw : 0u;
+    }
+    for (uint32_t i = tid; i <= ncnt; i += kFT) cnt[i] = 0u;
+    range_stage_wait(sm);
+    __syncthreads();
+    auto digit = [&](uint64_t k) -> uint32_t {
+        uint32_t sg = 0;
+#pragma unroll
+        for (uint32_t st = kSeg / 2; st; st >>= 1) sg = k >= sm.fine[sg + st] ? sg + st : sg;
+        const unsigned long long c = key_code(k, vb), c0 = sm.fcode[sg];
+        const unsigned long long d = (c > c0 ? c - c0 : 0ull) >> shs[sg];
+        return sg * W + (uint32_t)min(d, (unsigned long long)(W - 1u));
+    };
+    LTRACE(1);
+    for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t i = i0 + (uint32_t)u * kFT;
+            if (i < rn) {
+                const uint32_t d = digit(S[i]);
+                dv[i] = d | (atomicAdd(&cnt[d], 1u) << 13);
+            }
+        }
+    }
+    __syncthreads();
+    LTRACE(2);
+    (void)smem_excl_scan<kFT, (1 << 13) / kFT + 1>(cnt, ncnt, sm.w32);
+    if (tid == 0) cnt[ncnt] = rn;
+    LTRACE(3);
+    for (uint32_t i0 = tid; i0 < rn; i0 += 4u * kFT) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t i = i0 + (uint32_t)u * kFT;
+            if (i < rn) {
+                const uint32_t v = dv[i], d = v & 0x1fffu, p = cnt[d] + (v >> 13);
+                A[p] = S[i];
+                dp[p] = (uint16_t)d;
+                if (pay) {
+                    Pd[p] = Hd[i];
+                    Pw[p] = Hw[i];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    LTRACE(4);
+    bool big = false;
+    for (uint32_t p = tid; p < rn; p += kFT) {
+        const uint64_t k = A[p];
+        const uint32_t d = dp[p], st = cnt[d], m2 = cnt[d + 1] - st;
+        uint32_t r = 0;
+        if (m2 <= 4u) {
+            if (m2 > 1u) {
+                r += A[st] < k ? 1u : 0u;
+                r += A[st + 1] < k ? 1u : 0u;
+                if (m2 > 2u) r += A[st + 2] < k ? 1u : 0u;
+                if (m2 > 3u) r += A[st + 3] < k ? 1u : 0u;
+            }
+        } else if (m2 <= kRangeRankM) {
+            for (uint32_t q = 0; q < m2; q++) r += A[st + q] < k ? 1u : 0u;
+        } else {
+            big = true;
+            continue;
+        }
+        S[o + st + r] = k;
+        if (pay) {
+            Hd[st + r] = Pd[p];
+            Hw[st + r] = Pw[p];
+        }
+    }
+    LTRACE(5);
+    if (__syncthreads_or(big)) return false;
+    const uint64_t* K = S + o;  // K[i] = the key of out[i]
+    const uint32_t i0 = o, i1 = o + ((rn - min(o, rn)) & ~1u);  // out[i0, i1): whole 16-B pairs
+    if (tid == 0 && i1 > i0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the rank pass's stores, then the copy
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\ncp.async.bulk.commit_group;" ::"l"(out + i0),
+                     "r"((uint32_t)__cvta_generic_to_shared(K + i0)), "r"((i1 - i0) * 8u) : "memory");
+    }
+    if (tid == 32u && i0 > 0u && rn) out[0] = K[0];
+    if (tid == 64u && i1 < rn) out[rn - 1u] = K[rn - 1u];
+    LTRACE(6);
+#undef LTRACE
+    return true;
+}
+// the issuing thread: the bulk store has read shared memory (before the CTA exits) / is complete
+// and visible to generic loads (before another CTA or a later phase reads out)
+__device__ __forceinline__ void bulk_store_read_wait() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_store_done() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // (Measured and not kept: range_sort_lean -- one L2 load, the digit recomputed

@@ -61,6 +61,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         }
     }
 
+    const bool hr0 = (a.flags & kStepHeadOnly) && G > 1u && !a.cold;  // head-only R (hr below)
+    if (tid == 0 && !a.cold && !hr0 && bins_fit(G) && s_hi > s_lo)  // the slots' range hints -> shared memory
+        range_hint_issue(sm.s.hbar, reinterpret_cast<uint8_t*>(sm.s.cnt), b.rhint, s_lo, s_hi);
     TRACE(0);
     if (b.trace && tid == 0) {  // diagnostics: the kernel's start on the global clock (slot 29)
         unsigned long long g0;
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         __syncthreads();
     }
     if (tid < (uint32_t)kMaxCtas) sm.s.lcnt[tid] = 0u;  // R's per-range counts
+    if (tid == 0) { sm.s.novf = 0u; sm.s.nmiss = 0u; }
     if (a.cold) {
         for (uint32_t i = tid; i < (uint32_t)kMaxBuckets / 4u; i += kFT)
             reinterpret_cast<uint4*>(sm.s.cnt)[i] = make_uint4(0, 0, 0, 0);
@@ -157,6 +161,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     };
     // keys stay at their slot's position in kbuf (position = slot - s_lo); which positions hold
     // keys: one ballot word per warp and slot parity (vmask[2 * (q >> 5) + j], q = pair index)
+    // binned R (warm steps with the full R): layout over sm.s.cnt / start (free in warm steps)
+    const bool binm = !a.cold && !hr0 && bins_fit(G);
+    uint8_t* const rbase = reinterpret_cast<uint8_t*>(sm.s.cnt);
+    uint8_t* const rvb = rbase;                                                 // range hints by position
+    uint64_t* const bins = reinterpret_cast<uint64_t*>(rbase + kRbBins);        // [G][kBinCap]
+    uint32_t* const ovl = reinterpret_cast<uint32_t*>(rbase + kRbOvl);          // position | index << 14
+    uint16_t* const mq = reinterpret_cast<uint16_t*>(rbase + kRbMiss);          // queued hint misses
     {
         const uint32_t p_lo = s_lo >> 1, p_hi = s_hi >> 1;  // slot pairs
         const uint2* S2 = reinterpret_cast<const uint2*>(b.pool.sfc);
@@ -385,7 +396,64 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // warm head-only steps (F3): only the head matters -- range 0 = keys below the first
     // splitter, every other key "range 1" (kept on chip for the fallback, never stored)
     const bool hr = head_mode && !a.cold && G > 1u;
-    if (hr) {
+    if (binm) {
+        // binned R (warm steps): one pass over the keys -- each key's range from its slot's hint
+        // (the range it had in the last ranking step, copied to shared memory at kernel start:
+        // the splitters move little from step to step) verified by two compares, then its place
+        // in the range's bin (kBinCap keys; the rest by position in the overflow list, with its
+        // index in the range's run).  Keys whose hint misses are queued and searched after the
+        // pass (a miss inside the pass would make its whole warp search); their hints are updated.
+        const unsigned long long* spl = sm.s.spl;
+        uint8_t* const rvp = rvb + (s_lo & 15u);
+        auto bin_add = [&](uint32_t i, uint64_t k, uint32_t rg) {
+            const uint32_t j = atomicAdd(&sm.s.lcnt[rg], 1u);
+            if (j < kBinCap) bins[rg * kBinCap + j] = k;
+            else ovl[atomicAdd(&sm.s.novf, 1u)] = i | (j << 14);
+        };
+        auto search_add = [&](uint32_t i, uint64_t k) {
+            uint32_t r = 0;
+#pragma unroll
+            for (uint32_t st = kMaxCtas / 2u; st; st >>= 1) r = k >= spl[spl_pos(r + st)] ? r + st : r;
+            const uint32_t rg = min(r, G - 1u);
+            rvp[i] = (uint8_t)rg;
+            b.rhint[s_lo + i] = (uint8_t)rg;
+            bin_add(i, k, rg);
+        };
+        if (s_hi > s_lo) range_hint_wait(sm.s.hbar);  // (issued at kernel start)
+        for (uint32_t i = tid; i < npos; i += kFT) {
+            const uint32_t q = i >> 1;
+            if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
+            const uint64_t k = sm.s.kbuf[i];
+            const uint32_t h = rvp[i];
+            // the hint's range or a neighbour (the order drifts by the keys that changed since:
+            // e.g. newly starving keys move every other key back by their number)
+            const uint32_t hm = h ? h - 1u : 0u;
+            const unsigned long long sm1 = spl[spl_pos(hm)], s0 = spl[spl_pos(h)], s1 = spl[spl_pos(h + 1u)],
+                                     s2 = spl[spl_pos(h + 2u)];
+            const uint32_t rg = k < s0 ? (k >= sm1 || hm == 0u ? hm : 255u) : (k < s1 ? h : (k < s2 ? h + 1u : 255u));
+            if (h < G && rg < G) {
+                if (rg != h) {
+                    rvp[i] = (uint8_t)rg;
+                    b.rhint[s_lo + i] = (uint8_t)rg;
+                }
+                bin_add(i, k, rg);
+            } else {
+                const uint32_t m = atomicAdd(&sm.s.nmiss, 1u);
+                if (m < kMissCap) mq[m] = (uint16_t)i;
+                else search_add(i, k);
+            }
+        }
+        __syncthreads();
+        const uint32_t nm = min(sm.s.nmiss, kMissCap);
+        for (uint32_t m = tid; m < nm; m += kFT) {
+            const uint32_t i = mq[m];
+            search_add(i, sm.s.kbuf[i]);
+        }
+        if (b.trace && tid == 0) {  // diagnostics: hint misses, overflow keys
+            b.trace[(size_t)bid * kTraceSlots + 16] = sm.s.nmiss;
+            b.trace[(size_t)bid * kTraceSlots + 17] = sm.s.novf;
+        }
+    } else if (hr) {
         const unsigned long long s1 = sm.s.spl[spl_pos(1)];
         for (uint32_t i = tid; i < npos; i += kFT) {
             const uint32_t q = i >> 1;
@@ -394,8 +462,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             rv[i] = (uint8_t)rg;
             atomicAdd(&sm.s.lcnt[rg], 1u);
         }
-    } else {
+    } else if (!binm) {  // cold steps: a binary search over the splitters (seeds the range hints)
         const unsigned long long* spl = sm.s.spl;
+        uint8_t* const hint = b.rhint + s_lo;
         for (uint32_t i0 = tid; i0 < npos; i0 += 2u * kFT) {  // two searches advanced together
             uint64_t k[2];
             bool ok[2];
@@ -415,8 +484,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 if (!ok[u]) continue;
-                const uint32_t rg = min(r[u], G - 1u);
-                rv[i0 + (uint32_t)u * kFT] = (uint8_t)rg;
+                const uint32_t rg = min(r[u], G - 1u), i = i0 + (uint32_t)u * kFT;
+                rv[i] = (uint8_t)rg;
+                hint[i] = (uint8_t)rg;
                 atomicAdd(&sm.s.lcnt[rg], 1u);
             }
         }
@@ -427,28 +497,53 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         const uint32_t m = sm.s.lcnt[tid];
         sm.s.gbase[tid] = m ? atomicAdd(&rcur[tid], m) : 0u;
     }
-    if (tid < (uint32_t)kMaxCtas) sm.s.lst[tid] = sm.s.lcnt[tid];
-    __syncthreads();
-    (void)smem_excl_scan<kFT, 1>(sm.s.lst, kMaxCtas, sm.s.w32);
-    if (tid < (uint32_t)kMaxCtas) sm.s.lcnt[tid] = sm.s.lst[tid];  // run cursors
-    __syncthreads();
-    TRACE(5);
-    for (uint32_t i = tid; i < npos; i += kFT) {
-        const uint32_t q = i >> 1;
-        if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
-        if (hr && rv[i]) continue;  // head-only: only the head is placed and stored
-        const uint32_t r = rv[i], lp = atomicAdd(&sm.s.lcnt[r], 1u);  // order within a run is free
-        kb2[lp] = sm.s.kbuf[i];
-        rr[lp] = (uint8_t)r;
+    if (!binm) {
+        if (tid < (uint32_t)kMaxCtas) sm.s.lst[tid] = sm.s.lcnt[tid];
+        __syncthreads();
+        (void)smem_excl_scan<kFT, 1>(sm.s.lst, kMaxCtas, sm.s.w32);
+        if (tid < (uint32_t)kMaxCtas) sm.s.lcnt[tid] = sm.s.lst[tid];  // run cursors
     }
     __syncthreads();
+    TRACE(5);
+    if (!binm) {
+        for (uint32_t i = tid; i < npos; i += kFT) {
+            const uint32_t q = i >> 1;
+            if (!((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)) continue;
+            if (hr && rv[i]) continue;  // head-only: only the head is placed and stored
+            const uint32_t r = rv[i], lp = atomicAdd(&sm.s.lcnt[r], 1u);  // order within a run is free
+            kb2[lp] = sm.s.kbuf[i];
+            rr[lp] = (uint8_t)r;
+        }
+        __syncthreads();
+    }
     TRACE(12);
     // warm steps: range 0's keys (the admission head; run 0 = kb2[0, lst[1])) get their payload
     // -- demand blk(ctx + 1) and state word, this CTA's own slots (L2) -- stored beside them, so
     // CTA 0 sorts the head with it instead of gathering it after its sort
     const bool hpay = !a.cold && G > 1u && !(a.flags & kStepMerge);
+    auto store_key = [&](uint32_t r, uint32_t pos, uint64_t k) {
+        if (pos < (uint32_t)kKcap) {  // else: overflow -> fallback
+            b.keys[0][(size_t)r * kKcap + pos] = k;
+            if (hpay && r == 0u) {
+                const uint32_t slot = (a.id_base_mod + (uint32_t)(k & c.cap_mask)) & c.cap_mask;
+                b.hd[pos] = (uint32_t)blk((uint64_t)b.pool.ctx[slot] + 1u, c);
+                b.hw[pos] = b.pool.sfc[slot];
+            }
+        }
+    };
+    if (binm) {  // the bins (a warp per range, coalesced) and the overflow list
+        for (uint32_t r = warp; r < G; r += (uint32_t)kFW) {
+            const uint32_t m = min(sm.s.lcnt[r], kBinCap), gb = sm.s.gbase[r];
+            for (uint32_t l = lane; l < m; l += 32u) store_key(r, gb + l, bins[r * kBinCap + l]);
+        }
+        const uint8_t* const rvp = rvb + (s_lo & 15u);
+        for (uint32_t o = tid; o < sm.s.novf; o += kFT) {
+            const uint32_t e = ovl[o], i = e & 0x3fffu, r = rvp[i];
+            store_key(r, sm.s.gbase[r] + (e >> 14), sm.s.kbuf[i]);
+        }
+    }
     const uint32_t n0 = sm.s.lst[1];
-    for (uint32_t i = tid; i < (hr ? sm.s.lcnt[0] : nk_cta); i += kFT) {  // (head-only: run 0 = [0, lcnt[0]))
+    for (uint32_t i = tid; i < (binm ? 0u : (hr ? sm.s.lcnt[0] : nk_cta)); i += kFT) {  // (head-only: run 0 = [0, lcnt[0]))
         const uint32_t r = rr[i], pos = sm.s.gbase[r] + (i - sm.s.lst[r]);
         if (pos < (uint32_t)kKcap) {  // else: overflow -> fallback
             const uint64_t k = kb2[i];
@@ -496,11 +591,31 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
 #pragma unroll
         for (int o = 16; o; o >>= 1) nq += __shfl_xor_sync(0xffffffffu, nq, o);
         big = __any_sync(0xffffffffu, big != 0u) ? 1u : 0u;
-        if (lane == 0) { sm.l.w32[0] = nq; sm.l.w32[1] = big; }
+        __syncwarp();
+        if (lane == 0) {
+            sm.l.w32[0] = nq;
+            sm.l.w32[1] = big;
+            // this range's keys (CTA 0: and the head's payload) -> shared memory by bulk copies
+            // (range_sort_tma), when this CTA will sort its range by it (the same conditions as below)
+            const uint32_t rn0 = sm.l.rsz[bid], re0 = sm.l.rsz[0];
+            const bool fb0 = fallback || big;
+            const bool ho0 = head_mode && !fb0 && re0 >= min(nq, a.max_batch + 32u);
+            const bool sorts = !fb0 && !(hr && !ho0) && (!ho0 || bid == 0);
+            const bool keep = bid == 0 && rn0 <= kHeadPre && !(a.flags & kStepMerge);
+            const bool pay = keep && !a.cold && G > 1u;  // R stored the head's payload (hpay)
+            uint32_t tm = 0;
+            if (sorts && (rn0 > kSmallSort || (a.tune & 4u)) && rn0 <= kTmaMax && rn0) {
+                tm = 1u | (keep ? 2u : 0u) | (pay ? 4u : 0u);
+                range_stage_issue(sm.l, b.keys[0] + (size_t)bid * kKcap, rn0, pay ? b.hd : nullptr, pay ? b.hw : nullptr);
+            }
+            sm.l.w32[2] = tm;
+        }
     }
     __syncthreads();
     n = sm.l.w32[0];
     fallback = fallback || sm.l.w32[1] != 0u;
+    const uint32_t tmode = sm.l.w32[2];  // (read before the range sort's scan reuses w32)
+    const bool tma = (tmode & 1u) != 0u;
     rsz = sm.l.rsz[bid];
     rpre = sm.l.rpre[bid];
     const uint32_t r_end0 = sm.l.rsz[0];
@@ -513,12 +628,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     const uint32_t q1 = G > 1u ? min(n, a.max_batch + kHeadMargin) : n;
     // position of grid entry f (0 .. 16 G) in this step's order: range 0's 16 segments over
     // [0, q1), the other ranges' over [q1, n) evenly (past the last key: the last key)
-    auto qf = [&](uint32_t f) -> uint32_t {
-        const uint64_t p = f <= (uint32_t)kSeg
-                               ? (uint64_t)q1 * f / kSeg
-                               : q1 + (uint64_t)(f - kSeg) * (uint64_t)(n - q1) / ((uint64_t)kSeg * (G - 1u));
-        return n ? (uint32_t)min(p, (uint64_t)(n - 1u)) : 0u;
-    };
+    auto qf = [&](uint32_t f) -> uint32_t { return grid_q(f, q1, n, G); };
     unsigned long long* spl_next = b.spl + (size_t)(a.parity ^ 1u) * kSplG;
     // head-only: the grid is kept (the other ranges were not sorted), except range 0's entries,
     // which CTA 0 refreshes from its sorted head when it holds more than q1 keys
@@ -540,6 +650,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     bool head_dw = false;  // CTA 0: demands / state words of its head in sm.l.b (sorted order)
     bool written = false;  // the range sort wrote the sorted range to keys1 itself
     bool head_loop = false;  // CTA 0: head keys in sm.l.b, demands / states in sm.l.pos (range_sort_loop)
+    bool head_tq = false;    // CTA 0: head keys in sm.l.b, demands / states (if staged) beside (range_sort_tma)
+    bool kept = false;       // the sorted range is in shared memory at sm.l.b + (rpre & 1) (range_sort_tma)
     if (!fallback && (!head_only || bid == 0)) {
         const uint32_t rn = rsz;
         const uint64_t* src = b.keys[0] + (size_t)bid * kKcap;
@@ -554,7 +666,20 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             tr[28] = smid;  // diagnostics: SM of this CTA
             for (int q = 32; q < 64; q++) tr[q] = 0;
         }
-        if (rn <= kSmallSort && !(a.tune & 4u)) {
+        if (tma) {  // staged by the bulk copy issued after the barrier; written to keys1 directly
+            TRACE(13);
+            written = range_sort_tma(sm.l, rn, b.keys[1] + rpre, rpre & 1u, vb, tr ? tr + 32 : nullptr, (tmode & 4u) != 0u);
+            head_tq = (tmode & 2u) && written;
+            kept = written;
+            if (!written) {  // a counter held too many keys: sort the placed range (sm.a) by LSD
+                unsigned long long o, an;
+                block_or_and(sm.l, sm.l.a, rn, o, an);
+                const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
+                if (r != sm.l.a)
+                    for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
+                __syncthreads();
+            }
+        } else if (rn <= kSmallSort && !(a.tune & 4u)) {
             TRACE(13);
             if (bid == 0) {
                 small_sort<true>(sm.l, src, rn, c, &b.pool, a.id_base_mod);
@@ -597,17 +722,25 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         }
         if (!written)
             for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][rpre + i] = sm.l.a[i];
+        if (tid == kFT - 1u) {  // the next step's grid entries that fall in this range: [gf[0], gf[1])
+            sm.l.gf[0] = grid_f(rpre, q1, n, G);
+            sm.l.gf[1] = grid_f(rpre + rn, q1, n, G);
+        }
         __syncthreads();  // the range's keys are in place (visible to this CTA's threads)
+        const uint32_t gf0 = sm.l.gf[0], gf1 = sm.l.gf[1];
         // the next step's grid entries that fall in this range
-        if (!head_only && rn)
-            for (uint32_t f = tid; f <= kSeg * G; f += kFT) {
+        if (!head_only && rn) {  // (grid entries [gf0, gf1): grid_f in the range sizes' pass)
+            const uint64_t* K = sm.l.b + (rpre & 1u);
+            for (uint32_t f = gf0 + tid; f < gf1; f += kFT) {
                 const uint32_t q = qf(f);
-                if (q >= rpre && q < rpre + rn) spl_next[f] = __ldcg(&b.keys[1][q]);
+                spl_next[f] = kept ? K[q - rpre] : __ldcg(&b.keys[1][q]);
             }
+        }
         if (hrefresh && bid == 0 && tid <= (uint32_t)kSeg) spl_next[tid] = __ldcg(&b.keys[1][qf(tid)]);
         final_buf = 1;
         passes = 1;
     } else if (fallback) {
+        if (tma) range_stage_wait(sm.l);  // the bulk copy lands before shared memory is reused
         {   // the keys compacted into keys0 (this CTA's at the prefix of the CTAs' key counts)
             uint32_t off = 0;
             {
@@ -628,6 +761,18 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
                     if ((sm.s.vmask[2u * (q >> 5) + (i & 1u)] >> (q & 31u)) & 1u)
                         b.keys[0][off + atomicAdd(ctr, 1u)] = sm.s.kbuf[i];
                 }
+            } else if (binm) {  // binned R: the bins and the overflow list (intact likewise)
+                uint32_t* ctr = &sm.l.w32[kFW];
+                if (tid == 0) *ctr = 0u;
+                __syncthreads();
+                for (uint32_t r = warp; r < G; r += (uint32_t)kFW) {
+                    const uint32_t m = min(sm.s.lcnt[r], kBinCap);
+                    const uint32_t o0 = lane == 0 && m ? atomicAdd(ctr, m) : 0u, ob = __shfl_sync(0xffffffffu, o0, 0);
+                    for (uint32_t l = lane; l < m; l += 32u) b.keys[0][off + ob + l] = bins[r * kBinCap + l];
+                }
+                __syncthreads();
+                const uint32_t nb = *ctr;
+                for (uint32_t o = tid; o < sm.s.novf; o += kFT) b.keys[0][off + nb + o] = sm.s.kbuf[ovl[o] & 0x3fffu];
             } else {
                 for (uint32_t i = tid; i < nk_cta; i += kFT) b.keys[0][off + i] = kb2[i];
             }
@@ -657,6 +802,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         passes = lsd_sort_global(b, n, b.kmask, G, sm.g, bar);
         final_buf = passes & 1u;
     } else {
+        if (tma) range_stage_wait(sm.l);  // (cold head-only steps) no copy outlives the CTA
         final_buf = 1;  // head-only: CTA 0 ranked the head; this CTA is done
         passes = 1;
     }
@@ -680,10 +826,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         b.trace[56] = r_end0;
         b.trace[57] = wait ? 1u : 0u;
     }
+    if (wait && tma && tid == 0) bulk_store_done();  // CTA 0 reads the ranges from keys1
     if (wait) grid_barrier(b.flags, G, ++bar);
     if (fallback && bid == 0 && n)
         for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = __ldcg(&b.keys[final_buf][qf(f)]);
-    if (bid != 0) return;
+    if (bid != 0) {
+        if (tma && tid == 0) bulk_store_read_wait();  // the range's bulk store has left shared memory
+        return;
+    }
+    if (tma && tid == 0 && (a.flags & kStepMerge)) bulk_store_done();  // the records / merge read keys1
     if (tid == 0) sm.l.adm.w64[0] = pinned_all;
     __syncthreads();
     pinned_all = sm.l.adm.w64[0];
@@ -697,9 +848,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     TRACE(15);
     // CTA 0 holds [0, need) in shared memory unless it waited (or its range sort wrote them out)
     const bool hl = head_loop && !wait;  // head keys in sm.l.b, demands / states in sm.l.pos
+    const bool hq = head_tq && !wait;    // head keys in sm.l.b, demands / states (if staged) beside
     const uint64_t* head = wait ? b.keys[final_buf]
-                                : (hl ? (kSortedInA ? sm.l.a : reinterpret_cast<const uint64_t*>(sm.l.b))
-                                      : (written ? b.keys[final_buf] : sm.l.a));
+                                : ((hl || hq) ? (hq || !kSortedInA ? reinterpret_cast<const uint64_t*>(sm.l.b) : sm.l.a)
+                                              : (written ? b.keys[final_buf] : sm.l.a));
     const bool dw = head_dw && !wait;
     if (a.flags & kStepMerge) {
         // multi-GPU: publish this rank's head as exchange records instead of admitting
@@ -828,11 +980,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     while (hs < 2u * a.max_batch) hs <<= 1;
     const bool use_h = !wait && hs <= kHeadTC;
     const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);
-    uint32_t* htab = hl && !kSortedInA ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
+    uint32_t* htab = (hl && !kSortedInA) || hq ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
+    const bool hqp = hq && (tmode & 4u);  // the TMA-staged head's payload
     admit_cta(b, c, a, head, n, pinned_all, sm.l.adm, use_h ? htab : nullptr, use_h ? hs : 0u,
               b.trace ? b.trace + 40 : nullptr,
-              hl ? sm.l.pos + kHeadPre : (dw ? b32 + kHeadD : nullptr),
-              hl ? sm.l.pos + 2u * kHeadPre : (dw ? b32 + kHeadW : nullptr));
+              hl ? sm.l.pos + kHeadPre : (hqp ? tma_head_dem(sm.l) : (dw ? b32 + kHeadD : nullptr)),
+              hl ? sm.l.pos + 2u * kHeadPre : (hqp ? tma_head_st(sm.l) : (dw ? b32 + kHeadW : nullptr)));
+    if (tma && tid == 0) bulk_store_read_wait();
     TRACE(9);
 }
 

@@ -234,6 +234,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     size_t o_rcur = h->fused ? L.take((size_t)2 * 256 * 4) : 0;
     size_t o_nkp = L.take((size_t)gmax * 4);
     size_t o_hd = h->fused ? L.take((size_t)kFusedKcap * 4) : 0, o_hw = h->fused ? L.take((size_t)kFusedKcap * 4) : 0;
+    size_t o_rh = h->fused ? L.take((size_t)cap_pad + 16) : 0;
     const size_t bigr = big_max_ranges();
     size_t o_bspl = h->big ? L.take((size_t)2 * (16 * bigr + 16) * 8) : 0;
     size_t o_brc = h->big ? L.take((size_t)2 * bigr * 4) : 0;
@@ -281,6 +282,7 @@ size_t carve(lamps_t* h, uint8_t* base) {
     h->b.nk_part = reinterpret_cast<uint32_t*>(base + o_nkp);
     h->b.hd = h->fused ? reinterpret_cast<uint32_t*>(base + o_hd) : nullptr;
     h->b.hw = h->fused ? reinterpret_cast<uint32_t*>(base + o_hw) : nullptr;
+    h->b.rhint = h->fused ? base + o_rh : nullptr;
     h->b.big_ranges = h->big_ranges;
     h->b.big_grid = h->big_grid;
     h->b.big_cta_slots = h->big_cta_slots;

@@ -126,6 +126,8 @@ struct Bufs {
     uint32_t* hd;            // fused: [kFusedKcap] demand blk(ctx + 1) of range 0's keys (the admission
                              // head), beside range 0's region of keys[0] (warm steps)
     uint32_t* hw;            // fused: [kFusedKcap] their state words, likewise
+    uint8_t* rhint;          // fused: [cap_pad] each slot's key range in the last step that ranked it
+                             // (R's search starts there; any value is safe, it is verified)
     uint32_t score_grid, sort_grid;
     uint64_t* keys[2];       // ping-pong key buffers, capacity + pad
     uint32_t* adm_slot[2];   // admitted slots, by parity

@@ -67,6 +67,8 @@ if os.environ.get("TRACE"):
             print(f"  L.{part}.{nm:14s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
         nb = t[:, :, base + 5]
         print(f"  L.{part}.big groups   max {int(nb.max())} mean {nb.mean():.2f}")
+    nmiss, novf = t[:, 1:, 16], t[:, 1:, 17]
+    print(f"  binned R: hint misses per CTA median {np.median(nmiss):.0f} max {nmiss.max()}, overflow keys median {np.median(novf):.0f} max {novf.max()}")
     ms, nst = st.timing() if False else (None, None)
     if os.environ.get("PERCTA"):
         t0 = acc[-1]

@@ -5,5 +5,5 @@ for rnd in 1 2 3; do
   echo "== current"; TUNES=0 ROUNDS=1 python scripts/ab_tune.py
   for so in "$@"; do echo "== $so"; LAMPS_LIB=$so TUNES=0 ROUNDS=1 python scripts/ab_tune.py; done
 done
-TRACE=1 PERCTA=1 STEPS=3 timeout 300 python scripts/prof_step.py > gpurun_out/r02/ab_trace_cur.txt 2>&1
-for so in "$@"; do TRACE=1 PERCTA=1 STEPS=3 LAMPS_LIB=$so timeout 300 python scripts/prof_step.py > gpurun_out/r02/ab_trace_$(basename $so .so).txt 2>&1; done
+ADMIT=1 TRACE=1 PERCTA=1 STEPS=3 timeout 300 python scripts/prof_step.py > gpurun_out/r02/ab_trace_cur.txt 2>&1
+for so in "$@"; do ADMIT=1 TRACE=1 PERCTA=1 STEPS=3 LAMPS_LIB=$so timeout 300 python scripts/prof_step.py > gpurun_out/r02/ab_trace_$(basename $so .so).txt 2>&1; done
