@@ -135,6 +135,7 @@ struct FusedSmem {
         SortSmem g;
     };
     alignas(16) uint32_t btab[kTabW];  // this step's bucket table (bucket_t), every phase
+    unsigned long long pin_all;        // CTA 0: A5's pinned total (summed right after the grid barrier)
 };
 // After the union, untouched by every phase: the peer-memory exchange's state (peer
 // buffer pointers, prefetched at kernel start) and the in-kernel merge's small structures.

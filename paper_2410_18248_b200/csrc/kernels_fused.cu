@@ -61,6 +61,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         }
     }
 
+    if (bid == 0 && tid == 32u) {  // CTA 0: the admission's first loads (the previous admitted list) -> L2
+        const uint32_t prv = a.parity ^ 1u;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ctl));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b.adm_slot[prv]), "r"(((a.max_batch + 3u) & ~3u) * 4u)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b.adm_id[prv]), "r"(((a.max_batch + 1u) & ~1u) * 8u)
+                     : "memory");
+    }
     const bool hr0 = (a.flags & kStepHeadOnly) && G > 1u && !a.cold;  // head-only R (hr below)
     if (tid == 0 && !a.cold && !hr0 && bins_fit(G) && s_hi > s_lo)  // the slots' range hints -> shared memory
         range_hint_issue(sm.s.hbar, reinterpret_cast<uint8_t*>(sm.s.cnt), b.rhint, s_lo, s_hi);
@@ -611,6 +619,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             sm.l.w32[2] = tm;
         }
     }
+    if (bid == 0 && warp == 2) {  // A5's budget: the pinned total (beside the range sizes' round trip)
+        unsigned long long pa = 0;
+        for (uint32_t r = lane; r < G; r += 32) pa += __ldcg(&b.pin_part[r]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pa += __shfl_xor_sync(0xffffffffu, pa, o);
+        if (lane == 0) sm.pin_all = pa;
+    }
     __syncthreads();
     n = sm.l.w32[0];
     fallback = fallback || sm.l.w32[1] != 0u;
@@ -809,12 +824,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
     // the next step's splitters past the last key, and (after the LSD) all of them
     if (bid == 0 && !head_only && n == 0)  // no keys: an empty grid
         for (uint32_t f = tid; f <= kSeg * G; f += kFT) spl_next[f] = 0ull;
-    unsigned long long pinned_all = 0;
-    if (bid == 0 && warp == 0) {  // A5's budget: the pinned total
-        for (uint32_t r = lane; r < G; r += 32) pinned_all += __ldcg(&b.pin_part[r]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) pinned_all += __shfl_xor_sync(0xffffffffu, pinned_all, o);
-    }
+    unsigned long long pinned_all = 0;  // (CTA 0: sm.pin_all, summed right after the grid barrier)
 
     TRACE(8);
     // ---------------- A: admission by CTA 0
@@ -835,10 +845,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         return;
     }
     if (tma && tid == 0 && (a.flags & kStepMerge)) bulk_store_done();  // the records / merge read keys1
-    if (tid == 0) sm.l.adm.w64[0] = pinned_all;
-    __syncthreads();
-    pinned_all = sm.l.adm.w64[0];
-    __syncthreads();
+    pinned_all = sm.pin_all;
     if (tid == 0) {
         ctl->n_passes = passes;
         ctl->final_buf = final_buf;

@@ -22,7 +22,8 @@ for rnd in range(int(os.environ.get("ROUNDS", "3"))):
         for _ in range(300):
             s.step_async(kv)
         s.import_pool(snap, snap["id_base"], snap["next_id"])
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(40)]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(int(os.environ.get("STEPS", "40")))]
         for a, b in ev:
             flush.zero_()
             a.record()
