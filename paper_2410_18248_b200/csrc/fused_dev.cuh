@@ -125,6 +125,7 @@ struct PhaseL {                  // L
     uint32_t rsz[kMaxCtas], rpre[kMaxCtas];       // every range's size and position in the order
     unsigned long long fine[kSeg + 1], fcode[kSeg + 1];  // this range's grid entries, their key codes
     uint32_t shs[kSeg];                                  // range sort: per segment, the digit's shift
+    uint32_t shr[kSeg];                                  // range_sort_tma: per segment, the raw-key shift (or 255)
     alignas(8) unsigned long long mbar;                  // range_sort_tma: the staging copy's mbarrier
     uint32_t gf[2];                                      // the next step's grid entries [gf0, gf1) in this range
 };
@@ -504,20 +505,27 @@ __device__ __forceinline__ bool range_sort_loop(PhaseL& sm, const uint64_t* __re
 // head goes to [0, 8 rn) (kept keys) and its payload to the staged payload's places (dsm / wsm).
 // Position of the next step's grid entry f (0 .. 16 G) in this step's order of n keys: range 0's
 // 16 segments over [0, q1), the other ranges' over [q1, n) evenly (past the last key: the last key).
+// (in double precision: the products stay below 2^53 and the quotients' fractional parts are
+// at least 2^-44 relative away from an integer, so the correctly rounded division floors /
+// ceils exactly -- cheaper than a 64-bit integer division)
 __device__ __forceinline__ uint32_t grid_q(uint32_t f, uint32_t q1, uint32_t n, uint32_t G) {
-    const uint64_t p = f <= (uint32_t)kSeg ? (uint64_t)q1 * f / kSeg
-                                           : q1 + (uint64_t)(f - kSeg) * (uint64_t)(n - q1) / ((uint64_t)kSeg * (G - 1u));
-    return n ? (uint32_t)min(p, (uint64_t)(n - 1u)) : 0u;
+    if (!n) return 0u;
+    const uint32_t p = f <= (uint32_t)kSeg
+                           ? (uint32_t)(((uint64_t)q1 * f) >> 4)
+                           : q1 + (uint32_t)floor((double)((uint64_t)(f - kSeg) * (uint64_t)(n - q1)) /
+                                                  (double)((uint64_t)kSeg * (G - 1u)));
+    return min(p, n - 1u);
 }
+static_assert(kSeg == 16, "grid_q divides by 16 with a shift");
 // The first f with grid_q(f) >= q (16 G + 1 if none), in closed form: for q <= q1 the head's
 // floor(q1 f / 16) >= q <=> f >= ceil(16 q / q1); past the head floor((f - 16) D / M) >= q - q1 <=>
 // f - 16 >= ceil((q - q1) M / D) (D = n - q1, M = 16 (G - 1)); the clamp at n - 1 only bites q >= n.
 __device__ __forceinline__ uint32_t grid_f(uint32_t q, uint32_t q1, uint32_t n, uint32_t G) {
     if (q == 0u) return 0u;
     if (q >= n) return (uint32_t)kSeg * G + 1u;
-    if (q <= q1) return (uint32_t)(((uint64_t)q * kSeg + q1 - 1u) / q1);
-    const uint64_t D = n - q1, num = (uint64_t)(q - q1) * kSeg * (G - 1u);
-    return kSeg + (uint32_t)((num + D - 1u) / D);
+    if (q <= q1) return (uint32_t)ceil((double)q * kSeg / (double)q1);
+    const double num = (double)((uint64_t)(q - q1) * kSeg * (G - 1u)), D = (double)(n - q1);
+    return kSeg + (uint32_t)ceil(num / D);
 }
 constexpr uint32_t kTmaMax = 7167;  // (the kept keys sit one key later when the range starts at an odd position)
 constexpr uint32_t kTsCnt = 8u * (kTmaMax + 1u);                         // byte offsets from sm.b
@@ -597,16 +605,33 @@ __device__ __forceinline__ bool range_sort_tma(PhaseL& sm, uint32_t rn, uint64_t
         const unsigned long long d = sm.fcode[tid + 1] > sm.fcode[tid] ? sm.fcode[tid + 1] - sm.fcode[tid] : 0ull;
         const uint32_t nb = 64u - (uint32_t)__clzll((long long)d);
         shs[tid] = nb > lw ? nb - lw : 0u;
+        // a segment whose ends share the starving flag and whose key parts differ in bit length
+        // by at most one holds keys of about one density: its digit is linear in the raw key
+        // (one subtract and shift); others take the code (bit length, mantissa) of the key
+        const unsigned long long f0 = sm.fine[tid], f1 = sm.fine[tid + 1], vm = (1ull << vb) - 1ull;
+        const uint32_t e0 = 64u - (uint32_t)__clzll((long long)(f0 & vm)), e1 = 64u - (uint32_t)__clzll((long long)(f1 & vm));
+        const unsigned long long dr = f1 > f0 ? f1 - f0 : 0ull;
+        const uint32_t nr = 64u - (uint32_t)__clzll((long long)dr);
+        sm.shr[tid] = ((f0 >> vb) == (f1 >> vb) && e1 <= e0 + 1u) ? (nr > lw ? nr - lw : 0u) : 255u;
     }
     for (uint32_t i = tid; i <= ncnt; i += kFT) cnt[i] = 0u;
     range_stage_wait(sm);
     __syncthreads();
+    // any digit monotone inside each segment gives the exact order (segments own disjoint
+    // counter ranges; ties of a counter are ranked by comparison)
     auto digit = [&](uint64_t k) -> uint32_t {
         uint32_t sg = 0;
 #pragma unroll
         for (uint32_t st = kSeg / 2; st; st >>= 1) sg = k >= sm.fine[sg + st] ? sg + st : sg;
-        const unsigned long long c = key_code(k, vb), c0 = sm.fcode[sg];
-        const unsigned long long d = (c > c0 ? c - c0 : 0ull) >> shs[sg];
+        const uint32_t sr = sm.shr[sg];
+        unsigned long long d;
+        if (sr != 255u) {
+            const unsigned long long f0 = sm.fine[sg];
+            d = (k > f0 ? k - f0 : 0ull) >> sr;
+        } else {
+            const unsigned long long c = key_code(k, vb), c0 = sm.fcode[sg];
+            d = (c > c0 ? c - c0 : 0ull) >> shs[sg];
+        }
         return sg * W + (uint32_t)min(d, (unsigned long long)(W - 1u));
     };
     LTRACE(1);

@@ -742,6 +742,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             sm.l.gf[1] = grid_f(rpre + rn, q1, n, G);
         }
         __syncthreads();  // the range's keys are in place (visible to this CTA's threads)
+        if (!a.cold) TRACE(10);  // (slots 10 / 11: cold steps' bucket phases; diagnostics here)
         const uint32_t gf0 = sm.l.gf[0], gf1 = sm.l.gf[1];
         // the next step's grid entries that fall in this range
         if (!head_only && rn) {  // (grid entries [gf0, gf1): grid_f in the range sizes' pass)
@@ -752,6 +753,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
             }
         }
         if (hrefresh && bid == 0 && tid <= (uint32_t)kSeg) spl_next[tid] = __ldcg(&b.keys[1][qf(tid)]);
+        if (!a.cold) TRACE(11);
         final_buf = 1;
         passes = 1;
     } else if (fallback) {

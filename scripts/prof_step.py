@@ -67,6 +67,10 @@ if os.environ.get("TRACE"):
             print(f"  L.{part}.{nm:14s} max {np.median(d.max(axis=1)):7.2f}  mean {np.median(d.mean(axis=1)):7.2f}")
         nb = t[:, :, base + 5]
         print(f"  L.{part}.big groups   max {int(nb.max())} mean {nb.mean():.2f}")
+    for nm, a0, a1 in (("sort end -> gf sync", 14, 10), ("grid entries", 10, 11), ("-> A", 11, 8)):
+        d0 = (t[:, 0, a1] - t[:, 0, a0]) / 1.965e3
+        d1 = (t[:, 1:, a1] - t[:, 1:, a0]) / 1.965e3
+        print(f"  store.{nm:20s} cta0 {np.median(d0):6.2f}  others max {np.median(d1.max(axis=1)):6.2f} mean {np.median(d1.mean(axis=1)):6.2f}")
     nmiss, novf = t[:, 1:, 16], t[:, 1:, 17]
     print(f"  binned R: hint misses per CTA median {np.median(nmiss):.0f} max {nmiss.max()}, overflow keys median {np.median(novf):.0f} max {novf.max()}")
     ms, nst = st.timing() if False else (None, None)
