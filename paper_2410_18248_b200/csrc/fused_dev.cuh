@@ -584,7 +584,8 @@ __device__ __forceinline__ uint32_t* tma_head_st(PhaseL& sm) { return reinterpre
 // kRangeRankM keys (nothing stored): sm.a then holds the range placed by digit (the caller sorts
 // it otherwise).
 __device__ __forceinline__ bool range_sort_tma(PhaseL& sm, uint32_t rn, uint64_t* __restrict__ out, uint32_t o,
-                                               uint32_t vb, unsigned long long* tr, bool pay) {
+                                               uint32_t vb, unsigned long long* tr, bool pay, bool staged = true,
+                                               bool bulk = true) {
 #define LTRACE(k) do { if (tr && threadIdx.x == 0) tr[k] = clock64(); } while (0)
     const uint32_t tid = threadIdx.x;
     unsigned char* fb = reinterpret_cast<unsigned char*>(sm.b);
@@ -615,7 +616,7 @@ __device__ __forceinline__ bool range_sort_tma(PhaseL& sm, uint32_t rn, uint64_t
         sm.shr[tid] = ((f0 >> vb) == (f1 >> vb) && e1 <= e0 + 1u) ? (nr > lw ? nr - lw : 0u) : 255u;
     }
     for (uint32_t i = tid; i <= ncnt; i += kFT) cnt[i] = 0u;
-    range_stage_wait(sm);
+    if (staged) range_stage_wait(sm);  // (else the caller wrote S / the payload itself)
     __syncthreads();
     // any digit monotone inside each segment gives the exact order (segments own disjoint
     // counter ranges; ties of a counter are ranked by comparison)
@@ -694,6 +695,11 @@ __device__ __forceinline__ bool range_sort_tma(PhaseL& sm, uint32_t rn, uint64_t
     LTRACE(5);
     if (__syncthreads_or(big)) return false;
     const uint64_t* K = S + o;  // K[i] = the key of out[i]
+    if (!bulk) {  // (one-CTA kernel: plain coalesced stores, nothing outstanding at its end)
+        for (uint32_t i = tid; i < rn; i += kFT) out[i] = K[i];
+        LTRACE(6);
+        return true;
+    }
     const uint32_t i0 = o, i1 = o + ((rn - min(o, rn)) & ~1u);  // out[i0, i1): whole 16-B pairs
     if (tid == 0 && i1 > i0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the rank pass's stores, then the copy

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
     // ---- A0 default update, A1-A3 for this thread's slots (tid + u * kFT), keys in registers
     const Pool& P = b.pool;
     uint64_t key[kSmallPer];
+    uint32_t kdem[kSmallPer], kw[kSmallPer];  // the admission's demand blk(ctx + 1) and state word
     uint32_t nk = 0, pinned = 0;
     unsigned long long kmin = ~0ull, kmax = 0ull;
 #pragma unroll
@@ -74,9 +75,10 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
         uint64_t k;
         (void)score_slot<DBG>(P, c, a.id_base_mod, b.dbg, slot, w, ctx, pre, api, resp, post, pend, k);
         P.sfc[slot] = w;
+        const uint32_t dm = (uint32_t)blk((uint64_t)ctx + 1u, c);
 #pragma unroll
         for (int q = 0; q < kSmallPer; q++)  // packed to the front (no dynamic register index)
-            if (q == (int)nk) key[q] = k;
+            if (q == (int)nk) { key[q] = k; kdem[q] = dm; kw[q] = w; }
         nk++;
         kmin = min(kmin, (unsigned long long)k);
         kmax = max(kmax, (unsigned long long)k);
@@ -84,9 +86,23 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
     // ---- compaction into keys[0] (block scan), the pinned total, this step's key bounds
     uint32_t n;
     const uint32_t pos = block_excl_scan_u32<kFT>(nk, sm.l.w32, &n);
+    // keys (and, up to kHeadPre keys, their demand / state words) stay in shared memory for
+    // range_sort_tma (no copy to stage: the sort reads them where the compaction put them);
+    // the few-hundred-key all-pairs sort and the forced fallback read them from keys[0]
+    const bool onchip = n > kSmallSort && n <= kTmaMax && !(a.flags & kStepForceFallback) && !(a.tune & 4u);
+    const bool pay = onchip && n <= kHeadPre;
+    uint32_t* const Hd = tma_head_dem(sm.l);
+    uint32_t* const Hw = tma_head_st(sm.l);
 #pragma unroll
     for (int q = 0; q < kSmallPer; q++)
-        if ((uint32_t)q < nk) b.keys[0][pos + q] = key[q];
+        if ((uint32_t)q < nk) {
+            if (onchip) {
+                sm.l.b[pos + q] = key[q];
+                if (pay) { Hd[pos + q] = kdem[q]; Hw[pos + q] = kw[q]; }
+            } else {
+                b.keys[0][pos + q] = key[q];
+            }
+        }
     unsigned long long pin64 = pinned;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -134,6 +150,8 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
         small_sort<true>(sm.l, b.keys[0], n, c, &b.pool, a.id_base_mod);
         for (uint32_t i = tid; i < n; i += kFT) b.keys[1][i] = sm.l.a[i];
         tiny = true;
+    } else if (onchip) {
+        written = range_sort_tma(sm.l, n, b.keys[1], 0u, vb, nullptr, pay, false, false);
     } else if (n > 1u && !(a.flags & kStepForceFallback)) {
         written = LAMPS_RANGE_SORT(sm.l, b.keys[0], n, b.keys[1], vb, nullptr, &b.pool, a.id_base_mod, &c, dsm, wsm);
     }
@@ -168,11 +186,12 @@ __global__ void __launch_bounds__(kFT, 1) k_small(const __grid_constant__ Bufs b
     while (hs < 2u * a.max_batch) hs <<= 1;
     const bool use_h = hs <= kHeadTC;
     uint32_t* htab = written && !kSortedInA ? reinterpret_cast<uint32_t*>(sm.l.a) : reinterpret_cast<uint32_t*>(sm.l.b);
-    const bool dw = written && stage;
+    const bool dw = written && stage && !onchip;
+    const bool dq = written && pay;  // range_sort_tma: the payload by sorted position beside the keys
     const uint32_t* b32 = reinterpret_cast<const uint32_t*>(sm.l.b);  // small_sort's staged arrays
     static_assert(kHeadTC <= kHeadD, "small_sort's staged arrays lie past the hash table");
     admit_cta(b, c, a, srt, n, pinned_all, sm.l.adm, use_h ? htab : nullptr, use_h ? hs : 0u, nullptr,
-              dw ? dsm : (tiny ? b32 + kHeadD : nullptr), dw ? wsm : (tiny ? b32 + kHeadW : nullptr));
+              dq ? Hd : (dw ? dsm : (tiny ? b32 + kHeadD : nullptr)), dq ? Hw : (dw ? wsm : (tiny ? b32 + kHeadW : nullptr)));
     if (b.trace && tid == 0) b.trace[3] = clock64();
 }
 
