@@ -683,7 +683,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         }
         if (tma) {  // staged by the bulk copy issued after the barrier; written to keys1 directly
             TRACE(13);
-            written = range_sort_tma(sm.l, rn, b.keys[1] + rpre, rpre & 1u, vb, tr ? tr + 32 : nullptr, (tmode & 4u) != 0u);
+            // (CTA 0's head: plain stores, so no bulk copy is outstanding behind its admission)
+            written = range_sort_tma(sm.l, rn, b.keys[1] + rpre, rpre & 1u, vb, tr ? tr + 32 : nullptr, (tmode & 4u) != 0u,
+                                     true, bid != 0u);
             head_tq = (tmode & 2u) && written;
             kept = written;
             if (!written) {  // a counter held too many keys: sort the placed range (sm.a) by LSD
