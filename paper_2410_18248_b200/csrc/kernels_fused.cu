@@ -540,12 +540,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused(const __grid_constant__ Bufs b
         }
     };
     if (binm) {  // the bins (a warp per range, coalesced) and the overflow list
-        for (uint32_t r = warp; r < G; r += (uint32_t)kFW) {
+        // warp 0 takes the head's bin alone (its payload loads are the phase's latency chain);
+        // the other warps share the other ranges, the highest threads the overflow list
+        for (uint32_t r = warp == 0u ? 0u : warp - 1u + (G > 1u ? 1u : G); r < G; r += warp == 0u ? G : (uint32_t)kFW - 1u) {
             const uint32_t m = min(sm.s.lcnt[r], kBinCap), gb = sm.s.gbase[r];
             for (uint32_t l = lane; l < m; l += 32u) store_key(r, gb + l, bins[r * kBinCap + l]);
         }
         const uint8_t* const rvp = rvb + (s_lo & 15u);
-        for (uint32_t o = tid; o < sm.s.novf; o += kFT) {
+        for (uint32_t o = kFT - 1u - tid; o < sm.s.novf; o += kFT) {
             const uint32_t e = ovl[o], i = e & 0x3fffu, r = rvp[i];
             store_key(r, sm.s.gbase[r] + (e >> 14), sm.s.kbuf[i]);
         }
