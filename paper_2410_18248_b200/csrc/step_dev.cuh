@@ -355,18 +355,21 @@ __device__ __noinline__ ColdOut score_slot_cold(const Pool& P, const Cost& c, ui
 }
 
 // The step summary into mapped host memory (one thread, after the Ctl fields are final).
+// (three 16-B stores: each store to mapped memory is its own transaction over the host link)
 __device__ __forceinline__ void publish_host_result(const Bufs& b) {
     const Ctl* ctl = b.ctl;
     HostRes* r = b.hres;
-    r->n_elig = ctl->n_elig_out;
-    r->pinned = ctl->pinned_out;
-    r->budget = ctl->budget;
-    r->budget_used = *(volatile const unsigned long long*)&ctl->budget_used;
-    r->n_admitted = ctl->n_admitted;
-    r->n_preempted = ctl->n_preempted;
-    r->blocked_head = ctl->blocked_head;
-    r->final_buf = ctl->final_buf;
+    const unsigned long long bu = *(volatile const unsigned long long*)&ctl->budget_used;
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(&r->n_elig), "l"((unsigned long long)ctl->n_elig_out),
+                 "l"((unsigned long long)ctl->pinned_out) : "memory");
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(&r->budget), "l"((unsigned long long)ctl->budget), "l"(bu)
+                 : "memory");
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(&r->n_admitted), "r"(ctl->n_admitted),
+                 "r"(ctl->n_preempted), "r"(ctl->blocked_head), "r"(ctl->final_buf) : "memory");
 }
+static_assert(offsetof(HostRes, pinned) == 8 && offsetof(HostRes, budget) == 16 && offsetof(HostRes, budget_used) == 24 &&
+                  offsetof(HostRes, n_admitted) == 32 && offsetof(HostRes, final_buf) == 44,
+              "publish_host_result's vector stores follow HostRes");
 
 // A5 admission by one 1024-thread CTA over the ranked keys (see k_admit).
 struct AdmitSmem {
@@ -438,8 +441,10 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
             b.adm_slot[par][k] = slot;
             b.adm_id[par][k] = a.id_base + idoff;
             b.adm_strat[par][k] = (uint8_t)sfc_strat(w);
+#ifndef LAMPS_NO_HOSTRES  // (measurement-only build: the mapped host writes left out)
             b.h_adm_id[k] = a.id_base + idoff;  // the host's copy (mapped memory)
             b.h_adm_strat[k] = (uint8_t)sfc_strat(w);
+#endif
             if (htab) {
                 uint32_t h = slot_hash(slot, hmask);
                 while (atomicCAS(&htab[h], kEmpty, slot) != kEmpty) h = (h + 1u) & hmask;
@@ -482,7 +487,9 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
         const uint32_t pos = block_excl_scan_u32<NT>(f, sm.w32, &tot);
         if (f) {
             b.pre_id[npre + pos] = id;
+#ifndef LAMPS_NO_HOSTRES
             b.h_pre_id[npre + pos] = id;
+#endif
         }
         npre += tot;
     }
@@ -495,7 +502,9 @@ __device__ __forceinline__ void admit_cta(const Bufs& b, const Cost& c, const St
         ctl->pinned_out = pinned;
         ctl->n_elig = 0;  // accumulators of the next step
         ctl->pinned = 0;
+#ifndef LAMPS_NO_HOSTRES
         publish_host_result(b);
+#endif
     }
     ATRACE(4);
 #undef ATRACE

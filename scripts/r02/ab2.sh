@@ -16,6 +16,6 @@ for line in open("gpurun_out/ab2/ab.txt"):
     if m: res.setdefault(cur,[]).append(float(m.group(1)))
 for k,v in res.items(): print(k, sorted(v), "median", sorted(v)[len(v)//2])
 PY
-for so in "" "$@"; do
+for so in "" ${NOBENCH:+} $([ -z "$NOBENCH" ] && echo "$@"); do
   LAMPS_LIB=$so timeout 600 python bench.py --steps 100 --warmup 10 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('bench', '${so:-current}', round(d['us_per_step'],2), d['step_us'], d['clocks'])"
 done
