@@ -72,13 +72,13 @@ struct PhaseS {                  // S, H, X (cold), R
 // position (the copy starts at the 16-B boundary below the CTA's first slot), G bins of kBinCap
 // keys, the overflow list (position | index in the run << 14, every key of the CTA fits), the
 // queue of hint misses.
-constexpr uint32_t kBinCap = 48;
+constexpr uint32_t kBinCap = 56;
 constexpr uint32_t kRbBins = (kKcap + 32u + 63u) & ~63u;
 constexpr uint32_t kRbBinsMax = 148u * kBinCap * 8u;
 constexpr uint32_t kRbOvl = kRbBins + kRbBinsMax;
 constexpr uint32_t kRbMiss = kRbOvl + 4u * kKcap;
 constexpr uint32_t kMissCap = (sizeof(uint32_t) * 2u * kMaxBuckets - kRbMiss) / 2u;
-static_assert(kMissCap >= 2048u, "binned R: the miss queue is too small");
+static_assert(kMissCap >= 512u, "binned R: the miss queue is too small");
 __host__ __device__ constexpr bool bins_fit(uint32_t G) { return G <= 148u; }
 // thread 0 at kernel start: the hints of slots [s_lo, s_hi) (16-B aligned around them) -> dst
 __device__ __forceinline__ void range_hint_issue(unsigned long long& bar, uint8_t* dst, const uint8_t* hint,
