@@ -268,8 +268,24 @@ __global__ void __launch_bounds__(kFT, 1) k_big_sort(const __grid_constant__ Buf
             __syncthreads();
             const uint64_t* src = b.big_keysr + (size_t)v * kKcap;
             const bool stage = v == 0 && rn <= kHeadPre;
+            // ranges other than the staged head: the keys into shared memory by one bulk copy
+            // and the shared-memory range sort (plain stores out: nothing asynchronous is left
+            // behind when the next range reuses shared memory)
+            const bool tma = !stage && rn > kSmallSort && rn <= kTmaMax && !(a.tune & 4u);
+            if (tma && tid == 0) range_stage_issue(sm.l, src, rn);
             bool written = false;
-            if (rn) {
+            if (rn && tma) {
+                written = range_sort_tma(sm.l, rn, b.keys[1] + rp, rp & 1u, vb, nullptr, false, true, false);
+                if (!written) {  // a counter held too many keys: the placed range by LSD
+                    unsigned long long o, an;
+                    block_or_and(sm.l, sm.l.a, rn, o, an);
+                    const uint64_t* r = local_lsd(sm.l, sm.l.a, sm.l.b, rn, o ^ an);
+                    if (r != sm.l.a)
+                        for (uint32_t i = tid; i < rn; i += kFT) sm.l.a[i] = r[i];
+                    __syncthreads();
+                    for (uint32_t i = tid; i < rn; i += kFT) b.keys[1][rp + i] = sm.l.a[i];
+                }
+            } else if (rn) {
                 written = range_sort_loop(sm.l, src, rn, b.keys[1] + rp, vb, nullptr, &b.pool, a.id_base_mod, &c,
                                           stage ? sm.l.pos + kHeadPre : nullptr, stage ? sm.l.pos + 2u * kHeadPre : nullptr);
                 if (!written) {  // a counter held too many keys: the placed range by LSD
